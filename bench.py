@@ -1,0 +1,520 @@
+"""bench.py -- Tempo in-place activation operators on B200.
+
+One "step" = forward + backward of the Tempo activation-operator chain of one
+BERT-large encoder layer (BASELINE.json configs[3]: B=64 per GPU, S=512,
+H=1024, A=16, p=0.1), in encoder order (proj/src/encoder.cpp:155-210):
+
+  fwd: softmax+dropout_recompute [B*A*S, S] -> attn-out dropout [T,H] ->
+       LayerNorm1 [T,H] -> GELU [T,4H] -> ffn dropout [T,H] -> LayerNorm2 [T,H]
+  bwd: LN2 -> ffn dropout -> GELU -> LN1 -> attn-out dropout ->
+       attn-probs (dropout bwd + softmax bwd + recomputed D for the dV GEMM)
+  (+ at N>1: one NCCL all-reduce of the bucketed LN dgamma/dbeta, 4H floats)
+
+GEMMs and residual adds are outside the path and are
+replaced by synthetic fp32 buffers of the layer shapes.  Scaling is weak:
+every rank runs B=64 rows, so N=8 is configs[4] (B=512 sharded 8 ways).
+
+metric: fwd+bwd GB/s = algorithmic HBM bytes of the chain (SURVEY 8d:
+GELU 8.125+12.125 B/elem, LN 8NM+4N+8M / 12NM+4N+16M, attention 12.125 +
+16.125 B/elem, dropouts 8.125+8.125 B/elem) / device time, summed over ranks.
+
+Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+B, S, H, A, P_DROP = 64, 512, 1024, 16, 0.1
+T = B * S                # tokens per rank
+ATT_ROWS = B * A * S     # attention-probability rows per rank
+METRIC = "fwd+bwd GB/s per op vs B200 HBM peak at 1/2/4/8 GPU; activation bytes/layer"
+WORKLOAD = "bert-large-layer-tempo-op-chain"
+
+
+# ----------------------------------------------------------------- bytes
+def op_bytes(batch=B):
+    """Algorithmic HBM bytes per op, for `batch` sequences."""
+    t, ar = batch * S, batch * A * S
+    n_g, n_h, n_a = t * 4 * H, t * H, ar * S
+    bits = 1.0 / 8
+    return {
+        "softmax_dropout_fwd": n_a * (4 + 4 + 4 + bits),     # z -> P, D, mask
+        "attn_probs_bwd": n_a * (4 + 4 + bits + 4 + 4),      # dD, P, mask -> dZ, D
+        "gelu_fwd": n_g * (4 + 4 + bits),
+        "gelu_bwd": n_g * (4 + 4 + bits + 4),
+        "layernorm_fwd": 2 * (8 * n_h + 4 * t + 8 * H),
+        "layernorm_bwd": 2 * (12 * n_h + 4 * t + 16 * H),
+        "dropout_fwd": 2 * n_h * (8 + bits),
+        "dropout_bwd": 2 * n_h * (8 + bits),
+    }
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            pk = json.load(f)
+        return float(pk["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+# ------------------------------------------------------------ the chain
+class Chain:
+    """Device buffers + the step of the Tempo op chain (weak-scaled rank)."""
+
+    def __init__(self, dev, rank, world, seed=1234):
+        import torch
+        from paper_2210_10246_b200 import ops
+        self.ops, self.torch, self.dev = ops, torch, dev
+        self.rank, self.world = rank, world
+        g = torch.Generator(device=dev)
+        g.manual_seed(seed + rank)
+        rn = lambda *s: torch.randn(*s, device=dev, generator=g)  # noqa: E731
+        self.table = ops.GeluTable.default()
+        # forward inputs (GEMM outputs in the real layer: synthetic here)
+        self.z = rn(ATT_ROWS, S)            # attention scores
+        self.x_attn_out = rn(T, H)          # attention output projection
+        self.x_ffn1 = rn(T, 4 * H)          # first FFN linear output
+        self.x_ffn2 = rn(T, H)              # second FFN linear output
+        self.g1 = (1 + 0.2 * rn(H)).contiguous()
+        self.b1 = (0.1 * rn(H)).contiguous()
+        self.g2 = (1 + 0.2 * rn(H)).contiguous()
+        self.b2 = (0.1 * rn(H)).contiguous()
+        # backward seeds (GEMM input-gradients in the real layer)
+        self.dy_ln2 = rn(T, H)
+        self.dy_gelu = rn(T, 4 * H)
+        self.dy_ln1 = rn(T, H)
+        self.dD = rn(ATT_ROWS, S)
+        # outputs / stashes, allocated once
+        e = torch.empty_like
+        mw = lambda n: torch.empty(ops.mask_words(n), dtype=torch.int32, device=dev)  # noqa: E731
+        self.P, self.D, self.m_att = e(self.z), e(self.z), mw(self.z.numel())
+        self.d1, self.m1 = e(self.x_attn_out), mw(T * H)
+        self.y_ln1, self.rs1 = e(self.x_attn_out), torch.empty(T, device=dev)
+        self.y_g, self.m_g = e(self.x_ffn1), mw(T * 4 * H)
+        self.d2, self.m2 = e(self.x_ffn2), mw(T * H)
+        self.y_ln2, self.rs2 = e(self.x_ffn2), torch.empty(T, device=dev)
+        self.dx_ln2, self.dx_d2 = e(self.x_ffn2), e(self.x_ffn2)
+        self.dx_g = e(self.x_ffn1)
+        self.dx_ln1, self.dx_d1 = e(self.x_attn_out), e(self.x_attn_out)
+        self.dZ, self.Drec = e(self.z), e(self.z)
+        self.dparams = torch.zeros(4 * H, device=dev)  # [dg2, db2, dg1, db1] bucket
+        self.ws = ops.ln_workspace(T, H, dev)
+        self.status = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.step_idx = 0
+        # global element offsets: rank shards reproduce the unsharded masks
+        self.off_att = rank * ATT_ROWS * S
+        self.off_h = rank * T * H
+
+    def retained_bytes(self):
+        """Bytes held between forward and backward by this chain (the stash):
+        P, the three dropout masks and the GELU mask (bits), GELU y, both LN
+        y + rstd.  D, the inputs and the grads are not retained."""
+        ts = [self.P, self.m_att, self.m1, self.y_ln1, self.rs1, self.y_g, self.m_g, self.m2,
+              self.y_ln2, self.rs2]
+        return int(sum(t.numel() * t.element_size() for t in ts))
+
+    def forward(self, seed):
+        o = self.ops
+        o.softmax_dropout_fwd(self.z, P_DROP, mask=self.m_att, generate=True, seed=seed,
+                              offset=self.off_att, P=self.P, D=self.D)
+        o.dropout_fwd(self.x_attn_out, P_DROP, mask=self.m1, generate=True, seed=seed + 1,
+                      offset=self.off_h, y=self.d1)
+        o.layernorm_ip_fwd(self.d1, self.g1, self.b1, check_gamma=False, y=self.y_ln1,
+                           rstd=self.rs1, dev_status=self.status)
+        o.gelu_ip_fwd(self.x_ffn1, self.table, y=self.y_g, mask=self.m_g)
+        o.dropout_fwd(self.x_ffn2, P_DROP, mask=self.m2, generate=True, seed=seed + 2,
+                      offset=self.off_h, y=self.d2)
+        o.layernorm_ip_fwd(self.d2, self.g2, self.b2, check_gamma=False, y=self.y_ln2,
+                           rstd=self.rs2, dev_status=self.status)
+
+    def backward(self, allreduce):
+        o = self.ops
+        dp = self.dparams
+        o.layernorm_ip_bwd(self.dy_ln2, self.y_ln2, self.rs2, self.g2, self.b2, dx=self.dx_ln2,
+                           dgamma=dp[0:H], dbeta=dp[H:2 * H], workspace=self.ws)
+        o.dropout_bwd(self.dx_ln2, self.m2, P_DROP, dx=self.dx_d2)
+        o.gelu_ip_bwd(self.dy_gelu, self.y_g, self.m_g, self.table, dx=self.dx_g)
+        o.layernorm_ip_bwd(self.dy_ln1, self.y_ln1, self.rs1, self.g1, self.b1, dx=self.dx_ln1,
+                           dgamma=dp[2 * H:3 * H], dbeta=dp[3 * H:], workspace=self.ws)
+        if allreduce is not None:
+            allreduce(dp)  # the one collective: bucketed LN dgamma/dbeta (16 KB)
+        o.dropout_bwd(self.dx_ln1, self.m1, P_DROP, dx=self.dx_d1)
+        o.attn_probs_bwd(self.dD, self.P, self.m_att, P_DROP, write_d=True, dZ=self.dZ,
+                         D=self.Drec)
+
+    def step(self, allreduce=None):
+        self.step_idx += 1
+        self.forward(1000 + 3 * self.step_idx)
+        self.backward(allreduce)
+
+    # kernels launched per step (ours): softmax fwd 1, dropout fwd 2, LN fwd 2,
+    # GELU fwd 1, LN bwd 2x(stage1+stage2), dropout bwd 2, GELU bwd 1, attn bwd 1
+    LAUNCHES_PER_STEP = 14
+
+    def per_op_timings(self, reps, flush):
+        """Per-kernel device time (CUDA events on the launching stream, L2
+        flushed before every rep), for the roofline and the per-op table."""
+        torch, o = self.torch, self.ops
+        dp = self.dparams
+        H_ = H
+        calls = {
+            "softmax_dropout_fwd": lambda: o.softmax_dropout_fwd(self.z, P_DROP, mask=self.m_att, generate=True, seed=7, P=self.P, D=self.D),
+            "attn_probs_bwd": lambda: o.attn_probs_bwd(self.dD, self.P, self.m_att, P_DROP, write_d=True, dZ=self.dZ, D=self.Drec),
+            "gelu_fwd": lambda: o.gelu_ip_fwd(self.x_ffn1, self.table, y=self.y_g, mask=self.m_g),
+            "gelu_bwd": lambda: o.gelu_ip_bwd(self.dy_gelu, self.y_g, self.m_g, self.table, dx=self.dx_g),
+            "layernorm_fwd": lambda: o.layernorm_ip_fwd(self.d1, self.g1, self.b1, check_gamma=False, y=self.y_ln1, rstd=self.rs1),
+            "layernorm_bwd": lambda: o.layernorm_ip_bwd(self.dy_ln1, self.y_ln1, self.rs1, self.g1, self.b1, dx=self.dx_ln1, dgamma=dp[:H_], dbeta=dp[H_:2 * H_], workspace=self.ws),
+            "dropout_fwd": lambda: o.dropout_fwd(self.x_ffn2, P_DROP, mask=self.m2, generate=True, seed=9, y=self.d2),
+            "dropout_bwd": lambda: o.dropout_bwd(self.dx_ln2, self.m2, P_DROP, dx=self.dx_d2),
+        }
+        # ops that run twice per step (both LNs / both dropouts): time one
+        # instance and count it twice
+        mult = {"layernorm_fwd": 2, "layernorm_bwd": 2, "dropout_fwd": 2, "dropout_bwd": 2}
+        out = {}
+        st = torch.cuda.current_stream()
+        for name, fn in calls.items():
+            fn()
+            ts = []
+            for _ in range(reps):
+                flush()
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(st)
+                fn()
+                b.record(st)
+                b.synchronize()
+                ts.append(a.elapsed_time(b))
+            out[name] = (statistics.median(ts) * mult.get(name, 1), mult.get(name, 1))
+        return out
+
+
+# ------------------------------------------------------------ clocks
+class ClockSampler:
+    def __init__(self, index=0):
+        self.index, self.proc, self.path = index, None, None
+
+    def start(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except Exception:
+            self.proc.kill()
+            out, _ = self.proc.communicate()
+        sm, mx, reasons = [], 0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(int(f[0]))
+                mx = max(mx, int(f[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return None
+        return {"sm_mhz": int(statistics.median(sm)), "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------ CPU reference arm
+def cpu_reference_sample(frac_rows: int, threads: int, steps: int, warmup: int):
+    """The reference's own CPU implementation (oracle/_ref/libtempo_ref.so,
+    compiled from /root/reference/proj/src) of the same chain on a bounded
+    row sample: 1/frac_rows of one rank's rows of every op, sharded across
+    `threads` host threads (one reference Graph per thread; distinct tapes may
+    run concurrently).  Returns (GB/s, seconds per step, sample)."""
+    import oracle
+    ref = oracle.Ref()
+    table = open(os.path.join(ROOT, "tests", "golden", "gelu_table_default_v1.txt")).read()
+    g = np.random.default_rng(0)
+    t_rows = T // frac_rows                # token rows of the sample
+    a_rows = ATT_ROWS // frac_rows         # attention rows of the sample
+    work = []  # per-thread closures
+    for k in range(threads):
+        tr = slice(k * t_rows // threads, (k + 1) * t_rows // threads)
+        ar = slice(k * a_rows // threads, (k + 1) * a_rows // threads)
+        nt, na = tr.stop - tr.start, ar.stop - ar.start
+        x_g = g.standard_normal(nt * 4 * H).astype(np.float32)
+        dy_g = g.standard_normal(nt * 4 * H).astype(np.float32)
+        x_ln = g.standard_normal((nt, H)).astype(np.float32)
+        dy_ln = g.standard_normal((nt, H)).astype(np.float32)
+        gam = (1 + 0.2 * g.standard_normal(H)).astype(np.float32)
+        bet = (0.1 * g.standard_normal(H)).astype(np.float32)
+        z = g.standard_normal((na, S)).astype(np.float32)
+        dD = g.standard_normal((na, S)).astype(np.float32)
+        keep_a = ref.bernoulli_keep(na * S, P_DROP, 11 + k)
+        keep_h = ref.bernoulli_keep(nt * H, P_DROP, 13 + k)
+        x_h = g.standard_normal(nt * H).astype(np.float32)
+
+        def job(x_g=x_g, dy_g=dy_g, x_ln=x_ln, dy_ln=dy_ln, gam=gam, bet=bet, z=z, dD=dD,
+                keep_a=keep_a, keep_h=keep_h, x_h=x_h):
+            ref.softmax_dropout(z, keep_a, P_DROP, dD)          # fwd + bwd + recompute D
+            for _ in range(2):
+                ref.dropout(x_h, keep_h, P_DROP, x_h)           # hidden dropouts fwd + bwd
+                ref.layernorm_ip(x_ln, gam, bet, dy_ln)          # both LNs fwd + bwd
+            ref.gelu_ip(table, x_g, dy_g)                       # GELU fwd + bwd
+        work.append(job)
+
+    def run_step():
+        ths = [threading.Thread(target=w) for w in work]
+        for t in ths:
+            t.start()
+        for t in ths:
+            t.join()
+
+    for _ in range(warmup):
+        run_step()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        run_step()
+    dt = (time.perf_counter() - t0) / steps
+    nbytes = sum(op_bytes().values()) / frac_rows
+    sample = (f"1/{frac_rows} of the per-GPU chain rows ({t_rows} tokens, {a_rows} attention "
+              f"rows; {nbytes / 1e9:.3f} GB algorithmic) per step, {threads} threads")
+    return nbytes / dt / 1e9, dt, sample
+
+
+# ---------------------------------------------------------------- main
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        return main_reference(args, rank, world)
+
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    chain = Chain(dev, rank, world)
+    allreduce = (lambda t: dist.all_reduce(t)) if world > 1 else None
+    flush_buf = torch.empty(256 * 1024 * 1024 // 4, device=dev)
+    flush = lambda: flush_buf.fill_(0.0)  # noqa: E731  (256 MB > 126 MB L2)
+
+    for _ in range(max(args.warmup, 3)):
+        chain.step(allreduce)
+    torch.cuda.synchronize()
+    if int(chain.status.item()) != 0:
+        raise RuntimeError("layernorm gamma refused on device")
+
+    # ---- timed region: K steps, barrier + sync on both sides -------------
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    st = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    for _ in range(args.steps):
+        chain.step(allreduce)
+    e1.record(st)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    ms = e0.elapsed_time(e1) / args.steps
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+
+    per_rank_bytes = sum(op_bytes().values())
+    value = per_rank_bytes * world / (ms * 1e-3) / 1e9
+    peak, peak_kind = peaks()
+
+    # ---- per-op device times (outside the timed region) -------------------
+    per_op = chain.per_op_timings(reps=5, flush=flush)
+    ob = op_bytes()
+    per_op_rows = []
+    for name, (t_ms, mult) in per_op.items():
+        gbs = ob[name] / (t_ms * 1e-3) / 1e9
+        per_op_rows.append({"op": name, "ms": round(t_ms, 4), "bytes": int(ob[name]),
+                            "gbs": round(gbs, 1), "frac": round(gbs / peak, 4),
+                            "launches": mult})
+    top = max(per_op_rows, key=lambda r: r["ms"])
+    roofline = {"bound": "hbm", "kernel": top["op"], "achieved": top["gbs"], "peak": peak,
+                "unit": "GB/s", "frac": top["frac"], "traffic": None,
+                "peak_kind": f"{peak_kind} copy bandwidth (MEASURED_PEAKS.json hbm_gbs)",
+                "bytes_per_launch": top["bytes"], "per_unit": "see DESIGN.md (SURVEY 8d)"}
+    prof_traffic = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(prof_traffic):
+        try:
+            tr = json.load(open(prof_traffic)).get(top["op"])
+            if tr:
+                roofline["traffic"] = tr
+        except Exception:
+            pass
+
+    # ---- e2e: the public API with host buffers -----------------------------
+    e2e = None
+    if not args.no_e2e:
+        e2e = e2e_measure(chain, args, world, allreduce, dist if world > 1 else None)
+
+    # ---- CPU baseline (reference library on host cores, rank 0, N=1) -------
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            threads = len(os.sched_getaffinity(0))
+            v, dt, sample = cpu_reference_sample(frac_rows=32, threads=threads, steps=2, warmup=1)
+            cpu = {"value": round(v, 4), "unit": "GB/s", "cores": threads, "kind": "reference",
+                   "sample": sample, "s_per_step": round(dt, 3)}
+        except Exception as ex:  # the reference library is prebuilt here; report if absent
+            cpu = {"value": None, "unit": "GB/s", "cores": 0, "kind": "reference",
+                   "sample": f"unavailable: {ex}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (torch.randn inputs of the layer shapes; Philox dropout masks)",
+            "config": {"workload": WORKLOAD, "batch_per_gpu": B, "global_batch": B * world,
+                       "seq_len": S, "hidden": H, "heads": A, "dropout_p": P_DROP,
+                       "parallelism": f"rows{world}", "l2": "working set 12.7 GB/step >> 126 MB L2",
+                       "baseline_config": "configs[3] at N=1; configs[4] (B=512) at N=8"},
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": Chain.LAUNCHES_PER_STEP * args.steps,
+            "clocks": clk,
+            "per_op": per_op_rows,
+            "frac_of_peak": round(value / world / peak, 4),
+            "stash": stash_report(chain),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def stash_report(chain):
+    from paper_2210_10246_b200 import ops
+    ref_tok = ops.layer_stash_bytes_per_token(S, H, A, tempo=False, mask_bits=False)
+    tmp1_tok = ops.layer_stash_bytes_per_token(S, H, A, tempo=True, mask_bits=False)
+    ours_tok = ops.layer_stash_bytes_per_token(S, H, A, tempo=True, mask_bits=True)
+    # in-path retained buffers, measured from the device allocations
+    measured = chain.retained_bytes()
+    # what the reference keeps for the SAME ops (memory_model.cpp:31-65): scores,
+    # probs, dropped-out map + 1-byte mask; both LN inputs + outputs; GELU input
+    # + output; 1-byte hidden dropout masks
+    ref_same = (3 * 4 + 1) * ATT_ROWS * S + 4 * (4 * T * H) + 2 * 4 * T * 4 * H + 2 * T * H
+    return {"unit": "bytes/layer", "tokens": T,
+            "reference_layer": ref_tok * T, "tempo_1byte_masks_layer": tmp1_tok * T,
+            "tempo_b200_layer": ours_tok * T,
+            "in_path_retained_measured": measured, "in_path_reference": ref_same,
+            "saving_vs_reference": round(1 - ours_tok / ref_tok, 4)}
+
+
+def e2e_measure(chain, args, world, allreduce, dist):
+    """Same metric through the public API with HOST buffers: every step
+    copies its inputs from pinned host memory (H2D) and reads every result
+    back (D2H) inside the timed region."""
+    torch = chain.torch
+    ins = [chain.z, chain.x_attn_out, chain.x_ffn1, chain.x_ffn2, chain.dy_ln2, chain.dy_gelu,
+           chain.dy_ln1, chain.dD]
+    outs = [chain.dZ, chain.dx_d1, chain.dx_g, chain.dx_d2, chain.dparams]
+    h_in = [torch.empty(t.shape, dtype=t.dtype, pin_memory=True).copy_(t) for t in ins]
+    h_out = [torch.empty(t.shape, dtype=t.dtype, pin_memory=True) for t in outs]
+    bi = sum(t.numel() * t.element_size() for t in ins)
+    bo = sum(t.numel() * t.element_size() for t in outs)
+
+    def step():
+        for d, h in zip(ins, h_in):
+            d.copy_(h, non_blocking=True)
+        chain.step(allreduce)
+        for h, d in zip(h_out, outs):
+            h.copy_(d, non_blocking=True)
+
+    step()
+    torch.cuda.synchronize()
+    k = max(1, min(args.steps, 5))
+    if dist is not None:
+        dist.barrier()
+    st = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    for _ in range(k):
+        step()
+    e1.record(st)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / k
+    if dist is not None:
+        t = torch.tensor([ms], device=chain.dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    v = sum(op_bytes().values()) * world / (ms * 1e-3) / 1e9
+    return {"value": round(v, 2), "unit": "GB/s", "h2d_bytes_per_step": int(bi),
+            "d2h_bytes_per_step": int(bo), "ms_per_step": round(ms, 3), "steps": k}
+
+
+def main_reference(args, rank, world):
+    """--impl reference: the reference's own CPU implementation of the path
+    (oracle/_ref, compiled from /root/reference/proj/src) on the host cores,
+    same metric/config/unit; each step a bounded sample (1/32 of one rank's
+    rows).  Under torchrun only rank 0 runs."""
+    if rank != 0:
+        return
+    threads = len(os.sched_getaffinity(0))
+    v, dt, sample = cpu_reference_sample(frac_rows=32, threads=threads, steps=args.steps,
+                                         warmup=max(1, min(args.warmup, 2)))
+    line = {
+        "metric": METRIC, "value": round(v, 4), "unit": "GB/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dt * 1e3, 2),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic", "impl": "reference",
+        "config": {"workload": WORKLOAD, "batch_per_gpu": B, "global_batch": B * world,
+                   "seq_len": S, "hidden": H, "heads": A, "dropout_p": P_DROP,
+                   "parallelism": f"rows{world}"},
+        "cpu_baseline": {"value": round(v, 4), "unit": "GB/s", "cores": threads,
+                         "kind": "reference", "sample": sample},
+        "e2e": {"value": round(v, 4), "unit": "GB/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

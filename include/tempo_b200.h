@@ -1,0 +1,206 @@
+/*
+ * tempo_b200.h -- the C-ABI drop-in boundary of the Tempo in-place
+ * activation operators (arXiv 2210.10246) on NVIDIA B200 (sm_100a).
+ *
+ * Every entry point replaces one reference interface; the citation next to it
+ * names the reference file:line (under /root/reference/proj) whose behaviour
+ * it reproduces.  INTEGRATION.md shows the binding a maintainer adds on the
+ * reference side (its C++ tempo_ops builders calling these from their
+ * forward bodies and BackwardFn closures).
+ *
+ * Conventions
+ *   - Tensor pointers are DEVICE pointers, caller-allocated, fp32, row-major,
+ *     contiguous.  Nothing here allocates device memory or retains a pointer
+ *     past the call (the LayerNorm backward's scratch is a caller workspace).
+ *   - Masks are bit-packed uint32 words: bit (i % 32) of word (i / 32) is
+ *     element i of the flattened tensor -- the reference's BoolMask byte
+ *     order (proj/src/tensor.cpp:199-201) at 1 bit instead of 1 byte.
+ *     bit 1 = kept (dropout, tensor.cpp:200) / right-of-minimum (GELU,
+ *     ops_tempo.cpp:78).
+ *   - Work is enqueued on `stream` (cudaStream_t; NULL = legacy default
+ *     stream) and is asynchronous; argument errors are reported before
+ *     anything is enqueued.
+ *   - Return value: TEMPO_OK or a tempo_status_t mirroring the reference's
+ *     exception taxonomy (proj/include/tempo/errors.hpp:14-61);
+ *     tempo_last_error() holds the message (thread-local).
+ *   - Reentrant; no global mutable state beyond a per-device launch-config
+ *     cache.  A table handle is immutable after creation and shareable.
+ */
+#ifndef TEMPO_B200_H
+#define TEMPO_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef void* tempo_stream_t; /* a cudaStream_t */
+
+/* errors.hpp:14-61, one code per exception class, plus device-side failures */
+typedef enum {
+    TEMPO_OK = 0,
+    TEMPO_ERR_UNKNOWN = 1,    /* tempo::Error                                  */
+    TEMPO_ERR_DIMENSION = 2,  /* DimensionError: shapes / sizes                 */
+    TEMPO_ERR_PARAM = 3,      /* ParamError: p not in [0,1), eps <= 0, |gamma|<1e-12 */
+    TEMPO_ERR_STATE = 4,      /* StateError                                     */
+    TEMPO_ERR_CONFIG = 5,     /* ConfigError: missing / unverified table        */
+    TEMPO_ERR_LIFECYCLE = 6,  /* LifecycleError                                 */
+    TEMPO_ERR_DOMAIN = 7,     /* DomainError                                    */
+    TEMPO_ERR_PARSE = 8,      /* ParseError: malformed v1 table text            */
+    TEMPO_ERR_FIT = 9,        /* FitError                                       */
+    TEMPO_ERR_INVARIANT = 10, /* InvariantError                                 */
+    TEMPO_ERR_ALIGNMENT = 11, /* pointer not aligned as the call requires       */
+    TEMPO_ERR_CUDA = 20,      /* a CUDA runtime error (message has the name)    */
+    TEMPO_ERR_UNSUPPORTED = 21
+} tempo_status_t;
+
+const char* tempo_last_error(void);
+const char* tempo_version(void);
+
+/* ---------------------------------------------------------------------- */
+/* GELU derivative-from-output table  (gelu_table.hpp:27-91)               */
+/* ---------------------------------------------------------------------- */
+typedef struct tempo_gelu_table_s* tempo_gelu_table_t;
+
+/* Parse + validate the v1 text form (GeluPolyTable::parse,
+ * gelu_table.cpp:227-301, tiling invariants :106-148).  Host only; the device
+ * copy travels as a kernel parameter, so no GPU is touched.  ParseError codes
+ * exactly where the reference throws. */
+int tempo_gelu_table_create(const char* v1_text, tempo_gelu_table_t* out);
+int tempo_gelu_table_destroy(tempo_gelu_table_t table);
+/* GeluPolyTable::minimum(), verified(), verified_max_error(), tolerance(),
+ * and the segment count/max degree (gelu_table.hpp:55-63). */
+int tempo_gelu_table_info(tempo_gelu_table_t table, double* x_star, double* y_min,
+                          double* tolerance, double* verified_max_error, int* verified,
+                          int* n_segments, int* max_degree);
+/* Re-serialize (GeluPolyTable::serialize, gelu_table.cpp:204-218);
+ * returns the needed length (without NUL) in *len. */
+int tempo_gelu_table_serialize(tempo_gelu_table_t table, char* buf, size_t cap, size_t* len);
+/* The table every default-configured reference process fits
+ * (fit::fit_table() with default FitOptions, gelu_fit.cpp:331-382),
+ * shipped as data so no fit runs at startup.  Static string. */
+const char* tempo_gelu_default_table_v1(void);
+/* Host-side GeluPolyTable::eval(y, m) (gelu_table.cpp:172-188), double. */
+int tempo_gelu_table_eval_host(tempo_gelu_table_t table, const double* y, const uint8_t* m,
+                               double* out, int64_t n);
+
+/* ---------------------------------------------------------------------- */
+/* In-Place GELU  (tempo_ops::gelu, ops_tempo.cpp:89-96 -> 32-87)          */
+/* ---------------------------------------------------------------------- */
+/* Forward: y = x*Phi(x) (math.hpp:26-28) and the branch mask
+ * m_i = x_i > table.x_star (ops_tempo.cpp:77-78).  mask has ceil(n/32) words.
+ * Refuses a NULL/empty table (ConfigError, ops_tempo.cpp:91-94). */
+int tempo_gelu_ip_fwd(const float* x, float* y, uint32_t* mask, int64_t n,
+                      tempo_gelu_table_t table, tempo_stream_t stream);
+/* Backward closure (ops_tempo.cpp:59-68 + gelu_spec :79-85):
+ * dx = dy * table.eval(y, m).  Refuses an unverified table with ConfigError
+ * (ops_tempo.cpp:80-83).  dx may alias dy (in place). */
+int tempo_gelu_ip_bwd(const float* dy, const float* y, const uint32_t* mask,
+                      tempo_gelu_table_t table, float* dx, int64_t n, tempo_stream_t stream);
+
+/* ---------------------------------------------------------------------- */
+/* In-Place LayerNorm  (tempo_ops::layernorm, ops_tempo.cpp:98-156)        */
+/* ---------------------------------------------------------------------- */
+/* Forward over rows of `cols`: two-pass moments (kernels.cpp:153-179), y =
+ * gamma*(x-mean)*rstd+beta (ops_reference.cpp:47-65), stashes y and
+ * rstd = 1/sqrt(var+eps) per row (ops_tempo.cpp:110-118).  eps <= 0 ->
+ * ParamError (ops_reference.cpp:50-52).  The |gamma_j| < 1e-12 refusal
+ * (ops_tempo.cpp:100-106) needs gamma's values: pass dev_status (an int32 in
+ * device memory, may be NULL) and the kernel writes TEMPO_ERR_PARAM there
+ * when any |gamma_j| < 1e-12, or call tempo_ln_check_gamma() up front. */
+int tempo_ln_ip_fwd(const float* x, const float* gamma, const float* beta, double eps,
+                    float* y, float* rstd, int64_t rows, int64_t cols, int32_t* dev_status,
+                    tempo_stream_t stream);
+/* Synchronous refusal check of ops_tempo.cpp:100-106 (copies gamma to host). */
+int tempo_ln_check_gamma(const float* gamma, int64_t cols, tempo_stream_t stream);
+/* Scratch bytes tempo_ln_ip_bwd needs (two-stage dgamma/dbeta reduction). */
+size_t tempo_ln_ip_bwd_workspace_size(int64_t rows, int64_t cols);
+/* Backward closure (ops_tempo.cpp:121-155): xhat = (y-beta)/gamma,
+ * s1 = sum g*gamma, s2 = sum g*gamma*xhat, dx = (g*gamma - s1/M -
+ * xhat*s2/M)*rstd; dgamma_j = sum_i g*xhat, dbeta_j = sum_i g over ALL rows,
+ * reduced in a fixed order (bitwise reproducible run to run). */
+int tempo_ln_ip_bwd(const float* dy, const float* y, const float* rstd, const float* gamma,
+                    const float* beta, float* dx, float* dgamma, float* dbeta, void* workspace,
+                    size_t workspace_bytes, int64_t rows, int64_t cols, tempo_stream_t stream);
+
+/* ---------------------------------------------------------------------- */
+/* Output-only softmax + Sub-Layer Dropout Recomputation                   */
+/* (tempo_ops::softmax ops_tempo.cpp:158-166, dropout_recompute :168-194)   */
+/* ---------------------------------------------------------------------- */
+typedef enum {
+    TEMPO_MASK_SUPPLIED = 0, /* mask is an input (e.g. the reference's
+                                BoolMask::bernoulli_keep stream, packed)     */
+    TEMPO_MASK_PHILOX = 1    /* mask is generated in-kernel (Philox4x32-10,
+                                counter = global element index + offset) and
+                                written: keep <=> u >= p, u = r * 2^-32       */
+} tempo_mask_mode_t;
+
+/* softmax_forward (ops_reference.cpp:104-125) alone. */
+int tempo_softmax_ip_fwd(const float* z, float* P, int64_t rows, int64_t cols,
+                         tempo_stream_t stream);
+/* softmax_backward_from_output (ops_reference.cpp:127-145): dZ = P*(dP - sum dP*P). */
+int tempo_softmax_ip_bwd(const float* dP, const float* P, float* dZ, int64_t rows, int64_t cols,
+                         tempo_stream_t stream);
+/* Fused forward: P = softmax(z) and D = dropout_apply(P, mask, p)
+ * (ops_reference.cpp:147-153) in one pass; the stash is P + mask bits only.
+ * `mask` is read (SUPPLIED) or written (PHILOX, with seed and
+ * `offset` = global index of element 0, so row shards reproduce the
+ * unsharded mask).  p not in [0,1) -> ParamError.  D may be NULL. */
+int tempo_softmax_dropout_fwd(const float* z, double p, tempo_mask_mode_t mode, uint32_t* mask,
+                              uint64_t seed, uint64_t offset, float* P, float* D, int64_t rows,
+                              int64_t cols, tempo_stream_t stream);
+/* Fused attention-probs backward: dropout_backward (ops_tempo.cpp:188-190),
+ * softmax_backward_from_output on the stashed P, and optionally the
+ * "dropout-rescale" recompute of D (ops_tempo.cpp:17-26, run by the
+ * consumer at tape.cpp:255-260) written to D_out (NULL = skip) -- bitwise
+ * equal to the forward D. */
+int tempo_attn_probs_bwd(const float* dD, const float* P, const uint32_t* mask, double p,
+                         float* dZ, float* D_out, int64_t rows, int64_t cols,
+                         tempo_stream_t stream);
+
+/* ---------------------------------------------------------------------- */
+/* Dropout with bit masks (dropout_apply / dropout_backward,               */
+/* ops_reference.cpp:147-161; ref_ops::dropout :214-225)                   */
+/* ---------------------------------------------------------------------- */
+/* y = mask ? x*(1/(1-p)) : 0.  SUPPLIED reads mask, PHILOX writes it.
+ * Also the recompute rule "dropout-rescale" (ops_tempo.cpp:17-26). */
+int tempo_dropout_fwd(const float* x, double p, tempo_mask_mode_t mode, uint32_t* mask,
+                      uint64_t seed, uint64_t offset, float* y, int64_t n, tempo_stream_t stream);
+/* dx = mask ? dy*(1/(1-p)) : 0.  dx may alias dy. */
+int tempo_dropout_bwd(const float* dy, const uint32_t* mask, double p, float* dx, int64_t n,
+                      tempo_stream_t stream);
+
+/* ---------------------------------------------------------------------- */
+/* Masks                                                                   */
+/* ---------------------------------------------------------------------- */
+/* BoolMask byte form <-> packed bits, on device.  pack refuses bytes > 1
+ * like BoolMask::from_bytes (tensor.cpp:205-220) by writing TEMPO_ERR_PARAM
+ * to dev_status (may be NULL). */
+int tempo_mask_pack(const uint8_t* bytes, uint32_t* bits, int64_t n, int32_t* dev_status,
+                    tempo_stream_t stream);
+int tempo_mask_unpack(const uint32_t* bits, uint8_t* bytes, int64_t n, tempo_stream_t stream);
+/* The reference's own mask stream, on the HOST, packed:
+ * BoolMask::bernoulli_keep(shape, p, seed) (tensor.cpp:186-203 --
+ * std::mt19937_64 + uniform_real_distribution<double>, keep <=> u >= p).
+ * bits has ceil(n/32) words. */
+int tempo_bernoulli_keep_bits_host(int64_t n, double p, uint64_t seed, uint32_t* bits);
+/* encoder::mask_stream_seed (encoder.cpp:39-46). */
+uint64_t tempo_mask_stream_seed(uint64_t mask_seed, uint64_t salt, int site);
+
+/* ---------------------------------------------------------------------- */
+/* Stash accounting (memory_model.cpp:31-137; ledger semantics)            */
+/* ---------------------------------------------------------------------- */
+/* Bytes one BERT layer retains between forward and backward, per token.
+ * mask_bits = 0: the reference's 1-byte masks (66H+13AS baseline,
+ * 46H+5AS+8 Tempo); mask_bits = 1: this library's bit-packed masks.
+ * tempo_variant = 0: baseline inventory, 1: all four Tempo optimizations. */
+int64_t tempo_layer_stash_bytes_per_token(int64_t seq, int64_t hidden, int64_t heads,
+                                          int tempo_variant, int mask_bits);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TEMPO_B200_H */

@@ -1,0 +1,127 @@
+// common.cuh -- device helpers shared by the Tempo in-place operator kernels.
+//
+// All kernels here are HBM-streaming kernels: 128-bit
+// coalesced loads/stores, read-once data loaded with L1::no_allocate and
+// written with the streaming (.cs) hint, grids sized as a multiple of the SM
+// count x resident CTAs per SM (grid-stride persistent loops).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace tb {
+
+constexpr int kWarp = 32;
+constexpr unsigned kFull = 0xffffffffu;
+
+// ---- streaming global memory access -------------------------------------
+__device__ __forceinline__ float4 ld_stream(const float4* p) {
+    float4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                 : "l"(p));
+    return v;
+}
+__device__ __forceinline__ float ld_stream(const float* p) {
+    float v;
+    asm volatile("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(v) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ uint32_t ld_stream(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(v) : "l"(p));
+    return v;
+}
+// Plain cached load (data read by several lanes / re-read from L2).
+__device__ __forceinline__ uint32_t ld_cached(const uint32_t* p) { return __ldg(p); }
+
+__device__ __forceinline__ void st_stream(float4* p, float4 v) {
+    asm volatile("st.global.cs.v4.f32 [%0], {%1,%2,%3,%4};"
+                 :
+                 : "l"(p), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
+                 : "memory");
+}
+__device__ __forceinline__ void st_stream(float* p, float v) {
+    asm volatile("st.global.cs.f32 [%0], %1;" : : "l"(p), "f"(v) : "memory");
+}
+__device__ __forceinline__ void st_stream(uint32_t* p, uint32_t v) {
+    asm volatile("st.global.cs.u32 [%0], %1;" : : "l"(p), "r"(v) : "memory");
+}
+
+// ---- bit-packed masks ----------------------------------------------------
+// Chunk = 128 consecutive elements handled by one warp, lane L owning
+// elements 4L..4L+3 (one float4).  The chunk's mask is 4 words; word w holds
+// lanes 8w..8w+7, bit (4j + k) = element 4(8w+j) + k: the linear BoolMask
+// order (tensor.cpp:199-201).
+//
+// pack: four warp ballots (one per float4 component) are bit-interleaved;
+// lane w (w < 4) returns word w.  Every lane computes its w = lane & 3 copy.
+__device__ __forceinline__ uint32_t spread8(uint32_t b) {  // bit j -> bit 4j
+    b &= 0xffu;
+    b = (b | (b << 12)) & 0x000f000fu;
+    b = (b | (b << 6)) & 0x03030303u;
+    b = (b | (b << 3)) & 0x11111111u;
+    return b;
+}
+__device__ __forceinline__ uint32_t pack_chunk_bits(bool k0, bool k1, bool k2, bool k3, int lane) {
+    uint32_t b0 = __ballot_sync(kFull, k0);
+    uint32_t b1 = __ballot_sync(kFull, k1);
+    uint32_t b2 = __ballot_sync(kFull, k2);
+    uint32_t b3 = __ballot_sync(kFull, k3);
+    int sh = 8 * (lane & 3);
+    return spread8(b0 >> sh) | (spread8(b1 >> sh) << 1) | (spread8(b2 >> sh) << 2) |
+           (spread8(b3 >> sh) << 3);
+}
+// unpack: the 4 bits of lane L's float4 from the chunk's word (L >> 3).
+__device__ __forceinline__ uint32_t chunk_nibble(const uint32_t* chunk_words, int lane) {
+    uint32_t w = ld_cached(chunk_words + (lane >> 3));
+    return (w >> (4 * (lane & 7))) & 0xfu;
+}
+
+// ---- Philox4x32-10 (Salmon et al., SC'11) --------------------------------
+struct U4 {
+    uint32_t x, y, z, w;
+};
+__device__ __forceinline__ U4 philox4x32_10(U4 c, uint32_t k0, uint32_t k1) {
+    const uint32_t M0 = 0xD2511F53u, M1 = 0xCD9E8D57u;
+    const uint32_t W0 = 0x9E3779B9u, W1 = 0xBB67AE85u;
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        uint32_t hi0 = __umulhi(M0, c.x), lo0 = M0 * c.x;
+        uint32_t hi1 = __umulhi(M1, c.z), lo1 = M1 * c.z;
+        c = U4{hi1 ^ c.y ^ k0, lo1, hi0 ^ c.w ^ k1, lo0};
+        k0 += W0;
+        k1 += W1;
+    }
+    return c;
+}
+// Four uniform draws for elements 4q..4q+3 of a tensor whose element 0 has
+// global index `offset` (offset % 4 == 0 required for the vector paths; the
+// scalar path draws per element with the same counter mapping).
+__device__ __forceinline__ U4 philox_quad(uint64_t seed, uint64_t quad_index) {
+    U4 c{(uint32_t)quad_index, (uint32_t)(quad_index >> 32), 0x7e3a1b5du, 0x0u};
+    return philox4x32_10(c, (uint32_t)seed, (uint32_t)(seed >> 32));
+}
+__device__ __forceinline__ uint32_t philox_at(uint64_t seed, uint64_t global_index) {
+    U4 r = philox_quad(seed, global_index >> 2);
+    switch (global_index & 3) {
+        case 0: return r.x;
+        case 1: return r.y;
+        case 2: return r.z;
+        default: return r.w;
+    }
+}
+
+// ---- warp reductions -----------------------------------------------------
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+    return v;
+}
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(kFull, v, o));
+    return v;
+}
+
+}  // namespace tb

@@ -1,0 +1,182 @@
+// dropout_kernels.cu -- elementwise dropout with bit-packed masks (sm_100a).
+//
+// dropout_apply / dropout_backward (ops_reference.cpp:147-161 -> mask_scale
+// kernels.cpp:285-295): out = mask ? in * (1/(1-p)) : 0, the product taken
+// in fp64 and rounded once, so results are bit-exact with the reference on
+// the same inputs.  Used for the hidden dropouts (ref_ops::dropout,
+// ops_reference.cpp:214-225; encoder.cpp:180-184, 200-203) and as the
+// "dropout-rescale" recompute rule (ops_tempo.cpp:17-26).
+// HBM: read 4 B + write 4 B + 1 bit  = 8.125 B/elem each direction.
+//
+// Plus the BoolMask byte <-> bit converters (tensor.cpp:205-220).
+#include "common.cuh"
+#include "tempo_internal.h"
+
+namespace tb {
+namespace {
+
+constexpr int kBlock = 256;
+constexpr int kUnroll = 2;
+
+__device__ __forceinline__ float dscale(float v, double s) { return (float)((double)v * s); }
+
+// PHILOX: generate + write the mask; otherwise read it.
+template <bool PHILOX>
+__device__ __forceinline__ void dropout_scalar_words(const float* __restrict__ x,
+                                                     uint32_t* __restrict__ mask, double scale,
+                                                     uint64_t thresh, uint64_t seed,
+                                                     uint64_t offset, float* __restrict__ y,
+                                                     int64_t n, int64_t w_begin, int64_t w_step,
+                                                     int lane) {
+    const int64_t nwords = (n + 31) >> 5;
+    for (int64_t w = w_begin; w < nwords; w += w_step) {
+        const int64_t i = (w << 5) + lane;
+        const bool in = i < n;
+        bool keep;
+        if (PHILOX) {
+            keep = in && (uint64_t)philox_at(seed, offset + (uint64_t)i) >= thresh;
+            uint32_t bits = __ballot_sync(kFull, keep);
+            if (lane == 0) mask[w] = bits;
+        } else {
+            keep = (mask[w] >> lane) & 1u;
+        }
+        if (in) y[i] = keep ? dscale(x[i], scale) : 0.0f;
+    }
+}
+
+template <bool PHILOX>
+__global__ void __launch_bounds__(kBlock) dropout_fwd_vec_kernel(
+    const float* __restrict__ x, uint32_t* __restrict__ mask, double scale, uint64_t thresh,
+    uint64_t seed, uint64_t offset, float* __restrict__ y, int64_t n) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = ((int64_t)blockIdx.x * kBlock + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * kBlock) >> 5;
+    const int64_t nchunks = n >> 7;
+    const float4* x4 = reinterpret_cast<const float4*>(x);
+    float4* y4 = reinterpret_cast<float4*>(y);
+    for (int64_t c0 = warp * kUnroll; c0 < nchunks; c0 += nwarps * kUnroll) {
+        float4 v[kUnroll];
+        uint32_t nib[kUnroll];
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+            if (c0 + u < nchunks) {
+                v[u] = ld_stream(x4 + ((c0 + u) << 5) + lane);
+                if (!PHILOX) nib[u] = chunk_nibble(mask + ((c0 + u) << 2), lane);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+            if (c0 + u < nchunks) {
+                if (PHILOX) {
+                    const uint64_t e0 = ((uint64_t)(c0 + u) << 7) + (uint64_t)lane * 4;
+                    U4 r = philox_quad(seed, (offset + e0) >> 2);
+                    bool k0 = (uint64_t)r.x >= thresh, k1 = (uint64_t)r.y >= thresh;
+                    bool k2 = (uint64_t)r.z >= thresh, k3 = (uint64_t)r.w >= thresh;
+                    uint32_t word = pack_chunk_bits(k0, k1, k2, k3, lane);
+                    if (lane < 4) st_stream(mask + ((c0 + u) << 2) + lane, word);
+                    nib[u] = (uint32_t)k0 | ((uint32_t)k1 << 1) | ((uint32_t)k2 << 2) |
+                             ((uint32_t)k3 << 3);
+                }
+                float4 o;
+                o.x = (nib[u] & 1u) ? dscale(v[u].x, scale) : 0.0f;
+                o.y = (nib[u] & 2u) ? dscale(v[u].y, scale) : 0.0f;
+                o.z = (nib[u] & 4u) ? dscale(v[u].z, scale) : 0.0f;
+                o.w = (nib[u] & 8u) ? dscale(v[u].w, scale) : 0.0f;
+                st_stream(y4 + ((c0 + u) << 5) + lane, o);
+            }
+        }
+    }
+    if (warp == nwarps - 1)
+        dropout_scalar_words<PHILOX>(x, mask, scale, thresh, seed, offset, y, n, nchunks << 2, 1,
+                                     lane);
+}
+
+template <bool PHILOX>
+__global__ void __launch_bounds__(kBlock) dropout_fwd_scalar_kernel(
+    const float* __restrict__ x, uint32_t* __restrict__ mask, double scale, uint64_t thresh,
+    uint64_t seed, uint64_t offset, float* __restrict__ y, int64_t n) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = ((int64_t)blockIdx.x * kBlock + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * kBlock) >> 5;
+    dropout_scalar_words<PHILOX>(x, mask, scale, thresh, seed, offset, y, n, warp, nwarps, lane);
+}
+
+// Byte mask -> bits; a byte > 1 is a ParamError (BoolMask::from_bytes).
+__global__ void __launch_bounds__(kBlock) mask_pack_kernel(const uint8_t* __restrict__ bytes,
+                                                           uint32_t* __restrict__ bits, int64_t n,
+                                                           int32_t* __restrict__ status) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = ((int64_t)blockIdx.x * kBlock + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * kBlock) >> 5;
+    const int64_t nwords = (n + 31) >> 5;
+    for (int64_t w = warp; w < nwords; w += nwarps) {
+        const int64_t i = (w << 5) + lane;
+        uint8_t b = i < n ? bytes[i] : 0;
+        if (b > 1 && status) *status = TEMPO_ERR_PARAM;
+        uint32_t word = __ballot_sync(kFull, b != 0);
+        if (lane == 0) bits[w] = word;
+    }
+}
+
+__global__ void __launch_bounds__(kBlock) mask_unpack_kernel(const uint32_t* __restrict__ bits,
+                                                             uint8_t* __restrict__ bytes,
+                                                             int64_t n) {
+    const int64_t stride = (int64_t)gridDim.x * kBlock;
+    for (int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x; i < n; i += stride)
+        bytes[i] = (bits[i >> 5] >> (i & 31)) & 1u;
+}
+
+inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+template <bool PHILOX>
+cudaError_t fwd(const float* x, double scale, uint64_t thresh, uint32_t* mask, uint64_t seed,
+                uint64_t offset, float* y, int64_t n, cudaStream_t st) {
+    const bool vec = aligned16(x) && aligned16(y) && aligned16(mask) && (offset & 3u) == 0;
+    if (vec) {
+        auto k = dropout_fwd_vec_kernel<PHILOX>;
+        const int64_t warps = ((n >> 7) + kUnroll - 1) / kUnroll + 1;
+        int grid = grid_for((const void*)k, kBlock, 0, (warps * 32 + kBlock - 1) / kBlock);
+        k<<<grid, kBlock, 0, st>>>(x, mask, scale, thresh, seed, offset, y, n);
+    } else {
+        auto k = dropout_fwd_scalar_kernel<PHILOX>;
+        const int64_t warps = (n + 31) >> 5;
+        int grid = grid_for((const void*)k, kBlock, 0, (warps * 32 + kBlock - 1) / kBlock);
+        k<<<grid, kBlock, 0, st>>>(x, mask, scale, thresh, seed, offset, y, n);
+    }
+    return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t launch_dropout_fwd(const float* x, double scale, uint64_t thresh, int philox,
+                               uint32_t* mask, uint64_t seed, uint64_t offset, float* y, int64_t n,
+                               cudaStream_t st) {
+    if (n == 0) return cudaSuccess;
+    return philox ? fwd<true>(x, scale, thresh, mask, seed, offset, y, n, st)
+                  : fwd<false>(x, scale, thresh, mask, seed, offset, y, n, st);
+}
+
+cudaError_t launch_dropout_bwd(const float* dy, const uint32_t* mask, double scale, float* dx,
+                               int64_t n, cudaStream_t st) {
+    if (n == 0) return cudaSuccess;
+    // dropout_backward is mask_scale on the gradient: the SUPPLIED forward.
+    return fwd<false>(dy, scale, 0, const_cast<uint32_t*>(mask), 0, 0, dx, n, st);
+}
+
+cudaError_t launch_mask_pack(const uint8_t* bytes, uint32_t* bits, int64_t n, int32_t* status,
+                             cudaStream_t st) {
+    if (n == 0) return cudaSuccess;
+    const int64_t warps = (n + 31) >> 5;
+    int grid = grid_for((const void*)mask_pack_kernel, kBlock, 0, (warps * 32 + kBlock - 1) / kBlock);
+    mask_pack_kernel<<<grid, kBlock, 0, st>>>(bytes, bits, n, status);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_mask_unpack(const uint32_t* bits, uint8_t* bytes, int64_t n, cudaStream_t st) {
+    if (n == 0) return cudaSuccess;
+    int grid = grid_for((const void*)mask_unpack_kernel, kBlock, 0, (n + kBlock - 1) / kBlock);
+    mask_unpack_kernel<<<grid, kBlock, 0, st>>>(bits, bytes, n);
+    return cudaGetLastError();
+}
+
+}  // namespace tb

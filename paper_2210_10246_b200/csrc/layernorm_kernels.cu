@@ -1,0 +1,386 @@
+// layernorm_kernels.cu -- In-Place LayerNorm forward/backward for sm_100a.
+//
+// Forward  (tempo_ops::layernorm, ops_tempo.cpp:98-119 -> layernorm_forward
+//           ops_reference.cpp:47-65 -> row_moments kernels.cpp:153-179):
+//   mean = sum x / M and var = sum (x - mean)^2 / M in fp64 (two-pass, as the
+//   reference), both rounded to fp32 like its F32-stored moments; y =
+//   gamma * ((x - mean_f) * rstd) + beta with rstd = 1/sqrt(var_f + eps),
+//   evaluated in fp64 WITHOUT contraction (the reference's x86-64 build has
+//   no FMA), so y matches the reference bit for bit whenever the row sums
+//   agree.  Stash: y and rstd[row] only.
+//   HBM: read x (4 B) + write y (4 B) per element, + 4 B/row + 8 B/column.
+// Backward (closure ops_tempo.cpp:121-155): xhat = (y - beta)/gamma,
+//   s1 = sum g*gamma, s2 = sum g*gamma*xhat (fp64 row reductions),
+//   dx = (g*gamma - s1/M - xhat*s2/M) * rstd; dgamma/dbeta: fp64 per-CTA
+//   column partials (stage 1, in registers) reduced across CTAs in a fixed
+//   order by a second kernel (stage 2) -- bitwise reproducible.
+//   HBM: read dy, y (8 B) + write dx (4 B) per element, + rows/cols terms.
+//
+// Layout: a CTA spans the columns of a row (thread t owns the float4 at
+// column 4t), gamma/beta for its columns stay in registers, and the CTA
+// walks rows with a grid stride, kRows rows in flight.  Row reductions are
+// warp shuffles plus one smem exchange (fixed order, identical in every
+// thread).  cols % 4 != 0, cols > 2048 or unaligned pointers use the
+// generic kernels (one element per thread per pass).
+#include "common.cuh"
+#include "tempo_internal.h"
+
+namespace tb {
+namespace {
+
+constexpr int kRows = 4;           // rows in flight per CTA iteration (forward)
+constexpr int kRowsB = 2;          // rows in flight per CTA iteration (backward)
+constexpr int kMaxThreads = 512;  // cols <= 2048 on the vector path
+constexpr double kGammaMin = 1e-12;  // ops_tempo.hpp:46
+
+// Block-wide fp64 sum of kN values per thread.  `red` holds 2 buffers of
+// [kN][32] doubles; `phase` alternates so one __syncthreads per reduction
+// suffices.  Every thread gets the same result (fixed summation order).
+template <int kN>
+__device__ __forceinline__ void block_sum(double (&v)[kN], double* red, int& phase) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int nw = blockDim.x >> 5;
+    double* buf = red + phase * (kN * 32);
+#pragma unroll
+    for (int i = 0; i < kN; ++i) {
+        double s = warp_sum(v[i]);
+        if (lane == 0) buf[i * 32 + wid] = s;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < kN; ++i) {
+        double s = 0.0;
+        for (int w = 0; w < nw; ++w) s += buf[i * 32 + w];
+        v[i] = s;
+    }
+    phase ^= 1;
+}
+
+__device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
+
+// y = gamma * ((x - mean) * rs) + beta, no contraction (ops_reference.cpp:61-62).
+__device__ __forceinline__ float ln_y(float x, double mean_f, double rs, double g, double b) {
+    return (float)dadd(dmul(g, dmul(dadd((double)x, -mean_f), rs)), b);
+}
+
+// ------------------------------------------------------------------ forward
+__global__ void __launch_bounds__(kMaxThreads) ln_fwd_vec_kernel(
+    const float* __restrict__ x, const float* __restrict__ gamma, const float* __restrict__ beta,
+    double eps, float* __restrict__ y, float* __restrict__ rstd, int64_t rows, int cols,
+    int32_t* __restrict__ status) {
+    __shared__ double red[2 * 2 * kRows * 32];
+    int phase = 0;
+    const int c4 = threadIdx.x;  // float4 column group
+    const bool act = c4 * 4 < cols;
+    float4 g = make_float4(1.f, 1.f, 1.f, 1.f), b = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (act) {
+        g = reinterpret_cast<const float4*>(gamma)[c4];
+        b = reinterpret_cast<const float4*>(beta)[c4];
+        if (status && blockIdx.x == 0) {
+            if (fabs((double)g.x) < kGammaMin || fabs((double)g.y) < kGammaMin ||
+                fabs((double)g.z) < kGammaMin || fabs((double)g.w) < kGammaMin) {
+                *status = TEMPO_ERR_PARAM;
+            }
+        }
+    }
+    for (int64_t r0 = (int64_t)blockIdx.x * kRows; r0 < rows; r0 += (int64_t)gridDim.x * kRows) {
+        float4 v[kRows];
+        double s[kRows];
+#pragma unroll
+        for (int i = 0; i < kRows; ++i) {
+            v[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (act && r0 + i < rows)
+                v[i] = ld_stream(reinterpret_cast<const float4*>(x + (r0 + i) * cols) + c4);
+            s[i] = ((double)v[i].x + (double)v[i].y) + ((double)v[i].z + (double)v[i].w);
+        }
+        block_sum<kRows>(s, red, phase);
+        double mean[kRows], q[kRows];
+#pragma unroll
+        for (int i = 0; i < kRows; ++i) {
+            mean[i] = s[i] / (double)cols;  // kernels.cpp:170
+            double d0 = (double)v[i].x - mean[i], d1 = (double)v[i].y - mean[i];
+            double d2 = (double)v[i].z - mean[i], d3 = (double)v[i].w - mean[i];
+            q[i] = act ? dadd(dadd(dmul(d0, d0), dmul(d1, d1)), dadd(dmul(d2, d2), dmul(d3, d3)))
+                       : 0.0;
+        }
+        block_sum<kRows>(q, red, phase);
+#pragma unroll
+        for (int i = 0; i < kRows; ++i) {
+            const int64_t r = r0 + i;
+            if (r >= rows) break;
+            const double mean_f = (double)(float)mean[i];    // F32 store, kernels.cpp:174
+            const float var_f = (float)(q[i] / (double)cols);  // F32 store, kernels.cpp:176
+            const double rs = 1.0 / sqrt((double)var_f + eps);  // ops_reference.cpp:58
+            if (act) {
+                float4 o;
+                o.x = ln_y(v[i].x, mean_f, rs, (double)g.x, (double)b.x);
+                o.y = ln_y(v[i].y, mean_f, rs, (double)g.y, (double)b.y);
+                o.z = ln_y(v[i].z, mean_f, rs, (double)g.z, (double)b.z);
+                o.w = ln_y(v[i].w, mean_f, rs, (double)g.w, (double)b.w);
+                st_stream(reinterpret_cast<float4*>(y + r * cols) + c4, o);
+            }
+            if (threadIdx.x == 0) rstd[r] = (float)rs;  // ops_tempo.cpp:111-112
+        }
+    }
+}
+
+// Generic: any cols, any alignment; thread t handles columns t, t+bs, ...
+// Three passes over the row (L1/L2 resident for moderate cols).
+__global__ void __launch_bounds__(256) ln_fwd_generic_kernel(
+    const float* __restrict__ x, const float* __restrict__ gamma, const float* __restrict__ beta,
+    double eps, float* __restrict__ y, float* __restrict__ rstd, int64_t rows, int cols,
+    int32_t* __restrict__ status) {
+    __shared__ double red[2 * 32];
+    int phase = 0;
+    if (status && blockIdx.x == 0) {
+        for (int j = threadIdx.x; j < cols; j += blockDim.x)
+            if (fabs((double)gamma[j]) < kGammaMin) *status = TEMPO_ERR_PARAM;
+    }
+    for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
+        const float* xr = x + r * cols;
+        double s[1] = {0.0};
+        for (int j = threadIdx.x; j < cols; j += blockDim.x) s[0] += (double)xr[j];
+        block_sum<1>(s, red, phase);
+        const double mean = s[0] / (double)cols;
+        double q[1] = {0.0};
+        for (int j = threadIdx.x; j < cols; j += blockDim.x) {
+            double d = (double)xr[j] - mean;
+            q[0] = dadd(q[0], dmul(d, d));
+        }
+        block_sum<1>(q, red, phase);
+        const double mean_f = (double)(float)mean;
+        const float var_f = (float)(q[0] / (double)cols);
+        const double rs = 1.0 / sqrt((double)var_f + eps);
+        for (int j = threadIdx.x; j < cols; j += blockDim.x)
+            y[r * cols + j] = ln_y(xr[j], mean_f, rs, (double)gamma[j], (double)beta[j]);
+        if (threadIdx.x == 0) rstd[r] = (float)rs;
+    }
+}
+
+// ----------------------------------------------------------------- backward
+// Stage 1, vector path: dx per row, per-CTA fp64 column partials of
+// dgamma = sum g*xhat and dbeta = sum g, written to ws[cta][2][cols].
+__global__ void __launch_bounds__(kMaxThreads) ln_bwd_vec_kernel(
+    const float* __restrict__ dy, const float* __restrict__ y, const float* __restrict__ rstd,
+    const float* __restrict__ gamma, const float* __restrict__ beta, float* __restrict__ dx,
+    double* __restrict__ ws, int64_t rows, int cols) {
+    __shared__ double red[2 * 2 * kRowsB * 32];
+    int phase = 0;
+    const int c4 = threadIdx.x;
+    const bool act = c4 * 4 < cols;
+    double gm[4] = {1, 1, 1, 1}, bt[4] = {0, 0, 0, 0}, ig[4] = {1, 1, 1, 1};
+    if (act) {
+        float4 g = reinterpret_cast<const float4*>(gamma)[c4];
+        float4 b = reinterpret_cast<const float4*>(beta)[c4];
+        gm[0] = g.x; gm[1] = g.y; gm[2] = g.z; gm[3] = g.w;
+        bt[0] = b.x; bt[1] = b.y; bt[2] = b.z; bt[3] = b.w;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) ig[k] = 1.0 / gm[k];
+    }
+    double pg[4] = {0, 0, 0, 0}, pb[4] = {0, 0, 0, 0};  // column partials
+    const double inv_m = 1.0 / (double)cols;
+    for (int64_t r0 = (int64_t)blockIdx.x * kRowsB; r0 < rows; r0 += (int64_t)gridDim.x * kRowsB) {
+        float4 gv[kRowsB], yv[kRowsB];
+        float rsv[kRowsB];
+#pragma unroll
+        for (int i = 0; i < kRowsB; ++i) {
+            gv[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+            yv[i] = gv[i];
+            rsv[i] = 0.f;
+            if (r0 + i < rows) {
+                if (act) {
+                    gv[i] = ld_stream(reinterpret_cast<const float4*>(dy + (r0 + i) * cols) + c4);
+                    yv[i] = ld_stream(reinterpret_cast<const float4*>(y + (r0 + i) * cols) + c4);
+                }
+                rsv[i] = __ldg(rstd + r0 + i);
+            }
+        }
+        double s[2 * kRowsB];
+#pragma unroll
+        for (int i = 0; i < kRowsB; ++i) {
+            const float ga[4] = {gv[i].x, gv[i].y, gv[i].z, gv[i].w};
+            const float ya[4] = {yv[i].x, yv[i].y, yv[i].z, yv[i].w};
+            double s1 = 0.0, s2 = 0.0;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                double gg = (double)ga[k] * gm[k];
+                double xh = ((double)ya[k] - bt[k]) * ig[k];
+                s1 += gg;
+                s2 += gg * xh;
+            }
+            s[2 * i] = act ? s1 : 0.0;
+            s[2 * i + 1] = act ? s2 : 0.0;
+        }
+        block_sum<2 * kRowsB>(s, red, phase);
+#pragma unroll
+        for (int i = 0; i < kRowsB; ++i) {
+            if (r0 + i >= rows || !act) continue;
+            const double c1 = s[2 * i] * inv_m, c2 = s[2 * i + 1] * inv_m;
+            const double rs = (double)rsv[i];
+            const float ga[4] = {gv[i].x, gv[i].y, gv[i].z, gv[i].w};
+            const float ya[4] = {yv[i].x, yv[i].y, yv[i].z, yv[i].w};
+            float o[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                double g = (double)ga[k];
+                double xh = ((double)ya[k] - bt[k]) * ig[k];
+                o[k] = (float)((g * gm[k] - c1 - xh * c2) * rs);
+                pg[k] += g * xh;
+                pb[k] += g;
+            }
+            st_stream(reinterpret_cast<float4*>(dx + (r0 + i) * cols) + c4,
+                      make_float4(o[0], o[1], o[2], o[3]));
+        }
+    }
+    if (act) {
+        double* wg = ws + (size_t)blockIdx.x * 2 * cols;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            wg[c4 * 4 + k] = pg[k];
+            wg[cols + c4 * 4 + k] = pb[k];
+        }
+    }
+}
+
+// Stage 1, generic path: partials accumulated in shared memory (each column
+// owned by one thread, so no races), then written to ws[cta][2][cols].
+__global__ void __launch_bounds__(256) ln_bwd_generic_kernel(
+    const float* __restrict__ dy, const float* __restrict__ y, const float* __restrict__ rstd,
+    const float* __restrict__ gamma, const float* __restrict__ beta, float* __restrict__ dx,
+    double* __restrict__ ws, int64_t rows, int cols) {
+    extern __shared__ double part[];  // [2][cols]
+    __shared__ double red[2 * 2 * 32];
+    int phase = 0;
+    for (int j = threadIdx.x; j < 2 * cols; j += blockDim.x) part[j] = 0.0;
+    const double inv_m = 1.0 / (double)cols;
+    for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
+        const float* gr = dy + r * cols;
+        const float* yr = y + r * cols;
+        double s[2] = {0.0, 0.0};
+        for (int j = threadIdx.x; j < cols; j += blockDim.x) {
+            double gg = (double)gr[j] * (double)gamma[j];
+            double xh = ((double)yr[j] - (double)beta[j]) / (double)gamma[j];
+            s[0] += gg;
+            s[1] += gg * xh;
+        }
+        block_sum<2>(s, red, phase);
+        const double c1 = s[0] * inv_m, c2 = s[1] * inv_m, rs = (double)rstd[r];
+        for (int j = threadIdx.x; j < cols; j += blockDim.x) {
+            double g = (double)gr[j];
+            double xh = ((double)yr[j] - (double)beta[j]) / (double)gamma[j];
+            dx[r * cols + j] = (float)((g * (double)gamma[j] - c1 - xh * c2) * rs);
+            part[j] += g * xh;
+            part[cols + j] += g;
+        }
+    }
+    __syncthreads();
+    double* wg = ws + (size_t)blockIdx.x * 2 * cols;
+    for (int j = threadIdx.x; j < 2 * cols; j += blockDim.x) wg[j] = part[j];
+}
+
+// Stage 2: out[j] = sum over CTAs c (fixed order) of ws[c][j], j < 2*cols.
+// One warp per 4 consecutive outputs; lanes stride over c, then a butterfly
+// (identical result in every lane).
+__global__ void __launch_bounds__(256) ln_param_reduce_kernel(const double* __restrict__ ws,
+                                                              int nparts, int cols,
+                                                              float* __restrict__ dgamma,
+                                                              float* __restrict__ dbeta) {
+    const int lane = threadIdx.x & 31;
+    const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t j0 = wid * 4;
+    const int64_t total = 2 * (int64_t)cols;
+    if (j0 >= total) return;
+    double acc[4] = {0, 0, 0, 0};
+    for (int c = lane; c < nparts; c += 32) {
+        const double* row = ws + (size_t)c * total;
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            if (j0 + k < total) acc[k] += row[j0 + k];
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        double v = warp_sum(acc[k]);
+        if (lane == 0 && j0 + k < total) {
+            int64_t j = j0 + k;
+            if (j < cols) dgamma[j] = (float)v; else dbeta[j - cols] = (float)v;
+        }
+    }
+}
+
+inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+bool use_vec(int64_t cols, const void* a, const void* b, const void* c, const void* d,
+             const void* e) {
+    return cols % 4 == 0 && cols <= 4 * kMaxThreads && aligned16(a) && aligned16(b) &&
+           aligned16(c) && aligned16(d) && aligned16(e);
+}
+
+int vec_threads(int64_t cols) { return (int)(((cols / 4) + 31) / 32 * 32); }
+
+// Stage-1 grid for the backward: its CTA count is also the number of
+// partial rows in the workspace, so it depends only on (rows, cols, device).
+int bwd_grid(int64_t rows, int64_t cols, bool vec) {
+    int64_t work = vec ? (rows + kRowsB - 1) / kRowsB : rows;
+    const void* k = vec ? (const void*)ln_bwd_vec_kernel : (const void*)ln_bwd_generic_kernel;
+    int block = vec ? vec_threads(cols) : 256;
+    size_t smem = vec ? 0 : (size_t)2 * cols * sizeof(double);
+    return grid_for(k, block, smem, work);
+}
+
+}  // namespace
+
+cudaError_t launch_ln_fwd(const float* x, const float* gamma, const float* beta, double eps,
+                          float* y, float* rstd, int64_t rows, int64_t cols, int32_t* dev_status,
+                          cudaStream_t st) {
+    if (rows == 0) return cudaSuccess;
+    if (use_vec(cols, x, y, gamma, beta, x)) {
+        int block = vec_threads(cols);
+        int grid = grid_for((const void*)ln_fwd_vec_kernel, block, 0, (rows + kRows - 1) / kRows);
+        ln_fwd_vec_kernel<<<grid, block, 0, st>>>(x, gamma, beta, eps, y, rstd, rows, (int)cols,
+                                                   dev_status);
+    } else {
+        int grid = grid_for((const void*)ln_fwd_generic_kernel, 256, 0, rows);
+        ln_fwd_generic_kernel<<<grid, 256, 0, st>>>(x, gamma, beta, eps, y, rstd, rows,
+                                                     (int)cols, dev_status);
+    }
+    return cudaGetLastError();
+}
+
+size_t ln_bwd_workspace(int64_t rows, int64_t cols) {
+    if (rows == 0 || cols == 0) return 0;
+    // The vector/generic choice also depends on pointer alignment; size for
+    // the larger of the two grids.
+    int gv = (cols % 4 == 0 && cols <= 4 * kMaxThreads) ? bwd_grid(rows, cols, true) : 0;
+    int gg = bwd_grid(rows, cols, false);
+    int g = gv > gg ? gv : gg;
+    return (size_t)g * 2 * (size_t)cols * sizeof(double);
+}
+
+cudaError_t launch_ln_bwd(const float* dy, const float* y, const float* rstd, const float* gamma,
+                          const float* beta, float* dx, float* dgamma, float* dbeta, void* ws,
+                          int64_t rows, int64_t cols, cudaStream_t st) {
+    if (cols == 0) return cudaSuccess;
+    if (rows == 0) {
+        cudaMemsetAsync(dgamma, 0, cols * sizeof(float), st);
+        cudaMemsetAsync(dbeta, 0, cols * sizeof(float), st);
+        return cudaGetLastError();
+    }
+    const bool vec = use_vec(cols, dy, y, dx, gamma, beta);
+    const int grid = bwd_grid(rows, cols, vec);
+    double* w = static_cast<double*>(ws);
+    if (vec) {
+        ln_bwd_vec_kernel<<<grid, vec_threads(cols), 0, st>>>(dy, y, rstd, gamma, beta, dx, w,
+                                                              rows, (int)cols);
+    } else {
+        size_t smem = (size_t)2 * cols * sizeof(double);
+        ln_bwd_generic_kernel<<<grid, 256, smem, st>>>(dy, y, rstd, gamma, beta, dx, w, rows,
+                                                       (int)cols);
+    }
+    const int64_t warps = (2 * cols + 3) / 4;
+    const int rgrid = (int)((warps * 32 + 255) / 256);
+    ln_param_reduce_kernel<<<rgrid, 256, 0, st>>>(w, grid, (int)cols, dgamma, dbeta);
+    return cudaGetLastError();
+}
+
+}  // namespace tb

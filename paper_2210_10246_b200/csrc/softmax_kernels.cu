@@ -1,0 +1,359 @@
+// softmax_kernels.cu -- output-only softmax + sub-layer dropout recomputation
+// for sm_100a (attention probabilities, rows of S columns).
+//
+// Forward (tempo_ops::softmax ops_tempo.cpp:158-166 -> softmax_forward
+//   ops_reference.cpp:104-125; tempo_ops::dropout_recompute :168-194 ->
+//   dropout_apply :147-153 -> mask_scale kernels.cpp:285-295), fused:
+//   read z (4 B), write P (4 B), D (4 B) and the mask bit  = 12.125 B/elem.
+//   The stash is P + bits; D goes to the consumer and is never stashed.
+// Backward (dropout_backward ops_tempo.cpp:188-190 -> softmax_backward_
+//   from_output ops_reference.cpp:127-145, plus the "dropout-rescale"
+//   recompute of D for the consumer, ops_tempo.cpp:17-26), fused:
+//   read dD, P (8 B) + bit, write dZ (4 B)   = 12.125 B/elem (+4 B with D).
+//
+// Numerics follow the reference's F32 path: dP and D are the fp64 products
+// rounded once (bit-exact with mask_scale on the same inputs), the row dot
+// sum(dP*P) and the softmax denominator accumulate in fp64, exp runs in fp32
+// with the rounding error of (z - max) folded back in (TwoSum), and
+// P = float(e / denom) via the fp64 reciprocal of the row denominator.
+//
+// Layout: one warp per row, VPL float4 per lane (cols = 128*VPL <= 1024),
+// the whole row in registers (one HBM read per element, no smem staging
+// needed at S <= 1024).  Other shapes use the generic warp-per-row kernels.
+#include <initializer_list>
+
+#include "common.cuh"
+#include "tempo_internal.h"
+
+namespace tb {
+namespace {
+
+constexpr int kBlock = 256;
+
+enum FwdMode { kPlain = 0, kSupplied = 1, kPhilox = 2 };
+
+// exp(z - mx) with the rounding error of the subtraction restored.
+__device__ __forceinline__ float exp_shift(float z, float mx) {
+    float d = z - mx;
+    float bb = d - z;
+    float err = (z - (d - bb)) + (-mx - bb);  // TwoSum: (z - mx) = d + err exactly
+    float e = expf(d);
+    return fmaf(e, err, e);
+}
+
+__device__ __forceinline__ float dscale(float v, double s) { return (float)((double)v * s); }
+
+template <int VPL, int MODE>
+__global__ void __launch_bounds__(kBlock) softmax_fwd_vec_kernel(
+    const float* __restrict__ z, float* __restrict__ P, float* __restrict__ D,
+    uint32_t* __restrict__ mask, double scale, uint64_t thresh, uint64_t seed, uint64_t offset,
+    int64_t rows) {
+    constexpr int C = VPL * 128;
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = ((int64_t)blockIdx.x * kBlock + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * kBlock) >> 5;
+    for (int64_t r = warp; r < rows; r += nwarps) {
+        const float4* zr = reinterpret_cast<const float4*>(z + r * C);
+        float4 v[VPL];
+        uint32_t nib[VPL];
+#pragma unroll
+        for (int k = 0; k < VPL; ++k) v[k] = ld_stream(zr + k * 32 + lane);
+        if (MODE == kSupplied) {
+#pragma unroll
+            for (int k = 0; k < VPL; ++k) nib[k] = chunk_nibble(mask + ((r * C) >> 5) + k * 4, lane);
+        }
+        float mx = v[0].x;
+#pragma unroll
+        for (int k = 0; k < VPL; ++k)
+            mx = fmaxf(mx, fmaxf(fmaxf(v[k].x, v[k].y), fmaxf(v[k].z, v[k].w)));
+        mx = warp_max(mx);
+        double acc = 0.0;
+#pragma unroll
+        for (int k = 0; k < VPL; ++k) {
+            v[k].x = exp_shift(v[k].x, mx);
+            v[k].y = exp_shift(v[k].y, mx);
+            v[k].z = exp_shift(v[k].z, mx);
+            v[k].w = exp_shift(v[k].w, mx);
+            acc += ((double)v[k].x + (double)v[k].y) + ((double)v[k].z + (double)v[k].w);
+        }
+        const double inv = 1.0 / warp_sum(acc);
+        float4* Pr = reinterpret_cast<float4*>(P + r * C);
+        float4* Dr = reinterpret_cast<float4*>(D + r * C);
+#pragma unroll
+        for (int k = 0; k < VPL; ++k) {
+            float4 p;
+            p.x = (float)((double)v[k].x * inv);
+            p.y = (float)((double)v[k].y * inv);
+            p.z = (float)((double)v[k].z * inv);
+            p.w = (float)((double)v[k].w * inv);
+            st_stream(Pr + k * 32 + lane, p);
+            if (MODE == kPlain) continue;
+            uint32_t bits;
+            if (MODE == kPhilox) {
+                U4 rnd = philox_quad(seed, (offset + (uint64_t)(r * C + k * 128 + lane * 4)) >> 2);
+                bool k0 = (uint64_t)rnd.x >= thresh, k1 = (uint64_t)rnd.y >= thresh;
+                bool k2 = (uint64_t)rnd.z >= thresh, k3 = (uint64_t)rnd.w >= thresh;
+                uint32_t word = pack_chunk_bits(k0, k1, k2, k3, lane);
+                if (lane < 4) st_stream(mask + ((r * C) >> 5) + k * 4 + lane, word);
+                bits = (uint32_t)k0 | ((uint32_t)k1 << 1) | ((uint32_t)k2 << 2) | ((uint32_t)k3 << 3);
+            } else {
+                bits = nib[k];
+            }
+            if (D) {
+                float4 d;
+                d.x = (bits & 1u) ? dscale(p.x, scale) : 0.0f;
+                d.y = (bits & 2u) ? dscale(p.y, scale) : 0.0f;
+                d.z = (bits & 4u) ? dscale(p.z, scale) : 0.0f;
+                d.w = (bits & 8u) ? dscale(p.w, scale) : 0.0f;
+                st_stream(Dr + k * 32 + lane, d);
+            }
+        }
+    }
+}
+
+// Backward.  DROP: dP = mask ? dD*scale : 0 (else dP = dD, plain softmax);
+// WRITE_D: recomputed D = mask ? P*scale : 0.
+template <int VPL, bool DROP, bool WRITE_D>
+__global__ void __launch_bounds__(kBlock) softmax_bwd_vec_kernel(
+    const float* __restrict__ dD, const float* __restrict__ P, const uint32_t* __restrict__ mask,
+    double scale, float* __restrict__ dZ, float* __restrict__ D, int64_t rows) {
+    constexpr int C = VPL * 128;
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = ((int64_t)blockIdx.x * kBlock + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * kBlock) >> 5;
+    for (int64_t r = warp; r < rows; r += nwarps) {
+        const float4* gr = reinterpret_cast<const float4*>(dD + r * C);
+        const float4* pr = reinterpret_cast<const float4*>(P + r * C);
+        float4 g[VPL], p[VPL];
+        uint32_t nib[VPL];
+#pragma unroll
+        for (int k = 0; k < VPL; ++k) {
+            g[k] = ld_stream(gr + k * 32 + lane);
+            p[k] = ld_stream(pr + k * 32 + lane);
+            if (DROP) nib[k] = chunk_nibble(mask + ((r * C) >> 5) + k * 4, lane);
+        }
+        double acc = 0.0;
+#pragma unroll
+        for (int k = 0; k < VPL; ++k) {
+            if (DROP) {  // dropout_backward: F32-stored dP (ops_reference.cpp:155-161)
+                g[k].x = (nib[k] & 1u) ? dscale(g[k].x, scale) : 0.0f;
+                g[k].y = (nib[k] & 2u) ? dscale(g[k].y, scale) : 0.0f;
+                g[k].z = (nib[k] & 4u) ? dscale(g[k].z, scale) : 0.0f;
+                g[k].w = (nib[k] & 8u) ? dscale(g[k].w, scale) : 0.0f;
+            }
+            acc = fma((double)g[k].x, (double)p[k].x, acc);
+            acc = fma((double)g[k].y, (double)p[k].y, acc);
+            acc = fma((double)g[k].z, (double)p[k].z, acc);
+            acc = fma((double)g[k].w, (double)p[k].w, acc);
+        }
+        const double s = warp_sum(acc);
+        float4* zr = reinterpret_cast<float4*>(dZ + r * C);
+        float4* Dr = reinterpret_cast<float4*>(D + r * C);
+#pragma unroll
+        for (int k = 0; k < VPL; ++k) {
+            float4 o;
+            o.x = (float)((double)p[k].x * ((double)g[k].x - s));
+            o.y = (float)((double)p[k].y * ((double)g[k].y - s));
+            o.z = (float)((double)p[k].z * ((double)g[k].z - s));
+            o.w = (float)((double)p[k].w * ((double)g[k].w - s));
+            st_stream(zr + k * 32 + lane, o);
+            if (WRITE_D) {
+                float4 d;
+                d.x = (nib[k] & 1u) ? dscale(p[k].x, scale) : 0.0f;
+                d.y = (nib[k] & 2u) ? dscale(p[k].y, scale) : 0.0f;
+                d.z = (nib[k] & 4u) ? dscale(p[k].z, scale) : 0.0f;
+                d.w = (nib[k] & 8u) ? dscale(p[k].w, scale) : 0.0f;
+                st_stream(Dr + k * 32 + lane, d);
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------- generic
+__device__ __forceinline__ bool mask_bit(const uint32_t* mask, int64_t i) {
+    return (__ldg(mask + (i >> 5)) >> (i & 31)) & 1u;
+}
+
+__global__ void __launch_bounds__(kBlock) softmax_fwd_generic_kernel(
+    const float* __restrict__ z, float* __restrict__ P, float* __restrict__ D,
+    uint32_t* __restrict__ mask, int mode, double scale, uint64_t thresh, uint64_t seed,
+    uint64_t offset, int64_t rows, int64_t C) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = ((int64_t)blockIdx.x * kBlock + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * kBlock) >> 5;
+    for (int64_t r = warp; r < rows; r += nwarps) {
+        const float* zr = z + r * C;
+        float mx = -INFINITY;
+        for (int64_t j = lane; j < C; j += 32) mx = fmaxf(mx, zr[j]);
+        mx = warp_max(mx);
+        double acc = 0.0;
+        for (int64_t j = lane; j < C; j += 32) acc += (double)exp_shift(zr[j], mx);
+        const double inv = 1.0 / warp_sum(acc);
+        for (int64_t j = lane; j < C; j += 32) {
+            const int64_t i = r * C + j;
+            float p = (float)((double)exp_shift(zr[j], mx) * inv);
+            P[i] = p;
+            if (mode == kPlain) continue;
+            bool keep;
+            if (mode == kPhilox) {
+                keep = (uint64_t)philox_at(seed, offset + (uint64_t)i) >= thresh;
+                if (keep) atomicOr(mask + (i >> 5), 1u << (i & 31));
+            } else {
+                keep = mask_bit(mask, i);
+            }
+            if (D) D[i] = keep ? dscale(p, scale) : 0.0f;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kBlock) softmax_bwd_generic_kernel(
+    const float* __restrict__ dD, const float* __restrict__ P, const uint32_t* __restrict__ mask,
+    int drop, double scale, float* __restrict__ dZ, float* __restrict__ D, int64_t rows,
+    int64_t C) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = ((int64_t)blockIdx.x * kBlock + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * kBlock) >> 5;
+    for (int64_t r = warp; r < rows; r += nwarps) {
+        double acc = 0.0;
+        for (int64_t j = lane; j < C; j += 32) {
+            const int64_t i = r * C + j;
+            float g = dD[i];
+            if (drop) g = mask_bit(mask, i) ? dscale(g, scale) : 0.0f;
+            acc = fma((double)g, (double)P[i], acc);
+        }
+        const double s = warp_sum(acc);
+        for (int64_t j = lane; j < C; j += 32) {
+            const int64_t i = r * C + j;
+            float g = dD[i];
+            const bool keep = drop ? mask_bit(mask, i) : true;
+            if (drop) g = keep ? dscale(g, scale) : 0.0f;
+            dZ[i] = (float)((double)P[i] * ((double)g - s));
+            if (D) D[i] = keep ? dscale(P[i], scale) : 0.0f;
+        }
+    }
+}
+
+inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+template <int MODE>
+cudaError_t fwd_vec(int vpl, const float* z, float* P, float* D, uint32_t* mask, double scale,
+                    uint64_t thresh, uint64_t seed, uint64_t offset, int64_t rows,
+                    cudaStream_t st) {
+#define TB_FWD_CASE(V)                                                                       \
+    case V: {                                                                                \
+        auto k = softmax_fwd_vec_kernel<V, MODE>;                                            \
+        int grid = grid_for((const void*)k, kBlock, 0, (rows * 32 + kBlock - 1) / kBlock);  \
+        k<<<grid, kBlock, 0, st>>>(z, P, D, mask, scale, thresh, seed, offset, rows);        \
+        break;                                                                               \
+    }
+    switch (vpl) {
+        TB_FWD_CASE(1)
+        TB_FWD_CASE(2)
+        TB_FWD_CASE(3)
+        TB_FWD_CASE(4)
+        TB_FWD_CASE(5)
+        TB_FWD_CASE(6)
+        TB_FWD_CASE(7)
+        TB_FWD_CASE(8)
+        default: return cudaErrorInvalidValue;
+    }
+#undef TB_FWD_CASE
+    return cudaGetLastError();
+}
+
+template <bool DROP, bool WRITE_D>
+cudaError_t bwd_vec(int vpl, const float* dD, const float* P, const uint32_t* mask, double scale,
+                    float* dZ, float* D, int64_t rows, cudaStream_t st) {
+#define TB_BWD_CASE(V)                                                                       \
+    case V: {                                                                                \
+        auto k = softmax_bwd_vec_kernel<V, DROP, WRITE_D>;                                   \
+        int grid = grid_for((const void*)k, kBlock, 0, (rows * 32 + kBlock - 1) / kBlock);  \
+        k<<<grid, kBlock, 0, st>>>(dD, P, mask, scale, dZ, D, rows);                         \
+        break;                                                                               \
+    }
+    switch (vpl) {
+        TB_BWD_CASE(1)
+        TB_BWD_CASE(2)
+        TB_BWD_CASE(3)
+        TB_BWD_CASE(4)
+        TB_BWD_CASE(5)
+        TB_BWD_CASE(6)
+        TB_BWD_CASE(7)
+        TB_BWD_CASE(8)
+        default: return cudaErrorInvalidValue;
+    }
+#undef TB_BWD_CASE
+    return cudaGetLastError();
+}
+
+bool vec_ok(int64_t cols, uint64_t offset, std::initializer_list<const void*> ptrs) {
+    if (cols % 128 != 0 || cols > 1024 || cols == 0 || (offset & 3u)) return false;
+    for (const void* p : ptrs)
+        if (p && !aligned16(p)) return false;
+    return true;
+}
+
+int generic_grid(const void* k, int64_t rows) {
+    return grid_for(k, kBlock, 0, (rows * 32 + kBlock - 1) / kBlock);
+}
+
+}  // namespace
+
+cudaError_t launch_softmax_fwd(const float* z, float* P, int64_t rows, int64_t cols,
+                               cudaStream_t st) {
+    if (rows == 0 || cols == 0) return cudaSuccess;
+    if (vec_ok(cols, 0, {z, P}))
+        return fwd_vec<kPlain>((int)(cols / 128), z, P, nullptr, nullptr, 1.0, 0, 0, 0, rows, st);
+    softmax_fwd_generic_kernel<<<generic_grid((const void*)softmax_fwd_generic_kernel, rows),
+                                 kBlock, 0, st>>>(z, P, nullptr, nullptr, kPlain, 1.0, 0, 0, 0,
+                                                  rows, cols);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_softmax_bwd(const float* dP, const float* P, float* dZ, int64_t rows,
+                               int64_t cols, cudaStream_t st) {
+    if (rows == 0 || cols == 0) return cudaSuccess;
+    if (vec_ok(cols, 0, {dP, P, dZ}))
+        return bwd_vec<false, false>((int)(cols / 128), dP, P, nullptr, 1.0, dZ, nullptr, rows,
+                                     st);
+    softmax_bwd_generic_kernel<<<generic_grid((const void*)softmax_bwd_generic_kernel, rows),
+                                 kBlock, 0, st>>>(dP, P, nullptr, 0, 1.0, dZ, nullptr, rows,
+                                                  cols);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_softmax_dropout_fwd(const float* z, double scale, uint64_t thresh, int philox,
+                                       uint32_t* mask, uint64_t seed, uint64_t offset, float* P,
+                                       float* D, int64_t rows, int64_t cols, cudaStream_t st) {
+    if (rows == 0 || cols == 0) return cudaSuccess;
+    if (vec_ok(cols, offset, {z, P, D, mask})) {
+        const int vpl = (int)(cols / 128);
+        return philox ? fwd_vec<kPhilox>(vpl, z, P, D, mask, scale, thresh, seed, offset, rows, st)
+                      : fwd_vec<kSupplied>(vpl, z, P, D, mask, scale, thresh, seed, offset, rows,
+                                           st);
+    }
+    if (philox) {
+        cudaError_t e = cudaMemsetAsync(mask, 0, (size_t)((rows * cols + 31) / 32) * 4, st);
+        if (e != cudaSuccess) return e;
+    }
+    softmax_fwd_generic_kernel<<<generic_grid((const void*)softmax_fwd_generic_kernel, rows),
+                                 kBlock, 0, st>>>(z, P, D, mask, philox ? kPhilox : kSupplied,
+                                                  scale, thresh, seed, offset, rows, cols);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_attn_probs_bwd(const float* dD, const float* P, const uint32_t* mask,
+                                  double scale, float* dZ, float* D, int64_t rows, int64_t cols,
+                                  cudaStream_t st) {
+    if (rows == 0 || cols == 0) return cudaSuccess;
+    if (vec_ok(cols, 0, {dD, P, dZ, D, mask})) {
+        const int vpl = (int)(cols / 128);
+        return D ? bwd_vec<true, true>(vpl, dD, P, mask, scale, dZ, D, rows, st)
+                 : bwd_vec<true, false>(vpl, dD, P, mask, scale, dZ, nullptr, rows, st);
+    }
+    softmax_bwd_generic_kernel<<<generic_grid((const void*)softmax_bwd_generic_kernel, rows),
+                                 kBlock, 0, st>>>(dD, P, mask, 1, scale, dZ, D, rows, cols);
+    return cudaGetLastError();
+}
+
+}  // namespace tb

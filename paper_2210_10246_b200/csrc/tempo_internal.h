@@ -1,0 +1,72 @@
+// tempo_internal.h -- host/device shared definitions of the Tempo B200 library.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/tempo_b200.h"
+
+namespace tb {
+
+// ---- GELU table, device form -------------------------------------------
+// Host-precomputed from the parsed v1 table (gelu_table.cpp) so that every
+// double comparison of GeluPolyTable::eval becomes an fp32 comparison with
+// the same outcome for every float input (hard part 2):
+//   y < y_min      <=>  y_f < ymin_up      (ymin_up = smallest float >= y_min)
+//   lo <= y        <=>  y_f >= lo_up       (lo_up   = smallest float >= lo)
+//   x > x_star     <=>  x_f >= xstar_gt    (xstar_gt = smallest float > x_star)
+constexpr int kMaxSeg = 32;   // total over both branches
+constexpr int kMaxCoef = 64;  // gelu_table.cpp:123 allows up to 64
+
+struct GeluDevTable {
+    float xstar_gt;
+    float ymin_up;
+    float ymin_hi, ymin_lo;  // y_min as a float-float pair
+    int nseg[2];             // branch 0 segments are [0, nseg0), branch 1 follow
+    int ncoef;               // max coefficient count over all segments
+    int stride;              // odd smem stride >= ncoef (bank-conflict free)
+    float lo_up[kMaxSeg];
+    float s[kMaxSeg];  // t = clamp(u * s + b, -1, 1); constant segments: s = b = 0
+    float b[kMaxSeg];
+    int sqrt_shift[kMaxSeg];
+    float coef[kMaxSeg][kMaxCoef];  // Chebyshev coefficients, zero padded
+};
+
+// Kernel launchers (defined in the .cu files; return cudaGetLastError()).
+cudaError_t launch_gelu_fwd(const float* x, float* y, uint32_t* mask, int64_t n, float xstar_gt,
+                            cudaStream_t st);
+cudaError_t launch_gelu_bwd(const float* dy, const float* y, const uint32_t* mask,
+                            const GeluDevTable& t, float* dx, int64_t n, cudaStream_t st);
+
+cudaError_t launch_ln_fwd(const float* x, const float* gamma, const float* beta, double eps,
+                          float* y, float* rstd, int64_t rows, int64_t cols, int32_t* dev_status,
+                          cudaStream_t st);
+size_t ln_bwd_workspace(int64_t rows, int64_t cols);
+cudaError_t launch_ln_bwd(const float* dy, const float* y, const float* rstd, const float* gamma,
+                          const float* beta, float* dx, float* dgamma, float* dbeta, void* ws,
+                          int64_t rows, int64_t cols, cudaStream_t st);
+
+cudaError_t launch_softmax_fwd(const float* z, float* P, int64_t rows, int64_t cols,
+                               cudaStream_t st);
+cudaError_t launch_softmax_bwd(const float* dP, const float* P, float* dZ, int64_t rows,
+                               int64_t cols, cudaStream_t st);
+cudaError_t launch_softmax_dropout_fwd(const float* z, double scale, uint64_t thresh, int philox,
+                                       uint32_t* mask, uint64_t seed, uint64_t offset, float* P,
+                                       float* D, int64_t rows, int64_t cols, cudaStream_t st);
+cudaError_t launch_attn_probs_bwd(const float* dD, const float* P, const uint32_t* mask,
+                                  double scale, float* dZ, float* D, int64_t rows, int64_t cols,
+                                  cudaStream_t st);
+
+cudaError_t launch_dropout_fwd(const float* x, double scale, uint64_t thresh, int philox,
+                               uint32_t* mask, uint64_t seed, uint64_t offset, float* y, int64_t n,
+                               cudaStream_t st);
+cudaError_t launch_dropout_bwd(const float* dy, const uint32_t* mask, double scale, float* dx,
+                               int64_t n, cudaStream_t st);
+cudaError_t launch_mask_pack(const uint8_t* bytes, uint32_t* bits, int64_t n, int32_t* status,
+                             cudaStream_t st);
+cudaError_t launch_mask_unpack(const uint32_t* bits, uint8_t* bytes, int64_t n, cudaStream_t st);
+
+// Persistent-grid sizing: SM count x resident CTAs per SM (cached per device).
+int grid_for(const void* kernel, int block, size_t smem, int64_t work_items);
+
+}  // namespace tb

@@ -1,0 +1,321 @@
+"""Host-side mirror of the reference's operator API for the Tempo in-place path.
+
+Each function here is the device counterpart of one reference entry point
+(``proj/include/tempo/ops_tempo.hpp:33-63``, ``ops_reference.hpp:18-47``,
+``gelu_table.hpp:48-91``), taking CUDA ``torch.Tensor`` buffers (fp32,
+contiguous) and calling the C-ABI of ``include/tempo_b200.h`` on the current
+CUDA stream.  PyTorch only provides device memory and streams; every
+operator runs in this package's sm_100a kernels.  Errors surface as
+:class:`TempoError` whose ``kind`` is the reference's exception class name.
+
+Bit-packed masks are ``torch.int32`` tensors of ``ceil(n/32)`` words (bit i
+of word w = element 32w+i, the reference's BoolMask order).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import Optional, Tuple
+
+import torch
+
+from ._capi import MASK_PHILOX, MASK_SUPPLIED, TempoError, check, lib
+
+__all__ = [
+    "GeluTable", "TempoError", "gelu_ip_fwd", "gelu_ip_bwd", "layernorm_ip_fwd",
+    "layernorm_ip_bwd", "ln_check_gamma", "softmax_ip_fwd", "softmax_ip_bwd",
+    "softmax_dropout_fwd", "attn_probs_bwd", "dropout_fwd", "dropout_bwd", "mask_words",
+    "pack_mask", "unpack_mask", "bernoulli_keep_bits", "mask_stream_seed",
+    "layer_stash_bytes_per_token", "MASK_SUPPLIED", "MASK_PHILOX",
+]
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def _stream():
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _f32(t: torch.Tensor, name: str) -> torch.Tensor:
+    if t.dtype != torch.float32:
+        raise TempoError(2, f"{name}: expected float32, got {t.dtype}")
+    if not t.is_cuda:
+        raise TempoError(2, f"{name}: expected a CUDA tensor")
+    return t.contiguous()
+
+
+def mask_words(n: int) -> int:
+    return (int(n) + 31) // 32
+
+
+def _rows_cols(t: torch.Tensor) -> Tuple[int, int]:
+    if t.dim() == 0:
+        raise TempoError(2, "expected rank >= 1")
+    cols = t.shape[-1]
+    return (t.numel() // cols if cols else 0), cols
+
+
+# --------------------------------------------------------------------------
+# GeluPolyTable (gelu_table.hpp:48-91)
+# --------------------------------------------------------------------------
+class GeluTable:
+    """Parsed, validated v1 GELU derivative table (immutable, shareable)."""
+
+    def __init__(self, v1_text: str):
+        h = C.c_void_p()
+        check(lib().tempo_gelu_table_create(v1_text.encode(), C.byref(h)))
+        self._h = h
+
+    @classmethod
+    def default(cls) -> "GeluTable":
+        """fit::fit_table() with default FitOptions (gelu_fit.cpp:331-382)."""
+        return cls(lib().tempo_gelu_default_table_v1().decode())
+
+    @property
+    def handle(self) -> C.c_void_p:
+        return self._h
+
+    def info(self) -> dict:
+        xs, ym, tol, me = C.c_double(), C.c_double(), C.c_double(), C.c_double()
+        ver, nseg, deg = C.c_int(), C.c_int(), C.c_int()
+        check(lib().tempo_gelu_table_info(self._h, C.byref(xs), C.byref(ym), C.byref(tol),
+                                          C.byref(me), C.byref(ver), C.byref(nseg), C.byref(deg)))
+        return {"x_star": xs.value, "y_min": ym.value, "tolerance": tol.value,
+                "verified_max_error": me.value, "verified": bool(ver.value),
+                "n_segments": nseg.value, "max_degree": deg.value}
+
+    def serialize(self) -> str:
+        n = C.c_size_t()
+        check(lib().tempo_gelu_table_serialize(self._h, None, 0, C.byref(n)))
+        buf = C.create_string_buffer(n.value + 1)
+        check(lib().tempo_gelu_table_serialize(self._h, buf, n.value + 1, C.byref(n)))
+        return buf.value.decode()
+
+    def eval_host(self, y, m):
+        """GeluPolyTable::eval on the host (double), for numpy arrays."""
+        import numpy as np
+        y = np.ascontiguousarray(y, np.float64).reshape(-1)
+        m = np.ascontiguousarray(m, np.uint8).reshape(-1)
+        out = np.empty_like(y)
+        check(lib().tempo_gelu_table_eval_host(self._h, y.ctypes.data, m.ctypes.data,
+                                               out.ctypes.data, y.size))
+        return out
+
+    def close(self) -> None:
+        if getattr(self, "_h", None) is not None and self._h.value:
+            lib().tempo_gelu_table_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+# --------------------------------------------------------------------------
+# In-Place GELU (tempo_ops::gelu, ops_tempo.cpp:89-96)
+# --------------------------------------------------------------------------
+def gelu_ip_fwd(x: torch.Tensor, table: GeluTable, y: torch.Tensor = None,
+                mask: torch.Tensor = None):
+    """Returns (y, mask_bits).  Stash = y + mask (the input is not kept)."""
+    if table is None:
+        raise TempoError(5, "in-place gelu needs a fitted table")
+    x = _f32(x, "x")
+    y = torch.empty_like(x) if y is None else y
+    mask = torch.empty(mask_words(x.numel()), dtype=torch.int32, device=x.device) \
+        if mask is None else mask
+    check(lib().tempo_gelu_ip_fwd(_ptr(x), _ptr(y), _ptr(mask), x.numel(), table.handle,
+                                  _stream()))
+    return y, mask
+
+
+def gelu_ip_bwd(dy: torch.Tensor, y: torch.Tensor, mask: torch.Tensor, table: GeluTable,
+                dx: torch.Tensor = None) -> torch.Tensor:
+    if table is None:
+        raise TempoError(5, "in-place gelu needs a fitted table")
+    dy, y = _f32(dy, "dy"), _f32(y, "y")
+    if dy.shape != y.shape:
+        raise TempoError(2, f"gelu backward shapes {tuple(dy.shape)} and {tuple(y.shape)} differ")
+    dx = torch.empty_like(dy) if dx is None else dx
+    check(lib().tempo_gelu_ip_bwd(_ptr(dy), _ptr(y), _ptr(mask), table.handle, _ptr(dx),
+                                  y.numel(), _stream()))
+    return dx
+
+
+# --------------------------------------------------------------------------
+# In-Place LayerNorm (tempo_ops::layernorm, ops_tempo.cpp:98-156)
+# --------------------------------------------------------------------------
+def ln_check_gamma(gamma: torch.Tensor) -> None:
+    """ops_tempo.cpp:100-106 (synchronous)."""
+    gamma = _f32(gamma, "gamma")
+    check(lib().tempo_ln_check_gamma(_ptr(gamma), gamma.numel(), _stream()))
+
+
+def layernorm_ip_fwd(x: torch.Tensor, gamma: torch.Tensor, beta: torch.Tensor,
+                     eps: float = 1e-5, check_gamma: bool = True, y: torch.Tensor = None,
+                     rstd: torch.Tensor = None, dev_status: torch.Tensor = None):
+    """Returns (y, rstd).  Stash = y + rstd[row]."""
+    x, gamma, beta = _f32(x, "x"), _f32(gamma, "gamma"), _f32(beta, "beta")
+    rows, cols = _rows_cols(x)
+    if gamma.numel() != cols or beta.numel() != cols:
+        raise TempoError(2, f"layernorm affine params {tuple(gamma.shape)}, {tuple(beta.shape)} "
+                            f"do not match {tuple(x.shape)}")
+    if check_gamma:
+        ln_check_gamma(gamma)
+    y = torch.empty_like(x) if y is None else y
+    rstd = torch.empty(x.shape[:-1], dtype=torch.float32, device=x.device) if rstd is None else rstd
+    check(lib().tempo_ln_ip_fwd(_ptr(x), _ptr(gamma), _ptr(beta), float(eps), _ptr(y), _ptr(rstd),
+                                rows, cols, _ptr(dev_status), _stream()))
+    return y, rstd
+
+
+_ws_cache = {}
+
+
+def ln_workspace(rows: int, cols: int, device) -> torch.Tensor:
+    nbytes = int(lib().tempo_ln_ip_bwd_workspace_size(rows, cols))
+    key = (str(device), nbytes)
+    ws = _ws_cache.get(key)
+    if ws is None:
+        ws = torch.empty(max(nbytes, 16), dtype=torch.uint8, device=device)
+        _ws_cache[key] = ws
+    return ws
+
+
+def layernorm_ip_bwd(dy: torch.Tensor, y: torch.Tensor, rstd: torch.Tensor,
+                     gamma: torch.Tensor, beta: torch.Tensor, dx: torch.Tensor = None,
+                     dgamma: torch.Tensor = None, dbeta: torch.Tensor = None,
+                     workspace: torch.Tensor = None):
+    """Returns (dx, dgamma, dbeta); dgamma/dbeta summed over all rows."""
+    dy, y = _f32(dy, "dy"), _f32(y, "y")
+    rows, cols = _rows_cols(y)
+    dx = torch.empty_like(dy) if dx is None else dx
+    dgamma = torch.empty(cols, dtype=torch.float32, device=y.device) if dgamma is None else dgamma
+    dbeta = torch.empty(cols, dtype=torch.float32, device=y.device) if dbeta is None else dbeta
+    ws = ln_workspace(rows, cols, y.device) if workspace is None else workspace
+    check(lib().tempo_ln_ip_bwd(_ptr(dy), _ptr(y), _ptr(rstd), _ptr(gamma), _ptr(beta), _ptr(dx),
+                                _ptr(dgamma), _ptr(dbeta), _ptr(ws), ws.numel(), rows, cols,
+                                _stream()))
+    return dx, dgamma, dbeta
+
+
+# --------------------------------------------------------------------------
+# Output-only softmax + dropout recomputation (ops_tempo.cpp:158-194)
+# --------------------------------------------------------------------------
+def softmax_ip_fwd(z: torch.Tensor, P: torch.Tensor = None) -> torch.Tensor:
+    z = _f32(z, "z")
+    rows, cols = _rows_cols(z)
+    P = torch.empty_like(z) if P is None else P
+    check(lib().tempo_softmax_ip_fwd(_ptr(z), _ptr(P), rows, cols, _stream()))
+    return P
+
+
+def softmax_ip_bwd(dP: torch.Tensor, P: torch.Tensor, dZ: torch.Tensor = None) -> torch.Tensor:
+    dP, P = _f32(dP, "dP"), _f32(P, "P")
+    rows, cols = _rows_cols(P)
+    dZ = torch.empty_like(P) if dZ is None else dZ
+    check(lib().tempo_softmax_ip_bwd(_ptr(dP), _ptr(P), _ptr(dZ), rows, cols, _stream()))
+    return dZ
+
+
+def softmax_dropout_fwd(z: torch.Tensor, p: float, mask: torch.Tensor = None,
+                        seed: int = 0, offset: int = 0, P: torch.Tensor = None,
+                        D: torch.Tensor = None, write_d: bool = True, generate: bool = None):
+    """Fused softmax -> dropout_recompute forward.  SUPPLIED mode reads
+    ``mask`` (e.g. the reference's bernoulli_keep stream); Philox mode
+    (``generate``, the default when ``mask`` is None) writes a fresh mask into
+    ``mask`` (allocated if None).  Returns (P, D, mask)."""
+    z = _f32(z, "z")
+    rows, cols = _rows_cols(z)
+    if generate is None:
+        generate = mask is None
+    mode = MASK_PHILOX if generate else MASK_SUPPLIED
+    if mask is None:
+        mask = torch.empty(mask_words(z.numel()), dtype=torch.int32, device=z.device)
+    P = torch.empty_like(z) if P is None else P
+    if write_d and D is None:
+        D = torch.empty_like(z)
+    check(lib().tempo_softmax_dropout_fwd(_ptr(z), float(p), mode, _ptr(mask), int(seed),
+                                          int(offset), _ptr(P), _ptr(D if write_d else None),
+                                          rows, cols, _stream()))
+    return P, (D if write_d else None), mask
+
+
+def attn_probs_bwd(dD: torch.Tensor, P: torch.Tensor, mask: torch.Tensor, p: float,
+                   write_d: bool = False, dZ: torch.Tensor = None, D: torch.Tensor = None):
+    """Fused dropout bwd + output-only softmax bwd (+ recomputed D).
+    Returns (dZ, D or None)."""
+    dD, P = _f32(dD, "dD"), _f32(P, "P")
+    rows, cols = _rows_cols(P)
+    dZ = torch.empty_like(P) if dZ is None else dZ
+    if write_d and D is None:
+        D = torch.empty_like(P)
+    check(lib().tempo_attn_probs_bwd(_ptr(dD), _ptr(P), _ptr(mask), float(p), _ptr(dZ),
+                                     _ptr(D if write_d else None), rows, cols, _stream()))
+    return dZ, (D if write_d else None)
+
+
+# --------------------------------------------------------------------------
+# Dropout (ops_reference.cpp:147-161, ref_ops::dropout :214-225)
+# --------------------------------------------------------------------------
+def dropout_fwd(x: torch.Tensor, p: float, mask: torch.Tensor = None, seed: int = 0,
+                offset: int = 0, y: torch.Tensor = None, generate: bool = None):
+    """y = mask ? x/(1-p) : 0.  Mask supplied (read) or generated (Philox,
+    written into ``mask``; default when ``mask`` is None).  Returns (y, mask)."""
+    x = _f32(x, "x")
+    if generate is None:
+        generate = mask is None
+    mode = MASK_PHILOX if generate else MASK_SUPPLIED
+    if mask is None:
+        mask = torch.empty(mask_words(x.numel()), dtype=torch.int32, device=x.device)
+    y = torch.empty_like(x) if y is None else y
+    check(lib().tempo_dropout_fwd(_ptr(x), float(p), mode, _ptr(mask), int(seed), int(offset),
+                                  _ptr(y), x.numel(), _stream()))
+    return y, mask
+
+
+def dropout_bwd(dy: torch.Tensor, mask: torch.Tensor, p: float,
+                dx: torch.Tensor = None) -> torch.Tensor:
+    dy = _f32(dy, "dy")
+    dx = torch.empty_like(dy) if dx is None else dx
+    check(lib().tempo_dropout_bwd(_ptr(dy), _ptr(mask), float(p), _ptr(dx), dy.numel(),
+                                  _stream()))
+    return dx
+
+
+# --------------------------------------------------------------------------
+# Masks
+# --------------------------------------------------------------------------
+def pack_mask(bytes_: torch.Tensor, dev_status: torch.Tensor = None) -> torch.Tensor:
+    """BoolMask bytes (uint8 CUDA tensor) -> packed bits."""
+    b = bytes_.contiguous()
+    bits = torch.empty(mask_words(b.numel()), dtype=torch.int32, device=b.device)
+    check(lib().tempo_mask_pack(_ptr(b), _ptr(bits), b.numel(), _ptr(dev_status), _stream()))
+    return bits
+
+
+def unpack_mask(bits: torch.Tensor, n: int) -> torch.Tensor:
+    out = torch.empty(n, dtype=torch.uint8, device=bits.device)
+    check(lib().tempo_mask_unpack(_ptr(bits), _ptr(out), int(n), _stream()))
+    return out
+
+
+def bernoulli_keep_bits(n: int, p: float, seed: int):
+    """BoolMask::bernoulli_keep (tensor.cpp:186-203) on the host, packed:
+    returns a numpy uint32 array of ceil(n/32) words."""
+    import numpy as np
+    out = np.zeros(mask_words(n), np.uint32)
+    check(lib().tempo_bernoulli_keep_bits_host(int(n), float(p), int(seed), out.ctypes.data))
+    return out
+
+
+def mask_stream_seed(seed: int, salt: int, site: int) -> int:
+    return int(lib().tempo_mask_stream_seed(seed, salt, site))
+
+
+def layer_stash_bytes_per_token(seq: int, hidden: int, heads: int, tempo: bool = True,
+                                mask_bits: bool = True) -> int:
+    return int(lib().tempo_layer_stash_bytes_per_token(seq, hidden, heads, int(tempo),
+                                                       int(mask_bits)))

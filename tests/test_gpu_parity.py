@@ -1,0 +1,380 @@
+"""Parity of the sm_100a kernels (through the C-ABI) with the CPU oracle
+(oracle/tempo_oracle.c, itself pinned bit-exact to the reference in
+test_oracle.py) on identical seeded inputs.
+
+Tolerances (the reference's rel_err = |a-b| / max(1,|a|,|b|),
+gradcheck.cpp:15-17, unless stated):
+  GELU   mask bits: bit-exact.  y: <= 5 ulp (exhaustive host sweep bound of
+         the fp32 fast path, tests/tools/gelu_fwd_sweep.c) and bit-exact in
+         the fp64 window |x - x*| < 1/64.  dx on identical (dy, y, mask):
+         rel_err <= 1e-5.  fwd->bwd chain: rel_err <= 1e-5.
+  LN     y, dx: rel_err <= 1e-5; rstd: rel <= 1e-6; dgamma/dbeta vs the
+         reference's F64 path: rel_err <= 1e-5; run-to-run bitwise.
+  softmax P: |d| <= 1e-5*|ref| + 1e-9; dZ: |d| <= 1e-5*|ref| + 1e-8.
+  dropout D, dP, hidden y/dx: bit-exact; recomputed D == forward D bitwise.
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+XSTAR_D = -0.7517915246935645
+
+
+def rel_err(a, b):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    both_nan = np.isnan(a) & np.isnan(b)
+    d = np.abs(a - b) / np.maximum(1.0, np.maximum(np.abs(a), np.abs(b)))
+    d[both_nan] = 0.0
+    return float(d.max()) if d.size else 0.0
+
+
+def ulp_diff(a, b):
+    a = np.asarray(a, np.float32).view(np.int32).astype(np.int64)
+    b = np.asarray(b, np.float32).view(np.int32).astype(np.int64)
+    a = np.where(a < 0, -(a & 0x7FFFFFFF), a)
+    b = np.where(b < 0, -(b & 0x7FFFFFFF), b)
+    return np.abs(a - b)
+
+
+def unpack(bits_t, n):
+    b = bits_t.cpu().numpy().view(np.uint32)
+    return np.unpackbits(b.view(np.uint8), bitorder="little")[:n]
+
+
+def to_dev(a, cuda):
+    import torch
+    return torch.from_numpy(np.ascontiguousarray(a)).to(cuda)
+
+
+def bits_to_dev(bits_np, cuda):
+    import torch
+    return torch.from_numpy(bits_np.view(np.int32).copy()).to(cuda)
+
+
+# ------------------------------------------------------------------- GELU
+def gelu_inputs(n, seed):
+    g = np.random.default_rng(seed)
+    x = (g.standard_normal(n) * 2.5).astype(np.float32)
+    k = min(n, 64)
+    x[:k] = np.linspace(-0.8, -0.7, k, dtype=np.float32)  # the minimum window
+    if n > 200:
+        x[100:110] = [0.0, -0.0, 13.5, -13.5, -20.0, 40.0, np.inf, -np.inf, np.nan, 1e-42]
+    return x
+
+
+@pytest.mark.parametrize("n", [1, 31, 32, 127, 128, 129, 1000, 4101, 1024 * 3072])
+def test_gelu_forward(tops, port, table_text, cuda, n):
+    import torch
+    table = tops.GeluTable(table_text)
+    x = gelu_inputs(n, n)
+    y, mask = tops.gelu_ip_fwd(to_dev(x, cuda), table)
+    torch.cuda.synchronize()
+    ry, rm = port.gelu_fwd(x, table.info()["x_star"])
+    assert np.array_equal(unpack(mask, n), rm)
+    yg = y.cpu().numpy()
+    fin = np.isfinite(ry)
+    assert np.array_equal(np.isnan(yg), np.isnan(ry))
+    assert ulp_diff(yg[fin], ry[fin]).max(initial=0) <= 5
+    win = np.abs(x.astype(np.float64) - XSTAR_D) < 1.0 / 64
+    assert np.array_equal(yg[win], ry[win])  # fp64 window: bit-exact
+    # padding bits of the last word are zero
+    words = mask.cpu().numpy().view(np.uint32)
+    if n % 32:
+        assert words[-1] >> (n % 32) == 0
+
+
+def test_gelu_forward_unaligned(tops, port, table_text, cuda):
+    import torch
+    table = tops.GeluTable(table_text)
+    x = gelu_inputs(5001, 3)
+    xt = to_dev(np.concatenate([[0.0], x]).astype(np.float32), cuda)[1:]  # 4-byte offset
+    y, mask = tops.gelu_ip_fwd(xt, table)
+    torch.cuda.synchronize()
+    ry, rm = port.gelu_fwd(x, table.info()["x_star"])
+    assert np.array_equal(unpack(mask, x.size), rm)
+    fin = np.isfinite(ry)
+    assert ulp_diff(y.cpu().numpy()[fin], ry[fin]).max() <= 5
+
+
+@pytest.mark.parametrize("n", [1, 33, 128, 1000, 4101, 1024 * 3072])
+def test_gelu_backward_identical_inputs(tops, port, table_text, cuda, n):
+    import torch
+    table = tops.GeluTable(table_text)
+    pt = port.table(table_text)
+    x = gelu_inputs(n, 7 + n)
+    y, m = port.gelu_fwd(x, pt.x_star)  # the oracle's stash, fed to both
+    g = np.random.default_rng(n)
+    dy = g.standard_normal(n).astype(np.float32)
+    bits = np.packbits(m, bitorder="little")
+    bits = np.concatenate([bits, np.zeros((-bits.size) % 4, np.uint8)]).view(np.uint32)
+    dx = tops.gelu_ip_bwd(to_dev(dy, cuda), to_dev(y, cuda), bits_to_dev(bits, cuda), table)
+    torch.cuda.synchronize()
+    rdx = pt.gelu_bwd(dy, y, m)
+    assert rel_err(dx.cpu().numpy(), rdx) <= 1e-5
+
+
+def test_gelu_backward_table_eval_grid(tops, port, table_text, cuda):
+    """h(y, m) over a dense grid of outputs incl. clamps, seams and the tail."""
+    import torch
+    table = tops.GeluTable(table_text)
+    pt = port.table(table_text)
+    info = table.info()
+    ys = np.concatenate([np.linspace(-0.3, 10.0, 200000), [info["y_min"], 0.0, -0.0, 8.0,
+                                                           1.8725215943900724, 1e30, -1.0]])
+    ys = ys.astype(np.float32)
+    for m in (0, 1):
+        mm = np.full(ys.size, m, np.uint8)
+        bits = np.packbits(mm, bitorder="little")
+        bits = np.concatenate([bits, np.zeros((-bits.size) % 4, np.uint8)]).view(np.uint32)
+        ones = np.ones(ys.size, np.float32)
+        h = tops.gelu_ip_bwd(to_dev(ones, cuda), to_dev(ys, cuda), bits_to_dev(bits, cuda), table)
+        torch.cuda.synchronize()
+        assert rel_err(h.cpu().numpy(), pt.gelu_bwd(ones, ys, mm)) <= 1e-5
+
+
+def test_gelu_chain_forward_backward(tops, port, table_text, cuda):
+    import torch
+    table = tops.GeluTable(table_text)
+    pt = port.table(table_text)
+    n = 1 << 20
+    x = gelu_inputs(n, 11)
+    x[:4096] = np.linspace(-0.77, -0.73, 4096, dtype=np.float32)  # dense around x*
+    dy = np.random.default_rng(5).standard_normal(n).astype(np.float32)
+    y, mask = tops.gelu_ip_fwd(to_dev(x, cuda), table)
+    dx = tops.gelu_ip_bwd(to_dev(dy, cuda), y, mask, table)
+    torch.cuda.synchronize()
+    ry, rm = port.gelu_fwd(x, pt.x_star)
+    rdx = pt.gelu_bwd(dy, ry, rm)
+    assert rel_err(dx.cpu().numpy(), rdx) <= 1e-5
+
+
+def test_gelu_refusals(tops, table_text, cuda):
+    import torch
+    from paper_2210_10246_b200 import TempoError
+    x = torch.randn(64, device=cuda)
+    with pytest.raises(TempoError) as e:
+        tops.gelu_ip_fwd(x, None)
+    assert e.value.kind == "ConfigError"
+    unver = tops.GeluTable(table_text.replace("max_err=7.9034905239312725e-05", "max_err=-1"))
+    y, m = tops.gelu_ip_fwd(x, unver)  # forward builds
+    with pytest.raises(TempoError) as e:
+        tops.gelu_ip_bwd(torch.ones_like(x), y, m, unver)
+    assert e.value.kind == "ConfigError" and "sweep-verified" in str(e.value)
+
+
+# -------------------------------------------------------------- LayerNorm
+def ln_inputs(rows, cols, seed):
+    g = np.random.default_rng(seed)
+    x = (g.standard_normal((rows, cols)) * 1.7 + 0.4).astype(np.float32)
+    gam = (np.sign(g.standard_normal(cols)) * (1 + 0.2 * g.standard_normal(cols))).astype(np.float32)
+    bet = (0.1 * g.standard_normal(cols)).astype(np.float32)
+    dy = g.standard_normal((rows, cols)).astype(np.float32)
+    return x, gam, bet, dy
+
+
+@pytest.mark.parametrize("rows,cols", [(1, 768), (7, 1024), (333, 768), (64, 4), (5, 1000),
+                                       (3, 2052), (16384, 768)])
+def test_layernorm_forward(tops, port, cuda, rows, cols):
+    import torch
+    x, gam, bet, _ = ln_inputs(rows, cols, rows * cols)
+    y, rstd = tops.layernorm_ip_fwd(to_dev(x, cuda), to_dev(gam, cuda), to_dev(bet, cuda))
+    torch.cuda.synchronize()
+    ry, rrs, _ = port.ln_fwd(x, gam, bet, 1e-5)
+    assert rel_err(y.cpu().numpy(), ry) <= 1e-5
+    assert np.abs(rstd.cpu().numpy().astype(np.float64) / rrs - 1).max() <= 1e-6
+    # the fp64 moments reproduce the reference's y bit for bit almost always
+    assert np.mean(y.cpu().numpy() == ry) > 0.999
+
+
+@pytest.mark.parametrize("rows,cols", [(1, 768), (7, 1024), (333, 768), (64, 4), (5, 1000),
+                                       (3, 2052), (16384, 768)])
+def test_layernorm_backward_identical_inputs(tops, port, cuda, rows, cols):
+    import torch
+    x, gam, bet, dy = ln_inputs(rows, cols, 3 + rows * cols)
+    ry, rrs, _ = port.ln_fwd(x, gam, bet, 1e-5)
+    args = [to_dev(a, cuda) for a in (dy, ry, rrs, gam, bet)]
+    dx, dg, db = tops.layernorm_ip_bwd(*args)
+    torch.cuda.synchronize()
+    rdx, _, _ = port.ln_bwd(dy, ry, rrs, gam, bet, False)
+    _, dg64, db64 = port.ln_bwd(dy, ry, rrs, gam, bet, True)
+    assert rel_err(dx.cpu().numpy(), rdx) <= 1e-5
+    assert rel_err(dg.cpu().numpy(), dg64) <= 1e-5
+    assert rel_err(db.cpu().numpy(), db64) <= 1e-5
+    dx2, dg2, db2 = tops.layernorm_ip_bwd(*args)  # fixed reduction order
+    torch.cuda.synchronize()
+    assert torch.equal(dx, dx2) and torch.equal(dg, dg2) and torch.equal(db, db2)
+
+
+def test_layernorm_refusals(tops, cuda):
+    import torch
+    from paper_2210_10246_b200 import TempoError
+    x = torch.randn(2, 4, device=cuda)
+    gam = torch.ones(4, device=cuda)
+    gam[2] = 1e-13
+    with pytest.raises(TempoError) as e:
+        tops.layernorm_ip_fwd(x, gam, torch.zeros(4, device=cuda))
+    assert e.value.kind == "ParamError" and "gamma" in str(e.value)
+    status = torch.zeros(1, dtype=torch.int32, device=cuda)
+    tops.layernorm_ip_fwd(x, gam, torch.zeros(4, device=cuda), check_gamma=False,
+                          dev_status=status)
+    assert int(status.item()) == 3
+    with pytest.raises(TempoError) as e:
+        tops.layernorm_ip_fwd(x, torch.ones(4, device=cuda), torch.zeros(4, device=cuda), eps=0.0)
+    assert e.value.kind == "ParamError"
+
+
+# ------------------------------------------------- softmax + attention dropout
+@pytest.mark.parametrize("rows,cols", [(1, 512), (24, 512), (7, 384), (9, 1024), (5, 100),
+                                       (3, 77), (12 * 512, 512)])
+def test_softmax_dropout_supplied_mask(tops, port, cuda, rows, cols):
+    import torch
+    g = np.random.default_rng(rows + cols)
+    z = (g.standard_normal((rows, cols)) * 3).astype(np.float32)
+    p = 0.1
+    bits = tops.bernoulli_keep_bits(rows * cols, p, 1234)  # the reference's stream
+    keep = port.bernoulli_keep(rows * cols, p, 1234)
+    mask = bits_to_dev(bits, cuda)
+    P, D, mask_out = tops.softmax_dropout_fwd(to_dev(z, cuda), p, mask=mask)
+    torch.cuda.synchronize()
+    rP = port.softmax_fwd(z)
+    Pg = P.cpu().numpy()
+    assert np.all(np.abs(Pg - rP) <= 1e-5 * np.abs(rP) + 1e-9)
+    assert np.array_equal(D.cpu().numpy(), port.dropout_apply(Pg, keep, p).reshape(rows, cols))
+    assert np.array_equal(unpack(mask_out, rows * cols), keep)
+
+    dD = g.standard_normal((rows, cols)).astype(np.float32)
+    dZ, Drec = tops.attn_probs_bwd(to_dev(dD, cuda), P, mask, p, write_d=True)
+    torch.cuda.synchronize()
+    rdP = port.dropout_apply(dD, keep, p).reshape(rows, cols)
+    rdZ = port.softmax_bwd(rdP, Pg)
+    dZg = dZ.cpu().numpy()
+    assert np.all(np.abs(dZg - rdZ) <= 1e-5 * np.abs(rdZ) + 1e-8)
+    assert torch.equal(Drec, D)  # recompute == forward D, bitwise
+
+
+@pytest.mark.parametrize("rows,cols", [(24, 512), (5, 100)])
+def test_softmax_dropout_philox(tops, port, cuda, rows, cols):
+    import torch
+    g = np.random.default_rng(1)
+    z = (g.standard_normal((rows, cols)) * 2).astype(np.float32)
+    p = 0.25
+    zt = to_dev(z, cuda)
+    P, D, mask = tops.softmax_dropout_fwd(zt, p, seed=77)
+    torch.cuda.synchronize()
+    keep = unpack(mask, rows * cols)
+    assert abs(keep.mean() - (1 - p)) < 0.03
+    assert np.array_equal(D.cpu().numpy(), port.dropout_apply(P.cpu().numpy(), keep, p).reshape(rows, cols))
+    # same seed -> same mask; row shards with global offsets -> same mask
+    _, _, mask2 = tops.softmax_dropout_fwd(zt, p, seed=77)
+    assert torch.equal(mask, mask2)
+    if cols % 128 == 0:
+        half = rows // 2
+        _, _, ma = tops.softmax_dropout_fwd(zt[:half].contiguous(), p, seed=77, offset=0)
+        _, _, mb = tops.softmax_dropout_fwd(zt[half:].contiguous(), p, seed=77, offset=half * cols)
+        torch.cuda.synchronize()
+        assert np.array_equal(np.concatenate([unpack(ma, half * cols), unpack(mb, (rows - half) * cols)]), keep)
+
+
+@pytest.mark.parametrize("rows,cols", [(4, 512), (3, 130)])
+def test_plain_softmax(tops, port, cuda, rows, cols):
+    import torch
+    g = np.random.default_rng(2)
+    z = (g.standard_normal((rows, cols)) * 4).astype(np.float32)
+    P = tops.softmax_ip_fwd(to_dev(z, cuda))
+    dP = g.standard_normal((rows, cols)).astype(np.float32)
+    dZ = tops.softmax_ip_bwd(to_dev(dP, cuda), P)
+    torch.cuda.synchronize()
+    rP = port.softmax_fwd(z)
+    assert np.all(np.abs(P.cpu().numpy() - rP) <= 1e-5 * np.abs(rP) + 1e-9)
+    rdZ = port.softmax_bwd(dP, P.cpu().numpy())
+    assert np.all(np.abs(dZ.cpu().numpy() - rdZ) <= 1e-5 * np.abs(rdZ) + 1e-8)
+
+
+def test_softmax_frozen_row(tops, cuda):
+    import math
+    import torch
+    z = torch.tensor([[math.log(1.0), math.log(3.0)]], device=cuda)
+    P = tops.softmax_ip_fwd(z)
+    dZ = tops.softmax_ip_bwd(torch.tensor([[1.0, 0.0]], device=cuda), P)
+    torch.cuda.synchronize()
+    assert P.cpu().numpy() == pytest.approx([[0.25, 0.75]], rel=1e-6)
+    assert dZ.cpu().numpy() == pytest.approx([[0.1875, -0.1875]], rel=1e-5)
+
+
+# ---------------------------------------------------------------- dropout
+@pytest.mark.parametrize("n", [1, 33, 128, 1000, 128 * 77 + 5, 1 << 22])
+def test_hidden_dropout(tops, port, cuda, n):
+    import torch
+    g = np.random.default_rng(n)
+    x = g.standard_normal(n).astype(np.float32)
+    dy = g.standard_normal(n).astype(np.float32)
+    p = 0.1
+    bits = tops.bernoulli_keep_bits(n, p, 99)
+    keep = port.bernoulli_keep(n, p, 99)
+    mask = bits_to_dev(bits, cuda)
+    y, _ = tops.dropout_fwd(to_dev(x, cuda), p, mask=mask)
+    dx = tops.dropout_bwd(to_dev(dy, cuda), mask, p)
+    torch.cuda.synchronize()
+    assert np.array_equal(y.cpu().numpy(), port.dropout_apply(x, keep, p))
+    assert np.array_equal(dx.cpu().numpy(), port.dropout_apply(dy, keep, p))
+    # Philox: generated mask consistent with the output, shard-invariant
+    y2, m2 = tops.dropout_fwd(to_dev(x, cuda), p, seed=5)
+    torch.cuda.synchronize()
+    k2 = unpack(m2, n)
+    assert np.array_equal(y2.cpu().numpy(), port.dropout_apply(x, k2, p))
+    if n >= 256 and n % 128 == 0:
+        xt = to_dev(x, cuda)
+        h = (n // 2) // 128 * 128
+        _, ma = tops.dropout_fwd(xt[:h], p, seed=5, offset=0)
+        _, mb = tops.dropout_fwd(xt[h:], p, seed=5, offset=h)
+        torch.cuda.synchronize()
+        assert np.array_equal(np.concatenate([unpack(ma, h), unpack(mb, n - h)]), k2)
+
+
+def test_golden_fixtures_on_gpu(tops, golden, table_text, cuda):
+    """The reference-generated fixtures, end to end on the device."""
+    import torch
+    g = golden
+    table = tops.GeluTable(table_text)
+    y, m = tops.gelu_ip_fwd(to_dev(g["gelu_x"], cuda), table)
+    dx = tops.gelu_ip_bwd(to_dev(g["gelu_dy"], cuda), y, m, table)
+    torch.cuda.synchronize()
+    assert np.array_equal(unpack(m, g["gelu_x"].size), g["gelu_mask"])
+    fin = np.isfinite(g["gelu_y"])
+    assert ulp_diff(y.cpu().numpy()[fin], g["gelu_y"][fin]).max() <= 5
+    assert rel_err(dx.cpu().numpy(), g["gelu_dx"]) <= 1e-5
+    ly, lrs = tops.layernorm_ip_fwd(to_dev(g["ln_x"], cuda), to_dev(g["ln_gamma"], cuda),
+                                    to_dev(g["ln_beta"], cuda))
+    ldx, ldg, ldb = tops.layernorm_ip_bwd(to_dev(g["ln_dy"], cuda), ly, lrs,
+                                          to_dev(g["ln_gamma"], cuda), to_dev(g["ln_beta"], cuda))
+    torch.cuda.synchronize()
+    assert rel_err(ly.cpu().numpy(), g["ln_y"]) <= 1e-5
+    assert rel_err(ldx.cpu().numpy(), g["ln_dx"]) <= 1e-5
+    assert rel_err(ldg.cpu().numpy(), g["ln_dgamma_f64"]) <= 1e-5
+    assert rel_err(ldb.cpu().numpy(), g["ln_dbeta_f64"]) <= 1e-5
+    keep = g["sm_keep"].reshape(-1)
+    bits = np.packbits(keep, bitorder="little")
+    bits = np.concatenate([bits, np.zeros((-bits.size) % 4, np.uint8)]).view(np.uint32)
+    mask = bits_to_dev(bits, cuda)
+    P, D, _ = tops.softmax_dropout_fwd(to_dev(g["sm_z"], cuda), float(g["sm_p"]), mask=mask)
+    dZ, _ = tops.attn_probs_bwd(to_dev(g["sm_dD"], cuda), P, mask, float(g["sm_p"]))
+    torch.cuda.synchronize()
+    rP = g["sm_P"]
+    assert np.all(np.abs(P.cpu().numpy() - rP) <= 1e-5 * np.abs(rP) + 1e-9)
+    assert np.all(np.abs(dZ.cpu().numpy() - g["sm_dZ"]) <= 1e-5 * np.abs(g["sm_dZ"]) + 1e-8)
+
+
+def test_mask_pack_roundtrip(tops, cuda):
+    import torch
+    g = np.random.default_rng(0)
+    for n in (1, 31, 32, 1000, 4097):
+        b = (g.random(n) < 0.5).astype(np.uint8)
+        bits = tops.pack_mask(to_dev(b, cuda))
+        back = tops.unpack_mask(bits, n)
+        torch.cuda.synchronize()
+        assert np.array_equal(back.cpu().numpy(), b)
+    st = torch.zeros(1, dtype=torch.int32, device=cuda)
+    tops.pack_mask(to_dev(np.array([0, 1, 2], np.uint8), cuda), dev_status=st)
+    assert int(st.item()) == 3  # BoolMask::from_bytes refuses bytes > 1
