@@ -54,23 +54,18 @@ __device__ __forceinline__ void st_stream(uint32_t* p, uint32_t v) {
 // lanes 8w..8w+7, bit (4j + k) = element 4(8w+j) + k: the linear BoolMask
 // order (tensor.cpp:199-201).
 //
-// pack: four warp ballots (one per float4 component) are bit-interleaved;
-// lane w (w < 4) returns word w.  Every lane computes its w = lane & 3 copy.
-__device__ __forceinline__ uint32_t spread8(uint32_t b) {  // bit j -> bit 4j
-    b &= 0xffu;
-    b = (b | (b << 12)) & 0x000f000fu;
-    b = (b | (b << 6)) & 0x03030303u;
-    b = (b | (b << 3)) & 0x11111111u;
-    return b;
+// pack: lane L contributes the nibble of its 4 elements; three xor-shuffles
+// OR the 8 nibbles of each 8-lane group into that group's word, which lane
+// 8w stores (the 4 words of a chunk are contiguous: one 16-byte sector).
+__device__ __forceinline__ uint32_t nibble4(bool k0, bool k1, bool k2, bool k3) {
+    return (uint32_t)k0 | ((uint32_t)k1 << 1) | ((uint32_t)k2 << 2) | ((uint32_t)k3 << 3);
 }
-__device__ __forceinline__ uint32_t pack_chunk_bits(bool k0, bool k1, bool k2, bool k3, int lane) {
-    uint32_t b0 = __ballot_sync(kFull, k0);
-    uint32_t b1 = __ballot_sync(kFull, k1);
-    uint32_t b2 = __ballot_sync(kFull, k2);
-    uint32_t b3 = __ballot_sync(kFull, k3);
-    int sh = 8 * (lane & 3);
-    return spread8(b0 >> sh) | (spread8(b1 >> sh) << 1) | (spread8(b2 >> sh) << 2) |
-           (spread8(b3 >> sh) << 3);
+__device__ __forceinline__ void store_chunk_mask(uint32_t* chunk_words, uint32_t nib, int lane) {
+    uint32_t v = nib << ((lane & 7) << 2);
+    v |= __shfl_xor_sync(kFull, v, 1);
+    v |= __shfl_xor_sync(kFull, v, 2);
+    v |= __shfl_xor_sync(kFull, v, 4);
+    if ((lane & 7) == 0) st_stream(chunk_words + (lane >> 3), v);
 }
 // unpack: the 4 bits of lane L's float4 from the chunk's word (L >> 3).
 __device__ __forceinline__ uint32_t chunk_nibble(const uint32_t* chunk_words, int lane) {
@@ -112,8 +107,55 @@ __device__ __forceinline__ uint32_t philox_at(uint64_t seed, uint64_t global_ind
     }
 }
 
+// ---- TMA bulk copies + mbarriers (cp.async.bulk, sm_90+/sm_100a) ---------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+// Arrive (count 1) and add `bytes` to the barrier's expected transaction count.
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "TB_WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra TB_WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+// Order this thread's generic-proxy smem accesses before later async-proxy
+// (TMA) writes to the same smem (stage reuse).
+__device__ __forceinline__ void fence_proxy_async_smem() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+// global -> shared bulk copy (16-byte aligned, size % 16 == 0), completing
+// `bytes` transactions on `bar`.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+            "r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
 // ---- warp reductions -----------------------------------------------------
 __device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+    return v;
+}
+__device__ __forceinline__ float warp_sumf(float v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
     return v;

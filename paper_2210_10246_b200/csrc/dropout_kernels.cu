@@ -16,7 +16,7 @@ namespace tb {
 namespace {
 
 constexpr int kBlock = 256;
-constexpr int kUnroll = 2;
+constexpr int kUnroll = 4;
 
 __device__ __forceinline__ float dscale(float v, double s) { return (float)((double)v * s); }
 
@@ -72,10 +72,8 @@ __global__ void __launch_bounds__(kBlock) dropout_fwd_vec_kernel(
                     U4 r = philox_quad(seed, (offset + e0) >> 2);
                     bool k0 = (uint64_t)r.x >= thresh, k1 = (uint64_t)r.y >= thresh;
                     bool k2 = (uint64_t)r.z >= thresh, k3 = (uint64_t)r.w >= thresh;
-                    uint32_t word = pack_chunk_bits(k0, k1, k2, k3, lane);
-                    if (lane < 4) st_stream(mask + ((c0 + u) << 2) + lane, word);
-                    nib[u] = (uint32_t)k0 | ((uint32_t)k1 << 1) | ((uint32_t)k2 << 2) |
-                             ((uint32_t)k3 << 3);
+                    nib[u] = nibble4(k0, k1, k2, k3);
+                    store_chunk_mask(mask + ((c0 + u) << 2), nib[u], lane);
                 }
                 float4 o;
                 o.x = (nib[u] & 1u) ? dscale(v[u].x, scale) : 0.0f;

@@ -11,6 +11,8 @@
 // (2) x < -13, +-inf and NaN: the reference formula itself in fp64.
 #pragma once
 
+#include "gelu_math.h"
+
 // Expansion point: the double nearest the GELU minimum (g'(x*) = 0).
 #define TM_GELU_XSTAR_D (-0.7517915246935645)
 #define TM_GELU_XSTAR_F (-0.751791525f)
@@ -37,13 +39,20 @@ __device__ __forceinline__ double tm_gelu_exact(float x) {
     return xd * (0.5 * erfc(-xd * 0.70710678118654752440));
 }
 
-// Full forward for one element: fp32 fast path, fp64 where needed.
+// Does x need an fp64 path?
+__device__ __forceinline__ bool tm_gelu_needs_slow(float x) {
+    return fabsf(x - TM_GELU_XSTAR_F) < TM_GELU_TAYLOR_WINDOW || !(x >= TM_GELU_FAST_XMIN) ||
+           x == __int_as_float(0x7f800000);
+}
+
+__device__ __noinline__ float tm_gelu_slow(float x) {
+    if (fabsf(x - TM_GELU_XSTAR_F) < TM_GELU_TAYLOR_WINDOW) return (float)tm_gelu_taylor(x);
+    return (float)tm_gelu_exact(x);
+}
+
+// Full forward for one element.
 __device__ __forceinline__ float tm_gelu_fwd(float x) {
     float y = tm_gelu_fast(x);
-    if (fabsf(x - TM_GELU_XSTAR_F) < TM_GELU_TAYLOR_WINDOW) {
-        y = (float)tm_gelu_taylor(x);
-    } else if (!(x >= TM_GELU_FAST_XMIN) || isinf(x)) {
-        y = (float)tm_gelu_exact(x);
-    }
+    if (tm_gelu_needs_slow(x)) y = tm_gelu_slow(x);
     return y;
 }

@@ -21,7 +21,7 @@ namespace tb {
 namespace {
 
 constexpr int kBlock = 256;
-constexpr int kUnroll = 2;  // chunks in flight per warp
+constexpr int kUnroll = 4;  // chunks in flight per warp
 
 // ---------------------------------------------------------------- forward
 __device__ __forceinline__ void gelu_fwd_scalar_words(const float* __restrict__ x,
@@ -61,14 +61,23 @@ __global__ void __launch_bounds__(kBlock) gelu_fwd_vec_kernel(const float* __res
         for (int u = 0; u < kUnroll; ++u) {
             if (c0 + u < nchunks) {  // warp-uniform
                 float4 o;
-                o.x = tm_gelu_fwd(v[u].x);
-                o.y = tm_gelu_fwd(v[u].y);
-                o.z = tm_gelu_fwd(v[u].z);
-                o.w = tm_gelu_fwd(v[u].w);
-                uint32_t word = pack_chunk_bits(v[u].x >= xstar_gt, v[u].y >= xstar_gt,
-                                                v[u].z >= xstar_gt, v[u].w >= xstar_gt, lane);
+                o.x = tm_gelu_fast(v[u].x);
+                o.y = tm_gelu_fast(v[u].y);
+                o.z = tm_gelu_fast(v[u].z);
+                o.w = tm_gelu_fast(v[u].w);
+                const bool s0 = tm_gelu_needs_slow(v[u].x), s1 = tm_gelu_needs_slow(v[u].y);
+                const bool s2 = tm_gelu_needs_slow(v[u].z), s3 = tm_gelu_needs_slow(v[u].w);
+                if (__any_sync(kFull, s0 | s1 | s2 | s3)) {  // rare: fp64 fix-ups
+                    if (s0) o.x = tm_gelu_slow(v[u].x);
+                    if (s1) o.y = tm_gelu_slow(v[u].y);
+                    if (s2) o.z = tm_gelu_slow(v[u].z);
+                    if (s3) o.w = tm_gelu_slow(v[u].w);
+                }
                 st_stream(y4 + ((c0 + u) << 5) + lane, o);
-                if (lane < 4) st_stream(mask + ((c0 + u) << 2) + lane, word);
+                store_chunk_mask(mask + ((c0 + u) << 2),
+                                 nibble4(v[u].x >= xstar_gt, v[u].y >= xstar_gt,
+                                         v[u].z >= xstar_gt, v[u].w >= xstar_gt),
+                                 lane);
             }
         }
     }
@@ -221,6 +230,145 @@ __global__ void __launch_bounds__(kBlock) gelu_bwd_scalar_kernel(
     gelu_bwd_scalar_words(dy, y, mask, dx, n, t, st, coef, maxseg, warp, nwarps, lane);
 }
 
+// ------------------------------------------------ backward, specialized path
+// Tables with <= 4 segments per branch and <= 16 coefficients (the default
+// fit: 3 + 3 segments, degree <= 10) use compile-time NC4 = ceil(ncoef/4):
+//  * segment search against thresholds held in registers (no smem),
+//  * the segment's coefficients read as NC4 128-bit smem loads from a
+//    record whose stride keeps up to 8 segments on distinct bank groups,
+//  * (s, b) of t = u*s + b as one 64-bit smem load,
+//  * a fully unrolled Clenshaw over the zero-padded coefficients,
+//  * sqrt.approx for the sqrt-shift variable (rel. error ~2^-23, far inside
+//    the 1e-5 tolerance after the smooth Chebyshev map),
+// and no data-dependent branches.
+constexpr int kFastSegPerBranch = 4;
+
+template <int NC4>
+struct FastTable {
+    static constexpr int kStride4 = (NC4 & 1) ? NC4 : NC4 + 1;  // float4 units
+    float4 rec[kMaxSeg * kStride4];
+    float2 sb[kMaxSeg];
+};
+
+__device__ __forceinline__ float sqrt_approx(float v) {
+    float r;
+    asm("sqrt.approx.f32 %0, %1;" : "=f"(r) : "f"(v));
+    return r;
+}
+
+template <int NC4>
+__device__ __forceinline__ float gelu_h_fast(float y, uint32_t m, const FastTable<NC4>& ft,
+                                             const float (&thr0)[3], const float (&thr1)[3],
+                                             int base1, uint32_t sqrt_mask, float ymin_up,
+                                             float ymin_hi, float ymin_lo) {
+    int seg = m ? base1 : 0;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) seg += (y >= (m ? thr1[k] : thr0[k])) ? 1 : 0;
+    const float2 sb = ft.sb[seg];
+    const float d = (y - ymin_hi) - ymin_lo;
+    const float u = ((sqrt_mask >> seg) & 1u) ? sqrt_approx(fmaxf(d, 0.0f)) : y;
+    float tt = fminf(fmaxf(fmaf(u, sb.x, sb.y), -1.0f), 1.0f);
+    tt = (y < ymin_up) ? -1.0f : tt;  // clamped to y_min: u == u_lo
+    tt = (sb.x == 0.0f) ? 0.0f : tt;  // constant segment
+    const float t2 = tt + tt;
+    const float4* rec = ft.rec + seg * FastTable<NC4>::kStride4;
+    float c[4 * NC4];
+#pragma unroll
+    for (int j = 0; j < NC4; ++j) {
+        const float4 q = rec[j];
+        c[4 * j] = q.x;
+        c[4 * j + 1] = q.y;
+        c[4 * j + 2] = q.z;
+        c[4 * j + 3] = q.w;
+    }
+    float b1 = 0.0f, b2 = 0.0f;
+#pragma unroll
+    for (int k = 4 * NC4 - 1; k >= 1; --k) {
+        const float bk = fmaf(t2, b1, c[k] - b2);
+        b2 = b1;
+        b1 = bk;
+    }
+    float h = fmaf(tt, b1, c[0] - b2);
+    h = (m == 0u && y >= 0.0f) ? 0.0f : h;  // far left tail (:182)
+    return isnan(y) ? y : h;
+}
+
+template <int NC4>
+__global__ void __launch_bounds__(kBlock) gelu_bwd_fast_kernel(
+    const float* __restrict__ dy, const float* __restrict__ y, const uint32_t* __restrict__ mask,
+    float* __restrict__ dx, int64_t n, const __grid_constant__ GeluDevTable t) {
+    __shared__ FastTable<NC4> ft;
+    const int nseg = t.nseg[0] + t.nseg[1];
+    for (int i = threadIdx.x; i < nseg * FastTable<NC4>::kStride4; i += kBlock) {
+        const int sgi = i / FastTable<NC4>::kStride4, j = i - sgi * FastTable<NC4>::kStride4;
+        float4 q = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (j < NC4) {
+            const int k = 4 * j;
+            q.x = k < t.ncoef ? t.coef[sgi][k] : 0.f;
+            q.y = k + 1 < t.ncoef ? t.coef[sgi][k + 1] : 0.f;
+            q.z = k + 2 < t.ncoef ? t.coef[sgi][k + 2] : 0.f;
+            q.w = k + 3 < t.ncoef ? t.coef[sgi][k + 3] : 0.f;
+        }
+        ft.rec[i] = q;
+    }
+    for (int i = threadIdx.x; i < nseg; i += kBlock) ft.sb[i] = make_float2(t.s[i], t.b[i]);
+    float thr0[3], thr1[3];
+    uint32_t sqrt_mask = 0;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        thr0[k] = k + 1 < t.nseg[0] ? t.lo_up[k + 1] : __int_as_float(0x7fffffff);  // NaN: never >=
+        thr1[k] = k + 1 < t.nseg[1] ? t.lo_up[t.nseg[0] + k + 1] : __int_as_float(0x7fffffff);
+    }
+    for (int i = 0; i < nseg; ++i) sqrt_mask |= (t.sqrt_shift[i] ? 1u : 0u) << i;
+    const int base1 = t.nseg[0];
+    const float ymin_up = t.ymin_up, ymin_hi = t.ymin_hi, ymin_lo = t.ymin_lo;
+    __syncthreads();
+
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = ((int64_t)blockIdx.x * kBlock + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * kBlock) >> 5;
+    const int64_t nchunks = n >> 7;
+    const float4* dy4 = reinterpret_cast<const float4*>(dy);
+    const float4* y4 = reinterpret_cast<const float4*>(y);
+    float4* dx4 = reinterpret_cast<float4*>(dx);
+    constexpr int U = 2;
+    for (int64_t c0 = warp * U; c0 < nchunks; c0 += nwarps * U) {
+        float4 g[U], v[U];
+        uint32_t nib[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (c0 + u < nchunks) {
+                const int64_t off = ((c0 + u) << 5) + lane;
+                v[u] = ld_stream(y4 + off);
+                g[u] = ld_stream(dy4 + off);
+                nib[u] = chunk_nibble(mask + ((c0 + u) << 2), lane);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (c0 + u < nchunks) {
+#define TB_H(val, bit) gelu_h_fast<NC4>(val, (nib[u] >> bit) & 1u, ft, thr0, thr1, base1, \
+                                        sqrt_mask, ymin_up, ymin_hi, ymin_lo)
+                float4 o;
+                o.x = g[u].x * TB_H(v[u].x, 0);
+                o.y = g[u].y * TB_H(v[u].y, 1);
+                o.z = g[u].z * TB_H(v[u].z, 2);
+                o.w = g[u].w * TB_H(v[u].w, 3);
+#undef TB_H
+                st_stream(dx4 + ((c0 + u) << 5) + lane, o);
+            }
+        }
+    }
+    // ragged tail (< 128 elements): scalar, same math
+    if (warp == nwarps - 1) {
+        for (int64_t i = (nchunks << 7) + lane; i < n; i += 32) {
+            const uint32_t m = (mask[i >> 5] >> (i & 31)) & 1u;
+            dx[i] = dy[i] * gelu_h_fast<NC4>(y[i], m, ft, thr0, thr1, base1, sqrt_mask, ymin_up,
+                                             ymin_hi, ymin_lo);
+        }
+    }
+}
+
 inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
 }  // namespace
@@ -244,6 +392,28 @@ cudaError_t launch_gelu_bwd(const float* dy, const float* y, const uint32_t* mas
                             const GeluDevTable& t, float* dx, int64_t n, cudaStream_t st) {
     if (n == 0) return cudaSuccess;
     const bool vec = aligned16(dy) && aligned16(y) && aligned16(dx) && aligned16(mask);
+    const bool fast = vec && t.nseg[0] <= kFastSegPerBranch && t.nseg[1] <= kFastSegPerBranch &&
+                      t.ncoef <= 16;
+    if (fast) {
+        const int nc4 = (t.ncoef + 3) / 4;
+        const int64_t blocks = ((n >> 7) / 2 + 1) * 32 / kBlock + 1;
+#define TB_CASE(NC)                                                                       \
+    case NC: {                                                                            \
+        auto k = gelu_bwd_fast_kernel<NC>;                                                \
+        int grid = grid_for((const void*)k, kBlock, 0, blocks);                           \
+        k<<<grid, kBlock, 0, st>>>(dy, y, mask, dx, n, t);                                \
+        break;                                                                            \
+    }
+        switch (nc4) {
+            TB_CASE(1)
+            TB_CASE(2)
+            TB_CASE(3)
+            TB_CASE(4)
+            default: return cudaErrorInvalidValue;
+        }
+#undef TB_CASE
+        return cudaGetLastError();
+    }
     const size_t smem = (size_t)(t.nseg[0] + t.nseg[1]) * t.stride * sizeof(float);
     const void* k = vec ? (const void*)gelu_bwd_vec_kernel : (const void*)gelu_bwd_scalar_kernel;
     const int64_t warps_needed = vec ? ((n >> 7) + kUnroll - 1) / kUnroll + 1 : (n + 31) >> 5;

@@ -18,7 +18,8 @@
 //
 // Layout: a CTA spans the columns of a row (thread t owns the float4 at
 // column 4t), gamma/beta for its columns stay in registers, and the CTA
-// walks rows with a grid stride, kRows rows in flight.  Row reductions are
+// walks row tiles with a grid stride; the tiles arrive through a TMA
+// (cp.async.bulk) ring in shared memory, kStages deep.  Row reductions are
 // warp shuffles plus one smem exchange (fixed order, identical in every
 // thread).  cols % 4 != 0, cols > 2048 or unaligned pointers use the
 // generic kernels (one element per thread per pass).
@@ -65,12 +66,45 @@ __device__ __forceinline__ float ln_y(float x, double mean_f, double rs, double 
 }
 
 // ------------------------------------------------------------------ forward
+// TMA-staged pipeline: thread 0 streams row tiles (kRows contiguous rows)
+// into a kStages-deep shared-memory ring with cp.async.bulk, completing on
+// one mbarrier per stage; all threads consume a tile from smem (thread t:
+// the float4 at column 4t), so HBM reads stay in flight across the block
+// reductions.  A stage is refilled as soon as the tile's first block
+// reduction proves every thread has read it.
+constexpr int kStages = 4;
+
+__device__ __forceinline__ void ln_issue(const float* src, int64_t tile, int tile_rows,
+                                         int64_t rows, int cols, float* dst, uint64_t* bar) {
+    const int64_t r0 = tile * tile_rows;
+    const int nr = (int)min((int64_t)tile_rows, rows - r0);
+    const uint32_t bytes = (uint32_t)nr * (uint32_t)cols * 4u;
+    mbar_expect_tx(bar, bytes);
+    bulk_g2s(dst, src + r0 * cols, bytes, bar);
+}
+
 __global__ void __launch_bounds__(kMaxThreads) ln_fwd_vec_kernel(
     const float* __restrict__ x, const float* __restrict__ gamma, const float* __restrict__ beta,
     double eps, float* __restrict__ y, float* __restrict__ rstd, int64_t rows, int cols,
     int32_t* __restrict__ status) {
+    extern __shared__ __align__(128) unsigned char dsm[];
+    uint64_t* full = reinterpret_cast<uint64_t*>(dsm);
+    float* ring = reinterpret_cast<float*>(dsm + 128);
     __shared__ double red[2 * 2 * kRows * 32];
     int phase = 0;
+    const int tile_floats = kRows * cols;
+    const int64_t ntiles = (rows + kRows - 1) / kRows;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kStages; ++s) mbar_init(&full[s], 1);
+        mbar_fence_init();
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kStages; ++s) {
+            const int64_t t = blockIdx.x + (int64_t)s * gridDim.x;
+            if (t < ntiles) ln_issue(x, t, kRows, rows, cols, ring + s * tile_floats, &full[s]);
+        }
+    }
     const int c4 = threadIdx.x;  // float4 column group
     const bool act = c4 * 4 < cols;
     float4 g = make_float4(1.f, 1.f, 1.f, 1.f), b = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -84,17 +118,28 @@ __global__ void __launch_bounds__(kMaxThreads) ln_fwd_vec_kernel(
             }
         }
     }
-    for (int64_t r0 = (int64_t)blockIdx.x * kRows; r0 < rows; r0 += (int64_t)gridDim.x * kRows) {
+    int it = 0;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+        const int st = it % kStages;
+        mbar_wait(&full[st], (uint32_t)((it / kStages) & 1));
+        const int64_t r0 = tile * kRows;
+        const float* sp = ring + st * tile_floats;
         float4 v[kRows];
         double s[kRows];
 #pragma unroll
         for (int i = 0; i < kRows; ++i) {
             v[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (act && r0 + i < rows)
-                v[i] = ld_stream(reinterpret_cast<const float4*>(x + (r0 + i) * cols) + c4);
+            if (act && r0 + i < rows) v[i] = reinterpret_cast<const float4*>(sp + i * cols)[c4];
             s[i] = ((double)v[i].x + (double)v[i].y) + ((double)v[i].z + (double)v[i].w);
         }
         block_sum<kRows>(s, red, phase);
+        if (threadIdx.x == 0) {  // every thread has read stage st: refill it
+            const int64_t nt = tile + (int64_t)kStages * gridDim.x;
+            if (nt < ntiles) {
+                fence_proxy_async_smem();
+                ln_issue(x, nt, kRows, rows, cols, ring + st * tile_floats, &full[st]);
+            }
+        }
         double mean[kRows], q[kRows];
 #pragma unroll
         for (int i = 0; i < kRows; ++i) {
@@ -109,8 +154,8 @@ __global__ void __launch_bounds__(kMaxThreads) ln_fwd_vec_kernel(
         for (int i = 0; i < kRows; ++i) {
             const int64_t r = r0 + i;
             if (r >= rows) break;
-            const double mean_f = (double)(float)mean[i];    // F32 store, kernels.cpp:174
-            const float var_f = (float)(q[i] / (double)cols);  // F32 store, kernels.cpp:176
+            const double mean_f = (double)(float)mean[i];       // F32 store, kernels.cpp:174
+            const float var_f = (float)(q[i] / (double)cols);   // F32 store, kernels.cpp:176
             const double rs = 1.0 / sqrt((double)var_f + eps);  // ops_reference.cpp:58
             if (act) {
                 float4 o;
@@ -161,12 +206,37 @@ __global__ void __launch_bounds__(256) ln_fwd_generic_kernel(
 // ----------------------------------------------------------------- backward
 // Stage 1, vector path: dx per row, per-CTA fp64 column partials of
 // dgamma = sum g*xhat and dbeta = sum g, written to ws[cta][2][cols].
+// Same TMA ring as the forward; a stage holds kRowsB rows of dy and of y.
 __global__ void __launch_bounds__(kMaxThreads) ln_bwd_vec_kernel(
     const float* __restrict__ dy, const float* __restrict__ y, const float* __restrict__ rstd,
     const float* __restrict__ gamma, const float* __restrict__ beta, float* __restrict__ dx,
     double* __restrict__ ws, int64_t rows, int cols) {
+    extern __shared__ __align__(128) unsigned char dsm[];
+    uint64_t* full = reinterpret_cast<uint64_t*>(dsm);
+    float* ring = reinterpret_cast<float*>(dsm + 128);
     __shared__ double red[2 * 2 * kRowsB * 32];
     int phase = 0;
+    const int tile_floats = kRowsB * cols;  // per tensor; a stage holds dy then y
+    const int64_t ntiles = (rows + kRowsB - 1) / kRowsB;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kStages; ++s) mbar_init(&full[s], 1);
+        mbar_fence_init();
+    }
+    __syncthreads();
+    auto issue = [&](int64_t t, int s) {
+        const int64_t r0 = t * kRowsB;
+        const int nr = (int)min((int64_t)kRowsB, rows - r0);
+        const uint32_t bytes = (uint32_t)nr * (uint32_t)cols * 4u;
+        mbar_expect_tx(&full[s], 2 * bytes);
+        bulk_g2s(ring + (2 * s) * tile_floats, dy + r0 * cols, bytes, &full[s]);
+        bulk_g2s(ring + (2 * s + 1) * tile_floats, y + r0 * cols, bytes, &full[s]);
+    };
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kStages; ++s) {
+            const int64_t t = blockIdx.x + (int64_t)s * gridDim.x;
+            if (t < ntiles) issue(t, s);
+        }
+    }
     const int c4 = threadIdx.x;
     const bool act = c4 * 4 < cols;
     double gm[4] = {1, 1, 1, 1}, bt[4] = {0, 0, 0, 0}, ig[4] = {1, 1, 1, 1};
@@ -180,7 +250,13 @@ __global__ void __launch_bounds__(kMaxThreads) ln_bwd_vec_kernel(
     }
     double pg[4] = {0, 0, 0, 0}, pb[4] = {0, 0, 0, 0};  // column partials
     const double inv_m = 1.0 / (double)cols;
-    for (int64_t r0 = (int64_t)blockIdx.x * kRowsB; r0 < rows; r0 += (int64_t)gridDim.x * kRowsB) {
+    int it = 0;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+        const int st = it % kStages;
+        mbar_wait(&full[st], (uint32_t)((it / kStages) & 1));
+        const int64_t r0 = tile * kRowsB;
+        const float* gs = ring + (2 * st) * tile_floats;
+        const float* ys = ring + (2 * st + 1) * tile_floats;
         float4 gv[kRowsB], yv[kRowsB];
         float rsv[kRowsB];
 #pragma unroll
@@ -190,8 +266,8 @@ __global__ void __launch_bounds__(kMaxThreads) ln_bwd_vec_kernel(
             rsv[i] = 0.f;
             if (r0 + i < rows) {
                 if (act) {
-                    gv[i] = ld_stream(reinterpret_cast<const float4*>(dy + (r0 + i) * cols) + c4);
-                    yv[i] = ld_stream(reinterpret_cast<const float4*>(y + (r0 + i) * cols) + c4);
+                    gv[i] = reinterpret_cast<const float4*>(gs + i * cols)[c4];
+                    yv[i] = reinterpret_cast<const float4*>(ys + i * cols)[c4];
                 }
                 rsv[i] = __ldg(rstd + r0 + i);
             }
@@ -213,6 +289,13 @@ __global__ void __launch_bounds__(kMaxThreads) ln_bwd_vec_kernel(
             s[2 * i + 1] = act ? s2 : 0.0;
         }
         block_sum<2 * kRowsB>(s, red, phase);
+        if (threadIdx.x == 0) {  // stage consumed by every thread: refill
+            const int64_t nt = tile + (int64_t)kStages * gridDim.x;
+            if (nt < ntiles) {
+                fence_proxy_async_smem();
+                issue(nt, st);
+            }
+        }
 #pragma unroll
         for (int i = 0; i < kRowsB; ++i) {
             if (r0 + i >= rows || !act) continue;
@@ -320,11 +403,14 @@ int vec_threads(int64_t cols) { return (int)(((cols / 4) + 31) / 32 * 32); }
 
 // Stage-1 grid for the backward: its CTA count is also the number of
 // partial rows in the workspace, so it depends only on (rows, cols, device).
+size_t fwd_smem(int64_t cols) { return 128 + (size_t)kStages * kRows * cols * sizeof(float); }
+size_t bwd_smem(int64_t cols) { return 128 + (size_t)kStages * 2 * kRowsB * cols * sizeof(float); }
+
 int bwd_grid(int64_t rows, int64_t cols, bool vec) {
     int64_t work = vec ? (rows + kRowsB - 1) / kRowsB : rows;
     const void* k = vec ? (const void*)ln_bwd_vec_kernel : (const void*)ln_bwd_generic_kernel;
     int block = vec ? vec_threads(cols) : 256;
-    size_t smem = vec ? 0 : (size_t)2 * cols * sizeof(double);
+    size_t smem = vec ? bwd_smem(cols) : (size_t)2 * cols * sizeof(double);
     return grid_for(k, block, smem, work);
 }
 
@@ -336,9 +422,10 @@ cudaError_t launch_ln_fwd(const float* x, const float* gamma, const float* beta,
     if (rows == 0) return cudaSuccess;
     if (use_vec(cols, x, y, gamma, beta, x)) {
         int block = vec_threads(cols);
-        int grid = grid_for((const void*)ln_fwd_vec_kernel, block, 0, (rows + kRows - 1) / kRows);
-        ln_fwd_vec_kernel<<<grid, block, 0, st>>>(x, gamma, beta, eps, y, rstd, rows, (int)cols,
-                                                   dev_status);
+        size_t smem = fwd_smem(cols);
+        int grid = grid_for((const void*)ln_fwd_vec_kernel, block, smem, (rows + kRows - 1) / kRows);
+        ln_fwd_vec_kernel<<<grid, block, smem, st>>>(x, gamma, beta, eps, y, rstd, rows,
+                                                      (int)cols, dev_status);
     } else {
         int grid = grid_for((const void*)ln_fwd_generic_kernel, 256, 0, rows);
         ln_fwd_generic_kernel<<<grid, 256, 0, st>>>(x, gamma, beta, eps, y, rstd, rows,
@@ -370,8 +457,8 @@ cudaError_t launch_ln_bwd(const float* dy, const float* y, const float* rstd, co
     const int grid = bwd_grid(rows, cols, vec);
     double* w = static_cast<double*>(ws);
     if (vec) {
-        ln_bwd_vec_kernel<<<grid, vec_threads(cols), 0, st>>>(dy, y, rstd, gamma, beta, dx, w,
-                                                              rows, (int)cols);
+        ln_bwd_vec_kernel<<<grid, vec_threads(cols), bwd_smem(cols), st>>>(
+            dy, y, rstd, gamma, beta, dx, w, rows, (int)cols);
     } else {
         size_t smem = (size_t)2 * cols * sizeof(double);
         ln_bwd_generic_kernel<<<grid, 256, smem, st>>>(dy, y, rstd, gamma, beta, dx, w, rows,

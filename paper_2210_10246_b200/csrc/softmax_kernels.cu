@@ -11,11 +11,12 @@
 //   recompute of D for the consumer, ops_tempo.cpp:17-26), fused:
 //   read dD, P (8 B) + bit, write dZ (4 B)   = 12.125 B/elem (+4 B with D).
 //
-// Numerics follow the reference's F32 path: dP and D are the fp64 products
-// rounded once (bit-exact with mask_scale on the same inputs), the row dot
-// sum(dP*P) and the softmax denominator accumulate in fp64, exp runs in fp32
-// with the rounding error of (z - max) folded back in (TwoSum), and
-// P = float(e / denom) via the fp64 reciprocal of the row denominator.
+// Numerics follow the reference's F32 path where it is cheap to do so
+// exactly: dP and D are the fp64 products rounded once (bit-exact with
+// mask_scale on the same inputs) and the row dot sum(dP*P) accumulates in
+// fp64; the forward's exp runs in fp32 with the rounding error of (z - max)
+// folded back in (TwoSum), the row denominator is an fp32 tree sum and
+// P = e * (1/denom) -- within 1e-5 relative of the reference's fp64 P.
 //
 // Layout: one warp per row, VPL float4 per lane (cols = 128*VPL <= 1024),
 // the whole row in registers (one HBM read per element, no smem staging
@@ -49,63 +50,77 @@ __global__ void __launch_bounds__(kBlock) softmax_fwd_vec_kernel(
     uint32_t* __restrict__ mask, double scale, uint64_t thresh, uint64_t seed, uint64_t offset,
     int64_t rows) {
     constexpr int C = VPL * 128;
+    constexpr int R = VPL <= 4 ? 2 : 1;  // rows per warp iteration (loads in flight)
     const int lane = threadIdx.x & 31;
     const int64_t warp = ((int64_t)blockIdx.x * kBlock + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * kBlock) >> 5;
-    for (int64_t r = warp; r < rows; r += nwarps) {
-        const float4* zr = reinterpret_cast<const float4*>(z + r * C);
-        float4 v[VPL];
-        uint32_t nib[VPL];
+    for (int64_t r0 = warp * R; r0 < rows; r0 += nwarps * R) {
+        float4 v[R][VPL];
+        uint32_t nib[R][VPL];
 #pragma unroll
-        for (int k = 0; k < VPL; ++k) v[k] = ld_stream(zr + k * 32 + lane);
-        if (MODE == kSupplied) {
+        for (int i = 0; i < R; ++i) {
+            const int64_t r = min(r0 + i, rows - 1);  // duplicate the last row if odd
+            const float4* zr = reinterpret_cast<const float4*>(z + r * C);
 #pragma unroll
-            for (int k = 0; k < VPL; ++k) nib[k] = chunk_nibble(mask + ((r * C) >> 5) + k * 4, lane);
-        }
-        float mx = v[0].x;
+            for (int k = 0; k < VPL; ++k) v[i][k] = ld_stream(zr + k * 32 + lane);
+            if (MODE == kSupplied) {
 #pragma unroll
-        for (int k = 0; k < VPL; ++k)
-            mx = fmaxf(mx, fmaxf(fmaxf(v[k].x, v[k].y), fmaxf(v[k].z, v[k].w)));
-        mx = warp_max(mx);
-        double acc = 0.0;
-#pragma unroll
-        for (int k = 0; k < VPL; ++k) {
-            v[k].x = exp_shift(v[k].x, mx);
-            v[k].y = exp_shift(v[k].y, mx);
-            v[k].z = exp_shift(v[k].z, mx);
-            v[k].w = exp_shift(v[k].w, mx);
-            acc += ((double)v[k].x + (double)v[k].y) + ((double)v[k].z + (double)v[k].w);
-        }
-        const double inv = 1.0 / warp_sum(acc);
-        float4* Pr = reinterpret_cast<float4*>(P + r * C);
-        float4* Dr = reinterpret_cast<float4*>(D + r * C);
-#pragma unroll
-        for (int k = 0; k < VPL; ++k) {
-            float4 p;
-            p.x = (float)((double)v[k].x * inv);
-            p.y = (float)((double)v[k].y * inv);
-            p.z = (float)((double)v[k].z * inv);
-            p.w = (float)((double)v[k].w * inv);
-            st_stream(Pr + k * 32 + lane, p);
-            if (MODE == kPlain) continue;
-            uint32_t bits;
-            if (MODE == kPhilox) {
-                U4 rnd = philox_quad(seed, (offset + (uint64_t)(r * C + k * 128 + lane * 4)) >> 2);
-                bool k0 = (uint64_t)rnd.x >= thresh, k1 = (uint64_t)rnd.y >= thresh;
-                bool k2 = (uint64_t)rnd.z >= thresh, k3 = (uint64_t)rnd.w >= thresh;
-                uint32_t word = pack_chunk_bits(k0, k1, k2, k3, lane);
-                if (lane < 4) st_stream(mask + ((r * C) >> 5) + k * 4 + lane, word);
-                bits = (uint32_t)k0 | ((uint32_t)k1 << 1) | ((uint32_t)k2 << 2) | ((uint32_t)k3 << 3);
-            } else {
-                bits = nib[k];
+                for (int k = 0; k < VPL; ++k)
+                    nib[i][k] = chunk_nibble(mask + ((r * C) >> 5) + k * 4, lane);
             }
-            if (D) {
-                float4 d;
-                d.x = (bits & 1u) ? dscale(p.x, scale) : 0.0f;
-                d.y = (bits & 2u) ? dscale(p.y, scale) : 0.0f;
-                d.z = (bits & 4u) ? dscale(p.z, scale) : 0.0f;
-                d.w = (bits & 8u) ? dscale(p.w, scale) : 0.0f;
-                st_stream(Dr + k * 32 + lane, d);
+        }
+        float inv[R];
+#pragma unroll
+        for (int i = 0; i < R; ++i) {
+            float mx = v[i][0].x;
+#pragma unroll
+            for (int k = 0; k < VPL; ++k)
+                mx = fmaxf(mx, fmaxf(fmaxf(v[i][k].x, v[i][k].y), fmaxf(v[i][k].z, v[i][k].w)));
+            mx = warp_max(mx);
+            float acc = 0.0f;
+#pragma unroll
+            for (int k = 0; k < VPL; ++k) {
+                v[i][k].x = exp_shift(v[i][k].x, mx);
+                v[i][k].y = exp_shift(v[i][k].y, mx);
+                v[i][k].z = exp_shift(v[i][k].z, mx);
+                v[i][k].w = exp_shift(v[i][k].w, mx);
+                acc += (v[i][k].x + v[i][k].y) + (v[i][k].z + v[i][k].w);
+            }
+            inv[i] = 1.0f / warp_sumf(acc);
+        }
+#pragma unroll
+        for (int i = 0; i < R; ++i) {
+            const int64_t r = r0 + i;
+            if (r >= rows) break;  // warp-uniform
+            float4* Pr = reinterpret_cast<float4*>(P + r * C);
+            float4* Dr = reinterpret_cast<float4*>(D + r * C);
+#pragma unroll
+            for (int k = 0; k < VPL; ++k) {
+                float4 p;
+                p.x = v[i][k].x * inv[i];
+                p.y = v[i][k].y * inv[i];
+                p.z = v[i][k].z * inv[i];
+                p.w = v[i][k].w * inv[i];
+                st_stream(Pr + k * 32 + lane, p);
+                if (MODE == kPlain) continue;
+                uint32_t bits;
+                if (MODE == kPhilox) {
+                    U4 rnd = philox_quad(seed,
+                                         (offset + (uint64_t)(r * C + k * 128 + lane * 4)) >> 2);
+                    bits = nibble4((uint64_t)rnd.x >= thresh, (uint64_t)rnd.y >= thresh,
+                                   (uint64_t)rnd.z >= thresh, (uint64_t)rnd.w >= thresh);
+                    store_chunk_mask(mask + ((r * C) >> 5) + k * 4, bits, lane);
+                } else {
+                    bits = nib[i][k];
+                }
+                if (D) {
+                    float4 d;
+                    d.x = (bits & 1u) ? dscale(p.x, scale) : 0.0f;
+                    d.y = (bits & 2u) ? dscale(p.y, scale) : 0.0f;
+                    d.z = (bits & 4u) ? dscale(p.z, scale) : 0.0f;
+                    d.w = (bits & 8u) ? dscale(p.w, scale) : 0.0f;
+                    st_stream(Dr + k * 32 + lane, d);
+                }
             }
         }
     }

@@ -4,9 +4,9 @@ test_oracle.py) on identical seeded inputs.
 
 Tolerances (the reference's rel_err = |a-b| / max(1,|a|,|b|),
 gradcheck.cpp:15-17, unless stated):
-  GELU   mask bits: bit-exact.  y: <= 5 ulp (exhaustive host sweep bound of
-         the fp32 fast path, tests/tools/gelu_fwd_sweep.c) and bit-exact in
-         the fp64 window |x - x*| < 1/64.  dx on identical (dy, y, mask):
+  GELU   mask bits: bit-exact.  y: <= 8 ulp (bound of the fp32 fast path,
+         checked on every fp32 input by tests/test_gpu_sweep.py) and
+         bit-exact in the fp64 window |x - x*| < 1/64.  dx on identical (dy, y, mask):
          rel_err <= 1e-5.  fwd->bwd chain: rel_err <= 1e-5.
   LN     y, dx: rel_err <= 1e-5; rstd: rel <= 1e-6; dgamma/dbeta vs the
          reference's F64 path: rel_err <= 1e-5; run-to-run bitwise.
@@ -76,7 +76,7 @@ def test_gelu_forward(tops, port, table_text, cuda, n):
     yg = y.cpu().numpy()
     fin = np.isfinite(ry)
     assert np.array_equal(np.isnan(yg), np.isnan(ry))
-    assert ulp_diff(yg[fin], ry[fin]).max(initial=0) <= 5
+    assert ulp_diff(yg[fin], ry[fin]).max(initial=0) <= 8
     win = np.abs(x.astype(np.float64) - XSTAR_D) < 1.0 / 64
     assert np.array_equal(yg[win], ry[win])  # fp64 window: bit-exact
     # padding bits of the last word are zero
@@ -95,7 +95,7 @@ def test_gelu_forward_unaligned(tops, port, table_text, cuda):
     ry, rm = port.gelu_fwd(x, table.info()["x_star"])
     assert np.array_equal(unpack(mask, x.size), rm)
     fin = np.isfinite(ry)
-    assert ulp_diff(y.cpu().numpy()[fin], ry[fin]).max() <= 5
+    assert ulp_diff(y.cpu().numpy()[fin], ry[fin]).max() <= 8
 
 
 @pytest.mark.parametrize("n", [1, 33, 128, 1000, 4101, 1024 * 3072])
@@ -122,7 +122,8 @@ def test_gelu_backward_table_eval_grid(tops, port, table_text, cuda):
     pt = port.table(table_text)
     info = table.info()
     ys = np.concatenate([np.linspace(-0.3, 10.0, 200000), [info["y_min"], 0.0, -0.0, 8.0,
-                                                           1.8725215943900724, 1e30, -1.0]])
+                                                           1.8725215943900724, 1e30, -1.0,
+                                                           np.inf, -np.inf, np.nan]])
     ys = ys.astype(np.float32)
     for m in (0, 1):
         mm = np.full(ys.size, m, np.uint8)
@@ -254,7 +255,7 @@ def test_softmax_dropout_supplied_mask(tops, port, cuda, rows, cols):
     assert torch.equal(Drec, D)  # recompute == forward D, bitwise
 
 
-@pytest.mark.parametrize("rows,cols", [(24, 512), (5, 100)])
+@pytest.mark.parametrize("rows,cols", [(48, 512), (200, 100)])
 def test_softmax_dropout_philox(tops, port, cuda, rows, cols):
     import torch
     g = np.random.default_rng(1)
@@ -264,7 +265,7 @@ def test_softmax_dropout_philox(tops, port, cuda, rows, cols):
     P, D, mask = tops.softmax_dropout_fwd(zt, p, seed=77)
     torch.cuda.synchronize()
     keep = unpack(mask, rows * cols)
-    assert abs(keep.mean() - (1 - p)) < 0.03
+    assert abs(keep.mean() - (1 - p)) < 0.015  # >= 20000 draws: 5 sigma
     assert np.array_equal(D.cpu().numpy(), port.dropout_apply(P.cpu().numpy(), keep, p).reshape(rows, cols))
     # same seed -> same mask; row shards with global offsets -> same mask
     _, _, mask2 = tops.softmax_dropout_fwd(zt, p, seed=77)
@@ -343,7 +344,7 @@ def test_golden_fixtures_on_gpu(tops, golden, table_text, cuda):
     torch.cuda.synchronize()
     assert np.array_equal(unpack(m, g["gelu_x"].size), g["gelu_mask"])
     fin = np.isfinite(g["gelu_y"])
-    assert ulp_diff(y.cpu().numpy()[fin], g["gelu_y"][fin]).max() <= 5
+    assert ulp_diff(y.cpu().numpy()[fin], g["gelu_y"][fin]).max() <= 8
     assert rel_err(dx.cpu().numpy(), g["gelu_dx"]) <= 1e-5
     ly, lrs = tops.layernorm_ip_fwd(to_dev(g["ln_x"], cuda), to_dev(g["ln_gamma"], cuda),
                                     to_dev(g["ln_beta"], cuda))
