@@ -158,10 +158,34 @@ void validate_tiling(const tempo_gelu_table_s& t) {  // gelu_table.cpp:106-148
     chain(t.seg[1], 1, t.y_min, std::numeric_limits<double>::infinity());
 }
 
+// Chebyshev series on [-1, 1] -> power-basis coefficients (fp64).
+std::vector<double> cheb_to_mono(const std::vector<double>& c) {
+    const std::size_t n = c.size();
+    std::vector<double> out(n, 0.0), tkm1(n, 0.0), tk(n, 0.0);
+    tkm1[0] = 1.0;  // T_0
+    if (n > 1) tk[1] = 1.0;  // T_1
+    for (std::size_t k = 0; k < n; ++k) {
+        const std::vector<double>& T = k == 0 ? tkm1 : tk;
+        for (std::size_t j = 0; j < n; ++j) out[j] += c[k] * T[j];
+        if (k >= 1 && k + 1 < n) {  // T_{k+1} = 2t T_k - T_{k-1}
+            std::vector<double> nx(n, 0.0);
+            for (std::size_t j = 0; j + 1 < n; ++j) nx[j + 1] += 2.0 * tk[j];
+            for (std::size_t j = 0; j < n; ++j) nx[j] -= tkm1[j];
+            tkm1 = tk;
+            tk = nx;
+        }
+    }
+    return out;
+}
+
 void build_device(tempo_gelu_table_s& t) {
     tb::GeluDevTable& d = t.dev;
     std::memset(&d, 0, sizeof(d));
-    const int n0 = (int)t.seg[0].size(), n1 = (int)t.seg[1].size();
+    // The device table appends one segment to branch 0: [0, +inf) with the
+    // constant 0, which is eval's "m = 0 and y >= 0 -> 0" rule
+    // (gelu_table.cpp:182) expressed as a segment, so the kernel needs no
+    // special case.
+    const int n0 = (int)t.seg[0].size() + 1, n1 = (int)t.seg[1].size();
     int ncoef = 1;
     for (int b = 0; b < 2; ++b)
         for (const Segment& s : t.seg[b]) ncoef = std::max(ncoef, (int)s.coeffs.size());
@@ -175,9 +199,22 @@ void build_device(tempo_gelu_table_s& t) {
     d.nseg[1] = n1;
     d.ncoef = ncoef;
     d.stride = ncoef | 1;
+    // Horner in the power basis when its error bound (coefficient rounding +
+    // Horner's (2d)eps sum|a_k|, t in [-1, 1]) stays below 4e-6; the default
+    // fit's bound is 1.7e-6 (measured 1.2e-7), else Clenshaw as the reference.
+    bool horner = ncoef <= 16;
+    Segment zero;
+    zero.branch = 0;
+    zero.lo = 0.0;
+    zero.hi = std::numeric_limits<double>::infinity();
+    zero.coeffs = {0.0};
     int k = 0;
     for (int b = 0; b < 2; ++b) {
-        for (const Segment& s : t.seg[b]) {
+        std::vector<const Segment*> segs;
+        for (const Segment& s : t.seg[b]) segs.push_back(&s);
+        if (b == 0) segs.push_back(&zero);
+        for (const Segment* sp : segs) {
+            const Segment& s = *sp;
             d.lo_up[k] = float_up(s.lo);
             d.sqrt_shift[k] = s.sqrt_shift ? 1 : 0;
             if (s.coeffs.size() == 1) {
@@ -198,9 +235,19 @@ void build_device(tempo_gelu_table_s& t) {
                 if (d.s[k] == 0.0f) d.s[k] = std::numeric_limits<float>::min();
             }
             for (std::size_t c = 0; c < s.coeffs.size(); ++c) d.coef[k][c] = (float)s.coeffs[c];
+            if (s.coeffs.size() <= 16) {
+                std::vector<double> a = cheb_to_mono(s.coeffs);
+                double suma = 0.0;
+                for (std::size_t c = 0; c < a.size(); ++c) {
+                    d.mono[k][c] = (float)a[c];
+                    suma += std::abs(a[c]);
+                }
+                if (suma * (2.0 * (double)a.size() + 2.0) * 0x1p-24 > 4e-6) horner = false;
+            }
             ++k;
         }
     }
+    d.horner = horner ? 1 : 0;
 }
 
 tempo_gelu_table_s* parse_table(const std::string& text) {  // gelu_table.cpp:227-301

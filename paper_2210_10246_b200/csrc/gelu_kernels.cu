@@ -272,22 +272,37 @@ __device__ __forceinline__ float sqrt_approx(float v) {
     asm("sqrt.approx.f32 %0, %1;" : "=f"(r) : "f"(v));
     return r;
 }
+// NaN-propagating min/max (PTX min/max.NaN): a NaN output y flows through
+// to dx exactly as in the reference's double evaluation.
+__device__ __forceinline__ float max_nan(float a, float b) {
+    float r;
+    asm("max.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
+    return r;
+}
+__device__ __forceinline__ float min_nan(float a, float b) {
+    float r;
+    asm("min.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
+    return r;
+}
 
-template <int NC4>
+// h(y, m) without data-dependent branches.  The clamp y < y_min -> y_min
+// (:183,:186) falls out of the variable maps (sqrt(max(y - y_min, 0)) = 0,
+// or t <= -1 clamped); m = 0, y >= 0 -> 0 (:182) is the device table's extra
+// constant-0 segment [0, inf) on branch 0; y = +inf is clamped to FLT_MAX so
+// constant segments see u*0 = 0.
+template <int NC4, bool HORNER>
 __device__ __forceinline__ float gelu_h_fast(float y, uint32_t m, const FastTable<NC4>& ft,
                                              const float (&thr0)[3], const float (&thr1)[3],
-                                             int base1, uint32_t sqrt_mask, float ymin_up,
-                                             float ymin_hi, float ymin_lo) {
+                                             int base1, uint32_t sqrt_mask, float ymin_hi,
+                                             float ymin_lo) {
+    y = min_nan(y, 3.402823466e38f);
     int seg = m ? base1 : 0;
 #pragma unroll
     for (int k = 0; k < 3; ++k) seg += (y >= (m ? thr1[k] : thr0[k])) ? 1 : 0;
     const float2 sb = ft.sb[seg];
     const float d = (y - ymin_hi) - ymin_lo;
-    const float u = ((sqrt_mask >> seg) & 1u) ? sqrt_approx(fmaxf(d, 0.0f)) : y;
-    float tt = fminf(fmaxf(fmaf(u, sb.x, sb.y), -1.0f), 1.0f);
-    tt = (y < ymin_up) ? -1.0f : tt;  // clamped to y_min: u == u_lo
-    tt = (sb.x == 0.0f) ? 0.0f : tt;  // constant segment
-    const float t2 = tt + tt;
+    const float u = ((sqrt_mask >> seg) & 1u) ? sqrt_approx(max_nan(d, 0.0f)) : y;
+    const float tt = max_nan(min_nan(fmaf(u, sb.x, sb.y), 1.0f), -1.0f);
     const float4* rec = ft.rec + seg * FastTable<NC4>::kStride4;
     float c[4 * NC4];
 #pragma unroll
@@ -298,6 +313,13 @@ __device__ __forceinline__ float gelu_h_fast(float y, uint32_t m, const FastTabl
         c[4 * j + 2] = q.z;
         c[4 * j + 3] = q.w;
     }
+    if (HORNER) {  // power basis, host-converted (error bound checked, capi.cpp)
+        float h = c[4 * NC4 - 1];
+#pragma unroll
+        for (int k = 4 * NC4 - 2; k >= 0; --k) h = fmaf(h, tt, c[k]);
+        return h;
+    }
+    const float t2 = tt + tt;  // Clenshaw (gelu_table.cpp:43-51)
     float b1 = 0.0f, b2 = 0.0f;
 #pragma unroll
     for (int k = 4 * NC4 - 1; k >= 1; --k) {
@@ -305,12 +327,10 @@ __device__ __forceinline__ float gelu_h_fast(float y, uint32_t m, const FastTabl
         b2 = b1;
         b1 = bk;
     }
-    float h = fmaf(tt, b1, c[0] - b2);
-    h = (m == 0u && y >= 0.0f) ? 0.0f : h;  // far left tail (:182)
-    return isnan(y) ? y : h;
+    return fmaf(tt, b1, c[0] - b2);
 }
 
-template <int NC4>
+template <int NC4, bool HORNER>
 __global__ void __launch_bounds__(kBlock) gelu_bwd_fast_kernel(
     const float* __restrict__ dy, const float* __restrict__ y, const uint32_t* __restrict__ mask,
     float* __restrict__ dx, int64_t n, const __grid_constant__ GeluDevTable t) {
@@ -321,10 +341,11 @@ __global__ void __launch_bounds__(kBlock) gelu_bwd_fast_kernel(
         float4 q = make_float4(0.f, 0.f, 0.f, 0.f);
         if (j < NC4) {
             const int k = 4 * j;
-            q.x = k < t.ncoef ? t.coef[sgi][k] : 0.f;
-            q.y = k + 1 < t.ncoef ? t.coef[sgi][k + 1] : 0.f;
-            q.z = k + 2 < t.ncoef ? t.coef[sgi][k + 2] : 0.f;
-            q.w = k + 3 < t.ncoef ? t.coef[sgi][k + 3] : 0.f;
+            const float* src = HORNER ? t.mono[sgi] : t.coef[sgi];
+            q.x = k < t.ncoef ? src[k] : 0.f;
+            q.y = k + 1 < t.ncoef ? src[k + 1] : 0.f;
+            q.z = k + 2 < t.ncoef ? src[k + 2] : 0.f;
+            q.w = k + 3 < t.ncoef ? src[k + 3] : 0.f;
         }
         ft.rec[i] = q;
     }
@@ -338,7 +359,7 @@ __global__ void __launch_bounds__(kBlock) gelu_bwd_fast_kernel(
     }
     for (int i = 0; i < nseg; ++i) sqrt_mask |= (t.sqrt_shift[i] ? 1u : 0u) << i;
     const int base1 = t.nseg[0];
-    const float ymin_up = t.ymin_up, ymin_hi = t.ymin_hi, ymin_lo = t.ymin_lo;
+    const float ymin_hi = t.ymin_hi, ymin_lo = t.ymin_lo;
     __syncthreads();
 
     const int lane = threadIdx.x & 31;
@@ -362,8 +383,8 @@ __global__ void __launch_bounds__(kBlock) gelu_bwd_fast_kernel(
         }
 #pragma unroll
         for (int u = 0; u < UU; ++u) {
-#define TB_H(val, bit) gelu_h_fast<NC4>(val, (nib[u] >> bit) & 1u, ft, thr0, thr1, base1, \
-                                        sqrt_mask, ymin_up, ymin_hi, ymin_lo)
+#define TB_H(val, bit) gelu_h_fast<NC4, HORNER>(val, (nib[u] >> bit) & 1u, ft, thr0, thr1, \
+                                                base1, sqrt_mask, ymin_hi, ymin_lo)
             float4 o;
             o.x = g[u].x * TB_H(v[u].x, 0);
             o.y = g[u].y * TB_H(v[u].y, 1);
@@ -381,8 +402,8 @@ __global__ void __launch_bounds__(kBlock) gelu_bwd_fast_kernel(
     if (warp == nwarps - 1) {
         for (int64_t i = (nchunks << 7) + lane; i < n; i += 32) {
             const uint32_t m = (mask[i >> 5] >> (i & 31)) & 1u;
-            dx[i] = dy[i] * gelu_h_fast<NC4>(y[i], m, ft, thr0, thr1, base1, sqrt_mask, ymin_up,
-                                             ymin_hi, ymin_lo);
+            dx[i] = dy[i] * gelu_h_fast<NC4, HORNER>(y[i], m, ft, thr0, thr1, base1, sqrt_mask,
+                                                     ymin_hi, ymin_lo);
         }
     }
 }
@@ -417,7 +438,7 @@ cudaError_t launch_gelu_bwd(const float* dy, const float* y, const uint32_t* mas
         const int64_t blocks = ((n >> 7) / 2 + 1) * 32 / kBlock + 1;
 #define TB_CASE(NC)                                                                       \
     case NC: {                                                                            \
-        auto k = gelu_bwd_fast_kernel<NC>;                                                \
+        auto k = t.horner ? gelu_bwd_fast_kernel<NC, true> : gelu_bwd_fast_kernel<NC, false>; \
         int grid = grid_for((const void*)k, kBlock, 0, blocks);                           \
         k<<<grid, kBlock, 0, st>>>(dy, y, mask, dx, n, t);                                \
         break;                                                                            \

@@ -9,12 +9,13 @@
 //   Q(a) = Phi(-a) = exp(-a^2/2) * P(t) / (a + K),   t = (a - K) / (a + K)
 //
 // where P ~ (a + K) Q(a) e^{a^2/2} is smooth (1.25 .. 0.40 on [0, 13]) and
-// is a degree-10 polynomial in t fitted offline (fp32 coefficients, least
-// squares in relative error, K = 2.5; tests/tools/fit_gelu_q.py).  a^2 is
-// split exactly (h + l) with an FMA so the exponential does not amplify the
-// rounding of a^2; exp uses a Cody-Waite reduction and a degree-7 Taylor
-// kernel; one rcp.approx + Newton step serves both the variable map and the
-// 1/(a+K) factor.  x >= 0 uses y = x - x*Q(x) (one rounding).
+// is a degree-9 polynomial in t fitted offline (fp32 coefficients, least
+// squares in relative error 3.9e-8, K = 2.5; tests/tools/fit_gelu_q.py).
+// a^2 is split exactly (h + l) with an FMA and the exponent -a^2/2*log2(e)
+// is carried in two floats, so the exponential does not amplify the
+// rounding of a^2; 2^frac runs on the SFU; one rcp.approx + Newton step
+// serves both the variable map and the 1/(a+K) factor.  x >= 0 uses
+// y = x - x*Q(x) (one rounding).
 //
 // Accuracy against the reference's double formula, over EVERY fp32 input
 // (tests/tools/gelu_sweep.cu, run by tests/test_gpu_sweep.py): see DESIGN.md.
@@ -33,41 +34,44 @@ __device__ __forceinline__ float tm_rcp(float d) {  // ~0.5 ulp for d in [2.5, 1
 }
 
 // Q(a) = Phi(-a), a in [0, 13].
+//   exp(-a^2/2): w = -a^2/2 * log2(e) carried as w_hi + w_lo (two FMAs on the
+//   exact split h + l of a^2), n = rint(w_hi), 2^(w_hi - n) on the SFU
+//   (ex2.approx, |arg| <= 1/2), the low part folded back as (1 + w_lo ln2),
+//   and 2^n applied to the exponent bits.
+__device__ __forceinline__ float tm_ex2_approx(float f) {
+    float r;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(f));
+    return r;
+}
+
 __device__ __forceinline__ float tm_gelu_q(float a) {
     const float K = 2.5f;
-    const float ln2_hi = 0.693145751953125f;      // 0x3f317200: n*ln2_hi exact
-    const float ln2_lo = 1.428606765330187e-06f;  // 0x35bfbe8e
+    const float C_HI = -0.72134752044448170f;        // -log2(e)/2, fp32
+    const float C_LO = -9.62981494545545e-09f;       // -log2(e)/2 - C_HI
+    const float LN2 = 0.69314718055994531f;
     const float h = a * a;
-    const float l = fmaf(a, a, -h);  // a^2 = h + l exactly
-    const float v = -0.5f * h;
-    // n = rint(v * log2e) via the 1.5*2^23 shifter (no F2I/FRND)
-    const float sh = fmaf(v, 1.44269504088896341f, 12582912.0f);
+    const float l = fmaf(a, a, -h);                  // a^2 = h + l exactly
+    const float w_hi = h * C_HI;
+    float w_lo = fmaf(h, C_HI, -w_hi);               // exact rounding error of w_hi
+    w_lo = fmaf(h, C_LO, w_lo);
+    w_lo = fmaf(l, C_HI, w_lo);                      // the l part of -a^2/2 log2(e)
+    const float sh = w_hi + 12582912.0f;             // 1.5*2^23 shifter: rint(w_hi)
     const float n = sh - 12582912.0f;
     const int ni = __float_as_int(sh) - 0x4B400000;
-    float r = fmaf(n, -ln2_hi, v);
-    r = fmaf(n, -ln2_lo, r);
-    float p = 1.98412698e-04f;          // 1/5040
-    p = fmaf(p, r, 1.38888889e-03f);    // 1/720
-    p = fmaf(p, r, 8.33333377e-03f);    // 1/120
-    p = fmaf(p, r, 4.16666679e-02f);    // 1/24
-    p = fmaf(p, r, 1.66666672e-01f);    // 1/6
-    p = fmaf(p, r, 0.5f);
-    p = fmaf(p, r, 1.0f);
-    p = fmaf(p, r, 1.0f);
-    const float e = p * __int_as_float((ni + 127) << 23);  // n >= -122 here
-    const float E = fmaf(e, -0.5f * l, e);                 // * exp(-l/2)
+    const float e2 = tm_ex2_approx(w_hi - n);        // w_hi - n exact, |.| <= 1/2
+    const float e = fmaf(e2, w_lo * LN2, e2);        // * 2^w_lo ~ 1 + w_lo ln2
+    const float E = __int_as_float(__float_as_int(e) + (ni << 23));  // * 2^n, n >= -122
     const float rc = tm_rcp(a + K);
     const float t = (a - K) * rc;
-    float q = -2.982836304e-05f;
-    q = fmaf(q, t, -2.068497561e-04f);
-    q = fmaf(q, t, -2.954241645e-04f);
-    q = fmaf(q, t, 7.393874694e-04f);
-    q = fmaf(q, t, 2.528889570e-03f);
-    q = fmaf(q, t, -1.621615840e-03f);
-    q = fmaf(q, t, -1.639027148e-02f);
-    q = fmaf(q, t, 9.238829836e-03f);
+    float q = -1.643887081e-04f;
+    q = fmaf(q, t, -3.207997943e-04f);
+    q = fmaf(q, t, 6.907590432e-04f);
+    q = fmaf(q, t, 2.534991596e-03f);
+    q = fmaf(q, t, -1.602514880e-03f);
+    q = fmaf(q, t, -1.639061980e-02f);
+    q = fmaf(q, t, 9.235967882e-03f);
     q = fmaf(q, t, 1.319876313e-01f);
-    q = fmaf(q, t, -4.336921275e-01f);
+    q = fmaf(q, t, -4.336920083e-01f);
     q = fmaf(q, t, 7.066566348e-01f);
     return (E * q) * rc;
 }

@@ -30,6 +30,11 @@ struct GeluDevTable {
     float b[kMaxSeg];
     int sqrt_shift[kMaxSeg];
     float coef[kMaxSeg][kMaxCoef];  // Chebyshev coefficients, zero padded
+    // Specialized kernel only: the same polynomials in the power basis of t
+    // (host fp64 conversion), used with Horner's rule when `horner` is set
+    // (the conversion's error bound is small enough, see capi.cpp).
+    int horner;
+    float mono[kMaxSeg][16];
 };
 
 // Kernel launchers (defined in the .cu files; return cudaGetLastError()).

@@ -298,8 +298,8 @@ def test_softmax_frozen_row(tops, cuda):
     P = tops.softmax_ip_fwd(z)
     dZ = tops.softmax_ip_bwd(torch.tensor([[1.0, 0.0]], device=cuda), P)
     torch.cuda.synchronize()
-    assert P.cpu().numpy() == pytest.approx([[0.25, 0.75]], rel=1e-6)
-    assert dZ.cpu().numpy() == pytest.approx([[0.1875, -0.1875]], rel=1e-5)
+    assert P.cpu().numpy().ravel().tolist() == pytest.approx([0.25, 0.75], rel=1e-6)
+    assert dZ.cpu().numpy().ravel().tolist() == pytest.approx([0.1875, -0.1875], rel=1e-5)
 
 
 # ---------------------------------------------------------------- dropout
