@@ -52,23 +52,24 @@ __device__ __forceinline__ void gelu_fwd_chunks(const float4* __restrict__ x4,
     float4 v[U], o[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) v[u] = ld_stream(x4 + ((c0 + u) << 5) + lane);
-    bool slow = false;
+    uint32_t slow = 0;  // bit 4u+k: element k of chunk u needs an fp64 path
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-        o[u].x = tm_gelu_fast(v[u].x);
-        o[u].y = tm_gelu_fast(v[u].y);
-        o[u].z = tm_gelu_fast(v[u].z);
-        o[u].w = tm_gelu_fast(v[u].w);
-        slow |= tm_gelu_needs_slow(v[u].x) | tm_gelu_needs_slow(v[u].y) |
-                tm_gelu_needs_slow(v[u].z) | tm_gelu_needs_slow(v[u].w);
+        const float2 lo = tm_gelu_fast2(make_float2(v[u].x, v[u].y));
+        const float2 hi = tm_gelu_fast2(make_float2(v[u].z, v[u].w));
+        o[u] = make_float4(lo.x, lo.y, hi.x, hi.y);
+        slow |= (uint32_t)tm_gelu_needs_slow(v[u].x) << (4 * u);
+        slow |= (uint32_t)tm_gelu_needs_slow(v[u].y) << (4 * u + 1);
+        slow |= (uint32_t)tm_gelu_needs_slow(v[u].z) << (4 * u + 2);
+        slow |= (uint32_t)tm_gelu_needs_slow(v[u].w) << (4 * u + 3);
     }
-    if (__any_sync(kFull, slow)) {  // rare: the fp64 window / tail
+    if (__any_sync(kFull, slow != 0u)) {  // rare per element: the fp64 window / tail
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            if (tm_gelu_needs_slow(v[u].x)) o[u].x = tm_gelu_slow(v[u].x);
-            if (tm_gelu_needs_slow(v[u].y)) o[u].y = tm_gelu_slow(v[u].y);
-            if (tm_gelu_needs_slow(v[u].z)) o[u].z = tm_gelu_slow(v[u].z);
-            if (tm_gelu_needs_slow(v[u].w)) o[u].w = tm_gelu_slow(v[u].w);
+            if (slow & (1u << (4 * u))) o[u].x = tm_gelu_slow(v[u].x);
+            if (slow & (1u << (4 * u + 1))) o[u].y = tm_gelu_slow(v[u].y);
+            if (slow & (1u << (4 * u + 2))) o[u].z = tm_gelu_slow(v[u].z);
+            if (slow & (1u << (4 * u + 3))) o[u].w = tm_gelu_slow(v[u].w);
         }
     }
 #pragma unroll
@@ -369,7 +370,7 @@ __global__ void __launch_bounds__(kBlock) gelu_bwd_fast_kernel(
     const float4* dy4 = reinterpret_cast<const float4*>(dy);
     const float4* y4 = reinterpret_cast<const float4*>(y);
     float4* dx4 = reinterpret_cast<float4*>(dx);
-    constexpr int U = 2;
+    constexpr int U = 4;
     auto body = [&](int64_t c0, auto uconst) {
         constexpr int UU = decltype(uconst)::value;
         float4 g[UU], v[UU];
@@ -435,7 +436,7 @@ cudaError_t launch_gelu_bwd(const float* dy, const float* y, const uint32_t* mas
                       t.ncoef <= 16;
     if (fast) {
         const int nc4 = (t.ncoef + 3) / 4;
-        const int64_t blocks = ((n >> 7) / 2 + 1) * 32 / kBlock + 1;
+        const int64_t blocks = ((n >> 7) / 4 + 1) * 32 / kBlock + 1;
 #define TB_CASE(NC)                                                                       \
     case NC: {                                                                            \
         auto k = t.horner ? gelu_bwd_fast_kernel<NC, true> : gelu_bwd_fast_kernel<NC, false>; \

@@ -82,3 +82,56 @@ __device__ __forceinline__ float tm_gelu_fast(float x) {
     const float q = tm_gelu_q(fminf(fabsf(x), 13.0f));
     return x < 0.0f ? x * q : fmaf(-x, q, x);
 }
+
+// ---- two elements per instruction: Blackwell's packed fp32x2 pipe ----------
+// The same arithmetic as tm_gelu_q / tm_gelu_fast, element for element (each
+// FFMA2 lane rounds exactly like the scalar FFMA), issued as FFMA2/FMUL2/
+// FADD2 so the forward's FMA-pipe instruction count halves.
+__device__ __forceinline__ float2 f2(float v) { return make_float2(v, v); }
+__device__ __forceinline__ float2 neg2(float2 v) { return make_float2(-v.x, -v.y); }
+
+__device__ __forceinline__ float2 tm_gelu_q2(float2 a) {
+    const float2 K = f2(2.5f), NK = f2(-2.5f);
+    const float2 C_HI = f2(-0.72134752044448170f);
+    const float2 C_LO = f2(-9.62981494545545e-09f);
+    const float2 LN2 = f2(0.69314718055994531f);
+    const float2 h = __fmul2_rn(a, a);
+    const float2 l = __ffma2_rn(a, a, neg2(h));
+    const float2 w_hi = __fmul2_rn(h, C_HI);
+    float2 w_lo = __ffma2_rn(h, C_HI, neg2(w_hi));
+    w_lo = __ffma2_rn(h, C_LO, w_lo);
+    w_lo = __ffma2_rn(l, C_HI, w_lo);
+    const float2 sh = __fadd2_rn(w_hi, f2(12582912.0f));
+    const float2 n = __fadd2_rn(sh, f2(-12582912.0f));
+    const float2 fr = __fadd2_rn(w_hi, neg2(n));
+    const float2 e2 = make_float2(tm_ex2_approx(fr.x), tm_ex2_approx(fr.y));
+    const float2 e = __ffma2_rn(e2, __fmul2_rn(w_lo, LN2), e2);
+    const float2 E = make_float2(
+        __int_as_float(__float_as_int(e.x) + ((__float_as_int(sh.x) - 0x4B400000) << 23)),
+        __int_as_float(__float_as_int(e.y) + ((__float_as_int(sh.y) - 0x4B400000) << 23)));
+    const float2 d = __fadd2_rn(a, K);
+    float2 r0;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r0.x) : "f"(d.x));
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r0.y) : "f"(d.y));
+    const float2 rc = __ffma2_rn(r0, __ffma2_rn(neg2(d), r0, f2(1.0f)), r0);
+    const float2 t = __fmul2_rn(__fadd2_rn(a, NK), rc);
+    float2 q = f2(-1.643887081e-04f);
+    q = __ffma2_rn(q, t, f2(-3.207997943e-04f));
+    q = __ffma2_rn(q, t, f2(6.907590432e-04f));
+    q = __ffma2_rn(q, t, f2(2.534991596e-03f));
+    q = __ffma2_rn(q, t, f2(-1.602514880e-03f));
+    q = __ffma2_rn(q, t, f2(-1.639061980e-02f));
+    q = __ffma2_rn(q, t, f2(9.235967882e-03f));
+    q = __ffma2_rn(q, t, f2(1.319876313e-01f));
+    q = __ffma2_rn(q, t, f2(-4.336920083e-01f));
+    q = __ffma2_rn(q, t, f2(7.066566348e-01f));
+    return __fmul2_rn(__fmul2_rn(E, q), rc);
+}
+
+__device__ __forceinline__ float2 tm_gelu_fast2(float2 x) {
+    const float2 a = make_float2(fminf(fabsf(x.x), 13.0f), fminf(fabsf(x.y), 13.0f));
+    const float2 q = tm_gelu_q2(a);
+    const float2 neg = __fmul2_rn(x, q);              // x < 0: x*Q
+    const float2 pos = __ffma2_rn(neg2(x), q, x);     // x >= 0: x - x*Q
+    return make_float2(x.x < 0.0f ? neg.x : pos.x, x.y < 0.0f ? neg.y : pos.y);
+}

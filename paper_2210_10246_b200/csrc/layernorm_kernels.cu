@@ -75,7 +75,7 @@ __device__ __forceinline__ float ln_y(float x, double mean_f, double rs, double 
 // the float4 at column 4t), so HBM reads stay in flight across the block
 // reductions.  A stage is refilled as soon as the tile's first block
 // reduction proves every thread has read it.
-constexpr int kStages = 4;
+constexpr int kStages = 3;
 
 __device__ __forceinline__ void ln_issue(const float* src, int64_t tile, int tile_rows,
                                          int64_t rows, int cols, float* dst, uint64_t* bar) {
@@ -86,7 +86,8 @@ __device__ __forceinline__ void ln_issue(const float* src, int64_t tile, int til
     bulk_g2s(dst, src + r0 * cols, bytes, bar);
 }
 
-__global__ void __launch_bounds__(kMaxThreads) ln_fwd_vec_kernel(
+template <int NT>
+__global__ void __launch_bounds__(NT, NT <= 256 ? 3 : 1) ln_fwd_vec_kernel(
     const float* __restrict__ x, const float* __restrict__ gamma, const float* __restrict__ beta,
     double eps, float* __restrict__ y, float* __restrict__ rstd, int64_t rows, int cols,
     int32_t* __restrict__ status) {
@@ -210,7 +211,8 @@ __global__ void __launch_bounds__(256) ln_fwd_generic_kernel(
 // Stage 1, vector path: dx per row, per-CTA fp64 column partials of
 // dgamma = sum g*xhat and dbeta = sum g, written to ws[cta][2][cols].
 // Same TMA ring as the forward; a stage holds kRowsB rows of dy and of y.
-__global__ void __launch_bounds__(kMaxThreads) ln_bwd_vec_kernel(
+template <int NT>
+__global__ void __launch_bounds__(NT, NT <= 256 ? 3 : 1) ln_bwd_vec_kernel(
     const float* __restrict__ dy, const float* __restrict__ y, const float* __restrict__ rstd,
     const float* __restrict__ gamma, const float* __restrict__ beta, float* __restrict__ dx,
     double* __restrict__ ws, int64_t rows, int cols) {
@@ -418,7 +420,9 @@ size_t bwd_smem(int64_t cols) { return 128 + (size_t)kStages * 2 * kRowsB * cols
 
 int bwd_grid(int64_t rows, int64_t cols, bool vec) {
     int64_t work = vec ? (rows + kRowsB - 1) / kRowsB : rows;
-    const void* k = vec ? (const void*)ln_bwd_vec_kernel : (const void*)ln_bwd_generic_kernel;
+    const void* k = !vec ? (const void*)ln_bwd_generic_kernel
+                    : vec_threads(cols) <= 256 ? (const void*)ln_bwd_vec_kernel<256>
+                                               : (const void*)ln_bwd_vec_kernel<kMaxThreads>;
     int block = vec ? vec_threads(cols) : 256;
     size_t smem = vec ? bwd_smem(cols) : (size_t)2 * cols * sizeof(double);
     return grid_for(k, block, smem, work);
@@ -433,9 +437,9 @@ cudaError_t launch_ln_fwd(const float* x, const float* gamma, const float* beta,
     if (use_vec(cols, x, y, gamma, beta, x)) {
         int block = vec_threads(cols);
         size_t smem = fwd_smem(cols);
-        int grid = grid_for((const void*)ln_fwd_vec_kernel, block, smem, (rows + kRows - 1) / kRows);
-        ln_fwd_vec_kernel<<<grid, block, smem, st>>>(x, gamma, beta, eps, y, rstd, rows,
-                                                      (int)cols, dev_status);
+        auto k = block <= 256 ? ln_fwd_vec_kernel<256> : ln_fwd_vec_kernel<kMaxThreads>;
+        int grid = grid_for((const void*)k, block, smem, (rows + kRows - 1) / kRows);
+        k<<<grid, block, smem, st>>>(x, gamma, beta, eps, y, rstd, rows, (int)cols, dev_status);
     } else {
         int grid = grid_for((const void*)ln_fwd_generic_kernel, 256, 0, rows);
         ln_fwd_generic_kernel<<<grid, 256, 0, st>>>(x, gamma, beta, eps, y, rstd, rows,
@@ -467,8 +471,9 @@ cudaError_t launch_ln_bwd(const float* dy, const float* y, const float* rstd, co
     const int grid = bwd_grid(rows, cols, vec);
     double* w = static_cast<double*>(ws);
     if (vec) {
-        ln_bwd_vec_kernel<<<grid, vec_threads(cols), bwd_smem(cols), st>>>(
-            dy, y, rstd, gamma, beta, dx, w, rows, (int)cols);
+        auto k = vec_threads(cols) <= 256 ? ln_bwd_vec_kernel<256> : ln_bwd_vec_kernel<kMaxThreads>;
+        k<<<grid, vec_threads(cols), bwd_smem(cols), st>>>(dy, y, rstd, gamma, beta, dx, w, rows,
+                                                           (int)cols);
     } else {
         size_t smem = (size_t)2 * cols * sizeof(double);
         ln_bwd_generic_kernel<<<grid, 256, smem, st>>>(dy, y, rstd, gamma, beta, dx, w, rows,
