@@ -54,35 +54,52 @@ __global__ void __launch_bounds__(kBlock) dropout_fwd_vec_kernel(
     const int64_t nchunks = n >> 7;
     const float4* x4 = reinterpret_cast<const float4*>(x);
     float4* y4 = reinterpret_cast<float4*>(y);
-    for (int64_t c0 = warp * kUnroll; c0 < nchunks; c0 += nwarps * kUnroll) {
+    struct Group {
         float4 v[kUnroll];
         uint32_t nib[kUnroll];
+    };
+    auto load = [&](Group& G, int64_t c0, int uu) {
 #pragma unroll
         for (int u = 0; u < kUnroll; ++u) {
-            if (c0 + u < nchunks) {
-                v[u] = ld_stream(x4 + ((c0 + u) << 5) + lane);
-                if (!PHILOX) nib[u] = chunk_nibble(mask + ((c0 + u) << 2), lane);
+            if (u < uu) {
+                G.v[u] = ld_stream(x4 + ((c0 + u) << 5) + lane);
+                if (!PHILOX) G.nib[u] = chunk_nibble(mask + ((c0 + u) << 2), lane);
             }
         }
+    };
+    auto compute = [&](Group& G, int64_t c0, int uu) {
 #pragma unroll
         for (int u = 0; u < kUnroll; ++u) {
-            if (c0 + u < nchunks) {
+            if (u < uu) {
                 if (PHILOX) {
                     const uint64_t e0 = ((uint64_t)(c0 + u) << 7) + (uint64_t)lane * 4;
                     U4 r = philox_quad(seed, (offset + e0) >> 2);
-                    bool k0 = (uint64_t)r.x >= thresh, k1 = (uint64_t)r.y >= thresh;
-                    bool k2 = (uint64_t)r.z >= thresh, k3 = (uint64_t)r.w >= thresh;
-                    nib[u] = nibble4(k0, k1, k2, k3);
-                    store_chunk_mask(mask + ((c0 + u) << 2), nib[u], lane);
+                    G.nib[u] = nibble4((uint64_t)r.x >= thresh, (uint64_t)r.y >= thresh,
+                                       (uint64_t)r.z >= thresh, (uint64_t)r.w >= thresh);
+                    store_chunk_mask(mask + ((c0 + u) << 2), G.nib[u], lane);
                 }
                 float4 o;
-                o.x = (nib[u] & 1u) ? dscale(v[u].x, scale) : 0.0f;
-                o.y = (nib[u] & 2u) ? dscale(v[u].y, scale) : 0.0f;
-                o.z = (nib[u] & 4u) ? dscale(v[u].z, scale) : 0.0f;
-                o.w = (nib[u] & 8u) ? dscale(v[u].w, scale) : 0.0f;
+                o.x = (G.nib[u] & 1u) ? dscale(G.v[u].x, scale) : 0.0f;
+                o.y = (G.nib[u] & 2u) ? dscale(G.v[u].y, scale) : 0.0f;
+                o.z = (G.nib[u] & 4u) ? dscale(G.v[u].z, scale) : 0.0f;
+                o.w = (G.nib[u] & 8u) ? dscale(G.v[u].w, scale) : 0.0f;
                 st_stream(y4 + ((c0 + u) << 5) + lane, o);
             }
         }
+    };
+    // whole groups, next group's loads in flight during this group's work
+    const int64_t ngroups = nchunks / kUnroll;
+    Group nxt;
+    if (warp < ngroups) load(nxt, warp * kUnroll, kUnroll);
+    for (int64_t gi = warp; gi < ngroups; gi += nwarps) {
+        Group cur = nxt;
+        if (gi + nwarps < ngroups) load(nxt, (gi + nwarps) * kUnroll, kUnroll);
+        compute(cur, gi * kUnroll, kUnroll);
+    }
+    for (int64_t c = ngroups * kUnroll + warp; c < nchunks; c += nwarps) {
+        Group one;
+        load(one, c, 1);
+        compute(one, c, 1);
     }
     if (warp == nwarps - 1)
         dropout_scalar_words<PHILOX>(x, mask, scale, thresh, seed, offset, y, n, nchunks << 2, 1,

@@ -43,15 +43,12 @@ __device__ __forceinline__ void gelu_fwd_scalar_words(const float* __restrict__ 
     }
 }
 
-// U chunks (U float4 per lane) in flight; fp64 fix-ups behind one vote.
+// Compute + store U chunks already loaded in v; fp64 fix-ups behind one vote.
 template <int U>
-__device__ __forceinline__ void gelu_fwd_chunks(const float4* __restrict__ x4,
-                                                float4* __restrict__ y4,
-                                                uint32_t* __restrict__ mask, int64_t c0,
-                                                float xstar_gt, int lane) {
-    float4 v[U], o[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) v[u] = ld_stream(x4 + ((c0 + u) << 5) + lane);
+__device__ __forceinline__ void gelu_fwd_compute(const float4 (&v)[U], float4* __restrict__ y4,
+                                                 uint32_t* __restrict__ mask, int64_t c0,
+                                                 float xstar_gt, int lane) {
+    float4 o[U];
     uint32_t slow = 0;  // bit 4u+k: element k of chunk u needs an fp64 path
 #pragma unroll
     for (int u = 0; u < U; ++u) {
@@ -92,13 +89,31 @@ __global__ void __launch_bounds__(kBlock) gelu_fwd_vec_kernel(const float* __res
     const int64_t nchunks = n >> 7;
     const float4* x4 = reinterpret_cast<const float4*>(x);
     float4* y4 = reinterpret_cast<float4*>(y);
-    // main loop: whole groups of kUnroll chunks (warp-uniform, no guards)
+    // main loop: whole groups of kUnroll chunks (warp-uniform, no guards),
+    // the next group's loads issued before this group's math (register
+    // double buffering keeps HBM reads in flight through the compute)
     const int64_t ngroups = nchunks / kUnroll;
-    for (int64_t gi = warp; gi < ngroups; gi += nwarps)
-        gelu_fwd_chunks<kUnroll>(x4, y4, mask, gi * kUnroll, xstar_gt, lane);
+    float4 nxt[kUnroll];
+    if (warp < ngroups) {
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) nxt[u] = ld_stream(x4 + ((warp * kUnroll + u) << 5) + lane);
+    }
+    for (int64_t gi = warp; gi < ngroups; gi += nwarps) {
+        float4 v[kUnroll];
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) v[u] = nxt[u];
+        const int64_t gn = gi + nwarps;
+        if (gn < ngroups) {
+#pragma unroll
+            for (int u = 0; u < kUnroll; ++u) nxt[u] = ld_stream(x4 + ((gn * kUnroll + u) << 5) + lane);
+        }
+        gelu_fwd_compute<kUnroll>(v, y4, mask, gi * kUnroll, xstar_gt, lane);
+    }
     // leftover whole chunks, one per warp
-    for (int64_t c = ngroups * kUnroll + warp; c < nchunks; c += nwarps)
-        gelu_fwd_chunks<1>(x4, y4, mask, c, xstar_gt, lane);
+    for (int64_t c = ngroups * kUnroll + warp; c < nchunks; c += nwarps) {
+        float4 v[1] = {ld_stream(x4 + (c << 5) + lane)};
+        gelu_fwd_compute<1>(v, y4, mask, c, xstar_gt, lane);
+    }
     // Ragged tail: words [4*nchunks, ceil(n/32)) on the last warp.
     if (warp == nwarps - 1) {
         gelu_fwd_scalar_words(x, y, mask, n, xstar_gt, nchunks << 2, 1, lane);
@@ -370,35 +385,53 @@ __global__ void __launch_bounds__(kBlock) gelu_bwd_fast_kernel(
     const float4* dy4 = reinterpret_cast<const float4*>(dy);
     const float4* y4 = reinterpret_cast<const float4*>(y);
     float4* dx4 = reinterpret_cast<float4*>(dx);
-    constexpr int U = 4;
-    auto body = [&](int64_t c0, auto uconst) {
-        constexpr int UU = decltype(uconst)::value;
-        float4 g[UU], v[UU];
-        uint32_t nib[UU];
+    constexpr int U = 2;
+    struct Group {
+        float4 g[U], v[U];
+        uint32_t nib[U];
+    };
+    auto load = [&](Group& G, int64_t c0, int uu) {
 #pragma unroll
-        for (int u = 0; u < UU; ++u) {
-            const int64_t off = ((c0 + u) << 5) + lane;
-            v[u] = ld_stream(y4 + off);
-            g[u] = ld_stream(dy4 + off);
-            nib[u] = chunk_nibble(mask + ((c0 + u) << 2), lane);
-        }
-#pragma unroll
-        for (int u = 0; u < UU; ++u) {
-#define TB_H(val, bit) gelu_h_fast<NC4, HORNER>(val, (nib[u] >> bit) & 1u, ft, thr0, thr1, \
-                                                base1, sqrt_mask, ymin_hi, ymin_lo)
-            float4 o;
-            o.x = g[u].x * TB_H(v[u].x, 0);
-            o.y = g[u].y * TB_H(v[u].y, 1);
-            o.z = g[u].z * TB_H(v[u].z, 2);
-            o.w = g[u].w * TB_H(v[u].w, 3);
-#undef TB_H
-            st_stream(dx4 + ((c0 + u) << 5) + lane, o);
+        for (int u = 0; u < U; ++u) {
+            if (u < uu) {
+                const int64_t off = ((c0 + u) << 5) + lane;
+                G.v[u] = ld_stream(y4 + off);
+                G.g[u] = ld_stream(dy4 + off);
+                G.nib[u] = chunk_nibble(mask + ((c0 + u) << 2), lane);
+            }
         }
     };
+    auto compute = [&](const Group& G, int64_t c0, int uu) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (u < uu) {
+#define TB_H(val, bit) gelu_h_fast<NC4, HORNER>(val, (G.nib[u] >> bit) & 1u, ft, thr0, thr1, \
+                                                base1, sqrt_mask, ymin_hi, ymin_lo)
+                float4 o;
+                o.x = G.g[u].x * TB_H(G.v[u].x, 0);
+                o.y = G.g[u].y * TB_H(G.v[u].y, 1);
+                o.z = G.g[u].z * TB_H(G.v[u].z, 2);
+                o.w = G.g[u].w * TB_H(G.v[u].w, 3);
+#undef TB_H
+                st_stream(dx4 + ((c0 + u) << 5) + lane, o);
+            }
+        }
+    };
+    // whole groups of U chunks with the next group's loads in flight during
+    // this group's math (register double buffering)
     const int64_t ngroups = nchunks / U;
-    for (int64_t gi = warp; gi < ngroups; gi += nwarps) body(gi * U, std::integral_constant<int, U>());
-    for (int64_t c = ngroups * U + warp; c < nchunks; c += nwarps)
-        body(c, std::integral_constant<int, 1>());
+    Group nxt;
+    if (warp < ngroups) load(nxt, warp * U, U);
+    for (int64_t gi = warp; gi < ngroups; gi += nwarps) {
+        const Group cur = nxt;
+        if (gi + nwarps < ngroups) load(nxt, (gi + nwarps) * U, U);
+        compute(cur, gi * U, U);
+    }
+    for (int64_t c = ngroups * U + warp; c < nchunks; c += nwarps) {
+        Group one;
+        load(one, c, 1);
+        compute(one, c, 1);
+    }
     // ragged tail (< 128 elements): scalar, same math
     if (warp == nwarps - 1) {
         for (int64_t i = (nchunks << 7) + lane; i < n; i += 32) {
@@ -436,7 +469,7 @@ cudaError_t launch_gelu_bwd(const float* dy, const float* y, const uint32_t* mas
                       t.ncoef <= 16;
     if (fast) {
         const int nc4 = (t.ncoef + 3) / 4;
-        const int64_t blocks = ((n >> 7) / 4 + 1) * 32 / kBlock + 1;
+        const int64_t blocks = ((n >> 7) / 2 + 1) * 32 / kBlock + 1;
 #define TB_CASE(NC)                                                                       \
     case NC: {                                                                            \
         auto k = t.horner ? gelu_bwd_fast_kernel<NC, true> : gelu_bwd_fast_kernel<NC, false>; \

@@ -212,7 +212,7 @@ __global__ void __launch_bounds__(256) ln_fwd_generic_kernel(
 // dgamma = sum g*xhat and dbeta = sum g, written to ws[cta][2][cols].
 // Same TMA ring as the forward; a stage holds kRowsB rows of dy and of y.
 template <int NT>
-__global__ void __launch_bounds__(NT, NT <= 256 ? 3 : 1) ln_bwd_vec_kernel(
+__global__ void __launch_bounds__(NT) ln_bwd_vec_kernel(
     const float* __restrict__ dy, const float* __restrict__ y, const float* __restrict__ rstd,
     const float* __restrict__ gamma, const float* __restrict__ beta, float* __restrict__ dx,
     double* __restrict__ ws, int64_t rows, int cols) {
