@@ -1,0 +1,267 @@
+// test_host.cpp -- GPU test of the C++ operator API (include/tempo_b200/tempo.hpp),
+// the analogue of the reference's proj/tests/test_ops_tempo.cpp on device
+// buffers.  Run by tests/test_cpp_api.py (-m gpu); prints PASS/FAIL lines,
+// exit code = number of failures.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <random>
+#include <string>
+#include <vector>
+
+#include "../../include/tempo_b200/tempo.hpp"
+
+using namespace tempo_b200;
+
+static int g_fail = 0;
+#define CHECK(cond)                                                                      \
+    do {                                                                                 \
+        if (!(cond)) {                                                                   \
+            std::printf("  check failed: %s (%s:%d)\n", #cond, __FILE__, __LINE__);     \
+            ++g_fail;                                                                    \
+            return;                                                                      \
+        }                                                                                \
+    } while (0)
+
+template <typename E, typename F>
+static bool throws(F&& f, const char* needle = nullptr) {
+    try {
+        f();
+    } catch (const E& e) {
+        return needle == nullptr || std::strstr(e.what(), needle) != nullptr;
+    } catch (...) {
+        return false;
+    }
+    return false;
+}
+
+static std::vector<float> randn(std::size_t n, unsigned seed, double scale = 1.0) {
+    std::mt19937_64 rng(seed);
+    std::normal_distribution<double> d(0.0, 1.0);
+    std::vector<float> v(n);
+    for (auto& x : v) x = (float)(scale * d(rng));
+    return v;
+}
+
+static double rel_err(double a, double b) {  // gradcheck.cpp:15-17
+    return std::abs(a - b) / std::max({1.0, std::abs(a), std::abs(b)});
+}
+
+static void run(const char* name, void (*fn)()) {
+    int before = g_fail;
+    try {
+        fn();
+    } catch (const std::exception& e) {
+        std::printf("  exception: %s\n", e.what());
+        ++g_fail;
+    }
+    std::printf("%s %s\n", g_fail == before ? "PASS" : "FAIL", name);
+}
+
+// test_ops_tempo.cpp:51-69 analogue: forward = the reference formula, mask =
+// branch bit, backward = dy * table.eval(y, m).
+static void test_gelu() {
+    GeluPolyTable table = GeluPolyTable::default_fit();
+    CHECK(table.verified());
+    const std::int64_t n = 1000;
+    std::vector<float> xh = randn(n, 1, 2.0), gh = randn(n, 2);
+    Graph g;
+    NodeId x = g.leaf(Tensor::from_host({n}, xh), "x");
+    NodeId y = tempo_ops::gelu(g, x, &table, "y", "y_mask");
+    std::vector<float> yh = g.value(y).to_host();
+    for (std::int64_t i = 0; i < n; ++i) {
+        double ref = (double)xh[i] * 0.5 * std::erfc(-(double)xh[i] * 0.70710678118654752440);
+        CHECK(rel_err(yh[i], (float)ref) <= 1e-6);
+    }
+    auto by_tag = g.ledger.live_by_tag();
+    CHECK(by_tag.at("y") == n * 4);
+    CHECK(by_tag.at("y_mask") == (n + 31) / 32 * 4);  // bit-packed
+    CHECK(g.ledger.reference_bytes() == n * 4 + n);    // reference's 1 B/elem accounting
+    CHECK(by_tag.count("x") == 0);
+    GradientMap gm = g.tape.backward(y, Tensor::from_host({n}, gh));
+    std::vector<float> dx = gm.at(x).to_host();
+    for (std::int64_t i = 0; i < n; ++i) {
+        std::uint8_t m = (double)xh[i] > table.x_star() ? 1 : 0;
+        double ref = (double)gh[i] * table.eval((double)yh[i], m);
+        CHECK(rel_err(dx[i], (float)ref) <= 1e-5);
+    }
+    CHECK(g.ledger.current_bytes() == 0);  // charges released after backward
+}
+
+// test_ops_tempo.cpp:267-289: the unverified table builds, then refuses.
+static void test_gelu_refusals() {
+    Graph g;
+    NodeId x = g.leaf(Tensor::from_host({8}, randn(8, 3)), "x");
+    CHECK(throws<ConfigError>([&] { tempo_ops::gelu(g, x, nullptr, "y", "m"); }, "fitted table"));
+    GeluPolyTable empty;
+    CHECK(throws<ConfigError>([&] { tempo_ops::gelu(g, x, &empty, "y", "m"); }));
+    std::string text = GeluPolyTable::default_fit().serialize();
+    std::size_t at = text.find("max_err=");
+    std::string unver = text.substr(0, at) + "max_err=-1" + text.substr(text.find('\n'));
+    GeluPolyTable u = GeluPolyTable::parse_string(unver);
+    CHECK(!u.verified());
+    Graph g2;
+    NodeId x2 = g2.leaf(Tensor::from_host({8}, randn(8, 4)), "x");
+    NodeId y2 = tempo_ops::gelu(g2, x2, &u, "y", "y_mask");
+    CHECK(throws<ConfigError>([&] { g2.tape.backward(y2, Tensor::from_host({8}, randn(8, 5))); },
+                              "sweep-verified"));
+    CHECK(throws<ParseError>([&] { GeluPolyTable::parse_string("not-a-table v1\n"); }));
+}
+
+// test_ops_tempo.cpp:93-134 analogue.
+static void test_layernorm() {
+    const std::int64_t rows = 3, m = 8;
+    std::vector<float> xh = randn(rows * m, 5), gam = randn(m, 6, 0.3), bet = randn(m, 7),
+                       gh = randn(rows * m, 8);
+    for (auto& v : gam) v += v >= 0 ? 0.5f : -0.5f;
+    Graph g;
+    NodeId x = g.leaf(Tensor::from_host({rows, m}, xh), "x");
+    NodeId gn = g.param(Tensor::from_host({m}, gam), "gamma");
+    NodeId bn = g.param(Tensor::from_host({m}, bet), "beta");
+    NodeId y = tempo_ops::layernorm(g, x, gn, bn, 1e-5, "y", "y_rstd");
+    auto by_tag = g.ledger.live_by_tag();
+    CHECK(by_tag.at("y") == rows * m * 4 && by_tag.at("y_rstd") == rows * 4);
+    std::vector<float> yh = g.value(y).to_host();
+    GradientMap gm = g.tape.backward(y, Tensor::from_host({rows, m}, gh));
+    std::vector<float> dx = gm.at(x).to_host(), dg = gm.at(gn).to_host(), db = gm.at(bn).to_host();
+    // host fp64 reference of the input-based LayerNorm (ops_reference.cpp:47-102)
+    std::vector<double> rdg(m, 0.0), rdb(m, 0.0);
+    for (std::int64_t i = 0; i < rows; ++i) {
+        double mean = 0, var = 0;
+        for (std::int64_t j = 0; j < m; ++j) mean += xh[i * m + j];
+        mean /= m;
+        for (std::int64_t j = 0; j < m; ++j) var += (xh[i * m + j] - mean) * (xh[i * m + j] - mean);
+        var /= m;
+        double rs = 1.0 / std::sqrt(var + 1e-5), s1 = 0, s2 = 0;
+        for (std::int64_t j = 0; j < m; ++j) {
+            double xhat = (xh[i * m + j] - mean) * rs;
+            CHECK(rel_err(yh[i * m + j], gam[j] * xhat + bet[j]) <= 1e-5);
+            s1 += gh[i * m + j] * gam[j];
+            s2 += gh[i * m + j] * gam[j] * xhat;
+        }
+        for (std::int64_t j = 0; j < m; ++j) {
+            double xhat = (xh[i * m + j] - mean) * rs;
+            double r = (gh[i * m + j] * gam[j] - s1 / m - xhat * s2 / m) * rs;
+            CHECK(rel_err(dx[i * m + j], r) <= 1e-5);
+            rdg[j] += gh[i * m + j] * xhat;
+            rdb[j] += gh[i * m + j];
+        }
+    }
+    for (std::int64_t j = 0; j < m; ++j) {
+        CHECK(rel_err(dg[j], rdg[j]) <= 1e-5);
+        CHECK(rel_err(db[j], rdb[j]) <= 1e-5);
+    }
+    // gamma refusal (test_ops_tempo.cpp:124-134)
+    Graph g2;
+    std::vector<float> bad(4, 1.0f);
+    bad[2] = 1e-13f;
+    NodeId x2 = g2.leaf(Tensor::from_host({2, 4}, randn(8, 9)), "x");
+    NodeId gb = g2.param(Tensor::from_host({4}, bad), "gamma");
+    NodeId bb = g2.param(Tensor::zeros({4}), "beta");
+    CHECK(throws<ParamError>([&] { tempo_ops::layernorm(g2, x2, gb, bb, 1e-5, "y", "r"); }, "gamma"));
+}
+
+// test_ops_reference.cpp:65-75 frozen row through the output-only softmax.
+static void test_softmax() {
+    Graph g;
+    NodeId z = g.leaf(Tensor::from_host({1, 2}, {(float)std::log(1.0), (float)std::log(3.0)}), "z");
+    NodeId y = tempo_ops::softmax(g, z, "y");
+    std::vector<float> yh = g.value(y).to_host();
+    CHECK(std::abs(yh[0] - 0.25f) < 1e-6f && std::abs(yh[1] - 0.75f) < 1e-6f);
+    CHECK(g.ledger.current_bytes() == 8);  // output only, not the input (128 -> 64 analogue)
+    GradientMap gm = g.tape.backward(y, Tensor::from_host({1, 2}, {1.0f, 0.0f}));
+    std::vector<float> dz = gm.at(z).to_host();
+    CHECK(std::abs(dz[0] - 0.1875f) < 1e-6f && std::abs(dz[1] + 0.1875f) < 1e-6f);
+}
+
+// ops_tempo.cpp:168-194 + tape.cpp:244-264: dropout keeps only its mask;
+// the recompute rule rebuilds D bit for bit.
+static void test_dropout_recompute() {
+    const std::int64_t rows = 4, c = 64;
+    Graph g;
+    NodeId z = g.leaf(Tensor::from_host({rows, c}, randn(rows * c, 10)), "z");
+    NodeId pr = tempo_ops::softmax(g, z, "sm");
+    BoolMask mask = BoolMask::bernoulli_keep({rows, c}, 0.25, 19);
+    NodeId d = tempo_ops::dropout_recompute(g, pr, 0.25, mask, "d", "d_mask");
+    auto by_tag = g.ledger.live_by_tag();
+    CHECK(by_tag.count("d") == 0);
+    CHECK(by_tag.at("d_mask") == (rows * c) / 8);  // bits, vs 256 B in the reference
+    std::vector<float> P = g.value(pr).to_host(), D = g.value(d).to_host();
+    std::vector<std::uint8_t> keep = mask.to_bytes();
+    for (std::int64_t i = 0; i < rows * c; ++i) {
+        float r = keep[i] ? (float)((double)P[i] * (1.0 / 0.75)) : 0.0f;
+        CHECK(D[i] == r);  // bit-exact mask_scale
+    }
+    // the consumer's lazy stash recomputes D (graph.cpp:23-30, tape.cpp:255-260)
+    LazyStash s = g.input_stash(d, StashRole::SharedDownstream);
+    CHECK(!s.is_materialized());
+    Tensor rec = run_recompute_rule(s.recipe());
+    std::vector<float> R = rec.to_host();
+    CHECK(std::memcmp(R.data(), D.data(), D.size() * 4) == 0);  // bitwise equal
+    GradientMap gm = g.tape.backward(d, Tensor::from_host({rows, c}, randn(rows * c, 11)));
+    CHECK(gm.has(z));
+    // not retained upstream -> ConfigError (ops_tempo.cpp:172-175)
+    Graph g2;
+    NodeId x2 = g2.leaf(Tensor::from_host({rows, c}, randn(rows * c, 12)), "x");
+    CHECK(throws<ConfigError>([&] { tempo_ops::dropout_recompute(g2, x2, 0.1, mask, "d", "m"); }));
+    CHECK(throws<ParamError>([&] { BoolMask::bernoulli_keep({4}, 1.0, 0); }));
+    CHECK(throws<ParamError>([&] { BoolMask::from_bytes({3}, {0, 1, 2}); }));
+}
+
+// fused softmax + dropout: same values as the two-op chain on the same mask
+static void test_softmax_dropout_fused() {
+    const std::int64_t rows = 6, c = 512;
+    std::vector<float> zh = randn(rows * c, 13, 3.0);
+    BoolMask mask = BoolMask::bernoulli_keep({rows, c}, 0.1, 42);
+    Graph a;
+    NodeId za = a.leaf(Tensor::from_host({rows, c}, zh), "z");
+    NodeId pa = tempo_ops::softmax(a, za, "p");
+    NodeId da = tempo_ops::dropout_recompute(a, pa, 0.1, mask, "d", "m");
+    Graph b;
+    NodeId zb = b.leaf(Tensor::from_host({rows, c}, zh), "z");
+    NodeId pb = -1;
+    NodeId db = tempo_ops::softmax_dropout(b, zb, 0.1, mask, 0, 0, "p", "d", "m", &pb);
+    std::vector<float> Pa = a.value(pa).to_host(), Pb = b.value(pb).to_host();
+    std::vector<float> Da = a.value(da).to_host(), Db = b.value(db).to_host();
+    CHECK(std::memcmp(Pa.data(), Pb.data(), Pa.size() * 4) == 0);
+    CHECK(std::memcmp(Da.data(), Db.data(), Da.size() * 4) == 0);
+    // Philox mode: generated mask is consistent with D
+    Graph cgr;
+    NodeId zc = cgr.leaf(Tensor::from_host({rows, c}, zh), "z");
+    NodeId pc = -1;
+    NodeId dc = tempo_ops::softmax_dropout(cgr, zc, 0.1, BoolMask(), 7, 0, "p", "d", "m", &pc);
+    std::vector<float> Pc = cgr.value(pc).to_host(), Dc = cgr.value(dc).to_host();
+    int kept = 0;
+    for (std::int64_t i = 0; i < rows * c; ++i) {
+        bool k = Dc[i] != 0.0f || Pc[i] == 0.0f;
+        kept += k;
+    }
+    CHECK(std::abs(kept / double(rows * c) - 0.9) < 0.02);
+}
+
+static void test_hidden_dropout() {
+    const std::int64_t n = 1000;
+    std::vector<float> xh = randn(n, 14);
+    BoolMask mask = BoolMask::bernoulli_keep({n}, 0.1, 11);
+    Graph g;
+    NodeId x = g.leaf(Tensor::from_host({n}, xh), "x");
+    NodeId y = ref_ops::dropout(g, x, 0.1, mask, "d", "d_mask");
+    CHECK(g.ledger.live_by_tag().at("d_mask") == (n + 31) / 32 * 4);
+    std::vector<float> yh = g.value(y).to_host();
+    std::vector<std::uint8_t> keep = mask.to_bytes();
+    for (std::int64_t i = 0; i < n; ++i)
+        CHECK(yh[i] == (keep[i] ? (float)((double)xh[i] * (1.0 / 0.9)) : 0.0f));
+    CHECK(throws<ParamError>([&] { ref_ops::dropout(g, x, 1.0, mask, "d2", "m2"); }));
+}
+
+int main() {
+    run("gelu forward/backward + ledger", test_gelu);
+    run("gelu refusals", test_gelu_refusals);
+    run("layernorm forward/backward + gamma refusal", test_layernorm);
+    run("softmax frozen row", test_softmax);
+    run("dropout recompute + lazy stash", test_dropout_recompute);
+    run("fused softmax+dropout", test_softmax_dropout_fused);
+    run("hidden dropout", test_hidden_dropout);
+    std::printf("%d failure(s)\n", g_fail);
+    return g_fail;
+}

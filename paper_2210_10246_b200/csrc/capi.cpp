@@ -615,6 +615,13 @@ int tempo_dropout_bwd(const float* dy, const uint32_t* mask, double p, float* dx
                        "tempo_dropout_bwd");
 }
 
+int tempo_tensor_add(const float* a, const float* b, float* out, int64_t n,
+                     tempo_stream_t stream) {
+    if (int rc = check_n(n, "add")) return rc;
+    if (n > 0 && (!a || !b || !out)) return fail(TEMPO_ERR_PARAM, "add: null pointer");
+    return cuda_status(tb::launch_add(a, b, out, n, S(stream)), "tempo_tensor_add");
+}
+
 // ---- masks ---------------------------------------------------------------------
 int tempo_mask_pack(const uint8_t* bytes, uint32_t* bits, int64_t n, int32_t* dev_status,
                     tempo_stream_t stream) {

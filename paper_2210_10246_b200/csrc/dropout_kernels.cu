@@ -141,6 +141,14 @@ __global__ void __launch_bounds__(kBlock) mask_unpack_kernel(const uint32_t* __r
         bytes[i] = (bits[i >> 5] >> (i & 31)) & 1u;
 }
 
+__global__ void __launch_bounds__(kBlock) add_kernel(const float* __restrict__ a,
+                                                     const float* __restrict__ b,
+                                                     float* __restrict__ out, int64_t n) {
+    const int64_t stride = (int64_t)gridDim.x * kBlock;
+    for (int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x; i < n; i += stride)
+        out[i] = a[i] + b[i];
+}
+
 inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
 template <bool PHILOX>
@@ -184,6 +192,13 @@ cudaError_t launch_mask_pack(const uint8_t* bytes, uint32_t* bits, int64_t n, in
     const int64_t warps = (n + 31) >> 5;
     int grid = grid_for((const void*)mask_pack_kernel, kBlock, 0, (warps * 32 + kBlock - 1) / kBlock);
     mask_pack_kernel<<<grid, kBlock, 0, st>>>(bytes, bits, n, status);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_add(const float* a, const float* b, float* out, int64_t n, cudaStream_t st) {
+    if (n == 0) return cudaSuccess;
+    int grid = grid_for((const void*)add_kernel, kBlock, 0, (n + kBlock - 1) / kBlock);
+    add_kernel<<<grid, kBlock, 0, st>>>(a, b, out, n);
     return cudaGetLastError();
 }
 
