@@ -18,7 +18,7 @@ def test_host_library_links_the_c_abi():
     for sym in ["tempo_b200::tempo_ops::gelu(", "tempo_b200::tempo_ops::layernorm(",
                 "tempo_b200::tempo_ops::softmax(", "tempo_b200::tempo_ops::dropout_recompute(",
                 "tempo_b200::ref_ops::dropout(", "tempo_b200::Tape::backward(",
-                "tempo_b200::StashLedger::live_by_tag() const"]:
+                "tempo_b200::StashLedger::live_by_tag"]:
         assert sym in out, sym
     deps = subprocess.run(["ldd", so], capture_output=True, text=True).stdout
     assert "libtempo_b200.so" in deps
