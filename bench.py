@@ -187,6 +187,8 @@ class Chain:
         st = torch.cuda.current_stream()
         for name, fn in calls.items():
             fn()
+            if reps == 0:
+                continue
             ts = []
             for _ in range(reps):
                 flush()

@@ -1,8 +1,7 @@
-"""Run each Tempo kernel of the bench chain a few times at the bench shapes
-(BERT-large layer, B=64) -- the command ncu wraps for profiles/.
-
-    ncu --set full -k regex:<kernel> -c 1 python tools/profile_ops.py [op ...]
-"""
+"""Run one bench step, then each Tempo kernel of the chain ONCE at the bench
+shapes (BERT-large layer, B=64) -- the command tools/profile_round.sh wraps in
+`ncu --set full -s 14 -c 9` (skip the step's 14 launches, capture the 9
+distinct kernels: 8 ops + the LayerNorm dgamma/dbeta reduce)."""
 import os
 import sys
 
@@ -17,10 +16,9 @@ def main():
     chain = bench.Chain(dev, 0, 1)
     chain.step()
     torch.cuda.synchronize()
-    flush_buf = torch.empty(64 * 1024 * 1024, device=dev)
-    calls = chain.per_op_timings(reps=2, flush=lambda: flush_buf.fill_(0.0))
-    for name, (ms, _) in calls.items():
-        print(f"{name:22s} {ms:.4f} ms")
+    res = chain.per_op_timings(reps=0, flush=lambda: None)
+    torch.cuda.synchronize()
+    print("ran", list(res))
 
 
 if __name__ == "__main__":
