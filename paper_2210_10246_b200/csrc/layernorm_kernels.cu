@@ -375,31 +375,29 @@ __global__ void __launch_bounds__(256) ln_bwd_generic_kernel(
 }
 
 // Stage 2: out[j] = sum over CTAs c (fixed order) of ws[c][j], j < 2*cols.
-// One warp per 4 consecutive outputs; lanes stride over c, then a butterfly
-// (identical result in every lane).
-__global__ void __launch_bounds__(256) ln_param_reduce_kernel(const double* __restrict__ ws,
-                                                              int nparts, int cols,
-                                                              float* __restrict__ dgamma,
-                                                              float* __restrict__ dbeta) {
-    const int lane = threadIdx.x & 31;
-    const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int64_t j0 = wid * 4;
+// A 32 x 32 block: column lane tx owns output j0 + tx, slice ty sums the
+// partial rows c = ty, ty + 32, ... (coalesced 256-byte rows, ~nparts/32
+// independent loads per thread); the 32 slices are then added in a fixed
+// order by ty == 0 -- bitwise reproducible.
+__global__ void __launch_bounds__(1024) ln_param_reduce_kernel(const double* __restrict__ ws,
+                                                               int nparts, int cols,
+                                                               float* __restrict__ dgamma,
+                                                               float* __restrict__ dbeta) {
+    __shared__ double part[32][33];
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
     const int64_t total = 2 * (int64_t)cols;
-    if (j0 >= total) return;
-    double acc[4] = {0, 0, 0, 0};
-    for (int c = lane; c < nparts; c += 32) {
-        const double* row = ws + (size_t)c * total;
-#pragma unroll
-        for (int k = 0; k < 4; ++k)
-            if (j0 + k < total) acc[k] += row[j0 + k];
+    const int64_t j = (int64_t)blockIdx.x * 32 + tx;
+    double acc = 0.0;
+    if (j < total) {
+#pragma unroll 4
+        for (int c = ty; c < nparts; c += 32) acc += ws[(size_t)c * total + j];
     }
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-        double v = warp_sum(acc[k]);
-        if (lane == 0 && j0 + k < total) {
-            int64_t j = j0 + k;
-            if (j < cols) dgamma[j] = (float)v; else dbeta[j - cols] = (float)v;
-        }
+    part[ty][tx] = acc;
+    __syncthreads();
+    if (ty == 0 && j < total) {
+        double v = 0.0;
+        for (int k = 0; k < 32; ++k) v += part[k][tx];
+        if (j < cols) dgamma[j] = (float)v; else dbeta[j - cols] = (float)v;
     }
 }
 
@@ -479,9 +477,8 @@ cudaError_t launch_ln_bwd(const float* dy, const float* y, const float* rstd, co
         ln_bwd_generic_kernel<<<grid, 256, smem, st>>>(dy, y, rstd, gamma, beta, dx, w, rows,
                                                        (int)cols);
     }
-    const int64_t warps = (2 * cols + 3) / 4;
-    const int rgrid = (int)((warps * 32 + 255) / 256);
-    ln_param_reduce_kernel<<<rgrid, 256, 0, st>>>(w, grid, (int)cols, dgamma, dbeta);
+    const int rgrid = (int)((2 * cols + 31) / 32);
+    ln_param_reduce_kernel<<<rgrid, 1024, 0, st>>>(w, grid, (int)cols, dgamma, dbeta);
     return cudaGetLastError();
 }
 
