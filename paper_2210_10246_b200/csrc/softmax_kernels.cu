@@ -50,74 +50,77 @@ __global__ void __launch_bounds__(kBlock) softmax_fwd_vec_kernel(
     uint32_t* __restrict__ mask, double scale, uint64_t thresh, uint64_t seed, uint64_t offset,
     int64_t rows) {
     constexpr int C = VPL * 128;
+    constexpr int R = VPL <= 4 ? 2 : 1;  // rows per warp iteration (loads in flight)
     const int lane = threadIdx.x & 31;
     const int64_t warp = ((int64_t)blockIdx.x * kBlock + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * kBlock) >> 5;
-    // one row per warp iteration, the next row's loads issued before this
-    // row's math (register double buffering)
-    float4 nv[VPL];
-    uint32_t nn[VPL];
-    auto load = [&](int64_t r, float4 (&v)[VPL], uint32_t (&nib)[VPL]) {
-        const float4* zr = reinterpret_cast<const float4*>(z + r * C);
+    for (int64_t r0 = warp * R; r0 < rows; r0 += nwarps * R) {
+        float4 v[R][VPL];
+        uint32_t nib[R][VPL];
 #pragma unroll
-        for (int k = 0; k < VPL; ++k) v[k] = ld_stream(zr + k * 32 + lane);
-        if (MODE == kSupplied) {
+        for (int i = 0; i < R; ++i) {
+            const int64_t r = min(r0 + i, rows - 1);  // duplicate the last row if odd
+            const float4* zr = reinterpret_cast<const float4*>(z + r * C);
 #pragma unroll
-            for (int k = 0; k < VPL; ++k) nib[k] = chunk_nibble(mask + ((r * C) >> 5) + k * 4, lane);
-        }
-    };
-    if (warp < rows) load(warp, nv, nn);
-    for (int64_t r = warp; r < rows; r += nwarps) {
-        float4 v[VPL];
-        uint32_t nib[VPL];
+            for (int k = 0; k < VPL; ++k) v[i][k] = ld_stream(zr + k * 32 + lane);
+            if (MODE == kSupplied) {
 #pragma unroll
-        for (int k = 0; k < VPL; ++k) {
-            v[k] = nv[k];
-            nib[k] = nn[k];
-        }
-        if (r + nwarps < rows) load(r + nwarps, nv, nn);
-        float mx = v[0].x;
-#pragma unroll
-        for (int k = 0; k < VPL; ++k)
-            mx = fmaxf(mx, fmaxf(fmaxf(v[k].x, v[k].y), fmaxf(v[k].z, v[k].w)));
-        mx = warp_max(mx);
-        float acc = 0.0f;
-#pragma unroll
-        for (int k = 0; k < VPL; ++k) {
-            v[k].x = exp_shift(v[k].x, mx);
-            v[k].y = exp_shift(v[k].y, mx);
-            v[k].z = exp_shift(v[k].z, mx);
-            v[k].w = exp_shift(v[k].w, mx);
-            acc += (v[k].x + v[k].y) + (v[k].z + v[k].w);
-        }
-        const float inv = 1.0f / warp_sumf(acc);
-        float4* Pr = reinterpret_cast<float4*>(P + r * C);
-        float4* Dr = reinterpret_cast<float4*>(D + r * C);
-#pragma unroll
-        for (int k = 0; k < VPL; ++k) {
-            float4 p;
-            p.x = v[k].x * inv;
-            p.y = v[k].y * inv;
-            p.z = v[k].z * inv;
-            p.w = v[k].w * inv;
-            st_stream(Pr + k * 32 + lane, p);
-            if (MODE == kPlain) continue;
-            uint32_t bits;
-            if (MODE == kPhilox) {
-                U4 rnd = philox_quad(seed, (offset + (uint64_t)(r * C + k * 128 + lane * 4)) >> 2);
-                bits = nibble4((uint64_t)rnd.x >= thresh, (uint64_t)rnd.y >= thresh,
-                               (uint64_t)rnd.z >= thresh, (uint64_t)rnd.w >= thresh);
-                store_chunk_mask(mask + ((r * C) >> 5) + k * 4, bits, lane);
-            } else {
-                bits = nib[k];
+                for (int k = 0; k < VPL; ++k)
+                    nib[i][k] = chunk_nibble(mask + ((r * C) >> 5) + k * 4, lane);
             }
-            if (D) {
-                float4 d;
-                d.x = (bits & 1u) ? dscale(p.x, scale) : 0.0f;
-                d.y = (bits & 2u) ? dscale(p.y, scale) : 0.0f;
-                d.z = (bits & 4u) ? dscale(p.z, scale) : 0.0f;
-                d.w = (bits & 8u) ? dscale(p.w, scale) : 0.0f;
-                st_stream(Dr + k * 32 + lane, d);
+        }
+        float inv[R];
+#pragma unroll
+        for (int i = 0; i < R; ++i) {
+            float mx = v[i][0].x;
+#pragma unroll
+            for (int k = 0; k < VPL; ++k)
+                mx = fmaxf(mx, fmaxf(fmaxf(v[i][k].x, v[i][k].y), fmaxf(v[i][k].z, v[i][k].w)));
+            mx = warp_max(mx);
+            float acc = 0.0f;
+#pragma unroll
+            for (int k = 0; k < VPL; ++k) {
+                v[i][k].x = exp_shift(v[i][k].x, mx);
+                v[i][k].y = exp_shift(v[i][k].y, mx);
+                v[i][k].z = exp_shift(v[i][k].z, mx);
+                v[i][k].w = exp_shift(v[i][k].w, mx);
+                acc += (v[i][k].x + v[i][k].y) + (v[i][k].z + v[i][k].w);
+            }
+            inv[i] = 1.0f / warp_sumf(acc);
+        }
+#pragma unroll
+        for (int i = 0; i < R; ++i) {
+            const int64_t r = r0 + i;
+            if (r >= rows) break;  // warp-uniform
+            float4* Pr = reinterpret_cast<float4*>(P + r * C);
+            float4* Dr = reinterpret_cast<float4*>(D + r * C);
+#pragma unroll
+            for (int k = 0; k < VPL; ++k) {
+                float4 p;
+                p.x = v[i][k].x * inv[i];
+                p.y = v[i][k].y * inv[i];
+                p.z = v[i][k].z * inv[i];
+                p.w = v[i][k].w * inv[i];
+                st_stream(Pr + k * 32 + lane, p);
+                if (MODE == kPlain) continue;
+                uint32_t bits;
+                if (MODE == kPhilox) {
+                    U4 rnd = philox_quad(seed,
+                                         (offset + (uint64_t)(r * C + k * 128 + lane * 4)) >> 2);
+                    bits = nibble4((uint64_t)rnd.x >= thresh, (uint64_t)rnd.y >= thresh,
+                                   (uint64_t)rnd.z >= thresh, (uint64_t)rnd.w >= thresh);
+                    store_chunk_mask(mask + ((r * C) >> 5) + k * 4, bits, lane);
+                } else {
+                    bits = nib[i][k];
+                }
+                if (D) {
+                    float4 d;
+                    d.x = (bits & 1u) ? dscale(p.x, scale) : 0.0f;
+                    d.y = (bits & 2u) ? dscale(p.y, scale) : 0.0f;
+                    d.z = (bits & 4u) ? dscale(p.z, scale) : 0.0f;
+                    d.w = (bits & 8u) ? dscale(p.w, scale) : 0.0f;
+                    st_stream(Dr + k * 32 + lane, d);
+                }
             }
         }
     }
