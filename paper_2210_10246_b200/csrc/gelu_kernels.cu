@@ -47,7 +47,7 @@ __device__ __forceinline__ void gelu_fwd_scalar_words(const float* __restrict__ 
 template <int U>
 __device__ __forceinline__ void gelu_fwd_compute(const float4 (&v)[U], float4* __restrict__ y4,
                                                  uint32_t* __restrict__ mask, int64_t c0,
-                                                 float xstar_gt, int lane) {
+                                                 float xstar_gt, int lane, float* stage) {
     float4 o[U];
     uint32_t slow = 0;  // bit 4u+k: element k of chunk u needs an fp64 path
 #pragma unroll
@@ -60,13 +60,37 @@ __device__ __forceinline__ void gelu_fwd_compute(const float4 (&v)[U], float4* _
         slow |= (uint32_t)tm_gelu_needs_slow(v[u].z) << (4 * u + 2);
         slow |= (uint32_t)tm_gelu_needs_slow(v[u].w) << (4 * u + 3);
     }
-    if (__any_sync(kFull, slow != 0u)) {  // rare per element: the fp64 window / tail
+    if (__any_sync(kFull, slow != 0u)) {
+        // The fp64 window / tail elements (~1 % of N(0,1) inputs, but nearly
+        // every warp iteration has one): stage x and y in this warp's smem
+        // slice and let every lane with a pending element process its next
+        // one, so one pass of the fp64 code serves up to 32 elements.
+        float* xs = stage;           // [U*4][32]
+        float* ys = stage + U * 128; // [U*4][32]
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            if (slow & (1u << (4 * u))) o[u].x = tm_gelu_slow(v[u].x);
-            if (slow & (1u << (4 * u + 1))) o[u].y = tm_gelu_slow(v[u].y);
-            if (slow & (1u << (4 * u + 2))) o[u].z = tm_gelu_slow(v[u].z);
-            if (slow & (1u << (4 * u + 3))) o[u].w = tm_gelu_slow(v[u].w);
+            xs[(4 * u + 0) * 32 + lane] = v[u].x;
+            xs[(4 * u + 1) * 32 + lane] = v[u].y;
+            xs[(4 * u + 2) * 32 + lane] = v[u].z;
+            xs[(4 * u + 3) * 32 + lane] = v[u].w;
+            ys[(4 * u + 0) * 32 + lane] = o[u].x;
+            ys[(4 * u + 1) * 32 + lane] = o[u].y;
+            ys[(4 * u + 2) * 32 + lane] = o[u].z;
+            ys[(4 * u + 3) * 32 + lane] = o[u].w;
+        }
+        uint32_t pending = slow;
+        while (pending) {  // lane-divergent; the warp runs max(popc) passes
+            const int k = __ffs(pending) - 1;
+            pending &= pending - 1;
+            ys[k * 32 + lane] = tm_gelu_slow(xs[k * 32 + lane]);
+        }
+        __syncwarp();
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            o[u].x = ys[(4 * u + 0) * 32 + lane];
+            o[u].y = ys[(4 * u + 1) * 32 + lane];
+            o[u].z = ys[(4 * u + 2) * 32 + lane];
+            o[u].w = ys[(4 * u + 3) * 32 + lane];
         }
     }
 #pragma unroll
@@ -83,7 +107,9 @@ __global__ void __launch_bounds__(kBlock) gelu_fwd_vec_kernel(const float* __res
                                                               float* __restrict__ y,
                                                               uint32_t* __restrict__ mask,
                                                               int64_t n, float xstar_gt) {
+    __shared__ float stage_all[kBlock / 32][2 * kUnroll * 128];
     const int lane = threadIdx.x & 31;
+    float* stage = stage_all[threadIdx.x >> 5];
     const int64_t warp = ((int64_t)blockIdx.x * kBlock + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * kBlock) >> 5;
     const int64_t nchunks = n >> 7;
@@ -107,12 +133,12 @@ __global__ void __launch_bounds__(kBlock) gelu_fwd_vec_kernel(const float* __res
 #pragma unroll
             for (int u = 0; u < kUnroll; ++u) nxt[u] = ld_stream(x4 + ((gn * kUnroll + u) << 5) + lane);
         }
-        gelu_fwd_compute<kUnroll>(v, y4, mask, gi * kUnroll, xstar_gt, lane);
+        gelu_fwd_compute<kUnroll>(v, y4, mask, gi * kUnroll, xstar_gt, lane, stage);
     }
     // leftover whole chunks, one per warp
     for (int64_t c = ngroups * kUnroll + warp; c < nchunks; c += nwarps) {
         float4 v[1] = {ld_stream(x4 + (c << 5) + lane)};
-        gelu_fwd_compute<1>(v, y4, mask, c, xstar_gt, lane);
+        gelu_fwd_compute<1>(v, y4, mask, c, xstar_gt, lane, stage);
     }
     // Ragged tail: words [4*nchunks, ceil(n/32)) on the last warp.
     if (warp == nwarps - 1) {

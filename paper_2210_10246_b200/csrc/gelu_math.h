@@ -128,10 +128,11 @@ __device__ __forceinline__ float2 tm_gelu_q2(float2 a) {
     return __fmul2_rn(__fmul2_rn(E, q), rc);
 }
 
+// y = fma(-|x|, Q(|x|), max(x, 0)): x < 0 gives x*Q, x >= 0 gives x - x*Q,
+// each with a single rounding, and no per-element select.
 __device__ __forceinline__ float2 tm_gelu_fast2(float2 x) {
     const float2 a = make_float2(fminf(fabsf(x.x), 13.0f), fminf(fabsf(x.y), 13.0f));
     const float2 q = tm_gelu_q2(a);
-    const float2 neg = __fmul2_rn(x, q);              // x < 0: x*Q
-    const float2 pos = __ffma2_rn(neg2(x), q, x);     // x >= 0: x - x*Q
-    return make_float2(x.x < 0.0f ? neg.x : pos.x, x.y < 0.0f ? neg.y : pos.y);
+    return __ffma2_rn(make_float2(-fabsf(x.x), -fabsf(x.y)), q,
+                      make_float2(fmaxf(x.x, 0.0f), fmaxf(x.y, 0.0f)));
 }
