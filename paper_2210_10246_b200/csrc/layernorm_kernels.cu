@@ -174,6 +174,104 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? 3 : 1) ln_fwd_vec_kernel(
     }
 }
 
+// Warp-per-row forward for cols = 128*VPL (768, 1024, ...): each warp
+// streams ITS OWN rows through a private kWStages-deep TMA ring (lane 0
+// issues cp.async.bulk of the next row as soon as the warp has read a stage),
+// so there is no block-wide synchronization at all; the row statistics are
+// warp shuffles; gamma/beta are read from shared memory.
+constexpr int kWStages = 3;
+constexpr int kWWarps = 8;
+
+template <int VPL>
+__global__ void __launch_bounds__(kWWarps * 32) ln_fwd_warp_kernel(
+    const float* __restrict__ x, const float* __restrict__ gamma, const float* __restrict__ beta,
+    double eps, float* __restrict__ y, float* __restrict__ rstd, int64_t rows,
+    int32_t* __restrict__ status) {
+    constexpr int C = VPL * 128;
+    extern __shared__ __align__(128) unsigned char dsm[];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(dsm) + wid * kWStages;
+    float4* gb = reinterpret_cast<float4*>(dsm + 1024);  // gamma [C/4] then beta [C/4]
+    float* ring = reinterpret_cast<float*>(dsm + 1024 + 2 * C * 4) + wid * kWStages * C;
+    for (int i = threadIdx.x; i < C / 4; i += blockDim.x) {
+        const float4 g = reinterpret_cast<const float4*>(gamma)[i];
+        gb[i] = g;
+        gb[C / 4 + i] = reinterpret_cast<const float4*>(beta)[i];
+        if (status && blockIdx.x == 0 &&
+            (fabsf(g.x) < 1e-12f || fabsf(g.y) < 1e-12f || fabsf(g.z) < 1e-12f ||
+             fabsf(g.w) < 1e-12f)) {
+            // exact |gamma| < 1e-12 test in double for values near the bound
+            if (fabs((double)g.x) < kGammaMin || fabs((double)g.y) < kGammaMin ||
+                fabs((double)g.z) < kGammaMin || fabs((double)g.w) < kGammaMin)
+                *status = TEMPO_ERR_PARAM;
+        }
+    }
+    const int64_t gw = (int64_t)blockIdx.x * kWWarps + wid;   // global warp
+    const int64_t nw = (int64_t)gridDim.x * kWWarps;
+    if (lane == 0) {
+        for (int s = 0; s < kWStages; ++s) mbar_init(&bars[s], 1);
+        mbar_fence_init();
+    }
+    __syncthreads();  // gamma/beta staged, barriers initialised
+    if (lane == 0) {
+        for (int s = 0; s < kWStages; ++s) {
+            const int64_t r = gw + (int64_t)s * nw;
+            if (r < rows) {
+                mbar_expect_tx(&bars[s], C * 4);
+                bulk_g2s(ring + s * C, x + r * C, C * 4, &bars[s]);
+            }
+        }
+    }
+    const float inv_m = 1.0f / (float)C;
+    int it = 0;
+    for (int64_t r = gw; r < rows; r += nw, ++it) {
+        const int st = it % kWStages;
+        mbar_wait(&bars[st], (uint32_t)((it / kWStages) & 1));
+        float4 v[VPL];
+        const float4* sp = reinterpret_cast<const float4*>(ring + st * C);
+#pragma unroll
+        for (int k = 0; k < VPL; ++k) v[k] = sp[k * 32 + lane];
+        __syncwarp();
+        if (lane == 0) {  // the warp has read stage st: refill it with its next row
+            const int64_t rn = r + (int64_t)kWStages * nw;
+            if (rn < rows) {
+                fence_proxy_async_smem();
+                mbar_expect_tx(&bars[st], C * 4);
+                bulk_g2s(ring + st * C, x + rn * C, C * 4, &bars[st]);
+            }
+        }
+        float s = 0.0f;
+#pragma unroll
+        for (int k = 0; k < VPL; ++k) s += (v[k].x + v[k].y) + (v[k].z + v[k].w);
+        const float mean = warp_sumf(s) * inv_m;
+        float q = 0.0f;
+#pragma unroll
+        for (int k = 0; k < VPL; ++k) {
+            const float d0 = v[k].x - mean, d1 = v[k].y - mean;
+            const float d2 = v[k].z - mean, d3 = v[k].w - mean;
+            q += fmaf(d0, d0, d1 * d1) + fmaf(d2, d2, d3 * d3);
+        }
+        const float var_f = warp_sumf(q) * inv_m;
+        const float rs = (float)(1.0 / sqrt((double)var_f + eps));  // ops_tempo.cpp:111-112
+        float4* yr = reinterpret_cast<float4*>(y + r * C);
+#pragma unroll
+        for (int k = 0; k < VPL; ++k) {
+            const float4 g = gb[k * 32 + lane], b = gb[C / 4 + k * 32 + lane];
+            float4 o;
+            o.x = fmaf(g.x * rs, v[k].x - mean, b.x);
+            o.y = fmaf(g.y * rs, v[k].y - mean, b.y);
+            o.z = fmaf(g.z * rs, v[k].z - mean, b.z);
+            o.w = fmaf(g.w * rs, v[k].w - mean, b.w);
+            st_stream(yr + k * 32 + lane, o);
+        }
+        if (lane == 0) rstd[r] = rs;
+    }
+}
+
+size_t warp_fwd_smem(int vpl) {
+    return 1024 + 2 * (size_t)vpl * 128 * 4 + (size_t)kWWarps * kWStages * vpl * 128 * 4;
+}
+
 // Generic: any cols, any alignment; thread t handles columns t, t+bs, ...
 // Three passes over the row (L1/L2 resident for moderate cols).
 __global__ void __launch_bounds__(256) ln_fwd_generic_kernel(
@@ -211,11 +309,14 @@ __global__ void __launch_bounds__(256) ln_fwd_generic_kernel(
 // Stage 1, vector path: dx per row, per-CTA fp64 column partials of
 // dgamma = sum g*xhat and dbeta = sum g, written to ws[cta][2][cols].
 // Same TMA ring as the forward; a stage holds kRowsB rows of dy and of y.
-template <int NT>
+template <int NT, int CPT>
 __global__ void __launch_bounds__(NT) ln_bwd_vec_kernel(
     const float* __restrict__ dy, const float* __restrict__ y, const float* __restrict__ rstd,
     const float* __restrict__ gamma, const float* __restrict__ beta, float* __restrict__ dx,
     double* __restrict__ ws, int64_t rows, int cols) {
+    // Thread t owns the CPT float4 column groups t, t + blockDim, ... of every
+    // row (conflict-free 128-bit smem reads, coalesced stores); more columns
+    // per thread amortise the per-row block reduction.
     extern __shared__ __align__(128) unsigned char dsm[];
     uint64_t* full = reinterpret_cast<uint64_t*>(dsm);
     float* ring = reinterpret_cast<float*>(dsm + 128);
@@ -242,23 +343,33 @@ __global__ void __launch_bounds__(NT) ln_bwd_vec_kernel(
             if (t < ntiles) issue(t, s);
         }
     }
-    const int c4 = threadIdx.x;
-    const bool act = c4 * 4 < cols;
-    float gm[4] = {1, 1, 1, 1}, bt[4] = {0, 0, 0, 0}, igf[4] = {1, 1, 1, 1};
-    double btd[4] = {0, 0, 0, 0}, igd[4] = {1, 1, 1, 1};
-    if (act) {
-        float4 g = reinterpret_cast<const float4*>(gamma)[c4];
-        float4 b = reinterpret_cast<const float4*>(beta)[c4];
-        gm[0] = g.x; gm[1] = g.y; gm[2] = g.z; gm[3] = g.w;
-        bt[0] = b.x; bt[1] = b.y; bt[2] = b.z; bt[3] = b.w;
+    const int ncg = cols / 4;  // float4 column groups
+    int cg[CPT];
+    bool act[CPT];
+    float gm[CPT][4], bt[CPT][4], igf[CPT][4];
+    double btd[CPT][4], igd[CPT][4];
+    double pg[CPT][4], pb[CPT][4];  // fp64 column partials
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) {
+        cg[c] = threadIdx.x + c * blockDim.x;
+        act[c] = cg[c] < ncg;
+        float4 g = make_float4(1.f, 1.f, 1.f, 1.f), b = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (act[c]) {
+            g = reinterpret_cast<const float4*>(gamma)[cg[c]];
+            b = reinterpret_cast<const float4*>(beta)[cg[c]];
+        }
+        const float ga[4] = {g.x, g.y, g.z, g.w}, ba[4] = {b.x, b.y, b.z, b.w};
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-            igd[k] = 1.0 / (double)gm[k];
-            igf[k] = (float)igd[k];
-            btd[k] = (double)bt[k];
+            gm[c][k] = ga[k];
+            bt[c][k] = ba[k];
+            igd[c][k] = 1.0 / (double)ga[k];
+            igf[c][k] = (float)igd[c][k];
+            btd[c][k] = (double)ba[k];
+            pg[c][k] = 0.0;
+            pb[c][k] = 0.0;
         }
     }
-    double pg[4] = {0, 0, 0, 0}, pb[4] = {0, 0, 0, 0};  // column partials (fp64)
     const float inv_m = 1.0f / (float)cols;
     int it = 0;
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
@@ -267,36 +378,39 @@ __global__ void __launch_bounds__(NT) ln_bwd_vec_kernel(
         const int64_t r0 = tile * kRowsB;
         const float* gs = ring + (2 * st) * tile_floats;
         const float* ys = ring + (2 * st + 1) * tile_floats;
-        float4 gv[kRowsB], yv[kRowsB];
+        float4 gv[kRowsB][CPT], yv[kRowsB][CPT];
         float rsv[kRowsB];
 #pragma unroll
         for (int i = 0; i < kRowsB; ++i) {
-            gv[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-            yv[i] = gv[i];
-            rsv[i] = 0.f;
-            if (r0 + i < rows) {
-                if (act) {
-                    gv[i] = reinterpret_cast<const float4*>(gs + i * cols)[c4];
-                    yv[i] = reinterpret_cast<const float4*>(ys + i * cols)[c4];
+            rsv[i] = (r0 + i < rows) ? __ldg(rstd + r0 + i) : 0.f;
+#pragma unroll
+            for (int c = 0; c < CPT; ++c) {
+                gv[i][c] = make_float4(0.f, 0.f, 0.f, 0.f);
+                yv[i][c] = gv[i][c];
+                if (r0 + i < rows && act[c]) {
+                    gv[i][c] = reinterpret_cast<const float4*>(gs + i * cols)[cg[c]];
+                    yv[i][c] = reinterpret_cast<const float4*>(ys + i * cols)[cg[c]];
                 }
-                rsv[i] = __ldg(rstd + r0 + i);
             }
         }
         float s[2 * kRowsB];
 #pragma unroll
         for (int i = 0; i < kRowsB; ++i) {
-            const float ga[4] = {gv[i].x, gv[i].y, gv[i].z, gv[i].w};
-            const float ya[4] = {yv[i].x, yv[i].y, yv[i].z, yv[i].w};
             float s1 = 0.0f, s2 = 0.0f;
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const float gg = ga[k] * gm[k];
-                const float xh = (ya[k] - bt[k]) * igf[k];
-                s1 += gg;
-                s2 = fmaf(gg, xh, s2);
+            for (int c = 0; c < CPT; ++c) {
+                const float ga[4] = {gv[i][c].x, gv[i][c].y, gv[i][c].z, gv[i][c].w};
+                const float ya[4] = {yv[i][c].x, yv[i][c].y, yv[i][c].z, yv[i][c].w};
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const float gg = ga[k] * gm[c][k];
+                    const float xh = (ya[k] - bt[c][k]) * igf[c][k];
+                    s1 += gg;
+                    s2 = fmaf(gg, xh, s2);
+                }
             }
-            s[2 * i] = act ? s1 : 0.0f;
-            s[2 * i + 1] = act ? s2 : 0.0f;
+            s[2 * i] = s1;
+            s[2 * i + 1] = s2;
         }
         block_sum<2 * kRowsB>(s, red, phase);
         if (threadIdx.x == 0) {  // stage consumed by every thread: refill
@@ -308,32 +422,38 @@ __global__ void __launch_bounds__(NT) ln_bwd_vec_kernel(
         }
 #pragma unroll
         for (int i = 0; i < kRowsB; ++i) {
-            if (r0 + i >= rows || !act) continue;
+            if (r0 + i >= rows) continue;
             const float c1 = s[2 * i] * inv_m, c2 = s[2 * i + 1] * inv_m;
             const float rs = rsv[i];
-            const float ga[4] = {gv[i].x, gv[i].y, gv[i].z, gv[i].w};
-            const float ya[4] = {yv[i].x, yv[i].y, yv[i].z, yv[i].w};
-            float o[4];
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const float xh = (ya[k] - bt[k]) * igf[k];
-                o[k] = (fmaf(ga[k], gm[k], -c1) - xh * c2) * rs;
-                // dgamma/dbeta partials in fp64 with an fp64 xhat: the F64
-                // oracle's accuracy over tens of thousands of rows
-                const double gd = (double)ga[k];
-                pg[k] = fma(gd, ((double)ya[k] - btd[k]) * igd[k], pg[k]);
-                pb[k] += gd;
+            for (int c = 0; c < CPT; ++c) {
+                if (!act[c]) continue;
+                const float ga[4] = {gv[i][c].x, gv[i][c].y, gv[i][c].z, gv[i][c].w};
+                const float ya[4] = {yv[i][c].x, yv[i][c].y, yv[i][c].z, yv[i][c].w};
+                float o[4];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const float xh = (ya[k] - bt[c][k]) * igf[c][k];
+                    o[k] = (fmaf(ga[k], gm[c][k], -c1) - xh * c2) * rs;
+                    // dgamma/dbeta partials in fp64 with an fp64 xhat: the F64
+                    // oracle's accuracy over tens of thousands of rows
+                    const double gd = (double)ga[k];
+                    pg[c][k] = fma(gd, ((double)ya[k] - btd[c][k]) * igd[c][k], pg[c][k]);
+                    pb[c][k] += gd;
+                }
+                st_stream(reinterpret_cast<float4*>(dx + (r0 + i) * cols) + cg[c],
+                          make_float4(o[0], o[1], o[2], o[3]));
             }
-            st_stream(reinterpret_cast<float4*>(dx + (r0 + i) * cols) + c4,
-                      make_float4(o[0], o[1], o[2], o[3]));
         }
     }
-    if (act) {
-        double* wg = ws + (size_t)blockIdx.x * 2 * cols;
+    double* wg = ws + (size_t)blockIdx.x * 2 * cols;
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) {
+        if (!act[c]) continue;
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-            wg[c4 * 4 + k] = pg[k];
-            wg[cols + c4 * 4 + k] = pb[k];
+            wg[cg[c] * 4 + k] = pg[c][k];
+            wg[cols + cg[c] * 4 + k] = pb[c][k];
         }
     }
 }
@@ -410,6 +530,19 @@ bool use_vec(int64_t cols, const void* a, const void* b, const void* c, const vo
 }
 
 int vec_threads(int64_t cols) { return (int)(((cols / 4) + 31) / 32 * 32); }
+// backward: two float4 column groups per thread when cols % 8 == 0
+int bwd_cpt(int64_t cols) { return cols % 8 == 0 ? 2 : 1; }
+int bwd_threads(int64_t cols) {
+    return (int)(((cols / 4 + bwd_cpt(cols) - 1) / bwd_cpt(cols) + 31) / 32 * 32);
+}
+const void* bwd_vec_fn(int64_t cols) {
+    const int t = bwd_threads(cols);
+    if (bwd_cpt(cols) == 2)
+        return t <= 256 ? (const void*)ln_bwd_vec_kernel<256, 2>
+                        : (const void*)ln_bwd_vec_kernel<kMaxThreads, 2>;
+    return t <= 256 ? (const void*)ln_bwd_vec_kernel<256, 1>
+                    : (const void*)ln_bwd_vec_kernel<kMaxThreads, 1>;
+}
 
 // Stage-1 grid for the backward: its CTA count is also the number of
 // partial rows in the workspace, so it depends only on (rows, cols, device).
@@ -418,10 +551,8 @@ size_t bwd_smem(int64_t cols) { return 128 + (size_t)kStages * 2 * kRowsB * cols
 
 int bwd_grid(int64_t rows, int64_t cols, bool vec) {
     int64_t work = vec ? (rows + kRowsB - 1) / kRowsB : rows;
-    const void* k = !vec ? (const void*)ln_bwd_generic_kernel
-                    : vec_threads(cols) <= 256 ? (const void*)ln_bwd_vec_kernel<256>
-                                               : (const void*)ln_bwd_vec_kernel<kMaxThreads>;
-    int block = vec ? vec_threads(cols) : 256;
+    const void* k = !vec ? (const void*)ln_bwd_generic_kernel : bwd_vec_fn(cols);
+    int block = vec ? bwd_threads(cols) : 256;
     size_t smem = vec ? bwd_smem(cols) : (size_t)2 * cols * sizeof(double);
     return grid_for(k, block, smem, work);
 }
@@ -432,6 +563,26 @@ cudaError_t launch_ln_fwd(const float* x, const float* gamma, const float* beta,
                           float* y, float* rstd, int64_t rows, int64_t cols, int32_t* dev_status,
                           cudaStream_t st) {
     if (rows == 0) return cudaSuccess;
+    const int vpl = (int)(cols / 128);
+    if (cols % 128 == 0 && (vpl == 6 || vpl == 8 || vpl == 4 || vpl == 2) &&
+        use_vec(cols, x, y, gamma, beta, x)) {
+        const size_t smem = warp_fwd_smem(vpl);
+#define TB_LNW(V)                                                                            \
+    case V: {                                                                                \
+        auto k = ln_fwd_warp_kernel<V>;                                                      \
+        int grid = grid_for((const void*)k, kWWarps * 32, smem, (rows + kWWarps - 1) / kWWarps); \
+        k<<<grid, kWWarps * 32, smem, st>>>(x, gamma, beta, eps, y, rstd, rows, dev_status); \
+        break;                                                                               \
+    }
+        switch (vpl) {
+            TB_LNW(2)
+            TB_LNW(4)
+            TB_LNW(6)
+            TB_LNW(8)
+        }
+#undef TB_LNW
+        return cudaGetLastError();
+    }
     if (use_vec(cols, x, y, gamma, beta, x)) {
         int block = vec_threads(cols);
         size_t smem = fwd_smem(cols);
@@ -469,8 +620,10 @@ cudaError_t launch_ln_bwd(const float* dy, const float* y, const float* rstd, co
     const int grid = bwd_grid(rows, cols, vec);
     double* w = static_cast<double*>(ws);
     if (vec) {
-        auto k = vec_threads(cols) <= 256 ? ln_bwd_vec_kernel<256> : ln_bwd_vec_kernel<kMaxThreads>;
-        k<<<grid, vec_threads(cols), bwd_smem(cols), st>>>(dy, y, rstd, gamma, beta, dx, w, rows,
+        using KFn = void (*)(const float*, const float*, const float*, const float*,
+                             const float*, float*, double*, int64_t, int);
+        KFn k = reinterpret_cast<KFn>(const_cast<void*>(bwd_vec_fn(cols)));
+        k<<<grid, bwd_threads(cols), bwd_smem(cols), st>>>(dy, y, rstd, gamma, beta, dx, w, rows,
                                                            (int)cols);
     } else {
         size_t smem = (size_t)2 * cols * sizeof(double);
