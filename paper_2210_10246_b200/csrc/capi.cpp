@@ -385,7 +385,9 @@ int grid_for(const void* kernel, int block, size_t smem, int64_t work_items) {
             sms = it->second >> 16;
         } else {
             cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-            if (smem > 48 * 1024)
+            // opt in whenever dynamic smem is used: static + dynamic may exceed
+            // the 48 KB default even when the dynamic part alone does not
+            if (smem > 0)
                 cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)smem);
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, block, smem);

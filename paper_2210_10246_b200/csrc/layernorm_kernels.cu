@@ -51,11 +51,13 @@ __device__ __forceinline__ void block_sum(T (&v)[kN], T* red, int& phase) {
         if (lane == 0) buf[i * 32 + wid] = s;
     }
     __syncthreads();
+    // cross-warp step, lane-parallel: lane l reads warp l's partial (l < nw)
+    // and a butterfly over the warp finishes the sum -- the same fixed order
+    // in every warp, so every thread gets the identical value.
 #pragma unroll
     for (int i = 0; i < kN; ++i) {
-        T s = 0;
-        for (int w = 0; w < nw; ++w) s += buf[i * 32 + w];
-        v[i] = s;
+        T s = lane < nw ? buf[i * 32 + lane] : T(0);
+        v[i] = warp_sum_t(s);
     }
     phase ^= 1;
 }
@@ -531,7 +533,7 @@ bool use_vec(int64_t cols, const void* a, const void* b, const void* c, const vo
 
 int vec_threads(int64_t cols) { return (int)(((cols / 4) + 31) / 32 * 32); }
 // backward: two float4 column groups per thread when cols % 8 == 0
-int bwd_cpt(int64_t cols) { return cols % 8 == 0 ? 2 : 1; }
+int bwd_cpt(int64_t) { return 1; }  // 2 columns groups/thread measured slower (r1)
 int bwd_threads(int64_t cols) {
     return (int)(((cols / 4 + bwd_cpt(cols) - 1) / bwd_cpt(cols) + 31) / 32 * 32);
 }
