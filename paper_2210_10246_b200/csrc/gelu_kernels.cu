@@ -306,8 +306,7 @@ template <int NC4>
 struct FastTable {
     static constexpr int kStride4 = (NC4 & 1) ? NC4 : NC4 + 1;  // float4 units
     float4 rec[kMaxSeg * kStride4];
-    float4 sbf[kMaxSeg];  // (s, b, sqrt-shift flag, 0)
-    float4 thr[2];        // per branch: lo_up of segments 1..3 (NaN pad), base
+    float2 sb[kMaxSeg];
 };
 
 __device__ __forceinline__ float sqrt_approx(float v) {
@@ -335,19 +334,24 @@ __device__ __forceinline__ float min_nan(float a, float b) {
 // constant segments see u*0 = 0.
 template <int NC4, bool HORNER>
 __device__ __forceinline__ float gelu_h_fast(float y, uint32_t m, const FastTable<NC4>& ft,
-                                             float ymin_hi, float ymin_lo) {
+                                             const float (&thr0)[3], const float (&thr1)[3],
+                                             int base1, uint32_t sqrt_mask, float ymin_hi,
+                                             float ymin_lo) {
     y = min_nan(y, 3.402823466e38f);
-    const float4 th = ft.thr[m];  // the branch's thresholds, base in .w
-    int seg = __float_as_int(th.w);
-    seg += (y >= th.x) ? 1 : 0;
-    seg += (y >= th.y) ? 1 : 0;
-    seg += (y >= th.z) ? 1 : 0;
-    const float4 sbf = ft.sbf[seg];
+    int seg = m ? base1 : 0;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) seg += (y >= (m ? thr1[k] : thr0[k])) ? 1 : 0;
+    const float2 sb = ft.sb[seg];
     const float d = (y - ymin_hi) - ymin_lo;
     // branch-free variable choice (the SFU sqrt is cheaper than a divergent branch)
     const float sq = sqrt_approx(max_nan(d, 0.0f));
-    const float u = (sbf.z != 0.0f) ? sq : y;
-    const float tt = max_nan(min_nan(fmaf(u, sbf.x, sbf.y), 1.0f), -1.0f);
+    float u;
+    asm("{\n\t.reg .pred p;\n\t"
+        "setp.ne.u32 p, %3, 0;\n\t"
+        "selp.f32 %0, %1, %2, p;\n}"
+        : "=f"(u)
+        : "f"(sq), "f"(y), "r"((sqrt_mask >> seg) & 1u));
+    const float tt = max_nan(min_nan(fmaf(u, sb.x, sb.y), 1.0f), -1.0f);
     const float4* rec = ft.rec + seg * FastTable<NC4>::kStride4;
     float c[4 * NC4];
 #pragma unroll
@@ -394,15 +398,16 @@ __global__ void __launch_bounds__(kBlock) gelu_bwd_fast_kernel(
         }
         ft.rec[i] = q;
     }
-    for (int i = threadIdx.x; i < nseg; i += kBlock)
-        ft.sbf[i] = make_float4(t.s[i], t.b[i], t.sqrt_shift[i] ? 1.0f : 0.0f, 0.0f);
-    if (threadIdx.x < 2) {
-        const int br = threadIdx.x, base = br ? t.nseg[0] : 0;
-        float th[3];
-        for (int k2 = 0; k2 < 3; ++k2)  // NaN pad: y >= NaN is never true
-            th[k2] = k2 + 1 < t.nseg[br] ? t.lo_up[base + k2 + 1] : __int_as_float(0x7fffffff);
-        ft.thr[br] = make_float4(th[0], th[1], th[2], __int_as_float(base));
+    for (int i = threadIdx.x; i < nseg; i += kBlock) ft.sb[i] = make_float2(t.s[i], t.b[i]);
+    float thr0[3], thr1[3];
+    uint32_t sqrt_mask = 0;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        thr0[k] = k + 1 < t.nseg[0] ? t.lo_up[k + 1] : __int_as_float(0x7fffffff);  // NaN: never >=
+        thr1[k] = k + 1 < t.nseg[1] ? t.lo_up[t.nseg[0] + k + 1] : __int_as_float(0x7fffffff);
     }
+    for (int i = 0; i < nseg; ++i) sqrt_mask |= (t.sqrt_shift[i] ? 1u : 0u) << i;
+    const int base1 = t.nseg[0];
     const float ymin_hi = t.ymin_hi, ymin_lo = t.ymin_lo;
     __syncthreads();
 
@@ -433,7 +438,8 @@ __global__ void __launch_bounds__(kBlock) gelu_bwd_fast_kernel(
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             if (u < uu) {
-#define TB_H(val, bit) gelu_h_fast<NC4, HORNER>(val, (G.nib[u] >> bit) & 1u, ft, ymin_hi, ymin_lo)
+#define TB_H(val, bit) gelu_h_fast<NC4, HORNER>(val, (G.nib[u] >> bit) & 1u, ft, thr0, thr1, \
+                                                base1, sqrt_mask, ymin_hi, ymin_lo)
                 float4 o;
                 o.x = G.g[u].x * TB_H(G.v[u].x, 0);
                 o.y = G.g[u].y * TB_H(G.v[u].y, 1);
@@ -447,14 +453,12 @@ __global__ void __launch_bounds__(kBlock) gelu_bwd_fast_kernel(
     // whole groups of U chunks with the next group's loads in flight during
     // this group's math (register double buffering)
     const int64_t ngroups = nchunks / U;
-    Group ga, gb;  // ping-pong: no register copies between iterations
-    if (warp < ngroups) load(ga, warp * U, U);
-    for (int64_t gi = warp; gi < ngroups; gi += 2 * nwarps) {
-        if (gi + nwarps < ngroups) load(gb, (gi + nwarps) * U, U);
-        compute(ga, gi * U, U);
-        if (gi + nwarps >= ngroups) break;
-        if (gi + 2 * nwarps < ngroups) load(ga, (gi + 2 * nwarps) * U, U);
-        compute(gb, (gi + nwarps) * U, U);
+    Group nxt;
+    if (warp < ngroups) load(nxt, warp * U, U);
+    for (int64_t gi = warp; gi < ngroups; gi += nwarps) {
+        const Group cur = nxt;
+        if (gi + nwarps < ngroups) load(nxt, (gi + nwarps) * U, U);
+        compute(cur, gi * U, U);
     }
     for (int64_t c = ngroups * U + warp; c < nchunks; c += nwarps) {
         Group one;
@@ -465,7 +469,8 @@ __global__ void __launch_bounds__(kBlock) gelu_bwd_fast_kernel(
     if (warp == nwarps - 1) {
         for (int64_t i = (nchunks << 7) + lane; i < n; i += 32) {
             const uint32_t m = (mask[i >> 5] >> (i & 31)) & 1u;
-            dx[i] = dy[i] * gelu_h_fast<NC4, HORNER>(y[i], m, ft, ymin_hi, ymin_lo);
+            dx[i] = dy[i] * gelu_h_fast<NC4, HORNER>(y[i], m, ft, thr0, thr1, base1, sqrt_mask,
+                                                     ymin_hi, ymin_lo);
         }
     }
 }
