@@ -10,7 +10,8 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "_lib", "libtempo_b200.so")
+# TEMPO_B200_LIB overrides the library path (A/B builds of the same C-ABI)
+LIB_PATH = os.environ.get("TEMPO_B200_LIB", os.path.join(HERE, "_lib", "libtempo_b200.so"))
 
 # tempo_status_t (include/tempo_b200.h), mirroring proj/include/tempo/errors.hpp
 STATUS_NAMES = {
