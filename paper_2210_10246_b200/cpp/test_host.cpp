@@ -161,6 +161,47 @@ static void test_layernorm() {
     CHECK(throws<ParamError>([&] { tempo_ops::layernorm(g2, x2, gb, bb, 1e-5, "y", "r"); }, "gamma"));
 }
 
+// Wide rows take the TMA (cp.async.bulk) kernels: warp-per-row forward,
+// CTA-per-row backward with the two-stage dgamma/dbeta reduction.
+static void test_layernorm_wide() {
+    const std::int64_t rows = 37, m = 1024;
+    std::vector<float> xh = randn(rows * m, 21), gam = randn(m, 22, 0.2), bet = randn(m, 23, 0.1),
+                       gh = randn(rows * m, 24);
+    for (auto& v : gam) v += 1.0f;
+    Graph g;
+    NodeId x = g.leaf(Tensor::from_host({rows, m}, xh), "x");
+    NodeId gn = g.param(Tensor::from_host({m}, gam), "gamma");
+    NodeId bn = g.param(Tensor::from_host({m}, bet), "beta");
+    NodeId y = tempo_ops::layernorm(g, x, gn, bn, 1e-5, "y", "y_rstd");
+    std::vector<float> yh = g.value(y).to_host();
+    GradientMap gm = g.tape.backward(y, Tensor::from_host({rows, m}, gh));
+    std::vector<float> dx = gm.at(x).to_host(), dg = gm.at(gn).to_host(), db = gm.at(bn).to_host();
+    std::vector<double> rdg(m, 0.0), rdb(m, 0.0);
+    for (std::int64_t i = 0; i < rows; ++i) {
+        double mean = 0, var = 0;
+        for (std::int64_t j = 0; j < m; ++j) mean += xh[i * m + j];
+        mean /= m;
+        for (std::int64_t j = 0; j < m; ++j) var += (xh[i * m + j] - mean) * (xh[i * m + j] - mean);
+        var /= m;
+        double rs = 1.0 / std::sqrt(var + 1e-5), s1 = 0, s2 = 0;
+        for (std::int64_t j = 0; j < m; ++j) {
+            double xhat = (xh[i * m + j] - mean) * rs;
+            CHECK(rel_err(yh[i * m + j], gam[j] * xhat + bet[j]) <= 1e-5);
+            s1 += gh[i * m + j] * gam[j];
+            s2 += gh[i * m + j] * gam[j] * xhat;
+        }
+        for (std::int64_t j = 0; j < m; ++j) {
+            double xhat = (xh[i * m + j] - mean) * rs;
+            CHECK(rel_err(dx[i * m + j], (gh[i * m + j] * gam[j] - s1 / m - xhat * s2 / m) * rs) <=
+                  1e-5);
+            rdg[j] += gh[i * m + j] * xhat;
+            rdb[j] += gh[i * m + j];
+        }
+    }
+    for (std::int64_t j = 0; j < m; ++j)
+        CHECK(rel_err(dg[j], rdg[j]) <= 1e-5 && rel_err(db[j], rdb[j]) <= 1e-5);
+}
+
 // test_ops_reference.cpp:65-75 frozen row through the output-only softmax.
 static void test_softmax() {
     Graph g;
@@ -258,6 +299,7 @@ int main() {
     run("gelu forward/backward + ledger", test_gelu);
     run("gelu refusals", test_gelu_refusals);
     run("layernorm forward/backward + gamma refusal", test_layernorm);
+    run("layernorm wide rows (TMA kernels)", test_layernorm_wide);
     run("softmax frozen row", test_softmax);
     run("dropout recompute + lazy stash", test_dropout_recompute);
     run("fused softmax+dropout", test_softmax_dropout_fused);
