@@ -373,11 +373,25 @@ namespace tb {
 int grid_for(const void* kernel, int block, size_t smem, int64_t work_items) {
     static std::mutex mu;
     static std::map<std::tuple<int, const void*, int, size_t>, int> cache;
+    static std::map<std::pair<int, const void*>, bool> optin;  // per (device, kernel)
     int dev = 0;
     cudaGetDevice(&dev);
     int per_sm = 0, sms = 0;
     {
         std::lock_guard<std::mutex> lock(mu);
+        // The dynamic-smem limit is a per-KERNEL attribute: raise it once to
+        // the device's opt-in maximum, so launches of the same kernel with
+        // different dynamic sizes never see a stale smaller limit (static +
+        // dynamic may exceed the 48 KB default even when dynamic alone does not).
+        if (smem > 0 && !optin[{dev, kernel}]) {
+            int maxopt = 0;
+            cudaDeviceGetAttribute(&maxopt, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+            cudaFuncAttributes fa{};
+            cudaFuncGetAttributes(&fa, kernel);
+            cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 maxopt - (int)fa.sharedSizeBytes);
+            optin[{dev, kernel}] = true;
+        }
         auto key = std::make_tuple(dev, kernel, block, smem);
         auto it = cache.find(key);
         if (it != cache.end()) {
@@ -385,11 +399,6 @@ int grid_for(const void* kernel, int block, size_t smem, int64_t work_items) {
             sms = it->second >> 16;
         } else {
             cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-            // opt in whenever dynamic smem is used: static + dynamic may exceed
-            // the 48 KB default even when the dynamic part alone does not
-            if (smem > 0)
-                cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)smem);
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, block, smem);
             if (per_sm < 1) per_sm = 1;
             if (sms < 1) sms = 1;

@@ -206,6 +206,22 @@ def test_layernorm_backward_identical_inputs(tops, port, cuda, rows, cols):
     assert torch.equal(dx, dx2) and torch.equal(dg, dg2) and torch.equal(db, db2)
 
 
+def test_layernorm_alternating_widths(tops, port, cuda):
+    """Same kernels launched with different dynamic smem sizes in turn (a
+    per-kernel attribute must not go stale)."""
+    import torch
+    for rows, cols in [(7, 1024), (5, 768), (9, 1024), (3, 512), (7, 1024)]:
+        x, gam, bet, dy = ln_inputs(rows, cols, rows + cols)
+        ry, rrs, _ = port.ln_fwd(x, gam, bet, 1e-5)
+        y, rstd = tops.layernorm_ip_fwd(to_dev(x, cuda), to_dev(gam, cuda), to_dev(bet, cuda))
+        dx, dg, db = tops.layernorm_ip_bwd(to_dev(dy, cuda), to_dev(ry, cuda), to_dev(rrs, cuda),
+                                           to_dev(gam, cuda), to_dev(bet, cuda))
+        torch.cuda.synchronize()
+        assert rel_err(y.cpu().numpy(), ry) <= 1e-5
+        rdx, _, _ = port.ln_bwd(dy, ry, rrs, gam, bet, False)
+        assert rel_err(dx.cpu().numpy(), rdx) <= 1e-5
+
+
 def test_layernorm_refusals(tops, cuda):
     import torch
     from paper_2210_10246_b200 import TempoError
