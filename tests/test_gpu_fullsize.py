@@ -41,7 +41,7 @@ def test_cfg3_attention_full(tops, port, cuda):
     assert torch.equal(D, Drec)                       # recompute == forward, bitwise
     s = P.double().sum(dim=1)
     assert float((s - 1).abs().max()) < 1e-5          # rows of P sum to 1
-    kept = (D != 0) | (P == 0)
+    dropped = float((D == 0).double().mean())            # P > 0 everywhere here
     words = mask.view(torch.int32)
     keep_rate = float(torch.tensor([bin(int(w) & 0xffffffff).count("1") for w in
                                     words[:4096].cpu()]).sum()) / (4096 * 32)
@@ -56,7 +56,7 @@ def test_cfg3_attention_full(tops, port, cuda):
     rdZ = port.softmax_bwd(port.dropout_apply(dDs, keep, p), Ps)
     dZs = dZ.cpu().numpy()[sel]
     assert np.all(np.abs(dZs - rdZ) <= 1e-5 * np.abs(rdZ) + 1e-8)
-    assert bool(kept.all())
+    assert abs(dropped - p) < 0.002
 
 
 def test_cfg4_layer_chain_full(tops, port, table_text, cuda):
