@@ -39,10 +39,14 @@ __device__ __forceinline__ double tm_gelu_exact(float x) {
     return xd * (0.5 * erfc(-xd * 0.70710678118654752440));
 }
 
-// Does x need an fp64 path?
+// Does x need an fp64 path?  Two unsigned range tests on the bit pattern:
+//  * the window around x* (bits of -0.7361665 .. -0.7674165, widened by 16
+//    ulps so it covers the float test |x - x*| < 1/64 used below),
+//  * x < -13, -inf and negative NaNs (every pattern above -13's).
+// +inf and positive NaNs are handled by the fast path itself.
 __device__ __forceinline__ bool tm_gelu_needs_slow(float x) {
-    return fabsf(x - TM_GELU_XSTAR_F) < TM_GELU_TAYLOR_WINDOW || !(x >= TM_GELU_FAST_XMIN) ||
-           x == __int_as_float(0x7f800000);
+    const uint32_t u = __float_as_uint(x);
+    return (u - (0xBF3C7569u - 16u)) <= (0xBF447569u - 0xBF3C7569u + 32u) || u > 0xC1500000u;
 }
 
 __device__ __noinline__ float tm_gelu_slow(float x) {

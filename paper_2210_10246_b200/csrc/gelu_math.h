@@ -78,9 +78,10 @@ __device__ __forceinline__ float tm_gelu_q(float a) {
 
 // Fast path: valid for finite x >= -13 (x > 13 gives Q < 2^-126 and y = x,
 // as the reference's double result rounds there).
+__device__ __forceinline__ float tm_min_nan(float a, float b);
 __device__ __forceinline__ float tm_gelu_fast(float x) {
     const float q = tm_gelu_q(fminf(fabsf(x), 13.0f));
-    return x < 0.0f ? x * q : fmaf(-x, q, x);
+    return fmaf(-tm_min_nan(fabsf(x), 3.402823466e38f), q, fmaxf(x, 0.0f));
 }
 
 // ---- two elements per instruction: Blackwell's packed fp32x2 pipe ----------
@@ -130,9 +131,17 @@ __device__ __forceinline__ float2 tm_gelu_q2(float2 a) {
 
 // y = fma(-|x|, Q(|x|), max(x, 0)): x < 0 gives x*Q, x >= 0 gives x - x*Q,
 // each with a single rounding, and no per-element select.
+// |x| is clamped to FLT_MAX NaN-propagatingly so +inf gives +inf and NaN
+// gives NaN without a separate path.
+__device__ __forceinline__ float tm_min_nan(float a, float b) {
+    float r;
+    asm("min.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
+    return r;
+}
 __device__ __forceinline__ float2 tm_gelu_fast2(float2 x) {
     const float2 a = make_float2(fminf(fabsf(x.x), 13.0f), fminf(fabsf(x.y), 13.0f));
     const float2 q = tm_gelu_q2(a);
-    return __ffma2_rn(make_float2(-fabsf(x.x), -fabsf(x.y)), q,
-                      make_float2(fmaxf(x.x, 0.0f), fmaxf(x.y, 0.0f)));
+    return __ffma2_rn(make_float2(-tm_min_nan(fabsf(x.x), 3.402823466e38f),
+                                  -tm_min_nan(fabsf(x.y), 3.402823466e38f)),
+                      q, make_float2(fmaxf(x.x, 0.0f), fmaxf(x.y, 0.0f)));
 }
