@@ -31,6 +31,10 @@
 
 #include "../tempo_b200.h"
 
+// tempo_b200/inplace_elementwise.cuh adds the templated graph builder when
+// this header was included first.
+#define TEMPO_B200_HAS_GRAPH_API 1
+
 namespace tempo_b200 {
 
 // ---- errors (errors.hpp:14-61) ----------------------------------------------

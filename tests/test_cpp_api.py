@@ -31,3 +31,14 @@ def test_cpp_operator_api_on_gpu(cuda):
     print(out.stdout)
     assert out.returncode == 0, out.stdout + out.stderr
     assert "0 failure(s)" in out.stdout
+
+
+@pytest.mark.gpu
+def test_inplace_elementwise_functor_kernels(cuda):
+    """include/tempo_b200/inplace_elementwise.cuh: the reference's generic
+    scheme (ops_tempo.cpp:32-71) as compile-time device specs."""
+    exe = os.path.join(LIB, "test_elementwise")
+    out = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    print(out.stdout)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert "0 failure(s)" in out.stdout

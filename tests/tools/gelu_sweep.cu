@@ -17,7 +17,7 @@
 
 __device__ unsigned long long g_hist[8];
 __device__ unsigned long long g_count, g_window, g_window_bad, g_nan_bad;
-__device__ unsigned int g_max, g_worst;
+__device__ unsigned int g_max, g_worst, g_band[8];
 
 __device__ __forceinline__ long long ordinal(float f) {
     int i = __float_as_int(f);
@@ -47,6 +47,17 @@ __global__ void sweep(unsigned long long begin, unsigned long long end) {
         ++cnt;
         if (ad > mx) { mx = ad; worst = (unsigned int)u; }
         if (fabsf(x - TM_GELU_XSTAR_F) < TM_GELU_TAYLOR_WINDOW) { ++win; winbad += (ad != 0); }
+        // fast-path error inside the window, by distance band 2^-(6+b)
+        const float dist = fabsf(x - TM_GELU_XSTAR_F);
+        if (dist < 0.015625f) {
+            const float fy = tm_gelu_fast2(make_float2(x, 1.0f)).x;
+            long long fd = ordinal(ref) - ordinal(fy);
+            unsigned int fad = (unsigned int)(fd < 0 ? -fd : fd);
+            int b = 0;
+            float lim = 0.0078125f;
+            while (b < 7 && dist < lim) { ++b; lim *= 0.5f; }
+            atomicMax(&g_band[b], fad);
+        }
     }
     for (int i = 0; i < 8; ++i) if (hist[i]) atomicAdd(&g_hist[i], hist[i]);
     atomicAdd(&g_count, cnt);
@@ -83,7 +94,11 @@ int main(int argc, char** argv) {
     memcpy(&wx, &worst, 4);
     printf("{\"checked\": %llu, \"max_ulp\": %u, \"worst_x\": %.9g, \"hist\": [", cnt, mx, wx);
     for (int i = 0; i < 8; ++i) printf("%llu%s", hist[i], i < 7 ? ", " : "");
-    printf("], \"window_checked\": %llu, \"window_mismatch\": %llu, \"nan_mismatch\": %llu}\n",
-           win, winbad, nanbad);
+    unsigned int band[8];
+    cudaMemcpyFromSymbol(band, g_band, sizeof(band));
+    printf("], \"window_checked\": %llu, \"window_mismatch\": %llu, \"nan_mismatch\": %llu, "
+           "\"fast_path_max_ulp_by_band\": [", win, winbad, nanbad);
+    for (int i = 0; i < 8; ++i) printf("%u%s", band[i], i < 7 ? ", " : "");
+    printf("]}\n");
     return 0;
 }
