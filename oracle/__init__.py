@@ -227,6 +227,7 @@ class Ref:
         self.L = L
         L.ref_last_error.restype = C.c_char_p
         L.ref_fit_table_default.argtypes = [C.c_char_p, _i64, C.POINTER(_i64)]
+        L.ref_fit_table.argtypes = [C.c_double, C.c_int, C.c_char_p, _i64, C.POINTER(_i64)]
         L.ref_table_eval.argtypes = [C.c_char_p, _f64p, _u8p, _f64p, _i64]
         L.ref_table_parse.argtypes = [C.c_char_p]
         L.ref_gelu_ip.argtypes = [C.c_char_p, _f32p, C.c_void_p, _i64, C.c_int, _f32p, _u8p,
@@ -261,6 +262,13 @@ class Ref:
         self._check(self.L.ref_fit_table_default(None, 0, C.byref(n)))
         buf = C.create_string_buffer(n.value + 1)
         self._check(self.L.ref_fit_table_default(buf, n.value + 1, C.byref(n)))
+        return buf.value.decode()
+
+    def fit_table(self, tol: float, max_degree: int) -> str:
+        n = _i64()
+        self._check(self.L.ref_fit_table(tol, max_degree, None, 0, C.byref(n)))
+        buf = C.create_string_buffer(n.value + 1)
+        self._check(self.L.ref_fit_table(tol, max_degree, buf, n.value + 1, C.byref(n)))
         return buf.value.decode()
 
     def table_parse(self, text: str) -> None:

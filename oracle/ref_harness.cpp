@@ -96,6 +96,20 @@ int ref_fit_table_default(char* buf, std::int64_t cap, std::int64_t* len) {
     });
 }
 
+// fit::fit_table(opts) with a chosen tolerance / degree cap (gelu_fit.hpp:32-46).
+int ref_fit_table(double tol, int max_degree, char* buf, std::int64_t cap, std::int64_t* len) {
+    return guarded([&] {
+        fit::FitOptions o;
+        o.tolerance = tol;
+        o.max_degree = max_degree;
+        std::string s = fit::fit_table(o).serialize();
+        *len = static_cast<std::int64_t>(s.size());
+        if (buf && cap > static_cast<std::int64_t>(s.size())) {
+            std::memcpy(buf, s.data(), s.size() + 1);
+        }
+    });
+}
+
 // GeluPolyTable::eval (gelu_table.cpp:172-188) on a parsed v1 table.
 int ref_table_eval(const char* table_text, const double* y,
                    const std::uint8_t* m, double* out, std::int64_t n) {

@@ -37,6 +37,15 @@ def main() -> None:
     with open(os.path.join(HERE, "gelu_table_default_v1.txt"), "w") as f:
         f.write(table)
 
+    # tables fitted with other options (more segments / other degrees), for the
+    # generic device paths (gelu_fit.hpp:32-46)
+    import json
+    extra = {}
+    for tol, deg in [(1e-5, 13), (1e-6, 13), (1e-4, 4), (3e-6, 8)]:
+        extra[f"tol{tol:g}_deg{deg}"] = ref.fit_table(tol, deg)
+    with open(os.path.join(HERE, "gelu_tables_extra.json"), "w") as f:
+        json.dump(extra, f, indent=1)
+
     g = np.random.default_rng(20221019)
     out = {}
 

@@ -174,3 +174,26 @@ def test_stash_bytes_match_memory_model(golden):
         assert ops.layer_stash_bytes_per_token(s, h, a, tempo=True, mask_bits=False) == o
     # bit-packed masks: BERT-large S=512 -> 75,528 B/token
     assert ops.layer_stash_bytes_per_token(512, 1024, 16, tempo=True, mask_bits=True) == 75528
+
+
+def _extra_tables():
+    import json
+    with open(os.path.join(ROOT, "tests", "golden", "gelu_tables_extra.json")) as f:
+        return json.load(f)
+
+
+@pytest.mark.parametrize("name", sorted(_extra_tables()))
+def test_extra_tables_parse_roundtrip_and_eval(name, port):
+    """Tables the reference fits with other tolerances / degree caps (more
+    segments than the default): parsed, re-serialized bitwise, and evaluated
+    on the host exactly like the reference (the C oracle is pinned to it)."""
+    text = _extra_tables()[name]
+    t = ops.GeluTable(text)
+    assert t.serialize() == text
+    info = t.info()
+    assert info["verified"] and info["n_segments"] >= 9
+    pt = port.table(text)
+    ys = np.concatenate([np.linspace(-0.2, 9.0, 50001), [info["y_min"], 0.0, 8.0, 1e30]])
+    for m in (0, 1):
+        mm = np.full(ys.size, m, np.uint8)
+        assert np.array_equal(t.eval_host(ys, mm), pt.eval(ys, mm))

@@ -135,6 +135,37 @@ def test_gelu_backward_table_eval_grid(tops, port, table_text, cuda):
         assert rel_err(h.cpu().numpy(), pt.gelu_bwd(ones, ys, mm)) <= 1e-5
 
 
+def _extra_tables():
+    import json
+    import os
+    here = os.path.dirname(os.path.abspath(__file__))
+    with open(os.path.join(here, "golden", "gelu_tables_extra.json")) as f:
+        return json.load(f)
+
+
+@pytest.mark.parametrize("name", sorted(_extra_tables()))
+def test_gelu_backward_other_tables(tops, port, cuda, name):
+    """Tables with more segments / other degrees (fitted by the reference):
+    the device table is a kernel input, not a compiled-in constant."""
+    import torch
+    text = _extra_tables()[name]
+    table = tops.GeluTable(text)
+    pt = port.table(text)
+    n = 1 << 20
+    x = gelu_inputs(n, 21)
+    y, m = port.gelu_fwd(x, pt.x_star)
+    dy = np.random.default_rng(22).standard_normal(n).astype(np.float32)
+    bits = np.packbits(m, bitorder="little")
+    bits = np.concatenate([bits, np.zeros((-bits.size) % 4, np.uint8)]).view(np.uint32)
+    dx = tops.gelu_ip_bwd(to_dev(dy, cuda), to_dev(y, cuda), bits_to_dev(bits, cuda), table)
+    torch.cuda.synchronize()
+    assert rel_err(dx.cpu().numpy(), pt.gelu_bwd(dy, y, m)) <= 1e-5
+    # forward mask uses this table's x*
+    yg, mg = tops.gelu_ip_fwd(to_dev(x, cuda), table)
+    torch.cuda.synchronize()
+    assert np.array_equal(unpack(mg, n), m)
+
+
 def test_gelu_chain_forward_backward(tops, port, table_text, cuda):
     import torch
     table = tops.GeluTable(table_text)
