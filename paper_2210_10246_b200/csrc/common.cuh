@@ -32,6 +32,33 @@ __device__ __forceinline__ uint32_t ld_stream(const uint32_t* p) {
     asm volatile("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(v) : "l"(p));
     return v;
 }
+// 256-bit accesses (sm_100: LDG/STG .256): eight consecutive floats per lane,
+// so a lane owns a whole byte of a bit-packed mask.
+struct F8 {
+    float v[8];
+};
+__device__ __forceinline__ F8 ld_stream8(const float* p) {
+    F8 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=f"(r.v[0]), "=f"(r.v[1]), "=f"(r.v[2]), "=f"(r.v[3]), "=f"(r.v[4]),
+                   "=f"(r.v[5]), "=f"(r.v[6]), "=f"(r.v[7])
+                 : "l"(p));
+    return r;
+}
+__device__ __forceinline__ void st_stream8(float* p, const F8& r) {
+    asm volatile("st.global.cs.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "f"(r.v[0]),
+                 "f"(r.v[1]), "f"(r.v[2]), "f"(r.v[3]), "f"(r.v[4]), "f"(r.v[5]), "f"(r.v[6]),
+                 "f"(r.v[7])
+                 : "memory");
+}
+__device__ __forceinline__ void st_stream(uint8_t* p, uint32_t v) {
+    asm volatile("st.global.cs.u8 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+// (acc << 1) | sign(v): one funnel shift collects a sign bit.
+__device__ __forceinline__ uint32_t push_sign(uint32_t acc, float v) {
+    return __funnelshift_l(__float_as_uint(v), acc, 1);
+}
+
 // Plain cached load (data read by several lanes / re-read from L2).
 __device__ __forceinline__ uint32_t ld_cached(const uint32_t* p) { return __ldg(p); }
 

@@ -39,24 +39,31 @@ __device__ __forceinline__ double tm_gelu_exact(float x) {
     return xd * (0.5 * erfc(-xd * 0.70710678118654752440));
 }
 
-// Does x need an fp64 path?  Two unsigned range tests on the bit pattern:
-//  * the window around x* (bits of -0.7361665 .. -0.7674165, widened by 16
-//    ulps so it covers the float test |x - x*| < 1/64 used below),
-//  * x < -13, -inf and negative NaNs (every pattern above -13's).
-// +inf and positive NaNs are handled by the fast path itself.
-__device__ __forceinline__ bool tm_gelu_needs_slow(float x) {
-    const uint32_t u = __float_as_uint(x);
-    return (u - (0xBF3C7569u - 16u)) <= (0xBF447569u - 0xBF3C7569u + 32u) || u > 0xC1500000u;
+// Does x need an fp64 path?  The window |x - xs_lo| < 1/64 around the GELU
+// minimum (xs_lo = the largest float <= the table's x*; for the default
+// table exactly TM_GELU_XSTAR_F) tested as the sign of fma(d, d, -2^-12)
+// with d = xs_lo - x (exact near the window edge by Sterbenz, and a fused
+// sign is the exact sign), plus x < -13 and -inf.  NaN and +inf are handled
+// by the fast path itself.  The vector kernel evaluates the same predicate
+// with FADD2/FFMA2 sign bits, so both paths fix exactly the same inputs.
+#define TM_GELU_WINDOW_SQ_NEG (-0.000244140625f)
+__device__ __forceinline__ bool tm_gelu_needs_fix(float x, float xs_lo) {
+    const float d = xs_lo - x;
+    return fmaf(d, d, TM_GELU_WINDOW_SQ_NEG) < 0.0f || x < TM_GELU_FAST_XMIN;
 }
 
-__device__ __noinline__ float tm_gelu_slow(float x) {
+__device__ __noinline__ float tm_gelu_exact_call(float x) { return (float)tm_gelu_exact(x); }
+
+// The fp64 value of a flagged element: the Taylor series inside the window,
+// the reference formula elsewhere.
+__device__ __forceinline__ float tm_gelu_fix(float x) {
     if (fabsf(x - TM_GELU_XSTAR_F) < TM_GELU_TAYLOR_WINDOW) return (float)tm_gelu_taylor(x);
-    return (float)tm_gelu_exact(x);
+    return tm_gelu_exact_call(x);
 }
 
 // Full forward for one element.
-__device__ __forceinline__ float tm_gelu_fwd(float x) {
+__device__ __forceinline__ float tm_gelu_fwd(float x, float xs_lo) {
     float y = tm_gelu_fast(x);
-    if (tm_gelu_needs_slow(x)) y = tm_gelu_slow(x);
+    if (tm_gelu_needs_fix(x, xs_lo)) y = tm_gelu_fix(x);
     return y;
 }

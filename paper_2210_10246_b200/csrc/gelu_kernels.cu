@@ -8,10 +8,13 @@
 //           table's piecewise Chebyshev series.
 //           HBM: read dy, y (8 B) + 1 bit, write dx (4 B) = 12.125 B/elem.
 //
-// Layout: a warp owns 128-element chunks (one float4 per lane, 128-bit
-// coalesced); the chunk's 4 mask words are packed with warp ballots.  A
-// ragged tail (< 128 elements) or unaligned pointers take the scalar path
-// (32 elements per warp step, one ballot = one mask word).
+// Layout: the forward's warp owns 256-element chunks (eight floats per lane,
+// one 256-bit LDG/STG, the lane's mask byte stored directly); the backward's
+// warp owns 128-element chunks (one float4 per lane).  A ragged tail or
+// unaligned pointers take the scalar path (32 elements per warp step, one
+// ballot = one mask word).
+#include <cmath>
+#include <limits>
 #include <type_traits>
 
 #include "common.cuh"
@@ -22,14 +25,26 @@
 namespace tb {
 namespace {
 
+#ifdef TM_GELU_FWD_MINB
+#define TM_GELU_FWD_BOUNDS __launch_bounds__(256, TM_GELU_FWD_MINB)
+#else
+#define TM_GELU_FWD_BOUNDS __launch_bounds__(256)
+#endif
+#ifndef TM_GELU_FWD_U8
+#define TM_GELU_FWD_U8 4
+#endif
+#ifndef TM_GELU_FWD_PP
+#define TM_GELU_FWD_PP 1
+#endif
 constexpr int kBlock = 256;
-constexpr int kUnroll = 4;  // chunks in flight per warp (forward)
+constexpr int kUnroll = 4;  // chunks in flight per warp (generic backward)
 
 // ---------------------------------------------------------------- forward
 __device__ __forceinline__ void gelu_fwd_scalar_words(const float* __restrict__ x,
                                                       float* __restrict__ y,
                                                       uint32_t* __restrict__ mask, int64_t n,
-                                                      float xstar_gt, int64_t w_begin,
+                                                      float xstar_gt, float xs_lo,
+                                                      int64_t w_begin,
                                                       int64_t w_step, int lane) {
     const int64_t nwords = (n + 31) >> 5;
     for (int64_t w = w_begin; w < nwords; w += w_step) {
@@ -38,122 +53,147 @@ __device__ __forceinline__ void gelu_fwd_scalar_words(const float* __restrict__ 
         float xv = in ? x[i] : 0.0f;
         bool m = in && (xv >= xstar_gt);
         uint32_t bits = __ballot_sync(kFull, m);
-        if (in) y[i] = tm_gelu_fwd(xv);
+        if (in) y[i] = tm_gelu_fwd(xv, xs_lo);
         if (lane == 0) mask[w] = bits;
     }
 }
 
-// Compute + store U chunks already loaded in v; fp64 fix-ups behind one vote.
+// ---- forward, 256-bit variant ---------------------------------------------
+// Chunk = 256 elements per warp step: lane L owns elements 8L..8L+7 (one
+// 32-byte LDG/STG.256) and therefore byte L of the chunk's 32-byte mask, so
+// the mask needs no cross-lane packing.  Per element, besides the fast-path
+// math (tm_gelu_fast2), one FADD2 gives d = xs_lo - x, whose sign bit IS the
+// mask bit (x > x*  <=>  x > xs_lo, the largest float <= x*; NaN gives a
+// positive canonical NaN, i.e. bit 0, as the reference's `x > x*`), and one
+// FFMA2 gives d*d - 2^-12, whose sign bit flags the fp64 window |x - x*| <
+// 1/64; both are collected with one funnel shift each.  The x < -13 tail
+// (and -inf) is caught by a running min and re-examined only in that rare
+// case.  Elements needing fp64 are fixed after the vector store by the
+// owning lane (same thread, same address: program order).
 template <int U>
-__device__ __forceinline__ void gelu_fwd_compute(const float4 (&v)[U], float4* __restrict__ y4,
-                                                 uint32_t* __restrict__ mask, int64_t c0,
-                                                 float xstar_gt, int lane, float* stage) {
-    float4 o[U];
-    uint32_t slow = 0;  // bit 4u+k: element k of chunk u needs an fp64 path
+__device__ __forceinline__ void gelu_fwd8_compute(const F8 (&v)[U], float* __restrict__ y,
+                                                  uint8_t* __restrict__ mask8, int64_t c0,
+                                                  float xs_lo, int lane, float* stage) {
+    const float2 XS = f2(xs_lo), NW = f2(-0.000244140625f);  // -(1/64)^2
+    uint32_t win = 0;  // bit 8u+k: element k of chunk u is in the fp64 window
+    float xmin = 0.0f;
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-        const float2 lo = tm_gelu_fast2(make_float2(v[u].x, v[u].y));
-        const float2 hi = tm_gelu_fast2(make_float2(v[u].z, v[u].w));
-        o[u] = make_float4(lo.x, lo.y, hi.x, hi.y);
-        slow |= (uint32_t)tm_gelu_needs_slow(v[u].x) << (4 * u);
-        slow |= (uint32_t)tm_gelu_needs_slow(v[u].y) << (4 * u + 1);
-        slow |= (uint32_t)tm_gelu_needs_slow(v[u].z) << (4 * u + 2);
-        slow |= (uint32_t)tm_gelu_needs_slow(v[u].w) << (4 * u + 3);
+    for (int u = U - 1; u >= 0; --u) {
+        F8 o;
+        uint32_t mb = 0;
+#pragma unroll
+        for (int k = 6; k >= 0; k -= 2) {
+            const float2 xx = make_float2(v[u].v[k], v[u].v[k + 1]);
+            const float2 r = tm_gelu_fast2(xx);
+            o.v[k] = r.x;
+            o.v[k + 1] = r.y;
+            const float2 d = __fadd2_rn(XS, neg2(xx));
+            const float2 w = __ffma2_rn(d, d, NW);
+            mb = push_sign(push_sign(mb, d.y), d.x);
+            win = push_sign(push_sign(win, w.y), w.x);
+            xmin = fminf(xmin, fminf(xx.x, xx.y));
+        }
+        const int64_t c = c0 + u;
+        st_stream8(y + (c << 8) + 8 * lane, o);
+        st_stream(mask8 + (c << 5) + lane, mb);
     }
-    if (__any_sync(kFull, slow != 0u)) {
-        // The fp64 window / tail elements (~1 % of N(0,1) inputs, but nearly
-        // every warp iteration has one): stage x and y in this warp's smem
-        // slice and let every lane with a pending element process its next
-        // one, so one pass of the fp64 code serves up to 32 elements.
-        float* xs = stage;           // [U*4][32]
-        float* ys = stage + U * 128; // [U*4][32]
+    if (xmin < TM_GELU_FAST_XMIN) {  // rare: x < -13 or -inf somewhere in this lane
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+                win |= (uint32_t)(v[u].v[k] < TM_GELU_FAST_XMIN) << (8 * u + k);
+    }
+    if (win != 0u) {
+        float4* xs = reinterpret_cast<float4*>(stage) + 2 * lane;  // [U][32 lanes][8]
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            xs[(4 * u + 0) * 32 + lane] = v[u].x;
-            xs[(4 * u + 1) * 32 + lane] = v[u].y;
-            xs[(4 * u + 2) * 32 + lane] = v[u].z;
-            xs[(4 * u + 3) * 32 + lane] = v[u].w;
-            ys[(4 * u + 0) * 32 + lane] = o[u].x;
-            ys[(4 * u + 1) * 32 + lane] = o[u].y;
-            ys[(4 * u + 2) * 32 + lane] = o[u].z;
-            ys[(4 * u + 3) * 32 + lane] = o[u].w;
+            xs[u * 64] = make_float4(v[u].v[0], v[u].v[1], v[u].v[2], v[u].v[3]);
+            xs[u * 64 + 1] = make_float4(v[u].v[4], v[u].v[5], v[u].v[6], v[u].v[7]);
         }
-        uint32_t pending = slow;
-        while (pending) {  // lane-divergent; the warp runs max(popc) passes
-            const int k = __ffs(pending) - 1;
-            pending &= pending - 1;
-            ys[k * 32 + lane] = tm_gelu_slow(xs[k * 32 + lane]);
-        }
-        __syncwarp();
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            o[u].x = ys[(4 * u + 0) * 32 + lane];
-            o[u].y = ys[(4 * u + 1) * 32 + lane];
-            o[u].z = ys[(4 * u + 2) * 32 + lane];
-            o[u].w = ys[(4 * u + 3) * 32 + lane];
-        }
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-        st_stream(y4 + ((c0 + u) << 5) + lane, o[u]);
-        store_chunk_mask(mask + ((c0 + u) << 2),
-                         nibble4(v[u].x >= xstar_gt, v[u].y >= xstar_gt, v[u].z >= xstar_gt,
-                                 v[u].w >= xstar_gt),
-                         lane);
+        const float* xsf = stage + 8 * lane;
+        float* yb = y + (c0 << 8) + 8 * lane;
+        do {
+            const int b = __ffs(win) - 1;
+            win &= win - 1;
+            const int off = (b >> 3) * 256 + (b & 7);
+            st_stream(yb + off, tm_gelu_fix(xsf[off]));
+        } while (win != 0u);
     }
 }
 
-__global__ void __launch_bounds__(kBlock) gelu_fwd_vec_kernel(const float* __restrict__ x,
-                                                              float* __restrict__ y,
-                                                              uint32_t* __restrict__ mask,
-                                                              int64_t n, float xstar_gt) {
-    __shared__ float stage_all[kBlock / 32][2 * kUnroll * 128];
+template <int U>
+__global__ void TM_GELU_FWD_BOUNDS gelu_fwd8_kernel(const float* __restrict__ x,
+                                                    float* __restrict__ y,
+                                                    uint32_t* __restrict__ mask, int64_t n,
+                                                    float xstar_gt, float xs_lo) {
+    __shared__ __align__(16) float stage_all[kBlock / 32][U * 256];
     const int lane = threadIdx.x & 31;
     float* stage = stage_all[threadIdx.x >> 5];
+    uint8_t* mask8 = reinterpret_cast<uint8_t*>(mask);
     const int64_t warp = ((int64_t)blockIdx.x * kBlock + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * kBlock) >> 5;
-    const int64_t nchunks = n >> 7;
-    const float4* x4 = reinterpret_cast<const float4*>(x);
-    float4* y4 = reinterpret_cast<float4*>(y);
-    // main loop: whole groups of kUnroll chunks (warp-uniform, no guards),
-    // the next group's loads issued before this group's math (register
-    // double buffering keeps HBM reads in flight through the compute)
-    const int64_t ngroups = nchunks / kUnroll;
-    float4 nxt[kUnroll];
+    const int64_t nchunks = n >> 8;
+    const int64_t ngroups = nchunks / U;
+#if TM_GELU_FWD_PP
+    // ping-pong register buffers: group gi computes from `a` while gi+nwarps
+    // loads into `b`, then the roles swap (no register copies)
+    F8 a[U], b[U];
     if (warp < ngroups) {
 #pragma unroll
-        for (int u = 0; u < kUnroll; ++u) nxt[u] = ld_stream(x4 + ((warp * kUnroll + u) << 5) + lane);
+        for (int u = 0; u < U; ++u) a[u] = ld_stream8(x + ((warp * U + u) << 8) + 8 * lane);
+    }
+    for (int64_t gi = warp; gi < ngroups; gi += 2 * nwarps) {
+        const int64_t g1 = gi + nwarps, g2 = gi + 2 * nwarps;
+        if (g1 < ngroups) {
+#pragma unroll
+            for (int u = 0; u < U; ++u) b[u] = ld_stream8(x + ((g1 * U + u) << 8) + 8 * lane);
+        }
+        gelu_fwd8_compute<U>(a, y, mask8, gi * U, xs_lo, lane, stage);
+        if (g1 >= ngroups) break;
+        if (g2 < ngroups) {
+#pragma unroll
+            for (int u = 0; u < U; ++u) a[u] = ld_stream8(x + ((g2 * U + u) << 8) + 8 * lane);
+        }
+        gelu_fwd8_compute<U>(b, y, mask8, g1 * U, xs_lo, lane, stage);
+    }
+#else
+    F8 nxt[U];
+    if (warp < ngroups) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) nxt[u] = ld_stream8(x + ((warp * U + u) << 8) + 8 * lane);
     }
     for (int64_t gi = warp; gi < ngroups; gi += nwarps) {
-        float4 v[kUnroll];
+        F8 v[U];
 #pragma unroll
-        for (int u = 0; u < kUnroll; ++u) v[u] = nxt[u];
+        for (int u = 0; u < U; ++u) v[u] = nxt[u];
         const int64_t gn = gi + nwarps;
         if (gn < ngroups) {
 #pragma unroll
-            for (int u = 0; u < kUnroll; ++u) nxt[u] = ld_stream(x4 + ((gn * kUnroll + u) << 5) + lane);
+            for (int u = 0; u < U; ++u) nxt[u] = ld_stream8(x + ((gn * U + u) << 8) + 8 * lane);
         }
-        gelu_fwd_compute<kUnroll>(v, y4, mask, gi * kUnroll, xstar_gt, lane, stage);
+        gelu_fwd8_compute<U>(v, y, mask8, gi * U, xs_lo, lane, stage);
     }
-    // leftover whole chunks, one per warp
-    for (int64_t c = ngroups * kUnroll + warp; c < nchunks; c += nwarps) {
-        float4 v[1] = {ld_stream(x4 + (c << 5) + lane)};
-        gelu_fwd_compute<1>(v, y4, mask, c, xstar_gt, lane, stage);
+#endif
+    for (int64_t c = ngroups * U + warp; c < nchunks; c += nwarps) {
+        F8 v[1] = {ld_stream8(x + (c << 8) + 8 * lane)};
+        gelu_fwd8_compute<1>(v, y, mask8, c, xs_lo, lane, stage);
     }
-    // Ragged tail: words [4*nchunks, ceil(n/32)) on the last warp.
+    // ragged tail: mask words [8*nchunks, ceil(n/32)) on the last warp
     if (warp == nwarps - 1) {
-        gelu_fwd_scalar_words(x, y, mask, n, xstar_gt, nchunks << 2, 1, lane);
+        gelu_fwd_scalar_words(x, y, mask, n, xstar_gt, xs_lo, nchunks << 3, 1, lane);
     }
 }
 
 __global__ void __launch_bounds__(kBlock) gelu_fwd_scalar_kernel(const float* __restrict__ x,
                                                                  float* __restrict__ y,
                                                                  uint32_t* __restrict__ mask,
-                                                                 int64_t n, float xstar_gt) {
+                                                                 int64_t n, float xstar_gt,
+                                                                 float xs_lo) {
     const int lane = threadIdx.x & 31;
     const int64_t warp = ((int64_t)blockIdx.x * kBlock + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * kBlock) >> 5;
-    gelu_fwd_scalar_words(x, y, mask, n, xstar_gt, warp, nwarps, lane);
+    gelu_fwd_scalar_words(x, y, mask, n, xstar_gt, xs_lo, warp, nwarps, lane);
 }
 
 // --------------------------------------------------------------- backward
@@ -476,20 +516,24 @@ __global__ void __launch_bounds__(kBlock) gelu_bwd_fast_kernel(
 }
 
 inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+inline bool aligned32(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 31u) == 0; }
 
 }  // namespace
 
 cudaError_t launch_gelu_fwd(const float* x, float* y, uint32_t* mask, int64_t n, float xstar_gt,
                             cudaStream_t st) {
     if (n == 0) return cudaSuccess;
-    const bool vec = aligned16(x) && aligned16(y) && aligned16(mask);
-    const void* k = vec ? (const void*)gelu_fwd_vec_kernel : (const void*)gelu_fwd_scalar_kernel;
-    const int64_t warps_needed = vec ? ((n >> 7) + kUnroll - 1) / kUnroll + 1 : (n + 31) >> 5;
-    int grid = grid_for(k, kBlock, 0, (warps_needed * 32 + kBlock - 1) / kBlock);
-    if (vec) {
-        gelu_fwd_vec_kernel<<<grid, kBlock, 0, st>>>(x, y, mask, n, xstar_gt);
+    const float xs_lo = std::nextafter(xstar_gt, -std::numeric_limits<float>::infinity());
+    if (aligned32(x) && aligned32(y) && aligned16(mask)) {
+        constexpr int U = TM_GELU_FWD_U8;
+        const int64_t warps_needed = ((n >> 8) + U - 1) / U + 1;
+        auto k = gelu_fwd8_kernel<U>;
+        int grid = grid_for((const void*)k, kBlock, 0, (warps_needed * 32 + kBlock - 1) / kBlock);
+        k<<<grid, kBlock, 0, st>>>(x, y, mask, n, xstar_gt, xs_lo);
     } else {
-        gelu_fwd_scalar_kernel<<<grid, kBlock, 0, st>>>(x, y, mask, n, xstar_gt);
+        int grid = grid_for((const void*)gelu_fwd_scalar_kernel, kBlock, 0,
+                            (((n + 31) >> 5) * 32 + kBlock - 1) / kBlock);
+        gelu_fwd_scalar_kernel<<<grid, kBlock, 0, st>>>(x, y, mask, n, xstar_gt, xs_lo);
     }
     return cudaGetLastError();
 }

@@ -32,10 +32,11 @@ __global__ void sweep(unsigned long long begin, unsigned long long end) {
          u < end; u += (unsigned long long)gridDim.x * blockDim.x) {
         float x = __uint_as_float((unsigned int)u);
         // exactly the kernel's per-element logic: the packed fp32x2 fast path
-        // (lane .x of a pair), fp64 where tm_gelu_needs_slow says so
+        // (lane .x of a pair), fp64 where tm_gelu_needs_fix says so
         float got = tm_gelu_fast2(make_float2(x, 1.0f)).x;
-        if (tm_gelu_needs_slow(x)) got = tm_gelu_slow(x);
-        if (got != tm_gelu_fwd(x) && !(isnan(got) && isnan(tm_gelu_fwd(x)))) ++nanbad;  // scalar path must agree
+        if (tm_gelu_needs_fix(x, TM_GELU_XSTAR_F)) got = tm_gelu_fix(x);
+        const float sc = tm_gelu_fwd(x, TM_GELU_XSTAR_F);
+        if (got != sc && !(isnan(got) && isnan(sc))) ++nanbad;  // scalar path must agree
         float ref = (float)tm_gelu_exact(x);
         if (isnan(ref) || isnan(got)) {
             nanbad += (isnan(ref) != isnan(got));

@@ -1,0 +1,79 @@
+"""A/B timing of single ops at the bench shapes (not part of the contract).
+
+  TEMPO_B200_LIB=_ab/X/libtempo_b200.so python tools/ab_time.py gelu_fwd ln_fwd ...
+
+Prints one line per op: median device time over reps (CUDA events on the
+launching stream, L2 flushed by a 1 GB fill before every rep so the GPU is
+busy while Python issues the launch), algorithmic GB/s, fraction of the
+measured HBM peak, and a checksum of the outputs (to spot A/B differences).
+"""
+import hashlib
+import json
+import os
+import statistics
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    import torch
+    from paper_2210_10246_b200 import ops
+    import bench
+
+    dev = torch.device("cuda:0")
+    peak, _ = bench.peaks()
+    chain = bench.Chain(dev, 0, 1)
+    chain.step()
+    torch.cuda.synchronize()
+    fb = torch.empty(256 * 1024 * 1024, device=dev)
+    flush = lambda: fb.fill_(0.0)  # noqa: E731
+    H, T = bench.H, bench.T
+    dp = chain.dparams
+    o = ops
+    c = chain
+    calls = {
+        "softmax_dropout_fwd": (lambda: o.softmax_dropout_fwd(c.z, bench.P_DROP, mask=c.m_att, generate=True, seed=7, P=c.P, D=c.D), [c.P, c.D, c.m_att]),
+        "attn_probs_bwd": (lambda: o.attn_probs_bwd(c.dD, c.P, c.m_att, bench.P_DROP, write_d=True, dZ=c.dZ, D=c.Drec), [c.dZ, c.Drec]),
+        "gelu_fwd": (lambda: o.gelu_ip_fwd(c.x_ffn1, c.table, y=c.y_g, mask=c.m_g), [c.y_g, c.m_g]),
+        "gelu_bwd": (lambda: o.gelu_ip_bwd(c.dy_gelu, c.y_g, c.m_g, c.table, dx=c.dx_g), [c.dx_g]),
+        "ln_fwd": (lambda: o.layernorm_ip_fwd(c.d1, c.g1, c.b1, check_gamma=False, y=c.y_ln1, rstd=c.rs1), [c.y_ln1, c.rs1]),
+        "ln_bwd": (lambda: o.layernorm_ip_bwd(c.dy_ln1, c.y_ln1, c.rs1, c.g1, c.b1, dx=c.dx_ln1, dgamma=dp[:H], dbeta=dp[H:2 * H], workspace=c.ws), [c.dx_ln1, dp[:2 * H]]),
+        "dropout_fwd": (lambda: o.dropout_fwd(c.x_ffn2, bench.P_DROP, mask=c.m2, generate=True, seed=9, y=c.d2), [c.d2, c.m2]),
+        "copy_g": (lambda: c.y_g.copy_(c.x_ffn1), [c.y_g[:1]]),
+        "copy_h": (lambda: c.d2.copy_(c.x_ffn2), [c.d2[:1]]),
+        "dropout_bwd": (lambda: o.dropout_bwd(c.dx_ln2, c.m2, bench.P_DROP, dx=c.dx_d2), [c.dx_d2]),
+    }
+    ob = bench.op_bytes()
+    ob["copy_g"] = 8 * c.x_ffn1.numel()
+    ob["copy_h"] = 2 * 8 * c.x_ffn2.numel()
+    names = {"ln_fwd": "layernorm_fwd", "ln_bwd": "layernorm_bwd"}
+    reps = int(os.environ.get("REPS", "20"))
+    st = torch.cuda.current_stream()
+    for name in sys.argv[1:]:
+        fn, outs = calls[name]
+        fn()
+        ts = []
+        for _ in range(reps):
+            flush()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(st)
+            fn()
+            b.record(st)
+            b.synchronize()
+            ts.append(a.elapsed_time(b))
+        t = statistics.median(ts)
+        key = names.get(name, name)
+        nbytes = ob[key] / (2 if key in ("layernorm_fwd", "layernorm_bwd", "dropout_fwd", "dropout_bwd", "copy_h") else 1)
+        h = hashlib.sha1()
+        for t_ in outs:
+            h.update(t_.detach().cpu().numpy().tobytes())
+        print(json.dumps({"op": name, "lib": os.environ.get("TEMPO_B200_LIB", "default"),
+                          "us": round(t * 1e3, 2), "min_us": round(min(ts) * 1e3, 2),
+                          "gbs": round(nbytes / t / 1e6, 1), "frac": round(nbytes / t / 1e6 / peak, 4),
+                          "sha": h.hexdigest()[:12]}), flush=True)
+
+
+if __name__ == "__main__":
+    main()
