@@ -54,6 +54,11 @@ __device__ __forceinline__ void st_stream8(float* p, const F8& r) {
 __device__ __forceinline__ void st_stream(uint8_t* p, uint32_t v) {
     asm volatile("st.global.cs.u8 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+__device__ __forceinline__ uint32_t ld_byte(const uint8_t* p) {
+    uint16_t v;
+    asm volatile("ld.global.nc.L1::no_allocate.u8 %0, [%1];" : "=h"(v) : "l"(p));
+    return v;
+}
 // (acc << 1) | sign(v): one funnel shift collects a sign bit.
 __device__ __forceinline__ uint32_t push_sign(uint32_t acc, float v) {
     return __funnelshift_l(__float_as_uint(v), acc, 1);

@@ -350,8 +350,10 @@ struct FastTable {
 };
 
 __device__ __forceinline__ float sqrt_approx(float v) {
+    // .ftz: d = y - y_min below 2^-126 flushes to 0 (u ~ 1e-19 either way,
+    // far below the evaluation tolerance) and saves the denormal rescaling
     float r;
-    asm("sqrt.approx.f32 %0, %1;" : "=f"(r) : "f"(v));
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(v));
     return r;
 }
 // NaN-propagating min/max (PTX min/max.NaN): a NaN output y flows through
@@ -419,7 +421,13 @@ __device__ __forceinline__ float gelu_h_fast(float y, uint32_t m, const FastTabl
     return fmaf(tt, b1, c[0] - b2);
 }
 
-template <int NC4, bool HORNER>
+#ifndef TM_GELU_BWD_V8
+#define TM_GELU_BWD_V8 1
+#endif
+#ifndef TM_GELU_BWD_U8
+#define TM_GELU_BWD_U8 2
+#endif
+template <int NC4, bool HORNER, bool V8>
 __global__ void __launch_bounds__(kBlock) gelu_bwd_fast_kernel(
     const float* __restrict__ dy, const float* __restrict__ y, const uint32_t* __restrict__ mask,
     float* __restrict__ dx, int64_t n, const __grid_constant__ GeluDevTable t) {
@@ -447,6 +455,7 @@ __global__ void __launch_bounds__(kBlock) gelu_bwd_fast_kernel(
         thr1[k] = k + 1 < t.nseg[1] ? t.lo_up[t.nseg[0] + k + 1] : __int_as_float(0x7fffffff);
     }
     for (int i = 0; i < nseg; ++i) sqrt_mask |= (t.sqrt_shift[i] ? 1u : 0u) << i;
+
     const int base1 = t.nseg[0];
     const float ymin_hi = t.ymin_hi, ymin_lo = t.ymin_lo;
     __syncthreads();
@@ -454,6 +463,55 @@ __global__ void __launch_bounds__(kBlock) gelu_bwd_fast_kernel(
     const int lane = threadIdx.x & 31;
     const int64_t warp = ((int64_t)blockIdx.x * kBlock + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * kBlock) >> 5;
+#define TB_H(val, m) gelu_h_fast<NC4, HORNER>(val, m, ft, thr0, thr1, base1, sqrt_mask, \
+                                              ymin_hi, ymin_lo)
+    if constexpr (V8) {
+        // 256-element chunks: lane L owns elements 8L..8L+7 (one 32-byte
+        // vector of y, of dy and of dx) and reads its own mask byte.
+        constexpr int U = TM_GELU_BWD_U8;
+        const uint8_t* mask8 = reinterpret_cast<const uint8_t*>(mask);
+        const int64_t nchunks = n >> 8;
+        const int64_t ngroups = nchunks / U;
+        struct Group {
+            F8 g[U], v[U];
+            uint32_t mb[U];
+        };
+        auto load = [&](Group& G, int64_t c0) {
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int64_t off = ((c0 + u) << 8) + 8 * lane;
+                G.v[u] = ld_stream8(y + off);
+                G.g[u] = ld_stream8(dy + off);
+                G.mb[u] = ld_byte(mask8 + ((c0 + u) << 5) + lane);
+            }
+        };
+        auto compute = [&](const Group& G, int64_t c0) {
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                F8 o;
+#pragma unroll
+                for (int k = 0; k < 8; ++k) o.v[k] = G.g[u].v[k] * TB_H(G.v[u].v[k], (G.mb[u] >> k) & 1u);
+                st_stream8(dx + ((c0 + u) << 8) + 8 * lane, o);
+            }
+        };
+        Group a, b;  // ping-pong register buffers
+        if (warp < ngroups) load(a, warp * U);
+        for (int64_t gi = warp; gi < ngroups; gi += 2 * nwarps) {
+            const int64_t g1 = gi + nwarps, g2 = gi + 2 * nwarps;
+            if (g1 < ngroups) load(b, g1 * U);
+            compute(a, gi * U);
+            if (g1 >= ngroups) break;
+            if (g2 < ngroups) load(a, g2 * U);
+            compute(b, g1 * U);
+        }
+        // leftover chunks and the ragged tail (< 256 elements): scalar
+        for (int64_t i = ((ngroups * U) << 8) + warp * 32 + lane; i < n; i += nwarps * 32) {
+            const uint32_t m = (mask[i >> 5] >> (i & 31)) & 1u;
+            dx[i] = dy[i] * TB_H(y[i], m);
+        }
+        return;
+    }
+#undef TB_H
     const int64_t nchunks = n >> 7;
     const float4* dy4 = reinterpret_cast<const float4*>(dy);
     const float4* y4 = reinterpret_cast<const float4*>(y);
@@ -546,10 +604,14 @@ cudaError_t launch_gelu_bwd(const float* dy, const float* y, const uint32_t* mas
                       t.ncoef <= 16;
     if (fast) {
         const int nc4 = (t.ncoef + 3) / 4;
+        const bool v8 = TM_GELU_BWD_V8 && aligned32(dy) && aligned32(y) && aligned32(dx);
         const int64_t blocks = ((n >> 7) / 2 + 1) * 32 / kBlock + 1;
 #define TB_CASE(NC)                                                                       \
     case NC: {                                                                            \
-        auto k = t.horner ? gelu_bwd_fast_kernel<NC, true> : gelu_bwd_fast_kernel<NC, false>; \
+        auto k = v8 ? (t.horner ? gelu_bwd_fast_kernel<NC, true, true>                      \
+                            : gelu_bwd_fast_kernel<NC, false, true>)                     \
+                    : (t.horner ? gelu_bwd_fast_kernel<NC, true, false>                  \
+                                : gelu_bwd_fast_kernel<NC, false, false>);               \
         int grid = grid_for((const void*)k, kBlock, 0, blocks);                           \
         k<<<grid, kBlock, 0, st>>>(dy, y, mask, dx, n, t);                                \
         break;                                                                            \
