@@ -181,6 +181,18 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
         : "memory");
 }
 
+// ---- programmatic dependent launch (PDL) --------------------------------
+// A kernel launched with the programmatic-stream-serialization attribute may
+// start while its predecessor drains; it must call grid_dep_wait() before
+// touching the predecessor's outputs (waits for its completion + memory
+// flush).  grid_dep_launch() lets the dependent grid launch early.
+__device__ __forceinline__ void grid_dep_wait() {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+__device__ __forceinline__ void grid_dep_launch() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 // ---- warp reductions -----------------------------------------------------
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll

@@ -30,7 +30,14 @@ namespace tb {
 namespace {
 
 constexpr int kRows = 4;           // rows in flight per CTA iteration (forward)
-constexpr int kRowsB = 2;          // rows in flight per CTA iteration (backward)
+#ifndef TM_LN_BWD_ROWS
+#define TM_LN_BWD_ROWS 4
+#endif
+#ifndef TM_LN_BWD_STAGES
+#define TM_LN_BWD_STAGES 3
+#endif
+constexpr int kRowsB = TM_LN_BWD_ROWS;  // rows per CTA iteration (backward)
+constexpr int kStagesB = TM_LN_BWD_STAGES;
 constexpr int kMaxThreads = 512;  // cols <= 2048 on the vector path
 constexpr double kGammaMin = 1e-12;  // ops_tempo.hpp:46
 
@@ -319,6 +326,7 @@ __global__ void __launch_bounds__(NT) ln_bwd_vec_kernel(
     // Thread t owns the CPT float4 column groups t, t + blockDim, ... of every
     // row (conflict-free 128-bit smem reads, coalesced stores); more columns
     // per thread amortise the per-row block reduction.
+    grid_dep_launch();  // let stage 2 (PDL) get launched; it waits for us to finish
     extern __shared__ __align__(128) unsigned char dsm[];
     uint64_t* full = reinterpret_cast<uint64_t*>(dsm);
     float* ring = reinterpret_cast<float*>(dsm + 128);
@@ -327,7 +335,7 @@ __global__ void __launch_bounds__(NT) ln_bwd_vec_kernel(
     const int tile_floats = kRowsB * cols;  // per tensor; a stage holds dy then y
     const int64_t ntiles = (rows + kRowsB - 1) / kRowsB;
     if (threadIdx.x == 0) {
-        for (int s = 0; s < kStages; ++s) mbar_init(&full[s], 1);
+        for (int s = 0; s < kStagesB; ++s) mbar_init(&full[s], 1);
         mbar_fence_init();
     }
     __syncthreads();
@@ -340,7 +348,7 @@ __global__ void __launch_bounds__(NT) ln_bwd_vec_kernel(
         bulk_g2s(ring + (2 * s + 1) * tile_floats, y + r0 * cols, bytes, &full[s]);
     };
     if (threadIdx.x == 0) {
-        for (int s = 0; s < kStages; ++s) {
+        for (int s = 0; s < kStagesB; ++s) {
             const int64_t t = blockIdx.x + (int64_t)s * gridDim.x;
             if (t < ntiles) issue(t, s);
         }
@@ -375,8 +383,8 @@ __global__ void __launch_bounds__(NT) ln_bwd_vec_kernel(
     const float inv_m = 1.0f / (float)cols;
     int it = 0;
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
-        const int st = it % kStages;
-        mbar_wait(&full[st], (uint32_t)((it / kStages) & 1));
+        const int st = it % kStagesB;
+        mbar_wait(&full[st], (uint32_t)((it / kStagesB) & 1));
         const int64_t r0 = tile * kRowsB;
         const float* gs = ring + (2 * st) * tile_floats;
         const float* ys = ring + (2 * st + 1) * tile_floats;
@@ -416,7 +424,7 @@ __global__ void __launch_bounds__(NT) ln_bwd_vec_kernel(
         }
         block_sum<2 * kRowsB>(s, red, phase);
         if (threadIdx.x == 0) {  // stage consumed by every thread: refill
-            const int64_t nt = tile + (int64_t)kStages * gridDim.x;
+            const int64_t nt = tile + (int64_t)kStagesB * gridDim.x;
             if (nt < ntiles) {
                 fence_proxy_async_smem();
                 issue(nt, st);
@@ -466,6 +474,7 @@ __global__ void __launch_bounds__(256) ln_bwd_generic_kernel(
     const float* __restrict__ dy, const float* __restrict__ y, const float* __restrict__ rstd,
     const float* __restrict__ gamma, const float* __restrict__ beta, float* __restrict__ dx,
     double* __restrict__ ws, int64_t rows, int cols) {
+    grid_dep_launch();
     extern __shared__ double part[];  // [2][cols]
     __shared__ double red[2 * 2 * 32];
     int phase = 0;
@@ -498,26 +507,40 @@ __global__ void __launch_bounds__(256) ln_bwd_generic_kernel(
 
 // Stage 2: out[j] = sum over CTAs c (fixed order) of ws[c][j], j < 2*cols.
 // A 32 x 32 block: column lane tx owns output j0 + tx, slice ty sums the
-// partial rows c = ty, ty + 32, ... (coalesced 256-byte rows, ~nparts/32
-// independent loads per thread); the 32 slices are then added in a fixed
-// order by ty == 0 -- bitwise reproducible.
+// partial rows c = ty, ty + 32, ... (coalesced 256-byte rows); all of a
+// slice's loads are issued before the first add (up to 16 in registers), and
+// the 32 slices are then added in a fixed order by ty == 0 -- bitwise
+// reproducible.  Launched as a programmatic dependent of stage 1 (PDL): the
+// launch overlaps stage 1's tail and griddepcontrol.wait orders the reads.
 __global__ void __launch_bounds__(1024) ln_param_reduce_kernel(const double* __restrict__ ws,
                                                                int nparts, int cols,
                                                                float* __restrict__ dgamma,
                                                                float* __restrict__ dbeta) {
+    grid_dep_wait();
     __shared__ double part[32][33];
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
     const int64_t total = 2 * (int64_t)cols;
     const int64_t j = (int64_t)blockIdx.x * 32 + tx;
     double acc = 0.0;
     if (j < total) {
-#pragma unroll 4
-        for (int c = ty; c < nparts; c += 32) acc += ws[(size_t)c * total + j];
+        constexpr int L = 16;
+        int c0 = ty;
+        for (; c0 < nparts; c0 += 32 * L) {
+            double a[L];
+#pragma unroll
+            for (int l = 0; l < L; ++l) {
+                const int c = c0 + 32 * l;
+                a[l] = c < nparts ? ws[(size_t)c * total + j] : 0.0;
+            }
+#pragma unroll
+            for (int l = 0; l < L; ++l) acc += a[l];  // adding +0.0 past the end is exact
+        }
     }
     part[ty][tx] = acc;
     __syncthreads();
     if (ty == 0 && j < total) {
         double v = 0.0;
+#pragma unroll
         for (int k = 0; k < 32; ++k) v += part[k][tx];
         if (j < cols) dgamma[j] = (float)v; else dbeta[j - cols] = (float)v;
     }
@@ -533,7 +556,7 @@ bool use_vec(int64_t cols, const void* a, const void* b, const void* c, const vo
 
 int vec_threads(int64_t cols) { return (int)(((cols / 4) + 31) / 32 * 32); }
 // backward: two float4 column groups per thread when cols % 8 == 0
-int bwd_cpt(int64_t) { return 1; }  // 2 columns groups/thread measured slower (r1)
+int bwd_cpt(int64_t) { return 1; }  // 2 column groups/thread measured slower (r1)
 int bwd_threads(int64_t cols) {
     return (int)(((cols / 4 + bwd_cpt(cols) - 1) / bwd_cpt(cols) + 31) / 32 * 32);
 }
@@ -549,7 +572,7 @@ const void* bwd_vec_fn(int64_t cols) {
 // Stage-1 grid for the backward: its CTA count is also the number of
 // partial rows in the workspace, so it depends only on (rows, cols, device).
 size_t fwd_smem(int64_t cols) { return 128 + (size_t)kStages * kRows * cols * sizeof(float); }
-size_t bwd_smem(int64_t cols) { return 128 + (size_t)kStages * 2 * kRowsB * cols * sizeof(float); }
+size_t bwd_smem(int64_t cols) { return 128 + (size_t)kStagesB * 2 * kRowsB * cols * sizeof(float); }
 
 int bwd_grid(int64_t rows, int64_t cols, bool vec) {
     int64_t work = vec ? (rows + kRowsB - 1) / kRowsB : rows;
@@ -633,8 +656,8 @@ cudaError_t launch_ln_bwd(const float* dy, const float* y, const float* rstd, co
                                                        (int)cols);
     }
     const int rgrid = (int)((2 * cols + 31) / 32);
-    ln_param_reduce_kernel<<<rgrid, 1024, 0, st>>>(w, grid, (int)cols, dgamma, dbeta);
-    return cudaGetLastError();
+    return launch_pdl((const void*)ln_param_reduce_kernel, rgrid, 1024, 0, st,
+                      (const double*)w, grid, (int)cols, dgamma, dbeta);
 }
 
 }  // namespace tb

@@ -72,7 +72,29 @@ cudaError_t launch_mask_pack(const uint8_t* bytes, uint32_t* bits, int64_t n, in
 cudaError_t launch_mask_unpack(const uint32_t* bits, uint8_t* bytes, int64_t n, cudaStream_t st);
 cudaError_t launch_add(const float* a, const float* b, float* out, int64_t n, cudaStream_t st);
 
+// Launch `kernel` as a programmatic dependent of the previous work on the
+// stream (PDL, cudaLaunchAttributeProgrammaticStreamSerialization): its
+// launch overlaps the predecessor's tail; the kernel itself must call
+// grid_dep_wait() before reading the predecessor's outputs.
+template <typename... Args>
+cudaError_t launch_pdl(const void* kernel, int grid, int block, size_t smem, cudaStream_t st,
+                       Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3((unsigned)block);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    void* argv[] = {(void*)&args...};
+    return cudaLaunchKernelExC(&cfg, kernel, argv);
+}
+
 // Persistent-grid sizing: SM count x resident CTAs per SM (cached per device).
-int grid_for(const void* kernel, int block, size_t smem, int64_t work_items);
+// cap_per_sm > 0 limits the CTAs per SM (fewer, longer-lived CTAs).
+int grid_for(const void* kernel, int block, size_t smem, int64_t work_items, int cap_per_sm = 0);
 
 }  // namespace tb

@@ -67,12 +67,15 @@ def main():
         key = names.get(name, name)
         nbytes = ob[key] / (2 if key in ("layernorm_fwd", "layernorm_bwd", "dropout_fwd", "dropout_bwd", "copy_h") else 1)
         h = hashlib.sha1()
+        parts = []
         for t_ in outs:
-            h.update(t_.detach().cpu().numpy().tobytes())
+            b_ = t_.detach().cpu().numpy().tobytes()
+            h.update(b_)
+            parts.append(hashlib.sha1(b_).hexdigest()[:6])
         print(json.dumps({"op": name, "lib": os.environ.get("TEMPO_B200_LIB", "default"),
                           "us": round(t * 1e3, 2), "min_us": round(min(ts) * 1e3, 2),
                           "gbs": round(nbytes / t / 1e6, 1), "frac": round(nbytes / t / 1e6 / peak, 4),
-                          "sha": h.hexdigest()[:12]}), flush=True)
+                          "sha": h.hexdigest()[:12], "parts": parts}), flush=True)
 
 
 if __name__ == "__main__":
