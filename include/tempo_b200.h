@@ -192,6 +192,22 @@ int tempo_mask_unpack(const uint32_t* bits, uint8_t* bytes, int64_t n, tempo_str
  * std::mt19937_64 + uniform_real_distribution<double>, keep <=> u >= p).
  * bits has ceil(n/32) words. */
 int tempo_bernoulli_keep_bits_host(int64_t n, double p, uint64_t seed, uint32_t* bits);
+/* The same stream generated ON THE DEVICE, bit for bit: the keep bits of
+ * elements [offset, offset + n) of BoolMask::bernoulli_keep(shape, p, seed)
+ * (for any shape with at least offset + n elements) into ceil(n/32) words at
+ * `bits` (device).  The std::mt19937_64 stream is cut into 2^18-output
+ * chunks whose states are reached by GF(2) jump-ahead (x^J mod the
+ * characteristic polynomial); row shards pass their global offset.
+ * offset % 32 != 0 or p not in [0,1) -> TEMPO_ERR_PARAM.  The workspace
+ * (device, size from the query) holds the chunk states; the jump polynomials
+ * are computed once per process (~1 s) and uploaded once per device. */
+size_t tempo_bernoulli_keep_bits_workspace_size(uint64_t offset, int64_t n);
+int tempo_bernoulli_keep_bits(int64_t n, double p, uint64_t seed, uint64_t offset,
+                              uint32_t* bits, void* workspace, size_t workspace_bytes,
+                              tempo_stream_t stream);
+/* Host reference of the jump construction (test helper): `count` outputs of
+ * std::mt19937_64(seed) after discard(steps), via x^steps mod P.  0 = ok. */
+int tempo_mt_outputs_after_host(uint64_t seed, uint64_t steps, int64_t count, uint64_t* out);
 /* encoder::mask_stream_seed (encoder.cpp:39-46). */
 uint64_t tempo_mask_stream_seed(uint64_t mask_seed, uint64_t salt, int site);
 

@@ -667,6 +667,30 @@ int tempo_bernoulli_keep_bits_host(int64_t n, double p, uint64_t seed, uint32_t*
     return TEMPO_OK;
 }
 
+size_t tempo_bernoulli_keep_bits_workspace_size(uint64_t offset, int64_t n) {
+    return n > 0 ? tb::mt_keep_workspace(offset, n) : 0;
+}
+
+int tempo_bernoulli_keep_bits(int64_t n, double p, uint64_t seed, uint64_t offset,
+                              uint32_t* bits, void* workspace, size_t workspace_bytes,
+                              tempo_stream_t stream) {
+    if (int rc = check_n(n, "mask")) return rc;
+    if (!(p >= 0.0) || p >= 1.0)  // tensor.cpp:188-191
+        return fail(TEMPO_ERR_PARAM,
+                    "drop probability must lie in [0, 1), got " + std::to_string(p));
+    if (offset % 32 != 0)
+        return fail(TEMPO_ERR_PARAM, "offset must be a multiple of 32 (whole mask words)");
+    if (n == 0) return TEMPO_OK;
+    if (!bits) return fail(TEMPO_ERR_PARAM, "null mask");
+    const size_t need = tb::mt_keep_workspace(offset, n);
+    if (workspace_bytes < need || (need && !workspace))
+        return fail(TEMPO_ERR_PARAM, "workspace too small: need " + std::to_string(need) +
+                                         " bytes");
+    return cuda_status(tb::launch_mt_keep_bits(seed, p, offset, n, bits, workspace,
+                                               workspace_bytes, S(stream)),
+                       "tempo_bernoulli_keep_bits");
+}
+
 uint64_t tempo_mask_stream_seed(uint64_t mask_seed, uint64_t salt, int site) {
     // encoder.cpp:39-46 (splitmix64 over a site-salted input)
     uint64_t z = mask_seed + 0x9E3779B97F4A7C15ull * (salt * 3 + (uint64_t)site + 1);

@@ -1,0 +1,46 @@
+// mt19937.h -- std::mt19937_64 (the reference's mask engine, tensor.cpp:197)
+// pieces shared by the host jump-ahead code and the device generator.
+#pragma once
+
+#include <stdint.h>
+
+#ifdef __CUDACC__
+#define TB_HD __host__ __device__ __forceinline__
+#else
+#define TB_HD inline
+#endif
+
+namespace tb {
+
+constexpr unsigned kMtN = 312;                  // state words
+constexpr int kMtDeg = 19937;                   // degree of the characteristic polynomial
+constexpr int kMtPolyWords = (kMtDeg + 63) / 64;  // 312 words per jump polynomial
+constexpr int kMtBaseWords = kMtDeg - 1 + kMtN;   // windows i <= 19936 of 312 words
+constexpr int64_t kMtChunk = int64_t(1) << 18;  // outputs per device stream
+constexpr int kMtLevels = 4;                    // 32^4 streams of kMtChunk: 2^38 outputs
+
+// w_{j} from w_{j-312}, w_{j-311}, w_{j-156} (mersenne_twister_engine::_M_gen_rand:
+// upper 33 bits of w_{j-312}, lower 31 of w_{j-311}, twisted, xor w_{j-156}).
+TB_HD uint64_t mt_next_word(uint64_t a, uint64_t b, uint64_t c) {
+    const uint64_t y = (a & 0xFFFFFFFF80000000ull) | (b & 0x7FFFFFFFull);
+    return c ^ (y >> 1) ^ ((y & 1u) ? 0xB5026F5AA96619E9ull : 0ull);
+}
+
+// Tempering of an output word (u=29 d=0x5555.. s=17 b t=37 c l=43).
+TB_HD uint64_t mt_temper(uint64_t z) {
+    z ^= (z >> 29) & 0x5555555555555555ull;
+    z ^= (z << 17) & 0x71D67FFFEDA60000ull;
+    z ^= (z << 37) & 0xFFF7EEE000000000ull;
+    z ^= z >> 43;
+    return z;
+}
+
+// Host only.
+void mt_seed_state(uint64_t seed, uint64_t* st312);
+// Jump polynomials x^(d * 32^l * kMtChunk) mod P, layout [l][d-1][kMtPolyWords]
+// (computed once per process; nullptr if the construction failed).
+const uint64_t* mt_jump_polys();
+// Smallest 64-bit output x that the reference keeps at drop probability p.
+uint64_t mt_keep_threshold(double p);
+
+}  // namespace tb

@@ -93,6 +93,12 @@ cudaError_t launch_pdl(const void* kernel, int grid, int block, size_t smem, cud
     return cudaLaunchKernelExC(&cfg, kernel, argv);
 }
 
+// The reference's mask stream (std::mt19937_64, tensor.cpp:186-203) on the
+// device: keep bits of elements [e_begin, e_begin + n), e_begin % 32 == 0.
+size_t mt_keep_workspace(uint64_t e_begin, int64_t n);
+cudaError_t launch_mt_keep_bits(uint64_t seed, double p, uint64_t e_begin, int64_t n,
+                                uint32_t* mask, void* ws, size_t ws_bytes, cudaStream_t st);
+
 // Persistent-grid sizing: SM count x resident CTAs per SM (cached per device).
 // cap_per_sm > 0 limits the CTAs per SM (fewer, longer-lived CTAs).
 int grid_for(const void* kernel, int block, size_t smem, int64_t work_items, int cap_per_sm = 0);

@@ -24,7 +24,8 @@ __all__ = [
     "GeluTable", "TempoError", "gelu_ip_fwd", "gelu_ip_bwd", "layernorm_ip_fwd",
     "layernorm_ip_bwd", "ln_check_gamma", "softmax_ip_fwd", "softmax_ip_bwd",
     "softmax_dropout_fwd", "attn_probs_bwd", "dropout_fwd", "dropout_bwd", "mask_words",
-    "pack_mask", "unpack_mask", "bernoulli_keep_bits", "mask_stream_seed",
+    "pack_mask", "unpack_mask", "bernoulli_keep_bits", "bernoulli_keep_bits_device",
+    "mt_outputs_after", "mask_stream_seed",
     "layer_stash_bytes_per_token", "MASK_SUPPLIED", "MASK_PHILOX",
 ]
 
@@ -308,6 +309,31 @@ def bernoulli_keep_bits(n: int, p: float, seed: int):
     import numpy as np
     out = np.zeros(mask_words(n), np.uint32)
     check(lib().tempo_bernoulli_keep_bits_host(int(n), float(p), int(seed), out.ctypes.data))
+    return out
+
+
+def bernoulli_keep_bits_device(n: int, p: float, seed: int, offset: int = 0,
+                               out: Optional[torch.Tensor] = None,
+                               device: Optional[torch.device] = None) -> torch.Tensor:
+    """The same BoolMask::bernoulli_keep stream generated on the device (bit
+    for bit, by jump-ahead): keep bits of elements [offset, offset + n) as
+    ceil(n/32) int32 words.  offset must be a multiple of 32."""
+    dev = device or (out.device if out is not None else torch.device("cuda", torch.cuda.current_device()))
+    if out is None:
+        out = torch.empty(mask_words(n), dtype=torch.int32, device=dev)
+    nbytes = int(lib().tempo_bernoulli_keep_bits_workspace_size(int(offset), int(n)))
+    ws = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=dev)
+    check(lib().tempo_bernoulli_keep_bits(int(n), float(p), int(seed), int(offset), _ptr(out),
+                                          _ptr(ws), nbytes, _stream()))
+    return out
+
+
+def mt_outputs_after(seed: int, steps: int, count: int):
+    """Host reference of the jump-ahead: `count` outputs of
+    std::mt19937_64(seed) after discard(steps) (numpy uint64)."""
+    import numpy as np
+    out = np.zeros(int(count), np.uint64)
+    check(lib().tempo_mt_outputs_after_host(int(seed), int(steps), int(count), out.ctypes.data))
     return out
 
 
