@@ -62,39 +62,53 @@ __global__ void __launch_bounds__(kGenThreads) mt_base_kernel(const uint64_t* __
     }
 }
 
-// Children states: out[(s * 32 + d) * 312 + j] for d in [d_lo, d_hi]
-// (d = 0: the source itself).  polys: this level's 31 polynomials.
+// Children states: child c = child0 + s * 32 + d (d = 0: the source itself),
+// stored at out[(c - child_lo) * 312] for c in [child_lo, child_hi].  The
+// 312 polynomial words are split over kJumpParts CTAs (grid.x); each stages
+// only the slice of the sequence its words touch in smem, accumulates the
+// windows of its set bits (64 predicated loads per word, no serial bit
+// scan) and XORs its partial state into the zeroed output.
+constexpr int kJumpParts = 8;
+constexpr int kJumpWordsPerPart = (kMtPolyWords + kJumpParts - 1) / kJumpParts;
+constexpr int kJumpSlice = 64 * kJumpWordsPerPart + kMtN;  // staged words per CTA
+
 __global__ void __launch_bounds__(kJumpThreads) mt_jump_kernel(const uint64_t* __restrict__ base,
                                                                const uint64_t* __restrict__ polys,
                                                                uint64_t* __restrict__ out,
                                                                int64_t child0, int64_t child_lo,
                                                                int64_t child_hi) {
-    extern __shared__ uint64_t sbase[];  // kMtBaseWords
-    const int s = blockIdx.x, d = blockIdx.y;
+    __shared__ uint64_t slice[kJumpSlice];
+    const int part = blockIdx.x, d = blockIdx.y, s = blockIdx.z;
     const int64_t child = child0 + (int64_t)s * 32 + d;
     if (child < child_lo || child > child_hi) return;  // not needed
     const uint64_t* b = base + (size_t)s * kMtBaseWords;
     uint64_t* o = out + (size_t)(child - child_lo) * kMtN;
+    const int j = threadIdx.x;
     if (d == 0) {
-        for (int j = threadIdx.x; j < (int)kMtN; j += kJumpThreads) o[j] = b[j];
+        if (part == 0 && j < (int)kMtN) atomicXor((unsigned long long*)(o + j), b[j]);
         return;
     }
-    for (int i = threadIdx.x; i < kMtBaseWords; i += kJumpThreads) sbase[i] = b[i];
+    const int w0 = part * kJumpWordsPerPart;
+    const int w1 = min(kMtPolyWords, w0 + kJumpWordsPerPart);
+    if (w0 >= w1) return;
+    const int lo = 64 * w0, hi = min(kMtBaseWords, 64 * w1 + (int)kMtN);
+    for (int i = lo + j; i < hi; i += kJumpThreads) slice[i - lo] = b[i];
     __syncthreads();
-    const uint64_t* g = polys + (size_t)(d - 1) * kMtPolyWords;
-    const int j = threadIdx.x;
     if (j >= (int)kMtN) return;
+    const uint64_t* g = polys + (size_t)(d - 1) * kMtPolyWords;
     uint64_t acc = 0;
-    for (int w = 0; w < kMtPolyWords; ++w) {
-        uint64_t bits = __ldg(g + w);  // warp-uniform
-        const uint64_t* sb = sbase + 64 * w + j;
-        while (bits) {
-            const int bt = __ffsll((long long)bits) - 1;
-            bits &= bits - 1;
-            acc ^= sb[bt];
-        }
+    for (int w = w0; w < w1; ++w) {
+        const uint64_t bits = __ldg(g + w);  // uniform over the CTA
+        const uint64_t* sb = slice + 64 * (w - w0) + j;
+        const uint32_t blo = (uint32_t)bits, bhi = (uint32_t)(bits >> 32);
+#pragma unroll
+        for (int t = 0; t < 32; ++t)
+            if ((blo >> t) & 1u) acc ^= sb[t];
+#pragma unroll
+        for (int t = 0; t < 32; ++t)
+            if ((bhi >> t) & 1u) acc ^= sb[32 + t];
     }
-    o[j] = acc;
+    atomicXor((unsigned long long*)(o + j), acc);
 }
 
 // Keep bits of elements [e_begin, e_end) of the stream; chunk k = k0 + blockIdx.x.
@@ -223,12 +237,6 @@ cudaError_t launch_mt_keep_bits(uint64_t seed, double p, uint64_t e_begin, int64
     const int64_t k1 = (int64_t)((e_begin + (uint64_t)n - 1) / kMtChunk);
     if ((k1 >> (5 * kMtLevels)) != 0) return cudaErrorInvalidValue;  // > 2^38 outputs
 
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaFuncSetAttribute(mt_jump_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             kMtBaseWords * (int)sizeof(uint64_t));
-        attr_set = true;
-    }
     // level states: prefixes [lo, hi] of k >> (5 * level), stored from `cur`
     const uint64_t* cur = seed_st;
     int64_t lo = 0, hi = 0;  // level kMtLevels: the single prefix 0
@@ -246,8 +254,10 @@ cudaError_t launch_mt_keep_bits(uint64_t seed, double p, uint64_t e_begin, int64
             if (err != cudaSuccess) return err;
         } else {
             mt_base_kernel<<<(unsigned)S, kGenThreads, 0, st>>>(cur, base);
-            dim3 grid((unsigned)S, 32);
-            mt_jump_kernel<<<grid, kJumpThreads, kMtBaseWords * sizeof(uint64_t), st>>>(
+            err = cudaMemsetAsync(nxt, 0, (size_t)(chi - clo + 1) * kMtN * sizeof(uint64_t), st);
+            if (err != cudaSuccess) return err;
+            dim3 grid(kJumpParts, 32, (unsigned)S);
+            mt_jump_kernel<<<grid, kJumpThreads, 0, st>>>(
                 base, polys + (size_t)l * 31 * kMtPolyWords, nxt, lo * 32, clo, chi);
             err = cudaGetLastError();
             if (err != cudaSuccess) return err;
