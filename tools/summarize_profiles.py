@@ -25,8 +25,10 @@ OP_OF_KERNEL = [  # kernel name prefix -> bench op
     ("softmax_fwd_vec_kernel", "softmax_dropout_fwd"),
     ("softmax_bwd_vec_kernel", "attn_probs_bwd"),
     ("gelu_fwd_vec_kernel", "gelu_fwd"),
+    ("gelu_fwd8_kernel", "gelu_fwd"),
     ("gelu_bwd_fast_kernel", "gelu_bwd"),
     ("ln_fwd_vec_kernel", "layernorm_fwd"),
+    ("ln_fwd_warp_kernel", "layernorm_fwd"),
     ("ln_bwd_vec_kernel", "layernorm_bwd"),
     ("ln_param_reduce_kernel", "layernorm_bwd"),
     ("dropout_fwd_vec_kernel<1>", "dropout_fwd"),
