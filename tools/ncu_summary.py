@@ -42,8 +42,9 @@ def main(path):
                     if u == "Kbyte": f *= 1e3
                     if u == "Mbyte": f *= 1e6
                     if u == "Gbyte": f *= 1e9
-                    if u == "msecond": f *= 1e3
-                    if u == "nsecond": f *= 1e-3
+                    if u in ("msecond", "ms"): f *= 1e3
+                    if u in ("second", "s"): f *= 1e6
+                    if u in ("nsecond", "ns"): f *= 1e-3
                     rec[k] = f
                 except ValueError:
                     rec[k] = v
