@@ -114,6 +114,7 @@ class Chain:
         self.ws = ops.ln_workspace(T, H, dev)
         self.status = torch.zeros(1, dtype=torch.int32, device=dev)
         self.step_idx = 0
+        self.mask_mode = "philox"  # or "reference" (bench.py --masks reference)
         # global element offsets: rank shards reproduce the unsharded masks
         self.off_att = rank * ATT_ROWS * S
         self.off_h = rank * T * H
@@ -126,16 +127,31 @@ class Chain:
               self.y_ln2, self.rs2]
         return int(sum(t.numel() * t.element_size() for t in ts))
 
+    def reference_masks(self, step):
+        """The reference's own mask streams for this step, generated on the
+        device bit for bit (BoolMask::bernoulli_keep with
+        encoder::mask_stream_seed(run seed, salt = step, site 0/1/2),
+        encoder.cpp:168-201), each rank at its global offset."""
+        o = self.ops
+        for site, (m, n, off) in enumerate([(self.m_att, ATT_ROWS * S, self.off_att),
+                                            (self.m1, T * H, self.off_h),
+                                            (self.m2, T * H, self.off_h)]):
+            o.bernoulli_keep_bits_device(n, P_DROP, o.mask_stream_seed(1234, step, site),
+                                         offset=off, out=m)
+
     def forward(self, seed):
         o = self.ops
-        o.softmax_dropout_fwd(self.z, P_DROP, mask=self.m_att, generate=True, seed=seed,
+        gen = self.mask_mode != "reference"
+        if not gen:
+            self.reference_masks(seed)
+        o.softmax_dropout_fwd(self.z, P_DROP, mask=self.m_att, generate=gen, seed=seed,
                               offset=self.off_att, P=self.P, D=self.D)
-        o.dropout_fwd(self.x_attn_out, P_DROP, mask=self.m1, generate=True, seed=seed + 1,
+        o.dropout_fwd(self.x_attn_out, P_DROP, mask=self.m1, generate=gen, seed=seed + 1,
                       offset=self.off_h, y=self.d1)
         o.layernorm_ip_fwd(self.d1, self.g1, self.b1, check_gamma=False, y=self.y_ln1,
                            rstd=self.rs1, dev_status=self.status)
         o.gelu_ip_fwd(self.x_ffn1, self.table, y=self.y_g, mask=self.m_g)
-        o.dropout_fwd(self.x_ffn2, P_DROP, mask=self.m2, generate=True, seed=seed + 2,
+        o.dropout_fwd(self.x_ffn2, P_DROP, mask=self.m2, generate=gen, seed=seed + 2,
                       offset=self.off_h, y=self.d2)
         o.layernorm_ip_fwd(self.d2, self.g2, self.b2, check_gamma=False, y=self.y_ln2,
                            rstd=self.rs2, dev_status=self.status)
@@ -163,6 +179,9 @@ class Chain:
     # kernels launched per step (ours): softmax fwd 1, dropout fwd 2, LN fwd 2,
     # GELU fwd 1, LN bwd 2x(stage1+stage2), dropout bwd 2, GELU bwd 1, attn bwd 1
     LAUNCHES_PER_STEP = 14
+    # --masks reference, per mask: seed, (base, jump) for each of the 2 digit
+    # levels the rank-0 offsets touch, keep = 6; three masks
+    REF_MASK_LAUNCHES = 18
 
     def per_op_timings(self, reps, flush):
         """Per-kernel device time (CUDA events on the launching stream, L2
@@ -315,6 +334,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--masks", default="philox", choices=["philox", "reference"],
+                    help="dropout masks: in-kernel Philox (default) or the reference's own "
+                         "std::mt19937_64 streams generated on the device every step")
     args = ap.parse_args()
 
     rank = int(os.environ.get("RANK", "0"))
@@ -331,6 +353,7 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     chain = Chain(dev, rank, world)
+    chain.mask_mode = args.masks
     from paper_2210_10246_b200.dist import allreduce_ln_params
     allreduce = allreduce_ln_params if world > 1 else None
     flush_buf = torch.empty(256 * 1024 * 1024 // 4, device=dev)
@@ -392,6 +415,24 @@ def main():
         except Exception:
             pass
 
+    # ---- the reference mask stream on the device (outside the timed region) --
+    ref_mask = None
+    if rank == 0:
+        n_att = ATT_ROWS * S
+        chain.ops.bernoulli_keep_bits_device(n_att, P_DROP, 7, out=chain.m_att)  # tables + warm-up
+        ts = []
+        for _ in range(3):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(st)
+            chain.ops.bernoulli_keep_bits_device(n_att, P_DROP, 8, out=chain.m_att)
+            b.record(st)
+            b.synchronize()
+            ts.append(a.elapsed_time(b))
+        t_ms = min(ts)
+        ref_mask = {"what": "BoolMask::bernoulli_keep stream (std::mt19937_64) of the attention "
+                            "mask, bit-exact, device jump-ahead", "elements": n_att,
+                    "ms": round(t_ms, 3), "gelem_per_s": round(n_att / t_ms / 1e6, 1)}
+
     # ---- e2e: the public API with host buffers -----------------------------
     e2e = None
     if not args.no_e2e:
@@ -414,7 +455,10 @@ def main():
             "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic (torch.randn inputs of the layer shapes; Philox dropout masks)",
+            "data": ("synthetic (torch.randn inputs of the layer shapes; " +
+                     ("Philox dropout masks)" if args.masks == "philox" else
+                      "the reference's mt19937_64 dropout masks, generated on the device "
+                      "every step)")),
             "config": {"workload": WORKLOAD, "batch_per_gpu": B, "global_batch": B * world,
                        "seq_len": S, "hidden": H, "heads": A, "dropout_p": P_DROP,
                        "parallelism": f"rows{world}", "l2": "working set 12.7 GB/step >> 126 MB L2",
@@ -422,7 +466,10 @@ def main():
             "roofline": roofline,
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "gpu_launches": Chain.LAUNCHES_PER_STEP * args.steps,
+            "gpu_launches": (Chain.LAUNCHES_PER_STEP +
+                             (Chain.REF_MASK_LAUNCHES if args.masks == "reference" else 0)) * args.steps,
+            "mask_stream": args.masks,
+            "reference_mask_generation": ref_mask,
             "clocks": clk,
             "per_op": per_op_rows,
             "frac_of_peak": round(value / world / peak, 4),
@@ -501,7 +548,7 @@ def e2e_measure(chain, args, world, allreduce, dist):
                 h.copy_(d, non_blocking=True)
             ev_out.record(s_out)
 
-    k = max(1, min(args.steps, 5))
+    k = max(1, min(args.steps, 20))  # steady state: the one undrained D2H amortised over k
     upload(0)
     step(0, upload_next=False)  # warm-up
     torch.cuda.synchronize()
