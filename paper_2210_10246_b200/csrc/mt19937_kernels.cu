@@ -64,19 +64,17 @@ __global__ void __launch_bounds__(kGenThreads) mt_base_kernel(const uint64_t* __
 
 // Children states: child c = child0 + s * 32 + d (d = 0: the source itself),
 // stored at out[(c - child_lo) * 312] for c in [child_lo, child_hi].  The
-// 312 polynomial words are split over kJumpParts CTAs (grid.x); each stages
-// only the slice of the sequence its words touch in smem, accumulates the
-// windows of its set bits (64 predicated loads per word, no serial bit
-// scan) and XORs its partial state into the zeroed output.
-constexpr int kJumpParts = 8;
-constexpr int kJumpWordsPerPart = (kMtPolyWords + kJumpParts - 1) / kJumpParts;
-constexpr int kJumpSlice = 64 * kJumpWordsPerPart + kMtN;  // staged words per CTA
+// 312 polynomial words are split over kMtJumpParts CTAs (grid.x); each
+// stages only the slice of the sequence its words touch (plus a zero tail
+// for the list padding) in smem and walks the part's precomputed list of
+// set-bit indices, four per uniform 64-bit load: per set bit one LDS and
+// half a 3-input XOR; the partial state is XORed into the zeroed output.
+constexpr int kJumpSlice = 64 * kMtJumpWords + 2 * (int)kMtN;  // words staged per CTA
 
-__global__ void __launch_bounds__(kJumpThreads) mt_jump_kernel(const uint64_t* __restrict__ base,
-                                                               const uint64_t* __restrict__ polys,
-                                                               uint64_t* __restrict__ out,
-                                                               int64_t child0, int64_t child_lo,
-                                                               int64_t child_hi) {
+__global__ void __launch_bounds__(kJumpThreads) mt_jump_kernel(
+    const uint64_t* __restrict__ base, const uint16_t* __restrict__ idx,
+    const int32_t* __restrict__ off, int poly0, uint64_t* __restrict__ out, int64_t child0,
+    int64_t child_lo, int64_t child_hi) {
     __shared__ uint64_t slice[kJumpSlice];
     const int part = blockIdx.x, d = blockIdx.y, s = blockIdx.z;
     const int64_t child = child0 + (int64_t)s * 32 + d;
@@ -88,30 +86,30 @@ __global__ void __launch_bounds__(kJumpThreads) mt_jump_kernel(const uint64_t* _
         if (part == 0 && j < (int)kMtN) atomicXor((unsigned long long*)(o + j), b[j]);
         return;
     }
-    const int w0 = part * kJumpWordsPerPart;
-    const int w1 = min(kMtPolyWords, w0 + kJumpWordsPerPart);
-    if (w0 >= w1) return;
-    const int lo = 64 * w0, hi = min(kMtBaseWords, 64 * w1 + (int)kMtN);
-    for (int i = lo + j; i < hi; i += kJumpThreads) slice[i - lo] = b[i];
+    const int g0 = 64 * part * kMtJumpWords;  // first sequence word of the slice
+    const int real = 64 * kMtJumpWords + (int)kMtN;
+    for (int i = j; i < kJumpSlice; i += kJumpThreads)
+        slice[i] = (i < real && g0 + i < kMtBaseWords) ? b[g0 + i] : 0ull;
     __syncthreads();
     if (j >= (int)kMtN) return;
-    const uint64_t* g = polys + (size_t)(d - 1) * kMtPolyWords;
+    const int pi = (poly0 + d - 1) * kMtJumpParts + part;
+    const int k0 = __ldg(off + pi), k1 = __ldg(off + pi + 1);
+    const uint64_t* L = reinterpret_cast<const uint64_t*>(idx + k0);
+    const uint64_t* sj = slice + j;
     uint64_t acc = 0;
-    for (int w = w0; w < w1; ++w) {
-        const uint64_t bits = __ldg(g + w);  // uniform over the CTA
-        const uint64_t* sb = slice + 64 * (w - w0) + j;
-        const uint32_t blo = (uint32_t)bits, bhi = (uint32_t)(bits >> 32);
-#pragma unroll
-        for (int t = 0; t < 32; ++t)
-            if ((blo >> t) & 1u) acc ^= sb[t];
-#pragma unroll
-        for (int t = 0; t < 32; ++t)
-            if ((bhi >> t) & 1u) acc ^= sb[32 + t];
+#pragma unroll 4
+    for (int k = 0; k < (k1 - k0) >> 2; ++k) {
+        const uint64_t q = __ldg(L + k);  // four indices, uniform over the CTA
+        acc ^= sj[q & 0xffff] ^ sj[(q >> 16) & 0xffff] ^ sj[(q >> 32) & 0xffff] ^ sj[q >> 48];
     }
     atomicXor((unsigned long long*)(o + j), acc);
 }
 
-// Keep bits of elements [e_begin, e_end) of the stream; chunk k = k0 + blockIdx.x.
+// Keep bits of elements [e_begin, e_end); chunk k = k0 + blockIdx.x.  Step t
+// of a chunk produces outputs 128 t .. 128 t + 127 (all independent: the
+// recurrence reaches back >= 156 words); warp w's ballot is the mask word of
+// outputs 128 t + 32 w .. + 31.  Steps before the requested range only
+// advance the recurrence (shard offsets that fall inside a chunk).
 __global__ void __launch_bounds__(kGenThreads) mt_keep_kernel(const uint64_t* __restrict__ states,
                                                               int64_t k0, uint64_t e_begin,
                                                               uint64_t e_end, uint64_t xmin,
@@ -120,24 +118,48 @@ __global__ void __launch_bounds__(kGenThreads) mt_keep_kernel(const uint64_t* __
     const int64_t k = k0 + blockIdx.x;
     const uint64_t* st = states + (size_t)blockIdx.x * kMtN;
     for (int i = threadIdx.x; i < (int)kMtN; i += kGenThreads) ring[i] = st[i];
-    __syncthreads();
     const uint64_t c0 = (uint64_t)k * (uint64_t)kMtChunk;  // global index of the chunk's output 0
-    const uint64_t stop = min(c0 + (uint64_t)kMtChunk, e_end);
+    // chunk-relative output range [r0, r1) to store (r0 % 32 == 0)
+    const uint32_t r0 = e_begin > c0 ? (uint32_t)(e_begin - c0) : 0u;
+    const uint32_t r1 = (uint32_t)(min(c0 + (uint64_t)kMtChunk, e_end) - c0);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    for (uint64_t t0 = c0; t0 < stop; t0 += kGenThreads) {
-        const int j = (int)(t0 - c0) + kMtN + threadIdx.x;  // sequence index of this output
-        const uint64_t w = mt_next_word(ring[(j - 312) & (kRing - 1)],
-                                        ring[(j - 311) & (kRing - 1)],
-                                        ring[(j - 156) & (kRing - 1)]);
-        ring[j & (kRing - 1)] = w;
-        const bool keep = mt_temper(w) >= xmin;
-        uint32_t word = __ballot_sync(kFull, keep);
-        const uint64_t e0 = t0 + 32 * warp;  // element of bit 0 of this warp's word
-        if (lane == 0 && e0 >= e_begin && e0 < e_end) {
-            if (e_end - e0 < 32) word &= (1u << (e_end - e0)) - 1u;
-            mask[(e0 - e_begin) >> 5] = word;
+    uint32_t* mrow = mask + ((c0 + r0 - e_begin) >> 5) - (r0 >> 5);  // word of chunk output 0
+    // ring slots of this thread's operands, per phase of the 4-step (512-word)
+    // cycle: loop-invariant, so a step costs no address arithmetic
+    const int tid = threadIdx.x;
+    int a312[4], a311[4], a156[4], aw[4];
+#pragma unroll
+    for (int ph = 0; ph < 4; ++ph) {
+        const int j = ph * kGenThreads + kMtN + tid;  // sequence index mod 512
+        a312[ph] = (j - 312) & (kRing - 1);
+        a311[ph] = (j - 311) & (kRing - 1);
+        a156[ph] = (j - 156) & (kRing - 1);
+        aw[ph] = j & (kRing - 1);
+    }
+    __syncthreads();
+    // batches of 32 steps: lane s keeps the ballot word of step s and the
+    // warp stores its 32 words at once (words 4 t + w of the chunk)
+    for (uint32_t tb = 0; tb < r1; tb += 32 * kGenThreads) {
+        uint32_t mine = 0;
+#pragma unroll 1
+        for (int s4 = 0; s4 < 32; s4 += 4) {
+#pragma unroll
+            for (int ph = 0; ph < 4; ++ph) {
+                const uint32_t t0 = tb + (s4 + ph) * kGenThreads;
+                if (t0 < r1) {  // uniform
+                    const uint64_t w = mt_next_word(ring[a312[ph]], ring[a311[ph]], ring[a156[ph]]);
+                    ring[aw[ph]] = w;
+                    const uint32_t word = __ballot_sync(kFull, mt_temper(w) >= xmin);
+                    if (lane == s4 + ph) mine = word;
+                }
+                __syncthreads();
+            }
         }
-        __syncthreads();
+        const uint32_t e = tb + lane * kGenThreads + 32 * warp;  // output of bit 0 of `mine`
+        if (e >= r0 && e < r1) {
+            if (r1 - e < 32) mine &= (1u << (r1 - e)) - 1u;  // ragged end
+            mrow[e >> 5] = mine;
+        }
     }
 }
 
@@ -152,40 +174,49 @@ __global__ void mt_seed_kernel(uint64_t seed, uint64_t* __restrict__ st) {
     }
 }
 
-struct DevPolys {
+struct DevTables {
     std::mutex mu;
-    std::vector<uint64_t*> ptr;  // per device
+    std::vector<uint16_t*> idx;  // per device
+    std::vector<int32_t*> off;
 };
-DevPolys& dev_polys() {
-    static DevPolys d;
+DevTables& dev_tables() {
+    static DevTables d;
     return d;
 }
 
-const uint64_t* device_polys(cudaError_t& err) {
-    const uint64_t* host = mt_jump_polys();
-    if (!host) {
-        err = cudaErrorUnknown;
-        return nullptr;
-    }
+// The jump index lists on this device (uploaded once per device).
+cudaError_t device_index(const uint16_t** idx_out, const int32_t** off_out) {
+    const int32_t* hoff = nullptr;
+    size_t count = 0;
+    const uint16_t* hidx = mt_jump_index(&hoff, &count);
+    if (!hidx) return cudaErrorUnknown;
     int dev = 0;
     cudaGetDevice(&dev);
-    DevPolys& D = dev_polys();
+    DevTables& D = dev_tables();
     std::lock_guard<std::mutex> lock(D.mu);
-    if ((int)D.ptr.size() <= dev) D.ptr.resize(dev + 1, nullptr);
-    if (!D.ptr[dev]) {
-        const size_t bytes = (size_t)kMtLevels * 31 * kMtPolyWords * sizeof(uint64_t);
-        uint64_t* p = nullptr;
-        err = cudaMalloc(&p, bytes);
-        if (err != cudaSuccess) return nullptr;
-        err = cudaMemcpy(p, host, bytes, cudaMemcpyHostToDevice);
-        if (err != cudaSuccess) {
-            cudaFree(p);
-            return nullptr;
-        }
-        D.ptr[dev] = p;
+    if ((int)D.idx.size() <= dev) {
+        D.idx.resize(dev + 1, nullptr);
+        D.off.resize(dev + 1, nullptr);
     }
-    err = cudaSuccess;
-    return D.ptr[dev];
+    if (!D.idx[dev]) {
+        const size_t noff = (size_t)kMtLevels * 31 * kMtJumpParts + 1;
+        uint16_t* di = nullptr;
+        int32_t* dof = nullptr;
+        cudaError_t e = cudaMalloc(&di, count * sizeof(uint16_t));
+        if (e == cudaSuccess) e = cudaMalloc(&dof, noff * sizeof(int32_t));
+        if (e == cudaSuccess) e = cudaMemcpy(di, hidx, count * sizeof(uint16_t), cudaMemcpyHostToDevice);
+        if (e == cudaSuccess) e = cudaMemcpy(dof, hoff, noff * sizeof(int32_t), cudaMemcpyHostToDevice);
+        if (e != cudaSuccess) {
+            cudaFree(di);
+            cudaFree(dof);
+            return e;
+        }
+        D.idx[dev] = di;
+        D.off[dev] = dof;
+    }
+    *idx_out = D.idx[dev];
+    *off_out = D.off[dev];
+    return cudaSuccess;
 }
 
 // Workspace layout (bytes, 256-aligned pieces): seed state, two state
@@ -222,9 +253,10 @@ cudaError_t launch_mt_keep_bits(uint64_t seed, double p, uint64_t e_begin, int64
     if (n <= 0) return cudaSuccess;
     const MtWs L = mt_ws_layout(e_begin, n);
     if (ws_bytes < L.total || (e_begin & 31u)) return cudaErrorInvalidValue;
-    cudaError_t err = cudaSuccess;
-    const uint64_t* polys = device_polys(err);
-    if (!polys) return err;
+    const uint16_t* jidx = nullptr;
+    const int32_t* joff = nullptr;
+    cudaError_t err = device_index(&jidx, &joff);
+    if (err != cudaSuccess) return err;
     char* w = static_cast<char*>(ws);
     uint64_t* seed_st = reinterpret_cast<uint64_t*>(w + L.seed_off);
     uint64_t* sa = reinterpret_cast<uint64_t*>(w + L.sa_off);
@@ -256,9 +288,9 @@ cudaError_t launch_mt_keep_bits(uint64_t seed, double p, uint64_t e_begin, int64
             mt_base_kernel<<<(unsigned)S, kGenThreads, 0, st>>>(cur, base);
             err = cudaMemsetAsync(nxt, 0, (size_t)(chi - clo + 1) * kMtN * sizeof(uint64_t), st);
             if (err != cudaSuccess) return err;
-            dim3 grid(kJumpParts, 32, (unsigned)S);
-            mt_jump_kernel<<<grid, kJumpThreads, 0, st>>>(
-                base, polys + (size_t)l * 31 * kMtPolyWords, nxt, lo * 32, clo, chi);
+            dim3 grid(kMtJumpParts, 32, (unsigned)S);
+            mt_jump_kernel<<<grid, kJumpThreads, 0, st>>>(base, jidx, joff, l * 31, nxt, lo * 32,
+                                                          clo, chi);
             err = cudaGetLastError();
             if (err != cudaSuccess) return err;
         }

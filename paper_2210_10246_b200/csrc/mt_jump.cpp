@@ -206,7 +206,28 @@ struct JumpTables {
     bool ok = false;
     Poly P;
     std::vector<uint64_t> polys;  // [kMtLevels][31][kMtPolyWords]
+    std::vector<uint16_t> idx;    // set-bit lists per (poly, part), padded
+    std::vector<int32_t> off;     // [kMtLevels * 31 * kMtJumpParts + 1]
 };
+
+void build_index(JumpTables& T) {
+    const int npoly = kMtLevels * 31;
+    T.off.assign((size_t)npoly * kMtJumpParts + 1, 0);
+    T.idx.clear();
+    for (int pi = 0; pi < npoly; ++pi) {
+        const uint64_t* g = T.polys.data() + (size_t)pi * kMtPolyWords;
+        for (int q = 0; q < kMtJumpParts; ++q) {
+            T.off[(size_t)pi * kMtJumpParts + q] = (int32_t)T.idx.size();
+            const int w0 = q * kMtJumpWords, w1 = std::min(kMtPolyWords, w0 + kMtJumpWords);
+            for (int w = w0; w < w1; ++w)
+                for (int b = 0; b < 64; ++b)
+                    if ((g[w] >> b) & 1u) T.idx.push_back((uint16_t)(64 * (w - w0) + b));
+            while ((T.idx.size() - T.off[(size_t)pi * kMtJumpParts + q]) % 4)
+                T.idx.push_back((uint16_t)kMtJumpSentinel);
+        }
+    }
+    T.off[(size_t)npoly * kMtJumpParts] = (int32_t)T.idx.size();
+}
 
 JumpTables& tables() {
     static JumpTables T;
@@ -233,6 +254,7 @@ JumpTables& tables() {
             }
             step = cur;  // x^(32 * 32^l * chunk)
         }
+        build_index(T);
         T.ok = true;
     });
     return T;
@@ -250,6 +272,14 @@ void mt_seed_state(uint64_t seed, uint64_t* st) {
 const uint64_t* mt_jump_polys() {
     JumpTables& T = tables();
     return T.ok ? T.polys.data() : nullptr;
+}
+
+const uint16_t* mt_jump_index(const int32_t** off, size_t* count) {
+    JumpTables& T = tables();
+    if (!T.ok) return nullptr;
+    *off = T.off.data();
+    *count = T.idx.size();
+    return T.idx.data();
 }
 
 // Apply x^J mod P (given as kMtPolyWords words) to `state` on the host.
