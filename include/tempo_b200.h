@@ -195,7 +195,7 @@ int tempo_bernoulli_keep_bits_host(int64_t n, double p, uint64_t seed, uint32_t*
 /* The same stream generated ON THE DEVICE, bit for bit: the keep bits of
  * elements [offset, offset + n) of BoolMask::bernoulli_keep(shape, p, seed)
  * (for any shape with at least offset + n elements) into ceil(n/32) words at
- * `bits` (device).  The std::mt19937_64 stream is cut into 2^18-output
+ * `bits` (device).  The std::mt19937_64 stream is cut into 2^19-output
  * chunks whose states are reached by GF(2) jump-ahead (x^J mod the
  * characteristic polynomial); row shards pass their global offset.
  * offset % 32 != 0 or p not in [0,1) -> TEMPO_ERR_PARAM.  The workspace

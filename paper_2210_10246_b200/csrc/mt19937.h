@@ -10,13 +10,17 @@
 #define TB_HD inline
 #endif
 
+#ifndef TM_MT_CHUNK_LOG2
+#define TM_MT_CHUNK_LOG2 19
+#endif
+
 namespace tb {
 
 constexpr unsigned kMtN = 312;                  // state words
 constexpr int kMtDeg = 19937;                   // degree of the characteristic polynomial
 constexpr int kMtPolyWords = (kMtDeg + 63) / 64;  // 312 words per jump polynomial
 constexpr int kMtBaseWords = kMtDeg - 1 + kMtN;   // windows i <= 19936 of 312 words
-constexpr int64_t kMtChunk = int64_t(1) << 18;  // outputs per device stream
+constexpr int64_t kMtChunk = int64_t(1) << TM_MT_CHUNK_LOG2;  // outputs per device stream
 constexpr int kMtLevels = 4;                    // 32^4 streams of kMtChunk: 2^38 outputs
 // The device jump splits each polynomial's words over kMtJumpParts CTAs.
 constexpr int kMtJumpParts = 8;

@@ -6,10 +6,10 @@
 // generate_canonical with a 64-bit engine), x_i the i-th tempered output.
 // Reproducing it bit for bit in parallel (mt_jump.cpp has the math):
 //
-//   1. the stream is cut into chunks of kMtChunk = 2^18 outputs; chunk k's
-//      starting state is T^(k * 2^18) s0, reached through base-32 digits of k
+//   1. the stream is cut into chunks of kMtChunk = 2^19 outputs; chunk k's
+//      starting state is T^(k * 2^19) s0, reached through base-32 digits of k
 //      (levels 3..0): a jump by digit d at level l applies the polynomial
-//      x^(d * 32^l * 2^18) mod P to a state;
+//      x^(d * 32^l * 2^19) mod P to a state;
 //   2. mt_base_kernel: the 20248-word sequence started at each source state
 //      (the recurrence, 128 words per step, ring buffer in smem);
 //   3. mt_jump_kernel: a jumped state = XOR of the 312-word windows of that

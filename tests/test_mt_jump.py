@@ -11,7 +11,7 @@ bit for bit, over several chunks, seeds, probabilities and shard offsets."""
 import numpy as np
 import pytest
 
-CHUNK = 1 << 18  # kMtChunk (mt19937.h)
+CHUNK = 1 << 19  # kMtChunk (mt19937.h)
 
 
 @pytest.mark.parametrize("seed", [5489, 42, 0xDEADBEEFCAFE])
