@@ -132,6 +132,22 @@ BoolMask BoolMask::empty(Shape shape) {
 
 BoolMask BoolMask::bernoulli_keep(Shape shape, double drop_p, std::uint64_t seed) {
     std::int64_t n = shape_numel(shape);
+    if (n >= (std::int64_t(1) << 22)) {
+        // large masks: the same std::mt19937_64 stream generated on the
+        // device by jump-ahead (tempo_bernoulli_keep_bits), bit for bit
+        if (!(drop_p >= 0.0) || drop_p >= 1.0)  // tensor.cpp:188-191
+            throw ParamError("drop probability must lie in [0, 1), got " + std::to_string(drop_p));
+        BoolMask m = empty(std::move(shape));
+        const size_t ws_bytes = tempo_bernoulli_keep_bits_workspace_size(0, n);
+        void* ws = nullptr;
+        cuda_check(cudaMalloc(&ws, ws_bytes), "cudaMalloc");
+        const int rc = tempo_bernoulli_keep_bits(n, drop_p, seed, 0, m.words(), ws, ws_bytes, nullptr);
+        cudaError_t e = cudaStreamSynchronize(nullptr);
+        cudaFree(ws);
+        check(rc);
+        cuda_check(e, "tempo_bernoulli_keep_bits");
+        return m;
+    }
     std::vector<std::uint32_t> host((size_t)words_of(n));
     check(tempo_bernoulli_keep_bits_host(n, drop_p, seed, host.data()));
     BoolMask m = empty(std::move(shape));

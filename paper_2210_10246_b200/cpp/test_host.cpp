@@ -9,6 +9,8 @@
 #include <string>
 #include <vector>
 
+#include <cuda_runtime.h>
+
 #include "../../include/tempo_b200/tempo.hpp"
 
 using namespace tempo_b200;
@@ -295,6 +297,18 @@ static void test_hidden_dropout() {
     CHECK(throws<ParamError>([&] { ref_ops::dropout(g, x, 1.0, mask, "d2", "m2"); }));
 }
 
+// A large mask goes through the device generator (jump-ahead): it must be
+// the reference's stream bit for bit (here: against the host engine).
+static void test_large_mask_device_stream() {
+    const std::int64_t n = (std::int64_t(1) << 22) + 4096 + 5;
+    BoolMask mask = BoolMask::bernoulli_keep({n}, 0.1, 31337);
+    std::vector<std::uint32_t> host((size_t)((n + 31) / 32));
+    CHECK(tempo_bernoulli_keep_bits_host(n, 0.1, 31337, host.data()) == 0);
+    std::vector<std::uint32_t> dev(host.size());
+    CHECK(cudaMemcpy(dev.data(), mask.words(), dev.size() * 4, cudaMemcpyDeviceToHost) == cudaSuccess);
+    CHECK(dev == host);
+}
+
 int main() {
     run("gelu forward/backward + ledger", test_gelu);
     run("gelu refusals", test_gelu_refusals);
@@ -304,6 +318,7 @@ int main() {
     run("dropout recompute + lazy stash", test_dropout_recompute);
     run("fused softmax+dropout", test_softmax_dropout_fused);
     run("hidden dropout", test_hidden_dropout);
+    run("large mask: device reference stream", test_large_mask_device_stream);
     std::printf("%d failure(s)\n", g_fail);
     return g_fail;
 }
