@@ -17,6 +17,12 @@ namespace {
 
 constexpr int kBlock = 256;
 constexpr int kUnroll = 4;
+#ifndef TM_DROPOUT_V8
+#define TM_DROPOUT_V8 1
+#endif
+#ifndef TM_DROPOUT_U8
+#define TM_DROPOUT_U8 1
+#endif
 
 __device__ __forceinline__ float dscale(float v, double s) { return (float)((double)v * s); }
 
@@ -106,6 +112,89 @@ __global__ void __launch_bounds__(kBlock) dropout_fwd_vec_kernel(
                                      lane);
 }
 
+// 256-bit variant: lane L owns elements 8L..8L+7 of each 256-element chunk
+// (one LDG/STG.256) and byte L of the chunk's mask (read or written
+// directly); Philox draws by global element index as above (same bits);
+// U chunks per group, ping-pong register buffers.
+template <bool PHILOX, int U>
+__global__ void __launch_bounds__(kBlock) dropout_fwd8_kernel(
+    const float* __restrict__ x, uint32_t* __restrict__ mask, double scale, uint64_t thresh,
+    uint64_t seed, uint64_t offset, float* __restrict__ y, int64_t n) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = ((int64_t)blockIdx.x * kBlock + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * kBlock) >> 5;
+    uint8_t* mask8 = reinterpret_cast<uint8_t*>(mask);
+    const int64_t nchunks = n >> 8;
+    const int64_t ngroups = nchunks / U;
+    struct Group {
+        F8 v[U];
+        uint32_t mb[U];
+    };
+    auto load = [&](Group& G, int64_t c0) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            G.v[u] = ld_stream8(x + ((c0 + u) << 8) + 8 * lane);
+            if (!PHILOX) G.mb[u] = ld_byte(mask8 + ((c0 + u) << 5) + lane);
+        }
+    };
+    auto compute = [&](Group& G, int64_t c0) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t e0 = ((c0 + u) << 8) + 8 * lane;
+            uint32_t bits;
+            if (PHILOX) {
+                const uint64_t q = (offset + (uint64_t)e0) >> 2;
+                const U4 a = philox_quad(seed, q), b = philox_quad(seed, q + 1);
+                bits = ((uint64_t)a.x >= thresh ? 1u : 0u) | ((uint64_t)a.y >= thresh ? 2u : 0u) |
+                       ((uint64_t)a.z >= thresh ? 4u : 0u) | ((uint64_t)a.w >= thresh ? 8u : 0u) |
+                       ((uint64_t)b.x >= thresh ? 16u : 0u) | ((uint64_t)b.y >= thresh ? 32u : 0u) |
+                       ((uint64_t)b.z >= thresh ? 64u : 0u) | ((uint64_t)b.w >= thresh ? 128u : 0u);
+                st_stream(mask8 + (e0 >> 3), bits);
+            } else {
+                bits = G.mb[u];
+            }
+            F8 o;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) o.v[j] = ((bits >> j) & 1u) ? dscale(G.v[u].v[j], scale) : 0.0f;
+            st_stream8(y + e0, o);
+        }
+    };
+    Group a, b;
+    if (warp < ngroups) load(a, warp * U);
+    for (int64_t gi = warp; gi < ngroups; gi += 2 * nwarps) {
+        const int64_t g1 = gi + nwarps, g2 = gi + 2 * nwarps;
+        if (g1 < ngroups) load(b, g1 * U);
+        compute(a, gi * U);
+        if (g1 >= ngroups) break;
+        if (g2 < ngroups) load(a, g2 * U);
+        compute(b, g1 * U);
+    }
+    // leftover chunks (< U per warp), then the ragged tail on the last warp
+    for (int64_t c = ngroups * U + warp; c < nchunks; c += nwarps) {
+        const F8 v = ld_stream8(x + (c << 8) + 8 * lane);
+        const int64_t e0 = (c << 8) + 8 * lane;
+        uint32_t bits;
+        if (PHILOX) {
+            const uint64_t q = (offset + (uint64_t)e0) >> 2;
+            const U4 ra = philox_quad(seed, q), rb = philox_quad(seed, q + 1);
+            bits = ((uint64_t)ra.x >= thresh ? 1u : 0u) | ((uint64_t)ra.y >= thresh ? 2u : 0u) |
+                   ((uint64_t)ra.z >= thresh ? 4u : 0u) | ((uint64_t)ra.w >= thresh ? 8u : 0u) |
+                   ((uint64_t)rb.x >= thresh ? 16u : 0u) | ((uint64_t)rb.y >= thresh ? 32u : 0u) |
+                   ((uint64_t)rb.z >= thresh ? 64u : 0u) | ((uint64_t)rb.w >= thresh ? 128u : 0u);
+            st_stream(mask8 + (e0 >> 3), bits);
+        } else {
+            bits = ld_byte(mask8 + (e0 >> 3));
+        }
+        F8 o;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) o.v[j] = ((bits >> j) & 1u) ? dscale(v.v[j], scale) : 0.0f;
+        st_stream8(y + e0, o);
+    }
+    if (warp == nwarps - 1)
+        dropout_scalar_words<PHILOX>(x, mask, scale, thresh, seed, offset, y, n, nchunks << 3, 1,
+                                     lane);
+}
+
 template <bool PHILOX>
 __global__ void __launch_bounds__(kBlock) dropout_fwd_scalar_kernel(
     const float* __restrict__ x, uint32_t* __restrict__ mask, double scale, uint64_t thresh,
@@ -150,10 +239,19 @@ __global__ void __launch_bounds__(kBlock) add_kernel(const float* __restrict__ a
 }
 
 inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+inline bool aligned32(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 31u) == 0; }
 
 template <bool PHILOX>
 cudaError_t fwd(const float* x, double scale, uint64_t thresh, uint32_t* mask, uint64_t seed,
                 uint64_t offset, float* y, int64_t n, cudaStream_t st) {
+    if (TM_DROPOUT_V8 && aligned32(x) && aligned32(y) && aligned16(mask) && (offset & 7u) == 0) {
+        constexpr int U = TM_DROPOUT_U8;
+        auto k = dropout_fwd8_kernel<PHILOX, U>;
+        const int64_t warps = ((n >> 8) + U - 1) / U + 1;
+        int grid = grid_for((const void*)k, kBlock, 0, (warps * 32 + kBlock - 1) / kBlock);
+        k<<<grid, kBlock, 0, st>>>(x, mask, scale, thresh, seed, offset, y, n);
+        return cudaGetLastError();
+    }
     const bool vec = aligned16(x) && aligned16(y) && aligned16(mask) && (offset & 3u) == 0;
     if (vec) {
         auto k = dropout_fwd_vec_kernel<PHILOX>;
