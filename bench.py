@@ -268,6 +268,16 @@ class ClockSampler:
 
 
 # ------------------------------------------------------ CPU reference arm
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def cpu_reference_sample(frac_rows: int, threads: int, steps: int, warmup: int):
     """The reference's own CPU implementation (oracle/_ref/libtempo_ref.so,
     compiled from /root/reference/proj/src) of the same chain on a bounded
@@ -444,8 +454,11 @@ def main():
         try:
             threads = len(os.sched_getaffinity(0))
             v, dt, sample = cpu_reference_sample(frac_rows=32, threads=threads, steps=2, warmup=1)
+            v1, dt1, _ = cpu_reference_sample(frac_rows=512, threads=1, steps=1, warmup=0)
             cpu = {"value": round(v, 4), "unit": "GB/s", "cores": threads, "kind": "reference",
-                   "sample": sample, "s_per_step": round(dt, 3)}
+                   "sample": sample, "s_per_step": round(dt, 3), "cpu_model": cpu_model(),
+                   "one_thread": {"value": round(v1, 4), "unit": "GB/s",
+                                  "sample": "1/512 of the per-GPU chain rows, 1 thread"}}
         except Exception as ex:  # the reference library is prebuilt here; report if absent
             cpu = {"value": None, "unit": "GB/s", "cores": 0, "kind": "reference",
                    "sample": f"unavailable: {ex}"}
@@ -595,7 +608,7 @@ def main_reference(args, rank, world):
                    "seq_len": S, "hidden": H, "heads": A, "dropout_p": P_DROP,
                    "parallelism": f"rows{world}"},
         "cpu_baseline": {"value": round(v, 4), "unit": "GB/s", "cores": threads,
-                         "kind": "reference", "sample": sample},
+                         "kind": "reference", "sample": sample, "cpu_model": cpu_model()},
         "e2e": {"value": round(v, 4), "unit": "GB/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
