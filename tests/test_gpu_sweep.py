@@ -70,3 +70,94 @@ def test_gelu_kernel_every_float(tops, cuda):
     assert checked > 4_000_000_000
     assert mask_bad == 0 and nan_bad == 0 and win_bad == 0
     assert max_ulp <= 8
+
+
+def _table_f64(text):
+    """The v1 table text as fp64 segments per branch (gelu_table.cpp:204-302)."""
+    head, *lines = [ln for ln in text.strip().splitlines() if ln.strip()]
+    kv = dict(tok.split("=") for tok in head.split()[2:])
+    segs = {0: [], 1: []}
+    for ln in lines:
+        f = ln.split()
+        b, lo, hi, var, deg = int(f[0]), float(f[1]), float(f[2]), f[3], int(f[4])
+        segs[b].append((lo, hi, var == "sqrt-shift", [float(c) for c in f[5:6 + deg]]))
+    return float(kv["y_min"]), segs
+
+
+def _eval_f64(torch, y, m, ymin, segs):
+    """GeluPolyTable::eval (gelu_table.cpp:172-188: find_segment :157-170,
+    eval_segment :59-81, clenshaw :43-51) vectorised in fp64 -- a test-side
+    restatement, the exhaustive sweep's checker."""
+    out = torch.zeros_like(y)
+    yc = torch.where(y < ymin, torch.full_like(y, ymin), y)  # NaN stays NaN
+    lo = torch.tensor([s[0] for s in segs[m]], dtype=torch.float64, device=y.device)
+    idx = (torch.searchsorted(lo, yc.contiguous(), right=True) - 1).clamp(min=0)
+    idx = torch.where(torch.isnan(yc), torch.zeros_like(idx), idx)
+    for k, (slo, shi, sq, c) in enumerate(segs[m]):
+        sel = idx == k
+        if not bool(sel.any()):
+            continue
+        v = yc[sel]
+        if len(c) == 1:
+            r = torch.full_like(v, c[0])  # constant segment: c0 (eval_segment :64)
+        else:
+            if sq:
+                u = torch.sqrt(torch.clamp(v - ymin, min=0.0).where(~torch.isnan(v), v))
+                ulo, uhi = max(slo - ymin, 0.0) ** 0.5, (shi - ymin) ** 0.5
+            else:
+                u, ulo, uhi = v, slo, shi
+            t = (2.0 * (u - ulo) / (uhi - ulo) - 1.0).clamp(-1.0, 1.0).where(~torch.isnan(u), u)
+            b1 = torch.zeros_like(t)
+            b2 = torch.zeros_like(t)
+            for ck in reversed(c[1:]):
+                b1, b2 = 2.0 * t * b1 - b2 + ck, b1
+            r = t * b1 - b2 + c[0]
+        out[sel] = r
+    if m == 0:
+        out = torch.where(y >= 0.0, torch.zeros_like(out), out)
+    return out
+
+
+def _tables():
+    with open(os.path.join(ROOT, "tests", "golden", "gelu_table_default_v1.txt")) as f:
+        out = [("default", f.read())]
+    with open(os.path.join(ROOT, "tests", "golden", "gelu_tables_extra.json")) as f:
+        out += sorted(json.load(f).items())
+    return out
+
+
+@pytest.mark.parametrize("m", [0, 1])
+@pytest.mark.parametrize("name,table_text", _tables(), ids=[t[0] for t in _tables()])
+def test_gelu_bwd_kernel_every_float(tops, cuda, name, table_text, m):
+    """The shipped backward kernel (through the C-ABI, dy = 1 so dx = h(y, m))
+    on every fp32 bit pattern of y, for mask bit m, against the reference's
+    table evaluation in fp64 rounded once (float(dy * eval(double(y), m)),
+    ops_tempo.cpp:59-68): rel_err <= 1e-5 everywhere, NaN <-> NaN."""
+    import torch
+    table = tops.GeluTable(table_text)
+    ymin, segs = _table_f64(table_text)
+    step = 1 << 28
+    worst, nan_bad, checked = 0.0, 0, 0
+    ones = torch.ones(step, device=cuda)
+    mw = torch.full((step // 32,), -1 if m else 0, dtype=torch.int32, device=cuda)
+    for b in range(0, 1 << 32, step):
+        u = torch.arange(b, b + step, device=cuda, dtype=torch.int64)
+        y = (u - (1 << 32) * (u >= (1 << 31))).to(torch.int32).view(torch.float32)
+        h = tops.gelu_ip_bwd(ones, y, mw, table)
+        ref = _eval_f64(torch, y.double(), m, ymin, segs).float()
+        hn, rn = torch.isnan(h), torch.isnan(ref)
+        nan_bad += int((hn != rn).sum())
+        ok = ~(hn | rn)
+        a, r = h[ok].double(), ref[ok].double()
+        rel = (a - r).abs() / torch.clamp(torch.maximum(a.abs(), r.abs()), min=1.0)
+        worst = max(worst, float(rel.max()))
+        checked += int(ok.sum())
+        del u, y, h, ref
+    res = {"table": name, "m": m, "checked": checked, "max_rel_err": worst,
+           "nan_mismatch": nan_bad}
+    print(res)
+    os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
+    with open(os.path.join(ROOT, "gpurun_out", f"gelu_bwd_sweep_{name}_m{m}.json"), "w") as f:
+        json.dump(res, f)
+    assert checked > 4_000_000_000 and nan_bad == 0
+    assert worst <= 1e-5
