@@ -54,6 +54,8 @@ template <bool PHILOX>
 __global__ void __launch_bounds__(kBlock) dropout_fwd_vec_kernel(
     const float* __restrict__ x, uint32_t* __restrict__ mask, double scale, uint64_t thresh,
     uint64_t seed, uint64_t offset, float* __restrict__ y, int64_t n) {
+    grid_dep_wait();  // PDL: predecessor complete and visible
+    grid_dep_launch();
     const int lane = threadIdx.x & 31;
     const int64_t warp = ((int64_t)blockIdx.x * kBlock + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * kBlock) >> 5;
@@ -120,6 +122,8 @@ template <bool PHILOX, int U>
 __global__ void __launch_bounds__(kBlock) dropout_fwd8_kernel(
     const float* __restrict__ x, uint32_t* __restrict__ mask, double scale, uint64_t thresh,
     uint64_t seed, uint64_t offset, float* __restrict__ y, int64_t n) {
+    grid_dep_wait();  // PDL: predecessor complete and visible
+    grid_dep_launch();
     const int lane = threadIdx.x & 31;
     const int64_t warp = ((int64_t)blockIdx.x * kBlock + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * kBlock) >> 5;
@@ -199,6 +203,8 @@ template <bool PHILOX>
 __global__ void __launch_bounds__(kBlock) dropout_fwd_scalar_kernel(
     const float* __restrict__ x, uint32_t* __restrict__ mask, double scale, uint64_t thresh,
     uint64_t seed, uint64_t offset, float* __restrict__ y, int64_t n) {
+    grid_dep_wait();  // PDL: predecessor complete and visible
+    grid_dep_launch();
     const int lane = threadIdx.x & 31;
     const int64_t warp = ((int64_t)blockIdx.x * kBlock + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * kBlock) >> 5;
@@ -209,6 +215,8 @@ __global__ void __launch_bounds__(kBlock) dropout_fwd_scalar_kernel(
 __global__ void __launch_bounds__(kBlock) mask_pack_kernel(const uint8_t* __restrict__ bytes,
                                                            uint32_t* __restrict__ bits, int64_t n,
                                                            int32_t* __restrict__ status) {
+    grid_dep_wait();  // PDL: predecessor complete and visible
+    grid_dep_launch();
     const int lane = threadIdx.x & 31;
     const int64_t warp = ((int64_t)blockIdx.x * kBlock + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * kBlock) >> 5;
@@ -225,6 +233,8 @@ __global__ void __launch_bounds__(kBlock) mask_pack_kernel(const uint8_t* __rest
 __global__ void __launch_bounds__(kBlock) mask_unpack_kernel(const uint32_t* __restrict__ bits,
                                                              uint8_t* __restrict__ bytes,
                                                              int64_t n) {
+    grid_dep_wait();  // PDL: predecessor complete and visible
+    grid_dep_launch();
     const int64_t stride = (int64_t)gridDim.x * kBlock;
     for (int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x; i < n; i += stride)
         bytes[i] = (bits[i >> 5] >> (i & 31)) & 1u;
@@ -233,6 +243,8 @@ __global__ void __launch_bounds__(kBlock) mask_unpack_kernel(const uint32_t* __r
 __global__ void __launch_bounds__(kBlock) add_kernel(const float* __restrict__ a,
                                                      const float* __restrict__ b,
                                                      float* __restrict__ out, int64_t n) {
+    grid_dep_wait();  // PDL: predecessor complete and visible
+    grid_dep_launch();
     const int64_t stride = (int64_t)gridDim.x * kBlock;
     for (int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x; i < n; i += stride)
         out[i] = a[i] + b[i];
@@ -249,7 +261,7 @@ cudaError_t fwd(const float* x, double scale, uint64_t thresh, uint32_t* mask, u
         auto k = dropout_fwd8_kernel<PHILOX, U>;
         const int64_t warps = ((n >> 8) + U - 1) / U + 1;
         int grid = grid_for((const void*)k, kBlock, 0, (warps * 32 + kBlock - 1) / kBlock);
-        k<<<grid, kBlock, 0, st>>>(x, mask, scale, thresh, seed, offset, y, n);
+        pdl(k, grid, kBlock, 0, st)(x, mask, scale, thresh, seed, offset, y, n);
         return cudaGetLastError();
     }
     const bool vec = aligned16(x) && aligned16(y) && aligned16(mask) && (offset & 3u) == 0;
@@ -257,12 +269,12 @@ cudaError_t fwd(const float* x, double scale, uint64_t thresh, uint32_t* mask, u
         auto k = dropout_fwd_vec_kernel<PHILOX>;
         const int64_t warps = ((n >> 7) + kUnroll - 1) / kUnroll + 1;
         int grid = grid_for((const void*)k, kBlock, 0, (warps * 32 + kBlock - 1) / kBlock);
-        k<<<grid, kBlock, 0, st>>>(x, mask, scale, thresh, seed, offset, y, n);
+        pdl(k, grid, kBlock, 0, st)(x, mask, scale, thresh, seed, offset, y, n);
     } else {
         auto k = dropout_fwd_scalar_kernel<PHILOX>;
         const int64_t warps = (n + 31) >> 5;
         int grid = grid_for((const void*)k, kBlock, 0, (warps * 32 + kBlock - 1) / kBlock);
-        k<<<grid, kBlock, 0, st>>>(x, mask, scale, thresh, seed, offset, y, n);
+        pdl(k, grid, kBlock, 0, st)(x, mask, scale, thresh, seed, offset, y, n);
     }
     return cudaGetLastError();
 }
@@ -289,21 +301,21 @@ cudaError_t launch_mask_pack(const uint8_t* bytes, uint32_t* bits, int64_t n, in
     if (n == 0) return cudaSuccess;
     const int64_t warps = (n + 31) >> 5;
     int grid = grid_for((const void*)mask_pack_kernel, kBlock, 0, (warps * 32 + kBlock - 1) / kBlock);
-    mask_pack_kernel<<<grid, kBlock, 0, st>>>(bytes, bits, n, status);
+    pdl(mask_pack_kernel, grid, kBlock, 0, st)(bytes, bits, n, status);
     return cudaGetLastError();
 }
 
 cudaError_t launch_add(const float* a, const float* b, float* out, int64_t n, cudaStream_t st) {
     if (n == 0) return cudaSuccess;
     int grid = grid_for((const void*)add_kernel, kBlock, 0, (n + kBlock - 1) / kBlock);
-    add_kernel<<<grid, kBlock, 0, st>>>(a, b, out, n);
+    pdl(add_kernel, grid, kBlock, 0, st)(a, b, out, n);
     return cudaGetLastError();
 }
 
 cudaError_t launch_mask_unpack(const uint32_t* bits, uint8_t* bytes, int64_t n, cudaStream_t st) {
     if (n == 0) return cudaSuccess;
     int grid = grid_for((const void*)mask_unpack_kernel, kBlock, 0, (n + kBlock - 1) / kBlock);
-    mask_unpack_kernel<<<grid, kBlock, 0, st>>>(bits, bytes, n);
+    pdl(mask_unpack_kernel, grid, kBlock, 0, st)(bits, bytes, n);
     return cudaGetLastError();
 }
 

@@ -127,6 +127,8 @@ __global__ void TM_GELU_FWD_BOUNDS gelu_fwd8_kernel(const float* __restrict__ x,
                                                     float* __restrict__ y,
                                                     uint32_t* __restrict__ mask, int64_t n,
                                                     float xstar_gt, float xs_lo) {
+    grid_dep_wait();  // PDL: predecessor complete and visible
+    grid_dep_launch();
     __shared__ __align__(16) float stage_all[kBlock / 32][U * 256];
     const int lane = threadIdx.x & 31;
     float* stage = stage_all[threadIdx.x >> 5];
@@ -190,6 +192,8 @@ __global__ void __launch_bounds__(kBlock) gelu_fwd_scalar_kernel(const float* __
                                                                  uint32_t* __restrict__ mask,
                                                                  int64_t n, float xstar_gt,
                                                                  float xs_lo) {
+    grid_dep_wait();  // PDL: predecessor complete and visible
+    grid_dep_launch();
     const int lane = threadIdx.x & 31;
     const int64_t warp = ((int64_t)blockIdx.x * kBlock + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * kBlock) >> 5;
@@ -276,6 +280,8 @@ __device__ __forceinline__ void gelu_bwd_scalar_words(const float* __restrict__ 
 __global__ void __launch_bounds__(kBlock) gelu_bwd_vec_kernel(
     const float* __restrict__ dy, const float* __restrict__ y, const uint32_t* __restrict__ mask,
     float* __restrict__ dx, int64_t n, const __grid_constant__ GeluDevTable t) {
+    grid_dep_wait();  // PDL: predecessor complete and visible
+    grid_dep_launch();
     __shared__ SmemTable st;
     extern __shared__ float coef[];
     load_table(t, st, coef);
@@ -319,6 +325,8 @@ __global__ void __launch_bounds__(kBlock) gelu_bwd_vec_kernel(
 __global__ void __launch_bounds__(kBlock) gelu_bwd_scalar_kernel(
     const float* __restrict__ dy, const float* __restrict__ y, const uint32_t* __restrict__ mask,
     float* __restrict__ dx, int64_t n, const __grid_constant__ GeluDevTable t) {
+    grid_dep_wait();  // PDL: predecessor complete and visible
+    grid_dep_launch();
     __shared__ SmemTable st;
     extern __shared__ float coef[];
     load_table(t, st, coef);
@@ -431,6 +439,8 @@ template <int NC4, bool HORNER, bool V8>
 __global__ void __launch_bounds__(kBlock) gelu_bwd_fast_kernel(
     const float* __restrict__ dy, const float* __restrict__ y, const uint32_t* __restrict__ mask,
     float* __restrict__ dx, int64_t n, const __grid_constant__ GeluDevTable t) {
+    grid_dep_wait();  // PDL: predecessor complete and visible
+    grid_dep_launch();
     __shared__ FastTable<NC4> ft;
     const int nseg = t.nseg[0] + t.nseg[1];
     for (int i = threadIdx.x; i < nseg * FastTable<NC4>::kStride4; i += kBlock) {
@@ -587,11 +597,11 @@ cudaError_t launch_gelu_fwd(const float* x, float* y, uint32_t* mask, int64_t n,
         const int64_t warps_needed = ((n >> 8) + U - 1) / U + 1;
         auto k = gelu_fwd8_kernel<U>;
         int grid = grid_for((const void*)k, kBlock, 0, (warps_needed * 32 + kBlock - 1) / kBlock);
-        k<<<grid, kBlock, 0, st>>>(x, y, mask, n, xstar_gt, xs_lo);
+        pdl(k, grid, kBlock, 0, st)(x, y, mask, n, xstar_gt, xs_lo);
     } else {
         int grid = grid_for((const void*)gelu_fwd_scalar_kernel, kBlock, 0,
                             (((n + 31) >> 5) * 32 + kBlock - 1) / kBlock);
-        gelu_fwd_scalar_kernel<<<grid, kBlock, 0, st>>>(x, y, mask, n, xstar_gt, xs_lo);
+        pdl(gelu_fwd_scalar_kernel, grid, kBlock, 0, st)(x, y, mask, n, xstar_gt, xs_lo);
     }
     return cudaGetLastError();
 }
@@ -613,7 +623,7 @@ cudaError_t launch_gelu_bwd(const float* dy, const float* y, const uint32_t* mas
                     : (t.horner ? gelu_bwd_fast_kernel<NC, true, false>                  \
                                 : gelu_bwd_fast_kernel<NC, false, false>);               \
         int grid = grid_for((const void*)k, kBlock, 0, blocks);                           \
-        k<<<grid, kBlock, 0, st>>>(dy, y, mask, dx, n, t);                                \
+        pdl(k, grid, kBlock, 0, st)(dy, y, mask, dx, n, t);                                \
         break;                                                                            \
     }
         switch (nc4) {
@@ -631,9 +641,9 @@ cudaError_t launch_gelu_bwd(const float* dy, const float* y, const uint32_t* mas
     const int64_t warps_needed = vec ? ((n >> 7) + kUnroll - 1) / kUnroll + 1 : (n + 31) >> 5;
     int grid = grid_for(k, kBlock, smem, (warps_needed * 32 + kBlock - 1) / kBlock);
     if (vec) {
-        gelu_bwd_vec_kernel<<<grid, kBlock, smem, st>>>(dy, y, mask, dx, n, t);
+        pdl(gelu_bwd_vec_kernel, grid, kBlock, smem, st)(dy, y, mask, dx, n, t);
     } else {
-        gelu_bwd_scalar_kernel<<<grid, kBlock, smem, st>>>(dy, y, mask, dx, n, t);
+        pdl(gelu_bwd_scalar_kernel, grid, kBlock, smem, st)(dy, y, mask, dx, n, t);
     }
     return cudaGetLastError();
 }

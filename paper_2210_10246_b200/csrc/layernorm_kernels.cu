@@ -100,6 +100,8 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? 3 : 1) ln_fwd_vec_kernel(
     const float* __restrict__ x, const float* __restrict__ gamma, const float* __restrict__ beta,
     double eps, float* __restrict__ y, float* __restrict__ rstd, int64_t rows, int cols,
     int32_t* __restrict__ status) {
+    grid_dep_wait();  // PDL: predecessor complete and visible
+    grid_dep_launch();
     extern __shared__ __align__(128) unsigned char dsm[];
     uint64_t* full = reinterpret_cast<uint64_t*>(dsm);
     float* ring = reinterpret_cast<float*>(dsm + 128);
@@ -196,6 +198,8 @@ __global__ void __launch_bounds__(kWWarps * 32) ln_fwd_warp_kernel(
     const float* __restrict__ x, const float* __restrict__ gamma, const float* __restrict__ beta,
     double eps, float* __restrict__ y, float* __restrict__ rstd, int64_t rows,
     int32_t* __restrict__ status) {
+    grid_dep_wait();  // PDL: predecessor complete and visible
+    grid_dep_launch();
     constexpr int C = VPL * 128;
     extern __shared__ __align__(128) unsigned char dsm[];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -287,6 +291,8 @@ __global__ void __launch_bounds__(256) ln_fwd_generic_kernel(
     const float* __restrict__ x, const float* __restrict__ gamma, const float* __restrict__ beta,
     double eps, float* __restrict__ y, float* __restrict__ rstd, int64_t rows, int cols,
     int32_t* __restrict__ status) {
+    grid_dep_wait();  // PDL: predecessor complete and visible
+    grid_dep_launch();
     __shared__ double red[2 * 32];
     int phase = 0;
     if (status && blockIdx.x == 0) {
@@ -323,6 +329,8 @@ __global__ void __launch_bounds__(NT) ln_bwd_vec_kernel(
     const float* __restrict__ dy, const float* __restrict__ y, const float* __restrict__ rstd,
     const float* __restrict__ gamma, const float* __restrict__ beta, float* __restrict__ dx,
     double* __restrict__ ws, int64_t rows, int cols) {
+    grid_dep_wait();  // PDL: predecessor complete and visible
+    grid_dep_launch();
     // Thread t owns the CPT float4 column groups t, t + blockDim, ... of every
     // row (conflict-free 128-bit smem reads, coalesced stores); more columns
     // per thread amortise the per-row block reduction.
@@ -474,6 +482,7 @@ __global__ void __launch_bounds__(256) ln_bwd_generic_kernel(
     const float* __restrict__ dy, const float* __restrict__ y, const float* __restrict__ rstd,
     const float* __restrict__ gamma, const float* __restrict__ beta, float* __restrict__ dx,
     double* __restrict__ ws, int64_t rows, int cols) {
+    grid_dep_wait();  // PDL: predecessor complete and visible
     grid_dep_launch();
     extern __shared__ double part[];  // [2][cols]
     __shared__ double red[2 * 2 * 32];
@@ -516,7 +525,8 @@ __global__ void __launch_bounds__(1024) ln_param_reduce_kernel(const double* __r
                                                                int nparts, int cols,
                                                                float* __restrict__ dgamma,
                                                                float* __restrict__ dbeta) {
-    grid_dep_wait();
+    grid_dep_wait();  // PDL: predecessor complete and visible
+    grid_dep_launch();
     __shared__ double part[32][33];
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
     const int64_t total = 2 * (int64_t)cols;
@@ -596,7 +606,7 @@ cudaError_t launch_ln_fwd(const float* x, const float* gamma, const float* beta,
     case V: {                                                                                \
         auto k = ln_fwd_warp_kernel<V>;                                                      \
         int grid = grid_for((const void*)k, kWWarps * 32, smem, (rows + kWWarps - 1) / kWWarps); \
-        k<<<grid, kWWarps * 32, smem, st>>>(x, gamma, beta, eps, y, rstd, rows, dev_status); \
+        pdl(k, grid, kWWarps * 32, smem, st)(x, gamma, beta, eps, y, rstd, rows, dev_status); \
         break;                                                                               \
     }
         switch (vpl) {
@@ -613,10 +623,10 @@ cudaError_t launch_ln_fwd(const float* x, const float* gamma, const float* beta,
         size_t smem = fwd_smem(cols);
         auto k = block <= 256 ? ln_fwd_vec_kernel<256> : ln_fwd_vec_kernel<kMaxThreads>;
         int grid = grid_for((const void*)k, block, smem, (rows + kRows - 1) / kRows);
-        k<<<grid, block, smem, st>>>(x, gamma, beta, eps, y, rstd, rows, (int)cols, dev_status);
+        pdl(k, grid, block, smem, st)(x, gamma, beta, eps, y, rstd, rows, (int)cols, dev_status);
     } else {
         int grid = grid_for((const void*)ln_fwd_generic_kernel, 256, 0, rows);
-        ln_fwd_generic_kernel<<<grid, 256, 0, st>>>(x, gamma, beta, eps, y, rstd, rows,
+        pdl(ln_fwd_generic_kernel, grid, 256, 0, st)(x, gamma, beta, eps, y, rstd, rows,
                                                      (int)cols, dev_status);
     }
     return cudaGetLastError();
@@ -648,11 +658,11 @@ cudaError_t launch_ln_bwd(const float* dy, const float* y, const float* rstd, co
         using KFn = void (*)(const float*, const float*, const float*, const float*,
                              const float*, float*, double*, int64_t, int);
         KFn k = reinterpret_cast<KFn>(const_cast<void*>(bwd_vec_fn(cols)));
-        k<<<grid, bwd_threads(cols), bwd_smem(cols), st>>>(dy, y, rstd, gamma, beta, dx, w, rows,
+        pdl(k, grid, bwd_threads(cols), bwd_smem(cols), st)(dy, y, rstd, gamma, beta, dx, w, rows,
                                                            (int)cols);
     } else {
         size_t smem = (size_t)2 * cols * sizeof(double);
-        ln_bwd_generic_kernel<<<grid, 256, smem, st>>>(dy, y, rstd, gamma, beta, dx, w, rows,
+        pdl(ln_bwd_generic_kernel, grid, 256, smem, st)(dy, y, rstd, gamma, beta, dx, w, rows,
                                                        (int)cols);
     }
     const int rgrid = (int)((2 * cols + 31) / 32);

@@ -40,6 +40,8 @@ constexpr int kJumpThreads = 320;
 // Sequence w_0 .. w_{kMtBaseWords-1} from each source state.
 __global__ void __launch_bounds__(kGenThreads) mt_base_kernel(const uint64_t* __restrict__ src,
                                                               uint64_t* __restrict__ base) {
+    grid_dep_wait();  // PDL: predecessor complete and visible
+    grid_dep_launch();
     __shared__ uint64_t ring[kRing];
     const uint64_t* st = src + (size_t)blockIdx.x * kMtN;
     uint64_t* out = base + (size_t)blockIdx.x * kMtBaseWords;
@@ -75,6 +77,8 @@ __global__ void __launch_bounds__(kJumpThreads) mt_jump_kernel(
     const uint64_t* __restrict__ base, const uint16_t* __restrict__ idx,
     const int32_t* __restrict__ off, int poly0, uint64_t* __restrict__ out, int64_t child0,
     int64_t child_lo, int64_t child_hi) {
+    grid_dep_wait();  // PDL: predecessor complete and visible
+    grid_dep_launch();
     __shared__ uint64_t slice[kJumpSlice];
     const int part = blockIdx.x, d = blockIdx.y, s = blockIdx.z;
     const int64_t child = child0 + (int64_t)s * 32 + d;
@@ -114,6 +118,8 @@ __global__ void __launch_bounds__(kGenThreads) mt_keep_kernel(const uint64_t* __
                                                               int64_t k0, uint64_t e_begin,
                                                               uint64_t e_end, uint64_t xmin,
                                                               uint32_t* __restrict__ mask) {
+    grid_dep_wait();  // PDL: predecessor complete and visible
+    grid_dep_launch();
     __shared__ uint64_t ring[kRing];
     const int64_t k = k0 + blockIdx.x;
     const uint64_t* st = states + (size_t)blockIdx.x * kMtN;
@@ -165,6 +171,8 @@ __global__ void __launch_bounds__(kGenThreads) mt_keep_kernel(const uint64_t* __
 
 // std::mersenne_twister_engine::seed on the device (one thread, 312 steps).
 __global__ void mt_seed_kernel(uint64_t seed, uint64_t* __restrict__ st) {
+    grid_dep_wait();  // PDL: predecessor complete and visible
+    grid_dep_launch();
     if (threadIdx.x != 0) return;
     uint64_t v = seed;
     st[0] = v;
@@ -263,7 +271,7 @@ cudaError_t launch_mt_keep_bits(uint64_t seed, double p, uint64_t e_begin, int64
     uint64_t* sb = reinterpret_cast<uint64_t*>(w + L.sb_off);
     uint64_t* base = reinterpret_cast<uint64_t*>(w + L.base_off);
 
-    mt_seed_kernel<<<1, 32, 0, st>>>(seed, seed_st);
+    pdl(mt_seed_kernel, 1, 32, 0, st)(seed, seed_st);
 
     const int64_t k0 = (int64_t)(e_begin / kMtChunk);
     const int64_t k1 = (int64_t)((e_begin + (uint64_t)n - 1) / kMtChunk);
@@ -285,11 +293,11 @@ cudaError_t launch_mt_keep_bits(uint64_t seed, double p, uint64_t e_begin, int64
                                   kMtN * sizeof(uint64_t), cudaMemcpyDeviceToDevice, st);
             if (err != cudaSuccess) return err;
         } else {
-            mt_base_kernel<<<(unsigned)S, kGenThreads, 0, st>>>(cur, base);
+            pdl(mt_base_kernel, (unsigned)S, kGenThreads, 0, st)(cur, base);
             err = cudaMemsetAsync(nxt, 0, (size_t)(chi - clo + 1) * kMtN * sizeof(uint64_t), st);
             if (err != cudaSuccess) return err;
             dim3 grid(kMtJumpParts, 32, (unsigned)S);
-            mt_jump_kernel<<<grid, kJumpThreads, 0, st>>>(base, jidx, joff, l * 31, nxt, lo * 32,
+            pdl(mt_jump_kernel, grid, kJumpThreads, 0, st)(base, jidx, joff, l * 31, nxt, lo * 32,
                                                           clo, chi);
             err = cudaGetLastError();
             if (err != cudaSuccess) return err;
@@ -299,7 +307,7 @@ cudaError_t launch_mt_keep_bits(uint64_t seed, double p, uint64_t e_begin, int64
         hi = chi;
     }
     const uint64_t xmin = mt_keep_threshold(p);
-    mt_keep_kernel<<<(unsigned)(k1 - k0 + 1), kGenThreads, 0, st>>>(cur, k0, e_begin,
+    pdl(mt_keep_kernel, (unsigned)(k1 - k0 + 1), kGenThreads, 0, st)(cur, k0, e_begin,
                                                                    e_begin + (uint64_t)n, xmin,
                                                                    mask);
     return cudaGetLastError();

@@ -49,6 +49,8 @@ __global__ void __launch_bounds__(kBlock) softmax_fwd_vec_kernel(
     const float* __restrict__ z, float* __restrict__ P, float* __restrict__ D,
     uint32_t* __restrict__ mask, double scale, uint64_t thresh, uint64_t seed, uint64_t offset,
     int64_t rows) {
+    grid_dep_wait();  // PDL: predecessor complete and visible
+    grid_dep_launch();
     constexpr int C = VPL * 128;
     constexpr int R = VPL <= 4 ? 2 : 1;  // rows per warp iteration (loads in flight)
     const int lane = threadIdx.x & 31;
@@ -132,6 +134,8 @@ template <int VPL, bool DROP, bool WRITE_D>
 __global__ void __launch_bounds__(kBlock) softmax_bwd_vec_kernel(
     const float* __restrict__ dD, const float* __restrict__ P, const uint32_t* __restrict__ mask,
     double scale, float* __restrict__ dZ, float* __restrict__ D, int64_t rows) {
+    grid_dep_wait();  // PDL: predecessor complete and visible
+    grid_dep_launch();
     constexpr int C = VPL * 128;
     const int lane = threadIdx.x & 31;
     const int64_t warp = ((int64_t)blockIdx.x * kBlock + threadIdx.x) >> 5;
@@ -193,6 +197,8 @@ __global__ void __launch_bounds__(kBlock) softmax_fwd_generic_kernel(
     const float* __restrict__ z, float* __restrict__ P, float* __restrict__ D,
     uint32_t* __restrict__ mask, int mode, double scale, uint64_t thresh, uint64_t seed,
     uint64_t offset, int64_t rows, int64_t C) {
+    grid_dep_wait();  // PDL: predecessor complete and visible
+    grid_dep_launch();
     const int lane = threadIdx.x & 31;
     const int64_t warp = ((int64_t)blockIdx.x * kBlock + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * kBlock) >> 5;
@@ -225,6 +231,8 @@ __global__ void __launch_bounds__(kBlock) softmax_bwd_generic_kernel(
     const float* __restrict__ dD, const float* __restrict__ P, const uint32_t* __restrict__ mask,
     int drop, double scale, float* __restrict__ dZ, float* __restrict__ D, int64_t rows,
     int64_t C) {
+    grid_dep_wait();  // PDL: predecessor complete and visible
+    grid_dep_launch();
     const int lane = threadIdx.x & 31;
     const int64_t warp = ((int64_t)blockIdx.x * kBlock + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * kBlock) >> 5;
@@ -258,7 +266,7 @@ cudaError_t fwd_vec(int vpl, const float* z, float* P, float* D, uint32_t* mask,
     case V: {                                                                                \
         auto k = softmax_fwd_vec_kernel<V, MODE>;                                            \
         int grid = grid_for((const void*)k, kBlock, 0, (rows * 32 + kBlock - 1) / kBlock);  \
-        k<<<grid, kBlock, 0, st>>>(z, P, D, mask, scale, thresh, seed, offset, rows);        \
+        pdl(k, grid, kBlock, 0, st)(z, P, D, mask, scale, thresh, seed, offset, rows);        \
         break;                                                                               \
     }
     switch (vpl) {
@@ -283,7 +291,7 @@ cudaError_t bwd_vec(int vpl, const float* dD, const float* P, const uint32_t* ma
     case V: {                                                                                \
         auto k = softmax_bwd_vec_kernel<V, DROP, WRITE_D>;                                   \
         int grid = grid_for((const void*)k, kBlock, 0, (rows * 32 + kBlock - 1) / kBlock);  \
-        k<<<grid, kBlock, 0, st>>>(dD, P, mask, scale, dZ, D, rows);                         \
+        pdl(k, grid, kBlock, 0, st)(dD, P, mask, scale, dZ, D, rows);                         \
         break;                                                                               \
     }
     switch (vpl) {
@@ -319,8 +327,8 @@ cudaError_t launch_softmax_fwd(const float* z, float* P, int64_t rows, int64_t c
     if (rows == 0 || cols == 0) return cudaSuccess;
     if (vec_ok(cols, 0, {z, P}))
         return fwd_vec<kPlain>((int)(cols / 128), z, P, nullptr, nullptr, 1.0, 0, 0, 0, rows, st);
-    softmax_fwd_generic_kernel<<<generic_grid((const void*)softmax_fwd_generic_kernel, rows),
-                                 kBlock, 0, st>>>(z, P, nullptr, nullptr, kPlain, 1.0, 0, 0, 0,
+    pdl(softmax_fwd_generic_kernel, generic_grid((const void*)softmax_fwd_generic_kernel, rows),
+                                 kBlock, 0, st)(z, P, nullptr, nullptr, kPlain, 1.0, 0, 0, 0,
                                                   rows, cols);
     return cudaGetLastError();
 }
@@ -331,8 +339,8 @@ cudaError_t launch_softmax_bwd(const float* dP, const float* P, float* dZ, int64
     if (vec_ok(cols, 0, {dP, P, dZ}))
         return bwd_vec<false, false>((int)(cols / 128), dP, P, nullptr, 1.0, dZ, nullptr, rows,
                                      st);
-    softmax_bwd_generic_kernel<<<generic_grid((const void*)softmax_bwd_generic_kernel, rows),
-                                 kBlock, 0, st>>>(dP, P, nullptr, 0, 1.0, dZ, nullptr, rows,
+    pdl(softmax_bwd_generic_kernel, generic_grid((const void*)softmax_bwd_generic_kernel, rows),
+                                 kBlock, 0, st)(dP, P, nullptr, 0, 1.0, dZ, nullptr, rows,
                                                   cols);
     return cudaGetLastError();
 }
@@ -351,8 +359,8 @@ cudaError_t launch_softmax_dropout_fwd(const float* z, double scale, uint64_t th
         cudaError_t e = cudaMemsetAsync(mask, 0, (size_t)((rows * cols + 31) / 32) * 4, st);
         if (e != cudaSuccess) return e;
     }
-    softmax_fwd_generic_kernel<<<generic_grid((const void*)softmax_fwd_generic_kernel, rows),
-                                 kBlock, 0, st>>>(z, P, D, mask, philox ? kPhilox : kSupplied,
+    pdl(softmax_fwd_generic_kernel, generic_grid((const void*)softmax_fwd_generic_kernel, rows),
+                                 kBlock, 0, st)(z, P, D, mask, philox ? kPhilox : kSupplied,
                                                   scale, thresh, seed, offset, rows, cols);
     return cudaGetLastError();
 }
@@ -366,8 +374,8 @@ cudaError_t launch_attn_probs_bwd(const float* dD, const float* P, const uint32_
         return D ? bwd_vec<true, true>(vpl, dD, P, mask, scale, dZ, D, rows, st)
                  : bwd_vec<true, false>(vpl, dD, P, mask, scale, dZ, nullptr, rows, st);
     }
-    softmax_bwd_generic_kernel<<<generic_grid((const void*)softmax_bwd_generic_kernel, rows),
-                                 kBlock, 0, st>>>(dD, P, mask, 1, scale, dZ, D, rows, cols);
+    pdl(softmax_bwd_generic_kernel, generic_grid((const void*)softmax_bwd_generic_kernel, rows),
+                                 kBlock, 0, st)(dD, P, mask, 1, scale, dZ, D, rows, cols);
     return cudaGetLastError();
 }
 

@@ -4,6 +4,12 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <utility>
+
+#ifndef TM_PDL
+#define TM_PDL 0
+#endif
+
 #include "../../include/tempo_b200.h"
 
 namespace tb {
@@ -98,6 +104,40 @@ cudaError_t launch_pdl(const void* kernel, int grid, int block, size_t smem, cud
 size_t mt_keep_workspace(uint64_t e_begin, int64_t n);
 cudaError_t launch_mt_keep_bits(uint64_t seed, double p, uint64_t e_begin, int64_t n,
                                 uint32_t* mask, void* ws, size_t ws_bytes, cudaStream_t st);
+
+// Type-checked launch: pdl(kernel, grid, block, smem, stream)(args...) is
+// `kernel<<<grid, block, smem, stream>>>(args...)`, with programmatic stream
+// serialization when TM_PDL=1.  Every kernel of this library starts with
+// grid_dep_wait() (before any global access), which makes PDL safe after any
+// predecessor -- but measured on the bench chain it LOST ~10 % (2.14 ->
+// 2.36-2.44 ms/step), so it is off by default; only the LayerNorm stage-2
+// reduce is launched as a dependent (launch_pdl), where it wins ~2 us.
+template <typename... KArgs>
+struct PdlLaunch {
+    void (*kernel)(KArgs...);
+    cudaLaunchConfig_t cfg;
+    cudaLaunchAttribute attr[1];
+    template <typename... A>
+    cudaError_t operator()(A&&... a) {
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        return cudaLaunchKernelEx(&cfg, kernel, std::forward<A>(a)...);
+    }
+};
+template <typename... KArgs>
+PdlLaunch<KArgs...> pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                        cudaStream_t st) {
+    PdlLaunch<KArgs...> L;
+    L.kernel = kernel;
+    L.cfg = cudaLaunchConfig_t{};
+    L.cfg.gridDim = grid;
+    L.cfg.blockDim = block;
+    L.cfg.dynamicSmemBytes = smem;
+    L.cfg.stream = st;
+    L.attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    L.attr[0].val.programmaticStreamSerializationAllowed = TM_PDL;
+    return L;
+}
 
 // Persistent-grid sizing: SM count x resident CTAs per SM (cached per device).
 // cap_per_sm > 0 limits the CTAs per SM (fewer, longer-lived CTAs).
