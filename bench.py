@@ -403,7 +403,7 @@ def main():
     peak, peak_kind = peaks()
 
     # ---- per-op device times (outside the timed region) -------------------
-    per_op = chain.per_op_timings(reps=5, flush=flush)
+    per_op = chain.per_op_timings(reps=11, flush=flush)
     ob = op_bytes()
     per_op_rows = []
     for name, (t_ms, mult) in per_op.items():

@@ -438,7 +438,7 @@ __device__ __forceinline__ float gelu_h_fast(float y, uint32_t m, const FastTabl
 template <int NC4, bool HORNER, bool V8>
 __global__ void __launch_bounds__(kBlock) gelu_bwd_fast_kernel(
     const float* __restrict__ dy, const float* __restrict__ y, const uint32_t* __restrict__ mask,
-    float* __restrict__ dx, int64_t n, const __grid_constant__ GeluDevTable t) {
+    float* __restrict__ dx, int64_t n, const __grid_constant__ GeluDevTable t, int vec) {
     grid_dep_wait();  // PDL: predecessor complete and visible
     grid_dep_launch();
     __shared__ FastTable<NC4> ft;
@@ -480,7 +480,9 @@ __global__ void __launch_bounds__(kBlock) gelu_bwd_fast_kernel(
         // vector of y, of dy and of dx) and reads its own mask byte.
         constexpr int U = TM_GELU_BWD_U8;
         const uint8_t* mask8 = reinterpret_cast<const uint8_t*>(mask);
-        const int64_t nchunks = n >> 8;
+        // vec == 0 (pointers not 32-byte aligned): everything through the
+        // scalar loop below -- the same evaluator, so the same bits
+        const int64_t nchunks = vec ? (n >> 8) : 0;
         const int64_t ngroups = nchunks / U;
         struct Group {
             F8 g[U], v[U];
@@ -610,11 +612,15 @@ cudaError_t launch_gelu_bwd(const float* dy, const float* y, const uint32_t* mas
                             const GeluDevTable& t, float* dx, int64_t n, cudaStream_t st) {
     if (n == 0) return cudaSuccess;
     const bool vec = aligned16(dy) && aligned16(y) && aligned16(dx) && aligned16(mask);
-    const bool fast = vec && t.nseg[0] <= kFastSegPerBranch && t.nseg[1] <= kFastSegPerBranch &&
+    // tables within the fast evaluator's limits always use it (any alignment:
+    // the 256-bit, float4 and scalar loops share gelu_h_fast -> same bits)
+    const bool fast = t.nseg[0] <= kFastSegPerBranch && t.nseg[1] <= kFastSegPerBranch &&
                       t.ncoef <= 16;
     if (fast) {
         const int nc4 = (t.ncoef + 3) / 4;
-        const bool v8 = TM_GELU_BWD_V8 && aligned32(dy) && aligned32(y) && aligned32(dx);
+        const bool v8a = TM_GELU_BWD_V8 && aligned32(dy) && aligned32(y) && aligned32(dx);
+        const bool v8 = v8a || !vec;  // unaligned: the V8 kernel's scalar loop
+        const int vflag = v8a ? 1 : 0;
         const int64_t blocks = ((n >> 7) / 2 + 1) * 32 / kBlock + 1;
 #define TB_CASE(NC)                                                                       \
     case NC: {                                                                            \
@@ -623,7 +629,7 @@ cudaError_t launch_gelu_bwd(const float* dy, const float* y, const uint32_t* mas
                     : (t.horner ? gelu_bwd_fast_kernel<NC, true, false>                  \
                                 : gelu_bwd_fast_kernel<NC, false, false>);               \
         int grid = grid_for((const void*)k, kBlock, 0, blocks);                           \
-        pdl(k, grid, kBlock, 0, st)(dy, y, mask, dx, n, t);                                \
+        pdl(k, grid, kBlock, 0, st)(dy, y, mask, dx, n, t, vflag);                         \
         break;                                                                            \
     }
         switch (nc4) {

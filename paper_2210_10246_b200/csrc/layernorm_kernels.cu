@@ -30,6 +30,9 @@ namespace tb {
 namespace {
 
 constexpr int kRows = 4;           // rows in flight per CTA iteration (forward)
+#ifndef TM_LN_BWD_CPT2
+#define TM_LN_BWD_CPT2 0
+#endif
 #ifndef TM_LN_BWD_ROWS
 #define TM_LN_BWD_ROWS 4
 #endif
@@ -566,7 +569,7 @@ bool use_vec(int64_t cols, const void* a, const void* b, const void* c, const vo
 
 int vec_threads(int64_t cols) { return (int)(((cols / 4) + 31) / 32 * 32); }
 // backward: two float4 column groups per thread when cols % 8 == 0
-int bwd_cpt(int64_t) { return 1; }  // 2 column groups/thread measured slower (r1)
+int bwd_cpt(int64_t cols) { return (TM_LN_BWD_CPT2 && cols % 8 == 0) ? 2 : 1; }
 int bwd_threads(int64_t cols) {
     return (int)(((cols / 4 + bwd_cpt(cols) - 1) / bwd_cpt(cols) + 31) / 32 * 32);
 }

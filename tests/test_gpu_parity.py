@@ -424,3 +424,40 @@ def test_mask_pack_roundtrip(tops, cuda):
     st = torch.zeros(1, dtype=torch.int32, device=cuda)
     tops.pack_mask(to_dev(np.array([0, 1, 2], np.uint8), cuda), dev_status=st)
     assert int(st.item()) == 3  # BoolMask::from_bytes refuses bytes > 1
+
+
+def _at_offset(t, k):
+    """A copy of 1-D tensor t whose storage starts k floats past a 256-byte
+    aligned allocation (k = 0: 32B-aligned -> 256-bit paths; 4: 16B-aligned ->
+    float4 paths; 1: 4B-aligned -> scalar paths)."""
+    import torch
+    buf = torch.empty(t.numel() + 64, device=t.device, dtype=t.dtype)
+    out = buf[k:k + t.numel()]
+    out.copy_(t)
+    return out
+
+
+@pytest.mark.parametrize("n", [4096 * 37 + 77, 1 << 20])
+def test_vector_paths_agree_bitwise(tops, table_text, cuda, n):
+    """Every kernel path (256-bit lanes, float4 lanes, scalar) gives the same
+    bits on the same data: GELU fwd (y + mask, incl. fp64-window elements),
+    GELU bwd, dropout fwd (supplied mask) and bwd."""
+    import torch
+    table = tops.GeluTable(table_text)
+    g = torch.Generator(device=cuda).manual_seed(5)
+    x = torch.randn(n, device=cuda, generator=g) * 2
+    x[::97] = -0.7517915  # many elements in the fp64 window around x*
+    dy = torch.randn(n, device=cuda, generator=g)
+    res = []
+    for k in (0, 4, 1):
+        xk, dyk = _at_offset(x, k), _at_offset(dy, k)
+        y, m = tops.gelu_ip_fwd(xk, table)
+        dx = tops.gelu_ip_bwd(dyk, _at_offset(y, k), m, table)
+        keep = torch.from_numpy(tops.bernoulli_keep_bits(n, 0.1, 9).view(np.int32)).to(cuda)
+        d, _ = tops.dropout_fwd(xk, 0.1, mask=keep)
+        dd = tops.dropout_bwd(dyk, keep, 0.1)
+        res.append((y.clone(), m.clone(), dx.clone(), d.clone(), dd.clone()))
+    torch.cuda.synchronize()
+    for other in res[1:]:
+        for a, b in zip(res[0], other):
+            assert torch.equal(a, b)
