@@ -42,6 +42,7 @@ def main():
         "ln_bwd": (lambda: o.layernorm_ip_bwd(c.dy_ln1, c.y_ln1, c.rs1, c.g1, c.b1, dx=c.dx_ln1, dgamma=dp[:H], dbeta=dp[H:2 * H], workspace=c.ws), [c.dx_ln1, dp[:2 * H]]),
         "dropout_fwd": (lambda: o.dropout_fwd(c.x_ffn2, bench.P_DROP, mask=c.m2, generate=True, seed=9, y=c.d2), [c.d2, c.m2]),
         "mt_mask": (lambda: o.bernoulli_keep_bits_device(c.z.numel(), bench.P_DROP, 7, out=c.m_att), [c.m_att]),
+        "mt_mask_h": (lambda: o.bernoulli_keep_bits_device(c.x_ffn2.numel(), bench.P_DROP, 7, out=c.m2), [c.m2]),
         "copy_g": (lambda: c.y_g.copy_(c.x_ffn1), [c.y_g[:1]]),
         "copy_h": (lambda: c.d2.copy_(c.x_ffn2), [c.d2[:1]]),
         "dropout_bwd": (lambda: o.dropout_bwd(c.dx_ln2, c.m2, bench.P_DROP, dx=c.dx_d2), [c.dx_d2]),
@@ -49,6 +50,7 @@ def main():
     ob = bench.op_bytes()
     ob["copy_g"] = 8 * c.x_ffn1.numel()
     ob["mt_mask"] = c.z.numel() / 8
+    ob["mt_mask_h"] = c.x_ffn2.numel() / 8
     ob["copy_h"] = 2 * 8 * c.x_ffn2.numel()
     names = {"ln_fwd": "layernorm_fwd", "ln_bwd": "layernorm_bwd"}
     reps = int(os.environ.get("REPS", "20"))
