@@ -370,7 +370,8 @@ int check_rows(int64_t rows, int64_t cols, const char* what) {
 
 namespace tb {
 
-int grid_for(const void* kernel, int block, size_t smem, int64_t work_items, int cap_per_sm) {
+int grid_for(const void* kernel, int block, size_t smem, int64_t work_items, int cap_per_sm,
+             int waves) {
     static std::mutex mu;
     static std::map<std::tuple<int, const void*, int, size_t>, int> cache;
     static std::map<std::pair<int, const void*>, bool> optin;  // per (device, kernel)
@@ -406,7 +407,7 @@ int grid_for(const void* kernel, int block, size_t smem, int64_t work_items, int
         }
     }
     if (cap_per_sm > 0 && per_sm > cap_per_sm) per_sm = cap_per_sm;
-    int64_t full = (int64_t)per_sm * sms;
+    int64_t full = (int64_t)per_sm * sms * (waves > 1 ? waves : 1);
     if (work_items < 1) work_items = 1;
     return (int)std::min<int64_t>(full, work_items);
 }

@@ -140,7 +140,10 @@ PdlLaunch<KArgs...> pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t 
 }
 
 // Persistent-grid sizing: SM count x resident CTAs per SM (cached per device).
-// cap_per_sm > 0 limits the CTAs per SM (fewer, longer-lived CTAs).
-int grid_for(const void* kernel, int block, size_t smem, int64_t work_items, int cap_per_sm = 0);
+// cap_per_sm > 0 limits the CTAs per SM (fewer, longer-lived CTAs); waves > 1
+// launches that many resident-capacity waves (CTAs that finish early are
+// replaced by fresh ones: load balance for loops without prefetch).
+int grid_for(const void* kernel, int block, size_t smem, int64_t work_items, int cap_per_sm = 0,
+             int waves = 1);
 
 }  // namespace tb
