@@ -20,6 +20,9 @@ constexpr int kUnroll = 4;
 #ifndef TM_DROPOUT_V8
 #define TM_DROPOUT_V8 1
 #endif
+#ifndef TM_DROPOUT_WAVES
+#define TM_DROPOUT_WAVES 8
+#endif
 #ifndef TM_DROPOUT_U8
 #define TM_DROPOUT_U8 1
 #endif
@@ -260,7 +263,10 @@ cudaError_t fwd(const float* x, double scale, uint64_t thresh, uint32_t* mask, u
         constexpr int U = TM_DROPOUT_U8;
         auto k = dropout_fwd8_kernel<PHILOX, U>;
         const int64_t warps = ((n >> 8) + U - 1) / U + 1;
-        int grid = grid_for((const void*)k, kBlock, 0, (warps * 32 + kBlock - 1) / kBlock);
+        // supplied masks: several waves of CTAs balance better; Philox (more
+        // work per element) keeps one persistent wave
+        int grid = grid_for((const void*)k, kBlock, 0, (warps * 32 + kBlock - 1) / kBlock, 0,
+                            PHILOX ? 1 : TM_DROPOUT_WAVES);
         pdl(k, grid, kBlock, 0, st)(x, mask, scale, thresh, seed, offset, y, n);
         return cudaGetLastError();
     }

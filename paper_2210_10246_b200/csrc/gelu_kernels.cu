@@ -30,6 +30,9 @@ namespace {
 #else
 #define TM_GELU_FWD_BOUNDS __launch_bounds__(256)
 #endif
+#ifndef TM_GELU_WAVES
+#define TM_GELU_WAVES 1
+#endif
 #ifndef TM_GELU_FWD_U8
 #define TM_GELU_FWD_U8 4
 #endif
@@ -598,7 +601,8 @@ cudaError_t launch_gelu_fwd(const float* x, float* y, uint32_t* mask, int64_t n,
         constexpr int U = TM_GELU_FWD_U8;
         const int64_t warps_needed = ((n >> 8) + U - 1) / U + 1;
         auto k = gelu_fwd8_kernel<U>;
-        int grid = grid_for((const void*)k, kBlock, 0, (warps_needed * 32 + kBlock - 1) / kBlock);
+        int grid = grid_for((const void*)k, kBlock, 0, (warps_needed * 32 + kBlock - 1) / kBlock, 0,
+                            TM_GELU_WAVES);
         pdl(k, grid, kBlock, 0, st)(x, y, mask, n, xstar_gt, xs_lo);
     } else {
         int grid = grid_for((const void*)gelu_fwd_scalar_kernel, kBlock, 0,
@@ -628,7 +632,7 @@ cudaError_t launch_gelu_bwd(const float* dy, const float* y, const uint32_t* mas
                             : gelu_bwd_fast_kernel<NC, false, true>)                     \
                     : (t.horner ? gelu_bwd_fast_kernel<NC, true, false>                  \
                                 : gelu_bwd_fast_kernel<NC, false, false>);               \
-        int grid = grid_for((const void*)k, kBlock, 0, blocks);                           \
+        int grid = grid_for((const void*)k, kBlock, 0, blocks, 0, TM_GELU_WAVES);         \
         pdl(k, grid, kBlock, 0, st)(dy, y, mask, dx, n, t, vflag);                         \
         break;                                                                            \
     }

@@ -30,6 +30,9 @@ namespace tb {
 namespace {
 
 constexpr int kRows = 4;           // rows in flight per CTA iteration (forward)
+#ifndef TM_LN_WAVES
+#define TM_LN_WAVES 8  // forward warp kernel: 8 waves measured 6 % faster than 1
+#endif
 #ifndef TM_LN_BWD_CPT2
 #define TM_LN_BWD_CPT2 0
 #endif
@@ -608,7 +611,7 @@ cudaError_t launch_ln_fwd(const float* x, const float* gamma, const float* beta,
 #define TB_LNW(V)                                                                            \
     case V: {                                                                                \
         auto k = ln_fwd_warp_kernel<V>;                                                      \
-        int grid = grid_for((const void*)k, kWWarps * 32, smem, (rows + kWWarps - 1) / kWWarps); \
+        int grid = grid_for((const void*)k, kWWarps * 32, smem, (rows + kWWarps - 1) / kWWarps, 0, TM_LN_WAVES); \
         pdl(k, grid, kWWarps * 32, smem, st)(x, gamma, beta, eps, y, rstd, rows, dev_status); \
         break;                                                                               \
     }
