@@ -358,10 +358,17 @@ def main():
 
     import torch
     import torch.distributed as dist
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    # TEMPO_BENCH_BACKEND=gloo: a functional check of the N>1 path on fewer
+    # GPUs than ranks (ranks share devices; the numbers are then meaningless)
+    backend = os.environ.get("TEMPO_BENCH_BACKEND", "nccl")
+    local_dev = local % max(1, torch.cuda.device_count()) if backend == "gloo" else local
+    torch.cuda.set_device(local_dev)
+    dev = torch.device("cuda", local_dev)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     chain = Chain(dev, rank, world)
     chain.mask_mode = args.masks
     from paper_2210_10246_b200.dist import allreduce_ln_params
