@@ -172,6 +172,10 @@ int tempo_dropout_fwd(const float* x, double p, tempo_mask_mode_t mode, uint32_t
 int tempo_dropout_bwd(const float* dy, const uint32_t* mask, double p, float* dx, int64_t n,
                       tempo_stream_t stream);
 
+/* out = float(double(a) * c): tempo::scale (kernels.cpp:209-213), used by
+ * Graph::scale (the 1/sqrt(d) of tempo_ops::sdpa).  out may alias a. */
+int tempo_tensor_scale(const float* a, double c, float* out, int64_t n, tempo_stream_t stream);
+
 /* out = a + b elementwise: the gradient accumulation at fan-out of
  * Tape::backward (tape.cpp:225-226 via tempo::add, kernels.cpp:183-186).
  * out may alias a or b. */

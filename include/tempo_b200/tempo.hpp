@@ -266,6 +266,19 @@ struct Graph {
     const Tensor& value(NodeId id) const { return tape.value(id); }
     // Stash helper honoring the producer's output recipe (graph.cpp:23-30).
     LazyStash input_stash(NodeId in, StashRole role) const;
+
+    // Generic nodes of graph.hpp:35-44 that tempo_ops::sdpa composes.  The
+    // GEMMs are plain library GEMMs (cuBLAS, fp32 pedantic: no TF32), batched
+    // over equal leading dims; they stash both inputs (through input_stash,
+    // so a dropout_recompute producer is rebuilt on demand in the backward).
+    // [.., m, k] x [.., k, n]
+    NodeId matmul(NodeId a, NodeId b, std::string tag = "");
+    // [.., m, k] x [.., n, k]^T
+    NodeId matmul_nt(NodeId a, NodeId b, std::string tag = "");
+    // c * a, no stash (graph.cpp:73-80)
+    NodeId scale(NodeId a, double c, std::string tag = "");
+    // a + b, no stash (graph.cpp:82-89)
+    NodeId add(NodeId a, NodeId b, std::string tag = "");
 };
 
 // ---- Tempo operators (ops_tempo.hpp:33-63) ---------------------------------
@@ -286,6 +299,10 @@ NodeId softmax_dropout(Graph& g, NodeId z, double p, BoolMask mask, std::uint64_
                        const std::string& drop_tag, const std::string& mask_tag,
                        NodeId* probs_out);
 void ensure_recompute_rules();
+// ops_tempo.cpp:196-210: q k^T -> scale 1/sqrt(d) -> softmax-ip ->
+// dropout_recompute -> x v, on [B, A, S, d] inputs (DimensionError otherwise).
+NodeId sdpa(Graph& g, NodeId q, NodeId k, NodeId v, double p, BoolMask mask,
+            const std::string& prefix = "");
 }  // namespace tempo_ops
 
 namespace ref_ops {

@@ -63,6 +63,7 @@ SIGNATURES = {
     "tempo_dropout_fwd": (C.c_int, [_vp, _dbl, C.c_int, _vp, _u64, _u64, _vp, _i64, _vp]),
     "tempo_dropout_bwd": (C.c_int, [_vp, _vp, _dbl, _vp, _i64, _vp]),
     "tempo_tensor_add": (C.c_int, [_vp, _vp, _vp, _i64, _vp]),
+    "tempo_tensor_scale": (C.c_int, [_vp, _dbl, _vp, _i64, _vp]),
     "tempo_mask_pack": (C.c_int, [_vp, _vp, _i64, _vp, _vp]),
     "tempo_mask_unpack": (C.c_int, [_vp, _vp, _i64, _vp]),
     "tempo_bernoulli_keep_bits_host": (C.c_int, [_i64, _dbl, _u64, _vp]),

@@ -2,12 +2,19 @@
 // (include/tempo_b200/tempo.hpp).  Types and control flow follow the
 // reference (tensor.cpp, ledger.cpp, tape.cpp, graph.cpp, ops_tempo.cpp,
 // ops_reference.cpp); every numeric op is a call through the C-ABI
-// (include/tempo_b200.h) into the sm_100a kernels -- there is no host math.
+// (include/tempo_b200.h) into the sm_100a kernels -- there is no host math;
+// the GEMMs of Graph::matmul/matmul_nt (sdpa) are plain cuBLAS calls.
+#include <cublas_v2.h>
+
 #include "../../include/tempo_b200/tempo.hpp"
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
+#include <cmath>
 #include <fstream>
+#include <map>
+#include <mutex>
 #include <sstream>
 
 namespace tempo_b200 {
@@ -521,6 +528,151 @@ LazyStash Graph::input_stash(NodeId in, StashRole role) const {
     return LazyStash::materialized(producer.tag, role, producer.value);
 }
 
+// ---- generic nodes (graph.cpp:32-89) ---------------------------------------------
+namespace {
+std::string fallback_tag(std::string tag, const char* op, std::size_t id) {
+    if (!tag.empty()) return tag;
+    return std::string(op) + "_" + std::to_string(id);
+}
+
+cublasHandle_t blas(tempo_stream_t st) {
+    static std::mutex mu;
+    static std::map<int, cublasHandle_t> handles;
+    int dev = 0;
+    cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+    std::lock_guard<std::mutex> lock(mu);
+    cublasHandle_t& h = handles[dev];
+    if (!h) {
+        if (cublasCreate(&h) != CUBLAS_STATUS_SUCCESS) throw StateError("cublasCreate failed");
+        cublasSetMathMode(h, CUBLAS_PEDANTIC_MATH);  // true fp32, never TF32
+    }
+    cublasSetStream(h, static_cast<cudaStream_t>(st));
+    return h;
+}
+
+// Row-major batched C[b] = op_a(A[b]) * op_b(B[b]) (m x n, inner k) as the
+// column-major product C^T = op_b(B)^T op_a(A)^T.
+void gemm(tempo_stream_t st, bool ta, bool tb, std::int64_t batch, std::int64_t m,
+          std::int64_t n, std::int64_t k, const float* A, const float* B, float* C) {
+    if (batch == 0 || m == 0 || n == 0) return;
+    if (k == 0) {
+        cuda_check(cudaMemsetAsync(C, 0, (size_t)(batch * m * n) * 4,
+                                   static_cast<cudaStream_t>(st)), "cudaMemsetAsync");
+        return;
+    }
+    const float one = 1.0f, zero = 0.0f;
+    const int lda = (int)(ta ? m : k), ldb = (int)(tb ? k : n);
+    cublasStatus_t r = cublasSgemmStridedBatched(
+        blas(st), tb ? CUBLAS_OP_T : CUBLAS_OP_N, ta ? CUBLAS_OP_T : CUBLAS_OP_N, (int)n, (int)m,
+        (int)k, &one, B, ldb, (long long)(k * n), A, lda, (long long)(m * k), &zero, C, (int)n,
+        (long long)(m * n), (int)batch);
+    if (r != CUBLAS_STATUS_SUCCESS) throw StateError("cublasSgemmStridedBatched failed");
+}
+
+struct MatDims {
+    std::int64_t batch, r, c;
+};
+MatDims mat_dims(const Shape& s, const char* what) {
+    if (s.size() < 2) throw DimensionError(std::string(what) + " needs rank >= 2, got " + shape_str(s));
+    std::int64_t b = 1;
+    for (size_t i = 0; i + 2 < s.size(); ++i) b *= s[i];
+    return {b, s[s.size() - 2], s.back()};
+}
+void same_batch(const Shape& a, const Shape& b, const char* what) {
+    if (a.size() != b.size() || !std::equal(a.begin(), a.end() - 2, b.begin()))
+        throw DimensionError(std::string(what) + " needs equal leading dims, got " +
+                             shape_str(a) + " and " + shape_str(b));
+}
+Shape with_last2(const Shape& s, std::int64_t r, std::int64_t c) {
+    Shape o = s;
+    o[o.size() - 2] = r;
+    o.back() = c;
+    return o;
+}
+// c = a b (nn), a b^T (nt), a^T b (tn) on device tensors
+Tensor mm(tempo_stream_t st, const Tensor& a, const Tensor& b, bool ta, bool tb) {
+    same_batch(a.shape(), b.shape(), "matmul");
+    MatDims da = mat_dims(a.shape(), "matmul"), db = mat_dims(b.shape(), "matmul");
+    const std::int64_t m = ta ? da.c : da.r, k = ta ? da.r : da.c;
+    const std::int64_t kb = tb ? db.c : db.r, n = tb ? db.r : db.c;
+    if (k != kb)
+        throw DimensionError("matmul inner dims differ: " + shape_str(a.shape()) + " and " +
+                             shape_str(b.shape()));
+    Tensor c = Tensor::empty(with_last2(a.shape(), m, n));
+    gemm(st, ta, tb, da.batch, m, n, k, a.data(), b.data(), c.data());
+    return c;
+}
+}  // namespace
+
+NodeId Graph::matmul(NodeId a, NodeId b, std::string tag) {  // graph.cpp:32-51
+    const Tensor& va = tape.value(a);
+    const Tensor& vb = tape.value(b);
+    if (va.shape().size() != vb.shape().size())
+        throw DimensionError("graph matmul needs equal-rank operands, got " +
+                             shape_str(va.shape()) + " and " + shape_str(vb.shape()));
+    Tensor out = mm(stream, va, vb, false, false);
+    tag = fallback_tag(std::move(tag), "matmul", tape.size());
+    tempo_stream_t st = stream;
+    return tape.record("matmul", tag, {a, b}, out,
+                       {input_stash(a, StashRole::SharedDownstream),
+                        input_stash(b, StashRole::SharedDownstream)},
+                       [st](BackwardCtx& ctx) -> std::vector<Tensor> {
+                           const Tensor& g = ctx.grad_out();
+                           Tensor da = mm(st, g, ctx.stash(1), false, true);
+                           Tensor db = mm(st, ctx.stash(0), g, true, false);
+                           return {da, db};
+                       });
+}
+
+NodeId Graph::matmul_nt(NodeId a, NodeId b, std::string tag) {  // graph.cpp:53-71
+    const Tensor& va = tape.value(a);
+    const Tensor& vb = tape.value(b);
+    if (va.shape().size() != vb.shape().size())
+        throw DimensionError("graph matmul_nt needs equal-rank operands, got " +
+                             shape_str(va.shape()) + " and " + shape_str(vb.shape()));
+    Tensor out = mm(stream, va, vb, false, true);
+    tag = fallback_tag(std::move(tag), "matmul_nt", tape.size());
+    tempo_stream_t st = stream;
+    return tape.record("matmul_nt", tag, {a, b}, out,
+                       {input_stash(a, StashRole::SharedDownstream),
+                        input_stash(b, StashRole::SharedDownstream)},
+                       [st](BackwardCtx& ctx) -> std::vector<Tensor> {
+                           // c = a b^T: da = g b, db = g^T a
+                           const Tensor& g = ctx.grad_out();
+                           Tensor da = mm(st, g, ctx.stash(1), false, false);
+                           Tensor db = mm(st, g, ctx.stash(0), true, false);
+                           return {da, db};
+                       });
+}
+
+NodeId Graph::scale(NodeId a, double c, std::string tag) {  // graph.cpp:73-80
+    const Tensor& va = tape.value(a);
+    Tensor out = Tensor::empty(va.shape());
+    check(tempo_tensor_scale(va.data(), c, out.data(), va.numel(), stream));
+    tag = fallback_tag(std::move(tag), "scale", tape.size());
+    tempo_stream_t st = stream;
+    return tape.record("scale", tag, {a}, out, {},
+                       [c, st](BackwardCtx& ctx) -> std::vector<Tensor> {
+                           const Tensor& g = ctx.grad_out();
+                           Tensor d = Tensor::empty(g.shape());
+                           check(tempo_tensor_scale(g.data(), c, d.data(), g.numel(), st));
+                           return {d};
+                       });
+}
+
+NodeId Graph::add(NodeId a, NodeId b, std::string tag) {  // graph.cpp:82-89
+    const Tensor& va = tape.value(a);
+    const Tensor& vb = tape.value(b);
+    require_same_shape(va.shape(), vb.shape(), "add");
+    Tensor out = Tensor::empty(va.shape());
+    check(tempo_tensor_add(va.data(), vb.data(), out.data(), va.numel(), stream));
+    tag = fallback_tag(std::move(tag), "add", tape.size());
+    return tape.record("add", tag, {a, b}, out, {},
+                       [](BackwardCtx& ctx) -> std::vector<Tensor> {
+                           return {ctx.grad_out(), ctx.grad_out()};
+                       });
+}
+
 // ---- operators (ops_tempo.cpp, ops_reference.cpp) ---------------------------------
 namespace tempo_ops {
 
@@ -698,6 +850,19 @@ NodeId softmax_dropout(Graph& g, NodeId z, double p, BoolMask mask, std::uint64_
                               });
     if (probs_out) *probs_out = pn;
     return record_dropout_recompute(g, pn, D, p, mask, drop_tag, mask_tag);
+}
+
+NodeId sdpa(Graph& g, NodeId q, NodeId k, NodeId v, double p, BoolMask mask,
+            const std::string& prefix) {  // ops_tempo.cpp:196-210
+    const Shape& qs = g.value(q).shape();
+    if (qs.size() != 4) throw DimensionError("sdpa expects [B,A,S,d] inputs, got " + shape_str(qs));
+    const std::int64_t d = qs.back();
+    NodeId raw = g.matmul_nt(q, k, prefix + "scores_raw");
+    NodeId scores = g.scale(raw, 1.0 / std::sqrt(double(d)), prefix + "scores");
+    NodeId probs = softmax(g, scores, prefix + "probs");
+    NodeId drop = dropout_recompute(g, probs, p, std::move(mask), prefix + "drop_out",
+                                    prefix + "drop_mask");
+    return g.matmul(drop, v, prefix + "context_heads");
 }
 
 }  // namespace tempo_ops

@@ -297,6 +297,83 @@ static void test_hidden_dropout() {
     CHECK(throws<ParamError>([&] { ref_ops::dropout(g, x, 1.0, mask, "d2", "m2"); }));
 }
 
+// tempo_ops::sdpa (ops_tempo.cpp:196-210): cuBLAS GEMMs around the Tempo
+// softmax + dropout_recompute, forward and all three input gradients against
+// a host fp64 restatement; the dropped-out map is recomputed, not stashed.
+static void test_sdpa() {
+    const std::int64_t B = 2, A = 2, S = 128, d = 32;
+    const double p = 0.25, sc = 1.0 / std::sqrt((double)d), keep_s = 1.0 / (1.0 - p);
+    const std::int64_t nq = B * A * S * d, ns = B * A * S * S;
+    std::vector<float> qh = randn(nq, 21), kh = randn(nq, 22), vh = randn(nq, 23), gh = randn(nq, 24);
+    BoolMask mask = BoolMask::bernoulli_keep({B, A, S, S}, p, 25);
+    std::vector<std::uint8_t> mk = mask.to_bytes();
+    Graph g;
+    NodeId q = g.leaf(Tensor::from_host({B, A, S, d}, qh), "q");
+    NodeId k = g.leaf(Tensor::from_host({B, A, S, d}, kh), "k");
+    NodeId v = g.leaf(Tensor::from_host({B, A, S, d}, vh), "v");
+    NodeId o = tempo_ops::sdpa(g, q, k, v, p, mask, "attn_");
+    auto tags = g.ledger.live_by_tag();
+    CHECK(tags.count("attn_drop_out") == 0);         // D is never stashed
+    CHECK(tags.at("attn_probs") == ns * 4);           // P (fp32)
+    CHECK(tags.at("attn_drop_mask") == ns / 8);       // bits
+    std::vector<float> oh = g.value(o).to_host();
+    GradientMap gm = g.tape.backward(o, Tensor::from_host({B, A, S, d}, gh));
+    std::vector<float> dq = gm.at(q).to_host(), dk = gm.at(k).to_host(), dv = gm.at(v).to_host();
+    double worst = 0.0;
+    for (std::int64_t h = 0; h < B * A; ++h) {
+        const float *Q = &qh[h * S * d], *K = &kh[h * S * d], *V = &vh[h * S * d], *G = &gh[h * S * d];
+        const std::uint8_t* M = &mk[h * S * S];
+        std::vector<double> P(S * S), D(S * S), dD(S * S), dS(S * S);
+        for (std::int64_t i = 0; i < S; ++i) {
+            double mx = -1e300;
+            for (std::int64_t j = 0; j < S; ++j) {
+                double a = 0;
+                for (std::int64_t t = 0; t < d; ++t) a += (double)Q[i * d + t] * K[j * d + t];
+                P[i * S + j] = a * sc;
+                mx = std::max(mx, P[i * S + j]);
+            }
+            double sum = 0;
+            for (std::int64_t j = 0; j < S; ++j) sum += (P[i * S + j] = std::exp(P[i * S + j] - mx));
+            for (std::int64_t j = 0; j < S; ++j) {
+                P[i * S + j] /= sum;
+                D[i * S + j] = M[i * S + j] ? P[i * S + j] * keep_s : 0.0;
+            }
+        }
+        for (std::int64_t i = 0; i < S; ++i)
+            for (std::int64_t t = 0; t < d; ++t) {
+                double a = 0;
+                for (std::int64_t j = 0; j < S; ++j) a += D[i * S + j] * V[j * d + t];
+                worst = std::max(worst, rel_err(oh[h * S * d + i * d + t], a));
+            }
+        for (std::int64_t i = 0; i < S; ++i) {  // dD = G V^T, dP, dS = P (dP - rowsum)
+            double dot = 0;
+            for (std::int64_t j = 0; j < S; ++j) {
+                double a = 0;
+                for (std::int64_t t = 0; t < d; ++t) a += (double)G[i * d + t] * V[j * d + t];
+                dD[i * S + j] = M[i * S + j] ? a * keep_s : 0.0;
+                dot += dD[i * S + j] * P[i * S + j];
+            }
+            for (std::int64_t j = 0; j < S; ++j) dS[i * S + j] = P[i * S + j] * (dD[i * S + j] - dot) * sc;
+        }
+        for (std::int64_t i = 0; i < S; ++i)
+            for (std::int64_t t = 0; t < d; ++t) {
+                double aq = 0, ak = 0, av = 0;
+                for (std::int64_t j = 0; j < S; ++j) {
+                    aq += dS[i * S + j] * K[j * d + t];
+                    ak += dS[j * S + i] * Q[j * d + t];
+                    av += D[j * S + i] * G[j * d + t];
+                }
+                const std::int64_t e = h * S * d + i * d + t;
+                worst = std::max({worst, rel_err(dq[e], aq), rel_err(dk[e], ak), rel_err(dv[e], av)});
+            }
+    }
+    std::printf("  sdpa max rel_err %.3g\n", worst);
+    CHECK(worst <= 1e-5);
+    Graph g2;  // ops_tempo.cpp:198-202: rank-4 inputs only
+    NodeId bad = g2.leaf(Tensor::from_host({4, 4}, randn(16, 1)), "x");
+    CHECK(throws<DimensionError>([&] { tempo_ops::sdpa(g2, bad, bad, bad, p, mask); }));
+}
+
 // A large mask goes through the device generator (jump-ahead): it must be
 // the reference's stream bit for bit (here: against the host engine).
 static void test_large_mask_device_stream() {
@@ -319,6 +396,7 @@ int main() {
     run("fused softmax+dropout", test_softmax_dropout_fused);
     run("hidden dropout", test_hidden_dropout);
     run("large mask: device reference stream", test_large_mask_device_stream);
+    run("sdpa (cuBLAS GEMMs + Tempo softmax/dropout)", test_sdpa);
     std::printf("%d failure(s)\n", g_fail);
     return g_fail;
 }

@@ -628,6 +628,11 @@ int tempo_dropout_bwd(const float* dy, const uint32_t* mask, double p, float* dx
                        "tempo_dropout_bwd");
 }
 
+int tempo_tensor_scale(const float* a, double c, float* out, int64_t n, tempo_stream_t stream) {
+    if (int rc = check_n(n, "tensor")) return rc;
+    return cuda_status(tb::launch_scale(a, c, out, n, S(stream)), "tempo_tensor_scale");
+}
+
 int tempo_tensor_add(const float* a, const float* b, float* out, int64_t n,
                      tempo_stream_t stream) {
     if (int rc = check_n(n, "add")) return rc;

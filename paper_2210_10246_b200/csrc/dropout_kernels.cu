@@ -243,6 +243,16 @@ __global__ void __launch_bounds__(kBlock) mask_unpack_kernel(const uint32_t* __r
         bytes[i] = (bits[i >> 5] >> (i & 31)) & 1u;
 }
 
+// out = float(double(a) * c) -- tempo::scale (kernels.cpp:209-213).
+__global__ void __launch_bounds__(kBlock) scale_kernel(const float* __restrict__ a, double c,
+                                                       float* __restrict__ out, int64_t n) {
+    grid_dep_wait();  // PDL: predecessor complete and visible
+    grid_dep_launch();
+    const int64_t stride = (int64_t)gridDim.x * kBlock;
+    for (int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x; i < n; i += stride)
+        out[i] = dscale(a[i], c);
+}
+
 __global__ void __launch_bounds__(kBlock) add_kernel(const float* __restrict__ a,
                                                      const float* __restrict__ b,
                                                      float* __restrict__ out, int64_t n) {
@@ -308,6 +318,13 @@ cudaError_t launch_mask_pack(const uint8_t* bytes, uint32_t* bits, int64_t n, in
     const int64_t warps = (n + 31) >> 5;
     int grid = grid_for((const void*)mask_pack_kernel, kBlock, 0, (warps * 32 + kBlock - 1) / kBlock);
     pdl(mask_pack_kernel, grid, kBlock, 0, st)(bytes, bits, n, status);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_scale(const float* a, double c, float* out, int64_t n, cudaStream_t st) {
+    if (n == 0) return cudaSuccess;
+    int grid = grid_for((const void*)scale_kernel, kBlock, 0, (n + kBlock - 1) / kBlock);
+    pdl(scale_kernel, grid, kBlock, 0, st)(a, c, out, n);
     return cudaGetLastError();
 }
 

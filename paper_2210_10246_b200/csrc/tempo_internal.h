@@ -76,6 +76,7 @@ cudaError_t launch_dropout_bwd(const float* dy, const uint32_t* mask, double sca
 cudaError_t launch_mask_pack(const uint8_t* bytes, uint32_t* bits, int64_t n, int32_t* status,
                              cudaStream_t st);
 cudaError_t launch_mask_unpack(const uint32_t* bits, uint8_t* bytes, int64_t n, cudaStream_t st);
+cudaError_t launch_scale(const float* a, double c, float* out, int64_t n, cudaStream_t st);
 cudaError_t launch_add(const float* a, const float* b, float* out, int64_t n, cudaStream_t st);
 
 // Launch `kernel` as a programmatic dependent of the previous work on the
