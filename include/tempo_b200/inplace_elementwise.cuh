@@ -33,51 +33,63 @@ namespace detail {
 constexpr int kBlock = 256;
 constexpr unsigned kFull = 0xffffffffu;
 
-__device__ __forceinline__ uint32_t nibble(bool a, bool b, bool c, bool d) {
-    return (uint32_t)a | ((uint32_t)b << 1) | ((uint32_t)c << 2) | ((uint32_t)d << 3);
+// Lane L owns elements 8L..8L+7 of a 256-element chunk: one 256-bit load or
+// store per tensor and a whole byte of the bit-packed mask (byte L of the
+// chunk's 32 bytes = BoolMask order), written or read directly.
+struct F8 {
+    float v[8];
+};
+__device__ __forceinline__ F8 ld8(const float* p) {
+    F8 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=f"(r.v[0]), "=f"(r.v[1]), "=f"(r.v[2]), "=f"(r.v[3]), "=f"(r.v[4]),
+                   "=f"(r.v[5]), "=f"(r.v[6]), "=f"(r.v[7])
+                 : "l"(p));
+    return r;
 }
-// Lane L owns elements 4L..4L+3 of a 128-element chunk; word w of the chunk
-// holds lanes 8w..8w+7 (bit 4j+k = element 4(8w+j)+k, BoolMask order).
-__device__ __forceinline__ void store_chunk_mask(uint32_t* words, uint32_t nib, int lane) {
-    uint32_t v = nib << ((lane & 7) << 2);
-    v |= __shfl_xor_sync(kFull, v, 1);
-    v |= __shfl_xor_sync(kFull, v, 2);
-    v |= __shfl_xor_sync(kFull, v, 4);
-    if ((lane & 7) == 0) words[lane >> 3] = v;
+__device__ __forceinline__ void st8(float* p, const F8& r) {
+    asm volatile("st.global.cs.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "f"(r.v[0]),
+                 "f"(r.v[1]), "f"(r.v[2]), "f"(r.v[3]), "f"(r.v[4]), "f"(r.v[5]), "f"(r.v[6]),
+                 "f"(r.v[7])
+                 : "memory");
 }
 
+// vec = 0 (pointers not 32-byte aligned): everything through the scalar
+// loops (same per-element functions, so the same bits).
 template <class Spec>
 __global__ void __launch_bounds__(kBlock) fwd_kernel(const float* __restrict__ x,
                                                      float* __restrict__ y,
-                                                     uint32_t* __restrict__ mask, int64_t n) {
+                                                     uint32_t* __restrict__ mask, int64_t n,
+                                                     int vec) {
     const int lane = threadIdx.x & 31;
     const int64_t warp = ((int64_t)blockIdx.x * kBlock + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * kBlock) >> 5;
-    const int64_t nchunks = n >> 7;
-    const float4* x4 = reinterpret_cast<const float4*>(x);
-    float4* y4 = reinterpret_cast<float4*>(y);
-    float4 nxt = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (warp < nchunks) nxt = __ldg(x4 + (warp << 5) + lane);
+    const int64_t nchunks = vec ? (n >> 8) : 0;
+    uint8_t* mask8 = reinterpret_cast<uint8_t*>(mask);
+    F8 nxt;
+    if (warp < nchunks) nxt = ld8(x + (warp << 8) + 8 * lane);
     for (int64_t c = warp; c < nchunks; c += nwarps) {
-        const float4 v = nxt;
-        if (c + nwarps < nchunks) nxt = __ldg(x4 + ((c + nwarps) << 5) + lane);
-        y4[(c << 5) + lane] = make_float4(Spec::fwd(v.x), Spec::fwd(v.y), Spec::fwd(v.z),
-                                          Spec::fwd(v.w));
-        store_chunk_mask(mask + (c << 2),
-                         nibble(Spec::branch(v.x), Spec::branch(v.y), Spec::branch(v.z),
-                                Spec::branch(v.w)),
-                         lane);
-    }
-    if (warp == nwarps - 1) {  // ragged tail: one ballot per mask word
-        const int64_t nwords = (n + 31) >> 5;
-        for (int64_t w = nchunks << 2; w < nwords; ++w) {
-            const int64_t i = (w << 5) + lane;
-            const bool in = i < n;
-            const float xv = in ? x[i] : 0.0f;
-            const uint32_t bits = __ballot_sync(kFull, in && Spec::branch(xv));
-            if (in) y[i] = Spec::fwd(xv);
-            if (lane == 0) mask[w] = bits;
+        const F8 v = nxt;
+        if (c + nwarps < nchunks) nxt = ld8(x + ((c + nwarps) << 8) + 8 * lane);
+        F8 o;
+        uint32_t b = 0;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            o.v[k] = Spec::fwd(v.v[k]);
+            b |= (uint32_t)Spec::branch(v.v[k]) << k;
         }
+        st8(y + (c << 8) + 8 * lane, o);
+        mask8[(c << 5) + lane] = (uint8_t)b;
+    }
+    // the rest (ragged tail, or everything when unaligned): one ballot per word
+    const int64_t nwords = (n + 31) >> 5;
+    for (int64_t w = (nchunks << 3) + warp; w < nwords; w += nwarps) {
+        const int64_t i = (w << 5) + lane;
+        const bool in = i < n;
+        const float xv = in ? x[i] : 0.0f;
+        const uint32_t bits = __ballot_sync(kFull, in && Spec::branch(xv));
+        if (in) y[i] = Spec::fwd(xv);
+        if (lane == 0) mask[w] = bits;
     }
 }
 
@@ -85,26 +97,22 @@ template <class Spec>
 __global__ void __launch_bounds__(kBlock) bwd_kernel(const float* __restrict__ dy,
                                                      const float* __restrict__ y,
                                                      const uint32_t* __restrict__ mask,
-                                                     float* __restrict__ dx, int64_t n) {
+                                                     float* __restrict__ dx, int64_t n, int vec) {
     const int lane = threadIdx.x & 31;
     const int64_t warp = ((int64_t)blockIdx.x * kBlock + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * kBlock) >> 5;
-    const int64_t nchunks = n >> 7;
-    const float4* g4 = reinterpret_cast<const float4*>(dy);
-    const float4* y4 = reinterpret_cast<const float4*>(y);
-    float4* d4 = reinterpret_cast<float4*>(dx);
+    const int64_t nchunks = vec ? (n >> 8) : 0;
+    const uint8_t* mask8 = reinterpret_cast<const uint8_t*>(mask);
     for (int64_t c = warp; c < nchunks; c += nwarps) {
-        const float4 g = __ldg(g4 + (c << 5) + lane), v = __ldg(y4 + (c << 5) + lane);
-        const uint32_t nib = (__ldg(mask + (c << 2) + (lane >> 3)) >> (4 * (lane & 7))) & 0xfu;
-        d4[(c << 5) + lane] = make_float4(g.x * Spec::grad_from_output(v.x, nib & 1u),
-                                          g.y * Spec::grad_from_output(v.y, (nib >> 1) & 1u),
-                                          g.z * Spec::grad_from_output(v.z, (nib >> 2) & 1u),
-                                          g.w * Spec::grad_from_output(v.w, (nib >> 3) & 1u));
+        const F8 g = ld8(dy + (c << 8) + 8 * lane), v = ld8(y + (c << 8) + 8 * lane);
+        const uint32_t b = __ldg(mask8 + (c << 5) + lane);
+        F8 o;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) o.v[k] = g.v[k] * Spec::grad_from_output(v.v[k], (b >> k) & 1u);
+        st8(dx + (c << 8) + 8 * lane, o);
     }
-    if (warp == nwarps - 1) {
-        for (int64_t i = (nchunks << 7) + lane; i < n; i += 32)
-            dx[i] = dy[i] * Spec::grad_from_output(y[i], (mask[i >> 5] >> (i & 31)) & 1u);
-    }
+    for (int64_t i = (nchunks << 8) + warp * 32 + lane; i < n; i += nwarps * 32)
+        dx[i] = dy[i] * Spec::grad_from_output(y[i], (mask[i >> 5] >> (i & 31)) & 1u);
 }
 
 inline int grid_of(const void* k, int64_t n) {
@@ -112,33 +120,33 @@ inline int grid_of(const void* k, int64_t n) {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k, kBlock, 0);
-    const int64_t need = (((n >> 7) + 1) * 32 + kBlock - 1) / kBlock;
+    const int64_t need = (((n >> 5) + 1) * 32 + kBlock - 1) / kBlock;
     const int64_t full = (int64_t)sms * (per > 0 ? per : 1);
     return (int)(need < full ? (need > 0 ? need : 1) : full);
 }
 
-inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+inline bool aligned32(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 31u) == 0; }
 }  // namespace detail
 
-// y = Spec::fwd(x), mask bit = Spec::branch(x).  x, y 16-byte aligned.
+// y = Spec::fwd(x), mask bit = Spec::branch(x).  Any alignment (32-byte
+// aligned x and y take the 256-bit path).
 template <class Spec>
 cudaError_t forward(const float* x, float* y, uint32_t* mask, int64_t n, cudaStream_t st) {
     if (n <= 0) return cudaSuccess;
-    if (!detail::aligned16(x) || !detail::aligned16(y)) return cudaErrorMisalignedAddress;
+    const int vec = detail::aligned32(x) && detail::aligned32(y) ? 1 : 0;
     auto k = detail::fwd_kernel<Spec>;
-    k<<<detail::grid_of((const void*)k, n), detail::kBlock, 0, st>>>(x, y, mask, n);
+    k<<<detail::grid_of((const void*)k, n), detail::kBlock, 0, st>>>(x, y, mask, n, vec);
     return cudaGetLastError();
 }
 
-// dx = dy * Spec::grad_from_output(y, mask bit).
+// dx = dy * Spec::grad_from_output(y, mask bit).  dx may alias dy.
 template <class Spec>
 cudaError_t backward(const float* dy, const float* y, const uint32_t* mask, float* dx, int64_t n,
                      cudaStream_t st) {
     if (n <= 0) return cudaSuccess;
-    if (!detail::aligned16(dy) || !detail::aligned16(y) || !detail::aligned16(dx))
-        return cudaErrorMisalignedAddress;
+    const int vec = detail::aligned32(dy) && detail::aligned32(y) && detail::aligned32(dx) ? 1 : 0;
     auto k = detail::bwd_kernel<Spec>;
-    k<<<detail::grid_of((const void*)k, n), detail::kBlock, 0, st>>>(dy, y, mask, dx, n);
+    k<<<detail::grid_of((const void*)k, n), detail::kBlock, 0, st>>>(dy, y, mask, dx, n, vec);
     return cudaGetLastError();
 }
 

@@ -30,6 +30,7 @@ struct LeakySpec {
     __device__ static float fwd(float x) { return x > 0.0f ? x : 0.1f * x; }
     __device__ static bool branch(float x) { return x > 0.0f; }
     __device__ static float grad_from_output(float, bool m) { return m ? 1.0f : 0.1f; }
+    static bool branch_host(float x) { return x > 0.0f; }
 };
 
 static int fails = 0;
@@ -71,7 +72,51 @@ static void run(const char* name, std::int64_t n, F f, G grad, B br) {
     std::printf("%s %s (n=%lld)\n", fails == before ? "PASS" : "FAIL", name, (long long)n);
 }
 
+// Direct kernel calls: mask bits = Spec::branch(x) in BoolMask order, and the
+// 256-bit path (32-byte aligned) and the scalar path (4-byte offset) agree
+// bitwise on y, the mask and dx.
+template <class Spec>
+static void paths_agree(const char* name, std::int64_t n) {
+    int before = fails;
+    [&] {
+        std::mt19937_64 rng(n + 7);
+        std::normal_distribution<double> d(0.0, 1.0);
+        std::vector<float> xh(n), gh(n);
+        for (auto& v : xh) v = (float)d(rng);
+        for (auto& v : gh) v = (float)d(rng);
+        const std::int64_t words = (n + 31) / 32;
+        float *xb, *yb, *gb, *db;
+        uint32_t* mb;
+        cudaMalloc(&xb, (n + 8) * 4); cudaMalloc(&yb, (n + 8) * 4); cudaMalloc(&gb, (n + 8) * 4);
+        cudaMalloc(&db, (n + 8) * 4); cudaMalloc(&mb, 2 * words * 4);
+        std::vector<float> y0, y1, d0, d1;
+        std::vector<uint32_t> m0(words), m1(words);
+        for (int off : {0, 1}) {
+            cudaMemcpy(xb + off, xh.data(), n * 4, cudaMemcpyHostToDevice);
+            cudaMemcpy(gb + off, gh.data(), n * 4, cudaMemcpyHostToDevice);
+            uint32_t* m = mb + off * words;
+            CHECK(tempo_b200::ew::forward<Spec>(xb + off, yb + off, m, n, nullptr) == cudaSuccess);
+            CHECK(tempo_b200::ew::backward<Spec>(gb + off, yb + off, m, db + off, n, nullptr) ==
+                  cudaSuccess);
+            std::vector<float> yh(n), dh(n);
+            cudaMemcpy(yh.data(), yb + off, n * 4, cudaMemcpyDeviceToHost);
+            cudaMemcpy(dh.data(), db + off, n * 4, cudaMemcpyDeviceToHost);
+            cudaMemcpy((off ? m1 : m0).data(), m, words * 4, cudaMemcpyDeviceToHost);
+            (off ? y1 : y0) = yh;
+            (off ? d1 : d0) = dh;
+        }
+        cudaFree(xb); cudaFree(yb); cudaFree(gb); cudaFree(db); cudaFree(mb);
+        CHECK(y0 == y1 && d0 == d1 && m0 == m1);
+        for (std::int64_t i = 0; i < n; ++i)
+            CHECK(((m0[i / 32] >> (i % 32)) & 1u) == (uint32_t)Spec::branch_host(xh[i]));
+        for (std::int64_t w = 0; w < words; ++w)  // bits past n are zero
+            if (w == words - 1 && n % 32) CHECK((m0[w] >> (n % 32)) == 0u);
+    }();
+    std::printf("%s %s paths agree (n=%lld)\n", fails == before ? "PASS" : "FAIL", name, (long long)n);
+}
+
 int main() {
+    for (std::int64_t n : {1, 255, 256, 4096 + 37, 1 << 20}) paths_agree<LeakySpec>("leaky relu", n);
     for (std::int64_t n : {1, 127, 128, 1000, 1 << 20}) {
         run<ExpSpec>("exp", n, [](double x) { return std::exp(x); },
                      [](double x) { return std::exp(x); }, 0);
