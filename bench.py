@@ -339,7 +339,7 @@ def cpu_reference_sample(frac_rows: int, threads: int, steps: int, warmup: int):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -385,7 +385,7 @@ def main():
     # ---- timed region: K steps, barrier + sync on both sides -------------
     clocks = ClockSampler(local)
     clocks.start()
-    time.sleep(0.3)
+    time.sleep(0.15)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
