@@ -521,52 +521,69 @@ def stash_report(chain):
 def e2e_measure(chain, args, world, allreduce, dist):
     """Same metric through the public API with HOST buffers: every step
     copies its inputs from pinned host memory (H2D) and reads every result
-    back (D2H) inside the timed region.  Copies are pipelined on two copy
-    streams against the compute stream: step i+1's inputs upload (into the
-    second of two device input sets) while step i computes and downloads, so
-    the step costs max(H2D, D2H + compute) rather than their sum."""
+    back (D2H) inside the timed region.  Inputs and results each live in ONE
+    contiguous pinned host buffer and ONE contiguous device buffer per set
+    (views per tensor), so a step is one H2D and one D2H copy; both are
+    double-buffered: step i+1's inputs upload while step i computes and step
+    i-1's results download, so the step costs about the PCIe time of its
+    copies (full duplex) rather than their sum plus compute."""
     torch = chain.torch
     names_in = ["z", "x_attn_out", "x_ffn1", "x_ffn2", "dy_ln2", "dy_gelu", "dy_ln1", "dD"]
-    outs = [chain.dZ, chain.dx_d1, chain.dx_g, chain.dx_d2, chain.dparams]
-    sets = [{n: getattr(chain, n) for n in names_in},
-            {n: torch.empty_like(getattr(chain, n)) for n in names_in}]
-    h_in = {n: torch.empty(getattr(chain, n).shape, dtype=torch.float32,
-                           pin_memory=True).copy_(getattr(chain, n)) for n in names_in}
-    h_out = [torch.empty(t.shape, dtype=t.dtype, pin_memory=True) for t in outs]
-    bi = sum(t.numel() * t.element_size() for t in h_in.values())
-    bo = sum(t.numel() * t.element_size() for t in outs)
+    names_out = ["dZ", "dx_d1", "dx_g", "dx_d2", "dparams"]
+    orig = {n: getattr(chain, n) for n in names_in + names_out}
+
+    def views(buf, names):
+        out, o = {}, 0
+        for n in names:
+            t = orig[n]
+            out[n] = buf[o:o + t.numel()].view(t.shape)
+            o += t.numel()
+        return out
+
+    n_in = sum(orig[n].numel() for n in names_in)
+    n_out = sum(orig[n].numel() for n in names_out)
+    d_in = [torch.empty(n_in, device=chain.dev) for _ in range(2)]
+    d_out = [torch.empty(n_out, device=chain.dev) for _ in range(2)]
+    in_sets = [views(b, names_in) for b in d_in]
+    out_sets = [views(b, names_out) for b in d_out]
+    h_in = torch.empty(n_in, dtype=torch.float32, pin_memory=True)
+    for n, v in views(h_in, names_in).items():
+        v.copy_(orig[n])
+    h_out = [torch.empty(n_out, dtype=torch.float32, pin_memory=True) for _ in range(2)]
+    bi, bo = n_in * 4, n_out * 4
     comp = torch.cuda.current_stream()
     s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
-    ev_in = [torch.cuda.Event(), torch.cuda.Event()]      # inputs of set j uploaded
-    ev_used = [torch.cuda.Event(), torch.cuda.Event()]    # set j consumed by compute
-    ev_comp, ev_out = torch.cuda.Event(), torch.cuda.Event()
-    for e in ev_used:
-        e.record(comp)
-    ev_out.record(s_out)
+    ev_in = [torch.cuda.Event(), torch.cuda.Event()]    # input set j uploaded
+    ev_used = [torch.cuda.Event(), torch.cuda.Event()]  # input set j consumed by compute
+    ev_done = [torch.cuda.Event(), torch.cuda.Event()]  # output set j computed
+    ev_out = [torch.cuda.Event(), torch.cuda.Event()]   # output set j downloaded
+    for j in range(2):
+        ev_used[j].record(comp)
+        ev_out[j].record(s_out)
 
     def upload(j):
         with torch.cuda.stream(s_in):
             s_in.wait_event(ev_used[j])
-            for n in names_in:
-                sets[j][n].copy_(h_in[n], non_blocking=True)
+            d_in[j].copy_(h_in, non_blocking=True)
             ev_in[j].record(s_in)
 
     def step(i, upload_next=True):
         j = i % 2
         comp.wait_event(ev_in[j])
-        comp.wait_event(ev_out)           # previous results downloaded
+        comp.wait_event(ev_out[j])  # results of step i-2 (same output set) downloaded
         for n in names_in:
-            setattr(chain, n, sets[j][n])
+            setattr(chain, n, in_sets[j][n])
+        for n in names_out:
+            setattr(chain, n, out_sets[j][n])
         chain.step(allreduce)
         ev_used[j].record(comp)
-        ev_comp.record(comp)
+        ev_done[j].record(comp)
         if upload_next:
-            upload(1 - j)                 # next step's inputs, overlapped
+            upload(1 - j)  # next step's inputs, overlapped
         with torch.cuda.stream(s_out):
-            s_out.wait_event(ev_comp)
-            for h, d in zip(h_out, outs):
-                h.copy_(d, non_blocking=True)
-            ev_out.record(s_out)
+            s_out.wait_event(ev_done[j])
+            h_out[j].copy_(d_out[j], non_blocking=True)
+            ev_out[j].record(s_out)
 
     k = max(1, min(args.steps, 20))  # steady state: the one undrained D2H amortised over k
     upload(0)
@@ -580,11 +597,12 @@ def e2e_measure(chain, args, world, allreduce, dist):
     upload(1)                   # step 1's inputs: inside the timed region
     for i in range(1, k + 1):
         step(i, upload_next=i < k)
-    comp.wait_event(ev_out)
+    for j in range(2):
+        comp.wait_event(ev_out[j])
     e1.record(comp)
     torch.cuda.synchronize()
-    for n in names_in:  # restore the chain's own buffers
-        setattr(chain, n, sets[0][n])
+    for n, t in orig.items():  # restore the chain's own buffers
+        setattr(chain, n, t)
     ms = e0.elapsed_time(e1) / k
     if dist is not None:
         t = torch.tensor([ms], device=chain.dev)
@@ -593,7 +611,8 @@ def e2e_measure(chain, args, world, allreduce, dist):
     v = sum(op_bytes().values()) * world / (ms * 1e-3) / 1e9
     return {"value": round(v, 2), "unit": "GB/s", "h2d_bytes_per_step": int(bi),
             "d2h_bytes_per_step": int(bo), "ms_per_step": round(ms, 3), "steps": k,
-            "overlap": "H2D of step i+1 || compute + D2H of step i (2 copy streams)"}
+            "overlap": "one H2D (step i+1) || compute (step i) || one D2H (step i-1); "
+                       "inputs and results double-buffered"}
 
 
 def main_reference(args, rank, world):
