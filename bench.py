@@ -450,6 +450,16 @@ def main():
                             "mask, bit-exact, device jump-ahead", "elements": n_att,
                     "ms": round(t_ms, 3), "gelem_per_s": round(n_att / t_ms / 1e6, 1)}
 
+    # ---- the same chain through the C++ operator API (Graph/Tape) ---------
+    cpp_api = None
+    exe = os.path.join(ROOT, "paper_2210_10246_b200", "_lib", "bench_graph")
+    if rank == 0 and world == 1 and os.path.exists(exe):
+        try:
+            r = subprocess.run([exe, "20", "3"], capture_output=True, text=True, timeout=300)
+            cpp_api = json.loads(r.stdout.strip().splitlines()[-1])
+        except Exception as ex:
+            cpp_api = {"unavailable": str(ex)[:200]}
+
     # ---- e2e: the public API with host buffers -----------------------------
     e2e = None
     if not args.no_e2e:
@@ -490,6 +500,7 @@ def main():
                              (Chain.REF_MASK_LAUNCHES if args.masks == "reference" else 0)) * args.steps,
             "mask_stream": args.masks,
             "reference_mask_generation": ref_mask,
+            "cpp_api": cpp_api,
             "clocks": clk,
             "per_op": per_op_rows,
             "frac_of_peak": round(value / world / peak, 4),

@@ -60,6 +60,23 @@ std::int64_t shape_numel(const Shape& s);
 std::string shape_str(const Shape& s);
 
 // ---- Tensor (tensor.hpp:34-102): shared handle over device fp32 storage ---
+// Device buffers are allocated stream-ordered (cudaMallocAsync from the
+// device's memory pool) on the thread's current stream and released on the
+// same stream; every op builder and backward closure runs under a
+// StreamScope of its Graph's stream.  Tensors made outside ops use the
+// enclosing scope (default: the legacy default stream).
+class StreamScope {
+public:
+    explicit StreamScope(tempo_stream_t s);
+    ~StreamScope();
+    StreamScope(const StreamScope&) = delete;
+    StreamScope& operator=(const StreamScope&) = delete;
+
+private:
+    tempo_stream_t prev_;
+};
+tempo_stream_t current_stream();
+
 class Tensor {
 public:
     struct Storage;
@@ -218,7 +235,8 @@ private:
 
 class Tape {
 public:
-    explicit Tape(StashLedger* ledger = nullptr) : ledger_(ledger) {}
+    explicit Tape(StashLedger* ledger = nullptr, const tempo_stream_t* stream = nullptr)
+        : ledger_(ledger), stream_(stream) {}
     NodeId leaf(Tensor value, std::string tag);
     NodeId record(std::string op, std::string tag, std::vector<NodeId> inputs, Tensor value,
                   std::vector<LazyStash> stashes, BackwardFn backward);
@@ -233,6 +251,7 @@ public:
 private:
     std::vector<TapeNode> nodes_;
     StashLedger* ledger_ = nullptr;
+    const tempo_stream_t* stream_ = nullptr;  // the owning Graph's stream
     bool backward_done_ = false;
     void check_node_id(NodeId id) const;
     friend class BackwardCtx;
@@ -258,8 +277,8 @@ private:
 // ---- Graph (graph.hpp:20-54) -----------------------------------------------
 struct Graph {
     StashLedger ledger;
-    Tape tape{&ledger};
-    tempo_stream_t stream = nullptr;  // cudaStream_t every op runs on
+    Tape tape{&ledger, &stream};
+    tempo_stream_t stream = nullptr;  // cudaStream_t every op (and its backward) runs on
 
     NodeId leaf(Tensor value, std::string tag) { return tape.leaf(std::move(value), std::move(tag)); }
     NodeId param(Tensor value, std::string tag) { return leaf(std::move(value), std::move(tag)); }
@@ -291,9 +310,12 @@ NodeId layernorm(Graph& g, NodeId x, NodeId gamma, NodeId beta, double epsilon,
 NodeId softmax(Graph& g, NodeId z, std::string tag);
 NodeId dropout_recompute(Graph& g, NodeId x, double p, BoolMask mask, std::string tag,
                          std::string mask_tag);
-// Fused device form of softmax -> dropout_recompute (one kernel; returns the
-// dropout node, *probs_out the softmax node).  A Philox mask is generated
-// when `mask` is undefined (seed/offset), else it is read.
+// Fused device form of softmax -> dropout_recompute (one forward kernel).
+// probs_out == nullptr: ONE node z -> D whose backward is the fused
+// attention-probs kernel (tempo_attn_probs_bwd); with probs_out, two nodes
+// (softmax_ip, then dropout_recompute) like the reference, *probs_out = the
+// softmax node.  A Philox mask is generated when `mask` is undefined
+// (seed/offset), else it is read.
 NodeId softmax_dropout(Graph& g, NodeId z, double p, BoolMask mask, std::uint64_t seed,
                        std::uint64_t offset, const std::string& probs_tag,
                        const std::string& drop_tag, const std::string& mask_tag,

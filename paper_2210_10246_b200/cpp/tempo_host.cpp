@@ -64,20 +64,59 @@ static void require_same_shape(const Shape& a, const Shape& b, const char* what)
                              shape_str(b) + " differ");
 }
 
+// ---- device memory: stream-ordered, pooled ---------------------------------------
+// Every device buffer of this API comes from the device's default memory pool
+// through cudaMallocAsync on the stream of the op that creates it (the
+// thread's current StreamScope) and goes back with cudaFreeAsync on the same
+// stream: no device-wide synchronization per tensor (cudaFree would), and the
+// pool keeps freed blocks for reuse (release threshold = unlimited).
+namespace {
+thread_local tempo_stream_t t_stream = nullptr;
+
+void pool_init() {
+    static std::mutex mu;
+    static std::map<int, bool> done;
+    int dev = 0;
+    cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+    std::lock_guard<std::mutex> lock(mu);
+    if (done[dev]) return;
+    cudaMemPool_t pool;
+    cuda_check(cudaDeviceGetDefaultMemPool(&pool, dev), "cudaDeviceGetDefaultMemPool");
+    std::uint64_t keep = ~0ull;
+    cuda_check(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep),
+               "cudaMemPoolSetAttribute");
+    done[dev] = true;
+}
+
+void* dev_alloc(std::size_t bytes, tempo_stream_t st) {
+    pool_init();
+    void* p = nullptr;
+    cuda_check(cudaMallocAsync(&p, bytes, static_cast<cudaStream_t>(st)), "cudaMallocAsync");
+    return p;
+}
+void dev_free(void* p, tempo_stream_t st) {
+    if (p) cudaFreeAsync(p, static_cast<cudaStream_t>(st));
+}
+}  // namespace
+
+StreamScope::StreamScope(tempo_stream_t s) : prev_(t_stream) { t_stream = s; }
+StreamScope::~StreamScope() { t_stream = prev_; }
+tempo_stream_t current_stream() { return t_stream; }
+
 // ---- Tensor ---------------------------------------------------------------------
 struct Tensor::Storage {
     Shape shape;
     float* ptr = nullptr;
-    ~Storage() {
-        if (ptr) cudaFree(ptr);
-    }
+    tempo_stream_t stream = nullptr;  // allocation (and release) stream
+    ~Storage() { dev_free(ptr, stream); }
 };
 
 Tensor Tensor::empty(Shape shape) {
     auto s = std::make_shared<Storage>();
     std::int64_t n = shape_numel(shape);
     s->shape = std::move(shape);
-    if (n > 0) cuda_check(cudaMalloc(&s->ptr, (size_t)n * sizeof(float)), "cudaMalloc");
+    s->stream = t_stream;
+    if (n > 0) s->ptr = static_cast<float*>(dev_alloc((size_t)n * sizeof(float), t_stream));
     Tensor t;
     t.storage_ = std::move(s);
     return t;
@@ -85,7 +124,9 @@ Tensor Tensor::empty(Shape shape) {
 
 Tensor Tensor::zeros(Shape shape) {
     Tensor t = empty(std::move(shape));
-    if (t.numel() > 0) cuda_check(cudaMemset(t.data(), 0, t.byte_size()), "cudaMemset");
+    if (t.numel() > 0)
+        cuda_check(cudaMemsetAsync(t.data(), 0, t.byte_size(), static_cast<cudaStream_t>(t_stream)),
+                   "cudaMemsetAsync");
     return t;
 }
 
@@ -102,6 +143,8 @@ Tensor Tensor::from_host(Shape shape, const std::vector<float>& values) {
 
 std::vector<float> Tensor::to_host() const {
     std::vector<float> out((size_t)numel());
+    // the producer may have run on any stream: finish the device work first
+    if (numel() > 0) cuda_check(cudaDeviceSynchronize(), "cudaDeviceSynchronize");
     if (numel() > 0)
         cuda_check(cudaMemcpy(out.data(), data(), byte_size(), cudaMemcpyDeviceToHost),
                    "cudaMemcpy");
@@ -130,10 +173,10 @@ BoolMask BoolMask::empty(Shape shape) {
     BoolMask m;
     std::int64_t n = shape_numel(shape);
     m.shape_ = std::move(shape);
-    std::uint32_t* p = nullptr;
     std::size_t bytes = (std::size_t)std::max<std::int64_t>(1, words_of(n)) * 4;
-    cuda_check(cudaMalloc(&p, bytes), "cudaMalloc");
-    m.words_ = std::shared_ptr<std::uint32_t>(p, [](std::uint32_t* q) { cudaFree(q); });
+    tempo_stream_t st = t_stream;
+    auto* p = static_cast<std::uint32_t*>(dev_alloc(bytes, st));
+    m.words_ = std::shared_ptr<std::uint32_t>(p, [st](std::uint32_t* q) { dev_free(q, st); });
     return m;
 }
 
@@ -146,13 +189,11 @@ BoolMask BoolMask::bernoulli_keep(Shape shape, double drop_p, std::uint64_t seed
             throw ParamError("drop probability must lie in [0, 1), got " + std::to_string(drop_p));
         BoolMask m = empty(std::move(shape));
         const size_t ws_bytes = tempo_bernoulli_keep_bits_workspace_size(0, n);
-        void* ws = nullptr;
-        cuda_check(cudaMalloc(&ws, ws_bytes), "cudaMalloc");
-        const int rc = tempo_bernoulli_keep_bits(n, drop_p, seed, 0, m.words(), ws, ws_bytes, nullptr);
-        cudaError_t e = cudaStreamSynchronize(nullptr);
-        cudaFree(ws);
+        void* ws = dev_alloc(ws_bytes, t_stream);
+        const int rc = tempo_bernoulli_keep_bits(n, drop_p, seed, 0, m.words(), ws, ws_bytes,
+                                                 t_stream);
+        dev_free(ws, t_stream);
         check(rc);
-        cuda_check(e, "tempo_bernoulli_keep_bits");
         return m;
     }
     std::vector<std::uint32_t> host((size_t)words_of(n));
@@ -185,6 +226,7 @@ BoolMask BoolMask::from_bytes(Shape shape, const std::vector<std::uint8_t>& byte
 std::vector<std::uint8_t> BoolMask::to_bytes() const {
     std::int64_t n = numel();
     std::vector<std::uint32_t> host((size_t)words_of(n));
+    cuda_check(cudaDeviceSynchronize(), "cudaDeviceSynchronize");
     if (!host.empty())
         cuda_check(cudaMemcpy(host.data(), words(), host.size() * 4, cudaMemcpyDeviceToHost),
                    "cudaMemcpy");
@@ -444,6 +486,8 @@ GradientMap Tape::backward(NodeId root, Tensor seed) {
                              " does not match root value shape " +
                              shape_str(nodes_[root].value.shape()));
     backward_done_ = true;
+    const tempo_stream_t st = stream_ ? *stream_ : nullptr;
+    StreamScope scope(st);
     std::vector<Tensor> grads(nodes_.size());
     grads[root] = std::move(seed);
     for (NodeId i = root; i >= 0; --i) {
@@ -466,7 +510,7 @@ GradientMap Tape::backward(NodeId root, Tensor seed) {
             if (grads[in].defined()) {  // fan-out accumulation (tape.cpp:225-226)
                 Tensor sum = Tensor::empty(gin[j].shape());
                 check(tempo_tensor_add(grads[in].data(), gin[j].data(), sum.data(), sum.numel(),
-                                       nullptr));
+                                       st));
                 grads[in] = sum;
             } else {
                 grads[in] = gin[j];
@@ -478,7 +522,7 @@ GradientMap Tape::backward(NodeId root, Tensor seed) {
         nd.charged.clear();
         if (i != root) grads[i] = Tensor();
     }
-    cuda_check(cudaDeviceSynchronize(), "backward");
+    cuda_check(cudaStreamSynchronize(static_cast<cudaStream_t>(st)), "backward");
     return GradientMap(std::move(grads));
 }
 
@@ -605,6 +649,7 @@ Tensor mm(tempo_stream_t st, const Tensor& a, const Tensor& b, bool ta, bool tb)
 }  // namespace
 
 NodeId Graph::matmul(NodeId a, NodeId b, std::string tag) {  // graph.cpp:32-51
+    StreamScope scope_(stream);
     const Tensor& va = tape.value(a);
     const Tensor& vb = tape.value(b);
     if (va.shape().size() != vb.shape().size())
@@ -625,6 +670,7 @@ NodeId Graph::matmul(NodeId a, NodeId b, std::string tag) {  // graph.cpp:32-51
 }
 
 NodeId Graph::matmul_nt(NodeId a, NodeId b, std::string tag) {  // graph.cpp:53-71
+    StreamScope scope_(stream);
     const Tensor& va = tape.value(a);
     const Tensor& vb = tape.value(b);
     if (va.shape().size() != vb.shape().size())
@@ -646,6 +692,7 @@ NodeId Graph::matmul_nt(NodeId a, NodeId b, std::string tag) {  // graph.cpp:53-
 }
 
 NodeId Graph::scale(NodeId a, double c, std::string tag) {  // graph.cpp:73-80
+    StreamScope scope_(stream);
     const Tensor& va = tape.value(a);
     Tensor out = Tensor::empty(va.shape());
     check(tempo_tensor_scale(va.data(), c, out.data(), va.numel(), stream));
@@ -661,6 +708,7 @@ NodeId Graph::scale(NodeId a, double c, std::string tag) {  // graph.cpp:73-80
 }
 
 NodeId Graph::add(NodeId a, NodeId b, std::string tag) {  // graph.cpp:82-89
+    StreamScope scope_(stream);
     const Tensor& va = tape.value(a);
     const Tensor& vb = tape.value(b);
     require_same_shape(va.shape(), vb.shape(), "add");
@@ -685,7 +733,8 @@ void ensure_recompute_rules() {  // ops_tempo.cpp:15-30
             const double p = recipe.scalars.at("p");
             Tensor d = Tensor::empty(src[0].shape());
             check(tempo_dropout_fwd(src[0].data(), p, TEMPO_MASK_SUPPLIED,
-                                    recipe.masks[0].words(), 0, 0, d.data(), d.numel(), nullptr));
+                                    recipe.masks[0].words(), 0, 0, d.data(), d.numel(),
+                                    current_stream()));
             return d;
         });
         return true;
@@ -700,6 +749,7 @@ static std::int64_t last_dim(const Shape& s) {
 
 NodeId gelu(Graph& g, NodeId x, const GeluPolyTable* table, std::string tag,
             std::string mask_tag) {  // ops_tempo.cpp:89-96, 32-71
+    StreamScope scope_(g.stream);
     if (table == nullptr || table->empty()) throw ConfigError("in-place gelu needs a fitted table");
     const Tensor& vx = g.value(x);
     Tensor y = Tensor::empty(vx.shape());
@@ -725,6 +775,7 @@ NodeId gelu(Graph& g, NodeId x, const GeluPolyTable* table, std::string tag,
 
 NodeId layernorm(Graph& g, NodeId x, NodeId gamma, NodeId beta, double epsilon, std::string tag,
                  std::string rstd_tag) {  // ops_tempo.cpp:98-156
+    StreamScope scope_(g.stream);
     const Tensor& vx = g.value(x);
     const Tensor& vg = g.value(gamma);
     const Tensor& vb = g.value(beta);
@@ -754,20 +805,17 @@ NodeId layernorm(Graph& g, NodeId x, NodeId gamma, NodeId beta, double epsilon, 
             Tensor dx = Tensor::empty(yv.shape());
             Tensor dg = Tensor::empty({m}), db = Tensor::empty({m});
             size_t ws_bytes = tempo_ln_ip_bwd_workspace_size(rows, m);
-            void* ws = nullptr;
-            if (ws_bytes) cuda_check(cudaMalloc(&ws, ws_bytes), "cudaMalloc");
+            void* ws = ws_bytes ? dev_alloc(ws_bytes, st) : nullptr;
             int rc = tempo_ln_ip_bwd(gy.data(), yv.data(), rs.data(), gv.data(), bv.data(),
                                      dx.data(), dg.data(), db.data(), ws, ws_bytes, rows, m, st);
-            if (ws) {
-                cudaStreamSynchronize(static_cast<cudaStream_t>(st));
-                cudaFree(ws);
-            }
+            dev_free(ws, st);
             check(rc);
             return {dx, dg, db};
         });
 }
 
 NodeId softmax(Graph& g, NodeId z, std::string tag) {  // ops_tempo.cpp:158-166
+    StreamScope scope_(g.stream);
     const Tensor& vz = g.value(z);
     const std::int64_t c = last_dim(vz.shape());
     const std::int64_t rows = c ? vz.numel() / c : 0;
@@ -811,6 +859,7 @@ static NodeId record_dropout_recompute(Graph& g, NodeId x, const Tensor& y, doub
 
 NodeId dropout_recompute(Graph& g, NodeId x, double p, BoolMask mask, std::string tag,
                          std::string mask_tag) {  // ops_tempo.cpp:168-194
+    StreamScope scope_(g.stream);
     ensure_recompute_rules();
     const Tensor& vx = g.value(x);
     if (!g.ledger.is_live(vx.ident()))
@@ -826,6 +875,7 @@ NodeId softmax_dropout(Graph& g, NodeId z, double p, BoolMask mask, std::uint64_
                        std::uint64_t offset, const std::string& probs_tag,
                        const std::string& drop_tag, const std::string& mask_tag,
                        NodeId* probs_out) {
+    StreamScope scope_(g.stream);
     ensure_recompute_rules();
     const Tensor& vz = g.value(z);
     const std::int64_t c = last_dim(vz.shape());
@@ -839,6 +889,30 @@ NodeId softmax_dropout(Graph& g, NodeId z, double p, BoolMask mask, std::uint64_
                                     mask.words(), seed, offset, P.data(), D.data(), rows, c,
                                     g.stream));
     tempo_stream_t st = g.stream;
+    if (!probs_out) {
+        // One node z -> D whose backward is the fused attention-probs backward
+        // (dropout bwd + output-only softmax bwd in one pass, stash = P + bits);
+        // consumers of D get it recomputed from P and the mask (dropout-rescale).
+        RecomputeRecipe recipe;
+        recipe.rule = "dropout-rescale";
+        recipe.sources = {P.weak_storage()};
+        recipe.masks = {mask};
+        recipe.scalars["p"] = p;
+        recipe.result_shape = D.shape();
+        NodeId id = g.tape.record(
+            "softmax_dropout", drop_tag, {z}, D,
+            {LazyStash::materialized(probs_tag, StashRole::OpOwnStash, P)},
+            [st, rows, c, mask, p](BackwardCtx& ctx) -> std::vector<Tensor> {
+                const Tensor& pv = ctx.stash(0);
+                Tensor dz = Tensor::empty(pv.shape());
+                check(tempo_attn_probs_bwd(ctx.grad_out().data(), pv.data(), mask.words(), p,
+                                           dz.data(), nullptr, rows, c, st));
+                return {dz};
+            });
+        g.tape.charge(id, mask_tag, StashRole::OpOwnStash, mask);
+        g.tape.set_output_recipe(id, std::move(recipe));
+        return id;
+    }
     NodeId pn = g.tape.record("softmax_ip", probs_tag, {z}, P,
                               {LazyStash::materialized(probs_tag, StashRole::OpOwnStash, P)},
                               [st, rows, c](BackwardCtx& ctx) -> std::vector<Tensor> {
@@ -854,6 +928,7 @@ NodeId softmax_dropout(Graph& g, NodeId z, double p, BoolMask mask, std::uint64_
 
 NodeId sdpa(Graph& g, NodeId q, NodeId k, NodeId v, double p, BoolMask mask,
             const std::string& prefix) {  // ops_tempo.cpp:196-210
+    StreamScope scope_(g.stream);
     const Shape& qs = g.value(q).shape();
     if (qs.size() != 4) throw DimensionError("sdpa expects [B,A,S,d] inputs, got " + shape_str(qs));
     const std::int64_t d = qs.back();
@@ -870,6 +945,7 @@ NodeId sdpa(Graph& g, NodeId q, NodeId k, NodeId v, double p, BoolMask mask,
 namespace ref_ops {
 NodeId dropout(Graph& g, NodeId x, double p, BoolMask mask, std::string tag,
                std::string mask_tag) {  // ops_reference.cpp:214-225
+    StreamScope scope_(g.stream);
     const Tensor& vx = g.value(x);
     require_same_shape(vx.shape(), mask.shape(), "mask_scale");
     Tensor y = Tensor::empty(vx.shape());

@@ -280,6 +280,22 @@ static void test_softmax_dropout_fused() {
         kept += k;
     }
     CHECK(std::abs(kept / double(rows * c) - 0.9) < 0.02);
+    // single-node form (probs_out = nullptr): same D, and its fused backward
+    // (attention-probs kernel) gives the same dZ as the two-node chain
+    Graph f;
+    NodeId zf = f.leaf(Tensor::from_host({rows, c}, zh), "z");
+    NodeId df = tempo_ops::softmax_dropout(f, zf, 0.1, mask, 0, 0, "p", "d", "m", nullptr);
+    std::vector<float> Df = f.value(df).to_host();
+    CHECK(std::memcmp(Da.data(), Df.data(), Da.size() * 4) == 0);
+    CHECK(f.ledger.live_by_tag().at("p") == rows * c * 4);
+    CHECK(f.ledger.live_by_tag().at("m") == rows * c / 8);
+    std::vector<float> gh = randn(rows * c, 17);
+    GradientMap ga = a.tape.backward(da, Tensor::from_host({rows, c}, gh));
+    GradientMap gf = f.tape.backward(df, Tensor::from_host({rows, c}, gh));
+    std::vector<float> dza = ga.at(za).to_host(), dzf = gf.at(zf).to_host();
+    double worst = 0;
+    for (std::int64_t i = 0; i < rows * c; ++i) worst = std::max(worst, rel_err(dza[i], dzf[i]));
+    CHECK(worst <= 1e-6);
 }
 
 static void test_hidden_dropout() {
