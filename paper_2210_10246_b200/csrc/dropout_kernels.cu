@@ -277,7 +277,7 @@ cudaError_t fwd(const float* x, double scale, uint64_t thresh, uint32_t* mask, u
         // work per element) keeps one persistent wave
         int grid = grid_for((const void*)k, kBlock, 0, (warps * 32 + kBlock - 1) / kBlock, 0,
                             PHILOX ? 1 : TM_DROPOUT_WAVES);
-        pdl(k, grid, kBlock, 0, st)(x, mask, scale, thresh, seed, offset, y, n);
+        launch(k, grid, kBlock, 0, st)(x, mask, scale, thresh, seed, offset, y, n);
         return cudaGetLastError();
     }
     const bool vec = aligned16(x) && aligned16(y) && aligned16(mask) && (offset & 3u) == 0;
@@ -285,12 +285,12 @@ cudaError_t fwd(const float* x, double scale, uint64_t thresh, uint32_t* mask, u
         auto k = dropout_fwd_vec_kernel<PHILOX>;
         const int64_t warps = ((n >> 7) + kUnroll - 1) / kUnroll + 1;
         int grid = grid_for((const void*)k, kBlock, 0, (warps * 32 + kBlock - 1) / kBlock);
-        pdl(k, grid, kBlock, 0, st)(x, mask, scale, thresh, seed, offset, y, n);
+        launch(k, grid, kBlock, 0, st)(x, mask, scale, thresh, seed, offset, y, n);
     } else {
         auto k = dropout_fwd_scalar_kernel<PHILOX>;
         const int64_t warps = (n + 31) >> 5;
         int grid = grid_for((const void*)k, kBlock, 0, (warps * 32 + kBlock - 1) / kBlock);
-        pdl(k, grid, kBlock, 0, st)(x, mask, scale, thresh, seed, offset, y, n);
+        launch(k, grid, kBlock, 0, st)(x, mask, scale, thresh, seed, offset, y, n);
     }
     return cudaGetLastError();
 }
@@ -317,28 +317,28 @@ cudaError_t launch_mask_pack(const uint8_t* bytes, uint32_t* bits, int64_t n, in
     if (n == 0) return cudaSuccess;
     const int64_t warps = (n + 31) >> 5;
     int grid = grid_for((const void*)mask_pack_kernel, kBlock, 0, (warps * 32 + kBlock - 1) / kBlock);
-    pdl(mask_pack_kernel, grid, kBlock, 0, st)(bytes, bits, n, status);
+    launch(mask_pack_kernel, grid, kBlock, 0, st)(bytes, bits, n, status);
     return cudaGetLastError();
 }
 
 cudaError_t launch_scale(const float* a, double c, float* out, int64_t n, cudaStream_t st) {
     if (n == 0) return cudaSuccess;
     int grid = grid_for((const void*)scale_kernel, kBlock, 0, (n + kBlock - 1) / kBlock);
-    pdl(scale_kernel, grid, kBlock, 0, st)(a, c, out, n);
+    launch(scale_kernel, grid, kBlock, 0, st)(a, c, out, n);
     return cudaGetLastError();
 }
 
 cudaError_t launch_add(const float* a, const float* b, float* out, int64_t n, cudaStream_t st) {
     if (n == 0) return cudaSuccess;
     int grid = grid_for((const void*)add_kernel, kBlock, 0, (n + kBlock - 1) / kBlock);
-    pdl(add_kernel, grid, kBlock, 0, st)(a, b, out, n);
+    launch(add_kernel, grid, kBlock, 0, st)(a, b, out, n);
     return cudaGetLastError();
 }
 
 cudaError_t launch_mask_unpack(const uint32_t* bits, uint8_t* bytes, int64_t n, cudaStream_t st) {
     if (n == 0) return cudaSuccess;
     int grid = grid_for((const void*)mask_unpack_kernel, kBlock, 0, (n + kBlock - 1) / kBlock);
-    pdl(mask_unpack_kernel, grid, kBlock, 0, st)(bits, bytes, n);
+    launch(mask_unpack_kernel, grid, kBlock, 0, st)(bits, bytes, n);
     return cudaGetLastError();
 }
 

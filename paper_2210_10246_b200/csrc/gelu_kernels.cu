@@ -603,11 +603,11 @@ cudaError_t launch_gelu_fwd(const float* x, float* y, uint32_t* mask, int64_t n,
         auto k = gelu_fwd8_kernel<U>;
         int grid = grid_for((const void*)k, kBlock, 0, (warps_needed * 32 + kBlock - 1) / kBlock, 0,
                             TM_GELU_WAVES);
-        pdl(k, grid, kBlock, 0, st)(x, y, mask, n, xstar_gt, xs_lo);
+        launch(k, grid, kBlock, 0, st)(x, y, mask, n, xstar_gt, xs_lo);
     } else {
         int grid = grid_for((const void*)gelu_fwd_scalar_kernel, kBlock, 0,
                             (((n + 31) >> 5) * 32 + kBlock - 1) / kBlock);
-        pdl(gelu_fwd_scalar_kernel, grid, kBlock, 0, st)(x, y, mask, n, xstar_gt, xs_lo);
+        launch(gelu_fwd_scalar_kernel, grid, kBlock, 0, st)(x, y, mask, n, xstar_gt, xs_lo);
     }
     return cudaGetLastError();
 }
@@ -633,7 +633,7 @@ cudaError_t launch_gelu_bwd(const float* dy, const float* y, const uint32_t* mas
                     : (t.horner ? gelu_bwd_fast_kernel<NC, true, false>                  \
                                 : gelu_bwd_fast_kernel<NC, false, false>);               \
         int grid = grid_for((const void*)k, kBlock, 0, blocks, 0, TM_GELU_WAVES);         \
-        pdl(k, grid, kBlock, 0, st)(dy, y, mask, dx, n, t, vflag);                         \
+        launch(k, grid, kBlock, 0, st)(dy, y, mask, dx, n, t, vflag);                         \
         break;                                                                            \
     }
         switch (nc4) {
@@ -651,9 +651,9 @@ cudaError_t launch_gelu_bwd(const float* dy, const float* y, const uint32_t* mas
     const int64_t warps_needed = vec ? ((n >> 7) + kUnroll - 1) / kUnroll + 1 : (n + 31) >> 5;
     int grid = grid_for(k, kBlock, smem, (warps_needed * 32 + kBlock - 1) / kBlock);
     if (vec) {
-        pdl(gelu_bwd_vec_kernel, grid, kBlock, smem, st)(dy, y, mask, dx, n, t);
+        launch(gelu_bwd_vec_kernel, grid, kBlock, smem, st)(dy, y, mask, dx, n, t);
     } else {
-        pdl(gelu_bwd_scalar_kernel, grid, kBlock, smem, st)(dy, y, mask, dx, n, t);
+        launch(gelu_bwd_scalar_kernel, grid, kBlock, smem, st)(dy, y, mask, dx, n, t);
     }
     return cudaGetLastError();
 }

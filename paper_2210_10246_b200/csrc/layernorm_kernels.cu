@@ -612,7 +612,7 @@ cudaError_t launch_ln_fwd(const float* x, const float* gamma, const float* beta,
     case V: {                                                                                \
         auto k = ln_fwd_warp_kernel<V>;                                                      \
         int grid = grid_for((const void*)k, kWWarps * 32, smem, (rows + kWWarps - 1) / kWWarps, 0, TM_LN_WAVES); \
-        pdl(k, grid, kWWarps * 32, smem, st)(x, gamma, beta, eps, y, rstd, rows, dev_status); \
+        launch(k, grid, kWWarps * 32, smem, st)(x, gamma, beta, eps, y, rstd, rows, dev_status); \
         break;                                                                               \
     }
         switch (vpl) {
@@ -629,10 +629,10 @@ cudaError_t launch_ln_fwd(const float* x, const float* gamma, const float* beta,
         size_t smem = fwd_smem(cols);
         auto k = block <= 256 ? ln_fwd_vec_kernel<256> : ln_fwd_vec_kernel<kMaxThreads>;
         int grid = grid_for((const void*)k, block, smem, (rows + kRows - 1) / kRows);
-        pdl(k, grid, block, smem, st)(x, gamma, beta, eps, y, rstd, rows, (int)cols, dev_status);
+        launch(k, grid, block, smem, st)(x, gamma, beta, eps, y, rstd, rows, (int)cols, dev_status);
     } else {
         int grid = grid_for((const void*)ln_fwd_generic_kernel, 256, 0, rows);
-        pdl(ln_fwd_generic_kernel, grid, 256, 0, st)(x, gamma, beta, eps, y, rstd, rows,
+        launch(ln_fwd_generic_kernel, grid, 256, 0, st)(x, gamma, beta, eps, y, rstd, rows,
                                                      (int)cols, dev_status);
     }
     return cudaGetLastError();
@@ -664,11 +664,11 @@ cudaError_t launch_ln_bwd(const float* dy, const float* y, const float* rstd, co
         using KFn = void (*)(const float*, const float*, const float*, const float*,
                              const float*, float*, double*, int64_t, int);
         KFn k = reinterpret_cast<KFn>(const_cast<void*>(bwd_vec_fn(cols)));
-        pdl(k, grid, bwd_threads(cols), bwd_smem(cols), st)(dy, y, rstd, gamma, beta, dx, w, rows,
+        launch(k, grid, bwd_threads(cols), bwd_smem(cols), st)(dy, y, rstd, gamma, beta, dx, w, rows,
                                                            (int)cols);
     } else {
         size_t smem = (size_t)2 * cols * sizeof(double);
-        pdl(ln_bwd_generic_kernel, grid, 256, smem, st)(dy, y, rstd, gamma, beta, dx, w, rows,
+        launch(ln_bwd_generic_kernel, grid, 256, smem, st)(dy, y, rstd, gamma, beta, dx, w, rows,
                                                        (int)cols);
     }
     const int rgrid = (int)((2 * cols + 31) / 32);

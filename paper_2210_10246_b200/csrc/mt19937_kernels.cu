@@ -271,7 +271,7 @@ cudaError_t launch_mt_keep_bits(uint64_t seed, double p, uint64_t e_begin, int64
     uint64_t* sb = reinterpret_cast<uint64_t*>(w + L.sb_off);
     uint64_t* base = reinterpret_cast<uint64_t*>(w + L.base_off);
 
-    pdl(mt_seed_kernel, 1, 32, 0, st)(seed, seed_st);
+    launch(mt_seed_kernel, 1, 32, 0, st)(seed, seed_st);
 
     const int64_t k0 = (int64_t)(e_begin / kMtChunk);
     const int64_t k1 = (int64_t)((e_begin + (uint64_t)n - 1) / kMtChunk);
@@ -293,11 +293,11 @@ cudaError_t launch_mt_keep_bits(uint64_t seed, double p, uint64_t e_begin, int64
                                   kMtN * sizeof(uint64_t), cudaMemcpyDeviceToDevice, st);
             if (err != cudaSuccess) return err;
         } else {
-            pdl(mt_base_kernel, (unsigned)S, kGenThreads, 0, st)(cur, base);
+            launch(mt_base_kernel, (unsigned)S, kGenThreads, 0, st)(cur, base);
             err = cudaMemsetAsync(nxt, 0, (size_t)(chi - clo + 1) * kMtN * sizeof(uint64_t), st);
             if (err != cudaSuccess) return err;
             dim3 grid(kMtJumpParts, 32, (unsigned)S);
-            pdl(mt_jump_kernel, grid, kJumpThreads, 0, st)(base, jidx, joff, l * 31, nxt, lo * 32,
+            launch(mt_jump_kernel, grid, kJumpThreads, 0, st)(base, jidx, joff, l * 31, nxt, lo * 32,
                                                           clo, chi);
             err = cudaGetLastError();
             if (err != cudaSuccess) return err;
@@ -307,7 +307,7 @@ cudaError_t launch_mt_keep_bits(uint64_t seed, double p, uint64_t e_begin, int64
         hi = chi;
     }
     const uint64_t xmin = mt_keep_threshold(p);
-    pdl(mt_keep_kernel, (unsigned)(k1 - k0 + 1), kGenThreads, 0, st)(cur, k0, e_begin,
+    launch(mt_keep_kernel, (unsigned)(k1 - k0 + 1), kGenThreads, 0, st)(cur, k0, e_begin,
                                                                    e_begin + (uint64_t)n, xmin,
                                                                    mask);
     return cudaGetLastError();

@@ -269,7 +269,7 @@ cudaError_t fwd_vec(int vpl, const float* z, float* P, float* D, uint32_t* mask,
     case V: {                                                                                \
         auto k = softmax_fwd_vec_kernel<V, MODE>;                                            \
         int grid = grid_for((const void*)k, kBlock, 0, (rows * 32 + kBlock - 1) / kBlock, 0, TM_SOFTMAX_WAVES);  \
-        pdl(k, grid, kBlock, 0, st)(z, P, D, mask, scale, thresh, seed, offset, rows);        \
+        launch(k, grid, kBlock, 0, st)(z, P, D, mask, scale, thresh, seed, offset, rows);        \
         break;                                                                               \
     }
     switch (vpl) {
@@ -294,7 +294,7 @@ cudaError_t bwd_vec(int vpl, const float* dD, const float* P, const uint32_t* ma
     case V: {                                                                                \
         auto k = softmax_bwd_vec_kernel<V, DROP, WRITE_D>;                                   \
         int grid = grid_for((const void*)k, kBlock, 0, (rows * 32 + kBlock - 1) / kBlock, 0, TM_SOFTMAX_WAVES);  \
-        pdl(k, grid, kBlock, 0, st)(dD, P, mask, scale, dZ, D, rows);                         \
+        launch(k, grid, kBlock, 0, st)(dD, P, mask, scale, dZ, D, rows);                         \
         break;                                                                               \
     }
     switch (vpl) {
@@ -330,7 +330,7 @@ cudaError_t launch_softmax_fwd(const float* z, float* P, int64_t rows, int64_t c
     if (rows == 0 || cols == 0) return cudaSuccess;
     if (vec_ok(cols, 0, {z, P}))
         return fwd_vec<kPlain>((int)(cols / 128), z, P, nullptr, nullptr, 1.0, 0, 0, 0, rows, st);
-    pdl(softmax_fwd_generic_kernel, generic_grid((const void*)softmax_fwd_generic_kernel, rows),
+    launch(softmax_fwd_generic_kernel, generic_grid((const void*)softmax_fwd_generic_kernel, rows),
                                  kBlock, 0, st)(z, P, nullptr, nullptr, kPlain, 1.0, 0, 0, 0,
                                                   rows, cols);
     return cudaGetLastError();
@@ -342,7 +342,7 @@ cudaError_t launch_softmax_bwd(const float* dP, const float* P, float* dZ, int64
     if (vec_ok(cols, 0, {dP, P, dZ}))
         return bwd_vec<false, false>((int)(cols / 128), dP, P, nullptr, 1.0, dZ, nullptr, rows,
                                      st);
-    pdl(softmax_bwd_generic_kernel, generic_grid((const void*)softmax_bwd_generic_kernel, rows),
+    launch(softmax_bwd_generic_kernel, generic_grid((const void*)softmax_bwd_generic_kernel, rows),
                                  kBlock, 0, st)(dP, P, nullptr, 0, 1.0, dZ, nullptr, rows,
                                                   cols);
     return cudaGetLastError();
@@ -362,7 +362,7 @@ cudaError_t launch_softmax_dropout_fwd(const float* z, double scale, uint64_t th
         cudaError_t e = cudaMemsetAsync(mask, 0, (size_t)((rows * cols + 31) / 32) * 4, st);
         if (e != cudaSuccess) return e;
     }
-    pdl(softmax_fwd_generic_kernel, generic_grid((const void*)softmax_fwd_generic_kernel, rows),
+    launch(softmax_fwd_generic_kernel, generic_grid((const void*)softmax_fwd_generic_kernel, rows),
                                  kBlock, 0, st)(z, P, D, mask, philox ? kPhilox : kSupplied,
                                                   scale, thresh, seed, offset, rows, cols);
     return cudaGetLastError();
@@ -377,7 +377,7 @@ cudaError_t launch_attn_probs_bwd(const float* dD, const float* P, const uint32_
         return D ? bwd_vec<true, true>(vpl, dD, P, mask, scale, dZ, D, rows, st)
                  : bwd_vec<true, false>(vpl, dD, P, mask, scale, dZ, nullptr, rows, st);
     }
-    pdl(softmax_bwd_generic_kernel, generic_grid((const void*)softmax_bwd_generic_kernel, rows),
+    launch(softmax_bwd_generic_kernel, generic_grid((const void*)softmax_bwd_generic_kernel, rows),
                                  kBlock, 0, st)(dD, P, mask, 1, scale, dZ, D, rows, cols);
     return cudaGetLastError();
 }

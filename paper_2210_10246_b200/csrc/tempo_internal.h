@@ -106,7 +106,7 @@ size_t mt_keep_workspace(uint64_t e_begin, int64_t n);
 cudaError_t launch_mt_keep_bits(uint64_t seed, double p, uint64_t e_begin, int64_t n,
                                 uint32_t* mask, void* ws, size_t ws_bytes, cudaStream_t st);
 
-// Type-checked launch: pdl(kernel, grid, block, smem, stream)(args...) is
+// Type-checked launch: launch(kernel, grid, block, smem, stream)(args...) is
 // `kernel<<<grid, block, smem, stream>>>(args...)`, with programmatic stream
 // serialization when TM_PDL=1.  Every kernel of this library starts with
 // grid_dep_wait() (before any global access), which makes PDL safe after any
@@ -114,7 +114,7 @@ cudaError_t launch_mt_keep_bits(uint64_t seed, double p, uint64_t e_begin, int64
 // 2.36-2.44 ms/step), so it is off by default; only the LayerNorm stage-2
 // reduce is launched as a dependent (launch_pdl), where it wins ~2 us.
 template <typename... KArgs>
-struct PdlLaunch {
+struct Launch {
     void (*kernel)(KArgs...);
     cudaLaunchConfig_t cfg;
     cudaLaunchAttribute attr[1];
@@ -126,9 +126,9 @@ struct PdlLaunch {
     }
 };
 template <typename... KArgs>
-PdlLaunch<KArgs...> pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+Launch<KArgs...> launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
                         cudaStream_t st) {
-    PdlLaunch<KArgs...> L;
+    Launch<KArgs...> L;
     L.kernel = kernel;
     L.cfg = cudaLaunchConfig_t{};
     L.cfg.gridDim = grid;
