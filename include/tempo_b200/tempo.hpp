@@ -64,7 +64,8 @@ std::string shape_str(const Shape& s);
 // device's memory pool) on the thread's current stream and released on the
 // same stream; every op builder and backward closure runs under a
 // StreamScope of its Graph's stream.  Tensors made outside ops use the
-// enclosing scope (default: the legacy default stream).
+// enclosing scope (default: the legacy default stream).  A stream must
+// outlive the tensors allocated on it (they are released on it).
 class StreamScope {
 public:
     explicit StreamScope(tempo_stream_t s);
