@@ -132,12 +132,20 @@ class Chain:
         device bit for bit (BoolMask::bernoulli_keep with
         encoder::mask_stream_seed(run seed, salt = step, site 0/1/2),
         encoder.cpp:168-201), each rank at its global offset."""
-        o = self.ops
+        o, torch = self.ops, self.torch
+        main = torch.cuda.current_stream()
+        if not hasattr(self, "_mask_streams"):  # one stream per mask: they overlap
+            self._mask_streams = [torch.cuda.Stream() for _ in range(3)]
         for site, (m, n, off) in enumerate([(self.m_att, ATT_ROWS * S, self.off_att),
                                             (self.m1, T * H, self.off_h),
                                             (self.m2, T * H, self.off_h)]):
-            o.bernoulli_keep_bits_device(n, P_DROP, o.mask_stream_seed(1234, step, site),
-                                         offset=off, out=m)
+            s_ = self._mask_streams[site]
+            s_.wait_stream(main)  # the previous step is done with this mask
+            with torch.cuda.stream(s_):
+                o.bernoulli_keep_bits_device(n, P_DROP, o.mask_stream_seed(1234, step, site),
+                                             offset=off, out=m)
+        for s_ in self._mask_streams:
+            main.wait_stream(s_)
 
     def forward(self, seed):
         o = self.ops
