@@ -207,7 +207,7 @@ def ln_inputs(rows, cols, seed):
 
 
 @pytest.mark.parametrize("rows,cols", [(1, 768), (7, 1024), (333, 768), (64, 4), (5, 1000),
-                                       (3, 2052), (16384, 768)])
+                                       (3, 2052), (16384, 768), (100, 256), (37, 512), (9, 1536)])
 def test_layernorm_forward(tops, port, cuda, rows, cols):
     import torch
     x, gam, bet, _ = ln_inputs(rows, cols, rows * cols)
@@ -219,7 +219,7 @@ def test_layernorm_forward(tops, port, cuda, rows, cols):
 
 
 @pytest.mark.parametrize("rows,cols", [(1, 768), (7, 1024), (333, 768), (64, 4), (5, 1000),
-                                       (3, 2052), (16384, 768)])
+                                       (3, 2052), (16384, 768), (100, 256), (37, 512), (9, 1536)])
 def test_layernorm_backward_identical_inputs(tops, port, cuda, rows, cols):
     import torch
     x, gam, bet, dy = ln_inputs(rows, cols, 3 + rows * cols)
@@ -273,7 +273,8 @@ def test_layernorm_refusals(tops, cuda):
 
 # ------------------------------------------------- softmax + attention dropout
 @pytest.mark.parametrize("rows,cols", [(1, 512), (24, 512), (7, 384), (9, 1024), (5, 100),
-                                       (3, 77), (12 * 512, 512)])
+                                       (3, 77), (12 * 512, 512), (10, 128), (6, 256), (5, 768),
+                                       (3, 1280)])
 def test_softmax_dropout_supplied_mask(tops, port, cuda, rows, cols):
     import torch
     g = np.random.default_rng(rows + cols)
