@@ -390,6 +390,48 @@ static void test_sdpa() {
     CHECK(throws<DimensionError>([&] { tempo_ops::sdpa(g2, bad, bad, bad, p, mask); }));
 }
 
+// The same graph on a non-blocking stream (stream-ordered pooled allocation,
+// tape and recompute on that stream) gives the same bits as on the default
+// stream, forward and backward, including the recomputed dropout map.
+static void test_graph_on_stream() {
+    const std::int64_t rows = 64, m = 1024, S = 512;
+    std::vector<float> xh = randn(rows * m, 31), gh = randn(rows * m, 32), zh = randn(rows * S, 33);
+    std::vector<float> gam(m, 1.1f), bet(m, 0.05f);
+    BoolMask mask = BoolMask::bernoulli_keep({rows, S}, 0.1, 34);
+    GeluPolyTable table = GeluPolyTable::default_fit();
+    auto run = [&](cudaStream_t st) -> std::vector<std::vector<float>> {
+        std::vector<std::vector<float>> out;
+        Graph g;
+        g.stream = st;
+        NodeId x = g.leaf(Tensor::from_host({rows, m}, xh), "x");
+        NodeId ga = g.param(Tensor::from_host({m}, gam), "g"), be = g.param(Tensor::from_host({m}, bet), "b");
+        NodeId y = tempo_ops::gelu(g, x, &table, "y", "ym");
+        NodeId l = tempo_ops::layernorm(g, y, ga, be, 1e-5, "l", "lr");
+        out.push_back(g.value(l).to_host());
+        GradientMap gm = g.tape.backward(l, Tensor::from_host({rows, m}, gh));
+        out.push_back(gm.at(x).to_host());
+        out.push_back(gm.at(ga).to_host());
+        Graph h;
+        h.stream = st;
+        NodeId z = h.leaf(Tensor::from_host({rows, S}, zh), "z");
+        NodeId d = tempo_ops::softmax_dropout(h, z, 0.1, mask, 0, 0, "p", "d", "dm", nullptr);
+        NodeId v = h.leaf(Tensor::from_host({S, 16}, randn(S * 16, 36)), "v");
+        NodeId c = h.matmul(d, v, "c");  // stashes D through the recompute recipe
+        out.push_back({(float)h.ledger.live_by_tag().count("d")});  // D is not stashed
+        out.push_back(h.value(c).to_host());
+        GradientMap hm = h.tape.backward(c, Tensor::from_host({rows, 16}, randn(rows * 16, 35)));
+        out.push_back(hm.at(z).to_host());
+        out.push_back(hm.at(v).to_host());
+        return out;
+    };
+    cudaStream_t st;
+    CHECK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) == cudaSuccess);
+    auto a = run(nullptr), b = run(st);
+    cudaStreamDestroy(st);
+    CHECK(a[3][0] == 0.0f);
+    for (size_t i = 0; i < a.size(); ++i) CHECK(a[i] == b[i]);
+}
+
 // A large mask goes through the device generator (jump-ahead): it must be
 // the reference's stream bit for bit (here: against the host engine).
 static void test_large_mask_device_stream() {
@@ -413,6 +455,7 @@ int main() {
     run("hidden dropout", test_hidden_dropout);
     run("large mask: device reference stream", test_large_mask_device_stream);
     run("sdpa (cuBLAS GEMMs + Tempo softmax/dropout)", test_sdpa);
+    run("graph on a non-blocking stream", test_graph_on_stream);
     std::printf("%d failure(s)\n", g_fail);
     return g_fail;
 }
