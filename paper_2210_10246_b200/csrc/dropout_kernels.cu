@@ -20,6 +20,9 @@ constexpr int kUnroll = 4;
 #ifndef TM_DROPOUT_V8
 #define TM_DROPOUT_V8 1
 #endif
+#ifndef TM_DROPOUT_PHILOX_WAVES
+#define TM_DROPOUT_PHILOX_WAVES 1
+#endif
 #ifndef TM_DROPOUT_WAVES
 #define TM_DROPOUT_WAVES 8
 #endif
@@ -276,7 +279,7 @@ cudaError_t fwd(const float* x, double scale, uint64_t thresh, uint32_t* mask, u
         // supplied masks: several waves of CTAs balance better; Philox (more
         // work per element) keeps one persistent wave
         int grid = grid_for((const void*)k, kBlock, 0, (warps * 32 + kBlock - 1) / kBlock, 0,
-                            PHILOX ? 1 : TM_DROPOUT_WAVES);
+                            PHILOX ? TM_DROPOUT_PHILOX_WAVES : TM_DROPOUT_WAVES);
         launch(k, grid, kBlock, 0, st)(x, mask, scale, thresh, seed, offset, y, n);
         return cudaGetLastError();
     }
