@@ -36,13 +36,40 @@ constexpr int kBlock = 256;
 
 enum FwdMode { kPlain = 0, kSupplied = 1, kPhilox = 2 };
 
+#ifndef TM_SOFTMAX_TWOSUM
+#define TM_SOFTMAX_TWOSUM 1
+#endif
+#ifndef TM_SOFTMAX_EXP
+#define TM_SOFTMAX_EXP 1  // 1: SFU ex2 + FMA-split exponent (+ TwoSum: 0.94 -> 0.96, P err 5e-7); 0: expf + TwoSum
+#endif
+__device__ __forceinline__ float ex2_approx_ftz(float f) {
+    float r;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(f));
+    return r;
+}
 // exp(z - mx) with the rounding error of the subtraction restored.
 __device__ __forceinline__ float exp_shift(float z, float mx) {
+#if TM_SOFTMAX_EXP == 1
+    // 2^(d log2 e): w = d*L2E rounded, its error folded back (~2 ulp total)
+    const float L2E = 1.44269502162933349609f, L2E_LO = 1.925963033500011e-08f;
+    const float d = z - mx;
+    const float w = d * L2E;
+    const float wl = fmaf(d, L2E_LO, fmaf(d, L2E, -w));
+    const float e = ex2_approx_ftz(w);
+#if TM_SOFTMAX_TWOSUM
+    const float bb = d - z;
+    const float err = (z - (d - bb)) + (-mx - bb);  // TwoSum: (z - mx) = d + err exactly
+    return fmaf(e, fmaf(wl, 0.69314718055994531f, err), e);
+#else
+    return fmaf(e, wl * 0.69314718055994531f, e);
+#endif
+#else
     float d = z - mx;
     float bb = d - z;
     float err = (z - (d - bb)) + (-mx - bb);  // TwoSum: (z - mx) = d + err exactly
     float e = expf(d);
     return fmaf(e, err, e);
+#endif
 }
 
 __device__ __forceinline__ float dscale(float v, double s) { return (float)((double)v * s); }

@@ -30,7 +30,10 @@ def main():
         "dropout_fwd": lambda: o.dropout_fwd(c.x_ffn2, 0.1, mask=c.m2, generate=True, seed=9, y=c.d2),
         "copy_1GB": lambda: c.dZ.copy_(c.z),
     }
+    only = [a for a in sys.argv[1:]]
     for name, fn in calls.items():
+        if only and name not in only:
+            continue
         fn()
         torch.cuda.synchronize()
         p = subprocess.Popen(["nvidia-smi", "--id=0", "--query-gpu=power.draw,clocks.sm",
