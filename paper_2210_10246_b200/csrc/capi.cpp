@@ -217,6 +217,7 @@ void build_device(tempo_gelu_table_s& t) {
             const Segment& s = *sp;
             d.lo_up[k] = float_up(s.lo);
             d.sqrt_shift[k] = s.sqrt_shift ? 1 : 0;
+            double sc = 0.0, u0 = 0.0;  // t = sc * (u - u0)
             if (s.coeffs.size() == 1) {
                 d.s[k] = 0.0f;
                 d.b[k] = 0.0f;
@@ -229,20 +230,38 @@ void build_device(tempo_gelu_table_s& t) {
                     ulo = s.lo;
                     uhi = s.hi;
                 }
-                double sc = 2.0 / (uhi - ulo);
+                sc = 2.0 / (uhi - ulo);
+                u0 = 0.5 * (uhi + ulo);
                 d.s[k] = (float)sc;
                 d.b[k] = (float)(-(uhi + ulo) / (uhi - ulo));
                 if (d.s[k] == 0.0f) d.s[k] = std::numeric_limits<float>::min();
             }
             for (std::size_t c = 0; c < s.coeffs.size(); ++c) d.coef[k][c] = (float)s.coeffs[c];
-            if (s.coeffs.size() <= 16) {
+            if (s.coeffs.size() <= 15) {
+                // power basis of t, then of v = u - u0 with t = sc * v:
+                // a'_k = a_k * sc^k; |sc * v| <= 1 inside the segment, so
+                // Horner's bound in v is the one in t
                 std::vector<double> a = cheb_to_mono(s.coeffs);
-                double suma = 0.0;
+                double suma = 0.0, sumd = 0.0, sk = 1.0;
+                d.u0[k] = (float)u0;
                 for (std::size_t c = 0; c < a.size(); ++c) {
-                    d.mono[k][c] = (float)a[c];
+                    const double ak = a[c] * sk;
+                    d.monov[k][c] = (float)ak;
+                    if (!std::isfinite(d.monov[k][c]) ||
+                        (ak != 0.0 && std::abs(ak) < (double)std::numeric_limits<float>::min()))
+                        horner = false;
+                    sk *= sc;
                     suma += std::abs(a[c]);
+                    sumd += (double)c * std::abs(a[c]);  // bounds |p'(t)| on [-1, 1]
                 }
-                if (suma * (2.0 * (double)a.size() + 2.0) * 0x1p-24 > 4e-6) horner = false;
+                // Horner's (2d+2)eps sum|a_k|, plus the fp32 roundings of u
+                // and u0 (each <= eps |u|) moved through t = sc * v
+                const double umax = std::abs(u0) + (sc > 0.0 ? 1.0 / sc : 0.0);
+                if (suma * (2.0 * (double)a.size() + 2.0) * 0x1p-24 +
+                        sumd * sc * 2.0 * umax * 0x1p-24 > 4e-6)
+                    horner = false;
+            } else {
+                horner = false;
             }
             ++k;
         }

@@ -380,12 +380,17 @@ __device__ __forceinline__ float min_nan(float a, float b) {
     return r;
 }
 
-// h(y, m) without data-dependent branches.  The clamp y < y_min -> y_min
-// (:183,:186) falls out of the variable maps (sqrt(max(y - y_min, 0)) = 0,
-// or t <= -1 clamped); m = 0, y >= 0 -> 0 (:182) is the device table's extra
-// constant-0 segment [0, inf) on branch 0; y = +inf is clamped to FLT_MAX so
-// constant segments see u*0 = 0.
-template <int NC4, bool HORNER>
+// h(y, m) without data-dependent branches.  y < y_min -> y_min (:183,:186)
+// is a clamp on y (the first segment of each branch starts at y_min, and
+// sqrt(max(y - y_min, 0)) = 0 for sqrt-shift segments); m = 0, y >= 0 -> 0
+// (:182) is the device table's extra constant-0 segment [0, inf) on branch
+// 0; y = +inf is clamped to FLT_MAX so constant segments see 0 * v = 0.
+// HV (Horner in v = u - u0): the segment record holds the power-basis
+// coefficients of v in its first 4*NC4-1 slots and u0 in the last, so one
+// segment costs NC4 128-bit smem loads and no (s, b) load or t clamp (the
+// segment search keeps v inside the segment up to fp32 rounding, which the
+// host's error bound covers).  Else Clenshaw in t as the reference.
+template <int NC4, bool HV>
 __device__ __forceinline__ float gelu_h_fast(float y, uint32_t m, const FastTable<NC4>& ft,
                                              const float (&thr0)[3], const float (&thr1)[3],
                                              int base1, uint32_t sqrt_mask, float ymin_hi,
@@ -394,7 +399,6 @@ __device__ __forceinline__ float gelu_h_fast(float y, uint32_t m, const FastTabl
     int seg = m ? base1 : 0;
 #pragma unroll
     for (int k = 0; k < 3; ++k) seg += (y >= (m ? thr1[k] : thr0[k])) ? 1 : 0;
-    const float2 sb = ft.sb[seg];
     const float d = (y - ymin_hi) - ymin_lo;
     // branch-free variable choice (the SFU sqrt is cheaper than a divergent branch)
     const float sq = sqrt_approx(max_nan(d, 0.0f));
@@ -403,8 +407,7 @@ __device__ __forceinline__ float gelu_h_fast(float y, uint32_t m, const FastTabl
         "setp.ne.u32 p, %3, 0;\n\t"
         "selp.f32 %0, %1, %2, p;\n}"
         : "=f"(u)
-        : "f"(sq), "f"(y), "r"((sqrt_mask >> seg) & 1u));
-    const float tt = max_nan(min_nan(fmaf(u, sb.x, sb.y), 1.0f), -1.0f);
+        : "f"(sq), "f"(HV ? max_nan(y, ymin_hi) : y), "r"((sqrt_mask >> seg) & 1u));
     const float4* rec = ft.rec + seg * FastTable<NC4>::kStride4;
     float c[4 * NC4];
 #pragma unroll
@@ -415,12 +418,15 @@ __device__ __forceinline__ float gelu_h_fast(float y, uint32_t m, const FastTabl
         c[4 * j + 2] = q.z;
         c[4 * j + 3] = q.w;
     }
-    if (HORNER) {  // power basis, host-converted (error bound checked, capi.cpp)
-        float h = c[4 * NC4 - 1];
+    if (HV) {
+        const float v = u - c[4 * NC4 - 1];
+        float h = c[4 * NC4 - 2];
 #pragma unroll
-        for (int k = 4 * NC4 - 2; k >= 0; --k) h = fmaf(h, tt, c[k]);
+        for (int k = 4 * NC4 - 3; k >= 0; --k) h = fmaf(h, v, c[k]);
         return h;
     }
+    const float2 sb = ft.sb[seg];
+    const float tt = max_nan(min_nan(fmaf(u, sb.x, sb.y), 1.0f), -1.0f);
     const float t2 = tt + tt;  // Clenshaw (gelu_table.cpp:43-51)
     float b1 = 0.0f, b2 = 0.0f;
 #pragma unroll
@@ -451,15 +457,19 @@ __global__ void __launch_bounds__(kBlock) gelu_bwd_fast_kernel(
         float4 q = make_float4(0.f, 0.f, 0.f, 0.f);
         if (j < NC4) {
             const int k = 4 * j;
-            const float* src = HORNER ? t.mono[sgi] : t.coef[sgi];
-            q.x = k < t.ncoef ? src[k] : 0.f;
-            q.y = k + 1 < t.ncoef ? src[k + 1] : 0.f;
-            q.z = k + 2 < t.ncoef ? src[k + 2] : 0.f;
-            q.w = k + 3 < t.ncoef ? src[k + 3] : 0.f;
+            const float* src = HORNER ? t.monov[sgi] : t.coef[sgi];
+            float e[4];
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                e[r] = k + r < t.ncoef ? src[k + r] : 0.f;
+                if (HORNER && k + r == 4 * NC4 - 1) e[r] = t.u0[sgi];  // last slot: u0
+            }
+            q = make_float4(e[0], e[1], e[2], e[3]);
         }
         ft.rec[i] = q;
     }
-    for (int i = threadIdx.x; i < nseg; i += kBlock) ft.sb[i] = make_float2(t.s[i], t.b[i]);
+    if (!HORNER)
+        for (int i = threadIdx.x; i < nseg; i += kBlock) ft.sb[i] = make_float2(t.s[i], t.b[i]);
     float thr0[3], thr1[3];
     uint32_t sqrt_mask = 0;
 #pragma unroll
@@ -620,17 +630,19 @@ cudaError_t launch_gelu_bwd(const float* dy, const float* y, const uint32_t* mas
     // the 256-bit, float4 and scalar loops share gelu_h_fast -> same bits)
     const bool fast = t.nseg[0] <= kFastSegPerBranch && t.nseg[1] <= kFastSegPerBranch &&
                       t.ncoef <= 16;
+    const bool hv = t.horner && t.ncoef <= 15;  // Horner in v: u0 takes one more slot
     if (fast) {
-        const int nc4 = (t.ncoef + 3) / 4;
+        // Horner in v needs one slot for u0 after the coefficients
+        const int nc4 = (t.ncoef + (hv ? 4 : 3)) / 4;
         const bool v8a = TM_GELU_BWD_V8 && aligned32(dy) && aligned32(y) && aligned32(dx);
         const bool v8 = v8a || !vec;  // unaligned: the V8 kernel's scalar loop
         const int vflag = v8a ? 1 : 0;
         const int64_t blocks = ((n >> 7) / 2 + 1) * 32 / kBlock + 1;
 #define TB_CASE(NC)                                                                       \
     case NC: {                                                                            \
-        auto k = v8 ? (t.horner ? gelu_bwd_fast_kernel<NC, true, true>                      \
+        auto k = v8 ? (hv ? gelu_bwd_fast_kernel<NC, true, true>                            \
                             : gelu_bwd_fast_kernel<NC, false, true>)                     \
-                    : (t.horner ? gelu_bwd_fast_kernel<NC, true, false>                  \
+                    : (hv ? gelu_bwd_fast_kernel<NC, true, false>                        \
                                 : gelu_bwd_fast_kernel<NC, false, false>);               \
         int grid = grid_for((const void*)k, kBlock, 0, blocks, 0, TM_GELU_WAVES);         \
         launch(k, grid, kBlock, 0, st)(dy, y, mask, dx, n, t, vflag);                         \

@@ -36,11 +36,15 @@ struct GeluDevTable {
     float b[kMaxSeg];
     int sqrt_shift[kMaxSeg];
     float coef[kMaxSeg][kMaxCoef];  // Chebyshev coefficients, zero padded
-    // Specialized kernel only: the same polynomials in the power basis of t
-    // (host fp64 conversion), used with Horner's rule when `horner` is set
-    // (the conversion's error bound is small enough, see capi.cpp).
+    // Specialized kernel only: the same polynomials in the power basis of
+    // v = u - u0 (u0 the segment's midpoint, t = s * v), i.e. coefficients
+    // a_k * s^k of the power basis a_k in t (host fp64 conversion), used with
+    // Horner's rule when `horner` is set (the conversion's error bound is
+    // small enough, see capi.cpp).  No (s, b) and no clamp: the segment
+    // search keeps v inside the segment, y < y_min is clamped on y.
     int horner;
-    float mono[kMaxSeg][16];
+    float monov[kMaxSeg][16];
+    float u0[kMaxSeg];
 };
 
 // Kernel launchers (defined in the .cu files; return cudaGetLastError()).
