@@ -61,6 +61,16 @@ def op_bytes(batch=B):
     }
 
 
+def op_elements(batch=B):
+    """Elements each op processes per step (the map it streams: n for the
+    elementwise ops, rows x cols for the row ops; both LNs / dropouts)."""
+    t, ar = batch * S, batch * A * S
+    n_g, n_h, n_a = t * 4 * H, t * H, ar * S
+    return {"softmax_dropout_fwd": n_a, "attn_probs_bwd": n_a, "gelu_fwd": n_g, "gelu_bwd": n_g,
+            "layernorm_fwd": 2 * n_h, "layernorm_bwd": 2 * n_h, "dropout_fwd": 2 * n_h,
+            "dropout_bwd": 2 * n_h}
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -419,12 +429,14 @@ def main():
 
     # ---- per-op device times (outside the timed region) -------------------
     per_op = chain.per_op_timings(reps=11, flush=flush)
-    ob = op_bytes()
+    ob, oe = op_bytes(), op_elements()
     per_op_rows = []
     for name, (t_ms, mult) in per_op.items():
         gbs = ob[name] / (t_ms * 1e-3) / 1e9
         per_op_rows.append({"op": name, "ms": round(t_ms, 4), "bytes": int(ob[name]),
                             "gbs": round(gbs, 1), "frac": round(gbs / peak, 4),
+                            "elements": int(oe[name]),
+                            "gelem_per_s": round(oe[name] / (t_ms * 1e-3) / 1e9, 2),
                             "launches": mult})
     top = max(per_op_rows, key=lambda r: r["ms"])
     roofline = {"bound": "hbm", "kernel": top["op"], "achieved": top["gbs"], "peak": peak,
@@ -512,6 +524,8 @@ def main():
             "clocks": clk,
             "per_op": per_op_rows,
             "frac_of_peak": round(value / world / peak, 4),
+            "elements_per_s": {"value": round(sum(op_elements().values()) * world / (ms * 1e-3) / 1e9, 2),
+                               "unit": "Gelem/s", "what": "elements streamed by all ops of the chain"},
             "stash": stash_report(chain),
         }
         print(json.dumps(line), flush=True)
