@@ -578,9 +578,11 @@ int bwd_threads(int64_t cols) {
 }
 const void* bwd_vec_fn(int64_t cols) {
     const int t = bwd_threads(cols);
+#if TM_LN_BWD_CPT2  // (off by default: measured slower; not instantiated)
     if (bwd_cpt(cols) == 2)
         return t <= 256 ? (const void*)ln_bwd_vec_kernel<256, 2>
                         : (const void*)ln_bwd_vec_kernel<kMaxThreads, 2>;
+#endif
     return t <= 256 ? (const void*)ln_bwd_vec_kernel<256, 1>
                     : (const void*)ln_bwd_vec_kernel<kMaxThreads, 1>;
 }
