@@ -67,7 +67,7 @@ def main():
             b.record(st)
             b.synchronize()
             ts.append(a.elapsed_time(b))
-        t = statistics.median(ts)
+        t = bench.trimmed_mean(ts)
         key = names.get(name, name)
         nbytes = ob[key] / (2 if key in ("layernorm_fwd", "layernorm_bwd", "dropout_fwd", "dropout_bwd", "copy_h") else 1)
         h = hashlib.sha1()
