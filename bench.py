@@ -61,6 +61,35 @@ def op_bytes(batch=B):
     }
 
 
+def setup_peer(chain, dist, rank, world, dev, backend):
+    """Map every rank's LN exchange buffers (CUDA IPC) and self-check one
+    exchange against the known answer on all ranks; None -> fall back to the
+    all-reduce.  Off for the gloo functional mode (ranks sharing one GPU) and
+    with TEMPO_PEER=0."""
+    import torch
+    if backend != "nccl" or os.environ.get("TEMPO_PEER", "1") != "1":
+        return None
+    peer, ok = None, 1
+    try:
+        peer = chain.ops.LnPeerRank.ipc(H, dev)
+        parts = torch.full((3, 2 * H), float(rank + 1), dtype=torch.float64, device=dev)
+        dg, db = chain.ops.ln_param_reduce_peer(parts, H, peer)
+        torch.cuda.synchronize()
+        peer.check_status()
+        want = 3.0 * sum(r + 1 for r in range(world))
+        ok = int(bool((dg == want).all()) and bool((db == want).all()))
+    except Exception as ex:  # noqa: BLE001  (any failure: use the all-reduce)
+        print(f"rank {rank}: peer exchange unavailable ({ex}); using all_reduce", file=sys.stderr)
+        ok = 0
+    flag = torch.tensor([ok], dtype=torch.int32, device=dev)
+    dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+    if int(flag.item()) == 0:
+        if peer is not None:
+            peer.close()
+        return None
+    return peer
+
+
 def trimmed_mean(ts):
     """Mean of the middle ~60 % of the samples.  CUDA event times on this
     GPU are quantised (~2.05 us steps), so for the 40-50 us ops a median
@@ -94,6 +123,7 @@ def peaks():
 # ------------------------------------------------------------ the chain
 class Chain:
     """Device buffers + the step of the Tempo op chain (weak-scaled rank)."""
+    peer = None  # ops.LnPeerRank at N>1: the fused dgamma/dbeta exchange
 
     def __init__(self, dev, rank, world, seed=1234):
         import torch
@@ -185,15 +215,23 @@ class Chain:
         o.layernorm_ip_fwd(self.d2, self.g2, self.b2, check_gamma=False, y=self.y_ln2,
                            rstd=self.rs2, dev_status=self.status)
 
+    def _ln_bwd(self, dy, y, rs, g, b, dx, dg, db):
+        if self.peer is not None:  # N>1: cross-rank sum fused into stage 2
+            self.ops.layernorm_ip_bwd_peer(dy, y, rs, g, b, self.peer, dx=dx, dgamma=dg, dbeta=db,
+                                           workspace=self.ws)
+        else:
+            self.ops.layernorm_ip_bwd(dy, y, rs, g, b, dx=dx, dgamma=dg, dbeta=db,
+                                      workspace=self.ws)
+
     def backward(self, allreduce):
         o = self.ops
         dp = self.dparams
-        o.layernorm_ip_bwd(self.dy_ln2, self.y_ln2, self.rs2, self.g2, self.b2, dx=self.dx_ln2,
-                           dgamma=dp[0:H], dbeta=dp[H:2 * H], workspace=self.ws)
+        self._ln_bwd(self.dy_ln2, self.y_ln2, self.rs2, self.g2, self.b2, self.dx_ln2,
+                     dp[0:H], dp[H:2 * H])
         o.dropout_bwd(self.dx_ln2, self.m2, P_DROP, dx=self.dx_d2)
         o.gelu_ip_bwd(self.dy_gelu, self.y_g, self.m_g, self.table, dx=self.dx_g)
-        o.layernorm_ip_bwd(self.dy_ln1, self.y_ln1, self.rs1, self.g1, self.b1, dx=self.dx_ln1,
-                           dgamma=dp[2 * H:3 * H], dbeta=dp[3 * H:], workspace=self.ws)
+        self._ln_bwd(self.dy_ln1, self.y_ln1, self.rs1, self.g1, self.b1, self.dx_ln1,
+                     dp[2 * H:3 * H], dp[3 * H:])
         if allreduce is not None:
             allreduce(dp)  # the one collective: bucketed LN dgamma/dbeta (16 KB)
         o.dropout_bwd(self.dx_ln1, self.m1, P_DROP, dx=self.dx_d1)
@@ -402,6 +440,16 @@ def main():
     chain.mask_mode = args.masks
     from paper_2210_10246_b200.dist import allreduce_ln_params
     allreduce = allreduce_ln_params if world > 1 else None
+    collective = None
+    if world > 1:
+        # the product path: the dgamma/dbeta sum fused into each LN backward's
+        # stage 2 over peer memory (CUDA IPC mappings); NCCL all-reduce only
+        # if the peer setup or its self-check fails
+        chain.peer = setup_peer(chain, dist, rank, world, dev, backend)
+        if chain.peer is not None:
+            allreduce = None
+        collective = ("fused peer-memory exchange in the LN backward stage 2"
+                      if chain.peer is not None else f"{backend} all_reduce of the dgamma/dbeta bucket")
     flush_buf = torch.empty(256 * 1024 * 1024 // 4, device=dev)
     flush = lambda: flush_buf.fill_(0.0)  # noqa: E731  (256 MB > 126 MB L2)
 
@@ -494,7 +542,12 @@ def main():
     # ---- e2e: the public API with host buffers -----------------------------
     e2e = None
     if not args.no_e2e:
+        if world > 1:
+            dist.barrier()  # rank 0's extra measurements above: realign before the exchanges
         e2e = e2e_measure(chain, args, world, allreduce, dist if world > 1 else None)
+    if chain.peer is not None:
+        torch.cuda.synchronize()
+        chain.peer.check_status()  # no exchange may have timed out (results would be partial)
 
     # ---- CPU baseline (reference library on host cores, rank 0, N=1) -------
     cpu = None
@@ -522,7 +575,8 @@ def main():
                       "every step)")),
             "config": {"workload": WORKLOAD, "batch_per_gpu": B, "global_batch": B * world,
                        "seq_len": S, "hidden": H, "heads": A, "dropout_p": P_DROP,
-                       "parallelism": f"rows{world}", "l2": "working set 12.7 GB/step >> 126 MB L2",
+                       "parallelism": f"rows{world}", "collective": collective,
+                       "l2": "working set 12.7 GB/step >> 126 MB L2",
                        "baseline_config": "configs[3] at N=1; configs[4] (B=512) at N=8"},
             "roofline": roofline,
             "cpu_baseline": cpu,

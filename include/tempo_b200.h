@@ -125,6 +125,44 @@ int tempo_ln_ip_bwd(const float* dy, const float* y, const float* rstd, const fl
                     const float* beta, float* dx, float* dgamma, float* dbeta, void* workspace,
                     size_t workspace_bytes, int64_t rows, int64_t cols, tempo_stream_t stream);
 
+/* Multi-GPU: the path's one collective -- the sum of every
+ * rank's LayerNorm dgamma/dbeta -- fused into the backward's stage 2 over
+ * peer memory instead of a separate all-reduce (replaces the reference's
+ * serial accumulation in the backward closure, ops_tempo.cpp:150-151, summed
+ * over row shards).  Each rank owns an inbox and a flag buffer (sizes below,
+ * zero-initialised once) that every rank can address: same process (tests),
+ * P2P peers, or CUDA IPC mappings (tempo_ipc_*).  `inbox` / `flags` are
+ * DEVICE arrays of `world` pointers (rank p's buffers as mapped here); epoch
+ * is 1, 2, 3, ... per exchange (the same on all ranks).  The result is the
+ * fixed-order (rank 0, 1, ...) sum of the ranks' fixed-order partial sums:
+ * bitwise identical on every rank.  A peer that never arrives sets *status
+ * to TEMPO_ERR_STATE after a bounded wait instead of hanging the GPU. */
+typedef struct {
+    int32_t rank;
+    int32_t world;
+    double* const* inbox;
+    uint32_t* const* flags;
+    uint32_t epoch;
+    int32_t* status;
+} tempo_ln_peer_t;
+size_t tempo_ln_peer_inbox_bytes(int32_t world, int64_t cols);
+size_t tempo_ln_peer_flag_bytes(int32_t world, int64_t cols);
+/* tempo_ln_ip_bwd with the cross-rank dgamma/dbeta sum fused in. */
+int tempo_ln_ip_bwd_peer(const float* dy, const float* y, const float* rstd, const float* gamma,
+                         const float* beta, float* dx, float* dgamma, float* dbeta,
+                         void* workspace, size_t workspace_bytes, int64_t rows, int64_t cols,
+                         const tempo_ln_peer_t* peer, tempo_stream_t stream);
+/* Stage 2 alone on caller-provided fp64 partial rows [nparts][2*cols]
+ * (dgamma partials, then dbeta partials): local fixed-order sum + exchange. */
+int tempo_ln_param_reduce_peer(const double* partials, int64_t nparts, int64_t cols,
+                               const tempo_ln_peer_t* peer, float* dgamma, float* dbeta,
+                               tempo_stream_t stream);
+/* CUDA IPC plumbing for the inbox/flag buffers of other processes:
+ * handle = 64 opaque bytes (cudaIpcMemHandle_t). */
+int tempo_ipc_get_handle(const void* dev_ptr, void* handle64);
+int tempo_ipc_open_handle(const void* handle64, void** dev_ptr);
+int tempo_ipc_close(void* dev_ptr);
+
 /* ---------------------------------------------------------------------- */
 /* Output-only softmax + Sub-Layer Dropout Recomputation                   */
 /* (tempo_ops::softmax ops_tempo.cpp:158-166, dropout_recompute :168-194)   */

@@ -55,6 +55,14 @@ SIGNATURES = {
     "tempo_ln_ip_bwd_workspace_size": (_sz, [_i64, _i64]),
     "tempo_ln_ip_bwd": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _i64, _i64,
                                   _vp]),
+    "tempo_ln_peer_inbox_bytes": (_sz, [C.c_int32, _i64]),
+    "tempo_ln_peer_flag_bytes": (_sz, [C.c_int32, _i64]),
+    "tempo_ln_ip_bwd_peer": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _i64,
+                                       _i64, _vp, _vp]),
+    "tempo_ln_param_reduce_peer": (C.c_int, [_vp, _i64, _i64, _vp, _vp, _vp, _vp]),
+    "tempo_ipc_get_handle": (C.c_int, [_vp, _vp]),
+    "tempo_ipc_open_handle": (C.c_int, [_vp, C.POINTER(_vp)]),
+    "tempo_ipc_close": (C.c_int, [_vp]),
     "tempo_softmax_ip_fwd": (C.c_int, [_vp, _vp, _i64, _i64, _vp]),
     "tempo_softmax_ip_bwd": (C.c_int, [_vp, _vp, _vp, _i64, _i64, _vp]),
     "tempo_softmax_dropout_fwd": (C.c_int, [_vp, _dbl, C.c_int, _vp, _u64, _u64, _vp, _vp, _i64,

@@ -586,6 +586,87 @@ int tempo_ln_ip_bwd(const float* dy, const float* y, const float* rstd, const fl
                        "tempo_ln_ip_bwd");
 }
 
+// ---- multi-GPU: stage 2 fused with the cross-rank sum --------------------------------
+size_t tempo_ln_peer_inbox_bytes(int32_t world, int64_t cols) {
+    return world > 0 && cols > 0 ? tb::ln_peer_inbox_bytes(world, cols) : 0;
+}
+size_t tempo_ln_peer_flag_bytes(int32_t world, int64_t cols) {
+    return world > 0 && cols > 0 ? tb::ln_peer_flag_bytes(world, cols) : 0;
+}
+
+static int check_peer(const tempo_ln_peer_t* peer) {
+    if (!peer) return fail(TEMPO_ERR_PARAM, "peer group: null");
+    if (peer->world < 1 || peer->rank < 0 || peer->rank >= peer->world)
+        return fail(TEMPO_ERR_PARAM, "peer group: bad rank/world");
+    if (!peer->inbox || !peer->flags || !peer->status)
+        return fail(TEMPO_ERR_PARAM, "peer group: null buffer array");
+    if (peer->epoch == 0) return fail(TEMPO_ERR_PARAM, "peer group: epoch starts at 1");
+    return TEMPO_OK;
+}
+
+static tb::LnPeer to_peer(const tempo_ln_peer_t* p) {
+    return tb::LnPeer{p->rank, p->world, p->inbox, p->flags, p->epoch, p->status};
+}
+
+int tempo_ln_ip_bwd_peer(const float* dy, const float* y, const float* rstd, const float* gamma,
+                         const float* beta, float* dx, float* dgamma, float* dbeta,
+                         void* workspace, size_t workspace_bytes, int64_t rows, int64_t cols,
+                         const tempo_ln_peer_t* peer, tempo_stream_t stream) {
+    if (int rc = check_peer(peer)) return rc;
+    if (int rc = check_rows(rows, cols, "layernorm backward")) return rc;
+    if (cols > std::numeric_limits<int>::max() / 2)
+        return fail(TEMPO_ERR_DIMENSION, "layernorm: row too long");
+    if (cols > 0 && (!gamma || !beta || !dgamma || !dbeta))
+        return fail(TEMPO_ERR_PARAM, "layernorm: null parameter pointer");
+    if (rows > 0 && (!dy || !y || !rstd || !dx))
+        return fail(TEMPO_ERR_PARAM, "layernorm: null tensor pointer");
+    size_t need = tempo_ln_ip_bwd_workspace_size(rows, cols);
+    if (workspace_bytes < need || (need > 0 && !workspace))
+        return fail(TEMPO_ERR_PARAM, "layernorm backward workspace too small: need " +
+                                         std::to_string(need) + " bytes");
+    const tb::LnPeer pg = to_peer(peer);
+    return cuda_status(tb::launch_ln_bwd(dy, y, rstd, gamma, beta, dx, dgamma, dbeta, workspace,
+                                         rows, cols, S(stream), &pg),
+                       "tempo_ln_ip_bwd_peer");
+}
+
+int tempo_ln_param_reduce_peer(const double* partials, int64_t nparts, int64_t cols,
+                               const tempo_ln_peer_t* peer, float* dgamma, float* dbeta,
+                               tempo_stream_t stream) {
+    if (int rc = check_peer(peer)) return rc;
+    if (nparts < 0 || cols < 0 || cols > std::numeric_limits<int>::max() / 2 ||
+        nparts > std::numeric_limits<int>::max())
+        return fail(TEMPO_ERR_DIMENSION, "param reduce: bad sizes");
+    if (cols > 0 && (!dgamma || !dbeta || (nparts > 0 && !partials)))
+        return fail(TEMPO_ERR_PARAM, "param reduce: null pointer");
+    return cuda_status(tb::launch_ln_param_reduce_peer(partials, nparts, cols, to_peer(peer),
+                                                       dgamma, dbeta, S(stream)),
+                       "tempo_ln_param_reduce_peer");
+}
+
+int tempo_ipc_get_handle(const void* dev_ptr, void* handle64) {
+    if (!dev_ptr || !handle64) return fail(TEMPO_ERR_PARAM, "ipc: null pointer");
+    cudaIpcMemHandle_t h;
+    cudaError_t e = cudaIpcGetMemHandle(&h, const_cast<void*>(dev_ptr));
+    if (e != cudaSuccess) return cuda_status(e, "tempo_ipc_get_handle");
+    static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t is 64 bytes");
+    std::memcpy(handle64, &h, sizeof(h));
+    return TEMPO_OK;
+}
+
+int tempo_ipc_open_handle(const void* handle64, void** dev_ptr) {
+    if (!handle64 || !dev_ptr) return fail(TEMPO_ERR_PARAM, "ipc: null pointer");
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle64, sizeof(h));
+    return cuda_status(cudaIpcOpenMemHandle(dev_ptr, h, cudaIpcMemLazyEnablePeerAccess),
+                       "tempo_ipc_open_handle");
+}
+
+int tempo_ipc_close(void* dev_ptr) {
+    if (!dev_ptr) return TEMPO_OK;
+    return cuda_status(cudaIpcCloseMemHandle(dev_ptr), "tempo_ipc_close");
+}
+
 // ---- softmax / attention dropout -------------------------------------------------
 int tempo_softmax_ip_fwd(const float* z, float* P, int64_t rows, int64_t cols,
                          tempo_stream_t stream) {

@@ -562,6 +562,93 @@ __global__ void __launch_bounds__(1024) ln_param_reduce_kernel(const double* __r
     }
 }
 
+// Stage 2 fused with the cross-rank sum (the path's one collective, SURVEY
+// 8e) over peer memory, in place of ln_param_reduce_kernel + an all-reduce.
+// CTA cb owns outputs j in [32 cb, 32 cb + 32) of the 2*cols (dgamma | dbeta):
+//  1. its local fixed-order sum over the nparts stage-1 partial rows (fp64);
+//  2. the 32 values are stored into slot [par][rank] of EVERY rank's inbox
+//     (P2P stores over NVLink; the own inbox included);
+//  3. one thread: system-scope fence, then flag[par][rank][cb] = epoch on
+//     every rank (st.release.sys);
+//  4. one thread waits for flag[par][s][cb] == epoch for all s on its own
+//     rank (ld.acquire.sys, bounded spin: a missing peer sets *status and
+//     the kernel finishes instead of hanging);
+//  5. the final value is the sum over s = 0 .. world-1 IN RANK ORDER of the
+//     inbox slots: every rank computes identical bits, independent of the
+//     arrival order (bitwise reproducible, unlike a generic all-reduce).
+// No grid-wide barrier: each column block synchronises only with the same
+// block on the other ranks.  par = epoch & 1 double-buffers the inbox: a
+// rank can only reach epoch e+2 (parity reuse) after every peer has set its
+// e+1 flags, i.e. after every peer finished reading its epoch-e slots.
+constexpr int kPeerCols = 32;
+constexpr int kPeerRowGroups = 8;
+
+__device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+constexpr uint64_t kPeerTimeoutNs = 2000000000ull;  // 2 s
+
+__global__ void __launch_bounds__(kPeerCols * kPeerRowGroups) ln_param_reduce_peer_kernel(
+    const double* __restrict__ ws, int nparts, int cols, int rank, int world,
+    double* const* __restrict__ inbox, uint32_t* const* __restrict__ flags, uint32_t epoch,
+    float* __restrict__ dgamma, float* __restrict__ dbeta, int32_t* __restrict__ status) {
+    grid_dep_wait();
+    __shared__ double part[kPeerRowGroups][kPeerCols + 1];
+    const int tx = threadIdx.x % kPeerCols, ty = threadIdx.x / kPeerCols;
+    const int64_t total = 2 * (int64_t)cols;
+    const int cb = blockIdx.x, ncb = gridDim.x;
+    const int64_t j = (int64_t)cb * kPeerCols + tx;
+    const int par = (int)(epoch & 1u);
+    const int64_t tstride = (int64_t)ncb * kPeerCols;  // inbox slot stride (padded)
+    double acc = 0.0;
+    if (j < total)
+        for (int c = ty; c < nparts; c += kPeerRowGroups) acc += ws[(size_t)c * total + j];
+    part[ty][tx] = acc;
+    __syncthreads();
+    if (ty == 0) {
+        double v = 0.0;
+#pragma unroll
+        for (int k = 0; k < kPeerRowGroups; ++k) v += part[k][tx];
+        // slot [par][rank] of every rank's inbox ([2][world][tstride] doubles)
+        for (int p = 0; p < world; ++p) inbox[p][((size_t)par * world + rank) * tstride + j] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence_system();
+        for (int p = 0; p < world; ++p)
+            st_release_sys(flags[p] + ((size_t)par * world + rank) * ncb + cb, epoch);
+        const uint32_t* mine = flags[rank] + (size_t)par * world * ncb + cb;
+        const uint64_t t0 = globaltimer_ns();
+        for (int s = 0; s < world; ++s) {
+            while (ld_acquire_sys(mine + (size_t)s * ncb) != epoch) {
+                if (globaltimer_ns() - t0 > kPeerTimeoutNs) {  // a peer never arrived
+                    atomicExch(status, TEMPO_ERR_STATE);
+                    break;
+                }
+                __nanosleep(128);
+            }
+        }
+    }
+    __syncthreads();
+    if (ty == 0 && j < cols * 2) {
+        const double* my = inbox[rank] + (size_t)par * world * tstride;
+        double v = 0.0;
+        for (int s = 0; s < world; ++s) v += __ldcg(my + (size_t)s * tstride + j);
+        if (j < cols) dgamma[j] = (float)v; else dbeta[j - cols] = (float)v;
+    }
+}
+
 inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
 bool use_vec(int64_t cols, const void* a, const void* b, const void* c, const void* d,
@@ -640,6 +727,25 @@ cudaError_t launch_ln_fwd(const float* x, const float* gamma, const float* beta,
     return cudaGetLastError();
 }
 
+size_t ln_peer_inbox_bytes(int world, int64_t cols) {
+    const int64_t ncb = (2 * cols + kPeerCols - 1) / kPeerCols;
+    return (size_t)2 * world * (size_t)(ncb * kPeerCols) * sizeof(double);
+}
+size_t ln_peer_flag_bytes(int world, int64_t cols) {
+    const int64_t ncb = (2 * cols + kPeerCols - 1) / kPeerCols;
+    return (size_t)2 * world * (size_t)ncb * sizeof(uint32_t);
+}
+
+cudaError_t launch_ln_param_reduce_peer(const double* partials, int64_t nparts, int64_t cols,
+                                        const LnPeer& peer, float* dgamma, float* dbeta,
+                                        cudaStream_t st) {
+    if (cols == 0) return cudaSuccess;
+    const int ncb = (int)((2 * cols + kPeerCols - 1) / kPeerCols);
+    return launch_pdl((const void*)ln_param_reduce_peer_kernel, ncb, kPeerCols * kPeerRowGroups, 0,
+                      st, partials, (int)nparts, (int)cols, peer.rank, peer.world, peer.inbox,
+                      peer.flags, peer.epoch, dgamma, dbeta, peer.status);
+}
+
 size_t ln_bwd_workspace(int64_t rows, int64_t cols) {
     if (rows == 0 || cols == 0) return 0;
     // The vector/generic choice also depends on pointer alignment; size for
@@ -652,9 +758,10 @@ size_t ln_bwd_workspace(int64_t rows, int64_t cols) {
 
 cudaError_t launch_ln_bwd(const float* dy, const float* y, const float* rstd, const float* gamma,
                           const float* beta, float* dx, float* dgamma, float* dbeta, void* ws,
-                          int64_t rows, int64_t cols, cudaStream_t st) {
+                          int64_t rows, int64_t cols, cudaStream_t st, const LnPeer* peer) {
     if (cols == 0) return cudaSuccess;
     if (rows == 0) {
+        if (peer) return launch_ln_param_reduce_peer(nullptr, 0, cols, *peer, dgamma, dbeta, st);
         cudaMemsetAsync(dgamma, 0, cols * sizeof(float), st);
         cudaMemsetAsync(dbeta, 0, cols * sizeof(float), st);
         return cudaGetLastError();
@@ -673,6 +780,7 @@ cudaError_t launch_ln_bwd(const float* dy, const float* y, const float* rstd, co
         launch(ln_bwd_generic_kernel, grid, 256, smem, st)(dy, y, rstd, gamma, beta, dx, w, rows,
                                                        (int)cols);
     }
+    if (peer) return launch_ln_param_reduce_peer(w, grid, cols, *peer, dgamma, dbeta, st);
     const int rgrid = (int)((2 * cols + 31) / 32);
     return launch_pdl((const void*)ln_param_reduce_kernel, rgrid, 1024, 0, st,
                       (const double*)w, grid, (int)cols, dgamma, dbeta);

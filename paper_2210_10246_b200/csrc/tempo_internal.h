@@ -57,9 +57,24 @@ cudaError_t launch_ln_fwd(const float* x, const float* gamma, const float* beta,
                           float* y, float* rstd, int64_t rows, int64_t cols, int32_t* dev_status,
                           cudaStream_t st);
 size_t ln_bwd_workspace(int64_t rows, int64_t cols);
+// The cross-rank exchange fused into stage 2 (layernorm_kernels.cu): every
+// rank's inbox / flag buffers, mapped into this process (P2P / IPC).
+struct LnPeer {
+    int rank, world;
+    double* const* inbox;     // device array [world]: rank p's inbox
+    uint32_t* const* flags;   // device array [world]: rank p's flags
+    uint32_t epoch;           // 1, 2, 3, ... per exchange
+    int32_t* status;          // device int: TEMPO_ERR_STATE if a peer never arrived
+};
+size_t ln_peer_inbox_bytes(int world, int64_t cols);
+size_t ln_peer_flag_bytes(int world, int64_t cols);
+cudaError_t launch_ln_param_reduce_peer(const double* partials, int64_t nparts, int64_t cols,
+                                        const LnPeer& peer, float* dgamma, float* dbeta,
+                                        cudaStream_t st);
 cudaError_t launch_ln_bwd(const float* dy, const float* y, const float* rstd, const float* gamma,
                           const float* beta, float* dx, float* dgamma, float* dbeta, void* ws,
-                          int64_t rows, int64_t cols, cudaStream_t st);
+                          int64_t rows, int64_t cols, cudaStream_t st,
+                          const LnPeer* peer = nullptr);
 
 cudaError_t launch_softmax_fwd(const float* z, float* P, int64_t rows, int64_t cols,
                                cudaStream_t st);

@@ -202,6 +202,119 @@ def layernorm_ip_bwd(dy: torch.Tensor, y: torch.Tensor, rstd: torch.Tensor,
     return dx, dgamma, dbeta
 
 
+class _PeerStruct(C.Structure):
+    """tempo_ln_peer_t (include/tempo_b200.h)."""
+    _fields_ = [("rank", C.c_int32), ("world", C.c_int32),
+                ("inbox", C.c_void_p), ("flags", C.c_void_p),
+                ("epoch", C.c_uint32), ("status", C.c_void_p)]
+
+
+class LnPeerRank:
+    """One rank's view of the fused dgamma/dbeta exchange: its own inbox and
+    flag buffers plus the device arrays of every rank's buffers as mapped in
+    this process.  Build with ``LnPeerRank.local_group`` (all ranks in one
+    process on one device: tests) or ``LnPeerRank.ipc`` (one process per GPU:
+    buffers shared by CUDA IPC handles over torch.distributed)."""
+
+    def __init__(self, rank, world, cols, device):
+        self.rank, self.world, self.cols, self.device = rank, world, cols, device
+        L = lib()
+        ib, fb = L.tempo_ln_peer_inbox_bytes(world, cols), L.tempo_ln_peer_flag_bytes(world, cols)
+        self.inbox = torch.zeros(ib // 8, dtype=torch.float64, device=device)
+        self.flags = torch.zeros(fb // 4, dtype=torch.int32, device=device)
+        self.status = torch.zeros(1, dtype=torch.int32, device=device)
+        self.epoch = 0
+        self._ptrs = None
+        self._mapped = []
+
+    def _set_peers(self, inbox_ptrs, flag_ptrs):
+        self._ptrs = (torch.tensor(inbox_ptrs, dtype=torch.int64, device=self.device),
+                      torch.tensor(flag_ptrs, dtype=torch.int64, device=self.device))
+
+    @classmethod
+    def local_group(cls, world, cols, device):
+        ranks = [cls(r, world, cols, device) for r in range(world)]
+        ib = [r.inbox.data_ptr() for r in ranks]
+        fl = [r.flags.data_ptr() for r in ranks]
+        for r in ranks:
+            r._set_peers(ib, fl)
+        return ranks
+
+    @classmethod
+    def ipc(cls, cols, device, group=None):
+        """Collective over torch.distributed: every rank maps every other
+        rank's buffers through CUDA IPC handles."""
+        import torch.distributed as dist
+        me = cls(dist.get_rank(group), dist.get_world_size(group), cols, device)
+        L = lib()
+        hs = []
+        for t in (me.inbox, me.flags):
+            h = C.create_string_buffer(64)
+            check(L.tempo_ipc_get_handle(C.c_void_p(t.data_ptr()), h))
+            hs.append(h.raw)
+        allh = [None] * me.world
+        dist.all_gather_object(allh, hs, group=group)
+        ib, fl = [], []
+        for r, (hi, hf) in enumerate(allh):
+            if r == me.rank:
+                ib.append(me.inbox.data_ptr())
+                fl.append(me.flags.data_ptr())
+                continue
+            ptrs = []
+            for h in (hi, hf):
+                p = C.c_void_p()
+                check(L.tempo_ipc_open_handle(C.create_string_buffer(h, 64), C.byref(p)))
+                me._mapped.append(p.value)
+                ptrs.append(p.value)
+            ib.append(ptrs[0])
+            fl.append(ptrs[1])
+        me._set_peers(ib, fl)
+        return me
+
+    def next_struct(self):
+        self.epoch += 1
+        return _PeerStruct(self.rank, self.world, self._ptrs[0].data_ptr(),
+                           self._ptrs[1].data_ptr(), self.epoch, self.status.data_ptr())
+
+    def check_status(self):
+        if int(self.status.item()) != 0:
+            raise RuntimeError("peer exchange: a rank never arrived (TEMPO_ERR_STATE)")
+
+    def close(self):
+        L = lib()
+        for p in self._mapped:
+            L.tempo_ipc_close(C.c_void_p(p))
+        self._mapped = []
+
+
+def ln_param_reduce_peer(partials: torch.Tensor, cols: int, peer: "LnPeerRank",
+                         dgamma: torch.Tensor = None, dbeta: torch.Tensor = None):
+    """Stage 2 on fp64 partial rows [nparts][2*cols] + the cross-rank sum."""
+    dev = partials.device
+    dgamma = torch.empty(cols, dtype=torch.float32, device=dev) if dgamma is None else dgamma
+    dbeta = torch.empty(cols, dtype=torch.float32, device=dev) if dbeta is None else dbeta
+    st = peer.next_struct()
+    check(lib().tempo_ln_param_reduce_peer(_ptr(partials), partials.shape[0], cols,
+                                           C.byref(st), _ptr(dgamma), _ptr(dbeta), _stream()))
+    return dgamma, dbeta
+
+
+def layernorm_ip_bwd_peer(dy, y, rstd, gamma, beta, peer: "LnPeerRank", dx=None, dgamma=None,
+                          dbeta=None, workspace=None):
+    """layernorm_ip_bwd with dgamma/dbeta summed over every rank of ``peer``."""
+    dy, y = _f32(dy, "dy"), _f32(y, "y")
+    rows, cols = _rows_cols(y)
+    dx = torch.empty_like(dy) if dx is None else dx
+    dgamma = torch.empty(cols, dtype=torch.float32, device=y.device) if dgamma is None else dgamma
+    dbeta = torch.empty(cols, dtype=torch.float32, device=y.device) if dbeta is None else dbeta
+    ws = ln_workspace(rows, cols, y.device) if workspace is None else workspace
+    st = peer.next_struct()
+    check(lib().tempo_ln_ip_bwd_peer(_ptr(dy), _ptr(y), _ptr(rstd), _ptr(gamma), _ptr(beta),
+                                     _ptr(dx), _ptr(dgamma), _ptr(dbeta), _ptr(ws), ws.numel(),
+                                     rows, cols, C.byref(st), _stream()))
+    return dx, dgamma, dbeta
+
+
 # --------------------------------------------------------------------------
 # Output-only softmax + dropout recomputation (ops_tempo.cpp:158-194)
 # --------------------------------------------------------------------------

@@ -1,0 +1,170 @@
+"""The path's one collective -- the cross-rank sum of the LayerNorm
+dgamma/dbeta -- fused into the backward's stage 2 over peer
+memory (layernorm_kernels.cu: ln_param_reduce_peer_kernel).
+
+One B200 here, so the ranks are simulated inside one process on one device:
+each rank has its own inbox/flag buffers and its kernels run on its own
+stream, concurrently, exactly as ranks on different GPUs would (the
+kernels see plain device pointers either way; on a multi-GPU node they are
+CUDA IPC mappings, ops.LnPeerRank.ipc).  Checked: the result is bit for bit
+the fixed-order sum (rank 0, 1, ... of each rank's fixed-order partial sum),
+identical on every rank, across consecutive epochs (inbox parity reuse), and
+a sharded LayerNorm backward reproduces the unsharded one."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _local_sums(parts):
+    """The kernel's local order: row group ty sums rows ty, ty+8, ... ; the 8
+    group sums are then added in order (ln_param_reduce_peer_kernel)."""
+    nparts, total = parts.shape
+    g = np.zeros((8, total))
+    for ty in range(8):
+        acc = np.zeros(total)
+        for c in range(ty, nparts, 8):
+            acc = acc + parts[c]
+        g[ty] = acc
+    v = np.zeros(total)
+    for k in range(8):
+        v = v + g[k]
+    return v
+
+
+def _run_group(tops, ranks, parts, cols):
+    import torch
+    streams = [torch.cuda.Stream() for _ in ranks]
+    outs = []
+    for r, st in zip(ranks, streams):
+        with torch.cuda.stream(st):
+            outs.append(tops.ln_param_reduce_peer(parts[r.rank], cols, r))
+    torch.cuda.synchronize()
+    for r in ranks:
+        r.check_status()
+    return [(g.cpu().numpy(), b.cpu().numpy()) for g, b in outs]
+
+
+@pytest.mark.parametrize("world,cols,nparts", [(1, 1024, 296), (2, 1024, 296), (3, 768, 37),
+                                               (4, 1024, 5), (2, 37, 3), (8, 256, 64)])
+def test_peer_reduce_is_the_fixed_order_sum(tops, cuda, world, cols, nparts):
+    import torch
+    ranks = tops.LnPeerRank.local_group(world, cols, cuda)
+    g = np.random.default_rng(world * 1000 + cols)
+    for epoch in range(4):  # consecutive exchanges reuse the two inbox parities
+        parts = [g.standard_normal((nparts, 2 * cols)) * (1 + epoch) for _ in range(world)]
+        dev = [torch.from_numpy(p).to(cuda) for p in parts]
+        res = _run_group(tops, ranks, dev, cols)
+        want = np.zeros(2 * cols)
+        for s in range(world):
+            want = want + _local_sums(parts[s])
+        want = want.astype(np.float32)
+        for dg, db in res:
+            assert np.array_equal(dg, want[:cols]), epoch
+            assert np.array_equal(db, want[cols:]), epoch
+
+
+def test_peer_reduce_missing_rank_times_out(tops, cuda):
+    """A rank that never arrives: the kernel gives up after a bounded wait,
+    reports TEMPO_ERR_STATE and returns (no hung GPU)."""
+    import torch
+    ranks = tops.LnPeerRank.local_group(2, 32, cuda)
+    parts = torch.zeros((1, 64), dtype=torch.float64, device=cuda)
+    tops.ln_param_reduce_peer(parts, 32, ranks[0])  # rank 1 never runs
+    torch.cuda.synchronize()
+    with pytest.raises(RuntimeError):
+        ranks[0].check_status()
+
+
+def test_sharded_layernorm_backward(tops, cuda):
+    """Row shards + the fused exchange == the unsharded backward: dx bit for
+    bit, dgamma/dbeta identical on every rank and equal to the single-GPU
+    values up to the summation order (fp64 partials, one float rounding)."""
+    import torch
+    rows, cols, world = 4096, 1024, 2
+    g = np.random.default_rng(7)
+    x = torch.from_numpy(g.standard_normal((rows, cols)).astype(np.float32)).to(cuda)
+    gam = torch.from_numpy((1 + 0.2 * g.standard_normal(cols)).astype(np.float32)).to(cuda)
+    bet = torch.from_numpy((0.1 * g.standard_normal(cols)).astype(np.float32)).to(cuda)
+    dy = torch.from_numpy(g.standard_normal((rows, cols)).astype(np.float32)).to(cuda)
+    y, rstd = tops.layernorm_ip_fwd(x, gam, bet)
+    dx1, dg1, db1 = tops.layernorm_ip_bwd(dy, y, rstd, gam, bet)
+    torch.cuda.synchronize()
+    ranks = tops.LnPeerRank.local_group(world, cols, cuda)
+    from paper_2210_10246_b200.dist import shard_rows
+    streams = [torch.cuda.Stream() for _ in range(world)]
+    outs = []
+    for r, st in zip(ranks, streams):
+        b, e = shard_rows(rows, r.rank, world)
+        with torch.cuda.stream(st):
+            outs.append((b, e) + tops.layernorm_ip_bwd_peer(dy[b:e], y[b:e], rstd[b:e], gam, bet, r))
+    torch.cuda.synchronize()
+    for r in ranks:
+        r.check_status()
+    for b, e, dx, dg, db in outs:
+        assert torch.equal(dx, dx1[b:e])
+        assert torch.equal(dg, outs[0][3]) and torch.equal(db, outs[0][4])
+        assert torch.allclose(dg, dg1, rtol=1e-6, atol=1e-6)
+        assert torch.allclose(db, db1, rtol=1e-6, atol=1e-6)
+
+
+def _ipc_worker(rank, world, port, cols, q):
+    import ctypes
+    import os
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2210_10246_b200 import ops
+        from paper_2210_10246_b200._capi import lib
+        dev = torch.device("cuda:0")
+        peer = ops.LnPeerRank.ipc(cols, dev)
+        peer.inbox.fill_(float(rank + 1))          # a pattern in this rank's inbox
+        torch.cuda.synchronize()
+        dist.barrier()
+        # read every rank's inbox through the pointer this process mapped
+        # (the device pointer array the exchange kernel uses), with a plain
+        # device-to-device op of the C-ABI (out = a * 1.0 on float words)
+        ptrs = peer._ptrs[0].cpu().tolist()
+        seen = []
+        for r in range(world):
+            out = torch.empty(2 * peer.inbox.numel(), dtype=torch.float32, device=dev)
+            rc = lib().tempo_tensor_scale(ctypes.c_void_p(ptrs[r]), 1.0,
+                                          ctypes.c_void_p(out.data_ptr()), out.numel(), None)
+            torch.cuda.synchronize()
+            seen.append((rc, out.view(torch.float64).cpu().numpy().copy()))
+        dist.barrier()
+        peer.close()
+        q.put((rank, "ok", seen))
+    except Exception as ex:  # noqa: BLE001
+        q.put((rank, repr(ex), None))
+    dist.destroy_process_group()
+
+
+def test_ipc_two_processes(cuda):
+    """The multi-process plumbing (ops.LnPeerRank.ipc: CUDA IPC handles over
+    torch.distributed): two processes on the one GPU of this box map each
+    other's inbox and read the other's pattern through the mapped pointer.
+    (The exchange itself needs the ranks' kernels running concurrently; two
+    processes on one GPU only time-slice, so it is checked in-process above.)"""
+    import socket
+    import torch.multiprocessing as mp
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    world, cols = 2, 64
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_ipc_worker, args=(r, world, port, cols, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = sorted([q.get(timeout=300) for _ in range(world)], key=lambda t: t[0])
+    for p in procs:
+        p.join(timeout=60)
+    for rank, status, seen in out:
+        assert status == "ok", (rank, status)
+        for r, (rc, vals) in enumerate(seen):
+            assert rc == 0 and np.all(vals == float(r + 1)), (rank, r)
