@@ -64,10 +64,11 @@ def op_bytes(batch=B):
 def setup_peer(chain, dist, rank, world, dev, backend):
     """Map every rank's LN exchange buffers (CUDA IPC) and self-check one
     exchange against the known answer on all ranks; None -> fall back to the
-    all-reduce.  Off for the gloo functional mode (ranks sharing one GPU) and
-    with TEMPO_PEER=0."""
+    all-reduce.  Off for the gloo functional mode (ranks sharing one GPU)
+    unless TEMPO_PEER=force, and with TEMPO_PEER=0."""
     import torch
-    if backend != "nccl" or os.environ.get("TEMPO_PEER", "1") != "1":
+    mode = os.environ.get("TEMPO_PEER", "1")  # "0": off; "force": also with gloo (tests)
+    if mode == "0" or (backend != "nccl" and mode != "force"):
         return None
     peer, ok = None, 1
     try:

@@ -157,8 +157,14 @@ int tempo_ln_ip_bwd_peer(const float* dy, const float* y, const float* rstd, con
 int tempo_ln_param_reduce_peer(const double* partials, int64_t nparts, int64_t cols,
                                const tempo_ln_peer_t* peer, float* dgamma, float* dbeta,
                                tempo_stream_t stream);
+/* Exchange buffers: a dedicated, zero-filled cudaMalloc allocation (an IPC
+ * handle always maps the START of an allocation, so sub-allocations of a
+ * caching allocator cannot be shared this way). */
+int tempo_peer_alloc(size_t bytes, void** dev_ptr);
+int tempo_peer_free(void* dev_ptr);
 /* CUDA IPC plumbing for the inbox/flag buffers of other processes:
- * handle = 64 opaque bytes (cudaIpcMemHandle_t). */
+ * handle = 64 opaque bytes (cudaIpcMemHandle_t) of a tempo_peer_alloc
+ * pointer. */
 int tempo_ipc_get_handle(const void* dev_ptr, void* handle64);
 int tempo_ipc_open_handle(const void* handle64, void** dev_ptr);
 int tempo_ipc_close(void* dev_ptr);

@@ -60,6 +60,8 @@ SIGNATURES = {
     "tempo_ln_ip_bwd_peer": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _i64,
                                        _i64, _vp, _vp]),
     "tempo_ln_param_reduce_peer": (C.c_int, [_vp, _i64, _i64, _vp, _vp, _vp, _vp]),
+    "tempo_peer_alloc": (C.c_int, [_sz, C.POINTER(_vp)]),
+    "tempo_peer_free": (C.c_int, [_vp]),
     "tempo_ipc_get_handle": (C.c_int, [_vp, _vp]),
     "tempo_ipc_open_handle": (C.c_int, [_vp, C.POINTER(_vp)]),
     "tempo_ipc_close": (C.c_int, [_vp]),

@@ -644,6 +644,19 @@ int tempo_ln_param_reduce_peer(const double* partials, int64_t nparts, int64_t c
                        "tempo_ln_param_reduce_peer");
 }
 
+int tempo_peer_alloc(size_t bytes, void** dev_ptr) {
+    if (!dev_ptr) return fail(TEMPO_ERR_PARAM, "peer alloc: null out pointer");
+    *dev_ptr = nullptr;
+    cudaError_t e = cudaMalloc(dev_ptr, bytes > 0 ? bytes : 1);
+    if (e == cudaSuccess) e = cudaMemset(*dev_ptr, 0, bytes > 0 ? bytes : 1);
+    return cuda_status(e, "tempo_peer_alloc");
+}
+
+int tempo_peer_free(void* dev_ptr) {
+    if (!dev_ptr) return TEMPO_OK;
+    return cuda_status(cudaFree(dev_ptr), "tempo_peer_free");
+}
+
 int tempo_ipc_get_handle(const void* dev_ptr, void* handle64) {
     if (!dev_ptr || !handle64) return fail(TEMPO_ERR_PARAM, "ipc: null pointer");
     cudaIpcMemHandle_t h;

@@ -219,13 +219,33 @@ class LnPeerRank:
     def __init__(self, rank, world, cols, device):
         self.rank, self.world, self.cols, self.device = rank, world, cols, device
         L = lib()
-        ib, fb = L.tempo_ln_peer_inbox_bytes(world, cols), L.tempo_ln_peer_flag_bytes(world, cols)
-        self.inbox = torch.zeros(ib // 8, dtype=torch.float64, device=device)
-        self.flags = torch.zeros(fb // 4, dtype=torch.int32, device=device)
+        self.inbox_bytes = int(L.tempo_ln_peer_inbox_bytes(world, cols))
+        self.flag_bytes = int(L.tempo_ln_peer_flag_bytes(world, cols))
+        # dedicated zero-filled allocations (IPC maps whole allocations), on
+        # `device`; raw device pointers
+        self._owned = []
+        with torch.cuda.device(device):
+            self.inbox = self._alloc(self.inbox_bytes)
+            self.flags = self._alloc(self.flag_bytes)
         self.status = torch.zeros(1, dtype=torch.int32, device=device)
         self.epoch = 0
         self._ptrs = None
         self._mapped = []
+
+    def _alloc(self, nbytes):
+        p = C.c_void_p()
+        check(lib().tempo_peer_alloc(nbytes, C.byref(p)))
+        self._owned.append(p.value)
+        return p.value
+
+    def __del__(self):
+        try:
+            self.close()
+            for p in self._owned:
+                lib().tempo_peer_free(C.c_void_p(p))
+            self._owned = []
+        except Exception:  # noqa: BLE001  (interpreter shutdown)
+            pass
 
     def _set_peers(self, inbox_ptrs, flag_ptrs):
         self._ptrs = (torch.tensor(inbox_ptrs, dtype=torch.int64, device=self.device),
@@ -234,8 +254,8 @@ class LnPeerRank:
     @classmethod
     def local_group(cls, world, cols, device):
         ranks = [cls(r, world, cols, device) for r in range(world)]
-        ib = [r.inbox.data_ptr() for r in ranks]
-        fl = [r.flags.data_ptr() for r in ranks]
+        ib = [r.inbox for r in ranks]
+        fl = [r.flags for r in ranks]
         for r in ranks:
             r._set_peers(ib, fl)
         return ranks
@@ -248,17 +268,17 @@ class LnPeerRank:
         me = cls(dist.get_rank(group), dist.get_world_size(group), cols, device)
         L = lib()
         hs = []
-        for t in (me.inbox, me.flags):
+        for ptr in (me.inbox, me.flags):
             h = C.create_string_buffer(64)
-            check(L.tempo_ipc_get_handle(C.c_void_p(t.data_ptr()), h))
+            check(L.tempo_ipc_get_handle(C.c_void_p(ptr), h))
             hs.append(h.raw)
         allh = [None] * me.world
         dist.all_gather_object(allh, hs, group=group)
         ib, fl = [], []
         for r, (hi, hf) in enumerate(allh):
             if r == me.rank:
-                ib.append(me.inbox.data_ptr())
-                fl.append(me.flags.data_ptr())
+                ib.append(me.inbox)
+                fl.append(me.flags)
                 continue
             ptrs = []
             for h in (hi, hf):

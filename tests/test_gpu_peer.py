@@ -121,7 +121,10 @@ def _ipc_worker(rank, world, port, cols, q):
         from paper_2210_10246_b200._capi import lib
         dev = torch.device("cuda:0")
         peer = ops.LnPeerRank.ipc(cols, dev)
-        peer.inbox.fill_(float(rank + 1))          # a pattern in this rank's inbox
+        n = peer.inbox_bytes // 4                  # a pattern in this rank's inbox
+        src = torch.full((n // 2,), float(rank + 1), dtype=torch.float64, device=dev)
+        assert lib().tempo_tensor_scale(ctypes.c_void_p(src.data_ptr()), 1.0,
+                                        ctypes.c_void_p(peer.inbox), n, None) == 0
         torch.cuda.synchronize()
         dist.barrier()
         # read every rank's inbox through the pointer this process mapped
@@ -130,25 +133,35 @@ def _ipc_worker(rank, world, port, cols, q):
         ptrs = peer._ptrs[0].cpu().tolist()
         seen = []
         for r in range(world):
-            out = torch.empty(2 * peer.inbox.numel(), dtype=torch.float32, device=dev)
+            out = torch.empty(peer.inbox_bytes // 4, dtype=torch.float32, device=dev)
             rc = lib().tempo_tensor_scale(ctypes.c_void_p(ptrs[r]), 1.0,
                                           ctypes.c_void_p(out.data_ptr()), out.numel(), None)
             torch.cuda.synchronize()
             seen.append((rc, out.view(torch.float64).cpu().numpy().copy()))
+        # the exchange itself across the two processes (time-sliced on one GPU)
+        sums = []
+        for epoch in range(3):
+            parts = torch.full((5, 2 * cols), float((rank + 1) * (epoch + 1)), dtype=torch.float64,
+                               device=dev)
+            dist.barrier()
+            dg, db = ops.ln_param_reduce_peer(parts, cols, peer)
+            torch.cuda.synchronize()
+            peer.check_status()
+            sums.append((dg.cpu().numpy().copy(), db.cpu().numpy().copy()))
         dist.barrier()
         peer.close()
-        q.put((rank, "ok", seen))
+        q.put((rank, "ok", (seen, sums)))
     except Exception as ex:  # noqa: BLE001
         q.put((rank, repr(ex), None))
     dist.destroy_process_group()
 
 
 def test_ipc_two_processes(cuda):
-    """The multi-process plumbing (ops.LnPeerRank.ipc: CUDA IPC handles over
-    torch.distributed): two processes on the one GPU of this box map each
-    other's inbox and read the other's pattern through the mapped pointer.
-    (The exchange itself needs the ranks' kernels running concurrently; two
-    processes on one GPU only time-slice, so it is checked in-process above.)"""
+    """The multi-process path (ops.LnPeerRank.ipc: CUDA IPC handles over
+    torch.distributed) with two processes on the one GPU of this box: each
+    reads the other's inbox pattern through its mapped pointer, then three
+    exchanges run across the processes (their kernels time-slice on one GPU,
+    so the waits are longer than over NVLink, but the protocol is the same)."""
     import socket
     import torch.multiprocessing as mp
     s = socket.socket()
@@ -164,7 +177,11 @@ def test_ipc_two_processes(cuda):
     out = sorted([q.get(timeout=300) for _ in range(world)], key=lambda t: t[0])
     for p in procs:
         p.join(timeout=60)
-    for rank, status, seen in out:
+    for rank, status, res in out:
         assert status == "ok", (rank, status)
+        seen, sums = res
         for r, (rc, vals) in enumerate(seen):
             assert rc == 0 and np.all(vals == float(r + 1)), (rank, r)
+        for epoch, (dg, db) in enumerate(sums):
+            want = 5.0 * (epoch + 1) * (1 + 2)
+            assert np.all(dg == want) and np.all(db == want), (rank, epoch)
