@@ -189,8 +189,24 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 __device__ __forceinline__ void grid_dep_wait() {
     asm volatile("griddepcontrol.wait;" ::: "memory");
 }
+#ifndef TM_PDL_TRIGGER
+#define TM_PDL_TRIGGER 0  // 1: early trigger (measured -7 %: dependents steal slots from multi-wave grids)
+#endif
 __device__ __forceinline__ void grid_dep_launch() {
+#if TM_PDL_TRIGGER
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
+}
+// Early trigger for single-wave persistent grids: all their CTAs are already
+// resident, so the dependent's CTAs can only take leftover slots (no slot
+// stealing) and start the moment this grid's memory is flushed.
+#ifndef TM_PDL_TRIGGER_PERSISTENT
+#define TM_PDL_TRIGGER_PERSISTENT 1
+#endif
+__device__ __forceinline__ void grid_dep_launch_persistent() {
+#if TM_PDL_TRIGGER_PERSISTENT
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
 }
 
 // ---- warp reductions -----------------------------------------------------

@@ -129,7 +129,7 @@ __global__ void __launch_bounds__(kBlock) dropout_fwd8_kernel(
     const float* __restrict__ x, uint32_t* __restrict__ mask, double scale, uint64_t thresh,
     uint64_t seed, uint64_t offset, float* __restrict__ y, int64_t n) {
     grid_dep_wait();  // PDL: predecessor complete and visible
-    grid_dep_launch();
+    if (PHILOX) grid_dep_launch_persistent();  // Philox: one persistent wave
     const int lane = threadIdx.x & 31;
     const int64_t warp = ((int64_t)blockIdx.x * kBlock + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * kBlock) >> 5;

@@ -131,7 +131,7 @@ __global__ void TM_GELU_FWD_BOUNDS gelu_fwd8_kernel(const float* __restrict__ x,
                                                     uint32_t* __restrict__ mask, int64_t n,
                                                     float xstar_gt, float xs_lo) {
     grid_dep_wait();  // PDL: predecessor complete and visible
-    grid_dep_launch();
+    grid_dep_launch_persistent();  // one persistent wave (TM_GELU_WAVES)
     __shared__ __align__(16) float stage_all[kBlock / 32][U * 256];
     const int lane = threadIdx.x & 31;
     float* stage = stage_all[threadIdx.x >> 5];
@@ -449,7 +449,7 @@ __global__ void __launch_bounds__(kBlock) gelu_bwd_fast_kernel(
     const float* __restrict__ dy, const float* __restrict__ y, const uint32_t* __restrict__ mask,
     float* __restrict__ dx, int64_t n, const __grid_constant__ GeluDevTable t, int vec) {
     grid_dep_wait();  // PDL: predecessor complete and visible
-    grid_dep_launch();
+    grid_dep_launch_persistent();  // one persistent wave (TM_GELU_WAVES)
     __shared__ FastTable<NC4> ft;
     const int nseg = t.nseg[0] + t.nseg[1];
     for (int i = threadIdx.x; i < nseg * FastTable<NC4>::kStride4; i += kBlock) {

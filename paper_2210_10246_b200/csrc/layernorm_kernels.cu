@@ -336,11 +336,12 @@ __global__ void __launch_bounds__(NT) ln_bwd_vec_kernel(
     const float* __restrict__ gamma, const float* __restrict__ beta, float* __restrict__ dx,
     double* __restrict__ ws, int64_t rows, int cols) {
     grid_dep_wait();  // PDL: predecessor complete and visible
-    grid_dep_launch();
+    // persistent grid: let stage 2 (a PDL dependent) get resident in the
+    // leftover slots; it waits for us to finish
+    grid_dep_launch_persistent();
     // Thread t owns the CPT float4 column groups t, t + blockDim, ... of every
     // row (conflict-free 128-bit smem reads, coalesced stores); more columns
     // per thread amortise the per-row block reduction.
-    grid_dep_launch();  // let stage 2 (PDL) get launched; it waits for us to finish
     extern __shared__ __align__(128) unsigned char dsm[];
     uint64_t* full = reinterpret_cast<uint64_t*>(dsm);
     float* ring = reinterpret_cast<float*>(dsm + 128);

@@ -7,7 +7,7 @@
 #include <utility>
 
 #ifndef TM_PDL
-#define TM_PDL 0
+#define TM_PDL 1
 #endif
 
 #include "../../include/tempo_b200.h"
@@ -127,11 +127,14 @@ cudaError_t launch_mt_keep_bits(uint64_t seed, double p, uint64_t e_begin, int64
 
 // Type-checked launch: launch(kernel, grid, block, smem, stream)(args...) is
 // `kernel<<<grid, block, smem, stream>>>(args...)`, with programmatic stream
-// serialization when TM_PDL=1.  Every kernel of this library starts with
-// grid_dep_wait() (before any global access), which makes PDL safe after any
-// predecessor -- but measured on the bench chain it LOST ~10 % (2.14 ->
-// 2.36-2.44 ms/step), so it is off by default; only the LayerNorm stage-2
-// reduce is launched as a dependent (launch_pdl), where it wins ~2 us.
+// serialization when TM_PDL=1 (default).  Every kernel of this library
+// starts with grid_dep_wait() (before any global access), which makes PDL
+// safe after any predecessor.  Measured on the bench chain: with every kernel
+// triggering its dependents at its start it LOST 7-10 % (2.05 -> 2.20 ms:
+// the dependents' early CTAs take the slots of the later waves of the
+// multi-wave row kernels); with the trigger only in the single-wave
+// persistent kernels (grid_dep_launch_persistent) and implicit at exit
+// elsewhere it WINS 1.4 % (2.048 -> 2.021 ms/step: launch gaps hidden).
 template <typename... KArgs>
 struct Launch {
     void (*kernel)(KArgs...);
