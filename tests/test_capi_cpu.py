@@ -197,3 +197,30 @@ def test_extra_tables_parse_roundtrip_and_eval(name, port):
     for m in (0, 1):
         mm = np.full(ys.size, m, np.uint8)
         assert np.array_equal(t.eval_host(ys, mm), pt.eval(ys, mm))
+
+
+def test_peer_exchange_sizes_and_argument_errors():
+    """The fused multi-GPU dgamma/dbeta exchange: buffer sizes (two epoch
+    parities x world slots of the padded 2*cols fp64 / one flag per 32-column
+    block) and the argument errors raised before any GPU work."""
+    import ctypes
+    L = _capi.lib()
+    for world, cols in [(1, 1024), (2, 1024), (8, 768), (3, 37)]:
+        ncb = (2 * cols + 31) // 32
+        assert L.tempo_ln_peer_inbox_bytes(world, cols) == 2 * world * ncb * 32 * 8
+        assert L.tempo_ln_peer_flag_bytes(world, cols) == 2 * world * ncb * 4
+    assert L.tempo_ln_peer_inbox_bytes(0, 1024) == 0
+    fake = ctypes.c_void_p(16)  # never dereferenced: every case fails validation first
+
+    def run(rank, world, epoch, arrays=True):
+        st = ops._PeerStruct(rank, world, fake.value if arrays else None,
+                             fake.value if arrays else None, epoch, fake.value)
+        return L.tempo_ln_param_reduce_peer(fake, 1, 8, ctypes.byref(st), fake, fake, None)
+
+    assert L.tempo_ln_param_reduce_peer(fake, 1, 8, None, fake, fake, None) == 3  # null group
+    assert run(2, 2, 1) == 3      # rank outside [0, world)
+    assert run(0, 0, 1) == 3      # empty world
+    assert run(0, 2, 0) == 3      # epochs start at 1
+    assert run(0, 2, 1, arrays=False) == 3  # missing buffer arrays
+    st = ops._PeerStruct(0, 2, fake.value, fake.value, 1, fake.value)
+    assert L.tempo_ln_param_reduce_peer(fake, -1, 8, ctypes.byref(st), fake, fake, None) == 2
