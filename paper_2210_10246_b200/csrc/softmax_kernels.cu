@@ -72,6 +72,36 @@ __device__ __forceinline__ float exp_shift(float z, float mx) {
 #endif
 }
 
+// exp_shift for two elements on the packed fp32x2 pipe (FADD2/FMUL2/FFMA2):
+// every lane rounds exactly like the scalar exp_shift, so the bits are the
+// same; the instruction count per element roughly halves.
+#ifndef TM_SOFTMAX_PACKED
+#define TM_SOFTMAX_PACKED 1
+#endif
+__device__ __forceinline__ float2 exp_shift2(float2 z, float mx) {
+#if TM_SOFTMAX_EXP == 1
+    const float2 L2E = make_float2(1.44269502162933349609f, 1.44269502162933349609f);
+    const float2 L2E_LO = make_float2(1.925963033500011e-08f, 1.925963033500011e-08f);
+    const float2 NMX = make_float2(-mx, -mx);
+    const float2 d = __fadd2_rn(z, NMX);
+    const float2 w = __fmul2_rn(d, L2E);
+    const float2 wl = __ffma2_rn(d, L2E_LO, __ffma2_rn(d, L2E, make_float2(-w.x, -w.y)));
+    const float2 e = make_float2(ex2_approx_ftz(w.x), ex2_approx_ftz(w.y));
+    const float2 LN2 = make_float2(0.69314718055994531f, 0.69314718055994531f);
+#if TM_SOFTMAX_TWOSUM
+    const float2 bb = __fadd2_rn(d, make_float2(-z.x, -z.y));
+    const float2 t1 = __fadd2_rn(d, make_float2(-bb.x, -bb.y));
+    const float2 err = __fadd2_rn(__fadd2_rn(z, make_float2(-t1.x, -t1.y)),
+                                  __fadd2_rn(NMX, make_float2(-bb.x, -bb.y)));
+    return __ffma2_rn(e, __ffma2_rn(wl, LN2, err), e);
+#else
+    return __ffma2_rn(e, __fmul2_rn(wl, LN2), e);
+#endif
+#else
+    return make_float2(exp_shift(z.x, mx), exp_shift(z.y, mx));
+#endif
+}
+
 __device__ __forceinline__ float dscale(float v, double s) { return (float)((double)v * s); }
 
 template <int VPL, int MODE>
@@ -112,10 +142,16 @@ __global__ void __launch_bounds__(kBlock) softmax_fwd_vec_kernel(
             float acc = 0.0f;
 #pragma unroll
             for (int k = 0; k < VPL; ++k) {
+#if TM_SOFTMAX_PACKED
+                const float2 lo = exp_shift2(make_float2(v[i][k].x, v[i][k].y), mx);
+                const float2 hi = exp_shift2(make_float2(v[i][k].z, v[i][k].w), mx);
+                v[i][k] = make_float4(lo.x, lo.y, hi.x, hi.y);
+#else
                 v[i][k].x = exp_shift(v[i][k].x, mx);
                 v[i][k].y = exp_shift(v[i][k].y, mx);
                 v[i][k].z = exp_shift(v[i][k].z, mx);
                 v[i][k].w = exp_shift(v[i][k].w, mx);
+#endif
                 acc += (v[i][k].x + v[i][k].y) + (v[i][k].z + v[i][k].w);
             }
             inv[i] = 1.0f / warp_sumf(acc);
