@@ -22,11 +22,12 @@ constexpr int kMtPolyWords = (kMtDeg + 63) / 64;  // 312 words per jump polynomi
 constexpr int kMtBaseWords = kMtDeg - 1 + kMtN;   // windows i <= 19936 of 312 words
 constexpr int64_t kMtChunk = int64_t(1) << TM_MT_CHUNK_LOG2;  // outputs per device stream
 constexpr int kMtLevels = 4;                    // 32^4 streams of kMtChunk: 2^38 outputs
-// The device jump splits each polynomial's words over kMtJumpParts CTAs and
-// reads each part as 4-bit groups of exponents (method of four Russians).
-constexpr int kMtJumpParts = 16;
+// The device jump splits each polynomial's words over kMtJumpParts CTAs.
+constexpr int kMtJumpParts = 8;
 constexpr int kMtJumpWords = (kMtPolyWords + kMtJumpParts - 1) / kMtJumpParts;  // per part
-constexpr int kMtJumpGroups = 64 * kMtJumpWords / 4;  // 4-bit exponent groups per part
+// Sentinel index of the padded set-bit lists: points past the part's words
+// and past the 312-word tail, into a zero region of the staged slice.
+constexpr int kMtJumpSentinel = 64 * kMtJumpWords + (int)kMtN;
 
 // w_{j} from w_{j-312}, w_{j-311}, w_{j-156} (mersenne_twister_engine::_M_gen_rand:
 // upper 33 bits of w_{j-312}, lower 31 of w_{j-311}, twisted, xor w_{j-156}).
@@ -49,11 +50,9 @@ void mt_seed_state(uint64_t seed, uint64_t* st312);
 // Jump polynomials x^(d * 32^l * kMtChunk) mod P, layout [l][d-1][kMtPolyWords]
 // (computed once per process; nullptr if the construction failed).
 const uint64_t* mt_jump_polys();
-// The same polynomials as lists of nonzero 4-bit exponent groups per part:
-// entry = (group << 4) | pattern (group g covers exponents 4g..4g+3 relative
-// to the part's first bit, pattern bit a = exponent 4g+a set), each part's
-// list padded with 0 entries (pattern 0 adds nothing) to a multiple of 4;
-// part (l, d-1, q) spans [off[i], off[i+1]) with
+// The same polynomials as lists of set-bit indices RELATIVE to their part's
+// first bit (uint16), each part's list padded with kMtJumpSentinel to a
+// multiple of 4; part (l, d-1, q) spans [off[i], off[i+1]) with
 // i = (l * 31 + d - 1) * kMtJumpParts + q.
 const uint16_t* mt_jump_index(const int32_t** off, size_t* count);
 // Smallest 64-bit output x that the reference keeps at drop probability p.

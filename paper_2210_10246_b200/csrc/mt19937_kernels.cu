@@ -35,11 +35,7 @@ namespace {
 
 constexpr int kGenThreads = 128;  // outputs per recurrence step (<= 156)
 constexpr int kRing = 512;        // ring buffer words (>= 312 + 128, power of two)
-#ifndef TM_MT_JUMP_SPLIT
-#define TM_MT_JUMP_SPLIT 2
-#endif
-constexpr int kJumpSplit = TM_MT_JUMP_SPLIT;  // threads per state word (slices of the group list)
-constexpr int kJumpThreads = 320 * kJumpSplit;
+constexpr int kJumpThreads = 320;
 
 // Sequence w_0 .. w_{kMtBaseWords-1} from each source state.
 __global__ void __launch_bounds__(kGenThreads) mt_base_kernel(const uint64_t* __restrict__ src,
@@ -70,24 +66,20 @@ __global__ void __launch_bounds__(kGenThreads) mt_base_kernel(const uint64_t* __
 
 // Children states: child c = child0 + s * 32 + d (d = 0: the source itself),
 // stored at out[(c - child_lo) * 312] for c in [child_lo, child_hi].  The
-// 312 polynomial words are split over kMtJumpParts CTAs (grid.x).  A part's
-// exponents are read in 4-bit groups (method of four Russians): the CTA first
-// builds, for its slice of the sequence, the table U[p][x] = XOR over the set
-// bits a of p of w[x + a] (16 patterns, in smem), then thread j XORs
-// U[p][4 g + j] over the part's list of nonzero groups (g, p), four entries
-// per uniform 64-bit load -- one shared-memory load per GROUP instead of one
-// per set bit (about 15/32 of the loads, plus the table build); the partial
-// state is XORed into the zeroed output.
-constexpr int kJumpX = 4 * kMtJumpGroups + (int)kMtN - 4;  // table columns x
-constexpr int kJumpMaxEntries = kMtJumpGroups + 4;           // a part's padded group list
-constexpr size_t kJumpSmem = (size_t)16 * kJumpX * sizeof(uint64_t) + kJumpMaxEntries * 2;
+// 312 polynomial words are split over kMtJumpParts CTAs (grid.x); each
+// stages only the slice of the sequence its words touch (plus a zero tail
+// for the list padding) in smem and walks the part's precomputed list of
+// set-bit indices, four per uniform 64-bit load: per set bit one LDS and
+// half a 3-input XOR; the partial state is XORed into the zeroed output.
+constexpr int kJumpSlice = 64 * kMtJumpWords + 2 * (int)kMtN;  // words staged per CTA
 
 __global__ void __launch_bounds__(kJumpThreads) mt_jump_kernel(
     const uint64_t* __restrict__ base, const uint16_t* __restrict__ idx,
     const int32_t* __restrict__ off, int poly0, uint64_t* __restrict__ out, int64_t child0,
     int64_t child_lo, int64_t child_hi) {
     grid_dep_wait();  // PDL: predecessor complete and visible
-    extern __shared__ uint64_t U[];  // [16][kJumpX]
+    grid_dep_launch();
+    __shared__ uint64_t slice[kJumpSlice];
     const int part = blockIdx.x, d = blockIdx.y, s = blockIdx.z;
     const int64_t child = child0 + (int64_t)s * 32 + d;
     if (child < child_lo || child > child_hi) return;  // not needed
@@ -99,48 +91,22 @@ __global__ void __launch_bounds__(kJumpThreads) mt_jump_kernel(
         return;
     }
     const int g0 = 64 * part * kMtJumpWords;  // first sequence word of the slice
+    const int real = 64 * kMtJumpWords + (int)kMtN;
+    for (int i = j; i < kJumpSlice; i += kJumpThreads)
+        slice[i] = (i < real && g0 + i < kMtBaseWords) ? b[g0 + i] : 0ull;
+    __syncthreads();
+    if (j >= (int)kMtN) return;
     const int pi = (poly0 + d - 1) * kMtJumpParts + part;
     const int k0 = __ldg(off + pi), k1 = __ldg(off + pi + 1);
-    uint16_t* ent = reinterpret_cast<uint16_t*>(U + 16 * kJumpX);  // the part's list, staged
-    for (int k = j; k < k1 - k0; k += kJumpThreads) ent[k] = __ldg(idx + k0 + k);
-    auto word = [&](int x) { return g0 + x < (int)kMtBaseWords ? __ldg(b + g0 + x) : 0ull; };
-    for (int x = j; x < kJumpX; x += kJumpThreads) {
-        const uint64_t w0 = word(x), w1 = word(x + 1), w2 = word(x + 2), w3 = word(x + 3);
-        uint64_t* u = U + x;
-        u[0] = 0;
-        u[1 * kJumpX] = w0;
-        u[2 * kJumpX] = w1;
-        u[3 * kJumpX] = w0 ^ w1;
-        u[4 * kJumpX] = w2;
-        u[5 * kJumpX] = w2 ^ w0;
-        u[6 * kJumpX] = w2 ^ w1;
-        u[7 * kJumpX] = w2 ^ w1 ^ w0;
-        u[8 * kJumpX] = w3;
-        u[9 * kJumpX] = w3 ^ w0;
-        u[10 * kJumpX] = w3 ^ w1;
-        u[11 * kJumpX] = w3 ^ w1 ^ w0;
-        u[12 * kJumpX] = w3 ^ w2;
-        u[13 * kJumpX] = w3 ^ w2 ^ w0;
-        u[14 * kJumpX] = w3 ^ w2 ^ w1;
-        u[15 * kJumpX] = w3 ^ w2 ^ w1 ^ w0;
-    }
-    __syncthreads();
-    // kJumpSplit threads per state word: slice h walks its share of the quads
-    const int h = j / 320, jw = j - h * 320;
-    if (jw >= (int)kMtN) return;
-    const int nq = (k1 - k0) >> 2, qh = (nq + kJumpSplit - 1) / kJumpSplit;
-    const uint64_t* L = reinterpret_cast<const uint64_t*>(ent);
-    const uint64_t* uj = U + jw;
-    // entry e = (g << 4) | p  ->  U[p][4 g + jw] = uj[p * kJumpX + 4 g]
-    auto at = [&](uint32_t e) { return uj[(e & 15u) * kJumpX + ((e >> 4) << 2)]; };
+    const uint64_t* L = reinterpret_cast<const uint64_t*>(idx + k0);
+    const uint64_t* sj = slice + j;
     uint64_t acc = 0;
 #pragma unroll 4
-    for (int k = h * qh; k < min(nq, (h + 1) * qh); ++k) {
-        const uint64_t q = L[k];  // four entries, uniform over the warp
-        acc ^= at((uint32_t)q & 0xffffu) ^ at((uint32_t)(q >> 16) & 0xffffu) ^
-               at((uint32_t)(q >> 32) & 0xffffu) ^ at((uint32_t)(q >> 48));
+    for (int k = 0; k < (k1 - k0) >> 2; ++k) {
+        const uint64_t q = __ldg(L + k);  // four indices, uniform over the CTA
+        acc ^= sj[q & 0xffff] ^ sj[(q >> 16) & 0xffff] ^ sj[(q >> 32) & 0xffff] ^ sj[q >> 48];
     }
-    atomicXor((unsigned long long*)(o + jw), acc);
+    atomicXor((unsigned long long*)(o + j), acc);
 }
 
 // Keep bits of elements [e_begin, e_end); chunk k = k0 + blockIdx.x.  Step t
@@ -306,9 +272,6 @@ cudaError_t launch_mt_keep_bits(uint64_t seed, double p, uint64_t e_begin, int64
     uint64_t* base = reinterpret_cast<uint64_t*>(w + L.base_off);
 
     launch(mt_seed_kernel, 1, 32, 0, st)(seed, seed_st);
-    // the jump kernel's 16-pattern table needs the opt-in smem limit (set
-    // once per device by grid_for)
-    (void)grid_for((const void*)mt_jump_kernel, kJumpThreads, kJumpSmem, 1);
 
     const int64_t k0 = (int64_t)(e_begin / kMtChunk);
     const int64_t k1 = (int64_t)((e_begin + (uint64_t)n - 1) / kMtChunk);
@@ -334,8 +297,7 @@ cudaError_t launch_mt_keep_bits(uint64_t seed, double p, uint64_t e_begin, int64
             err = cudaMemsetAsync(nxt, 0, (size_t)(chi - clo + 1) * kMtN * sizeof(uint64_t), st);
             if (err != cudaSuccess) return err;
             dim3 grid(kMtJumpParts, 32, (unsigned)S);
-            launch(mt_jump_kernel, grid, kJumpThreads, kJumpSmem, st)(base, jidx, joff, l * 31, nxt,
-                                                                  lo * 32,
+            launch(mt_jump_kernel, grid, kJumpThreads, 0, st)(base, jidx, joff, l * 31, nxt, lo * 32,
                                                           clo, chi);
             err = cudaGetLastError();
             if (err != cudaSuccess) return err;

@@ -220,12 +220,10 @@ void build_index(JumpTables& T) {
             T.off[(size_t)pi * kMtJumpParts + q] = (int32_t)T.idx.size();
             const int w0 = q * kMtJumpWords, w1 = std::min(kMtPolyWords, w0 + kMtJumpWords);
             for (int w = w0; w < w1; ++w)
-                for (int b = 0; b < 64; b += 4) {
-                    const unsigned pat = (unsigned)((g[w] >> b) & 15u);
-                    if (pat) T.idx.push_back((uint16_t)((((64 * (w - w0) + b) / 4) << 4) | pat));
-                }
+                for (int b = 0; b < 64; ++b)
+                    if ((g[w] >> b) & 1u) T.idx.push_back((uint16_t)(64 * (w - w0) + b));
             while ((T.idx.size() - T.off[(size_t)pi * kMtJumpParts + q]) % 4)
-                T.idx.push_back((uint16_t)0);
+                T.idx.push_back((uint16_t)kMtJumpSentinel);
         }
     }
     T.off[(size_t)npoly * kMtJumpParts] = (int32_t)T.idx.size();
