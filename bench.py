@@ -537,6 +537,10 @@ def main():
         try:
             r = subprocess.run([exe, "20", "3"], capture_output=True, text=True, timeout=300)
             cpp_api = json.loads(r.stdout.strip().splitlines()[-1])
+            # the same with Tape::backward(..., synchronize = false)
+            r = subprocess.run([exe, "20", "3", "async"], capture_output=True, text=True,
+                               timeout=300)
+            cpp_api["async_backward"] = json.loads(r.stdout.strip().splitlines()[-1])
         except Exception as ex:
             cpp_api = {"unavailable": str(ex)[:200]}
 

@@ -247,7 +247,13 @@ public:
     const TapeNode& node(NodeId id) const;
     const Tensor& value(NodeId id) const;
     std::size_t size() const { return nodes_.size(); }
-    GradientMap backward(NodeId root, Tensor seed);
+    // tape.hpp:139.  Like the reference's (synchronous, CPU) backward it
+    // returns with every gradient computed: it synchronizes the graph's
+    // stream.  `synchronize = false` returns as soon as the work is queued
+    // (results are stream-ordered on the graph's stream; host reads such as
+    // Tensor::to_host synchronize anyway) -- valid when every tensor the
+    // tape touches was allocated on that stream or outlives the work.
+    GradientMap backward(NodeId root, Tensor seed, bool synchronize = true);
 
 private:
     std::vector<TapeNode> nodes_;

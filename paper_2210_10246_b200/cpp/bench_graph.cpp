@@ -14,6 +14,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <random>
+#include <string>
 #include <vector>
 
 #include "../../include/tempo_b200/tempo.hpp"
@@ -32,6 +33,9 @@ static Tensor randn_dev(Shape s, unsigned seed, double scale = 1.0, double shift
 
 int main(int argc, char** argv) {
     const int steps = argc > 1 ? std::atoi(argv[1]) : 20, warmup = argc > 2 ? std::atoi(argv[2]) : 3;
+    // argv[3] == "async": Tape::backward(..., synchronize = false) -- every
+    // tensor here lives on stream `st` or outlives the loop
+    const bool kSync = !(argc > 3 && std::string(argv[3]) == "async");
     const std::int64_t B = 64, S = 512, H = 1024, A = 16, T = B * S, R = B * A * S;
     const double p = 0.1;
     cudaStream_t st;
@@ -56,7 +60,7 @@ int main(int argc, char** argv) {
             NodeId zn = g.leaf(z, "z");
             NodeId d = tempo_ops::softmax_dropout(g, zn, p, m_att, 0, 0, "attn_probs",
                                                   "attn_drop_out", "attn_drop_mask", nullptr);
-            g.tape.backward(d, dD);
+            g.tape.backward(d, dD, kSync);
         }
         {   // hidden dropout 1 -> LayerNorm 1
             Graph g;
@@ -64,14 +68,14 @@ int main(int argc, char** argv) {
             NodeId xn = g.leaf(x1, "x"), gn = g.param(g1, "g"), bn = g.param(b1, "b");
             NodeId d = ref_ops::dropout(g, xn, p, m1, "d1", "d1_mask");
             NodeId y = tempo_ops::layernorm(g, d, gn, bn, 1e-5, "ln1", "ln1_rstd");
-            g.tape.backward(y, dy1);
+            g.tape.backward(y, dy1, kSync);
         }
         {   // GELU
             Graph g;
             g.stream = st;
             NodeId xn = g.leaf(xg, "x");
             NodeId y = tempo_ops::gelu(g, xn, &table, "gelu", "gelu_mask");
-            g.tape.backward(y, dyg);
+            g.tape.backward(y, dyg, kSync);
         }
         {   // hidden dropout 2 -> LayerNorm 2
             Graph g;
@@ -79,7 +83,7 @@ int main(int argc, char** argv) {
             NodeId xn = g.leaf(x2, "x"), gn = g.param(g2, "g"), bn = g.param(b2, "b");
             NodeId d = ref_ops::dropout(g, xn, p, m2, "d2", "d2_mask");
             NodeId y = tempo_ops::layernorm(g, d, gn, bn, 1e-5, "ln2", "ln2_rstd");
-            g.tape.backward(y, dy2);
+            g.tape.backward(y, dy2, kSync);
         }
     };
     for (int i = 0; i < warmup; ++i) step();
@@ -106,9 +110,11 @@ int main(int argc, char** argv) {
                          2 * nh * (8.125 + 8.125) + 2 * (8 * nh + 4 * T + 8 * H) +
                          2 * (12 * nh + 4 * T + 16 * H);
     std::printf("{\"what\": \"bench.py op chain through the C++ operator API (Graph/Tape, "
-                "fresh graphs per step, stream-ordered pooled allocation)\", \"steps\": %d, "
+                "fresh graphs per step, stream-ordered pooled allocation)\", \"backward\": \"%s\", "
+                "\"steps\": %d, "
                 "\"ms_per_step\": %.4f, \"wall_ms_per_step\": %.4f, \"bytes_per_step\": %.0f, "
                 "\"gbs\": %.1f}\n",
-                steps, ms, wall_ms, bytes, bytes / (ms * 1e-3) / 1e9);
+                kSync ? "synchronous" : "async", steps, ms, wall_ms, bytes,
+                bytes / (ms * 1e-3) / 1e9);
     return 0;
 }

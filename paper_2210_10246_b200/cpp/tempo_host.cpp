@@ -477,7 +477,7 @@ const TapeNode& Tape::node(NodeId id) const {
 }
 const Tensor& Tape::value(NodeId id) const { return node(id).value; }
 
-GradientMap Tape::backward(NodeId root, Tensor seed) {
+GradientMap Tape::backward(NodeId root, Tensor seed, bool synchronize) {
     check_node_id(root);
     if (backward_done_) throw StateError("backward already ran on this tape");
     if (!seed.defined()) throw ParamError("backward needs a seed gradient");
@@ -522,7 +522,10 @@ GradientMap Tape::backward(NodeId root, Tensor seed) {
         nd.charged.clear();
         if (i != root) grads[i] = Tensor();
     }
-    cuda_check(cudaStreamSynchronize(static_cast<cudaStream_t>(st)), "backward");
+    if (synchronize)
+        cuda_check(cudaStreamSynchronize(static_cast<cudaStream_t>(st)), "backward");
+    else
+        cuda_check(cudaGetLastError(), "backward");
     return GradientMap(std::move(grads));
 }
 

@@ -432,6 +432,30 @@ static void test_graph_on_stream() {
     for (size_t i = 0; i < a.size(); ++i) CHECK(a[i] == b[i]);
 }
 
+// Tape::backward(..., synchronize = false) queues the same work: after the
+// host read (which synchronizes) the gradients equal the synchronous ones.
+static void test_async_backward() {
+    const std::int64_t rows = 32, m = 768;
+    std::vector<float> xh = randn(rows * m, 41), gh = randn(rows * m, 42);
+    std::vector<float> gam(m, 0.9f), bet(m, -0.02f);
+    GeluPolyTable table = GeluPolyTable::default_fit();
+    cudaStream_t st;
+    CHECK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) == cudaSuccess);
+    auto run = [&](bool sync) -> std::vector<std::vector<float>> {
+        Graph g;
+        g.stream = st;
+        NodeId x = g.leaf(Tensor::from_host({rows, m}, xh), "x");
+        NodeId ga = g.param(Tensor::from_host({m}, gam), "g"), be = g.param(Tensor::from_host({m}, bet), "b");
+        NodeId y = tempo_ops::gelu(g, x, &table, "y", "ym");
+        NodeId l = tempo_ops::layernorm(g, y, ga, be, 1e-5, "l", "lr");
+        GradientMap gm = g.tape.backward(l, Tensor::from_host({rows, m}, gh), sync);
+        return {gm.at(x).to_host(), gm.at(ga).to_host(), gm.at(be).to_host()};
+    };
+    auto a = run(true), b = run(false);
+    cudaStreamDestroy(st);
+    for (size_t i = 0; i < a.size(); ++i) CHECK(a[i] == b[i]);
+}
+
 // A large mask goes through the device generator (jump-ahead): it must be
 // the reference's stream bit for bit (here: against the host engine).
 static void test_large_mask_device_stream() {
@@ -456,6 +480,7 @@ int main() {
     run("large mask: device reference stream", test_large_mask_device_stream);
     run("sdpa (cuBLAS GEMMs + Tempo softmax/dropout)", test_sdpa);
     run("graph on a non-blocking stream", test_graph_on_stream);
+    run("asynchronous backward", test_async_backward);
     std::printf("%d failure(s)\n", g_fail);
     return g_fail;
 }
