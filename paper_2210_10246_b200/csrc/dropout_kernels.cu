@@ -27,7 +27,7 @@ constexpr int kUnroll = 4;
 #define TM_DROPOUT_WAVES 8
 #endif
 #ifndef TM_DROPOUT_U8
-#define TM_DROPOUT_U8 1
+#define TM_DROPOUT_U8 2  // re-tuned at r1l: bwd 49.8 -> 47.3 us, bit-identical
 #endif
 
 __device__ __forceinline__ float dscale(float v, double s) { return (float)((double)v * s); }
