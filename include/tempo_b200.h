@@ -135,8 +135,12 @@ int tempo_ln_ip_bwd(const float* dy, const float* y, const float* rstd, const fl
  * DEVICE arrays of `world` pointers (rank p's buffers as mapped here); epoch
  * is 1, 2, 3, ... per exchange (the same on all ranks).  The result is the
  * fixed-order (rank 0, 1, ...) sum of the ranks' fixed-order partial sums:
- * bitwise identical on every rank.  A peer that never arrives sets *status
- * to TEMPO_ERR_STATE after a bounded wait instead of hanging the GPU. */
+ * bitwise identical on every rank.  A peer that never arrives within
+ * timeout_ms (0 = the library default, 30 s) sets *status to
+ * TEMPO_ERR_STATE and the affected dgamma/dbeta entries to NaN (never a
+ * partial sum) instead of hanging the GPU.  *status is sticky: while it is
+ * nonzero every exchange on this rank writes NaN without waiting; rebuild
+ * the group (fresh zeroed buffers, epoch 1) to recover. */
 typedef struct {
     int32_t rank;
     int32_t world;
@@ -144,6 +148,7 @@ typedef struct {
     uint32_t* const* flags;
     uint32_t epoch;
     int32_t* status;
+    uint32_t timeout_ms;
 } tempo_ln_peer_t;
 size_t tempo_ln_peer_inbox_bytes(int32_t world, int64_t cols);
 size_t tempo_ln_peer_flag_bytes(int32_t world, int64_t cols);

@@ -158,6 +158,9 @@ namespace tempo_ops {
 // stashes its output (shared with downstream) and the bit mask, not x.
 template <class Spec>
 NodeId inplace_elementwise(Graph& g, NodeId x, std::string tag, std::string mask_tag) {
+    // allocate y / the mask on the graph's stream, where the kernel runs
+    // (as every builder in tempo_host.cpp does)
+    tempo_b200::StreamScope scope_(g.stream);
     const Tensor& vx = g.value(x);
     Tensor y = Tensor::empty(vx.shape());
     BoolMask mask = BoolMask::empty(vx.shape());

@@ -13,6 +13,7 @@
 #include <algorithm>
 #include <cmath>
 #include <fstream>
+#include <atomic>
 #include <map>
 #include <mutex>
 #include <sstream>
@@ -108,6 +109,11 @@ struct Tensor::Storage {
     Shape shape;
     float* ptr = nullptr;
     tempo_stream_t stream = nullptr;  // allocation (and release) stream
+    // The LayerNorm |gamma| >= 1e-12 refusal (ops_tempo.cpp:100-106) passed
+    // for these values: Tensors are immutable values (tensor.hpp:6-9), so the
+    // synchronous check (a D2H copy) runs once per gamma storage, not once
+    // per layernorm call.
+    std::atomic<bool> gamma_ok{false};
     ~Storage() { dev_free(ptr, stream); }
 };
 
@@ -582,13 +588,22 @@ std::string fallback_tag(std::string tag, const char* op, std::size_t id) {
     return std::string(op) + "_" + std::to_string(id);
 }
 
+// One cuBLAS handle per (thread, device): cublasSetStream + the GEMM on a
+// handle shared across threads would race (another thread's SetStream could
+// land between them and put the GEMM on the wrong stream).  Thread-local
+// handles need no lock; they are released at thread exit.
+struct BlasHandles {
+    std::map<int, cublasHandle_t> h;
+    ~BlasHandles() {
+        for (auto& kv : h)
+            if (kv.second) cublasDestroy(kv.second);
+    }
+};
 cublasHandle_t blas(tempo_stream_t st) {
-    static std::mutex mu;
-    static std::map<int, cublasHandle_t> handles;
+    thread_local BlasHandles handles;
     int dev = 0;
     cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
-    std::lock_guard<std::mutex> lock(mu);
-    cublasHandle_t& h = handles[dev];
+    cublasHandle_t& h = handles.h[dev];
     if (!h) {
         if (cublasCreate(&h) != CUBLAS_STATUS_SUCCESS) throw StateError("cublasCreate failed");
         cublasSetMathMode(h, CUBLAS_PEDANTIC_MATH);  // true fp32, never TF32
@@ -786,7 +801,13 @@ NodeId layernorm(Graph& g, NodeId x, NodeId gamma, NodeId beta, double epsilon, 
     if (vg.shape() != Shape{m} || vb.shape() != Shape{m})
         throw DimensionError("layernorm affine params " + shape_str(vg.shape()) + ", " +
                              shape_str(vb.shape()) + " do not match " + shape_str(vx.shape()));
-    check(tempo_ln_check_gamma(vg.data(), m, g.stream));  // |gamma| < 1e-12 -> ParamError
+    {  // |gamma| < 1e-12 -> ParamError; checked once per (immutable) gamma storage
+        std::shared_ptr<Tensor::Storage> gs = vg.weak_storage().lock();
+        if (!gs || !gs->gamma_ok.load(std::memory_order_acquire)) {
+            check(tempo_ln_check_gamma(vg.data(), m, g.stream));
+            if (gs) gs->gamma_ok.store(true, std::memory_order_release);
+        }
+    }
     const std::int64_t rows = m ? vx.numel() / m : 0;
     Shape rshape(vx.shape().begin(), vx.shape().end() - 1);
     Tensor y = Tensor::empty(vx.shape());

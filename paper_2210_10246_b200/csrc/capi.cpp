@@ -605,7 +605,7 @@ static int check_peer(const tempo_ln_peer_t* peer) {
 }
 
 static tb::LnPeer to_peer(const tempo_ln_peer_t* p) {
-    return tb::LnPeer{p->rank, p->world, p->inbox, p->flags, p->epoch, p->status};
+    return tb::LnPeer{p->rank, p->world, p->inbox, p->flags, p->epoch, p->status, p->timeout_ms};
 }
 
 int tempo_ln_ip_bwd_peer(const float* dy, const float* y, const float* rstd, const float* gamma,

@@ -3,8 +3,10 @@
 // Forward  (tempo_ops::layernorm, ops_tempo.cpp:98-119 -> layernorm_forward
 //           ops_reference.cpp:47-65 -> row_moments kernels.cpp:153-179):
 //   mean = sum x / M and var = sum (x - mean)^2 / M, two-pass as the
-//   reference, as fp32 tree sums (the reference sums in fp64 and stores fp32
-//   moments: identical to ~1 ulp); rstd = 1/sqrt(var + eps) in fp64 per row
+//   reference, as fp32 tree sums plus one refinement step of the mean
+//   (refine_moments: the reference sums in fp64 and stores float(mean); the
+//   refined fp32 mean rounds the same way at any |mean|/std); rstd =
+//   1/sqrt(var + eps) in fp64 per row
 //   (ops_tempo.cpp:111-112, F32-stored); y = fma(gamma*rstd, x - mean, beta)
 //   in fp32.  (The generic fallback kernel keeps the fp64 formulation.)
 //   Stash: y and rstd[row] only.
@@ -73,6 +75,24 @@ __device__ __forceinline__ void block_sum(T (&v)[kN], T* red, int& phase) {
         v[i] = warp_sum_t(s);
     }
     phase ^= 1;
+}
+
+// Row moments from a first mean estimate m0 (an fp32 tree sum / M) and the
+// sums over the row of d = x - m0 (t) and d^2 (q): one step of iterative
+// refinement.  The reference sums in fp64 and stores float(mean)
+// (kernels.cpp:165-176); an fp32 tree sum alone drifts by several ulps of the
+// mean when |mean| >> std (rel_err 1e-4 on y at |mean|/std = 1000).  Here
+// d = x - m0 is exact wherever x is within 2x of m0 (Sterbenz), so t/M is
+// the small correction mean - m0 accurate to ~M ulps of std, and
+// float(m0 + t/M) rounds to the reference's float(mean) except within
+// ~1e-7 std of a rounding tie.  var = q/M - (t/M)^2 (the sum of squares about
+// m0 minus the shift term), the reference's two-pass variance to fp32
+// accuracy.
+__device__ __forceinline__ void refine_moments(float m0, float t, float q, float inv_m,
+                                               float& mean, float& var) {
+    const double delta = (double)t * (double)inv_m;
+    mean = (float)((double)m0 + delta);
+    var = fmaxf(fmaf(-(float)delta, (float)delta, q * inv_m), 0.0f);
 }
 
 __device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
@@ -162,20 +182,22 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? 3 : 1) ln_fwd_vec_kernel(
                 ln_issue(x, nt, kRows, rows, cols, ring + st * tile_floats, &full[st]);
             }
         }
-        float mean[kRows], q[kRows];
+        float mean[kRows], q[2 * kRows];
 #pragma unroll
         for (int i = 0; i < kRows; ++i) {
-            mean[i] = s[i] * inv_m;
+            mean[i] = s[i] * inv_m;  // first estimate, refined below
             const float d0 = v[i].x - mean[i], d1 = v[i].y - mean[i];
             const float d2 = v[i].z - mean[i], d3 = v[i].w - mean[i];
             q[i] = act ? fmaf(d0, d0, d1 * d1) + fmaf(d2, d2, d3 * d3) : 0.0f;
+            q[kRows + i] = act ? (d0 + d1) + (d2 + d3) : 0.0f;
         }
-        block_sum<kRows>(q, red, phase);
+        block_sum<2 * kRows>(q, red, phase);
 #pragma unroll
         for (int i = 0; i < kRows; ++i) {
             const int64_t r = r0 + i;
             if (r >= rows) break;
-            const float var_f = q[i] * inv_m;
+            float var_f;
+            refine_moments(mean[i], q[kRows + i], q[i], inv_m, mean[i], var_f);
             const double rsd = 1.0 / sqrt((double)var_f + eps);  // ops_tempo.cpp:111-112
             const float rs = (float)rsd;
             if (act) {
@@ -203,7 +225,7 @@ constexpr int kWStages = TM_LN_FWD_STAGES;
 constexpr int kWWarps = 8;
 
 template <int VPL>
-__global__ void __launch_bounds__(kWWarps * 32) ln_fwd_warp_kernel(
+__global__ void __launch_bounds__(kWWarps * 32, 2) ln_fwd_warp_kernel(
     const float* __restrict__ x, const float* __restrict__ gamma, const float* __restrict__ beta,
     double eps, float* __restrict__ y, float* __restrict__ rstd, int64_t rows,
     int32_t* __restrict__ status) {
@@ -265,15 +287,17 @@ __global__ void __launch_bounds__(kWWarps * 32) ln_fwd_warp_kernel(
         float s = 0.0f;
 #pragma unroll
         for (int k = 0; k < VPL; ++k) s += (v[k].x + v[k].y) + (v[k].z + v[k].w);
-        const float mean = warp_sumf(s) * inv_m;
-        float q = 0.0f;
+        const float m0 = warp_sumf(s) * inv_m;  // first estimate of the mean
+        float q = 0.0f, t = 0.0f;
 #pragma unroll
         for (int k = 0; k < VPL; ++k) {
-            const float d0 = v[k].x - mean, d1 = v[k].y - mean;
-            const float d2 = v[k].z - mean, d3 = v[k].w - mean;
+            const float d0 = v[k].x - m0, d1 = v[k].y - m0;
+            const float d2 = v[k].z - m0, d3 = v[k].w - m0;
             q += fmaf(d0, d0, d1 * d1) + fmaf(d2, d2, d3 * d3);
+            t += (d0 + d1) + (d2 + d3);
         }
-        const float var_f = warp_sumf(q) * inv_m;
+        float mean, var_f;
+        refine_moments(m0, warp_sumf(t), warp_sumf(q), inv_m, mean, var_f);
         const float rs = (float)(1.0 / sqrt((double)var_f + eps));  // ops_tempo.cpp:111-112
         float4* yr = reinterpret_cast<float4*>(y + r * C);
 #pragma unroll
@@ -585,6 +609,7 @@ __global__ void __launch_bounds__(1024) ln_param_reduce_kernel(const double* __r
 // rank can only reach epoch e+2 (parity reuse) after every peer has set its
 // e+1 flags, i.e. after every peer finished reading its epoch-e slots.
 constexpr int kPeerCols = 32;
+constexpr uint64_t kPeerDefaultTimeoutNs = 30ull * 1000000000ull;  // 30 s
 constexpr int kPeerRowGroups = 8;
 
 __device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
@@ -601,20 +626,41 @@ __device__ __forceinline__ uint64_t globaltimer_ns() {
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     return t;
 }
-constexpr uint64_t kPeerTimeoutNs = 2000000000ull;  // 2 s
+// Failure semantics (a straggler or a dead peer): the wait is bounded by
+// timeout_ns (caller-chosen; the library default is 30 s, NCCL-like
+// patience for checkpoint saves / data stalls, yet finite so the GPU is never
+// hung); a block whose peers do not all arrive sets *status =
+// TEMPO_ERR_STATE and writes NaN to its dgamma/dbeta outputs instead of a
+// partial sum (the inbox may hold another epoch's data).  *status is
+// sticky: every later exchange on this rank sees it, skips the exchange
+// (no flags published, no waiting) and writes NaN, so a broken group fails
+// loudly until it is rebuilt -- never silently wrong.
+__device__ __forceinline__ int32_t ld_volatile_i32(const int32_t* p) {
+    return *reinterpret_cast<const volatile int32_t*>(p);
+}
 
 __global__ void __launch_bounds__(kPeerCols * kPeerRowGroups) ln_param_reduce_peer_kernel(
     const double* __restrict__ ws, int nparts, int cols, int rank, int world,
     double* const* __restrict__ inbox, uint32_t* const* __restrict__ flags, uint32_t epoch,
-    float* __restrict__ dgamma, float* __restrict__ dbeta, int32_t* __restrict__ status) {
+    uint64_t timeout_ns, float* __restrict__ dgamma, float* __restrict__ dbeta,
+    int32_t* __restrict__ status) {
     grid_dep_wait();
     __shared__ double part[kPeerRowGroups][kPeerCols + 1];
+    __shared__ int failed;
     const int tx = threadIdx.x % kPeerCols, ty = threadIdx.x / kPeerCols;
     const int64_t total = 2 * (int64_t)cols;
     const int cb = blockIdx.x, ncb = gridDim.x;
     const int64_t j = (int64_t)cb * kPeerCols + tx;
     const int par = (int)(epoch & 1u);
     const int64_t tstride = (int64_t)ncb * kPeerCols;  // inbox slot stride (padded)
+    if (threadIdx.x == 0) failed = ld_volatile_i32(status) != 0;  // sticky: an earlier failure
+    __syncthreads();
+    if (failed) {
+        if (ty == 0 && j < total) {
+            if (j < cols) dgamma[j] = __int_as_float(0x7fc00000); else dbeta[j - cols] = __int_as_float(0x7fc00000);
+        }
+        return;
+    }
     double acc = 0.0;
     if (j < total)
         for (int c = ty; c < nparts; c += kPeerRowGroups) acc += ws[(size_t)c * total + j];
@@ -634,10 +680,11 @@ __global__ void __launch_bounds__(kPeerCols * kPeerRowGroups) ln_param_reduce_pe
             st_release_sys(flags[p] + ((size_t)par * world + rank) * ncb + cb, epoch);
         const uint32_t* mine = flags[rank] + (size_t)par * world * ncb + cb;
         const uint64_t t0 = globaltimer_ns();
-        for (int s = 0; s < world; ++s) {
+        for (int s = 0; s < world && !failed; ++s) {
             while (ld_acquire_sys(mine + (size_t)s * ncb) != epoch) {
-                if (globaltimer_ns() - t0 > kPeerTimeoutNs) {  // a peer never arrived
+                if (globaltimer_ns() - t0 > timeout_ns) {  // a peer never arrived
                     atomicExch(status, TEMPO_ERR_STATE);
+                    failed = 1;
                     break;
                 }
                 __nanosleep(128);
@@ -649,7 +696,8 @@ __global__ void __launch_bounds__(kPeerCols * kPeerRowGroups) ln_param_reduce_pe
         const double* my = inbox[rank] + (size_t)par * world * tstride;
         double v = 0.0;
         for (int s = 0; s < world; ++s) v += __ldcg(my + (size_t)s * tstride + j);
-        if (j < cols) dgamma[j] = (float)v; else dbeta[j - cols] = (float)v;
+        const float out = failed ? __int_as_float(0x7fc00000) : (float)v;  // NaN: not a partial sum
+        if (j < cols) dgamma[j] = out; else dbeta[j - cols] = out;
     }
 }
 
@@ -745,9 +793,11 @@ cudaError_t launch_ln_param_reduce_peer(const double* partials, int64_t nparts, 
                                         cudaStream_t st) {
     if (cols == 0) return cudaSuccess;
     const int ncb = (int)((2 * cols + kPeerCols - 1) / kPeerCols);
+    const uint64_t tmo = peer.timeout_ms ? (uint64_t)peer.timeout_ms * 1000000ull
+                                         : kPeerDefaultTimeoutNs;
     return launch_pdl((const void*)ln_param_reduce_peer_kernel, ncb, kPeerCols * kPeerRowGroups, 0,
                       st, partials, (int)nparts, (int)cols, peer.rank, peer.world, peer.inbox,
-                      peer.flags, peer.epoch, dgamma, dbeta, peer.status);
+                      peer.flags, peer.epoch, tmo, dgamma, dbeta, peer.status);
 }
 
 size_t ln_bwd_workspace(int64_t rows, int64_t cols) {

@@ -42,6 +42,25 @@ enum FwdMode { kPlain = 0, kSupplied = 1, kPhilox = 2 };
 #ifndef TM_SOFTMAX_EXP
 #define TM_SOFTMAX_EXP 1  // 1: SFU ex2 + FMA-split exponent (+ TwoSum: 0.94 -> 0.96, P err 5e-7); 0: expf + TwoSum
 #endif
+// max that propagates NaN (the reference's row max: a NaN anywhere makes the
+// whole row NaN, ops_reference.cpp:113-121).
+__device__ __forceinline__ float fmax_nan(float a, float b) {
+    float r;
+    asm("max.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
+    return r;
+}
+__device__ __forceinline__ float warp_max_nan(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmax_nan(v, __shfl_xor_sync(kFull, v, o));
+    return v;
+}
+// Elements with z - max below -128 (masked scores: -inf, finfo(f32).min,
+// or a +inf max) give exactly 0, as the reference's double exp does to
+// within its float rounding (e^-128 < 2^-149).  The select also discards
+// the NaN that the exponent split / TwoSum produce from infinite operands.
+// A row whose max is NaN or -inf (NaN anywhere, or all -inf) then sums to 0
+// and P = 0 * (1/0) = NaN for the whole row -- the reference's result too.
+constexpr float kExpCut = -128.0f;
 __device__ __forceinline__ float ex2_approx_ftz(float f) {
     float r;
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(f));
@@ -59,17 +78,18 @@ __device__ __forceinline__ float exp_shift(float z, float mx) {
 #if TM_SOFTMAX_TWOSUM
     const float bb = d - z;
     const float err = (z - (d - bb)) + (-mx - bb);  // TwoSum: (z - mx) = d + err exactly
-    return fmaf(e, fmaf(wl, 0.69314718055994531f, err), e);
+    const float r = fmaf(e, fmaf(wl, 0.69314718055994531f, err), e);
 #else
-    return fmaf(e, wl * 0.69314718055994531f, e);
+    const float r = fmaf(e, wl * 0.69314718055994531f, e);
 #endif
 #else
     float d = z - mx;
     float bb = d - z;
     float err = (z - (d - bb)) + (-mx - bb);  // TwoSum: (z - mx) = d + err exactly
     float e = expf(d);
-    return fmaf(e, err, e);
+    const float r = fmaf(e, err, e);
 #endif
+    return d >= kExpCut ? r : 0.0f;
 }
 
 // exp_shift for two elements on the packed fp32x2 pipe (FADD2/FMUL2/FFMA2):
@@ -93,10 +113,11 @@ __device__ __forceinline__ float2 exp_shift2(float2 z, float mx) {
     const float2 t1 = __fadd2_rn(d, make_float2(-bb.x, -bb.y));
     const float2 err = __fadd2_rn(__fadd2_rn(z, make_float2(-t1.x, -t1.y)),
                                   __fadd2_rn(NMX, make_float2(-bb.x, -bb.y)));
-    return __ffma2_rn(e, __ffma2_rn(wl, LN2, err), e);
+    const float2 r = __ffma2_rn(e, __ffma2_rn(wl, LN2, err), e);
 #else
-    return __ffma2_rn(e, __fmul2_rn(wl, LN2), e);
+    const float2 r = __ffma2_rn(e, __fmul2_rn(wl, LN2), e);
 #endif
+    return make_float2(d.x >= kExpCut ? r.x : 0.0f, d.y >= kExpCut ? r.y : 0.0f);
 #else
     return make_float2(exp_shift(z.x, mx), exp_shift(z.y, mx));
 #endif
@@ -137,8 +158,9 @@ __global__ void __launch_bounds__(kBlock) softmax_fwd_vec_kernel(
             float mx = v[i][0].x;
 #pragma unroll
             for (int k = 0; k < VPL; ++k)
-                mx = fmaxf(mx, fmaxf(fmaxf(v[i][k].x, v[i][k].y), fmaxf(v[i][k].z, v[i][k].w)));
-            mx = warp_max(mx);
+                mx = fmax_nan(mx, fmax_nan(fmax_nan(v[i][k].x, v[i][k].y),
+                                           fmax_nan(v[i][k].z, v[i][k].w)));
+            mx = warp_max_nan(mx);
             float acc = 0.0f;
 #pragma unroll
             for (int k = 0; k < VPL; ++k) {
@@ -271,8 +293,8 @@ __global__ void __launch_bounds__(kBlock) softmax_fwd_generic_kernel(
     for (int64_t r = warp; r < rows; r += nwarps) {
         const float* zr = z + r * C;
         float mx = -INFINITY;
-        for (int64_t j = lane; j < C; j += 32) mx = fmaxf(mx, zr[j]);
-        mx = warp_max(mx);
+        for (int64_t j = lane; j < C; j += 32) mx = fmax_nan(mx, zr[j]);
+        mx = warp_max_nan(mx);
         double acc = 0.0;
         for (int64_t j = lane; j < C; j += 32) acc += (double)exp_shift(zr[j], mx);
         const double inv = 1.0 / warp_sum(acc);

@@ -64,7 +64,8 @@ struct LnPeer {
     double* const* inbox;     // device array [world]: rank p's inbox
     uint32_t* const* flags;   // device array [world]: rank p's flags
     uint32_t epoch;           // 1, 2, 3, ... per exchange
-    int32_t* status;          // device int: TEMPO_ERR_STATE if a peer never arrived
+    int32_t* status;          // device int: TEMPO_ERR_STATE if a peer never arrived (sticky)
+    uint32_t timeout_ms;      // bound on the wait for peers; 0 = library default (30 s)
 };
 size_t ln_peer_inbox_bytes(int world, int64_t cols);
 size_t ln_peer_flag_bytes(int world, int64_t cols);

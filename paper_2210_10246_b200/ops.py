@@ -14,6 +14,7 @@ of word w = element 32w+i, the reference's BoolMask order).
 from __future__ import annotations
 
 import ctypes as C
+import os
 from typing import Optional, Tuple
 
 import torch
@@ -38,12 +39,49 @@ def _stream():
     return C.c_void_p(torch.cuda.current_stream().cuda_stream)
 
 
-def _f32(t: torch.Tensor, name: str) -> torch.Tensor:
-    if t.dtype != torch.float32:
-        raise TempoError(2, f"{name}: expected float32, got {t.dtype}")
+def _dev(t: torch.Tensor, name: str, dtype, device=None, numel=None, min_numel=None):
+    """Validate a buffer handed to the C-ABI as a raw pointer: dtype, CUDA,
+    same device as the op's primary input, contiguous (the kernels index it
+    densely; no silent eager-torch copy is made), and its size."""
+    if not isinstance(t, torch.Tensor):
+        raise TempoError(2, f"{name}: expected a torch.Tensor")
+    if t.dtype != dtype:
+        raise TempoError(2, f"{name}: expected {dtype}, got {t.dtype}")
     if not t.is_cuda:
         raise TempoError(2, f"{name}: expected a CUDA tensor")
-    return t.contiguous()
+    if device is not None and t.device != device:
+        raise TempoError(2, f"{name}: on {t.device}, expected {device}")
+    if not t.is_contiguous():
+        raise TempoError(2, f"{name}: expected a contiguous tensor")
+    if numel is not None and t.numel() != numel:
+        raise TempoError(2, f"{name}: has {t.numel()} elements, expected {numel}")
+    if min_numel is not None and t.numel() < min_numel:
+        raise TempoError(2, f"{name}: has {t.numel()} elements, needs >= {min_numel}")
+    return t
+
+
+def _f32(t: torch.Tensor, name: str, device=None, numel=None) -> torch.Tensor:
+    return _dev(t, name, torch.float32, device, numel)
+
+
+def _out(t: Optional[torch.Tensor], name: str, like: torch.Tensor) -> torch.Tensor:
+    """A float32 output the size of `like`: allocated when None, else checked."""
+    if t is None:
+        return torch.empty_like(like)
+    return _dev(t, name, torch.float32, like.device, like.numel())
+
+
+def _vec_out(t: Optional[torch.Tensor], name: str, n: int, device) -> torch.Tensor:
+    if t is None:
+        return torch.empty(n, dtype=torch.float32, device=device)
+    return _dev(t, name, torch.float32, device, n)
+
+
+def _mask(t: Optional[torch.Tensor], name: str, n: int, device) -> torch.Tensor:
+    """Bit-packed mask of n elements: int32 words, >= ceil(n/32) of them."""
+    if t is None:
+        return torch.empty(mask_words(n), dtype=torch.int32, device=device)
+    return _dev(t, name, torch.int32, device, min_numel=mask_words(n))
 
 
 def mask_words(n: int) -> int:
@@ -124,9 +162,8 @@ def gelu_ip_fwd(x: torch.Tensor, table: GeluTable, y: torch.Tensor = None,
     if table is None:
         raise TempoError(5, "in-place gelu needs a fitted table")
     x = _f32(x, "x")
-    y = torch.empty_like(x) if y is None else y
-    mask = torch.empty(mask_words(x.numel()), dtype=torch.int32, device=x.device) \
-        if mask is None else mask
+    y = _out(y, "y", x)
+    mask = _mask(mask, "mask", x.numel(), x.device)
     check(lib().tempo_gelu_ip_fwd(_ptr(x), _ptr(y), _ptr(mask), x.numel(), table.handle,
                                   _stream()))
     return y, mask
@@ -139,7 +176,11 @@ def gelu_ip_bwd(dy: torch.Tensor, y: torch.Tensor, mask: torch.Tensor, table: Ge
     dy, y = _f32(dy, "dy"), _f32(y, "y")
     if dy.shape != y.shape:
         raise TempoError(2, f"gelu backward shapes {tuple(dy.shape)} and {tuple(y.shape)} differ")
-    dx = torch.empty_like(dy) if dx is None else dx
+    y = _f32(y, "y", dy.device)
+    if mask is None:
+        raise TempoError(2, "mask: the forward's bit mask is required")
+    mask = _mask(mask, "mask", y.numel(), y.device)
+    dx = _out(dx, "dx", dy)
     check(lib().tempo_gelu_ip_bwd(_ptr(dy), _ptr(y), _ptr(mask), table.handle, _ptr(dx),
                                   y.numel(), _stream()))
     return dx
@@ -158,15 +199,19 @@ def layernorm_ip_fwd(x: torch.Tensor, gamma: torch.Tensor, beta: torch.Tensor,
                      eps: float = 1e-5, check_gamma: bool = True, y: torch.Tensor = None,
                      rstd: torch.Tensor = None, dev_status: torch.Tensor = None):
     """Returns (y, rstd).  Stash = y + rstd[row]."""
-    x, gamma, beta = _f32(x, "x"), _f32(gamma, "gamma"), _f32(beta, "beta")
+    x = _f32(x, "x")
+    gamma, beta = _f32(gamma, "gamma", x.device), _f32(beta, "beta", x.device)
     rows, cols = _rows_cols(x)
     if gamma.numel() != cols or beta.numel() != cols:
         raise TempoError(2, f"layernorm affine params {tuple(gamma.shape)}, {tuple(beta.shape)} "
                             f"do not match {tuple(x.shape)}")
     if check_gamma:
         ln_check_gamma(gamma)
-    y = torch.empty_like(x) if y is None else y
-    rstd = torch.empty(x.shape[:-1], dtype=torch.float32, device=x.device) if rstd is None else rstd
+    y = _out(y, "y", x)
+    rstd = torch.empty(x.shape[:-1], dtype=torch.float32, device=x.device) if rstd is None \
+        else _f32(rstd, "rstd", x.device, rows)
+    if dev_status is not None:
+        _dev(dev_status, "dev_status", torch.int32, x.device, 1)
     check(lib().tempo_ln_ip_fwd(_ptr(x), _ptr(gamma), _ptr(beta), float(eps), _ptr(y), _ptr(rstd),
                                 rows, cols, _ptr(dev_status), _stream()))
     return y, rstd
@@ -175,9 +220,16 @@ def layernorm_ip_fwd(x: torch.Tensor, gamma: torch.Tensor, beta: torch.Tensor,
 _ws_cache = {}
 
 
-def ln_workspace(rows: int, cols: int, device) -> torch.Tensor:
+def ln_workspace(rows: int, cols: int, device, stream=None) -> torch.Tensor:
+    """The LayerNorm backward's scratch (per-CTA fp64 partial rows).  Cached
+    per (device, STREAM, size): two backwards of the same shape running
+    concurrently on different streams must not share partial rows, while
+    work on one stream is ordered, so one buffer per stream is enough."""
     nbytes = int(lib().tempo_ln_ip_bwd_workspace_size(rows, cols))
-    key = (str(device), nbytes)
+    if stream is None:
+        with torch.cuda.device(device):
+            stream = torch.cuda.current_stream()
+    key = (str(device), int(stream.cuda_stream), nbytes)
     ws = _ws_cache.get(key)
     if ws is None:
         ws = torch.empty(max(nbytes, 16), dtype=torch.uint8, device=device)
@@ -185,19 +237,33 @@ def ln_workspace(rows: int, cols: int, device) -> torch.Tensor:
     return ws
 
 
+def _ln_bwd_args(dy, y, rstd, gamma, beta, dx, dgamma, dbeta, workspace):
+    dy = _f32(dy, "dy")
+    y = _f32(y, "y", dy.device, dy.numel())
+    rows, cols = _rows_cols(y)
+    rstd = _f32(rstd, "rstd", y.device, rows)
+    gamma = _f32(gamma, "gamma", y.device, cols)
+    beta = _f32(beta, "beta", y.device, cols)
+    dx = _out(dx, "dx", dy)
+    dgamma = _vec_out(dgamma, "dgamma", cols, y.device)
+    dbeta = _vec_out(dbeta, "dbeta", cols, y.device)
+    if workspace is None:
+        ws = ln_workspace(rows, cols, y.device)
+    else:
+        ws = _dev(workspace, "workspace", workspace.dtype, y.device)
+    nbytes = ws.numel() * ws.element_size()
+    return dy, y, rstd, gamma, beta, dx, dgamma, dbeta, ws, nbytes, rows, cols
+
+
 def layernorm_ip_bwd(dy: torch.Tensor, y: torch.Tensor, rstd: torch.Tensor,
                      gamma: torch.Tensor, beta: torch.Tensor, dx: torch.Tensor = None,
                      dgamma: torch.Tensor = None, dbeta: torch.Tensor = None,
                      workspace: torch.Tensor = None):
     """Returns (dx, dgamma, dbeta); dgamma/dbeta summed over all rows."""
-    dy, y = _f32(dy, "dy"), _f32(y, "y")
-    rows, cols = _rows_cols(y)
-    dx = torch.empty_like(dy) if dx is None else dx
-    dgamma = torch.empty(cols, dtype=torch.float32, device=y.device) if dgamma is None else dgamma
-    dbeta = torch.empty(cols, dtype=torch.float32, device=y.device) if dbeta is None else dbeta
-    ws = ln_workspace(rows, cols, y.device) if workspace is None else workspace
+    dy, y, rstd, gamma, beta, dx, dgamma, dbeta, ws, nbytes, rows, cols = _ln_bwd_args(
+        dy, y, rstd, gamma, beta, dx, dgamma, dbeta, workspace)
     check(lib().tempo_ln_ip_bwd(_ptr(dy), _ptr(y), _ptr(rstd), _ptr(gamma), _ptr(beta), _ptr(dx),
-                                _ptr(dgamma), _ptr(dbeta), _ptr(ws), ws.numel(), rows, cols,
+                                _ptr(dgamma), _ptr(dbeta), _ptr(ws), nbytes, rows, cols,
                                 _stream()))
     return dx, dgamma, dbeta
 
@@ -206,7 +272,7 @@ class _PeerStruct(C.Structure):
     """tempo_ln_peer_t (include/tempo_b200.h)."""
     _fields_ = [("rank", C.c_int32), ("world", C.c_int32),
                 ("inbox", C.c_void_p), ("flags", C.c_void_p),
-                ("epoch", C.c_uint32), ("status", C.c_void_p)]
+                ("epoch", C.c_uint32), ("status", C.c_void_p), ("timeout_ms", C.c_uint32)]
 
 
 class LnPeerRank:
@@ -229,6 +295,8 @@ class LnPeerRank:
             self.flags = self._alloc(self.flag_bytes)
         self.status = torch.zeros(1, dtype=torch.int32, device=device)
         self.epoch = 0
+        # bound on the wait for peers (0 = library default, 30 s)
+        self.timeout_ms = int(os.environ.get("TEMPO_PEER_TIMEOUT_MS", "0"))
         self._ptrs = None
         self._mapped = []
 
@@ -294,11 +362,14 @@ class LnPeerRank:
     def next_struct(self):
         self.epoch += 1
         return _PeerStruct(self.rank, self.world, self._ptrs[0].data_ptr(),
-                           self._ptrs[1].data_ptr(), self.epoch, self.status.data_ptr())
+                           self._ptrs[1].data_ptr(), self.epoch, self.status.data_ptr(),
+                           self.timeout_ms)
 
     def check_status(self):
+        """Raise if any exchange so far timed out (the status is sticky)."""
         if int(self.status.item()) != 0:
-            raise RuntimeError("peer exchange: a rank never arrived (TEMPO_ERR_STATE)")
+            raise TempoError(4, "peer exchange: a rank never arrived; dgamma/dbeta were "
+                                "poisoned with NaN and the group must be rebuilt")
 
     def close(self):
         L = lib()
@@ -311,8 +382,11 @@ def ln_param_reduce_peer(partials: torch.Tensor, cols: int, peer: "LnPeerRank",
                          dgamma: torch.Tensor = None, dbeta: torch.Tensor = None):
     """Stage 2 on fp64 partial rows [nparts][2*cols] + the cross-rank sum."""
     dev = partials.device
-    dgamma = torch.empty(cols, dtype=torch.float32, device=dev) if dgamma is None else dgamma
-    dbeta = torch.empty(cols, dtype=torch.float32, device=dev) if dbeta is None else dbeta
+    _dev(partials, "partials", torch.float64, dev)
+    if partials.dim() != 2 or partials.shape[1] != 2 * cols:
+        raise TempoError(2, f"partials: expected [nparts, {2 * cols}], got {tuple(partials.shape)}")
+    dgamma = _vec_out(dgamma, "dgamma", cols, dev)
+    dbeta = _vec_out(dbeta, "dbeta", cols, dev)
     st = peer.next_struct()
     check(lib().tempo_ln_param_reduce_peer(_ptr(partials), partials.shape[0], cols,
                                            C.byref(st), _ptr(dgamma), _ptr(dbeta), _stream()))
@@ -321,16 +395,18 @@ def ln_param_reduce_peer(partials: torch.Tensor, cols: int, peer: "LnPeerRank",
 
 def layernorm_ip_bwd_peer(dy, y, rstd, gamma, beta, peer: "LnPeerRank", dx=None, dgamma=None,
                           dbeta=None, workspace=None):
-    """layernorm_ip_bwd with dgamma/dbeta summed over every rank of ``peer``."""
-    dy, y = _f32(dy, "dy"), _f32(y, "y")
-    rows, cols = _rows_cols(y)
-    dx = torch.empty_like(dy) if dx is None else dx
-    dgamma = torch.empty(cols, dtype=torch.float32, device=y.device) if dgamma is None else dgamma
-    dbeta = torch.empty(cols, dtype=torch.float32, device=y.device) if dbeta is None else dbeta
-    ws = ln_workspace(rows, cols, y.device) if workspace is None else workspace
+    """layernorm_ip_bwd with dgamma/dbeta summed over every rank of ``peer``.
+    A rank that never arrives (bounded wait, ``peer.timeout_ms``) makes
+    ``peer.status`` nonzero (sticky) and the affected dgamma/dbeta NaN;
+    every later exchange of this rank then poisons its outputs without
+    waiting -- check ``peer.check_status()`` (bench.py checks every step)."""
+    dy, y, rstd, gamma, beta, dx, dgamma, dbeta, ws, nbytes, rows, cols = _ln_bwd_args(
+        dy, y, rstd, gamma, beta, dx, dgamma, dbeta, workspace)
+    if cols != peer.cols:
+        raise TempoError(2, f"peer exchange set up for {peer.cols} columns, got {cols}")
     st = peer.next_struct()
     check(lib().tempo_ln_ip_bwd_peer(_ptr(dy), _ptr(y), _ptr(rstd), _ptr(gamma), _ptr(beta),
-                                     _ptr(dx), _ptr(dgamma), _ptr(dbeta), _ptr(ws), ws.numel(),
+                                     _ptr(dx), _ptr(dgamma), _ptr(dbeta), _ptr(ws), nbytes,
                                      rows, cols, C.byref(st), _stream()))
     return dx, dgamma, dbeta
 
@@ -341,15 +417,16 @@ def layernorm_ip_bwd_peer(dy, y, rstd, gamma, beta, peer: "LnPeerRank", dx=None,
 def softmax_ip_fwd(z: torch.Tensor, P: torch.Tensor = None) -> torch.Tensor:
     z = _f32(z, "z")
     rows, cols = _rows_cols(z)
-    P = torch.empty_like(z) if P is None else P
+    P = _out(P, "P", z)
     check(lib().tempo_softmax_ip_fwd(_ptr(z), _ptr(P), rows, cols, _stream()))
     return P
 
 
 def softmax_ip_bwd(dP: torch.Tensor, P: torch.Tensor, dZ: torch.Tensor = None) -> torch.Tensor:
-    dP, P = _f32(dP, "dP"), _f32(P, "P")
+    P = _f32(P, "P")
+    dP = _f32(dP, "dP", P.device, P.numel())
     rows, cols = _rows_cols(P)
-    dZ = torch.empty_like(P) if dZ is None else dZ
+    dZ = _out(dZ, "dZ", P)
     check(lib().tempo_softmax_ip_bwd(_ptr(dP), _ptr(P), _ptr(dZ), rows, cols, _stream()))
     return dZ
 
@@ -366,11 +443,11 @@ def softmax_dropout_fwd(z: torch.Tensor, p: float, mask: torch.Tensor = None,
     if generate is None:
         generate = mask is None
     mode = MASK_PHILOX if generate else MASK_SUPPLIED
-    if mask is None:
-        mask = torch.empty(mask_words(z.numel()), dtype=torch.int32, device=z.device)
-    P = torch.empty_like(z) if P is None else P
-    if write_d and D is None:
-        D = torch.empty_like(z)
+    if mask is None and not generate:
+        raise TempoError(2, "mask: a supplied-mask forward needs the mask")
+    mask = _mask(mask, "mask", z.numel(), z.device)
+    P = _out(P, "P", z)
+    D = _out(D, "D", z) if write_d else None
     check(lib().tempo_softmax_dropout_fwd(_ptr(z), float(p), mode, _ptr(mask), int(seed),
                                           int(offset), _ptr(P), _ptr(D if write_d else None),
                                           rows, cols, _stream()))
@@ -381,11 +458,14 @@ def attn_probs_bwd(dD: torch.Tensor, P: torch.Tensor, mask: torch.Tensor, p: flo
                    write_d: bool = False, dZ: torch.Tensor = None, D: torch.Tensor = None):
     """Fused dropout bwd + output-only softmax bwd (+ recomputed D).
     Returns (dZ, D or None)."""
-    dD, P = _f32(dD, "dD"), _f32(P, "P")
+    P = _f32(P, "P")
+    dD = _f32(dD, "dD", P.device, P.numel())
     rows, cols = _rows_cols(P)
-    dZ = torch.empty_like(P) if dZ is None else dZ
-    if write_d and D is None:
-        D = torch.empty_like(P)
+    if mask is None:
+        raise TempoError(2, "mask: the forward's bit mask is required")
+    mask = _mask(mask, "mask", P.numel(), P.device)
+    dZ = _out(dZ, "dZ", P)
+    D = _out(D, "D", P) if write_d else None
     check(lib().tempo_attn_probs_bwd(_ptr(dD), _ptr(P), _ptr(mask), float(p), _ptr(dZ),
                                      _ptr(D if write_d else None), rows, cols, _stream()))
     return dZ, (D if write_d else None)
@@ -402,9 +482,10 @@ def dropout_fwd(x: torch.Tensor, p: float, mask: torch.Tensor = None, seed: int 
     if generate is None:
         generate = mask is None
     mode = MASK_PHILOX if generate else MASK_SUPPLIED
-    if mask is None:
-        mask = torch.empty(mask_words(x.numel()), dtype=torch.int32, device=x.device)
-    y = torch.empty_like(x) if y is None else y
+    if mask is None and not generate:
+        raise TempoError(2, "mask: a supplied-mask forward needs the mask")
+    mask = _mask(mask, "mask", x.numel(), x.device)
+    y = _out(y, "y", x)
     check(lib().tempo_dropout_fwd(_ptr(x), float(p), mode, _ptr(mask), int(seed), int(offset),
                                   _ptr(y), x.numel(), _stream()))
     return y, mask
@@ -413,7 +494,10 @@ def dropout_fwd(x: torch.Tensor, p: float, mask: torch.Tensor = None, seed: int 
 def dropout_bwd(dy: torch.Tensor, mask: torch.Tensor, p: float,
                 dx: torch.Tensor = None) -> torch.Tensor:
     dy = _f32(dy, "dy")
-    dx = torch.empty_like(dy) if dx is None else dx
+    if mask is None:
+        raise TempoError(2, "mask: the forward's bit mask is required")
+    mask = _mask(mask, "mask", dy.numel(), dy.device)
+    dx = _out(dx, "dx", dy)
     check(lib().tempo_dropout_bwd(_ptr(dy), _ptr(mask), float(p), _ptr(dx), dy.numel(),
                                   _stream()))
     return dx
@@ -424,13 +508,16 @@ def dropout_bwd(dy: torch.Tensor, mask: torch.Tensor, p: float,
 # --------------------------------------------------------------------------
 def pack_mask(bytes_: torch.Tensor, dev_status: torch.Tensor = None) -> torch.Tensor:
     """BoolMask bytes (uint8 CUDA tensor) -> packed bits."""
-    b = bytes_.contiguous()
+    b = _dev(bytes_, "bytes", torch.uint8)
     bits = torch.empty(mask_words(b.numel()), dtype=torch.int32, device=b.device)
+    if dev_status is not None:
+        _dev(dev_status, "dev_status", torch.int32, b.device, 1)
     check(lib().tempo_mask_pack(_ptr(b), _ptr(bits), b.numel(), _ptr(dev_status), _stream()))
     return bits
 
 
 def unpack_mask(bits: torch.Tensor, n: int) -> torch.Tensor:
+    bits = _mask(bits, "bits", int(n), bits.device)
     out = torch.empty(n, dtype=torch.uint8, device=bits.device)
     check(lib().tempo_mask_unpack(_ptr(bits), _ptr(out), int(n), _stream()))
     return out
@@ -452,8 +539,7 @@ def bernoulli_keep_bits_device(n: int, p: float, seed: int, offset: int = 0,
     for bit, by jump-ahead): keep bits of elements [offset, offset + n) as
     ceil(n/32) int32 words.  offset must be a multiple of 32."""
     dev = device or (out.device if out is not None else torch.device("cuda", torch.cuda.current_device()))
-    if out is None:
-        out = torch.empty(mask_words(n), dtype=torch.int32, device=dev)
+    out = _mask(out, "out", int(n), dev)
     nbytes = int(lib().tempo_bernoulli_keep_bits_workspace_size(int(offset), int(n)))
     ws = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=dev)
     check(lib().tempo_bernoulli_keep_bits(int(n), float(p), int(seed), int(offset), _ptr(out),

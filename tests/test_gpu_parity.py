@@ -271,6 +271,25 @@ def test_layernorm_refusals(tops, cuda):
     assert e.value.kind == "ParamError"
 
 
+@pytest.mark.parametrize("offset", [1e2, 1e3, 1e4, -3e3])
+@pytest.mark.parametrize("rows,cols", [(64, 1024), (48, 768), (16, 1000), (8, 1536), (4, 2052)])
+def test_layernorm_forward_large_mean(tops, port, cuda, rows, cols, offset):
+    """Rows with |mean| >> std: the reference sums in fp64 and stores
+    float(mean) (kernels.cpp:165-176), so the row mean must be that rounding,
+    not an fp32 tree sum's (which drifts by several ulps of the mean and puts
+    y 1e-4 off at |mean|/std = 1000)."""
+    import torch
+    g = np.random.default_rng(int(abs(offset)) + cols)
+    x = (g.standard_normal((rows, cols)) + offset).astype(np.float32)
+    gam = (1 + 0.2 * g.standard_normal(cols)).astype(np.float32)
+    bet = (0.1 * g.standard_normal(cols)).astype(np.float32)
+    y, rstd = tops.layernorm_ip_fwd(to_dev(x, cuda), to_dev(gam, cuda), to_dev(bet, cuda))
+    torch.cuda.synchronize()
+    ry, rrs, _ = port.ln_fwd(x, gam, bet, 1e-5)
+    assert rel_err(y.cpu().numpy(), ry) <= 1e-5
+    assert np.abs(rstd.cpu().numpy().astype(np.float64) / rrs - 1).max() <= 1e-6
+
+
 # ------------------------------------------------- softmax + attention dropout
 @pytest.mark.parametrize("rows,cols", [(1, 512), (24, 512), (7, 384), (9, 1024), (5, 100),
                                        (3, 77), (12 * 512, 512), (10, 128), (6, 256), (5, 768),
@@ -338,6 +357,87 @@ def test_softmax_accuracy_margin(tops, port, cuda, scale):
     big = rP > 1e-30
     rel = np.abs(P.cpu().numpy() - rP)[big] / rP[big]
     assert float(rel.max()) <= 1e-6, float(rel.max())
+
+
+def _masked_scores(rows, cols, fill, frac, seed):
+    """randn*3 scores with a fraction `frac` of each row set to `fill` (the
+    attention-mask values HF / the reference's users put in: -inf,
+    finfo(float32).min, -1e4); row 0 fully masked when frac == 1."""
+    g = np.random.default_rng(seed)
+    z = (g.standard_normal((rows, cols)) * 3).astype(np.float32)
+    if frac > 0:
+        k = int(round(frac * cols))
+        for r in range(rows):
+            z[r, g.permutation(cols)[:k]] = fill
+    return z
+
+
+def _close_nan(a, b, rtol, atol):
+    """|a-b| <= rtol*|b| + atol where b is finite; NaN exactly where b is NaN."""
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    if not np.array_equal(np.isnan(a), np.isnan(b)):
+        return False
+    f = ~np.isnan(b)
+    return bool(np.all(np.abs(a[f] - b[f]) <= rtol * np.abs(b[f]) + atol))
+
+
+@pytest.mark.parametrize("fill", [-np.inf, float(np.finfo(np.float32).min), -1e4])
+@pytest.mark.parametrize("frac", [0.0, 0.5, 1.0])
+@pytest.mark.parametrize("rows,cols", [(64, 512), (9, 1024), (5, 100)])
+def test_softmax_masked_scores(tops, port, cuda, rows, cols, fill, frac):
+    """Masked attention scores (ops_reference.cpp:104-145): exp of a masked
+    score is 0, a row of finfo.min / -1e4 is uniform, a row of -inf is NaN
+    (the reference's -inf - -inf), and no NaN leaks into partly masked rows.
+    P, D and dZ match the oracle with NaN exactly where it has NaN."""
+    import torch
+    z = _masked_scores(rows, cols, fill, frac, rows + cols + int(frac * 10))
+    p = 0.1
+    bits = tops.bernoulli_keep_bits(rows * cols, p, 99)
+    keep = port.bernoulli_keep(rows * cols, p, 99)
+    mask = bits_to_dev(bits, cuda)
+    P, D, _ = tops.softmax_dropout_fwd(to_dev(z, cuda), p, mask=mask)
+    Pp = tops.softmax_ip_fwd(to_dev(z, cuda))
+    torch.cuda.synchronize()
+    rP = port.softmax_fwd(z)
+    Pg = P.cpu().numpy()
+    assert _close_nan(Pg, rP, 1e-5, 1e-9)
+    assert np.array_equal(Pp.cpu().numpy(), Pg, equal_nan=True)  # plain == fused P
+    rD = port.dropout_apply(Pg, keep, p).reshape(rows, cols)
+    assert np.array_equal(D.cpu().numpy(), rD, equal_nan=True)
+    g = np.random.default_rng(5)
+    dD = g.standard_normal((rows, cols)).astype(np.float32)
+    dZ, Drec = tops.attn_probs_bwd(to_dev(dD, cuda), P, mask, p, write_d=True)
+    torch.cuda.synchronize()
+    rdZ = port.softmax_bwd(port.dropout_apply(dD, keep, p).reshape(rows, cols), Pg)
+    assert _close_nan(dZ.cpu().numpy(), rdZ, 1e-5, 1e-8)
+    assert np.array_equal(Drec.cpu().numpy(), D.cpu().numpy(), equal_nan=True)
+
+
+def test_softmax_special_rows(tops, port, cuda):
+    """Rows with NaN (anywhere -> whole row NaN), +inf (NaN row), a single
+    finite score among -inf (P = 1 there), and huge logits (z - max
+    overflowing): all as the oracle."""
+    import torch
+    cols = 512
+    inf, nan, big = np.inf, np.nan, float(np.finfo(np.float32).max)
+    rows = []
+    r = np.zeros(cols, np.float32); r[7] = nan; rows.append(r)
+    r = np.zeros(cols, np.float32); r[0] = nan; rows.append(r)
+    r = np.zeros(cols, np.float32); r[3] = inf; rows.append(r)
+    r = np.full(cols, -inf, np.float32); r[100] = 2.0; rows.append(r)
+    r = np.full(cols, -big, np.float32); r[5] = big; rows.append(r)
+    r = np.linspace(-100, 0, cols).astype(np.float32); rows.append(r)
+    r = np.full(cols, 3e38, np.float32); r[::2] = -3e38; rows.append(r)
+    z = np.stack(rows)
+    P = tops.softmax_ip_fwd(to_dev(z, cuda))
+    torch.cuda.synchronize()
+    assert _close_nan(P.cpu().numpy(), port.softmax_fwd(z), 1e-5, 1e-9)
+    # the generic (non-vector) kernel: 500 columns
+    z2 = np.ascontiguousarray(z[:, :500])
+    P2 = tops.softmax_ip_fwd(to_dev(z2, cuda))
+    torch.cuda.synchronize()
+    assert _close_nan(P2.cpu().numpy(), port.softmax_fwd(z2), 1e-5, 1e-9)
 
 
 @pytest.mark.parametrize("rows,cols", [(4, 512), (3, 130)])

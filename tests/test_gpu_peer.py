@@ -65,15 +65,57 @@ def test_peer_reduce_is_the_fixed_order_sum(tops, cuda, world, cols, nparts):
 
 
 def test_peer_reduce_missing_rank_times_out(tops, cuda):
-    """A rank that never arrives: the kernel gives up after a bounded wait,
-    reports TEMPO_ERR_STATE and returns (no hung GPU)."""
+    """A rank that never arrives: the kernel gives up after the bounded wait
+    (peer.timeout_ms), reports TEMPO_ERR_STATE and writes NaN -- not a
+    partial sum -- to dgamma/dbeta (no hung GPU, nothing silently wrong).
+    The status is sticky: later exchanges on that rank poison their outputs
+    at once without waiting."""
+    import time
     import torch
     ranks = tops.LnPeerRank.local_group(2, 32, cuda)
-    parts = torch.zeros((1, 64), dtype=torch.float64, device=cuda)
-    tops.ln_param_reduce_peer(parts, 32, ranks[0])  # rank 1 never runs
+    for r in ranks:
+        r.timeout_ms = 200
+    parts = torch.ones((1, 64), dtype=torch.float64, device=cuda)
+    dg, db = tops.ln_param_reduce_peer(parts, 32, ranks[0])  # rank 1 never runs
     torch.cuda.synchronize()
-    with pytest.raises(RuntimeError):
+    with pytest.raises(tops.TempoError) as e:
         ranks[0].check_status()
+    assert e.value.kind == "StateError"
+    assert torch.isnan(dg).all() and torch.isnan(db).all()
+    t0 = time.perf_counter()
+    dg2, db2 = tops.ln_param_reduce_peer(parts, 32, ranks[0])  # sticky: no wait, NaN
+    torch.cuda.synchronize()
+    assert time.perf_counter() - t0 < 0.15
+    assert torch.isnan(dg2).all() and torch.isnan(db2).all()
+
+
+def test_concurrent_layernorm_backwards_on_two_streams(tops, cuda):
+    """Two LayerNorm backwards of the same shape running concurrently on two
+    streams with the DEFAULT workspace: each stream gets its own scratch
+    (ops.ln_workspace is keyed by stream), so both equal the serial result
+    bit for bit."""
+    import torch
+    rows, cols = 2048, 1024
+    g = np.random.default_rng(11)
+    mk = lambda *s: torch.from_numpy(g.standard_normal(s).astype(np.float32)).to(cuda)  # noqa: E731
+    gam = (1 + 0.2 * mk(cols)).contiguous()
+    bet = (0.1 * mk(cols)).contiguous()
+    ins = []
+    for _ in range(2):
+        y, rs = tops.layernorm_ip_fwd(mk(rows, cols), gam, bet)
+        ins.append((mk(rows, cols), y, rs))
+    want = [tops.layernorm_ip_bwd(dy, y, rs, gam, bet) for dy, y, rs in ins]
+    torch.cuda.synchronize()
+    for _ in range(5):
+        streams = [torch.cuda.Stream() for _ in range(2)]
+        got = []
+        for (dy, y, rs), st in zip(ins, streams):
+            with torch.cuda.stream(st):
+                got.append(tops.layernorm_ip_bwd(dy, y, rs, gam, bet))
+        torch.cuda.synchronize()
+        for w, o in zip(want, got):
+            for a, b in zip(w, o):
+                assert torch.equal(a, b)
 
 
 def test_sharded_layernorm_backward(tops, cuda):
