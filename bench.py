@@ -1,8 +1,8 @@
 """bench.py -- Tempo in-place activation operators on B200.
 
 One "step" = forward + backward of the Tempo activation-operator chain of one
-BERT-large encoder layer (BASELINE.json configs[3]: B=64 per GPU, S=512,
-H=1024, A=16, p=0.1), in encoder order (proj/src/encoder.cpp:155-210):
+BERT-large encoder layer (BASELINE.json configs[3]: B=64, S=512, H=1024,
+A=16, p=0.1), in encoder order (proj/src/encoder.cpp:155-210):
 
   fwd: softmax+dropout_recompute [B*A*S, S] -> attn-out dropout [T,H] ->
        LayerNorm1 [T,H] -> GELU [T,4H] -> ffn dropout [T,H] -> LayerNorm2 [T,H]
@@ -11,14 +11,20 @@ H=1024, A=16, p=0.1), in encoder order (proj/src/encoder.cpp:155-210):
   (+ at N>1: one NCCL all-reduce of the bucketed LN dgamma/dbeta, 4H floats)
 
 GEMMs and residual adds are outside the path and are
-replaced by synthetic fp32 buffers of the layer shapes.  Scaling is weak:
-every rank runs B=64 rows, so N=8 is configs[4] (B=512 sharded 8 ways).
+replaced by synthetic fp32 buffers of the layer shapes.
+
+N=1: configs[3] (B=64).  N>1 (`--gpus N`; run under torchrun, or bench.py
+re-launches itself as N ranks): configs[4] strong scaling by default -- the
+global batch of 512 sequences split by rows, 512/N per rank (SURVEY 8e);
+`--scaling weak` keeps B=64 per rank instead.
 
 metric: fwd+bwd GB/s = algorithmic HBM bytes of the chain (SURVEY 8d:
 GELU 8.125+12.125 B/elem, LN 8NM+4N+8M / 12NM+4N+16M, attention 12.125 +
 16.125 B/elem, dropouts 8.125+8.125 B/elem) / device time, summed over ranks.
 
 Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                       [--scaling strong|weak] [--global-batch 512] [--masks philox|reference]
+       TEMPO_BENCH_BACKEND=gloo python bench.py --gpus 2   # N>1 functional run on one GPU
 """
 from __future__ import annotations
 
@@ -37,6 +43,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 B, S, H, A, P_DROP = 64, 512, 1024, 16, 0.1
+GLOBAL_B_STRONG = 512    # configs[4]: B=512 sharded by rows over the N GPUs
 T = B * S                # tokens per rank
 ATT_ROWS = B * A * S     # attention-probability rows per rank
 METRIC = "fwd+bwd GB/s per op vs B200 HBM peak at 1/2/4/8 GPU; activation bytes/layer"
@@ -122,33 +129,53 @@ def peaks():
 
 
 # ------------------------------------------------------------ the chain
+def _numel(shapes):
+    n = 0
+    for shp in shapes.values():
+        k = 1
+        for d in shp:
+            k *= d
+        n += k
+    return n
+
+
 class Chain:
     """Device buffers + the step of the Tempo op chain (weak-scaled rank)."""
     peer = None  # ops.LnPeerRank at N>1: the fused dgamma/dbeta exchange
 
-    def __init__(self, dev, rank, world, seed=1234):
+    def __init__(self, dev, rank, world, seed=1234, batch=B):
         import torch
         from paper_2210_10246_b200 import ops
         self.ops, self.torch, self.dev = ops, torch, dev
         self.rank, self.world = rank, world
+        self.batch = batch
+        T, ATT_ROWS = batch * S, batch * A * S  # this rank's token / attention rows
+        self.T, self.ATT_ROWS = T, ATT_ROWS
         g = torch.Generator(device=dev)
         g.manual_seed(seed + rank)
-        rn = lambda *s: torch.randn(*s, device=dev, generator=g)  # noqa: E731
         self.table = ops.GeluTable.default()
-        # forward inputs (GEMM outputs in the real layer: synthetic here)
-        self.z = rn(ATT_ROWS, S)            # attention scores
-        self.x_attn_out = rn(T, H)          # attention output projection
-        self.x_ffn1 = rn(T, 4 * H)          # first FFN linear output
-        self.x_ffn2 = rn(T, H)              # second FFN linear output
+        # The per-step inputs (GEMM outputs / input-gradients in the real
+        # layer: synthetic here) live in ONE contiguous buffer and the per-step
+        # results in another, so the e2e measurement moves each set with one
+        # copy and double-buffers with a single extra set.
+        shapes_in = {"z": (ATT_ROWS, S),            # attention scores
+                     "x_attn_out": (T, H),          # attention output projection
+                     "x_ffn1": (T, 4 * H),          # first FFN linear output
+                     "x_ffn2": (T, H),              # second FFN linear output
+                     "dy_ln2": (T, H), "dy_gelu": (T, 4 * H), "dy_ln1": (T, H),
+                     "dD": (ATT_ROWS, S)}
+        shapes_out = {"dZ": (ATT_ROWS, S), "dx_d1": (T, H), "dx_g": (T, 4 * H),
+                      "dx_d2": (T, H), "dparams": (4 * H,)}  # [dg2, db2, dg1, db1]
+        self.shapes_in, self.shapes_out = shapes_in, shapes_out
+        self.in_buf = torch.empty(_numel(shapes_in), device=dev)
+        self.in_buf.normal_(generator=g)
+        self.out_buf = torch.zeros(_numel(shapes_out), device=dev)
+        self.bind(self.in_buf, self.out_buf)
+        rn = lambda *s: torch.randn(*s, device=dev, generator=g)  # noqa: E731
         self.g1 = (1 + 0.2 * rn(H)).contiguous()
         self.b1 = (0.1 * rn(H)).contiguous()
         self.g2 = (1 + 0.2 * rn(H)).contiguous()
         self.b2 = (0.1 * rn(H)).contiguous()
-        # backward seeds (GEMM input-gradients in the real layer)
-        self.dy_ln2 = rn(T, H)
-        self.dy_gelu = rn(T, 4 * H)
-        self.dy_ln1 = rn(T, H)
-        self.dD = rn(ATT_ROWS, S)
         # outputs / stashes, allocated once
         e = torch.empty_like
         mw = lambda n: torch.empty(ops.mask_words(n), dtype=torch.int32, device=dev)  # noqa: E731
@@ -158,11 +185,9 @@ class Chain:
         self.y_g, self.m_g = e(self.x_ffn1), mw(T * 4 * H)
         self.d2, self.m2 = e(self.x_ffn2), mw(T * H)
         self.y_ln2, self.rs2 = e(self.x_ffn2), torch.empty(T, device=dev)
-        self.dx_ln2, self.dx_d2 = e(self.x_ffn2), e(self.x_ffn2)
-        self.dx_g = e(self.x_ffn1)
-        self.dx_ln1, self.dx_d1 = e(self.x_attn_out), e(self.x_attn_out)
-        self.dZ, self.Drec = e(self.z), e(self.z)
-        self.dparams = torch.zeros(4 * H, device=dev)  # [dg2, db2, dg1, db1] bucket
+        self.dx_ln2 = e(self.x_ffn2)
+        self.dx_ln1 = e(self.x_attn_out)
+        self.Drec = e(self.z)
         self.ws = ops.ln_workspace(T, H, dev)
         self.status = torch.zeros(1, dtype=torch.int32, device=dev)
         self.step_idx = 0
@@ -170,6 +195,16 @@ class Chain:
         # global element offsets: rank shards reproduce the unsharded masks
         self.off_att = rank * ATT_ROWS * S
         self.off_h = rank * T * H
+
+    def bind(self, in_buf, out_buf):
+        """Point the step's inputs / results at views of one input buffer and
+        one result buffer."""
+        for shapes, buf in ((self.shapes_in, in_buf), (self.shapes_out, out_buf)):
+            o = 0
+            for name, shp in shapes.items():
+                n = _numel({name: shp})
+                setattr(self, name, buf[o:o + n].view(shp))
+                o += n
 
     def retained_bytes(self):
         """Bytes held between forward and backward by this chain (the stash):
@@ -188,6 +223,7 @@ class Chain:
         main = torch.cuda.current_stream()
         if not hasattr(self, "_mask_streams"):  # one stream per mask: they overlap
             self._mask_streams = [torch.cuda.Stream() for _ in range(3)]
+        T, ATT_ROWS = self.T, self.ATT_ROWS
         for site, (m, n, off) in enumerate([(self.m_att, ATT_ROWS * S, self.off_att),
                                             (self.m1, T * H, self.off_h),
                                             (self.m2, T * H, self.off_h)]):
@@ -238,6 +274,25 @@ class Chain:
         o.dropout_bwd(self.dx_ln1, self.m1, P_DROP, dx=self.dx_d1)
         o.attn_probs_bwd(self.dD, self.P, self.m_att, P_DROP, write_d=True, dZ=self.dZ,
                          D=self.Drec)
+
+    def poll_peer_status(self, final=False):
+        """Surface a timed-out dgamma/dbeta exchange every step without a host
+        sync: the device status word (sticky: once a peer failed to arrive it
+        stays nonzero and later exchanges NaN-poison their outputs) is copied
+        to pinned memory on the stream each step and the host reads the last
+        landed value; `final` synchronises and checks the exact value."""
+        if self.peer is None:
+            return
+        torch = self.torch
+        if not hasattr(self, "_status_host"):
+            self._status_host = torch.zeros(1, dtype=torch.int32, pin_memory=True)
+        if final:
+            torch.cuda.synchronize()
+            self.peer.check_status()
+            return
+        if int(self._status_host[0]) != 0:
+            self.peer.check_status()
+        self._status_host.copy_(self.peer.status, non_blocking=True)
 
     def step(self, allreduce=None):
         self.step_idx += 1
@@ -346,61 +401,62 @@ def cpu_model() -> str:
     return "unknown"
 
 
-def cpu_reference_sample(frac_rows: int, threads: int, steps: int, warmup: int):
+def cpu_reference_sample(frac_rows: int, threads: int, steps: int, warmup: int, batch=B):
     """The reference's own CPU implementation (oracle/_ref/libtempo_ref.so,
-    compiled from /root/reference/proj/src) of the same chain on a bounded
-    row sample: 1/frac_rows of one rank's rows of every op, sharded across
-    `threads` host threads (one reference Graph per thread; distinct tapes may
-    run concurrently).  Returns (GB/s, seconds per step, sample)."""
+    compiled from /root/reference/proj/src) of the same chain: 1/frac_rows of
+    one rank's rows of every op (frac_rows = 1: the whole configs[3] step),
+    sharded across `threads` host threads, each running the reference's own
+    Graphs / Tape::backward on its rows (distinct tapes may run concurrently,
+    SPEC.md:154).  Inputs and masks are built once per thread by the
+    reference's own generators outside the timed region (ref_chain_create);
+    a timed step copies nothing in or out.  Returns (GB/s, s/step, sample)."""
     import oracle
     ref = oracle.Ref()
     table = open(os.path.join(ROOT, "tests", "golden", "gelu_table_default_v1.txt")).read()
-    g = np.random.default_rng(0)
-    t_rows = T // frac_rows                # token rows of the sample
-    a_rows = ATT_ROWS // frac_rows         # attention rows of the sample
-    work = []  # per-thread closures
-    for k in range(threads):
-        tr = slice(k * t_rows // threads, (k + 1) * t_rows // threads)
-        ar = slice(k * a_rows // threads, (k + 1) * a_rows // threads)
-        nt, na = tr.stop - tr.start, ar.stop - ar.start
-        x_g = g.standard_normal(nt * 4 * H).astype(np.float32)
-        dy_g = g.standard_normal(nt * 4 * H).astype(np.float32)
-        x_ln = g.standard_normal((nt, H)).astype(np.float32)
-        dy_ln = g.standard_normal((nt, H)).astype(np.float32)
-        gam = (1 + 0.2 * g.standard_normal(H)).astype(np.float32)
-        bet = (0.1 * g.standard_normal(H)).astype(np.float32)
-        z = g.standard_normal((na, S)).astype(np.float32)
-        dD = g.standard_normal((na, S)).astype(np.float32)
-        keep_a = ref.bernoulli_keep(na * S, P_DROP, 11 + k)
-        keep_h = ref.bernoulli_keep(nt * H, P_DROP, 13 + k)
-        x_h = g.standard_normal(nt * H).astype(np.float32)
+    t_rows = batch * S // frac_rows        # token rows of the sample
+    a_rows = batch * A * S // frac_rows    # attention rows of the sample
+    handles = [None] * threads
 
-        def job(x_g=x_g, dy_g=dy_g, x_ln=x_ln, dy_ln=dy_ln, gam=gam, bet=bet, z=z, dD=dD,
-                keep_a=keep_a, keep_h=keep_h, x_h=x_h):
-            ref.softmax_dropout(z, keep_a, P_DROP, dD)          # fwd + bwd + recompute D
-            for _ in range(2):
-                ref.dropout(x_h, keep_h, P_DROP, x_h)           # hidden dropouts fwd + bwd
-                ref.layernorm_ip(x_ln, gam, bet, dy_ln)          # both LNs fwd + bwd
-            ref.gelu_ip(table, x_g, dy_g)                       # GELU fwd + bwd
-        work.append(job)
+    def create(k):
+        nt = (k + 1) * t_rows // threads - k * t_rows // threads
+        na = (k + 1) * a_rows // threads - k * a_rows // threads
+        handles[k] = ref.chain_create(table, P_DROP, na, S, nt, H, 1000 + k)
 
-    def run_step():
-        ths = [threading.Thread(target=w) for w in work]
+    def run_all(fn):
+        ths = [threading.Thread(target=fn, args=(k,)) for k in range(threads)]
         for t in ths:
             t.start()
         for t in ths:
             t.join()
 
-    for _ in range(warmup):
-        run_step()
-    t0 = time.perf_counter()
-    for _ in range(steps):
-        run_step()
-    dt = (time.perf_counter() - t0) / steps
-    nbytes = sum(op_bytes().values()) / frac_rows
-    sample = (f"1/{frac_rows} of the per-GPU chain rows ({t_rows} tokens, {a_rows} attention "
-              f"rows; {nbytes / 1e9:.3f} GB algorithmic) per step, {threads} threads")
+    run_all(create)
+    try:
+        run = lambda k: ref.chain_run(handles[k])  # noqa: E731
+        for _ in range(warmup):
+            run_all(run)
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            run_all(run)
+        dt = (time.perf_counter() - t0) / steps
+    finally:
+        for h in handles:
+            if h:
+                ref.chain_destroy(h)
+    nbytes = sum(op_bytes(batch).values()) / frac_rows
+    what = ("the whole per-GPU chain" if frac_rows == 1 else f"1/{frac_rows} of the per-GPU chain rows")
+    sample = (f"{what} ({t_rows} tokens, {a_rows} attention rows; {nbytes / 1e9:.3f} GB "
+              f"algorithmic) per step, {threads} threads, inputs built outside the timed region")
     return nbytes / dt / 1e9, dt, sample
+
+
+def reference_frac(steps: int, warmup: int, budget_steps: int = 40) -> int:
+    """Row fraction of the reference arm's step: the whole chain (1) while
+    steps + warmup full steps (~2.5 s each on 16 host threads) fit the time
+    budget, else the smallest power of two that brings them under it."""
+    f = 1
+    while (steps + warmup) / f > budget_steps and f < 512:
+        f *= 2
+    return f
 
 
 # ---------------------------------------------------------------- main
@@ -415,11 +471,28 @@ def main():
     ap.add_argument("--masks", default="philox", choices=["philox", "reference"],
                     help="dropout masks: in-kernel Philox (default) or the reference's own "
                          "std::mt19937_64 streams generated on the device every step")
+    ap.add_argument("--scaling", default=None, choices=["strong", "weak"],
+                    help="N>1: strong (default; configs[4], --global-batch rows split N ways) "
+                         "or weak (B=64 per rank)")
+    ap.add_argument("--global-batch", type=int, default=GLOBAL_B_STRONG,
+                    help="strong scaling: global batch split across the ranks (configs[4]: 512)")
     args = ap.parse_args()
 
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return relaunch(args.gpus)  # one process per GPU, as the driver's torchrun would
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.gpus != world and rank == 0:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}; measuring {world} ranks",
+              file=sys.stderr)
+    scaling = args.scaling or ("strong" if world > 1 else "weak")
+    if scaling == "strong" and world > 1:
+        if args.global_batch % world:
+            raise SystemExit(f"--global-batch {args.global_batch} does not split over {world} ranks")
+        batch = args.global_batch // world
+    else:
+        batch = B
 
     if args.impl == "reference":
         return main_reference(args, rank, world)
@@ -437,7 +510,7 @@ def main():
             dist.init_process_group("nccl", device_id=dev)
         else:
             dist.init_process_group(backend)
-    chain = Chain(dev, rank, world)
+    chain = Chain(dev, rank, world, batch=batch)
     chain.mask_mode = args.masks
     from paper_2210_10246_b200.dist import allreduce_ln_params
     allreduce = allreduce_ln_params if world > 1 else None
@@ -472,24 +545,26 @@ def main():
     e0.record(st)
     for _ in range(args.steps):
         chain.step(allreduce)
+        chain.poll_peer_status()  # a timed-out exchange fails the run at the next step
     e1.record(st)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     clk = clocks.stop()
+    chain.poll_peer_status(final=True)
     ms = e0.elapsed_time(e1) / args.steps
     if world > 1:
         t = torch.tensor([ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
 
-    per_rank_bytes = sum(op_bytes().values())
+    per_rank_bytes = sum(op_bytes(batch).values())
     value = per_rank_bytes * world / (ms * 1e-3) / 1e9
     peak, peak_kind = peaks()
 
     # ---- per-op device times (outside the timed region) -------------------
     per_op = chain.per_op_timings(reps=11, flush=flush)
-    ob, oe = op_bytes(), op_elements()
+    ob, oe = op_bytes(batch), op_elements(batch)
     per_op_rows = []
     for name, (t_ms, mult) in per_op.items():
         gbs = ob[name] / (t_ms * 1e-3) / 1e9
@@ -515,7 +590,7 @@ def main():
     # ---- the reference mask stream on the device (outside the timed region) --
     ref_mask = None
     if rank == 0:
-        n_att = ATT_ROWS * S
+        n_att = chain.ATT_ROWS * S
         chain.ops.bernoulli_keep_bits_device(n_att, P_DROP, 7, out=chain.m_att)  # tables + warm-up
         ts = []
         for _ in range(3):
@@ -559,7 +634,7 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
             threads = len(os.sched_getaffinity(0))
-            v, dt, sample = cpu_reference_sample(frac_rows=32, threads=threads, steps=2, warmup=1)
+            v, dt, sample = cpu_reference_sample(frac_rows=1, threads=threads, steps=2, warmup=1)
             v1, dt1, _ = cpu_reference_sample(frac_rows=512, threads=1, steps=1, warmup=0)
             cpu = {"value": round(v, 4), "unit": "GB/s", "cores": threads, "kind": "reference",
                    "sample": sample, "s_per_step": round(dt, 3), "cpu_model": cpu_model(),
@@ -573,16 +648,19 @@ def main():
         line = {
             "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "f32",
             "data": ("synthetic (torch.randn inputs of the layer shapes; " +
                      ("Philox dropout masks)" if args.masks == "philox" else
                       "the reference's mt19937_64 dropout masks, generated on the device "
                       "every step)")),
-            "config": {"workload": WORKLOAD, "batch_per_gpu": B, "global_batch": B * world,
+            "config": {"workload": WORKLOAD, "batch_per_gpu": batch, "global_batch": batch * world,
                        "seq_len": S, "hidden": H, "heads": A, "dropout_p": P_DROP,
                        "parallelism": f"rows{world}", "collective": collective,
-                       "l2": "working set 12.7 GB/step >> 126 MB L2",
-                       "baseline_config": "configs[3] at N=1; configs[4] (B=512) at N=8"},
+                       "l2": f"working set {per_rank_bytes / 1e9:.1f} GB/step per GPU >> 126 MB L2",
+                       "baseline_config": ("configs[3] (B=64, one GPU)" if world == 1 else
+                                           f"configs[4]: global B={batch * world} row-sharded "
+                                           f"over {world} GPUs" if scaling == "strong" else
+                                           f"weak: B={batch} per GPU")},
             "roofline": roofline,
             "cpu_baseline": cpu,
             "e2e": e2e,
@@ -594,13 +672,33 @@ def main():
             "clocks": clk,
             "per_op": per_op_rows,
             "frac_of_peak": round(value / world / peak, 4),
-            "elements_per_s": {"value": round(sum(op_elements().values()) * world / (ms * 1e-3) / 1e9, 2),
+            "elements_per_s": {"value": round(sum(op_elements(batch).values()) * world / (ms * 1e-3) / 1e9, 2),
                                "unit": "Gelem/s", "what": "elements streamed by all ops of the chain"},
             "stash": stash_report(chain),
         }
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def free_port() -> int:
+    import socket
+    s_ = socket.socket()
+    s_.bind(("127.0.0.1", 0))
+    p = s_.getsockname()[1]
+    s_.close()
+    return p
+
+
+def relaunch(n):
+    """`bench.py --gpus N` outside torchrun: re-run this command as N ranks
+    (torch.distributed.run, one process per GPU, rendezvous on 127.0.0.1);
+    rank 0 prints the JSON line."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={n}", "--master-addr=127.0.0.1", f"--master-port={free_port()}",
+           os.path.abspath(__file__)] + sys.argv[1:]
+    r = subprocess.run(cmd)
+    sys.exit(r.returncode)
 
 
 def stash_report(chain):
@@ -613,6 +711,7 @@ def stash_report(chain):
     # what the reference keeps for the SAME ops (memory_model.cpp:31-65): scores,
     # probs, dropped-out map + 1-byte mask; both LN inputs + outputs; GELU input
     # + output; 1-byte hidden dropout masks
+    T, ATT_ROWS = chain.T, chain.ATT_ROWS
     ref_same = (3 * 4 + 1) * ATT_ROWS * S + 4 * (4 * T * H) + 2 * 4 * T * 4 * H + 2 * T * H
     return {"unit": "bytes/layer", "tokens": T,
             "reference_layer": ref_tok * T, "tempo_1byte_masks_layer": tmp1_tok * T,
@@ -626,32 +725,17 @@ def e2e_measure(chain, args, world, allreduce, dist):
     copies its inputs from pinned host memory (H2D) and reads every result
     back (D2H) inside the timed region.  Inputs and results each live in ONE
     contiguous pinned host buffer and ONE contiguous device buffer per set
-    (views per tensor), so a step is one H2D and one D2H copy; both are
-    double-buffered: step i+1's inputs upload while step i computes and step
-    i-1's results download, so the step costs about the PCIe time of its
-    copies (full duplex) rather than their sum plus compute."""
+    (Chain.bind views), so a step is one H2D and one D2H copy; both are
+    double-buffered (set 0 = the chain's own buffers, set 1 one extra pair):
+    step i+1's inputs upload while step i computes and step i-1's results
+    download, so the step costs about the PCIe time of its copies (full
+    duplex) rather than their sum plus compute."""
     torch = chain.torch
-    names_in = ["z", "x_attn_out", "x_ffn1", "x_ffn2", "dy_ln2", "dy_gelu", "dy_ln1", "dD"]
-    names_out = ["dZ", "dx_d1", "dx_g", "dx_d2", "dparams"]
-    orig = {n: getattr(chain, n) for n in names_in + names_out}
-
-    def views(buf, names):
-        out, o = {}, 0
-        for n in names:
-            t = orig[n]
-            out[n] = buf[o:o + t.numel()].view(t.shape)
-            o += t.numel()
-        return out
-
-    n_in = sum(orig[n].numel() for n in names_in)
-    n_out = sum(orig[n].numel() for n in names_out)
-    d_in = [torch.empty(n_in, device=chain.dev) for _ in range(2)]
-    d_out = [torch.empty(n_out, device=chain.dev) for _ in range(2)]
-    in_sets = [views(b, names_in) for b in d_in]
-    out_sets = [views(b, names_out) for b in d_out]
+    n_in, n_out = chain.in_buf.numel(), chain.out_buf.numel()
+    d_in = [chain.in_buf, torch.empty(n_in, device=chain.dev)]
+    d_out = [chain.out_buf, torch.empty(n_out, device=chain.dev)]
     h_in = torch.empty(n_in, dtype=torch.float32, pin_memory=True)
-    for n, v in views(h_in, names_in).items():
-        v.copy_(orig[n])
+    h_in.copy_(chain.in_buf)
     h_out = [torch.empty(n_out, dtype=torch.float32, pin_memory=True) for _ in range(2)]
     bi, bo = n_in * 4, n_out * 4
     comp = torch.cuda.current_stream()
@@ -674,10 +758,7 @@ def e2e_measure(chain, args, world, allreduce, dist):
         j = i % 2
         comp.wait_event(ev_in[j])
         comp.wait_event(ev_out[j])  # results of step i-2 (same output set) downloaded
-        for n in names_in:
-            setattr(chain, n, in_sets[j][n])
-        for n in names_out:
-            setattr(chain, n, out_sets[j][n])
+        chain.bind(d_in[j], d_out[j])
         chain.step(allreduce)
         ev_used[j].record(comp)
         ev_done[j].record(comp)
@@ -704,14 +785,14 @@ def e2e_measure(chain, args, world, allreduce, dist):
         comp.wait_event(ev_out[j])
     e1.record(comp)
     torch.cuda.synchronize()
-    for n, t in orig.items():  # restore the chain's own buffers
-        setattr(chain, n, t)
+    chain.bind(chain.in_buf, chain.out_buf)  # back to the chain's own buffers
+    del d_in, d_out
     ms = e0.elapsed_time(e1) / k
     if dist is not None:
         t = torch.tensor([ms], device=chain.dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-    v = sum(op_bytes().values()) * world / (ms * 1e-3) / 1e9
+    v = sum(op_bytes(chain.batch).values()) * world / (ms * 1e-3) / 1e9
     return {"value": round(v, 2), "unit": "GB/s", "h2d_bytes_per_step": int(bi),
             "d2h_bytes_per_step": int(bo), "ms_per_step": round(ms, 3), "steps": k,
             "overlap": "one H2D (step i+1) || compute (step i) || one D2H (step i-1); "
@@ -721,21 +802,27 @@ def e2e_measure(chain, args, world, allreduce, dist):
 def main_reference(args, rank, world):
     """--impl reference: the reference's own CPU implementation of the path
     (oracle/_ref, compiled from /root/reference/proj/src) on the host cores,
-    same metric/config/unit; each step a bounded sample (1/32 of one rank's
-    rows).  Under torchrun only rank 0 runs."""
+    same metric/config/unit.  Each step is the whole per-GPU chain when
+    steps + warmup full steps fit a few minutes (reference_frac), else a
+    stated row fraction.  Under torchrun only rank 0 runs."""
     if rank != 0:
         return
+    scaling = args.scaling or ("strong" if world > 1 else "weak")
+    batch = args.global_batch // world if (scaling == "strong" and world > 1) else B
     threads = len(os.sched_getaffinity(0))
-    v, dt, sample = cpu_reference_sample(frac_rows=32, threads=threads, steps=args.steps,
-                                         warmup=max(1, min(args.warmup, 2)))
+    frac = reference_frac(args.steps, args.warmup)
+    v, dt, sample = cpu_reference_sample(frac_rows=frac, threads=threads, steps=args.steps,
+                                         warmup=args.warmup, batch=batch)
     line = {
         "metric": METRIC, "value": round(v, 4), "unit": "GB/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dt * 1e3, 2),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic", "impl": "reference",
-        "config": {"workload": WORKLOAD, "batch_per_gpu": B, "global_batch": B * world,
+        "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (the reference's Tensor::randn inputs, BoolMask::bernoulli_keep masks)",
+        "impl": "reference", "same_config": frac == 1,
+        "config": {"workload": WORKLOAD, "batch_per_gpu": batch, "global_batch": batch * world,
                    "seq_len": S, "hidden": H, "heads": A, "dropout_p": P_DROP,
-                   "parallelism": f"rows{world}"},
+                   "parallelism": f"rows{world}",
+                   "sample_rows": f"1/{frac} of one GPU's rows" if frac > 1 else "all of one GPU's rows"},
         "cpu_baseline": {"value": round(v, 4), "unit": "GB/s", "cores": threads,
                          "kind": "reference", "sample": sample, "cpu_model": cpu_model()},
         "e2e": {"value": round(v, 4), "unit": "GB/s", "h2d_bytes_per_step": 0,

@@ -248,6 +248,10 @@ class Ref:
         L.ref_memory_model.argtypes = [_i64, _i64, _i64, _i64, C.POINTER(_i64), C.POINTER(_i64),
                                        C.POINTER(_i64)]
         L.ref_ledger_bytes.argtypes = [C.c_int, _i64, _i64, C.c_char_p, C.POINTER(_i64)]
+        L.ref_chain_create.argtypes = [C.c_char_p, C.c_double, _i64, _i64, _i64, _i64, C.c_uint64]
+        L.ref_chain_create.restype = C.c_void_p
+        L.ref_chain_run.argtypes = [C.c_void_p]
+        L.ref_chain_destroy.argtypes = [C.c_void_p]
 
     def _check(self, rc: int) -> None:
         if rc:
@@ -256,6 +260,23 @@ class Ref:
     @staticmethod
     def _ptr(a):
         return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+    def chain_create(self, table_text: str, p: float, att_rows: int, seq: int, tokens: int,
+                     hidden: int, seed: int):
+        """bench.py's reference arm: one shard of the layer op chain with its
+        inputs built once by the reference's own generators (ref_harness.cpp
+        ref_chain_create).  Returns an opaque handle for chain_run."""
+        h = self.L.ref_chain_create(table_text.encode(), p, att_rows, seq, tokens, hidden, seed)
+        if not h:
+            raise OracleError(1, self.L.ref_last_error().decode())
+        return h
+
+    def chain_run(self, h) -> None:
+        """One forward + Tape::backward of the chain shard (the timed step)."""
+        self._check(self.L.ref_chain_run(h))
+
+    def chain_destroy(self, h) -> None:
+        self.L.ref_chain_destroy(h)
 
     def fit_table_default(self) -> str:
         n = _i64()

@@ -334,4 +334,96 @@ int ref_ledger_bytes(int op, std::int64_t rows, std::int64_t cols,
     });
 }
 
+// ---------------------------------------------------------------------------
+// The bench's reference arm: one rank-shard of the BERT-large layer's Tempo
+// op chain (bench.py Chain, encoder.cpp:155-210 order) run through the
+// reference's own builders and Tape::backward.  ref_chain_create builds the
+// inputs ONCE, outside the timed region, with the reference's own synthetic
+// generators (Tensor::randn, tensor.cpp:71-77; BoolMask::bernoulli_keep,
+// tensor.cpp:186-203) and parses the table once; ref_chain_run is the timed
+// step: four tapes (softmax -> dropout_recompute; hidden dropout -> LN1;
+// GELU; hidden dropout -> LN2), each forward + Tape::backward, plus the
+// consumer's recompute of D (recompute rule "dropout-rescale",
+// ops_tempo.cpp:17-26).  Nothing is copied in or out per step.
+struct RefChain {
+    GeluPolyTable table;
+    double p;
+    Tensor z, dD, x1, x2, xg, dyg, dy1, dy2, g1, b1, g2, b2;
+    BoolMask ka, k1, k2;
+};
+
+void* ref_chain_create(const char* table_text, double p, std::int64_t att_rows,
+                       std::int64_t seq, std::int64_t tokens, std::int64_t hidden,
+                       std::uint64_t seed) {
+    RefChain* c = nullptr;
+    int rc = guarded([&] {
+        c = new RefChain{GeluPolyTable::parse_string(table_text), p};
+        Shape sa{att_rows, seq}, sh{tokens, hidden}, sg{tokens, 4 * hidden};
+        std::uint64_t s = seed * 64;
+        c->z = Tensor::randn(sa, s + 1, Dtype::F32);
+        c->dD = Tensor::randn(sa, s + 2, Dtype::F32);
+        c->x1 = Tensor::randn(sh, s + 3, Dtype::F32);
+        c->x2 = Tensor::randn(sh, s + 4, Dtype::F32);
+        c->xg = Tensor::randn(sg, s + 5, Dtype::F32);
+        c->dyg = Tensor::randn(sg, s + 6, Dtype::F32);
+        c->dy1 = Tensor::randn(sh, s + 7, Dtype::F32);
+        c->dy2 = Tensor::randn(sh, s + 8, Dtype::F32);
+        Tensor n1 = Tensor::randn({hidden}, s + 9, Dtype::F64);
+        Tensor n2 = Tensor::randn({hidden}, s + 10, Dtype::F64);
+        c->g1 = Tensor::zeros({hidden}, Dtype::F32);
+        c->g2 = Tensor::zeros({hidden}, Dtype::F32);
+        c->b1 = Tensor::zeros({hidden}, Dtype::F32);
+        c->b2 = Tensor::zeros({hidden}, Dtype::F32);
+        for (std::int64_t j = 0; j < hidden; ++j) {
+            c->g1.set(j, 1 + 0.2 * n1.get(j));
+            c->g2.set(j, 1 - 0.2 * n2.get(j));
+            c->b1.set(j, 0.1 * n2.get(j));
+            c->b2.set(j, 0.1 * n1.get(j));
+        }
+        c->ka = BoolMask::bernoulli_keep(sa, p, s + 11);
+        c->k1 = BoolMask::bernoulli_keep(sh, p, s + 12);
+        c->k2 = BoolMask::bernoulli_keep(sh, p, s + 13);
+    });
+    if (rc != 0) {
+        delete c;
+        return nullptr;
+    }
+    return c;
+}
+
+int ref_chain_run(void* handle) {
+    return guarded([&] {
+        RefChain& c = *static_cast<RefChain*>(handle);
+        {   // attention probabilities: softmax -> dropout_recompute, backward
+            Graph g;
+            NodeId zn = g.leaf(c.z, "z");
+            NodeId pn = tempo_ops::softmax(g, zn, "probs");
+            NodeId dn = tempo_ops::dropout_recompute(g, pn, c.p, c.ka, "drop", "drop_mask");
+            GradientMap gm = g.tape.backward(dn, c.dD);
+            Tensor d_rec = dropout_apply(g.value(pn), c.ka, c.p);  // the dV GEMM's recompute
+            (void)gm.at(zn);
+        }
+        for (int k = 0; k < 2; ++k) {  // hidden dropout -> LayerNorm, backward
+            Graph g;
+            NodeId xn = g.leaf(k ? c.x2 : c.x1, "x");
+            NodeId dn = ref_ops::dropout(g, xn, c.p, k ? c.k2 : c.k1, "d", "d_mask");
+            NodeId gn = g.param(k ? c.g2 : c.g1, "gamma");
+            NodeId bn = g.param(k ? c.b2 : c.b1, "beta");
+            NodeId yn = tempo_ops::layernorm(g, dn, gn, bn, 1e-5, "y", "y_rstd");
+            GradientMap gm = g.tape.backward(yn, k ? c.dy2 : c.dy1);
+            (void)gm.at(xn);
+        }
+        {   // GELU, backward
+            Graph g;
+            NodeId xn = g.leaf(c.xg, "x");
+            NodeId yn = tempo_ops::gelu(g, xn, &c.table, "y", "y_mask");
+            GradientMap gm = g.tape.backward(yn, c.dyg);
+            (void)gm.at(xn);
+        }
+    });
+}
+
+void ref_chain_destroy(void* handle) { delete static_cast<RefChain*>(handle); }
+
 }  // extern "C"
+

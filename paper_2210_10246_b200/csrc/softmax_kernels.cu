@@ -54,13 +54,24 @@ __device__ __forceinline__ float warp_max_nan(float v) {
     for (int o = 16; o > 0; o >>= 1) v = fmax_nan(v, __shfl_xor_sync(kFull, v, o));
     return v;
 }
-// Elements with z - max below -128 (masked scores: -inf, finfo(f32).min,
-// or a +inf max) give exactly 0, as the reference's double exp does to
-// within its float rounding (e^-128 < 2^-149).  The select also discards
-// the NaN that the exponent split / TwoSum produce from infinite operands.
-// A row whose max is NaN or -inf (NaN anywhere, or all -inf) then sums to 0
-// and P = 0 * (1/0) = NaN for the whole row -- the reference's result too.
-constexpr float kExpCut = -128.0f;
+// Masked scores (-inf, finfo(f32).min, anything with z - max below the
+// fp32 exp range) must give exactly 0, as the reference's double exp does
+// (ops_reference.cpp:111-118).  There ex2 gives e = 0 while the exponent
+// split / TwoSum terms of an infinite or overflowed (z - max) are NaN or
+// inf, so the result is formed by ONE saturating FMA, r = sat(e + e*corr):
+// .sat maps NaN to +0 and r <= 1 holds anyway (z <= max), so a masked
+// element costs no extra instruction.  The NaN rows of the reference (NaN
+// anywhere, a +inf score, or an all -inf row: exp(inf - inf)) are exactly
+// the rows whose NaN-propagating max is not finite; they get 1/sum = NaN
+// once per row.
+__device__ __forceinline__ float fma_sat(float a, float b, float c) {
+    float r;
+    asm("fma.rn.sat.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+    return r;
+}
+__device__ __forceinline__ float row_inv(float sum, float mx) {
+    return isfinite(mx) ? 1.0f / sum : __int_as_float(0x7fffffff);
+}
 __device__ __forceinline__ float ex2_approx_ftz(float f) {
     float r;
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(f));
@@ -78,18 +89,17 @@ __device__ __forceinline__ float exp_shift(float z, float mx) {
 #if TM_SOFTMAX_TWOSUM
     const float bb = d - z;
     const float err = (z - (d - bb)) + (-mx - bb);  // TwoSum: (z - mx) = d + err exactly
-    const float r = fmaf(e, fmaf(wl, 0.69314718055994531f, err), e);
+    return fma_sat(e, fmaf(wl, 0.69314718055994531f, err), e);
 #else
-    const float r = fmaf(e, wl * 0.69314718055994531f, e);
+    return fma_sat(e, wl * 0.69314718055994531f, e);
 #endif
 #else
     float d = z - mx;
     float bb = d - z;
     float err = (z - (d - bb)) + (-mx - bb);  // TwoSum: (z - mx) = d + err exactly
     float e = expf(d);
-    const float r = fmaf(e, err, e);
+    return fma_sat(e, err, e);
 #endif
-    return d >= kExpCut ? r : 0.0f;
 }
 
 // exp_shift for two elements on the packed fp32x2 pipe (FADD2/FMUL2/FFMA2):
@@ -113,11 +123,12 @@ __device__ __forceinline__ float2 exp_shift2(float2 z, float mx) {
     const float2 t1 = __fadd2_rn(d, make_float2(-bb.x, -bb.y));
     const float2 err = __fadd2_rn(__fadd2_rn(z, make_float2(-t1.x, -t1.y)),
                                   __fadd2_rn(NMX, make_float2(-bb.x, -bb.y)));
-    const float2 r = __ffma2_rn(e, __ffma2_rn(wl, LN2, err), e);
+    const float2 c = __ffma2_rn(wl, LN2, err);
 #else
-    const float2 r = __ffma2_rn(e, __fmul2_rn(wl, LN2), e);
+    const float2 c = __fmul2_rn(wl, LN2);
 #endif
-    return make_float2(d.x >= kExpCut ? r.x : 0.0f, d.y >= kExpCut ? r.y : 0.0f);
+    // the final FMA per lane with .sat (no packed .sat form): see fma_sat
+    return make_float2(fma_sat(e.x, c.x, e.x), fma_sat(e.y, c.y, e.y));
 #else
     return make_float2(exp_shift(z.x, mx), exp_shift(z.y, mx));
 #endif
@@ -176,7 +187,7 @@ __global__ void __launch_bounds__(kBlock) softmax_fwd_vec_kernel(
 #endif
                 acc += (v[i][k].x + v[i][k].y) + (v[i][k].z + v[i][k].w);
             }
-            inv[i] = 1.0f / warp_sumf(acc);
+            inv[i] = row_inv(warp_sumf(acc), mx);
         }
 #pragma unroll
         for (int i = 0; i < R; ++i) {
@@ -297,7 +308,7 @@ __global__ void __launch_bounds__(kBlock) softmax_fwd_generic_kernel(
         mx = warp_max_nan(mx);
         double acc = 0.0;
         for (int64_t j = lane; j < C; j += 32) acc += (double)exp_shift(zr[j], mx);
-        const double inv = 1.0 / warp_sum(acc);
+        const double inv = isfinite(mx) ? 1.0 / warp_sum(acc) : __longlong_as_double(0x7ff8000000000000ll);
         for (int64_t j = lane; j < C; j += 32) {
             const int64_t i = r * C + j;
             float p = (float)((double)exp_shift(zr[j], mx) * inv);
