@@ -142,6 +142,7 @@ def _numel(shapes):
 class Chain:
     """Device buffers + the step of the Tempo op chain (weak-scaled rank)."""
     peer = None  # ops.LnPeerRank at N>1: the fused dgamma/dbeta exchange
+    kernel_events = None  # list: CUDA event pairs around attn_probs_bwd in each step
 
     def __init__(self, dev, rank, world, seed=1234, batch=B):
         import torch
@@ -272,8 +273,15 @@ class Chain:
         if allreduce is not None:
             allreduce(dp)  # the one collective: bucketed LN dgamma/dbeta (16 KB)
         o.dropout_bwd(self.dx_ln1, self.m1, P_DROP, dx=self.dx_d1)
+        ev = self.kernel_events
+        if ev is not None:  # in-chain duration of the dominant kernel (roofline)
+            ev.append((self.torch.cuda.Event(enable_timing=True),
+                       self.torch.cuda.Event(enable_timing=True)))
+            ev[-1][0].record()
         o.attn_probs_bwd(self.dD, self.P, self.m_att, P_DROP, write_d=True, dZ=self.dZ,
                          D=self.Drec)
+        if ev is not None:
+            ev[-1][1].record()
 
     def poll_peer_status(self, final=False):
         """Surface a timed-out dgamma/dbeta exchange every step without a host
@@ -306,9 +314,14 @@ class Chain:
     # levels the rank-0 offsets touch, keep = 6; three masks
     REF_MASK_LAUNCHES = 18
 
-    def per_op_timings(self, reps, flush):
+    def per_op_timings(self, reps, flush, flush_dirty=None):
         """Per-kernel device time (CUDA events on the launching stream, L2
-        flushed before every rep), for the roofline and the per-op table."""
+        flushed before every rep), for the roofline and the per-op table.
+        `flush` evicts L2 by READING a buffer larger than L2 (the timed op
+        starts with its inputs out of L2 and no foreign dirty lines to write
+        back -- the op's own traffic, as ncu's cache-controlled replay sees
+        it); `flush_dirty` (optional, reported beside it) WRITES such a
+        buffer, so the op also pays the write-back of ~126 MB of dirty lines."""
         torch, o = self.torch, self.ops
         dp = self.dparams
         H_ = H
@@ -331,17 +344,127 @@ class Chain:
             fn()
             if reps == 0:
                 continue
-            ts = []
-            for _ in range(reps):
-                flush()
-                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                a.record(st)
-                fn()
-                b.record(st)
-                b.synchronize()
-                ts.append(a.elapsed_time(b))
-            out[name] = (trimmed_mean(ts) * mult.get(name, 1), mult.get(name, 1))
+            res = []
+            for fl in (flush, flush_dirty):
+                if fl is None:
+                    res.append(None)
+                    continue
+                ts = []
+                for _ in range(reps):
+                    fl()
+                    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    a.record(st)
+                    fn()
+                    b.record(st)
+                    b.synchronize()
+                    ts.append(a.elapsed_time(b))
+                res.append(trimmed_mean(ts) * mult.get(name, 1))
+            out[name] = (res[0], mult.get(name, 1), res[1])
         return out
+
+
+# ------------------------------------------------ configs[0..2] at their shapes
+def per_config_timings(dev, peak, reps=40):
+    """BASELINE configs[0..2], each op pair (forward + backward) at its own
+    shape, captured in ONE CUDA graph (the launch-bound small case needs it)
+    and replayed with L2 cold -- a 512 MB read before every replay evicts the
+    inputs without leaving dirty lines for the timed op to write back -- and
+    L2 warm (back-to-back replays).  GB/s = algorithmic bytes /
+    device time (CUDA events on the capture/replay stream)."""
+    import torch
+    from paper_2210_10246_b200 import ops
+    g = torch.Generator(device=dev)
+    g.manual_seed(77)
+    rn = lambda *s_: torch.randn(*s_, device=dev, generator=g)  # noqa: E731
+    mw = lambda n: torch.empty(ops.mask_words(n), dtype=torch.int32, device=dev)  # noqa: E731
+    table = ops.GeluTable.default()
+    out = []
+
+    # configs[0]: In-Place GELU fwd+bwd, BERT-base FFN activation [8*128, 3072]
+    x1, dy1 = rn(1024, 3072), rn(1024, 3072)
+    y1, m1, dx1 = torch.empty_like(x1), mw(x1.numel()), torch.empty_like(x1)
+    n1 = x1.numel()
+
+    def cfg1():
+        ops.gelu_ip_fwd(x1, table, y=y1, mask=m1)
+        ops.gelu_ip_bwd(dy1, y1, m1, table, dx=dx1)
+
+    # configs[1]: In-Place LayerNorm fwd+bwd incl. dgamma/dbeta, [32*512, 768]
+    R2, C2 = 32 * 512, 768
+    x2, dy2 = rn(R2, C2), rn(R2, C2)
+    ga2, be2 = (1 + 0.2 * rn(C2)).contiguous(), (0.1 * rn(C2)).contiguous()
+    y2, rs2, dx2 = torch.empty_like(x2), torch.empty(R2, device=dev), torch.empty_like(x2)
+    dg2, db2 = torch.empty(C2, device=dev), torch.empty(C2, device=dev)
+    ws2 = torch.empty(max(16, int(ops.lib().tempo_ln_ip_bwd_workspace_size(R2, C2))),
+                      dtype=torch.uint8, device=dev)
+
+    def cfg2():
+        ops.layernorm_ip_fwd(x2, ga2, be2, check_gamma=False, y=y2, rstd=rs2)
+        ops.layernorm_ip_bwd(dy2, y2, rs2, ga2, be2, dx=dx2, dgamma=dg2, dbeta=db2, workspace=ws2)
+
+    # configs[2]: softmax + dropout recompute (p=0.1) fwd, attn-probs bwd (+D for dV)
+    R3 = 32 * 12 * 512
+    z3, dD3 = rn(R3, 512), rn(R3, 512)
+    P3, D3, m3 = torch.empty_like(z3), torch.empty_like(z3), mw(z3.numel())
+    dZ3, Dr3 = torch.empty_like(z3), torch.empty_like(z3)
+    n3 = z3.numel()
+
+    def cfg3():
+        ops.softmax_dropout_fwd(z3, P_DROP, mask=m3, generate=True, seed=5, P=P3, D=D3)
+        ops.attn_probs_bwd(dD3, P3, m3, P_DROP, write_d=True, dZ=dZ3, D=Dr3)
+
+    bits = 1.0 / 8
+    cases = [
+        ("configs[0] gelu fwd+bwd [1024,3072]", cfg1, n1 * (8 + bits + 12 + bits), n1,
+         n1 * 4 * 3),
+        ("configs[1] layernorm fwd+bwd [16384,768]", cfg2,
+         (8 * R2 * C2 + 4 * R2 + 8 * C2) + (12 * R2 * C2 + 4 * R2 + 16 * C2), R2 * C2,
+         R2 * C2 * 4 * 2),
+        ("configs[2] softmax+dropout fwd, attn-probs bwd [196608,512]", cfg3,
+         n3 * (12 + bits + 16 + bits), n3, n3 * 4 * 2),
+    ]
+    flush_buf = torch.empty(512 * 1024 * 1024 // 4, device=dev).fill_(1.0)
+    flush_out = torch.empty((), device=dev)
+    st_side = torch.cuda.Stream()
+    for name, fn, nbytes, nelem, in_bytes in cases:
+        fn()
+        torch.cuda.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(st_side):
+            with torch.cuda.graph(graph, stream=st_side):
+                fn()
+        torch.cuda.synchronize()
+        st = torch.cuda.current_stream()
+        cold, warm = [], []
+        for _ in range(reps):
+            torch.sum(flush_buf, dim=0, out=flush_out)  # read-only eviction of L2
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(st)
+            graph.replay()
+            b.record(st)
+            b.synchronize()
+            cold.append(a.elapsed_time(b))
+        graph.replay()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(st)
+        for _ in range(reps):
+            graph.replay()
+        b.record(st)
+        b.synchronize()
+        warm_ms = a.elapsed_time(b) / reps
+        cold_ms = trimmed_mean(cold)
+        gbs = nbytes / (cold_ms * 1e-3) / 1e9
+        out.append({"config": name, "ms": round(cold_ms, 4), "bytes": int(nbytes),
+                    "gbs": round(gbs, 1), "frac": round(gbs / peak, 4),
+                    "gelem_per_s": round(nelem / (cold_ms * 1e-3) / 1e9, 2),
+                    "l2": "cold (512 MB read before each replay)", "launches": 2,
+                    "cuda_graph": True,
+                    "l2_warm": {"ms": round(warm_ms, 4),
+                                "gbs": round(nbytes / (warm_ms * 1e-3) / 1e9, 1),
+                                "note": ("inputs L2-resident (back-to-back replays)"
+                                         if in_bytes < 100e6 else "working set > L2")}})
+        del graph
+    return out
 
 
 # ------------------------------------------------------------ clocks
@@ -474,6 +597,8 @@ def main():
     ap.add_argument("--scaling", default=None, choices=["strong", "weak"],
                     help="N>1: strong (default; configs[4], --global-batch rows split N ways) "
                          "or weak (B=64 per rank)")
+    ap.add_argument("--configs-only", action="store_true",
+                    help="time only BASELINE configs[0..2] at their own shapes (for ncu)")
     ap.add_argument("--global-batch", type=int, default=GLOBAL_B_STRONG,
                     help="strong scaling: global batch split across the ranks (configs[4]: 512)")
     args = ap.parse_args()
@@ -510,6 +635,9 @@ def main():
             dist.init_process_group("nccl", device_id=dev)
         else:
             dist.init_process_group(backend)
+    if args.configs_only:
+        print(json.dumps({"per_config": per_config_timings(dev, peaks()[0], reps=args.steps)}))
+        return
     chain = Chain(dev, rank, world, batch=batch)
     chain.mask_mode = args.masks
     from paper_2210_10246_b200.dist import allreduce_ln_params
@@ -524,8 +652,10 @@ def main():
             allreduce = None
         collective = ("fused peer-memory exchange in the LN backward stage 2"
                       if chain.peer is not None else f"{backend} all_reduce of the dgamma/dbeta bucket")
-    flush_buf = torch.empty(256 * 1024 * 1024 // 4, device=dev)
-    flush = lambda: flush_buf.fill_(0.0)  # noqa: E731  (256 MB > 126 MB L2)
+    flush_buf = torch.empty(512 * 1024 * 1024 // 4, device=dev).fill_(1.0)
+    flush_out = torch.empty((), device=dev)
+    flush = lambda: torch.sum(flush_buf, dim=0, out=flush_out)  # noqa: E731  (read 512 MB >> L2)
+    flush_dirty = lambda: flush_buf[:256 * 1024 * 1024 // 4].fill_(0.0)  # noqa: E731
 
     for _ in range(max(args.warmup, 3)):
         chain.step(allreduce)
@@ -563,29 +693,53 @@ def main():
     peak, peak_kind = peaks()
 
     # ---- per-op device times (outside the timed region) -------------------
-    per_op = chain.per_op_timings(reps=11, flush=flush)
+    per_op = chain.per_op_timings(reps=11, flush=flush, flush_dirty=flush_dirty)
     ob, oe = op_bytes(batch), op_elements(batch)
     per_op_rows = []
-    for name, (t_ms, mult) in per_op.items():
+    for name, (t_ms, mult, t_dirty) in per_op.items():
         gbs = ob[name] / (t_ms * 1e-3) / 1e9
         per_op_rows.append({"op": name, "ms": round(t_ms, 4), "bytes": int(ob[name]),
                             "gbs": round(gbs, 1), "frac": round(gbs / peak, 4),
                             "elements": int(oe[name]),
                             "gelem_per_s": round(oe[name] / (t_ms * 1e-3) / 1e9, 2),
-                            "launches": mult})
-    top = max(per_op_rows, key=lambda r: r["ms"])
-    roofline = {"bound": "hbm", "kernel": top["op"], "achieved": top["gbs"], "peak": peak,
-                "unit": "GB/s", "frac": top["frac"], "traffic": None,
+                            "launches": mult, "l2": "cold, clean (512 MB read before each rep)",
+                            "after_dirty_flush": {
+                                "ms": round(t_dirty, 4),
+                                "frac": round(ob[name] / (t_dirty * 1e-3) / 1e9 / peak, 4),
+                                "l2": "256 MB written before each rep: the op also writes back "
+                                      "~126 MB of foreign dirty lines"}})
+    # the dominant kernel's duration inside the running chain: the timed
+    # steps again with CUDA events around attn_probs_bwd on its stream (a
+    # separate pass, so the events cannot perturb the headline region)
+    chain.kernel_events = []
+    for _ in range(args.steps):
+        chain.step(allreduce)
+    torch.cuda.synchronize()
+    in_chain = [a.elapsed_time(b) for a, b in chain.kernel_events]
+    chain.kernel_events = None
+    k_ms = sum(in_chain) / len(in_chain)
+    k_bytes = op_bytes(batch)["attn_probs_bwd"]
+    k_gbs = k_bytes / (k_ms * 1e-3) / 1e9
+    roofline = {"bound": "hbm", "kernel": "attn_probs_bwd", "achieved": round(k_gbs, 1),
+                "peak": peak, "unit": "GB/s", "frac": round(k_gbs / peak, 4), "traffic": None,
                 "peak_kind": f"{peak_kind} copy bandwidth (MEASURED_PEAKS.json hbm_gbs)",
-                "bytes_per_launch": top["bytes"], "per_unit": "see DESIGN.md (SURVEY 8d)"}
+                "bytes_per_launch": int(k_bytes), "ms_per_launch": round(k_ms, 4),
+                "timing": f"CUDA events around the kernel in each of {len(in_chain)} chain steps",
+                "share_of_step": round(k_ms / ms, 4),
+                "isolated": {"ms": next(r["ms"] for r in per_op_rows if r["op"] == "attn_probs_bwd"),
+                             "frac": next(r["frac"] for r in per_op_rows if r["op"] == "attn_probs_bwd")},
+                "per_unit": "16.125 B/element: dD, P (4+4) + mask bit + dZ, D (4+4); SURVEY 8d"}
     prof_traffic = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(prof_traffic):
+    if os.path.exists(prof_traffic) and batch == B:  # captured at the configs[3] shapes
         try:
-            tr = json.load(open(prof_traffic)).get(top["op"])
+            tr = json.load(open(prof_traffic)).get("attn_probs_bwd")
             if tr:
                 roofline["traffic"] = tr
         except Exception:
             pass
+
+    # ---- configs[0..2] at their own shapes (outside the timed region) -------
+    per_config = per_config_timings(dev, peak) if rank == 0 else None
 
     # ---- the reference mask stream on the device (outside the timed region) --
     ref_mask = None
@@ -671,6 +825,7 @@ def main():
             "cpp_api": cpp_api,
             "clocks": clk,
             "per_op": per_op_rows,
+            "per_config": per_config,
             "frac_of_peak": round(value / world / peak, 4),
             "elements_per_s": {"value": round(sum(op_elements(batch).values()) * world / (ms * 1e-3) / 1e9, 2),
                                "unit": "Gelem/s", "what": "elements streamed by all ops of the chain"},
