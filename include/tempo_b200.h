@@ -165,6 +165,21 @@ int tempo_ln_param_reduce_peer(const double* partials, int64_t nparts, int64_t c
 /* Exchange buffers: a dedicated, zero-filled cudaMalloc allocation (an IPC
  * handle always maps the START of an allocation, so sub-allocations of a
  * caching allocator cannot be shared this way). */
+/* NCCL fallback of the same sum for callers without P2P / IPC peers
+ * (SURVEY 8b tempo_allreduce_ln_params): every rank's bucket of LayerNorm
+ * dgamma/dbeta (e.g. [dg2 | db2 | dg1 | db1], 2*cols floats per LN, as
+ * written by tempo_ln_ip_bwd) is summed in place over the ranks of
+ * `nccl_comm` (an ncclComm_t) on `stream` -- the reference's single-process
+ * dgamma/dbeta (ops_tempo.cpp:150-151) summed over row shards.  NCCL is
+ * loaded at first use (dlopen "libnccl.so.2"); TEMPO_ERR_UNSUPPORTED if it
+ * is absent.  The comm helpers build a communicator from a 128-byte
+ * ncclUniqueId that the caller distributes (any out-of-band channel). */
+int tempo_allreduce_ln_params(void* nccl_comm, float* bucket, int64_t count,
+                              tempo_stream_t stream);
+int tempo_nccl_unique_id(void* id128);
+int tempo_nccl_comm_init(int32_t world, int32_t rank, const void* id128, void** comm);
+int tempo_nccl_comm_destroy(void* comm);
+
 int tempo_peer_alloc(size_t bytes, void** dev_ptr);
 int tempo_peer_free(void* dev_ptr);
 /* CUDA IPC plumbing for the inbox/flag buffers of other processes:

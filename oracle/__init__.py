@@ -31,6 +31,7 @@ _f32p = np.ctypeslib.ndpointer(np.float32, flags="C_CONTIGUOUS")
 _f64p = np.ctypeslib.ndpointer(np.float64, flags="C_CONTIGUOUS")
 _u8p = np.ctypeslib.ndpointer(np.uint8, flags="C_CONTIGUOUS")
 _u64p = np.ctypeslib.ndpointer(np.uint64, flags="C_CONTIGUOUS")
+_u32p = np.ctypeslib.ndpointer(np.uint32, flags="C_CONTIGUOUS")
 _i64 = C.c_int64
 
 
@@ -70,6 +71,7 @@ class Port:
         self.L = L
         L.orc_bernoulli_keep.argtypes = [_i64, C.c_double, C.c_uint64, _u8p]
         L.orc_mt64_stream.argtypes = [C.c_uint64, _i64, _u64p]
+        L.orc_bernoulli_keep_bits_at.argtypes = [_i64, _i64, C.c_double, C.c_uint64, _u32p]
         L.orc_mt64_stream.restype = None
         L.orc_mask_stream_seed.argtypes = [C.c_uint64, C.c_uint64, C.c_int]
         L.orc_mask_stream_seed.restype = C.c_uint64
@@ -105,6 +107,15 @@ class Port:
     def bernoulli_keep(self, n: int, p: float, seed: int) -> np.ndarray:
         out = np.empty(n, np.uint8)
         rc = self.L.orc_bernoulli_keep(n, p, seed, out)
+        if rc:
+            raise OracleError(rc, "drop probability must lie in [0, 1)")
+        return out
+
+    def bernoulli_keep_bits_at(self, offset: int, n: int, p: float, seed: int) -> np.ndarray:
+        """Packed keep bits of elements [offset, offset+n) of the sequential
+        stream (the engine stepped past `offset` draws one by one)."""
+        out = np.empty((n + 31) // 32, np.uint32)
+        rc = self.L.orc_bernoulli_keep_bits_at(offset, n, p, seed, out)
         if rc:
             raise OracleError(rc, "drop probability must lie in [0, 1)")
         return out

@@ -61,6 +61,10 @@ SIGNATURES = {
                                        _i64, _vp, _vp]),
     "tempo_ln_param_reduce_peer": (C.c_int, [_vp, _i64, _i64, _vp, _vp, _vp, _vp]),
     "tempo_peer_alloc": (C.c_int, [_sz, C.POINTER(_vp)]),
+    "tempo_allreduce_ln_params": (C.c_int, [_vp, _vp, _i64, _vp]),
+    "tempo_nccl_unique_id": (C.c_int, [_vp]),
+    "tempo_nccl_comm_init": (C.c_int, [C.c_int32, C.c_int32, _vp, C.POINTER(_vp)]),
+    "tempo_nccl_comm_destroy": (C.c_int, [_vp]),
     "tempo_peer_free": (C.c_int, [_vp]),
     "tempo_ipc_get_handle": (C.c_int, [_vp, _vp]),
     "tempo_ipc_open_handle": (C.c_int, [_vp, C.POINTER(_vp)]),

@@ -18,6 +18,9 @@
 #include <tuple>
 #include <vector>
 
+#include <dlfcn.h>
+#include <nccl.h>
+
 #include "tempo_internal.h"
 
 namespace {
@@ -642,6 +645,92 @@ int tempo_ln_param_reduce_peer(const double* partials, int64_t nparts, int64_t c
     return cuda_status(tb::launch_ln_param_reduce_peer(partials, nparts, cols, to_peer(peer),
                                                        dgamma, dbeta, S(stream)),
                        "tempo_ln_param_reduce_peer");
+}
+
+// ---- NCCL fallback for the dgamma/dbeta sum -------------------
+// libnccl is loaded at first use (dlopen of the soname: inside a PyTorch
+// process this resolves to the NCCL torch already loaded), so the library
+// itself has no NCCL link dependency and the peer-memory path needs none.
+namespace {
+struct NcclApi {
+    decltype(&ncclGetUniqueId) get_unique_id = nullptr;
+    decltype(&ncclCommInitRank) comm_init_rank = nullptr;
+    decltype(&ncclCommDestroy) comm_destroy = nullptr;
+    decltype(&ncclAllReduce) all_reduce = nullptr;
+    decltype(&ncclGetErrorString) error_string = nullptr;
+    std::string load_error;
+};
+const NcclApi& nccl() {
+    static const NcclApi api = [] {
+        NcclApi a;
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) {
+            const char* e = dlerror();
+            a.load_error = std::string("cannot load libnccl: ") + (e ? e : "?");
+            return a;
+        }
+        a.get_unique_id = reinterpret_cast<decltype(a.get_unique_id)>(dlsym(h, "ncclGetUniqueId"));
+        a.comm_init_rank = reinterpret_cast<decltype(a.comm_init_rank)>(dlsym(h, "ncclCommInitRank"));
+        a.comm_destroy = reinterpret_cast<decltype(a.comm_destroy)>(dlsym(h, "ncclCommDestroy"));
+        a.all_reduce = reinterpret_cast<decltype(a.all_reduce)>(dlsym(h, "ncclAllReduce"));
+        a.error_string = reinterpret_cast<decltype(a.error_string)>(dlsym(h, "ncclGetErrorString"));
+        if (!a.get_unique_id || !a.comm_init_rank || !a.comm_destroy || !a.all_reduce ||
+            !a.error_string)
+            a.load_error = "libnccl lacks an expected symbol";
+        return a;
+    }();
+    return api;
+}
+int nccl_status(ncclResult_t r, const char* what) {
+    if (r == ncclSuccess) return TEMPO_OK;
+    return fail(TEMPO_ERR_CUDA, std::string(what) + ": " + nccl().error_string(r));
+}
+}  // namespace
+
+int tempo_nccl_unique_id(void* id128) {
+    if (!id128) return fail(TEMPO_ERR_PARAM, "nccl unique id: null pointer");
+    const NcclApi& a = nccl();
+    if (!a.load_error.empty()) return fail(TEMPO_ERR_UNSUPPORTED, a.load_error);
+    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId is 128 bytes");
+    ncclUniqueId id;
+    int rc = nccl_status(a.get_unique_id(&id), "ncclGetUniqueId");
+    if (rc == TEMPO_OK) std::memcpy(id128, &id, sizeof(id));
+    return rc;
+}
+
+int tempo_nccl_comm_init(int32_t world, int32_t rank, const void* id128, void** comm) {
+    if (!id128 || !comm) return fail(TEMPO_ERR_PARAM, "nccl comm init: null pointer");
+    if (world < 1 || rank < 0 || rank >= world)
+        return fail(TEMPO_ERR_PARAM, "nccl comm init: rank " + std::to_string(rank) + " of " +
+                                         std::to_string(world));
+    const NcclApi& a = nccl();
+    if (!a.load_error.empty()) return fail(TEMPO_ERR_UNSUPPORTED, a.load_error);
+    ncclUniqueId id;
+    std::memcpy(&id, id128, sizeof(id));
+    ncclComm_t c = nullptr;
+    int rc = nccl_status(a.comm_init_rank(&c, world, id, rank), "ncclCommInitRank");
+    *comm = rc == TEMPO_OK ? static_cast<void*>(c) : nullptr;
+    return rc;
+}
+
+int tempo_nccl_comm_destroy(void* comm) {
+    if (!comm) return TEMPO_OK;
+    const NcclApi& a = nccl();
+    if (!a.load_error.empty()) return fail(TEMPO_ERR_UNSUPPORTED, a.load_error);
+    return nccl_status(a.comm_destroy(static_cast<ncclComm_t>(comm)), "ncclCommDestroy");
+}
+
+int tempo_allreduce_ln_params(void* nccl_comm, float* bucket, int64_t count,
+                              tempo_stream_t stream) {
+    if (count < 0) return fail(TEMPO_ERR_DIMENSION, "allreduce: negative count");
+    if (count == 0) return TEMPO_OK;
+    if (!nccl_comm || !bucket) return fail(TEMPO_ERR_PARAM, "allreduce: null pointer");
+    const NcclApi& a = nccl();
+    if (!a.load_error.empty()) return fail(TEMPO_ERR_UNSUPPORTED, a.load_error);
+    return nccl_status(a.all_reduce(bucket, bucket, (size_t)count, ncclFloat32, ncclSum,
+                                    static_cast<ncclComm_t>(nccl_comm), S(stream)),
+                       "ncclAllReduce");
 }
 
 int tempo_peer_alloc(size_t bytes, void** dev_ptr) {

@@ -378,6 +378,37 @@ class LnPeerRank:
         self._mapped = []
 
 
+class NcclComm:
+    """An NCCL communicator built through the C-ABI (tempo_nccl_comm_init),
+    for tempo_allreduce_ln_params: the dgamma/dbeta sum for callers without
+    P2P / IPC peers.  `uid` is the 128-byte ncclUniqueId from rank 0
+    (NcclComm.unique_id()), distributed by the caller."""
+
+    def __init__(self, world: int, rank: int, uid: bytes):
+        if len(uid) != 128:
+            raise TempoError(3, "nccl unique id must be 128 bytes")
+        buf = C.create_string_buffer(uid, 128)
+        h = C.c_void_p()
+        check(lib().tempo_nccl_comm_init(int(world), int(rank), buf, C.byref(h)))
+        self._h, self.world, self.rank = h, world, rank
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = C.create_string_buffer(128)
+        check(lib().tempo_nccl_unique_id(buf))
+        return buf.raw
+
+    def allreduce_ln_params(self, bucket: torch.Tensor) -> None:
+        """Sum the bucketed LayerNorm dgamma/dbeta over the ranks, in place."""
+        _f32(bucket, "bucket")
+        check(lib().tempo_allreduce_ln_params(self._h, _ptr(bucket), bucket.numel(), _stream()))
+
+    def close(self) -> None:
+        if self._h is not None and self._h.value:
+            check(lib().tempo_nccl_comm_destroy(self._h))
+        self._h = None
+
+
 def ln_param_reduce_peer(partials: torch.Tensor, cols: int, peer: "LnPeerRank",
                          dgamma: torch.Tensor = None, dbeta: torch.Tensor = None):
     """Stage 2 on fp64 partial rows [nparts][2*cols] + the cross-rank sum."""

@@ -224,3 +224,15 @@ def test_peer_exchange_sizes_and_argument_errors():
     assert run(0, 2, 1, arrays=False) == 3  # missing buffer arrays
     st = ops._PeerStruct(0, 2, fake.value, fake.value, 1, fake.value)
     assert L.tempo_ln_param_reduce_peer(fake, -1, 8, ctypes.byref(st), fake, fake, None) == 2
+
+
+def test_allreduce_ln_params_argument_errors():
+    """tempo_allreduce_ln_params refuses bad arguments before touching NCCL
+    (or a GPU); an empty bucket is a no-op."""
+    L = _capi.lib()
+    assert L.tempo_allreduce_ln_params(None, None, 0, None) == 0
+    assert L.tempo_allreduce_ln_params(None, None, -1, None) == 2
+    assert L.tempo_allreduce_ln_params(None, None, 8, None) == 3
+    assert L.tempo_nccl_comm_init(2, 2, None, None) == 3
+    assert L.tempo_nccl_unique_id(None) == 3
+    assert L.tempo_nccl_comm_destroy(None) == 0

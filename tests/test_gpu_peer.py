@@ -227,3 +227,29 @@ def test_ipc_two_processes(cuda):
         for epoch, (dg, db) in enumerate(sums):
             want = 5.0 * (epoch + 1) * (1 + 2)
             assert np.all(dg == want) and np.all(db == want), (rank, epoch)
+
+
+@pytest.mark.gpu
+def test_nccl_allreduce_ln_params_world1(tops, cuda):
+    """The C-ABI NCCL fallback end to end on a one-rank communicator (the
+    only NCCL group one GPU can host): unique id -> comm -> in-place sum of
+    an LN backward's dgamma/dbeta bucket (identity at world 1) -> destroy."""
+    import torch
+    comm = tops.NcclComm(1, 0, tops.NcclComm.unique_id())
+    try:
+        rows, cols = 256, 1024
+        g = torch.Generator(device=cuda)
+        g.manual_seed(3)
+        dy = torch.randn(rows, cols, device=cuda, generator=g)
+        x = torch.randn(rows, cols, device=cuda, generator=g)
+        gam = 1 + 0.2 * torch.randn(cols, device=cuda, generator=g)
+        bet = 0.1 * torch.randn(cols, device=cuda, generator=g)
+        y, rs = tops.layernorm_ip_fwd(x, gam, bet)
+        bucket = torch.empty(2 * cols, device=cuda)
+        tops.layernorm_ip_bwd(dy, y, rs, gam, bet, dgamma=bucket[:cols], dbeta=bucket[cols:])
+        want = bucket.clone()
+        comm.allreduce_ln_params(bucket)
+        torch.cuda.synchronize()
+        assert torch.equal(bucket, want)
+    finally:
+        comm.close()

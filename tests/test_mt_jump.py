@@ -91,3 +91,42 @@ def test_device_stream_feeds_the_ops(tops, port, cuda):
     P1, D1, _ = tops.softmax_dropout_fwd(z, p, mask=m_dev)
     P2, D2, _ = tops.softmax_dropout_fwd(z, p, mask=m_host)
     assert torch.equal(D1, D2) and torch.equal(m_dev, m_host)
+
+
+def test_oracle_keep_bits_at_offset(port):
+    """The oracle's offset stream (engine stepped sequentially past the
+    offset) agrees with its own whole-stream bernoulli_keep."""
+    n, off, p, seed = 5000, 12345, 0.1, 77
+    whole = port.bernoulli_keep(off + n, p, seed)
+    got = _unpack(port.bernoulli_keep_bits_at(off, n, p, seed), n)
+    assert np.array_equal(got, whole[off:])
+
+
+ATT_SHARD = 1 << 28  # attention elements per rank at B=64 (64*16*512*512)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("rank", [2, 7])
+def test_device_stream_level2_shard_offsets(tops, port, cuda, rank):
+    """The N=8 attention shards start at rank * 2^28 elements = chunk
+    rank * 512: ranks >= 2 take the level-2 jump digits (32^2 chunks).  The
+    device stream there is checked against the engine stepped sequentially
+    past the offset (not the jump construction)."""
+    import torch
+    off, n, p, seed = rank * ATT_SHARD, 3 * CHUNK + 96, 0.1, 4242
+    dev = tops.bernoulli_keep_bits_device(n, p, seed, offset=off)
+    torch.cuda.synchronize()
+    assert np.array_equal(dev.cpu().numpy().view(np.uint32),
+                          port.bernoulli_keep_bits_at(off, n, p, seed))
+
+
+@pytest.mark.gpu
+def test_device_stream_full_attention_mask(tops, cuda):
+    """One whole 268,435,456-element BERT-large attention mask (512 chunks)
+    against the reference's own host stream."""
+    import torch
+    n, p, seed = ATT_SHARD, 0.1, 1234
+    dev = tops.bernoulli_keep_bits_device(n, p, seed)
+    torch.cuda.synchronize()
+    host = tops.bernoulli_keep_bits(n, p, seed)
+    assert np.array_equal(dev.cpu().numpy().view(np.uint32), host)

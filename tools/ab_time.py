@@ -3,7 +3,7 @@
   TEMPO_B200_LIB=_ab/X/libtempo_b200.so python tools/ab_time.py gelu_fwd ln_fwd ...
 
 Prints one line per op: median device time over reps (CUDA events on the
-launching stream, L2 flushed by a 1 GB fill before every rep so the GPU is
+launching stream, L2 evicted by a 512 MB read before every rep so the GPU is
 busy while Python issues the launch), algorithmic GB/s, fraction of the
 measured HBM peak, and a checksum of the outputs (to spot A/B differences).
 """
@@ -27,8 +27,14 @@ def main():
     chain = bench.Chain(dev, 0, 1)
     chain.step()
     torch.cuda.synchronize()
-    fb = torch.empty(256 * 1024 * 1024, device=dev)
-    flush = lambda: fb.fill_(0.0)  # noqa: E731
+    fb = torch.empty(128 * 1024 * 1024, device=dev).fill_(1.0)
+    fo = torch.empty((), device=dev)
+    # read-only L2 eviction (512 MB): no foreign dirty lines for the op to
+    # write back (bench.py per_op does the same); FLUSH=dirty for a 1 GB fill
+    if os.environ.get("FLUSH") == "dirty":
+        flush = lambda: fb.fill_(0.0)  # noqa: E731
+    else:
+        flush = lambda: torch.sum(fb, dim=0, out=fo)  # noqa: E731
     H, T = bench.H, bench.T
     dp = chain.dparams
     o = ops
