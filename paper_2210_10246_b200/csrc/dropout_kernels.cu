@@ -29,6 +29,12 @@ constexpr int kUnroll = 4;
 #ifndef TM_DROPOUT_U8
 #define TM_DROPOUT_U8 2  // re-tuned at r1l: bwd 49.8 -> 47.3 us, bit-identical
 #endif
+#ifndef TM_DROPOUT_PHILOX_MINB
+#define TM_DROPOUT_PHILOX_MINB 1  // min resident CTAs/SM for the Philox kernel (register cap)
+#endif
+#ifndef TM_DROPOUT_PHILOX_U8
+#define TM_DROPOUT_PHILOX_U8 TM_DROPOUT_U8
+#endif
 
 __device__ __forceinline__ float dscale(float v, double s) { return (float)((double)v * s); }
 
@@ -125,7 +131,7 @@ __global__ void __launch_bounds__(kBlock) dropout_fwd_vec_kernel(
 // directly); Philox draws by global element index as above (same bits);
 // U chunks per group, ping-pong register buffers.
 template <bool PHILOX, int U>
-__global__ void __launch_bounds__(kBlock) dropout_fwd8_kernel(
+__global__ void __launch_bounds__(kBlock, PHILOX ? TM_DROPOUT_PHILOX_MINB : 1) dropout_fwd8_kernel(
     const float* __restrict__ x, uint32_t* __restrict__ mask, double scale, uint64_t thresh,
     uint64_t seed, uint64_t offset, float* __restrict__ y, int64_t n) {
     grid_dep_wait();  // PDL: predecessor complete and visible
@@ -273,7 +279,7 @@ template <bool PHILOX>
 cudaError_t fwd(const float* x, double scale, uint64_t thresh, uint32_t* mask, uint64_t seed,
                 uint64_t offset, float* y, int64_t n, cudaStream_t st) {
     if (TM_DROPOUT_V8 && aligned32(x) && aligned32(y) && aligned16(mask) && (offset & 7u) == 0) {
-        constexpr int U = TM_DROPOUT_U8;
+        constexpr int U = PHILOX ? TM_DROPOUT_PHILOX_U8 : TM_DROPOUT_U8;
         auto k = dropout_fwd8_kernel<PHILOX, U>;
         const int64_t warps = ((n >> 8) + U - 1) / U + 1;
         // supplied masks: several waves of CTAs balance better; Philox (more

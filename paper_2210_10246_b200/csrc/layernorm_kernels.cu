@@ -487,10 +487,13 @@ __global__ void __launch_bounds__(NT) ln_bwd_vec_kernel(
                 for (int k = 0; k < 4; ++k) {
                     const float xh = (ya[k] - bt[c][k]) * igf[c][k];
                     o[k] = (fmaf(ga[k], gm[c][k], -c1) - xh * c2) * rs;
-                    // dgamma/dbeta partials in fp64 with an fp64 xhat: the F64
-                    // oracle's accuracy over tens of thousands of rows
+                    // dgamma/dbeta partials in fp64 (the F64 oracle's accuracy
+                    // over tens of thousands of rows).  sum_i g*xhat =
+                    // (sum_i g*y - beta*sum_i g)/gamma per column, so a row
+                    // costs one DFMA + one DADD; the column's correction is
+                    // applied once, after the row loop.
                     const double gd = (double)ga[k];
-                    pg[c][k] = fma(gd, ((double)ya[k] - btd[c][k]) * igd[c][k], pg[c][k]);
+                    pg[c][k] = fma(gd, (double)ya[k], pg[c][k]);
                     pb[c][k] += gd;
                 }
                 st_stream(reinterpret_cast<float4*>(dx + (r0 + i) * cols) + cg[c],
@@ -504,7 +507,7 @@ __global__ void __launch_bounds__(NT) ln_bwd_vec_kernel(
         if (!act[c]) continue;
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-            wg[cg[c] * 4 + k] = pg[c][k];
+            wg[cg[c] * 4 + k] = fma(-btd[c][k], pb[c][k], pg[c][k]) * igd[c][k];
             wg[cols + cg[c] * 4 + k] = pb[c][k];
         }
     }
