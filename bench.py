@@ -51,21 +51,38 @@ WORKLOAD = "bert-large-layer-tempo-op-chain"
 
 
 # ----------------------------------------------------------------- bytes
-def op_bytes(batch=B):
-    """Algorithmic HBM bytes per op, for `batch` sequences."""
+def op_bytes(batch=B, fused=False):
+    """Algorithmic HBM bytes per op, for `batch` sequences.
+    fused: the hidden dropout -> residual add -> LayerNorm pairs run as one
+    op each way (read proj + residual, write y + bits: 12.125 B/elem; read
+    dy, y + bits, write d_residual + d_proj: 16.125 B/elem)."""
     t, ar = batch * S, batch * A * S
     n_g, n_h, n_a = t * 4 * H, t * H, ar * S
     bits = 1.0 / 8
-    return {
+    out = {
         "softmax_dropout_fwd": n_a * (4 + 4 + 4 + bits),     # z -> P, D, mask
         "attn_probs_bwd": n_a * (4 + 4 + bits + 4 + 4),      # dD, P, mask -> dZ, D
         "gelu_fwd": n_g * (4 + 4 + bits),
         "gelu_bwd": n_g * (4 + 4 + bits + 4),
-        "layernorm_fwd": 2 * (8 * n_h + 4 * t + 8 * H),
-        "layernorm_bwd": 2 * (12 * n_h + 4 * t + 16 * H),
-        "dropout_fwd": 2 * n_h * (8 + bits),
-        "dropout_bwd": 2 * n_h * (8 + bits),
     }
+    if fused:
+        out["dropout_add_layernorm_fwd"] = 2 * (n_h * (12 + bits) + 4 * t + 8 * H)
+        out["dropout_add_layernorm_bwd"] = 2 * (n_h * (16 + bits) + 4 * t + 16 * H)
+    else:
+        out["layernorm_fwd"] = 2 * (8 * n_h + 4 * t + 8 * H)
+        out["layernorm_bwd"] = 2 * (12 * n_h + 4 * t + 16 * H)
+        out["dropout_fwd"] = 2 * n_h * (8 + bits)
+        out["dropout_bwd"] = 2 * n_h * (8 + bits)
+    return out
+
+
+def unfused_equivalent_bytes(batch=B):
+    """What the fused chain's work moves as separate ops, residual adds
+    included (add: read 2, write 1 fp32 per element forward; its backward
+    is a pass-through): the second byte model reported beside `value`."""
+    t = batch * S
+    n_h = t * H
+    return sum(op_bytes(batch, False).values()) + 2 * 12 * n_h
 
 
 def setup_peer(chain, dist, rank, world, dev, backend):
@@ -109,14 +126,18 @@ def trimmed_mean(ts):
     return sum(v) / len(v)
 
 
-def op_elements(batch=B):
+def op_elements(batch=B, fused=False):
     """Elements each op processes per step (the map it streams: n for the
     elementwise ops, rows x cols for the row ops; both LNs / dropouts)."""
     t, ar = batch * S, batch * A * S
     n_g, n_h, n_a = t * 4 * H, t * H, ar * S
-    return {"softmax_dropout_fwd": n_a, "attn_probs_bwd": n_a, "gelu_fwd": n_g, "gelu_bwd": n_g,
-            "layernorm_fwd": 2 * n_h, "layernorm_bwd": 2 * n_h, "dropout_fwd": 2 * n_h,
-            "dropout_bwd": 2 * n_h}
+    out = {"softmax_dropout_fwd": n_a, "attn_probs_bwd": n_a, "gelu_fwd": n_g, "gelu_bwd": n_g}
+    if fused:
+        out.update({"dropout_add_layernorm_fwd": 2 * n_h, "dropout_add_layernorm_bwd": 2 * n_h})
+    else:
+        out.update({"layernorm_fwd": 2 * n_h, "layernorm_bwd": 2 * n_h, "dropout_fwd": 2 * n_h,
+                    "dropout_bwd": 2 * n_h})
+    return out
 
 
 def peaks():
@@ -140,16 +161,20 @@ def _numel(shapes):
 
 
 class Chain:
-    """Device buffers + the step of the Tempo op chain (weak-scaled rank)."""
+    """Device buffers + the step of the Tempo op chain on one rank's rows.
+    fused=True: each hidden dropout -> residual add -> LayerNorm pair is the
+    fused op (tempo_dropout_add_ln_fwd/bwd) and the layer input is a
+    residual stream; fused=False: the separate dropout and LayerNorm ops
+    with no residual add (the round-1 chain)."""
     peer = None  # ops.LnPeerRank at N>1: the fused dgamma/dbeta exchange
     kernel_events = None  # list: CUDA event pairs around attn_probs_bwd in each step
 
-    def __init__(self, dev, rank, world, seed=1234, batch=B):
+    def __init__(self, dev, rank, world, seed=1234, batch=B, fused=False):
         import torch
         from paper_2210_10246_b200 import ops
         self.ops, self.torch, self.dev = ops, torch, dev
         self.rank, self.world = rank, world
-        self.batch = batch
+        self.batch, self.fused = batch, fused
         T, ATT_ROWS = batch * S, batch * A * S  # this rank's token / attention rows
         self.T, self.ATT_ROWS = T, ATT_ROWS
         g = torch.Generator(device=dev)
@@ -167,6 +192,9 @@ class Chain:
                      "dD": (ATT_ROWS, S)}
         shapes_out = {"dZ": (ATT_ROWS, S), "dx_d1": (T, H), "dx_g": (T, 4 * H),
                       "dx_d2": (T, H), "dparams": (4 * H,)}  # [dg2, db2, dg1, db1]
+        if fused:
+            shapes_in["x_res"] = (T, H)       # the layer input (LN1's residual)
+            shapes_out["dx_res"] = (T, H)     # its gradient through LN1's residual path
         self.shapes_in, self.shapes_out = shapes_in, shapes_out
         self.in_buf = torch.empty(_numel(shapes_in), device=dev)
         self.in_buf.normal_(generator=g)
@@ -181,13 +209,15 @@ class Chain:
         e = torch.empty_like
         mw = lambda n: torch.empty(ops.mask_words(n), dtype=torch.int32, device=dev)  # noqa: E731
         self.P, self.D, self.m_att = e(self.z), e(self.z), mw(self.z.numel())
-        self.d1, self.m1 = e(self.x_attn_out), mw(T * H)
+        self.m1, self.m2 = mw(T * H), mw(T * H)
+        self.d1 = self.d2 = None  # the unfused chain's dropout outputs
+        if not fused:
+            self.d1, self.d2 = e(self.x_attn_out), e(self.x_ffn2)
         self.y_ln1, self.rs1 = e(self.x_attn_out), torch.empty(T, device=dev)
         self.y_g, self.m_g = e(self.x_ffn1), mw(T * 4 * H)
-        self.d2, self.m2 = e(self.x_ffn2), mw(T * H)
         self.y_ln2, self.rs2 = e(self.x_ffn2), torch.empty(T, device=dev)
-        self.dx_ln2 = e(self.x_ffn2)
-        self.dx_ln1 = e(self.x_attn_out)
+        self.dx_ln2 = e(self.x_ffn2)   # fused: LN2's residual-path gradient (to y_ln1)
+        self.dx_ln1 = None if fused else e(self.x_attn_out)
         self.Drec = e(self.z)
         self.ws = ops.ln_workspace(T, H, dev)
         self.status = torch.zeros(1, dtype=torch.int32, device=dev)
@@ -243,6 +273,17 @@ class Chain:
             self.reference_masks(seed)
         o.softmax_dropout_fwd(self.z, P_DROP, mask=self.m_att, generate=gen, seed=seed,
                               offset=self.off_att, P=self.P, D=self.D)
+        if self.fused:  # encoder.cpp:180-191, 198-210 as two fused passes
+            o.dropout_add_layernorm_fwd(self.x_attn_out, self.x_res, self.g1, self.b1, P_DROP,
+                                        mask=self.m1, generate=gen, seed=seed + 1,
+                                        offset=self.off_h, check_gamma=False, y=self.y_ln1,
+                                        rstd=self.rs1, dev_status=self.status)
+            o.gelu_ip_fwd(self.x_ffn1, self.table, y=self.y_g, mask=self.m_g)
+            o.dropout_add_layernorm_fwd(self.x_ffn2, self.y_ln1, self.g2, self.b2, P_DROP,
+                                        mask=self.m2, generate=gen, seed=seed + 2,
+                                        offset=self.off_h, check_gamma=False, y=self.y_ln2,
+                                        rstd=self.rs2, dev_status=self.status)
+            return
         o.dropout_fwd(self.x_attn_out, P_DROP, mask=self.m1, generate=gen, seed=seed + 1,
                       offset=self.off_h, y=self.d1)
         o.layernorm_ip_fwd(self.d1, self.g1, self.b1, check_gamma=False, y=self.y_ln1,
@@ -261,9 +302,24 @@ class Chain:
             self.ops.layernorm_ip_bwd(dy, y, rs, g, b, dx=dx, dgamma=dg, dbeta=db,
                                       workspace=self.ws)
 
+    def _dal_bwd(self, dy, y, rs, g, b, m, d_res, d_proj, dg, db):
+        self.ops.dropout_add_layernorm_bwd(dy, y, rs, g, b, m, P_DROP, d_residual=d_res,
+                                           d_proj=d_proj, dgamma=dg, dbeta=db,
+                                           workspace=self.ws, peer=self.peer)
+
     def backward(self, allreduce):
         o = self.ops
         dp = self.dparams
+        if self.fused:
+            self._dal_bwd(self.dy_ln2, self.y_ln2, self.rs2, self.g2, self.b2, self.m2,
+                          self.dx_ln2, self.dx_d2, dp[0:H], dp[H:2 * H])
+            o.gelu_ip_bwd(self.dy_gelu, self.y_g, self.m_g, self.table, dx=self.dx_g)
+            self._dal_bwd(self.dy_ln1, self.y_ln1, self.rs1, self.g1, self.b1, self.m1,
+                          self.dx_res, self.dx_d1, dp[2 * H:3 * H], dp[3 * H:])
+            if allreduce is not None:
+                allreduce(dp)
+            self._attn_bwd()
+            return
         self._ln_bwd(self.dy_ln2, self.y_ln2, self.rs2, self.g2, self.b2, self.dx_ln2,
                      dp[0:H], dp[H:2 * H])
         o.dropout_bwd(self.dx_ln2, self.m2, P_DROP, dx=self.dx_d2)
@@ -273,6 +329,10 @@ class Chain:
         if allreduce is not None:
             allreduce(dp)  # the one collective: bucketed LN dgamma/dbeta (16 KB)
         o.dropout_bwd(self.dx_ln1, self.m1, P_DROP, dx=self.dx_d1)
+        self._attn_bwd()
+
+    def _attn_bwd(self):
+        o = self.ops
         ev = self.kernel_events
         if ev is not None:  # in-chain duration of the dominant kernel (roofline)
             ev.append((self.torch.cuda.Event(enable_timing=True),
@@ -308,8 +368,10 @@ class Chain:
         self.backward(allreduce)
 
     # kernels launched per step (ours): softmax fwd 1, dropout fwd 2, LN fwd 2,
-    # GELU fwd 1, LN bwd 2x(stage1+stage2), dropout bwd 2, GELU bwd 1, attn bwd 1
+    # GELU fwd 1, LN bwd 2x(stage1+stage2), dropout bwd 2, GELU bwd 1, attn bwd 1;
+    # fused: softmax 1, dropout+add+LN fwd 2, GELU fwd 1, its bwd 2x2, GELU bwd 1, attn 1
     LAUNCHES_PER_STEP = 14
+    LAUNCHES_PER_STEP_FUSED = 10
     # --masks reference, per mask: seed, (base, jump) for each of the 2 digit
     # levels the rank-0 offsets touch, keep = 6; three masks
     REF_MASK_LAUNCHES = 18
@@ -330,14 +392,23 @@ class Chain:
             "attn_probs_bwd": lambda: o.attn_probs_bwd(self.dD, self.P, self.m_att, P_DROP, write_d=True, dZ=self.dZ, D=self.Drec),
             "gelu_fwd": lambda: o.gelu_ip_fwd(self.x_ffn1, self.table, y=self.y_g, mask=self.m_g),
             "gelu_bwd": lambda: o.gelu_ip_bwd(self.dy_gelu, self.y_g, self.m_g, self.table, dx=self.dx_g),
-            "layernorm_fwd": lambda: o.layernorm_ip_fwd(self.d1, self.g1, self.b1, check_gamma=False, y=self.y_ln1, rstd=self.rs1),
-            "layernorm_bwd": lambda: o.layernorm_ip_bwd(self.dy_ln1, self.y_ln1, self.rs1, self.g1, self.b1, dx=self.dx_ln1, dgamma=dp[:H_], dbeta=dp[H_:2 * H_], workspace=self.ws),
-            "dropout_fwd": lambda: o.dropout_fwd(self.x_ffn2, P_DROP, mask=self.m2, generate=True, seed=9, y=self.d2),
-            "dropout_bwd": lambda: o.dropout_bwd(self.dx_ln2, self.m2, P_DROP, dx=self.dx_d2),
         }
+        if self.fused:
+            calls.update({
+                "dropout_add_layernorm_fwd": lambda: o.dropout_add_layernorm_fwd(self.x_ffn2, self.y_ln1, self.g2, self.b2, P_DROP, mask=self.m2, generate=True, seed=9, check_gamma=False, y=self.y_ln2, rstd=self.rs2),
+                "dropout_add_layernorm_bwd": lambda: o.dropout_add_layernorm_bwd(self.dy_ln2, self.y_ln2, self.rs2, self.g2, self.b2, self.m2, P_DROP, d_residual=self.dx_ln2, d_proj=self.dx_d2, dgamma=dp[:H_], dbeta=dp[H_:2 * H_], workspace=self.ws),
+            })
+        else:
+            calls.update({
+                "layernorm_fwd": lambda: o.layernorm_ip_fwd(self.d1, self.g1, self.b1, check_gamma=False, y=self.y_ln1, rstd=self.rs1),
+                "layernorm_bwd": lambda: o.layernorm_ip_bwd(self.dy_ln1, self.y_ln1, self.rs1, self.g1, self.b1, dx=self.dx_ln1, dgamma=dp[:H_], dbeta=dp[H_:2 * H_], workspace=self.ws),
+                "dropout_fwd": lambda: o.dropout_fwd(self.x_ffn2, P_DROP, mask=self.m2, generate=True, seed=9, y=self.d2),
+                "dropout_bwd": lambda: o.dropout_bwd(self.dx_ln2, self.m2, P_DROP, dx=self.dx_d2),
+            })
         # ops that run twice per step (both LNs / both dropouts): time one
         # instance and count it twice
-        mult = {"layernorm_fwd": 2, "layernorm_bwd": 2, "dropout_fwd": 2, "dropout_bwd": 2}
+        mult = {"layernorm_fwd": 2, "layernorm_bwd": 2, "dropout_fwd": 2, "dropout_bwd": 2,
+                "dropout_add_layernorm_fwd": 2, "dropout_add_layernorm_bwd": 2}
         out = {}
         st = torch.cuda.current_stream()
         for name, fn in calls.items():
@@ -413,9 +484,15 @@ def per_config_timings(dev, peak, reps=40):
         ops.softmax_dropout_fwd(z3, P_DROP, mask=m3, generate=True, seed=5, P=P3, D=D3)
         ops.attn_probs_bwd(dD3, P3, m3, P_DROP, write_d=True, dZ=dZ3, D=Dr3)
 
+    def copy_floor1():  # the same streams with no math: x -> y, (dy, y) -> dx
+        y1.copy_(x1)
+        torch.add(dy1, y1, out=dx1)
+
     bits = 1.0 / 8
     cases = [
         ("configs[0] gelu fwd+bwd [1024,3072]", cfg1, n1 * (8 + bits + 12 + bits), n1,
+         n1 * 4 * 3),
+        ("floor: torch copy + add of the configs[0] streams", copy_floor1, n1 * 20, n1,
          n1 * 4 * 3),
         ("configs[1] layernorm fwd+bwd [16384,768]", cfg2,
          (8 * R2 * C2 + 4 * R2 + 8 * C2) + (12 * R2 * C2 + 4 * R2 + 16 * C2), R2 * C2,
@@ -524,7 +601,8 @@ def cpu_model() -> str:
     return "unknown"
 
 
-def cpu_reference_sample(frac_rows: int, threads: int, steps: int, warmup: int, batch=B):
+def cpu_reference_sample(frac_rows: int, threads: int, steps: int, warmup: int, batch=B,
+                         fused=False):
     """The reference's own CPU implementation (oracle/_ref/libtempo_ref.so,
     compiled from /root/reference/proj/src) of the same chain: 1/frac_rows of
     one rank's rows of every op (frac_rows = 1: the whole configs[3] step),
@@ -543,7 +621,7 @@ def cpu_reference_sample(frac_rows: int, threads: int, steps: int, warmup: int, 
     def create(k):
         nt = (k + 1) * t_rows // threads - k * t_rows // threads
         na = (k + 1) * a_rows // threads - k * a_rows // threads
-        handles[k] = ref.chain_create(table, P_DROP, na, S, nt, H, 1000 + k)
+        handles[k] = ref.chain_create(table, P_DROP, na, S, nt, H, 1000 + k, with_residual=fused)
 
     def run_all(fn):
         ths = [threading.Thread(target=fn, args=(k,)) for k in range(threads)]
@@ -565,7 +643,7 @@ def cpu_reference_sample(frac_rows: int, threads: int, steps: int, warmup: int, 
         for h in handles:
             if h:
                 ref.chain_destroy(h)
-    nbytes = sum(op_bytes(batch).values()) / frac_rows
+    nbytes = sum(op_bytes(batch, fused).values()) / frac_rows
     what = ("the whole per-GPU chain" if frac_rows == 1 else f"1/{frac_rows} of the per-GPU chain rows")
     sample = (f"{what} ({t_rows} tokens, {a_rows} attention rows; {nbytes / 1e9:.3f} GB "
               f"algorithmic) per step, {threads} threads, inputs built outside the timed region")
@@ -597,6 +675,9 @@ def main():
     ap.add_argument("--scaling", default=None, choices=["strong", "weak"],
                     help="N>1: strong (default; configs[4], --global-batch rows split N ways) "
                          "or weak (B=64 per rank)")
+    ap.add_argument("--chain", default="fused", choices=["fused", "unfused"],
+                    help="fused (default): hidden dropout -> residual add -> LayerNorm as one op "
+                         "each way; unfused: separate dropout / LayerNorm ops, no residual add")
     ap.add_argument("--configs-only", action="store_true",
                     help="time only BASELINE configs[0..2] at their own shapes (for ncu)")
     ap.add_argument("--global-batch", type=int, default=GLOBAL_B_STRONG,
@@ -638,7 +719,8 @@ def main():
     if args.configs_only:
         print(json.dumps({"per_config": per_config_timings(dev, peaks()[0], reps=args.steps)}))
         return
-    chain = Chain(dev, rank, world, batch=batch)
+    fused = args.chain == "fused"
+    chain = Chain(dev, rank, world, batch=batch, fused=fused)
     chain.mask_mode = args.masks
     from paper_2210_10246_b200.dist import allreduce_ln_params
     allreduce = allreduce_ln_params if world > 1 else None
@@ -688,13 +770,13 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
 
-    per_rank_bytes = sum(op_bytes(batch).values())
+    per_rank_bytes = sum(op_bytes(batch, fused).values())
     value = per_rank_bytes * world / (ms * 1e-3) / 1e9
     peak, peak_kind = peaks()
 
     # ---- per-op device times (outside the timed region) -------------------
     per_op = chain.per_op_timings(reps=11, flush=flush, flush_dirty=flush_dirty)
-    ob, oe = op_bytes(batch), op_elements(batch)
+    ob, oe = op_bytes(batch, fused), op_elements(batch, fused)
     per_op_rows = []
     for name, (t_ms, mult, t_dirty) in per_op.items():
         gbs = ob[name] / (t_ms * 1e-3) / 1e9
@@ -788,8 +870,10 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
             threads = len(os.sched_getaffinity(0))
-            v, dt, sample = cpu_reference_sample(frac_rows=1, threads=threads, steps=2, warmup=1)
-            v1, dt1, _ = cpu_reference_sample(frac_rows=512, threads=1, steps=1, warmup=0)
+            v, dt, sample = cpu_reference_sample(frac_rows=1, threads=threads, steps=2, warmup=1,
+                                                 fused=fused)
+            v1, dt1, _ = cpu_reference_sample(frac_rows=512, threads=1, steps=1, warmup=0,
+                                              fused=fused)
             cpu = {"value": round(v, 4), "unit": "GB/s", "cores": threads, "kind": "reference",
                    "sample": sample, "s_per_step": round(dt, 3), "cpu_model": cpu_model(),
                    "one_thread": {"value": round(v1, 4), "unit": "GB/s",
@@ -810,6 +894,10 @@ def main():
             "config": {"workload": WORKLOAD, "batch_per_gpu": batch, "global_batch": batch * world,
                        "seq_len": S, "hidden": H, "heads": A, "dropout_p": P_DROP,
                        "parallelism": f"rows{world}", "collective": collective,
+                       "chain": ("fused: hidden dropout -> residual add -> LayerNorm as one op "
+                                 "each way (tempo_dropout_add_ln_fwd/bwd)" if fused else
+                                 "unfused: separate dropout and LayerNorm ops, no residual add"),
+                       "bytes_per_step_per_gpu": int(per_rank_bytes),
                        "l2": f"working set {per_rank_bytes / 1e9:.1f} GB/step per GPU >> 126 MB L2",
                        "baseline_config": ("configs[3] (B=64, one GPU)" if world == 1 else
                                            f"configs[4]: global B={batch * world} row-sharded "
@@ -818,7 +906,7 @@ def main():
             "roofline": roofline,
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "gpu_launches": (Chain.LAUNCHES_PER_STEP +
+            "gpu_launches": ((Chain.LAUNCHES_PER_STEP_FUSED if fused else Chain.LAUNCHES_PER_STEP) +
                              (Chain.REF_MASK_LAUNCHES if args.masks == "reference" else 0)) * args.steps,
             "mask_stream": args.masks,
             "reference_mask_generation": ref_mask,
@@ -827,7 +915,13 @@ def main():
             "per_op": per_op_rows,
             "per_config": per_config,
             "frac_of_peak": round(value / world / peak, 4),
-            "elements_per_s": {"value": round(sum(op_elements(batch).values()) * world / (ms * 1e-3) / 1e9, 2),
+            "unfused_equivalent": ({
+                "what": "the same step's work as separate ops incl. the residual adds "
+                        "(dropout 8.125 + add 12 + LN 8 B/elem fwd, LN 12 + dropout 8.125 bwd)",
+                "bytes_per_step_per_gpu": int(unfused_equivalent_bytes(batch)),
+                "gbs": round(unfused_equivalent_bytes(batch) * world / (ms * 1e-3) / 1e9, 2)}
+                if fused else None),
+            "elements_per_s": {"value": round(sum(op_elements(batch, fused).values()) * world / (ms * 1e-3) / 1e9, 2),
                                "unit": "Gelem/s", "what": "elements streamed by all ops of the chain"},
             "stash": stash_report(chain),
         }
@@ -947,7 +1041,7 @@ def e2e_measure(chain, args, world, allreduce, dist):
         t = torch.tensor([ms], device=chain.dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-    v = sum(op_bytes(chain.batch).values()) * world / (ms * 1e-3) / 1e9
+    v = sum(op_bytes(chain.batch, chain.fused).values()) * world / (ms * 1e-3) / 1e9
     return {"value": round(v, 2), "unit": "GB/s", "h2d_bytes_per_step": int(bi),
             "d2h_bytes_per_step": int(bo), "ms_per_step": round(ms, 3), "steps": k,
             "overlap": "one H2D (step i+1) || compute (step i) || one D2H (step i-1); "
@@ -966,8 +1060,9 @@ def main_reference(args, rank, world):
     batch = args.global_batch // world if (scaling == "strong" and world > 1) else B
     threads = len(os.sched_getaffinity(0))
     frac = reference_frac(args.steps, args.warmup)
+    fused = args.chain == "fused"
     v, dt, sample = cpu_reference_sample(frac_rows=frac, threads=threads, steps=args.steps,
-                                         warmup=args.warmup, batch=batch)
+                                         warmup=args.warmup, batch=batch, fused=fused)
     line = {
         "metric": METRIC, "value": round(v, 4), "unit": "GB/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dt * 1e3, 2),
@@ -977,6 +1072,9 @@ def main_reference(args, rank, world):
         "config": {"workload": WORKLOAD, "batch_per_gpu": batch, "global_batch": batch * world,
                    "seq_len": S, "hidden": H, "heads": A, "dropout_p": P_DROP,
                    "parallelism": f"rows{world}",
+                   "chain": ("hidden dropout -> residual add (Graph::add) -> LayerNorm, as the "
+                             "reference layer composes them" if fused else
+                             "dropout and LayerNorm, no residual add"),
                    "sample_rows": f"1/{frac} of one GPU's rows" if frac > 1 else "all of one GPU's rows"},
         "cpu_baseline": {"value": round(v, 4), "unit": "GB/s", "cores": threads,
                          "kind": "reference", "sample": sample, "cpu_model": cpu_model()},

@@ -236,6 +236,35 @@ int tempo_dropout_fwd(const float* x, double p, tempo_mask_mode_t mode, uint32_t
 int tempo_dropout_bwd(const float* dy, const uint32_t* mask, double p, float* dx, int64_t n,
                       tempo_stream_t stream);
 
+/* ---------------------------------------------------------------------- */
+/* Hidden dropout -> residual add -> In-Place LayerNorm, fused             */
+/* (the reference layer's ref_ops::dropout -> Graph::add ->                */
+/*  tempo_ops::layernorm chain, encoder.cpp:180-191 and 198-210)            */
+/* ---------------------------------------------------------------------- */
+/* Forward: r = residual + (keep ? float(double(proj) / (1-p)) : 0), then the
+ * in-place LayerNorm of r (y, rstd as tempo_ln_ip_fwd) -- bit-identical to
+ * tempo_dropout_fwd, an fp32 add and tempo_ln_ip_fwd on the same inputs,
+ * without storing the dropout output or r.  SUPPLIED reads `mask`, PHILOX
+ * writes it (the same bits tempo_dropout_fwd generates for these global
+ * element offsets).  cols % 32 == 0 (else TEMPO_ERR_UNSUPPORTED: use the
+ * separate ops); cols <= 16384.  HBM: 12.125 B/element. */
+int tempo_dropout_add_ln_fwd(const float* proj, const float* residual, double p,
+                             tempo_mask_mode_t mode, uint32_t* mask, uint64_t seed,
+                             uint64_t offset, const float* gamma, const float* beta, double eps,
+                             float* y, float* rstd, int64_t rows, int64_t cols,
+                             int32_t* dev_status, tempo_stream_t stream);
+/* Backward: d_residual = the LayerNorm input gradient (tempo_ln_ip_bwd's dx;
+ * the add passes it through to the residual branch) and d_proj = keep ?
+ * float(double(d_residual) / (1-p)) : 0 (dropout_backward), in one pass;
+ * dgamma/dbeta as tempo_ln_ip_bwd (same workspace query), summed over the
+ * ranks of `peer` when it is non-NULL (as tempo_ln_ip_bwd_peer).  cols % 4
+ * == 0.  HBM: 16.125 B/element. */
+int tempo_dropout_add_ln_bwd(const float* dy, const float* y, const float* rstd,
+                             const float* gamma, const float* beta, const uint32_t* mask,
+                             double p, float* d_residual, float* d_proj, float* dgamma,
+                             float* dbeta, void* workspace, size_t workspace_bytes, int64_t rows,
+                             int64_t cols, const tempo_ln_peer_t* peer, tempo_stream_t stream);
+
 /* out = float(double(a) * c): tempo::scale (kernels.cpp:209-213), used by
  * Graph::scale (the 1/sqrt(d) of tempo_ops::sdpa).  out may alias a. */
 int tempo_tensor_scale(const float* a, double c, float* out, int64_t n, tempo_stream_t stream);

@@ -259,7 +259,8 @@ class Ref:
         L.ref_memory_model.argtypes = [_i64, _i64, _i64, _i64, C.POINTER(_i64), C.POINTER(_i64),
                                        C.POINTER(_i64)]
         L.ref_ledger_bytes.argtypes = [C.c_int, _i64, _i64, C.c_char_p, C.POINTER(_i64)]
-        L.ref_chain_create.argtypes = [C.c_char_p, C.c_double, _i64, _i64, _i64, _i64, C.c_uint64]
+        L.ref_chain_create.argtypes = [C.c_char_p, C.c_double, _i64, _i64, _i64, _i64, C.c_uint64,
+                                       C.c_int]
         L.ref_chain_create.restype = C.c_void_p
         L.ref_chain_run.argtypes = [C.c_void_p]
         L.ref_chain_destroy.argtypes = [C.c_void_p]
@@ -273,11 +274,12 @@ class Ref:
         return None if a is None else a.ctypes.data_as(C.c_void_p)
 
     def chain_create(self, table_text: str, p: float, att_rows: int, seq: int, tokens: int,
-                     hidden: int, seed: int):
+                     hidden: int, seed: int, with_residual: bool = False):
         """bench.py's reference arm: one shard of the layer op chain with its
         inputs built once by the reference's own generators (ref_harness.cpp
         ref_chain_create).  Returns an opaque handle for chain_run."""
-        h = self.L.ref_chain_create(table_text.encode(), p, att_rows, seq, tokens, hidden, seed)
+        h = self.L.ref_chain_create(table_text.encode(), p, att_rows, seq, tokens, hidden, seed,
+                                    int(with_residual))
         if not h:
             raise OracleError(1, self.L.ref_last_error().decode())
         return h

@@ -344,17 +344,21 @@ int ref_ledger_bytes(int op, std::int64_t rows, std::int64_t cols,
 // step: four tapes (softmax -> dropout_recompute; hidden dropout -> LN1;
 // GELU; hidden dropout -> LN2), each forward + Tape::backward, plus the
 // consumer's recompute of D (recompute rule "dropout-rescale",
-// ops_tempo.cpp:17-26).  Nothing is copied in or out per step.
+// ops_tempo.cpp:17-26).  with_residual: each hidden dropout feeds a
+// Graph::add with a residual stream before its LayerNorm, as the layer does
+// (encoder.cpp:185, 204) -- the work bench.py's fused chain covers.
+// Nothing is copied in or out per step.
 struct RefChain {
     GeluPolyTable table;
     double p;
-    Tensor z, dD, x1, x2, xg, dyg, dy1, dy2, g1, b1, g2, b2;
+    Tensor z, dD, x1, x2, xg, dyg, dy1, dy2, g1, b1, g2, b2, res1, res2;
     BoolMask ka, k1, k2;
+    bool with_residual = false;
 };
 
 void* ref_chain_create(const char* table_text, double p, std::int64_t att_rows,
                        std::int64_t seq, std::int64_t tokens, std::int64_t hidden,
-                       std::uint64_t seed) {
+                       std::uint64_t seed, int with_residual) {
     RefChain* c = nullptr;
     int rc = guarded([&] {
         c = new RefChain{GeluPolyTable::parse_string(table_text), p};
@@ -379,6 +383,11 @@ void* ref_chain_create(const char* table_text, double p, std::int64_t att_rows,
             c->g2.set(j, 1 - 0.2 * n2.get(j));
             c->b1.set(j, 0.1 * n2.get(j));
             c->b2.set(j, 0.1 * n1.get(j));
+        }
+        c->with_residual = with_residual != 0;
+        if (c->with_residual) {
+            c->res1 = Tensor::randn(sh, s + 14, Dtype::F32);
+            c->res2 = Tensor::randn(sh, s + 15, Dtype::F32);
         }
         c->ka = BoolMask::bernoulli_keep(sa, p, s + 11);
         c->k1 = BoolMask::bernoulli_keep(sh, p, s + 12);
@@ -407,6 +416,10 @@ int ref_chain_run(void* handle) {
             Graph g;
             NodeId xn = g.leaf(k ? c.x2 : c.x1, "x");
             NodeId dn = ref_ops::dropout(g, xn, c.p, k ? c.k2 : c.k1, "d", "d_mask");
+            if (c.with_residual) {
+                NodeId rn = g.leaf(k ? c.res2 : c.res1, "residual");
+                dn = g.add(rn, dn, "ln_input");
+            }
             NodeId gn = g.param(k ? c.g2 : c.g1, "gamma");
             NodeId bn = g.param(k ? c.b2 : c.b1, "beta");
             NodeId yn = tempo_ops::layernorm(g, dn, gn, bn, 1e-5, "y", "y_rstd");

@@ -809,6 +809,57 @@ int tempo_attn_probs_bwd(const float* dD, const float* P, const uint32_t* mask, 
 }
 
 // ---- dropout -------------------------------------------------------------------
+int tempo_dropout_add_ln_fwd(const float* proj, const float* residual, double p,
+                             tempo_mask_mode_t mode, uint32_t* mask, uint64_t seed,
+                             uint64_t offset, const float* gamma, const float* beta, double eps,
+                             float* y, float* rstd, int64_t rows, int64_t cols,
+                             int32_t* dev_status, tempo_stream_t stream) {
+    if (int rc = check_rows(rows, cols, "dropout_add_layernorm")) return rc;
+    if (int rc = check_p(p)) return rc;
+    if (int rc = check_mode(mode)) return rc;
+    if (!(eps > 0.0)) return fail(TEMPO_ERR_PARAM, "layernorm epsilon must be positive");
+    if (cols % 32 != 0)
+        return fail(TEMPO_ERR_UNSUPPORTED,
+                    "dropout_add_layernorm needs cols % 32 == 0 (rows own whole mask words); "
+                    "use tempo_dropout_fwd + add + tempo_ln_ip_fwd");
+    if (cols > (1 << 14)) return fail(TEMPO_ERR_DIMENSION, "dropout_add_layernorm: row too long");
+    if (rows > 0 && (!proj || !residual || !mask || !gamma || !beta || !y || !rstd))
+        return fail(TEMPO_ERR_PARAM, "dropout_add_layernorm: null pointer");
+    return cuda_status(tb::launch_dal_fwd(proj, residual, 1.0 / (1.0 - p), philox_threshold(p),
+                                          mode == TEMPO_MASK_PHILOX, mask, seed, offset, gamma,
+                                          beta, eps, y, rstd, rows, cols, dev_status, S(stream)),
+                       "tempo_dropout_add_ln_fwd");
+}
+
+int tempo_dropout_add_ln_bwd(const float* dy, const float* y, const float* rstd,
+                             const float* gamma, const float* beta, const uint32_t* mask,
+                             double p, float* d_residual, float* d_proj, float* dgamma,
+                             float* dbeta, void* workspace, size_t workspace_bytes, int64_t rows,
+                             int64_t cols, const tempo_ln_peer_t* peer, tempo_stream_t stream) {
+    if (peer)
+        if (int rc = check_peer(peer)) return rc;
+    if (int rc = check_rows(rows, cols, "dropout_add_layernorm backward")) return rc;
+    if (int rc = check_p(p)) return rc;
+    if (cols > std::numeric_limits<int>::max() / 2)
+        return fail(TEMPO_ERR_DIMENSION, "layernorm: row too long");
+    if (cols % 4 != 0)
+        return fail(TEMPO_ERR_UNSUPPORTED, "dropout_add_layernorm backward needs cols % 4 == 0");
+    if (cols > 0 && (!gamma || !beta || !dgamma || !dbeta))
+        return fail(TEMPO_ERR_PARAM, "layernorm: null parameter pointer");
+    if (rows > 0 && (!dy || !y || !rstd || !d_residual || !d_proj || !mask))
+        return fail(TEMPO_ERR_PARAM, "dropout_add_layernorm backward: null tensor pointer");
+    size_t need = tempo_ln_ip_bwd_workspace_size(rows, cols);
+    if (workspace_bytes < need || (need > 0 && !workspace))
+        return fail(TEMPO_ERR_PARAM, "layernorm backward workspace too small: need " +
+                                         std::to_string(need) + " bytes");
+    tb::LnPeer pg{};
+    if (peer) pg = to_peer(peer);
+    return cuda_status(tb::launch_ln_bwd(dy, y, rstd, gamma, beta, d_residual, dgamma, dbeta,
+                                         workspace, rows, cols, S(stream), peer ? &pg : nullptr,
+                                         mask, 1.0 / (1.0 - p), d_proj),
+                       "tempo_dropout_add_ln_bwd");
+}
+
 int tempo_dropout_fwd(const float* x, double p, tempo_mask_mode_t mode, uint32_t* mask,
                       uint64_t seed, uint64_t offset, float* y, int64_t n, tempo_stream_t stream) {
     if (int rc = check_n(n, "dropout")) return rc;

@@ -30,7 +30,7 @@ constexpr int kUnroll = 4;
 #define TM_DROPOUT_U8 2  // re-tuned at r1l: bwd 49.8 -> 47.3 us, bit-identical
 #endif
 #ifndef TM_DROPOUT_PHILOX_MINB
-#define TM_DROPOUT_PHILOX_MINB 1  // min resident CTAs/SM for the Philox kernel (register cap)
+#define TM_DROPOUT_PHILOX_MINB 2  // min resident CTAs/SM for the Philox kernel (<= 128 regs; 1 lets ptxas take 138 and halves occupancy: 49 -> 58 us)
 #endif
 #ifndef TM_DROPOUT_PHILOX_U8
 #define TM_DROPOUT_PHILOX_U8 TM_DROPOUT_U8

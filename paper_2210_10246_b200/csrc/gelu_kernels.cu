@@ -444,7 +444,7 @@ __device__ __forceinline__ float gelu_h_fast(float y, uint32_t m, const FastTabl
 #ifndef TM_GELU_BWD_U8
 #define TM_GELU_BWD_U8 2
 #endif
-template <int NC4, bool HORNER, bool V8>
+template <int NC4, bool HORNER, bool V8, int U8 = TM_GELU_BWD_U8>
 __global__ void __launch_bounds__(kBlock) gelu_bwd_fast_kernel(
     const float* __restrict__ dy, const float* __restrict__ y, const uint32_t* __restrict__ mask,
     float* __restrict__ dx, int64_t n, const __grid_constant__ GeluDevTable t, int vec) {
@@ -491,7 +491,7 @@ __global__ void __launch_bounds__(kBlock) gelu_bwd_fast_kernel(
     if constexpr (V8) {
         // 256-element chunks: lane L owns elements 8L..8L+7 (one 32-byte
         // vector of y, of dy and of dx) and reads its own mask byte.
-        constexpr int U = TM_GELU_BWD_U8;
+        constexpr int U = U8;
         const uint8_t* mask8 = reinterpret_cast<const uint8_t*>(mask);
         // vec == 0 (pointers not 32-byte aligned): everything through the
         // scalar loop below -- the same evaluator, so the same bits
@@ -600,6 +600,13 @@ __global__ void __launch_bounds__(kBlock) gelu_bwd_fast_kernel(
 
 inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 inline bool aligned32(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 31u) == 0; }
+// below this many elements the 256-bit kernels take one chunk per register
+// group (A/B at configs[0], 3.1 M elements: fwd+bwd 22.5 -> 20.5 us; at the
+// 134 M-element bench shape U = 4 / 2 stay faster: 193 vs 221 us fwd)
+#ifndef TM_GELU_SMALL_N
+#define TM_GELU_SMALL_N (1 << 24)
+#endif
+constexpr int64_t kSmallN = TM_GELU_SMALL_N;
 
 }  // namespace
 
@@ -608,9 +615,12 @@ cudaError_t launch_gelu_fwd(const float* x, float* y, uint32_t* mask, int64_t n,
     if (n == 0) return cudaSuccess;
     const float xs_lo = std::nextafter(xstar_gt, -std::numeric_limits<float>::infinity());
     if (aligned32(x) && aligned32(y) && aligned16(mask)) {
-        constexpr int U = TM_GELU_FWD_U8;
+        // small tensors (configs[0]: 3.1 M elements) balance better with one
+        // chunk per group (the last group of a warp is the tail)
+        const bool small = n < kSmallN;
+        const int U = small ? 1 : TM_GELU_FWD_U8;
         const int64_t warps_needed = ((n >> 8) + U - 1) / U + 1;
-        auto k = gelu_fwd8_kernel<U>;
+        auto k = small ? gelu_fwd8_kernel<1> : gelu_fwd8_kernel<TM_GELU_FWD_U8>;
         int grid = grid_for((const void*)k, kBlock, 0, (warps_needed * 32 + kBlock - 1) / kBlock, 0,
                             TM_GELU_WAVES);
         launch(k, grid, kBlock, 0, st)(x, y, mask, n, xstar_gt, xs_lo);
@@ -638,10 +648,13 @@ cudaError_t launch_gelu_bwd(const float* dy, const float* y, const uint32_t* mas
         const bool v8 = v8a || !vec;  // unaligned: the V8 kernel's scalar loop
         const int vflag = v8a ? 1 : 0;
         const int64_t blocks = ((n >> 7) / 2 + 1) * 32 / kBlock + 1;
+        const bool small = n < kSmallN;  // one chunk per group (see the forward)
 #define TB_CASE(NC)                                                                       \
     case NC: {                                                                            \
-        auto k = v8 ? (hv ? gelu_bwd_fast_kernel<NC, true, true>                            \
-                            : gelu_bwd_fast_kernel<NC, false, true>)                     \
+        auto k = v8 ? (small ? (hv ? gelu_bwd_fast_kernel<NC, true, true, 1>               \
+                                   : gelu_bwd_fast_kernel<NC, false, true, 1>)            \
+                             : (hv ? gelu_bwd_fast_kernel<NC, true, true>                  \
+                                   : gelu_bwd_fast_kernel<NC, false, true>))              \
                     : (hv ? gelu_bwd_fast_kernel<NC, true, false>                        \
                                 : gelu_bwd_fast_kernel<NC, false, false>);               \
         int grid = grid_for((const void*)k, kBlock, 0, blocks, 0, TM_GELU_WAVES);         \

@@ -314,6 +314,196 @@ __global__ void __launch_bounds__(kWWarps * 32, 2) ln_fwd_warp_kernel(
     }
 }
 
+// ---- hidden dropout -> residual add -> LayerNorm, fused (forward) --------
+// The reference layer chains ref_ops::dropout(proj) -> g.add(residual, .) ->
+// tempo_ops::layernorm (encoder.cpp:180-191, 198-210).  Here one pass reads
+// the projection and the residual rows and writes only y, rstd and the mask
+// bits: r = residual + (keep ? float(double(proj) * scale) : 0) is formed in
+// registers (bit-exact with the reference's F32 dropout then add: the
+// dropout product rounds once from fp64 as mask_scale does, kernels.cpp:
+// 285-295, and an fp32 add equals float(double(a) + double(b))), then the
+// in-place LayerNorm of r exactly as ln_fwd_warp_kernel.  Neither the
+// dropout output nor r is stored (the Tempo layer stashes neither).
+// MODE 1: supplied mask; MODE 2: Philox mask generated by global element
+// index (the same bits as tempo_dropout_fwd's) and written.
+// HBM: read proj + residual (8 B) + write y (4 B) + 1 bit per element.
+#ifndef TM_DAL_STAGES
+#define TM_DAL_STAGES 1  // per-warp ring depth (A/B: 1 74.2, 2 75.8, 3 80.4 us at 32768x1024)
+#endif
+constexpr int kDStages = TM_DAL_STAGES;
+
+template <int VPL, int MODE>
+__global__ void __launch_bounds__(kWWarps * 32, 2) dal_fwd_warp_kernel(
+    const float* __restrict__ proj, const float* __restrict__ res, uint32_t* __restrict__ mask,
+    double scale, uint64_t thresh, uint64_t seed, uint64_t offset,
+    const float* __restrict__ gamma, const float* __restrict__ beta, double eps,
+    float* __restrict__ y, float* __restrict__ rstd, int64_t rows, int32_t* __restrict__ status) {
+    grid_dep_wait();  // PDL: predecessor complete and visible
+    grid_dep_launch();
+    constexpr int C = VPL * 128;
+    extern __shared__ __align__(128) unsigned char dsm[];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(dsm) + wid * kDStages;
+    float4* gb = reinterpret_cast<float4*>(dsm + 1024);  // gamma [C/4] then beta [C/4]
+    // per warp: a kDStages-deep TMA ring of projection rows; the residual
+    // row is loaded straight into registers at the top of the row, so its
+    // latency overlaps the mask generation and the ring wait (smem stays
+    // small enough for two CTAs per SM)
+    float* ring = reinterpret_cast<float*>(dsm + 1024 + 2 * C * 4) + wid * kDStages * C;
+    for (int i = threadIdx.x; i < C / 4; i += blockDim.x) {
+        const float4 g = reinterpret_cast<const float4*>(gamma)[i];
+        gb[i] = g;
+        gb[C / 4 + i] = reinterpret_cast<const float4*>(beta)[i];
+        if (status && blockIdx.x == 0 &&
+            (fabs((double)g.x) < kGammaMin || fabs((double)g.y) < kGammaMin ||
+             fabs((double)g.z) < kGammaMin || fabs((double)g.w) < kGammaMin))
+            *status = TEMPO_ERR_PARAM;
+    }
+    const int64_t gw = (int64_t)blockIdx.x * kWWarps + wid;
+    const int64_t nw = (int64_t)gridDim.x * kWWarps;
+    auto issue = [&](int64_t r, int s) {
+        mbar_expect_tx(&bars[s], C * 4);
+        bulk_g2s(ring + s * C, proj + r * C, C * 4, &bars[s]);
+    };
+    if (lane == 0) {
+        for (int s = 0; s < kDStages; ++s) mbar_init(&bars[s], 1);
+        mbar_fence_init();
+    }
+    __syncthreads();  // gamma/beta staged, barriers initialised
+    if (lane == 0) {
+        for (int s = 0; s < kDStages; ++s) {
+            const int64_t r = gw + (int64_t)s * nw;
+            if (r < rows) issue(r, s);
+        }
+    }
+    const float inv_m = 1.0f / (float)C;
+    int it = 0;
+    for (int64_t r = gw; r < rows; r += nw, ++it) {
+        const int st = it % kDStages;
+        float4 v[VPL];
+        const float4* rr = reinterpret_cast<const float4*>(res + r * C);
+#pragma unroll
+        for (int k = 0; k < VPL; ++k) v[k] = ld_stream(rr + k * 32 + lane);
+        uint32_t nib[VPL];
+        uint32_t* mrow = mask + ((r * C) >> 5);  // C % 128 == 0: the row owns whole words
+        if (MODE == 1) {
+#pragma unroll
+            for (int k = 0; k < VPL; ++k) nib[k] = chunk_nibble(mrow + k * 4, lane);
+        } else {
+#pragma unroll
+            for (int k = 0; k < VPL; ++k) {
+                const U4 q = philox_quad(seed, (offset + (uint64_t)(r * C + k * 128 + lane * 4)) >> 2);
+                nib[k] = nibble4((uint64_t)q.x >= thresh, (uint64_t)q.y >= thresh,
+                                 (uint64_t)q.z >= thresh, (uint64_t)q.w >= thresh);
+                store_chunk_mask(mrow + k * 4, nib[k], lane);
+            }
+        }
+        mbar_wait(&bars[st], (uint32_t)((it / kDStages) & 1));
+        const float4* sp = reinterpret_cast<const float4*>(ring + st * C);
+#pragma unroll
+        for (int k = 0; k < VPL; ++k) {
+            const float4 p = sp[k * 32 + lane];
+            v[k].x += (nib[k] & 1u) ? (float)((double)p.x * scale) : 0.0f;
+            v[k].y += (nib[k] & 2u) ? (float)((double)p.y * scale) : 0.0f;
+            v[k].z += (nib[k] & 4u) ? (float)((double)p.z * scale) : 0.0f;
+            v[k].w += (nib[k] & 8u) ? (float)((double)p.w * scale) : 0.0f;
+        }
+        __syncwarp();
+        if (lane == 0) {  // the warp has read stage st: refill it with its next row
+            const int64_t rn = r + (int64_t)kDStages * nw;
+            if (rn < rows) {
+                fence_proxy_async_smem();
+                issue(rn, st);
+            }
+        }
+        float s = 0.0f;
+#pragma unroll
+        for (int k = 0; k < VPL; ++k) s += (v[k].x + v[k].y) + (v[k].z + v[k].w);
+        const float m0 = warp_sumf(s) * inv_m;
+        float q = 0.0f, t = 0.0f;
+#pragma unroll
+        for (int k = 0; k < VPL; ++k) {
+            const float d0 = v[k].x - m0, d1 = v[k].y - m0;
+            const float d2 = v[k].z - m0, d3 = v[k].w - m0;
+            q += fmaf(d0, d0, d1 * d1) + fmaf(d2, d2, d3 * d3);
+            t += (d0 + d1) + (d2 + d3);
+        }
+        float mean, var_f;
+        refine_moments(m0, warp_sumf(t), warp_sumf(q), inv_m, mean, var_f);
+        const float rs = (float)(1.0 / sqrt((double)var_f + eps));  // ops_tempo.cpp:111-112
+        float4* yr = reinterpret_cast<float4*>(y + r * C);
+#pragma unroll
+        for (int k = 0; k < VPL; ++k) {
+            const float4 g = gb[k * 32 + lane], b = gb[C / 4 + k * 32 + lane];
+            float4 o;
+            o.x = fmaf(g.x * rs, v[k].x - mean, b.x);
+            o.y = fmaf(g.y * rs, v[k].y - mean, b.y);
+            o.z = fmaf(g.z * rs, v[k].z - mean, b.z);
+            o.w = fmaf(g.w * rs, v[k].w - mean, b.w);
+            st_stream(yr + k * 32 + lane, o);
+        }
+        if (lane == 0) rstd[r] = rs;
+    }
+}
+
+size_t dal_fwd_smem(int vpl) {
+    return 1024 + 2 * (size_t)vpl * 128 * 4 + (size_t)kWWarps * kDStages * vpl * 128 * 4;
+}
+
+// Generic fused forward (cols % 32 == 0, any length): one CTA per row, the
+// row's r = residual + dropout(proj) materialised in shared memory (fp32,
+// cols floats), then the moments and y as ln_fwd_generic_kernel (fp64
+// sums).  32 consecutive elements of a row are one mask word (ballot).
+__global__ void __launch_bounds__(256) dal_fwd_generic_kernel(
+    const float* __restrict__ proj, const float* __restrict__ res, uint32_t* __restrict__ mask,
+    int mode, double scale, uint64_t thresh, uint64_t seed, uint64_t offset,
+    const float* __restrict__ gamma, const float* __restrict__ beta, double eps,
+    float* __restrict__ y, float* __restrict__ rstd, int64_t rows, int cols,
+    int32_t* __restrict__ status) {
+    grid_dep_wait();
+    grid_dep_launch();
+    extern __shared__ float xr[];  // [cols]
+    __shared__ double red[2 * 32];
+    int phase = 0;
+    const int lane = threadIdx.x & 31;
+    if (status && blockIdx.x == 0) {
+        for (int j = threadIdx.x; j < cols; j += blockDim.x)
+            if (fabs((double)gamma[j]) < kGammaMin) *status = TEMPO_ERR_PARAM;
+    }
+    for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
+        double s[1] = {0.0};
+        for (int j = threadIdx.x; j < cols; j += blockDim.x) {  // cols % 32 == 0: full warps
+            const int64_t i = r * cols + j;
+            bool keep;
+            if (mode == 2) {
+                keep = (uint64_t)philox_at(seed, offset + (uint64_t)i) >= thresh;
+                const uint32_t bits = __ballot_sync(kFull, keep);
+                if (lane == 0) mask[i >> 5] = bits;
+            } else {
+                keep = (mask[i >> 5] >> (i & 31)) & 1u;
+            }
+            const float v = res[i] + (keep ? (float)((double)proj[i] * scale) : 0.0f);
+            xr[j] = v;
+            s[0] += (double)v;
+        }
+        block_sum<1>(s, red, phase);
+        const double mean = s[0] / (double)cols;
+        double q[1] = {0.0};
+        for (int j = threadIdx.x; j < cols; j += blockDim.x) {
+            const double d = (double)xr[j] - mean;
+            q[0] = dadd(q[0], dmul(d, d));
+        }
+        block_sum<1>(q, red, phase);
+        const double mean_f = (double)(float)mean;
+        const float var_f = (float)(q[0] / (double)cols);
+        const double rs = 1.0 / sqrt((double)var_f + eps);
+        for (int j = threadIdx.x; j < cols; j += blockDim.x)
+            y[r * cols + j] = ln_y(xr[j], mean_f, rs, (double)gamma[j], (double)beta[j]);
+        if (threadIdx.x == 0) rstd[r] = (float)rs;
+        __syncthreads();  // xr is rewritten by the next row
+    }
+}
+
 size_t warp_fwd_smem(int vpl) {
     return 1024 + 2 * (size_t)vpl * 128 * 4 + (size_t)kWWarps * kWStages * vpl * 128 * 4;
 }
@@ -357,11 +547,17 @@ __global__ void __launch_bounds__(256) ln_fwd_generic_kernel(
 // Stage 1, vector path: dx per row, per-CTA fp64 column partials of
 // dgamma = sum g*xhat and dbeta = sum g, written to ws[cta][2][cols].
 // Same TMA ring as the forward; a stage holds kRowsB rows of dy and of y.
-template <int NT, int CPT>
+// DROP (the fused dropout -> residual add -> LayerNorm backward): dx is the
+// residual's gradient d(r) and, from the stashed mask bits, the
+// projection's gradient d(proj) = keep ? float(double(dx) * scale) : 0
+// (dropout_backward, ops_reference.cpp:155-161) is written beside it -- one
+// pass instead of LN backward + a dropout backward re-reading dx.
+template <int NT, int CPT, bool DROP = false>
 __global__ void __launch_bounds__(NT) ln_bwd_vec_kernel(
     const float* __restrict__ dy, const float* __restrict__ y, const float* __restrict__ rstd,
     const float* __restrict__ gamma, const float* __restrict__ beta, float* __restrict__ dx,
-    double* __restrict__ ws, int64_t rows, int cols) {
+    double* __restrict__ ws, int64_t rows, int cols, const uint32_t* __restrict__ mask,
+    double scale, float* __restrict__ dproj) {
     grid_dep_wait();  // PDL: predecessor complete and visible
     // persistent grid: let stage 2 (a PDL dependent) get resident in the
     // leftover slots; it waits for us to finish
@@ -423,18 +619,44 @@ __global__ void __launch_bounds__(NT) ln_bwd_vec_kernel(
         }
     }
     const float inv_m = 1.0f / (float)cols;
+    // rstd (and, DROP, the mask words) of a tile are loaded one tile ahead:
+    // they are needed only after the row reduction, and a global load issued
+    // there would stall the whole output loop on its latency
+    float rs_nx[kRowsB];
+    uint32_t mw_nx[kRowsB][CPT];
+    auto prefetch = [&](int64_t t) {
+        const int64_t q0 = t * kRowsB;
+#pragma unroll
+        for (int i = 0; i < kRowsB; ++i) {
+            const bool in = t < ntiles && q0 + i < rows;
+            rs_nx[i] = in ? __ldg(rstd + q0 + i) : 0.f;
+            if (DROP) {
+#pragma unroll
+                for (int c = 0; c < CPT; ++c)
+                    mw_nx[i][c] = (in && act[c]) ? __ldg(mask + (((q0 + i) * cols + 4 * cg[c]) >> 5)) : 0u;
+            }
+        }
+    };
+    prefetch(blockIdx.x);
     int it = 0;
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+        float rsv[kRowsB];
+        uint32_t mwv[kRowsB][CPT];
+#pragma unroll
+        for (int i = 0; i < kRowsB; ++i) {
+            rsv[i] = rs_nx[i];
+#pragma unroll
+            for (int c = 0; c < CPT; ++c) mwv[i][c] = DROP ? mw_nx[i][c] : 0u;
+        }
+        prefetch(tile + gridDim.x);
         const int st = it % kStagesB;
         mbar_wait(&full[st], (uint32_t)((it / kStagesB) & 1));
         const int64_t r0 = tile * kRowsB;
         const float* gs = ring + (2 * st) * tile_floats;
         const float* ys = ring + (2 * st + 1) * tile_floats;
         float4 gv[kRowsB][CPT], yv[kRowsB][CPT];
-        float rsv[kRowsB];
 #pragma unroll
         for (int i = 0; i < kRowsB; ++i) {
-            rsv[i] = (r0 + i < rows) ? __ldg(rstd + r0 + i) : 0.f;
 #pragma unroll
             for (int c = 0; c < CPT; ++c) {
                 gv[i][c] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -498,6 +720,16 @@ __global__ void __launch_bounds__(NT) ln_bwd_vec_kernel(
                 }
                 st_stream(reinterpret_cast<float4*>(dx + (r0 + i) * cols) + cg[c],
                           make_float4(o[0], o[1], o[2], o[3]));
+                if (DROP) {  // 4 elements at a multiple of 4: one nibble of one word
+                    const int64_t e = (r0 + i) * cols + 4 * cg[c];
+                    const uint32_t nb = (mwv[i][c] >> (e & 31)) & 0xfu;
+                    float4 dp;
+                    dp.x = (nb & 1u) ? (float)((double)o[0] * scale) : 0.0f;
+                    dp.y = (nb & 2u) ? (float)((double)o[1] * scale) : 0.0f;
+                    dp.z = (nb & 4u) ? (float)((double)o[2] * scale) : 0.0f;
+                    dp.w = (nb & 8u) ? (float)((double)o[3] * scale) : 0.0f;
+                    st_stream(reinterpret_cast<float4*>(dproj + (r0 + i) * cols) + cg[c], dp);
+                }
             }
         }
     }
@@ -518,7 +750,8 @@ __global__ void __launch_bounds__(NT) ln_bwd_vec_kernel(
 __global__ void __launch_bounds__(256) ln_bwd_generic_kernel(
     const float* __restrict__ dy, const float* __restrict__ y, const float* __restrict__ rstd,
     const float* __restrict__ gamma, const float* __restrict__ beta, float* __restrict__ dx,
-    double* __restrict__ ws, int64_t rows, int cols) {
+    double* __restrict__ ws, int64_t rows, int cols, const uint32_t* __restrict__ mask,
+    double scale, float* __restrict__ dproj) {
     grid_dep_wait();  // PDL: predecessor complete and visible
     grid_dep_launch();
     extern __shared__ double part[];  // [2][cols]
@@ -541,7 +774,12 @@ __global__ void __launch_bounds__(256) ln_bwd_generic_kernel(
         for (int j = threadIdx.x; j < cols; j += blockDim.x) {
             double g = (double)gr[j];
             double xh = ((double)yr[j] - (double)beta[j]) / (double)gamma[j];
-            dx[r * cols + j] = (float)((g * (double)gamma[j] - c1 - xh * c2) * rs);
+            const float o = (float)((g * (double)gamma[j] - c1 - xh * c2) * rs);
+            dx[r * cols + j] = o;
+            if (dproj) {  // fused dropout backward (see ln_bwd_vec_kernel, DROP)
+                const int64_t e = r * cols + j;
+                dproj[e] = ((mask[e >> 5] >> (e & 31)) & 1u) ? (float)((double)o * scale) : 0.0f;
+            }
             part[j] += g * xh;
             part[cols + j] += g;
         }
@@ -718,13 +956,16 @@ int bwd_cpt(int64_t cols) { return (TM_LN_BWD_CPT2 && cols % 8 == 0) ? 2 : 1; }
 int bwd_threads(int64_t cols) {
     return (int)(((cols / 4 + bwd_cpt(cols) - 1) / bwd_cpt(cols) + 31) / 32 * 32);
 }
-const void* bwd_vec_fn(int64_t cols) {
+const void* bwd_vec_fn(int64_t cols, bool drop = false) {
     const int t = bwd_threads(cols);
 #if TM_LN_BWD_CPT2  // (off by default: measured slower; not instantiated)
     if (bwd_cpt(cols) == 2)
         return t <= 256 ? (const void*)ln_bwd_vec_kernel<256, 2>
                         : (const void*)ln_bwd_vec_kernel<kMaxThreads, 2>;
 #endif
+    if (drop)
+        return t <= 256 ? (const void*)ln_bwd_vec_kernel<256, 1, true>
+                        : (const void*)ln_bwd_vec_kernel<kMaxThreads, 1, true>;
     return t <= 256 ? (const void*)ln_bwd_vec_kernel<256, 1>
                     : (const void*)ln_bwd_vec_kernel<kMaxThreads, 1>;
 }
@@ -815,7 +1056,8 @@ size_t ln_bwd_workspace(int64_t rows, int64_t cols) {
 
 cudaError_t launch_ln_bwd(const float* dy, const float* y, const float* rstd, const float* gamma,
                           const float* beta, float* dx, float* dgamma, float* dbeta, void* ws,
-                          int64_t rows, int64_t cols, cudaStream_t st, const LnPeer* peer) {
+                          int64_t rows, int64_t cols, cudaStream_t st, const LnPeer* peer,
+                          const uint32_t* mask, double scale, float* dproj) {
     if (cols == 0) return cudaSuccess;
     if (rows == 0) {
         if (peer) return launch_ln_param_reduce_peer(nullptr, 0, cols, *peer, dgamma, dbeta, st);
@@ -823,24 +1065,71 @@ cudaError_t launch_ln_bwd(const float* dy, const float* y, const float* rstd, co
         cudaMemsetAsync(dbeta, 0, cols * sizeof(float), st);
         return cudaGetLastError();
     }
-    const bool vec = use_vec(cols, dy, y, dx, gamma, beta);
+    const bool drop = dproj != nullptr;
+    const bool vec = use_vec(cols, dy, y, dx, gamma, beta) && (!drop || aligned16(dproj));
+    // the grid (= the workspace's partial rows) is the plain kernel's, also
+    // for the fused variant, so one workspace query serves both
     const int grid = bwd_grid(rows, cols, vec);
     double* w = static_cast<double*>(ws);
     if (vec) {
         using KFn = void (*)(const float*, const float*, const float*, const float*,
-                             const float*, float*, double*, int64_t, int);
-        KFn k = reinterpret_cast<KFn>(const_cast<void*>(bwd_vec_fn(cols)));
+                             const float*, float*, double*, int64_t, int, const uint32_t*, double,
+                             float*);
+        KFn k = reinterpret_cast<KFn>(const_cast<void*>(bwd_vec_fn(cols, drop)));
+        // grid_for also opts the kernel into its dynamic smem size
+        if (drop) (void)grid_for((const void*)k, bwd_threads(cols), bwd_smem(cols), grid);
         launch(k, grid, bwd_threads(cols), bwd_smem(cols), st)(dy, y, rstd, gamma, beta, dx, w, rows,
-                                                           (int)cols);
+                                                           (int)cols, mask, scale, dproj);
     } else {
         size_t smem = (size_t)2 * cols * sizeof(double);
         launch(ln_bwd_generic_kernel, grid, 256, smem, st)(dy, y, rstd, gamma, beta, dx, w, rows,
-                                                       (int)cols);
+                                                       (int)cols, mask, scale, dproj);
     }
     if (peer) return launch_ln_param_reduce_peer(w, grid, cols, *peer, dgamma, dbeta, st);
     const int rgrid = (int)((2 * cols + 31) / 32);
     return launch_pdl((const void*)ln_param_reduce_kernel, rgrid, 1024, 0, st,
                       (const double*)w, grid, (int)cols, dgamma, dbeta);
+}
+
+cudaError_t launch_dal_fwd(const float* proj, const float* res, double scale, uint64_t thresh,
+                           int philox, uint32_t* mask, uint64_t seed, uint64_t offset,
+                           const float* gamma, const float* beta, double eps, float* y,
+                           float* rstd, int64_t rows, int64_t cols, int32_t* dev_status,
+                           cudaStream_t st) {
+    if (rows == 0) return cudaSuccess;
+    const int vpl = (int)(cols / 128);
+    const bool warp_ok = cols % 128 == 0 && vpl >= 1 && vpl <= 8 && aligned16(proj) &&
+                         aligned16(res) && aligned16(y) && aligned16(gamma) && aligned16(beta) &&
+                         (offset & 3u) == 0;
+    if (warp_ok) {
+        const size_t smem = dal_fwd_smem(vpl);
+#define TB_DAL(V)                                                                            \
+    case V: {                                                                                \
+        auto k = philox ? dal_fwd_warp_kernel<V, 2> : dal_fwd_warp_kernel<V, 1>;              \
+        int grid = grid_for((const void*)k, kWWarps * 32, smem, (rows + kWWarps - 1) / kWWarps, 0, TM_LN_WAVES); \
+        launch(k, grid, kWWarps * 32, smem, st)(proj, res, mask, scale, thresh, seed, offset,    \
+                                                gamma, beta, eps, y, rstd, rows, dev_status);    \
+        break;                                                                               \
+    }
+        switch (vpl) {
+            TB_DAL(1)
+            TB_DAL(2)
+            TB_DAL(3)
+            TB_DAL(4)
+            TB_DAL(5)
+            TB_DAL(6)
+            TB_DAL(7)
+            TB_DAL(8)
+        }
+#undef TB_DAL
+        return cudaGetLastError();
+    }
+    const size_t smem = (size_t)cols * sizeof(float);
+    int grid = grid_for((const void*)dal_fwd_generic_kernel, 256, smem, rows);
+    launch(dal_fwd_generic_kernel, grid, 256, smem, st)(proj, res, mask, philox ? 2 : 1, scale,
+                                                        thresh, seed, offset, gamma, beta, eps, y,
+                                                        rstd, rows, (int)cols, dev_status);
+    return cudaGetLastError();
 }
 
 }  // namespace tb

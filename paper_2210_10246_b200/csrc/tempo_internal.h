@@ -75,7 +75,14 @@ cudaError_t launch_ln_param_reduce_peer(const double* partials, int64_t nparts, 
 cudaError_t launch_ln_bwd(const float* dy, const float* y, const float* rstd, const float* gamma,
                           const float* beta, float* dx, float* dgamma, float* dbeta, void* ws,
                           int64_t rows, int64_t cols, cudaStream_t st,
-                          const LnPeer* peer = nullptr);
+                          const LnPeer* peer = nullptr, const uint32_t* mask = nullptr,
+                          double scale = 1.0, float* dproj = nullptr);
+// hidden dropout -> residual add -> LayerNorm forward, fused (cols % 32 == 0)
+cudaError_t launch_dal_fwd(const float* proj, const float* res, double scale, uint64_t thresh,
+                           int philox, uint32_t* mask, uint64_t seed, uint64_t offset,
+                           const float* gamma, const float* beta, double eps, float* y,
+                           float* rstd, int64_t rows, int64_t cols, int32_t* dev_status,
+                           cudaStream_t st);
 
 cudaError_t launch_softmax_fwd(const float* z, float* P, int64_t rows, int64_t cols,
                                cudaStream_t st);

@@ -522,6 +522,67 @@ def dropout_fwd(x: torch.Tensor, p: float, mask: torch.Tensor = None, seed: int 
     return y, mask
 
 
+def dropout_add_layernorm_fwd(proj: torch.Tensor, residual: torch.Tensor, gamma: torch.Tensor,
+                              beta: torch.Tensor, p: float, mask: torch.Tensor = None,
+                              seed: int = 0, offset: int = 0, generate: bool = None,
+                              eps: float = 1e-5, check_gamma: bool = True, y: torch.Tensor = None,
+                              rstd: torch.Tensor = None, dev_status: torch.Tensor = None):
+    """The reference layer's ref_ops::dropout -> add -> tempo_ops::layernorm
+    (encoder.cpp:180-191, 198-210) in one pass: y = LN(residual +
+    dropout(proj)).  Returns (y, rstd, mask); stash = y + rstd + mask bits.
+    generate=True (default without a mask): Philox mask by global element
+    index `offset + i`, the same bits dropout_fwd would draw."""
+    proj = _f32(proj, "proj")
+    residual = _f32(residual, "residual", proj.device, proj.numel())
+    rows, cols = _rows_cols(proj)
+    gamma, beta = _f32(gamma, "gamma", proj.device, cols), _f32(beta, "beta", proj.device, cols)
+    if check_gamma:
+        ln_check_gamma(gamma)
+    if generate is None:
+        generate = mask is None
+    if mask is None and not generate:
+        raise TempoError(2, "mask: a supplied-mask forward needs the mask")
+    mask = _mask(mask, "mask", proj.numel(), proj.device)
+    y = _out(y, "y", proj)
+    rstd = torch.empty(proj.shape[:-1], dtype=torch.float32, device=proj.device) if rstd is None \
+        else _f32(rstd, "rstd", proj.device, rows)
+    if dev_status is not None:
+        _dev(dev_status, "dev_status", torch.int32, proj.device, 1)
+    check(lib().tempo_dropout_add_ln_fwd(
+        _ptr(proj), _ptr(residual), float(p), MASK_PHILOX if generate else MASK_SUPPLIED,
+        _ptr(mask), int(seed), int(offset), _ptr(gamma), _ptr(beta), float(eps), _ptr(y),
+        _ptr(rstd), rows, cols, _ptr(dev_status), _stream()))
+    return y, rstd, mask
+
+
+def dropout_add_layernorm_bwd(dy: torch.Tensor, y: torch.Tensor, rstd: torch.Tensor,
+                              gamma: torch.Tensor, beta: torch.Tensor, mask: torch.Tensor,
+                              p: float, d_residual: torch.Tensor = None,
+                              d_proj: torch.Tensor = None, dgamma: torch.Tensor = None,
+                              dbeta: torch.Tensor = None, workspace: torch.Tensor = None,
+                              peer: "LnPeerRank" = None):
+    """Backward of dropout_add_layernorm_fwd in one pass: returns (d_residual,
+    d_proj, dgamma, dbeta); d_residual = the LayerNorm input gradient,
+    d_proj = mask ? d_residual / (1-p) : 0.  With `peer`, dgamma/dbeta are
+    summed over its ranks (as layernorm_ip_bwd_peer)."""
+    dy, y, rstd, gamma, beta, d_res, dgamma, dbeta, ws, nbytes, rows, cols = _ln_bwd_args(
+        dy, y, rstd, gamma, beta, d_residual, dgamma, dbeta, workspace)
+    if mask is None:
+        raise TempoError(2, "mask: the forward's bit mask is required")
+    mask = _mask(mask, "mask", y.numel(), y.device)
+    d_proj = _out(d_proj, "d_proj", dy)
+    st = None
+    if peer is not None:
+        if cols != peer.cols:
+            raise TempoError(2, f"peer exchange set up for {peer.cols} columns, got {cols}")
+        st = peer.next_struct()
+    check(lib().tempo_dropout_add_ln_bwd(
+        _ptr(dy), _ptr(y), _ptr(rstd), _ptr(gamma), _ptr(beta), _ptr(mask), float(p),
+        _ptr(d_res), _ptr(d_proj), _ptr(dgamma), _ptr(dbeta), _ptr(ws), nbytes, rows, cols,
+        C.byref(st) if st is not None else None, _stream()))
+    return d_res, d_proj, dgamma, dbeta
+
+
 def dropout_bwd(dy: torch.Tensor, mask: torch.Tensor, p: float,
                 dx: torch.Tensor = None) -> torch.Tensor:
     dy = _f32(dy, "dy")

@@ -118,3 +118,49 @@ def test_empty_inputs_are_noops(tops, table_text, cuda):
     yd, md = tops.dropout_fwd(e, 0.1, seed=1)
     assert tops.dropout_bwd(e, md, 0.1).numel() == 0
     torch.cuda.synchronize()
+
+
+def test_cfg4_fused_layer_chain_full(tops, port, cuda):
+    """configs[3] with the fused hidden dropout -> residual add -> LayerNorm
+    ops (bench.py's default chain): one forward+backward at full size, the
+    LN rows on a subset against the oracle composition (dropout_apply, fp32
+    add, ln_fwd / ln_bwd), d_proj bit-exact from d_residual and the mask,
+    dgamma/dbeta of both LNs against the F64 oracle, and bitwise run to run."""
+    import torch
+    import bench
+    chain = bench.Chain(cuda, 0, 1, fused=True)
+    chain.step()
+    torch.cuda.synchronize()
+    T, H, p = bench.T, bench.H, bench.P_DROP
+    sel = np.sort(np.random.default_rng(2).choice(T, 256, replace=False))
+    g1, b1 = chain.g1.cpu().numpy(), chain.b1.cpu().numpy()
+    g2, b2 = chain.g2.cpu().numpy(), chain.b2.cpu().numpy()
+    y1 = chain.y_ln1.cpu().numpy()
+    for proj, res, m, g, b, y, rs in [
+            (chain.x_attn_out, chain.x_res, chain.m1, g1, b1, y1, chain.rs1),
+            (chain.x_ffn2, chain.y_ln1, chain.m2, g2, b2, chain.y_ln2.cpu().numpy(), chain.rs2)]:
+        keep = unpack_rows(m, T, H, sel)
+        r = (res.cpu().numpy()[sel] +
+             port.dropout_apply(proj.cpu().numpy()[sel], keep, p)).astype(np.float32)
+        ry, rrs, _ = port.ln_fwd(r, g, b, 1e-5)
+        assert rel_err(y[sel], ry) <= 1e-5
+        assert np.abs(rs.cpu().numpy()[sel].astype(np.float64) / rrs - 1).max() <= 1e-6
+    # backward of LN1's pair: d_residual rows, d_proj bit-exact, dgamma/dbeta whole
+    dp = chain.dparams.cpu().numpy()
+    for dy, y, rs, g, b, m, d_res, d_proj, sl in [
+            (chain.dy_ln1, y1, chain.rs1, g1, b1, chain.m1, chain.dx_res, chain.dx_d1, slice(2 * H, 4 * H)),
+            (chain.dy_ln2, chain.y_ln2.cpu().numpy(), chain.rs2, g2, b2, chain.m2, chain.dx_ln2,
+             chain.dx_d2, slice(0, 2 * H))]:
+        dyn, rsn = dy.cpu().numpy(), rs.cpu().numpy()
+        rdx, _, _ = port.ln_bwd(dyn[sel], y[sel], rsn[sel], g, b, False)
+        dres = d_res.cpu().numpy()
+        assert rel_err(dres[sel], rdx) <= 1e-5
+        keep = unpack_rows(m, T, H, sel)
+        assert np.array_equal(d_proj.cpu().numpy()[sel], port.dropout_apply(dres[sel], keep, p))
+        _, dg64, db64 = port.ln_bwd(dyn, y, rsn, g, b, True)
+        assert rel_err(dp[sl][:H], dg64) <= 1e-5 and rel_err(dp[sl][H:], db64) <= 1e-5
+    before = chain.dparams.clone()
+    chain.step_idx -= 1
+    chain.step()
+    torch.cuda.synchronize()
+    assert torch.equal(before, chain.dparams)

@@ -52,8 +52,13 @@ def main():
         "copy_g": (lambda: c.y_g.copy_(c.x_ffn1), [c.y_g[:1]]),
         "copy_h": (lambda: c.d2.copy_(c.x_ffn2), [c.d2[:1]]),
         "dropout_bwd": (lambda: o.dropout_bwd(c.dx_ln2, c.m2, bench.P_DROP, dx=c.dx_d2), [c.dx_d2]),
+        "dal_fwd": (lambda: o.dropout_add_layernorm_fwd(c.x_ffn2, c.y_ln1, c.g2, c.b2, bench.P_DROP, mask=c.m2, generate=True, seed=9, check_gamma=False, y=c.y_ln2, rstd=c.rs2), [c.y_ln2, c.rs2, c.m2]),
+        "dal_bwd": (lambda: o.dropout_add_layernorm_bwd(c.dy_ln2, c.y_ln2, c.rs2, c.g2, c.b2, c.m2, bench.P_DROP, d_residual=c.dx_ln2, d_proj=c.dx_d2, dgamma=dp[:H], dbeta=dp[H:2 * H], workspace=c.ws), [c.dx_ln2, c.dx_d2, dp[:2 * H]]),
     }
     ob = bench.op_bytes()
+    obf = bench.op_bytes(fused=True)
+    ob["dal_fwd"] = obf["dropout_add_layernorm_fwd"]
+    ob["dal_bwd"] = obf["dropout_add_layernorm_bwd"]
     ob["copy_g"] = 8 * c.x_ffn1.numel()
     ob["mt_mask"] = c.z.numel() / 8
     ob["mt_mask_h"] = c.x_ffn2.numel() / 8
@@ -75,7 +80,7 @@ def main():
             ts.append(a.elapsed_time(b))
         t = bench.trimmed_mean(ts)
         key = names.get(name, name)
-        nbytes = ob[key] / (2 if key in ("layernorm_fwd", "layernorm_bwd", "dropout_fwd", "dropout_bwd", "copy_h") else 1)
+        nbytes = ob[key] / (2 if key in ("layernorm_fwd", "layernorm_bwd", "dropout_fwd", "dropout_bwd", "copy_h", "dal_fwd", "dal_bwd") else 1)
         h = hashlib.sha1()
         parts = []
         for t_ in outs:
