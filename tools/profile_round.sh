@@ -8,10 +8,10 @@
 set -u
 R=${1:-r1}
 mkdir -p gpurun_out
-KRE='regex:(gelu_|ln_|softmax_|dropout_|mask_|add_kernel)'
+KRE='regex:(gelu_|ln_|softmax_|dropout_|dal_|mask_|add_kernel)'
 timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum \
     --clock-control none -k "$KRE" -c 40 --csv --log-file gpurun_out/launches_$R.csv \
     python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e > gpurun_out/ncu_launches_$R.log 2>&1
-timeout 1500 ncu --set full --clock-control none --import-source on -k "$KRE" -s 14 -c 9 \
+timeout 1500 ncu --set full --clock-control none --import-source on -k "$KRE" -s 10 -c 19 \
     -o gpurun_out/prof_$R python tools/profile_ops.py > gpurun_out/ncu_full_$R.log 2>&1
 echo "profile_round $R done"

@@ -29,6 +29,8 @@ OP_OF_KERNEL = [  # kernel name prefix -> bench op
     ("gelu_bwd_fast_kernel", "gelu_bwd"),
     ("ln_fwd_vec_kernel", "layernorm_fwd"),
     ("ln_fwd_warp_kernel", "layernorm_fwd"),
+    ("ln_bwd_vec_kernel<256, 1, 1>", "dropout_add_layernorm_bwd"),
+    ("dal_fwd_warp_kernel", "dropout_add_layernorm_fwd"),
     ("ln_bwd_vec_kernel", "layernorm_bwd"),
     ("ln_param_reduce_kernel", "layernorm_bwd"),
     ("dropout_fwd_vec_kernel<1>", "dropout_fwd"),
@@ -77,7 +79,9 @@ def main(r):
         open(tmp, "w").write(raw)
         recs = ncu_summary.main(tmp)
         json.dump(recs, open(os.path.join(prof, f"{r}_ncu_full.json"), "w"), indent=1)
-        lines = [f"# {r}: ncu --set full, bench shapes (BERT-large layer, B=64)", "",
+        lines = [f"# {r}: ncu --set full, bench shapes (BERT-large layer, B=64; "
+                 "tools/profile_ops.py: the fused chain's ops, then the unfused LN/dropout ops, "
+                 "then configs[0..2])", "",
                  "| kernel | us | DRAM read MB | DRAM write MB | DRAM % (ncu peak) | issue % | "
                  "warps active % | regs |", "|---|---|---|---|---|---|---|---|"]
         traffic = {}
