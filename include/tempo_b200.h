@@ -236,6 +236,23 @@ int tempo_dropout_fwd(const float* x, double p, tempo_mask_mode_t mode, uint32_t
 int tempo_dropout_bwd(const float* dy, const uint32_t* mask, double p, float* dx, int64_t n,
                       tempo_stream_t stream);
 
+/* The dropout recompute fused into its consumer: the
+ * attention-context GEMM's input gradient dV = D^T @ dO, per (batch, head),
+ * where D = keep ? float(double(P) / (1-p)) : 0 is rebuilt tile by tile in
+ * the GEMM's shared-memory operand staging from the stashed P and mask --
+ * the consumer's BackwardCtx::stash of the "dropout-rescale" recipe
+ * (graph.cpp:46-50, tape.cpp:244-264, ops_tempo.cpp:17-26) without D ever
+ * reaching HBM.  P: [heads][s_q][s_k] (the softmax output, row = query),
+ * mask: its bit-packed keep bits (global element order), dO: [heads][s_q][d],
+ * dV: [heads][s_k][d]; fp32 in and out, computed on the tcgen05 tensor
+ * cores in 3xTF32 (within 1e-6 relative of the fp64 product).  Pair with
+ * tempo_attn_probs_bwd(..., D_out = NULL).  Needs s_q % 32 == 0,
+ * s_k % 256 == 0, d in {32, 64, 128} (else TEMPO_ERR_UNSUPPORTED) and
+ * 16-byte aligned P, dO, dV. */
+int tempo_attn_dropout_dv(const float* P, const uint32_t* mask, double p, const float* dO,
+                          float* dV, int64_t heads, int64_t s_q, int64_t s_k, int64_t d,
+                          tempo_stream_t stream);
+
 /* ---------------------------------------------------------------------- */
 /* Hidden dropout -> residual add -> In-Place LayerNorm, fused             */
 /* (the reference layer's ref_ops::dropout -> Graph::add ->                */

@@ -809,6 +809,25 @@ int tempo_attn_probs_bwd(const float* dD, const float* P, const uint32_t* mask, 
 }
 
 // ---- dropout -------------------------------------------------------------------
+int tempo_attn_dropout_dv(const float* P, const uint32_t* mask, double p, const float* dO,
+                          float* dV, int64_t heads, int64_t s_q, int64_t s_k, int64_t d,
+                          tempo_stream_t stream) {
+    if (heads < 0 || s_q < 0 || s_k < 0 || d < 0)
+        return fail(TEMPO_ERR_DIMENSION, "attn_dropout_dv: negative shape");
+    if (int rc = check_p(p)) return rc;
+    if (heads == 0) return TEMPO_OK;
+    if (!tb::dv_gemm_supported(s_q, s_k, d))
+        return fail(TEMPO_ERR_UNSUPPORTED,
+                    "attn_dropout_dv needs s_q % 32 == 0, s_k % 256 == 0 and d in {32, 64, 128}; "
+                    "use tempo_attn_probs_bwd with D_out and a GEMM");
+    if (!P || !mask || !dO || !dV) return fail(TEMPO_ERR_PARAM, "attn_dropout_dv: null pointer");
+    if (((uintptr_t)P | (uintptr_t)dO | (uintptr_t)dV) & 15u)
+        return fail(TEMPO_ERR_ALIGNMENT, "attn_dropout_dv: P, dO and dV must be 16-byte aligned");
+    return cuda_status(tb::launch_dv_recompute_gemm(P, mask, 1.0 / (1.0 - p), dO, dV, heads, s_q,
+                                                    s_k, d, S(stream)),
+                       "tempo_attn_dropout_dv");
+}
+
 int tempo_dropout_add_ln_fwd(const float* proj, const float* residual, double p,
                              tempo_mask_mode_t mode, uint32_t* mask, uint64_t seed,
                              uint64_t offset, const float* gamma, const float* beta, double eps,

@@ -95,6 +95,13 @@ cudaError_t launch_attn_probs_bwd(const float* dD, const float* P, const uint32_
                                   double scale, float* dZ, float* D, int64_t rows, int64_t cols,
                                   cudaStream_t st);
 
+// dV = D^T dO with D rebuilt from P and the mask in the GEMM's operand
+// staging (dv_gemm_kernels.cu; tcgen05, 3xTF32)
+bool dv_gemm_supported(int64_t s_q, int64_t s_k, int64_t d);
+cudaError_t launch_dv_recompute_gemm(const float* P, const uint32_t* mask, double scale,
+                                     const float* dO, float* dV, int64_t heads, int64_t s_q,
+                                     int64_t s_k, int64_t d, cudaStream_t st);
+
 cudaError_t launch_dropout_fwd(const float* x, double scale, uint64_t thresh, int philox,
                                uint32_t* mask, uint64_t seed, uint64_t offset, float* y, int64_t n,
                                cudaStream_t st);

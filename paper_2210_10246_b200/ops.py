@@ -522,6 +522,35 @@ def dropout_fwd(x: torch.Tensor, p: float, mask: torch.Tensor = None, seed: int 
     return y, mask
 
 
+def attn_dropout_dv(P: torch.Tensor, mask: torch.Tensor, p: float, dO: torch.Tensor,
+                    dV: torch.Tensor = None) -> torch.Tensor:
+    """dV = D^T @ dO per (batch, head) with the dropped-out map D = mask ?
+    P/(1-p) : 0 rebuilt inside the tcgen05 GEMM from the stashed P and mask
+    (the consumer of Sub-Layer Dropout Recomputation, graph.cpp:46-50 ->
+    ops_tempo.cpp:17-26), D never written to HBM.  P [..., s_q, s_k],
+    dO [..., s_q, d] -> dV [..., s_k, d]."""
+    P = _f32(P, "P")
+    if P.dim() < 2:
+        raise TempoError(2, "P: expected [..., s_q, s_k]")
+    s_q, s_k = P.shape[-2], P.shape[-1]
+    heads = P.numel() // max(1, s_q * s_k)
+    dO = _f32(dO, "dO", P.device)
+    if dO.dim() != P.dim() or dO.shape[:-1] != P.shape[:-1]:
+        raise TempoError(2, f"dO {tuple(dO.shape)} does not match P {tuple(P.shape)}")
+    d = dO.shape[-1]
+    if mask is None:
+        raise TempoError(2, "mask: the forward's bit mask is required")
+    mask = _mask(mask, "mask", P.numel(), P.device)
+    shape = tuple(P.shape[:-2]) + (s_k, d)
+    if dV is None:
+        dV = torch.empty(shape, dtype=torch.float32, device=P.device)
+    else:
+        _f32(dV, "dV", P.device, heads * s_k * d)
+    check(lib().tempo_attn_dropout_dv(_ptr(P), _ptr(mask), float(p), _ptr(dO), _ptr(dV), heads,
+                                      s_q, s_k, d, _stream()))
+    return dV
+
+
 def dropout_add_layernorm_fwd(proj: torch.Tensor, residual: torch.Tensor, gamma: torch.Tensor,
                               beta: torch.Tensor, p: float, mask: torch.Tensor = None,
                               seed: int = 0, offset: int = 0, generate: bool = None,

@@ -1,0 +1,92 @@
+"""The dropout recompute fused into the dV GEMM (tempo_attn_dropout_dv,
+tcgen05 3xTF32): dV = D^T @ dO with D = keep ? P/(1-p) : 0 rebuilt from the
+stashed P and mask inside the GEMM, against the oracle composition
+(port.dropout_apply -> fp64 D^T dO, rounded once).
+
+Tolerance: rel_err (the reference's |a-b|/max(1,|a|,|b|)) <= 1e-5, and
+elementwise |a-b| <= 1e-5 * (|ref| + sum_i |D_ij dO_ic|), the usual GEMM
+bound -- 3xTF32 products carry ~2^-21 relative error each and the tensor
+core's fp32 accumulation over K adds its own rounding (measured ~2e-6 of
+sum |D dO| at K = 512)."""
+import numpy as np
+import pytest
+
+from test_gpu_parity import bits_to_dev, rel_err, to_dev
+
+pytestmark = pytest.mark.gpu
+
+
+def case(heads, s_q, s_k, d, p, seed):
+    g = np.random.default_rng(seed)
+    z = g.standard_normal((heads, s_q, s_k)) * 2
+    P = np.exp(z - z.max(-1, keepdims=True))
+    P = (P / P.sum(-1, keepdims=True)).astype(np.float32)
+    dO = g.standard_normal((heads, s_q, d)).astype(np.float32)
+    keep = (g.random(heads * s_q * s_k) >= p).astype(np.uint8)
+    return P, dO, keep
+
+
+def pack(keep):
+    b = np.packbits(keep, bitorder="little")
+    b = np.concatenate([b, np.zeros((-b.size) % 4, np.uint8)])
+    return b.view(np.uint32)[:(keep.size + 31) // 32]
+
+
+@pytest.mark.parametrize("heads,s_q,s_k,d,p", [(3, 512, 512, 64, 0.1), (2, 512, 512, 32, 0.1),
+                                               (2, 256, 512, 128, 0.1), (1, 32, 256, 64, 0.5),
+                                               (5, 384, 256, 64, 0.0), (2, 1024, 512, 64, 0.1)])
+def test_dv_matches_oracle_composition(tops, port, cuda, heads, s_q, s_k, d, p):
+    import torch
+    P, dO, keep = case(heads, s_q, s_k, d, p, heads * s_q + d)
+    dV = tops.attn_dropout_dv(to_dev(P, cuda), bits_to_dev(pack(keep), cuda), p, to_dev(dO, cuda))
+    torch.cuda.synchronize()
+    D = port.dropout_apply(P.reshape(-1), keep, p).reshape(P.shape).astype(np.float64)
+    ref = np.einsum("hij,hic->hjc", D, dO.astype(np.float64))
+    mag = np.einsum("hij,hic->hjc", np.abs(D), np.abs(dO.astype(np.float64)))
+    got = dV.cpu().numpy().astype(np.float64)
+    assert rel_err(got, ref.astype(np.float32)) <= 1e-5
+    assert np.all(np.abs(got - ref) <= 1e-5 * (np.abs(ref) + mag))
+
+
+def test_dv_equals_materialised_d_gemm(tops, cuda):
+    """Against the unfused path: attn_probs_bwd's recomputed D (bitwise the
+    forward D) fed to an fp32 cuBLAS GEMM (TF32 off)."""
+    import torch
+    heads, s, d, p = 4, 512, 64, 0.1
+    g = torch.Generator(device=cuda)
+    g.manual_seed(11)
+    z = torch.randn(heads * s, s, device=cuda, generator=g)
+    P, D, m = tops.softmax_dropout_fwd(z, p, seed=3)
+    dO = torch.randn(heads, s, d, device=cuda, generator=g)
+    dV = tops.attn_dropout_dv(P.view(heads, s, s), m, p, dO)
+    prev = torch.backends.cuda.matmul.allow_tf32
+    torch.backends.cuda.matmul.allow_tf32 = False
+    try:
+        ref = torch.matmul(D.view(heads, s, s).transpose(1, 2), dO)
+    finally:
+        torch.backends.cuda.matmul.allow_tf32 = prev
+    torch.cuda.synchronize()
+    assert rel_err(dV.cpu().numpy(), ref.cpu().numpy()) <= 1e-5
+
+
+def test_dv_refusals(tops, cuda):
+    import torch
+    from paper_2210_10246_b200 import TempoError
+    P = torch.rand(1, 64, 200, device=cuda)
+    dO = torch.rand(1, 64, 64, device=cuda)
+    m = torch.zeros(64 * 200 // 32 + 1, dtype=torch.int32, device=cuda)
+    with pytest.raises(TempoError) as e:
+        tops.attn_dropout_dv(P, m, 0.1, dO)  # s_k % 256 != 0
+    assert e.value.kind == "Unsupported"
+
+
+def test_umma_probe_layouts():
+    """tests/tools/umma_probe: tcgen05 kind::tf32 on K-major SWIZZLE_128B
+    operands is exact (the layout dv_gemm_kernels.cu stages), MN-major gives
+    no result on this part (why the kernel transposes while staging)."""
+    import os
+    import subprocess
+    exe = os.path.join(os.path.dirname(__file__), "tools", "_build", "umma_probe")
+    out = subprocess.run([exe], capture_output=True, text=True, timeout=120).stdout
+    lines = {int(l.split()[1]): l for l in out.splitlines() if l.startswith("variant")}
+    assert "max|err|=0 " in lines[0]

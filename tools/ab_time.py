@@ -55,7 +55,31 @@ def main():
         "dal_fwd": (lambda: o.dropout_add_layernorm_fwd(c.x_ffn2, c.y_ln1, c.g2, c.b2, bench.P_DROP, mask=c.m2, generate=True, seed=9, check_gamma=False, y=c.y_ln2, rstd=c.rs2), [c.y_ln2, c.rs2, c.m2]),
         "dal_bwd": (lambda: o.dropout_add_layernorm_bwd(c.dy_ln2, c.y_ln2, c.rs2, c.g2, c.b2, c.m2, bench.P_DROP, d_residual=c.dx_ln2, d_proj=c.dx_d2, dgamma=dp[:H], dbeta=dp[H:2 * H], workspace=c.ws), [c.dx_ln2, c.dx_d2, dp[:2 * H]]),
     }
+    heads = bench.B * bench.A
+    dO = torch.randn(heads, bench.S, 64, device=dev)
+    dV = torch.empty(heads, bench.S, 64, device=dev)
+    torch.backends.cuda.matmul.allow_tf32 = False
+
+    def dv_unfused():  # D materialised by attn_probs_bwd, then an fp32 cuBLAS GEMM
+        o.attn_probs_bwd(c.dD, c.P, c.m_att, bench.P_DROP, write_d=True, dZ=c.dZ, D=c.Drec)
+        torch.matmul(c.Drec.view(heads, bench.S, bench.S).transpose(1, 2), dO, out=dV)
+
+    def dv_fused():  # no D: the tcgen05 GEMM rebuilds it from P and the mask
+        o.attn_probs_bwd(c.dD, c.P, c.m_att, bench.P_DROP, write_d=False, dZ=c.dZ)
+        o.attn_dropout_dv(c.P.view(heads, bench.S, bench.S), c.m_att, bench.P_DROP, dO, dV=dV)
+
+    calls["dv_unfused"] = (dv_unfused, [dV])
+    calls["dv_fused"] = (dv_fused, [dV])
+    calls["dv_gemm_only"] = (lambda: o.attn_dropout_dv(c.P.view(heads, bench.S, bench.S), c.m_att, bench.P_DROP, dO, dV=dV), [dV])
+    calls["cublas_dv_only"] = (lambda: torch.matmul(c.Drec.view(heads, bench.S, bench.S).transpose(1, 2), dO, out=dV), [dV])
+    calls["attn_bwd_noD"] = (lambda: o.attn_probs_bwd(c.dD, c.P, c.m_att, bench.P_DROP, write_d=False, dZ=c.dZ), [c.dZ])
     ob = bench.op_bytes()
+    n_a = c.P.numel()
+    ob["dv_unfused"] = n_a * 16.125 + n_a * 4 + dO.numel() * 8
+    ob["dv_fused"] = n_a * 12.125 + n_a * 4.125 + dO.numel() * 8
+    ob["dv_gemm_only"] = n_a * 4.125 + dO.numel() * 8
+    ob["cublas_dv_only"] = n_a * 4 + dO.numel() * 8
+    ob["attn_bwd_noD"] = n_a * 12.125
     obf = bench.op_bytes(fused=True)
     ob["dal_fwd"] = obf["dropout_add_layernorm_fwd"]
     ob["dal_bwd"] = obf["dropout_add_layernorm_bwd"]
