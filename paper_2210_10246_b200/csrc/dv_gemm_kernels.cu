@@ -41,6 +41,11 @@
 //     the last stage, -> acc_full;
 //   epilogue: the producer warps tcgen05.ld their TMEM lane quadrant
 //     (warp w: accumulator w/4, lanes 32*(w%4)..) and store dV rows.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <mutex>
+
 #include "common.cuh"
 #include "tempo_internal.h"
 
@@ -304,6 +309,271 @@ __global__ void __launch_bounds__(kThreadsG, 1) dv_recompute_gemm_kernel(
     }
 }
 
+// ---- v2: bulk-copy staging ----------------------------------------------
+// The register-prefetch producers above keep only ~40 KB per SM in flight
+// (one K-chunk of 32 rows per thread): the kernel waits on DRAM latency
+// (2.1 TB/s).  Here a loader lane streams 16-row slices of P, their mask
+// words and dO into a kSS-deep shared-memory staging ring with cp.async.bulk
+// (mbarrier completion, ~100 KB in flight per SM), 16 producer warps
+// transpose each slice from the ring (a warp reads 32 consecutive floats of a
+// row: conflict-free) into a kOS-deep ring of K-major SWIZZLE_64B operand
+// tiles (16 K-rows = 64-byte rows, 8-row 512-byte atoms), and the MMA lane
+// issues 2 K-steps x 2 M-blocks x 3 products per slice.  The dropout scale
+// 1/(1-p) is applied to dV in the epilogue, so staging D' = keep ? P : 0 is
+// a select.
+constexpr int kBKs = 16;  // K rows per staging slice = per operand stage
+constexpr int kSP = 512;  // 16 producer warps: 2 per dV row, 8 K-rows each
+
+__device__ __forceinline__ uint32_t sw64_k_offset(int mn, int kchunk) {
+    // byte offset of 16-byte K-chunk `kchunk` (< 4) of row mn, K-major
+    // SWIZZLE_64B: [mn/8][mn%8][64 B], chunk ^ ((mn%8) >> 1) (Swizzle<2,4,3>)
+    const int row = mn & 7;
+    return (uint32_t)((mn >> 3) * 512 + row * 64 + ((kchunk ^ (row >> 1)) << 4));
+}
+__device__ __forceinline__ uint64_t umma_desc_sw64(uint32_t smem_addr, uint32_t sbo_bytes) {
+    uint64_t d = 0;
+    d |= (uint64_t)((smem_addr >> 4) & 0x3fff);
+    d |= (uint64_t)1 << 16;  // LBO (unused for swizzled K-major)
+    d |= (uint64_t)((sbo_bytes >> 4) & 0x3fff) << 32;
+    d |= (uint64_t)1 << 46;  // version
+    d |= (uint64_t)4 << 61;  // SWIZZLE_64B
+    return d;
+}
+__device__ __forceinline__ void sts128(uint32_t addr, float a, float b, float c, float d) {
+    asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(addr), "f"(a), "f"(b), "f"(c),
+                 "f"(d)
+                 : "memory");
+}
+__device__ __forceinline__ void sts64(uint32_t addr, float a, float b) {
+    asm volatile("st.shared.v2.f32 [%0], {%1,%2};" ::"r"(addr), "f"(a), "f"(b) : "memory");
+}
+__device__ __forceinline__ void sts32(uint32_t addr, float a) {
+    asm volatile("st.shared.f32 [%0], %1;" ::"r"(addr), "f"(a) : "memory");
+}
+__device__ __forceinline__ float lds32(uint32_t addr) {
+    float v;
+    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr) : "memory");
+    return v;
+}
+__device__ __forceinline__ uint32_t ldsu32(uint32_t addr) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
+    return v;
+}
+
+template <int N>
+struct StagedCfg {
+    static constexpr int kSS = 5;                                  // staging slices in flight
+    static constexpr int kOS = 3;                                  // operand stages
+    static constexpr int kPbytes = kBKs * kBM * 4;                 // 16 KB
+    static constexpr int kObytes = kBKs * N * 4;                   // 2 / 4 KB
+    static constexpr int kMbytes = kBKs * (kBM / 32) * 4;          // 512 B of mask words
+    static constexpr int kSlice = kPbytes + kObytes + kMbytes;
+    static constexpr int kAbytes = kBM * kBKs * 4;                 // 16 KB
+    static constexpr int kBbytes = N * kBKs * 4;
+    static constexpr int kOpStage = 2 * kAbytes + 2 * kBbytes;
+    static constexpr size_t kSmem = 1024 + (size_t)kOS * kOpStage + (size_t)kSS * kSlice;
+    static_assert(kSmem <= 227 * 1024, "smem");
+};
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y,
+                                            uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::
+            "r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(bar))
+        : "memory");
+}
+
+template <int N>
+__global__ void __launch_bounds__(kSP + 64, 1) dv_recompute_gemm_staged_kernel(
+    const __grid_constant__ CUtensorMap tm_p, const __grid_constant__ CUtensorMap tm_m,
+    const __grid_constant__ CUtensorMap tm_o, double scale, float* __restrict__ dV, int s_q,
+    int s_k) {
+    using Cfg = StagedCfg<N>;
+    constexpr int kSets = 512 / (2 * N) >= 4 ? 4 : 512 / (2 * N);
+    constexpr int kTmemCols = kSets * 2 * N;
+    constexpr int kSS = Cfg::kSS, kOS = Cfg::kOS;
+    grid_dep_wait();
+    grid_dep_launch();
+    extern __shared__ __align__(1024) unsigned char gsm[];
+    const uint32_t base = (smem_u32(gsm) + 1023u) & ~1023u;      // shared-space addresses
+    const uint32_t stage_base = base + kOS * Cfg::kOpStage;       // staging ring after the operands
+    unsigned char* stage_ptr = gsm + (stage_base - smem_u32(gsm)); // generic view (bulk copies)
+    __shared__ uint64_t full[kOS], empty[kOS], acc_full, sfull[kSS], sempty[kSS];
+    __shared__ uint32_t tmem_base_sh;
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int jblocks = s_k / kBM;
+    const int64_t head = blockIdx.x / jblocks;
+    const int j0 = (blockIdx.x % jblocks) * kBM;
+    const int nsl = s_q / kBKs;  // slices = operand stages
+    constexpr int kMMAWarp = kSP / 32, kLoadWarp = kSP / 32 + 1;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kOS; ++s) {
+            mbar_init(&full[s], kSP);
+            mbar_init(&empty[s], 1);
+        }
+        for (int s = 0; s < kSS; ++s) {
+            mbar_init(&sfull[s], 1);
+            mbar_init(&sempty[s], kSP);
+        }
+        mbar_init(&acc_full, 1);
+        mbar_fence_init();
+    }
+    if (warp == kMMAWarp) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         smem_u32(&tmem_base_sh)),
+                     "n"(kTmemCols)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = tmem_base_sh;
+
+    if (warp < kMMAWarp) {
+        // ---------------- producers: staging slice -> K-major operands ----
+        // A: thread t owns dV row m = t % 256 and K-rows 8*(t/256)..+7 of the
+        //    slice: D' = keep ? P : 0, split hi/lo TF32.  B: dO column
+        //    bn = t % N, K-rows bk.. (1 or 2 per thread).
+        const int t = threadIdx.x;
+        const int m = t % kBM, kh = t / kBM;
+        constexpr int kOPT = kBKs * N / kSP;  // 1 (N = 32) or 2 (N = 64)
+        static_assert(kOPT == 1 || kOPT == 2, "dO slice split");
+        const int bn = t % N, bk = (t / N) * kOPT;
+        for (int sl = 0; sl < nsl; ++sl) {
+            const int ss = sl % kSS, s = sl % kOS;
+            mbar_wait(&sfull[ss], (uint32_t)((sl / kSS) & 1));
+            const uint32_t sp = stage_base + ss * Cfg::kSlice;
+            float pv[8];
+            uint32_t w[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                pv[k] = lds32(sp + (uint32_t)(((kh * 8 + k) * kBM + m) * 4));
+                w[k] = ldsu32(sp + Cfg::kPbytes + Cfg::kObytes + (uint32_t)(((kh * 8 + k) * (kBM / 32) + (m >> 5)) * 4));
+            }
+            float ov[kOPT];
+#pragma unroll
+            for (int k = 0; k < kOPT; ++k) ov[k] = lds32(sp + Cfg::kPbytes + (uint32_t)(((bk + k) * N + bn) * 4));
+            mbar_arrive(&sempty[ss]);  // this thread is done reading slice ss
+            if (sl >= kOS) mbar_wait(&empty[s], (uint32_t)(((sl / kOS) + 1) & 1));
+            const uint32_t a_hi = base + s * Cfg::kOpStage, a_lo = a_hi + Cfg::kAbytes;
+            const uint32_t b_hi = a_lo + Cfg::kAbytes, b_lo = b_hi + Cfg::kBbytes;
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+                float hi[4], lo[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int k = 4 * q + u;
+                    const float d = ((w[k] >> lane) & 1u) ? pv[k] : 0.0f;
+                    hi[u] = tf32_rna(d);
+                    lo[u] = tf32_rna(d - hi[u]);
+                }
+                const uint32_t off = sw64_k_offset(m, kh * 2 + q);
+                sts128(a_hi + off, hi[0], hi[1], hi[2], hi[3]);
+                sts128(a_lo + off, lo[0], lo[1], lo[2], lo[3]);
+            }
+            {
+                float hi[kOPT], lo[kOPT];
+#pragma unroll
+                for (int u = 0; u < kOPT; ++u) {
+                    hi[u] = tf32_rna(ov[u]);
+                    lo[u] = tf32_rna(ov[u] - hi[u]);
+                }
+                const uint32_t off = sw64_k_offset(bn, bk >> 2) + (uint32_t)((bk & 3) * 4);
+                if (kOPT == 2) {
+                    sts64(b_hi + off, hi[0], hi[kOPT - 1]);
+                    sts64(b_lo + off, lo[0], lo[kOPT - 1]);
+                } else {
+                    sts32(b_hi + off, hi[0]);
+                    sts32(b_lo + off, lo[0]);
+                }
+            }
+            fence_proxy_async_smem();
+            mbar_arrive(&full[s]);
+        }
+        // ---------------- epilogue: dV = (1/(1-p)) * sum of the sets ----------
+        mbar_wait(&acc_full, 0);
+        tc_fence_after();
+        const int quad = warp % 4, mb = (warp / 4) % 2, half = warp / 8;  // warp w, w+8: column halves
+        const int row = j0 + mb * 128 + quad * 32 + lane;
+        float* out = dV + head * (int64_t)s_k * N + (int64_t)row * N;
+        const float sc = (float)scale;
+#pragma unroll
+        for (int c0 = half * (N / 2); c0 < (half + 1) * (N / 2); c0 += 16) {
+            float v[16];
+            const uint32_t ta = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(mb * N + c0);
+            tmem_ld16(ta, v);
+#pragma unroll
+            for (int set = 1; set < kSets; ++set) {
+                float wv[16];
+                tmem_ld16(ta + (uint32_t)(set * 2 * N), wv);
+#pragma unroll
+                for (int i = 0; i < 16; ++i) v[i] += wv[i];
+            }
+#pragma unroll
+            for (int i = 0; i < 16; i += 4)
+                st_stream(reinterpret_cast<float4*>(out + c0 + i),
+                          make_float4(v[i] * sc, v[i + 1] * sc, v[i + 2] * sc, v[i + 3] * sc));
+        }
+    } else if (warp == kMMAWarp && lane == 0) {
+        // ---------------- MMA issuer ----------------
+        constexpr uint32_t idesc = idesc_tf32_k(128, N);
+        for (int sl = 0; sl < nsl; ++sl) {
+            const int s = sl % kOS;
+            mbar_wait(&full[s], (uint32_t)((sl / kOS) & 1));
+            tc_fence_after();
+            const uint32_t a_hi = base + s * Cfg::kOpStage, a_lo = a_hi + Cfg::kAbytes;
+            const uint32_t b_hi = a_lo + Cfg::kAbytes, b_lo = b_hi + Cfg::kBbytes;
+#pragma unroll
+            for (int kk = 0; kk < kBKs / 8; ++kk) {  // K = 8 per MMA: +32 bytes along 64-byte rows
+                const uint64_t bh = umma_desc_sw64(b_hi + kk * 32, 512);
+                const uint64_t bl = umma_desc_sw64(b_lo + kk * 32, 512);
+                const int gk = sl * (kBKs / 8) + kk;  // global K-step
+                const int set = gk % kSets;
+#pragma unroll
+                for (int mb = 0; mb < 2; ++mb) {
+                    const uint32_t ao = mb * 128 * 64 + kk * 32;  // 128 rows x 64 B per M-block
+                    const uint64_t ah = umma_desc_sw64(a_hi + ao, 512);
+                    const uint64_t al = umma_desc_sw64(a_lo + ao, 512);
+                    const uint32_t acc = tmem + (uint32_t)(set * 2 * N + mb * N);
+                    mma_tf32(acc, al, bh, idesc, gk >= kSets);
+                    mma_tf32(acc, ah, bl, idesc, 1);
+                    mma_tf32(acc, ah, bh, idesc, 1);
+                }
+            }
+            mma_commit(&empty[s]);
+        }
+        mma_commit(&acc_full);
+    } else if (warp == kLoadWarp && lane == 0) {
+        // ---------------- loader: three 2D TMA loads per slice ---------------
+        // (P rows [16 x 256], their mask words [16 x 8], dO rows [16 x N]);
+        // 33 one-dimensional bulk copies per slice were the limiter
+        const int y0 = (int)(head * s_q);
+        for (int sl = 0; sl < nsl; ++sl) {
+            const int ss = sl % kSS;
+            if (sl >= kSS) mbar_wait(&sempty[ss], (uint32_t)(((sl / kSS) + 1) & 1));
+            unsigned char* sp = stage_ptr + ss * Cfg::kSlice;
+            mbar_expect_tx(&sfull[ss], Cfg::kSlice);
+            const int y = y0 + sl * kBKs;
+            tma_load_2d(sp, &tm_p, j0, y, &sfull[ss]);
+            tma_load_2d(sp + Cfg::kPbytes + Cfg::kObytes, &tm_m, j0 / 32, y, &sfull[ss]);
+            tma_load_2d(sp + Cfg::kPbytes, &tm_o, 0, y, &sfull[ss]);
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (warp == kMMAWarp) {
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                     "n"(kTmemCols)
+                     : "memory");
+    }
+}
+
 template <int N>
 size_t dv_smem() {
     return 1024 + (size_t)kStagesG * (2 * kBM * kBK * 4 + 2 * N * kBK * 4);
@@ -320,6 +590,51 @@ cudaError_t launch_dv(const float* P, const uint32_t* mask, double scale, const 
     return cudaGetLastError();
 }
 
+PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+                cudaSuccess && q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    });
+    return fn;
+}
+
+// 2D row-major tensor [rows][cols] of 4-byte elements, box [box_rows][box_cols]
+bool make_tmap_2d(CUtensorMap* map, CUtensorMapDataType dt, const void* ptr, uint64_t rows,
+                  uint64_t cols, uint32_t box_rows, uint32_t box_cols) {
+    auto enc = tmap_encoder();
+    if (!enc) return false;
+    const cuuint64_t dims[2] = {cols, rows};
+    const cuuint64_t strides[1] = {cols * 4};
+    const cuuint32_t box[2] = {box_cols, box_rows};
+    const cuuint32_t estr[2] = {1, 1};
+    return enc(map, dt, 2, const_cast<void*>(ptr), dims, strides, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int N>
+cudaError_t launch_dv_staged(const float* P, const uint32_t* mask, double scale, const float* dO,
+                             float* dV, int64_t heads, int64_t s_q, int64_t s_k, cudaStream_t st) {
+    CUtensorMap tp, tmk, to;
+    const uint64_t rows = (uint64_t)(heads * s_q);
+    if (!make_tmap_2d(&tp, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, P, rows, (uint64_t)s_k, kBKs, kBM) ||
+        !make_tmap_2d(&tmk, CU_TENSOR_MAP_DATA_TYPE_UINT32, mask, rows, (uint64_t)(s_k / 32), kBKs,
+                      kBM / 32) ||
+        !make_tmap_2d(&to, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, dO, rows, (uint64_t)N, kBKs, N))
+        return launch_dv<N>(P, mask, scale, dO, dV, heads, s_q, s_k, st);  // no tensor maps
+    auto k = dv_recompute_gemm_staged_kernel<N>;
+    const size_t smem = StagedCfg<N>::kSmem;
+    (void)grid_for((const void*)k, kSP + 64, smem, 1);
+    const int64_t grid = heads * (s_k / kBM);
+    launch(k, (int)grid, kSP + 64, smem, st)(tp, tmk, to, scale, dV, (int)s_q, (int)s_k);
+    return cudaGetLastError();
+}
+
 }  // namespace
 
 bool dv_gemm_supported(int64_t s_q, int64_t s_k, int64_t d) {
@@ -332,8 +647,13 @@ cudaError_t launch_dv_recompute_gemm(const float* P, const uint32_t* mask, doubl
                                      int64_t s_k, int64_t d, cudaStream_t st) {
     if (heads == 0) return cudaSuccess;
     switch (d) {
-        case 32: return launch_dv<32>(P, mask, scale, dO, dV, heads, s_q, s_k, st);
-        case 64: return launch_dv<64>(P, mask, scale, dO, dV, heads, s_q, s_k, st);
+#ifndef TM_DV_STAGED
+#define TM_DV_STAGED 1
+#endif
+        case 32: return TM_DV_STAGED ? launch_dv_staged<32>(P, mask, scale, dO, dV, heads, s_q, s_k, st)
+                                     : launch_dv<32>(P, mask, scale, dO, dV, heads, s_q, s_k, st);
+        case 64: return TM_DV_STAGED ? launch_dv_staged<64>(P, mask, scale, dO, dV, heads, s_q, s_k, st)
+                                     : launch_dv<64>(P, mask, scale, dO, dV, heads, s_q, s_k, st);
         case 128: return launch_dv<128>(P, mask, scale, dO, dV, heads, s_q, s_k, st);
         default: return cudaErrorInvalidValue;
     }
