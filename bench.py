@@ -544,6 +544,71 @@ def per_config_timings(dev, peak, reps=40):
     return out
 
 
+# ------------------------------------- the recompute fused into its consumer
+def dv_consumer_timings(chain, peak, reps=11, flush=None):
+    """the attention-probability backward plus the
+    consumer of the dropped-out map D, the dV GEMM (dV = D^T dO per head,
+    d = 64), two ways at the configs[3] shape:
+      unfused: attn_probs_bwd writes the recomputed D (16.125 B/elem), then
+               an fp32 cuBLAS GEMM reads it back (TF32 off);
+      fused:   attn_probs_bwd without D (12.125 B/elem), then
+               tempo_attn_dropout_dv rebuilds D from P + mask inside its
+               tcgen05 3xTF32 GEMM (4.125 B/elem + dO + dV).
+    Device time per pair (CUDA events, L2 read-flushed before each rep)."""
+    torch, o = chain.torch, chain.ops
+    heads, dev = chain.batch * A, chain.dev
+    g = torch.Generator(device=dev)
+    g.manual_seed(99)
+    dO = torch.randn(heads, S, 64, device=dev, generator=g)
+    dV = torch.empty(heads, S, 64, device=dev)
+    P3 = chain.P.view(heads, S, S)
+    prev = torch.backends.cuda.matmul.allow_tf32
+    torch.backends.cuda.matmul.allow_tf32 = False
+
+    def unfused():
+        o.attn_probs_bwd(chain.dD, chain.P, chain.m_att, P_DROP, write_d=True, dZ=chain.dZ,
+                         D=chain.Drec)
+        torch.matmul(chain.Drec.view(heads, S, S).transpose(1, 2), dO, out=dV)
+
+    def fused():
+        o.attn_probs_bwd(chain.dD, chain.P, chain.m_att, P_DROP, write_d=False, dZ=chain.dZ)
+        o.attn_dropout_dv(P3, chain.m_att, P_DROP, dO, dV=dV)
+
+    def gemm_only():
+        o.attn_dropout_dv(P3, chain.m_att, P_DROP, dO, dV=dV)
+
+    n_a = chain.P.numel()
+    nb_o = dO.numel() * 4
+    cases = {"unfused": (unfused, n_a * (16 + 1 / 8) + n_a * 4 + 2 * nb_o),
+             "fused": (fused, n_a * (12 + 1 / 8) + n_a * (4 + 1 / 8) + 2 * nb_o),
+             "dv_gemm_only": (gemm_only, n_a * (4 + 1 / 8) + 2 * nb_o)}
+    st = torch.cuda.current_stream()
+    out = {}
+    try:
+        for name, (fn, nbytes) in cases.items():
+            fn()
+            ts = []
+            for _ in range(reps):
+                if flush is not None:
+                    flush()
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(st)
+                fn()
+                b.record(st)
+                b.synchronize()
+                ts.append(a.elapsed_time(b))
+            t_ms = trimmed_mean(ts)
+            gbs = nbytes / (t_ms * 1e-3) / 1e9
+            out[name] = {"ms": round(t_ms, 4), "bytes": int(nbytes), "gbs": round(gbs, 1),
+                         "frac": round(gbs / peak, 4)}
+    finally:
+        torch.backends.cuda.matmul.allow_tf32 = prev
+    out["speedup_fused_vs_unfused"] = round(out["unfused"]["ms"] / out["fused"]["ms"], 3)
+    out["what"] = ("attn_probs_bwd + dV = D^T dO (d=64): D written + fp32 cuBLAS GEMM vs "
+                   "D rebuilt inside the tcgen05 3xTF32 GEMM (tempo_attn_dropout_dv)")
+    return out
+
+
 # ------------------------------------------------------------ clocks
 class ClockSampler:
     def __init__(self, index=0):
@@ -822,6 +887,13 @@ def main():
 
     # ---- configs[0..2] at their own shapes (outside the timed region) -------
     per_config = per_config_timings(dev, peak) if rank == 0 else None
+    # ---- the dropout recompute fused into the dV GEMM ----
+    dv_consumer = None
+    if rank == 0:
+        try:
+            dv_consumer = dv_consumer_timings(chain, peak, flush=flush)
+        except Exception as ex:  # noqa: BLE001  (report, do not fail the bench)
+            dv_consumer = {"unavailable": str(ex)[:200]}
 
     # ---- the reference mask stream on the device (outside the timed region) --
     ref_mask = None
@@ -914,6 +986,7 @@ def main():
             "clocks": clk,
             "per_op": per_op_rows,
             "per_config": per_config,
+            "dv_consumer": dv_consumer,
             "frac_of_peak": round(value / world / peak, 4),
             "unfused_equivalent": ({
                 "what": "the same step's work as separate ops incl. the residual adds "

@@ -268,6 +268,10 @@ class BackwardCtx {
 public:
     const Tensor& grad_out() const { return grad_out_; }
     const Tensor& stash(std::size_t i);  // runs a recompute recipe on first use
+    // The stash itself, unmaterialised: a consumer that can fuse the
+    // recompute into its own kernel (Graph::matmul's dV with a dropout-rescale
+    // recipe) reads the recipe instead of calling stash(i).
+    const LazyStash& lazy_stash(std::size_t i) const;
     const Tensor& input_value(std::size_t i) const;
 
 private:

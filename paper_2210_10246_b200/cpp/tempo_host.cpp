@@ -559,6 +559,14 @@ const Tensor& BackwardCtx::stash(std::size_t i) {  // tape.cpp:244-264
     return cache_[i];
 }
 
+const LazyStash& BackwardCtx::lazy_stash(std::size_t i) const {
+    const TapeNode& nd = tape_->nodes_[id_];
+    if (i >= nd.stashes.size())
+        throw ParamError("stash index " + std::to_string(i) + " out of range for op '" + nd.op +
+                         "'");
+    return nd.stashes[i];
+}
+
 const Tensor& BackwardCtx::input_value(std::size_t i) const {
     const TapeNode& nd = tape_->nodes_[id_];
     if (i >= nd.inputs.size())
@@ -666,6 +674,29 @@ Tensor mm(tempo_stream_t st, const Tensor& a, const Tensor& b, bool ta, bool tb)
 }
 }  // namespace
 
+// dV = D^T g for D = the output of dropout_recompute, without D: the
+// consumer-side recompute fused into the tcgen05 GEMM (tempo_attn_dropout_dv,
+// SURVEY 8f rank 2).  Returns an undefined Tensor when the shapes are outside
+// the kernel's envelope; the caller then materialises D through the recipe.
+Tensor fused_dropout_dv(tempo_stream_t st, const RecomputeRecipe& recipe, const Tensor& g) {
+    if (recipe.rule != "dropout-rescale" || recipe.masks.size() != 1) return Tensor();
+    std::vector<Tensor> src = recipe.lock_sources();
+    if (src.size() != 1) return Tensor();
+    const Tensor& P = src[0];
+    const Shape& ps = P.shape();
+    const Shape& gs = g.shape();
+    if (ps.size() < 2 || gs.size() != ps.size() ||
+        !std::equal(ps.begin(), ps.end() - 1, gs.begin()))
+        return Tensor();
+    const MatDims dp = mat_dims(ps, "matmul"), dg = mat_dims(gs, "matmul");
+    Tensor dv = Tensor::empty(with_last2(gs, dp.c, dg.c));
+    const int rc = tempo_attn_dropout_dv(P.data(), recipe.masks[0].words(), recipe.scalars.at("p"),
+                                         g.data(), dv.data(), dp.batch, dp.r, dp.c, dg.c, st);
+    if (rc == TEMPO_ERR_UNSUPPORTED || rc == TEMPO_ERR_ALIGNMENT) return Tensor();
+    check(rc);
+    return dv;
+}
+
 NodeId Graph::matmul(NodeId a, NodeId b, std::string tag) {  // graph.cpp:32-51
     StreamScope scope_(stream);
     const Tensor& va = tape.value(a);
@@ -682,7 +713,12 @@ NodeId Graph::matmul(NodeId a, NodeId b, std::string tag) {  // graph.cpp:32-51
                        [st](BackwardCtx& ctx) -> std::vector<Tensor> {
                            const Tensor& g = ctx.grad_out();
                            Tensor da = mm(st, g, ctx.stash(1), false, true);
-                           Tensor db = mm(st, ctx.stash(0), g, true, false);
+                           // a dropout_recompute left operand: its consumer
+                           // rebuilds D inside the dV GEMM (no #recomputed D)
+                           const LazyStash& s0 = ctx.lazy_stash(0);
+                           Tensor db;
+                           if (!s0.is_materialized()) db = fused_dropout_dv(st, s0.recipe(), g);
+                           if (!db.defined()) db = mm(st, ctx.stash(0), g, true, false);
                            return {da, db};
                        });
 }

@@ -316,8 +316,8 @@ static void test_hidden_dropout() {
 // tempo_ops::sdpa (ops_tempo.cpp:196-210): cuBLAS GEMMs around the Tempo
 // softmax + dropout_recompute, forward and all three input gradients against
 // a host fp64 restatement; the dropped-out map is recomputed, not stashed.
-static void test_sdpa() {
-    const std::int64_t B = 2, A = 2, S = 128, d = 32;
+static void sdpa_case(std::int64_t B, std::int64_t A, std::int64_t S, std::int64_t d,
+                      bool fused_dv) {
     const double p = 0.25, sc = 1.0 / std::sqrt((double)d), keep_s = 1.0 / (1.0 - p);
     const std::int64_t nq = B * A * S * d, ns = B * A * S * S;
     std::vector<float> qh = randn(nq, 21), kh = randn(nq, 22), vh = randn(nq, 23), gh = randn(nq, 24);
@@ -383,8 +383,23 @@ static void test_sdpa() {
                 worst = std::max({worst, rel_err(dq[e], aq), rel_err(dk[e], ak), rel_err(dv[e], av)});
             }
     }
-    std::printf("  sdpa max rel_err %.3g\n", worst);
+    std::printf("  sdpa B=%lld A=%lld S=%lld d=%lld max rel_err %.3g\n", (long long)B, (long long)A,
+                (long long)S, (long long)d, worst);
     CHECK(worst <= 1e-5);
+    // dV: the recipe's D materialised for a cuBLAS GEMM (a "#recomputed"
+    // ledger charge, tape.cpp:255-260) or rebuilt inside the fused tcgen05
+    // dV GEMM (never materialised: no charge)
+    bool recomputed = false;
+    for (const auto& e : g.ledger.entries())
+        if (e.tag == "attn_drop_out#recomputed") recomputed = true;
+    CHECK(recomputed == !fused_dv);
+}
+
+static void test_sdpa() {
+    sdpa_case(2, 2, 128, 32, false);  // outside the fused dV kernel's envelope: recompute + GEMM
+    sdpa_case(1, 2, 512, 64, true);   // BERT-large head shape: D rebuilt inside the dV GEMM
+    const double p = 0.25;
+    BoolMask mask = BoolMask::bernoulli_keep({2, 2, 128, 128}, p, 25);
     Graph g2;  // ops_tempo.cpp:198-202: rank-4 inputs only
     NodeId bad = g2.leaf(Tensor::from_host({4, 4}, randn(16, 1)), "x");
     CHECK(throws<DimensionError>([&] { tempo_ops::sdpa(g2, bad, bad, bad, p, mask); }));
