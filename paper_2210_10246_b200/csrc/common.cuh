@@ -181,6 +181,12 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
         : "memory");
 }
 
+// Named barrier over `nthreads` threads (a multiple of 32) of the CTA: the
+// warps of one row group synchronise without stalling the CTA's other groups.
+__device__ __forceinline__ void group_bar(int id, int nthreads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
 // ---- programmatic dependent launch (PDL) --------------------------------
 // A kernel launched with the programmatic-stream-serialization attribute may
 // start while its predecessor drains; it must call grid_dep_wait() before

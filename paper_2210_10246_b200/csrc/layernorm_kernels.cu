@@ -23,8 +23,10 @@
 // walks row tiles with a grid stride; the tiles arrive through a TMA
 // (cp.async.bulk) ring in shared memory, kStages deep.  Row reductions are
 // warp shuffles plus one smem exchange (fixed order, identical in every
-// thread).  cols % 4 != 0, cols > 2048 or unaligned pointers use the
-// generic kernels (one element per thread per pass).
+// thread).  Rows longer than 2048 (cols % 128 == 0) are held in the
+// registers of a group of warps (ln_fwd_long_kernel / ln_bwd_long_kernel);
+// cols % 4 != 0, other long rows or unaligned pointers use the generic
+// kernels (one element per thread per pass).
 #include "common.cuh"
 #include "tempo_internal.h"
 
@@ -459,10 +461,10 @@ __global__ void __launch_bounds__(256) dal_fwd_generic_kernel(
     int mode, double scale, uint64_t thresh, uint64_t seed, uint64_t offset,
     const float* __restrict__ gamma, const float* __restrict__ beta, double eps,
     float* __restrict__ y, float* __restrict__ rstd, int64_t rows, int cols,
-    int32_t* __restrict__ status) {
+    int32_t* __restrict__ status, int r_in_y) {
     grid_dep_wait();
     grid_dep_launch();
-    extern __shared__ float xr[];  // [cols]
+    extern __shared__ float xr_sm[];  // [cols]; 0 bytes: r staged in the output row itself
     __shared__ double red[2 * 32];
     int phase = 0;
     const int lane = threadIdx.x & 31;
@@ -471,6 +473,9 @@ __global__ void __launch_bounds__(256) dal_fwd_generic_kernel(
             if (fabs((double)gamma[j]) < kGammaMin) *status = TEMPO_ERR_PARAM;
     }
     for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
+        // every element is written and read back by the same thread (same j
+        // loop), so the global staging needs no barrier
+        float* xr = r_in_y ? y + r * cols : xr_sm;
         double s[1] = {0.0};
         for (int j = threadIdx.x; j < cols; j += blockDim.x) {  // cols % 32 == 0: full warps
             const int64_t i = r * cols + j;
@@ -502,6 +507,176 @@ __global__ void __launch_bounds__(256) dal_fwd_generic_kernel(
         if (threadIdx.x == 0) rstd[r] = (float)rs;
         __syncthreads();  // xr is rewritten by the next row
     }
+}
+
+// ---- long rows (cols % 128 == 0, 1024 < cols <= 16384), forward ---------
+// One CTA = one row group of W warps, persistent over rows r = blockIdx.x +
+// i*gridDim.x; the rows (x, or proj and residual for the fused dropout -> add
+// -> LayerNorm: MODE 1 supplied mask, MODE 2 Philox, the same bits as
+// dal_fwd_warp_kernel's) stream into a shallow TMA ring in shared memory (one
+// mbarrier per stage, thread 0 issues), so the bytes in flight per SM are
+// bounded by smem, not by the registers holding a row.  The row's 128-column
+// chunks are dealt round-robin to the warps (warp w: chunks w, w+W, ..., at
+// most VPL) and read from the stage into registers; the row sums are warp
+// shuffles plus an exchange of the W warp partials through shared memory
+// (__syncthreads; combined in warp order in every thread, slots alternating by
+// row parity).  The first exchange proves every warp has read the stage, so
+// thread 0 refills it there.  One HBM read and one write per element;
+// statistics as ln_fwd_warp_kernel (fp32 sums refined once, rstd in fp64);
+// gamma/beta are L1-resident __ldg float4s.
+constexpr int kLongVPL = 8;
+#ifndef TM_LNL_STAGES
+#define TM_LNL_STAGES 1  // A/B at 2^25 elements: 1 stage 0.82/0.81/0.80 of the copy peak at H = 2048/4096/8192 vs 0.76/0.73/0.71 (2), 0.69/0.65/0.65 (3)
+#endif
+constexpr size_t kLnlRingBytes = 160 * 1024;
+
+template <int W, int MODE>
+__global__ void __launch_bounds__(W * 32) ln_fwd_long_kernel(
+    const float* __restrict__ x, const float* __restrict__ res, uint32_t* __restrict__ mask,
+    double scale, uint64_t thresh, uint64_t seed, uint64_t offset,
+    const float* __restrict__ gamma, const float* __restrict__ beta, double eps,
+    float* __restrict__ y, float* __restrict__ rstd, int64_t rows, int nch, int ns,
+    int32_t* __restrict__ status) {
+    grid_dep_wait();  // PDL: predecessor complete and visible
+    grid_dep_launch();
+    constexpr int T = MODE == 0 ? 1 : 2;  // tensors per stage: x | proj, residual
+    extern __shared__ __align__(128) unsigned char dsm[];
+    uint64_t* full = reinterpret_cast<uint64_t*>(dsm);
+    const float4* ring = reinterpret_cast<const float4*>(dsm + 128);
+    __shared__ float red[2][3][W];  // [row parity][s, t, q][warp]
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int64_t C = (int64_t)nch * 128;
+    const uint32_t row_bytes = (uint32_t)C * 4u;
+    auto issue = [&](int64_t r, int st) {
+        mbar_expect_tx(&full[st], T * row_bytes);
+        bulk_g2s((void*)(ring + (size_t)(T * st) * (C / 4)), x + r * C, row_bytes, &full[st]);
+        if (T == 2)
+            bulk_g2s((void*)(ring + (size_t)(T * st + 1) * (C / 4)), res + r * C, row_bytes, &full[st]);
+    };
+    if (threadIdx.x == 0) {
+        for (int st = 0; st < ns; ++st) mbar_init(&full[st], 1);
+        mbar_fence_init();
+    }
+    if (status && blockIdx.x == 0) {
+        for (int64_t i = threadIdx.x; i < C; i += W * 32)
+            if (fabs((double)gamma[i]) < kGammaMin) *status = TEMPO_ERR_PARAM;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int st = 0; st < ns; ++st) {
+            const int64_t r = blockIdx.x + (int64_t)st * gridDim.x;
+            if (r < rows) issue(r, st);
+        }
+    }
+    const float inv_m = 1.0f / (float)C;
+    int it = 0;
+    for (int64_t r = blockIdx.x; r < rows; r += gridDim.x, ++it) {
+        const int st = it % ns, par = it & 1;
+        uint32_t nb[kLongVPL];
+        uint32_t* mrow = mask + ((r * C) >> 5);
+        if (MODE != 0) {
+#pragma unroll
+            for (int k = 0; k < kLongVPL; ++k) {
+                const int c = w + k * W;
+                if (c >= nch) continue;
+                if (MODE == 1) {
+                    nb[k] = chunk_nibble(mrow + c * 4, lane);
+                } else {
+                    const U4 q = philox_quad(seed, (offset + (uint64_t)(r * C + c * 128 + lane * 4)) >> 2);
+                    nb[k] = nibble4((uint64_t)q.x >= thresh, (uint64_t)q.y >= thresh,
+                                    (uint64_t)q.z >= thresh, (uint64_t)q.w >= thresh);
+                    store_chunk_mask(mrow + c * 4, nb[k], lane);
+                }
+            }
+        }
+        mbar_wait(&full[st], (uint32_t)((it / ns) & 1));
+        const float4* sx = ring + (size_t)(T * st) * (C / 4);
+        float4 v[kLongVPL];
+        float s = 0.0f;
+#pragma unroll
+        for (int k = 0; k < kLongVPL; ++k) {
+            const int c = w + k * W;
+            if (c >= nch) continue;
+            v[k] = sx[c * 32 + lane];
+            if (MODE != 0) {  // v = residual + dropout(proj)
+                const float4 rv = sx[C / 4 + c * 32 + lane];
+                v[k].x = rv.x + ((nb[k] & 1u) ? (float)((double)v[k].x * scale) : 0.0f);
+                v[k].y = rv.y + ((nb[k] & 2u) ? (float)((double)v[k].y * scale) : 0.0f);
+                v[k].z = rv.z + ((nb[k] & 4u) ? (float)((double)v[k].z * scale) : 0.0f);
+                v[k].w = rv.w + ((nb[k] & 8u) ? (float)((double)v[k].w * scale) : 0.0f);
+            }
+            s += (v[k].x + v[k].y) + (v[k].z + v[k].w);
+        }
+        s = warp_sumf(s);
+        if (lane == 0) red[par][0][w] = s;
+        __syncthreads();  // every warp has read stage st: refill it
+        if (threadIdx.x == 0) {
+            const int64_t rn = r + (int64_t)ns * gridDim.x;
+            if (rn < rows) {
+                fence_proxy_async_smem();
+                issue(rn, st);
+            }
+        }
+        s = red[par][0][0];
+#pragma unroll
+        for (int i = 1; i < W; ++i) s += red[par][0][i];
+        const float m0 = s * inv_m;  // first estimate of the mean
+        float q = 0.0f, t = 0.0f;
+#pragma unroll
+        for (int k = 0; k < kLongVPL; ++k) {
+            if (w + k * W >= nch) continue;
+            const float d0 = v[k].x - m0, d1 = v[k].y - m0;
+            const float d2 = v[k].z - m0, d3 = v[k].w - m0;
+            q += fmaf(d0, d0, d1 * d1) + fmaf(d2, d2, d3 * d3);
+            t += (d0 + d1) + (d2 + d3);
+        }
+        t = warp_sumf(t);
+        q = warp_sumf(q);
+        if (lane == 0) {
+            red[par][1][w] = t;
+            red[par][2][w] = q;
+        }
+        __syncthreads();
+        t = red[par][1][0];
+        q = red[par][2][0];
+#pragma unroll
+        for (int i = 1; i < W; ++i) {
+            t += red[par][1][i];
+            q += red[par][2][i];
+        }
+        float mean, var_f;
+        refine_moments(m0, t, q, inv_m, mean, var_f);
+        const float rs = (float)(1.0 / sqrt((double)var_f + eps));  // ops_tempo.cpp:111-112
+        float4* yr = reinterpret_cast<float4*>(y + r * C);
+#pragma unroll
+        for (int k = 0; k < kLongVPL; ++k) {
+            const int c = w + k * W;
+            if (c >= nch) continue;
+            const float4 gm = __ldg(reinterpret_cast<const float4*>(gamma) + c * 32 + lane);
+            const float4 b = __ldg(reinterpret_cast<const float4*>(beta) + c * 32 + lane);
+            float4 o;
+            o.x = fmaf(gm.x * rs, v[k].x - mean, b.x);
+            o.y = fmaf(gm.y * rs, v[k].y - mean, b.y);
+            o.z = fmaf(gm.z * rs, v[k].z - mean, b.z);
+            o.w = fmaf(gm.w * rs, v[k].w - mean, b.w);
+            st_stream(yr + c * 32 + lane, o);
+        }
+        if (threadIdx.x == 0) rstd[r] = rs;
+    }
+}
+
+inline int lnl_stages(int64_t cols, int tensors) {
+    const int ns = (int)(kLnlRingBytes / ((size_t)tensors * cols * 4));
+    return ns < 1 ? 1 : ns > TM_LNL_STAGES ? TM_LNL_STAGES : ns;
+}
+inline size_t lnl_smem(int64_t cols, int tensors) {
+    return 128 + (size_t)lnl_stages(cols, tensors) * tensors * cols * 4;
+}
+// forward: W * 8 chunks cover the row
+inline int lnl_fwd_warps(int64_t nch) { return nch <= 16 ? 2 : nch <= 32 ? 4 : nch <= 64 ? 8 : 16; }
+
+inline int long_warps(int64_t nch) {
+    return nch <= 4 * kLongVPL ? 4 : nch <= 8 * kLongVPL ? 8 : 16;
 }
 
 size_t warp_fwd_smem(int vpl) {
@@ -751,12 +926,13 @@ __global__ void __launch_bounds__(256) ln_bwd_generic_kernel(
     const float* __restrict__ dy, const float* __restrict__ y, const float* __restrict__ rstd,
     const float* __restrict__ gamma, const float* __restrict__ beta, float* __restrict__ dx,
     double* __restrict__ ws, int64_t rows, int cols, const uint32_t* __restrict__ mask,
-    double scale, float* __restrict__ dproj) {
+    double scale, float* __restrict__ dproj, int part_in_ws) {
     grid_dep_wait();  // PDL: predecessor complete and visible
     grid_dep_launch();
-    extern __shared__ double part[];  // [2][cols]
+    extern __shared__ double part_sm[];  // [2][cols], or the CTA's own ws row for very long rows
     __shared__ double red[2 * 2 * 32];
     int phase = 0;
+    double* part = part_in_ws ? ws + (size_t)blockIdx.x * 2 * cols : part_sm;
     for (int j = threadIdx.x; j < 2 * cols; j += blockDim.x) part[j] = 0.0;
     const double inv_m = 1.0 / (double)cols;
     for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
@@ -784,10 +960,150 @@ __global__ void __launch_bounds__(256) ln_bwd_generic_kernel(
             part[cols + j] += g;
         }
     }
+    if (part_in_ws) return;  // each column's partial is one thread's: already in place
     __syncthreads();
     double* wg = ws + (size_t)blockIdx.x * 2 * cols;
     for (int j = threadIdx.x; j < 2 * cols; j += blockDim.x) wg[j] = part[j];
 }
+
+// Stage 1, long rows (cols % 128 == 0, 2048 < cols <= 8192): one CTA = one
+// row group of W warps (W = 4 or 8), the row's 128-column chunks dealt
+// round-robin to its warps and held in registers (dy and y read once from
+// HBM); the two row sums are exchanged through shared memory.  The per-CTA
+// fp64 dgamma/dbeta column partials (too many columns for registers) live in
+// shared memory, lane-transposed ([chunk][k][lane]: conflict-free 64-bit
+// accesses); each column belongs to one thread, so they are updated without
+// synchronisation.  gamma, beta and 1/gamma are staged in shared memory
+// (float4 per lane, conflict-free).  28 B of smem per column.  DROP as in
+// ln_bwd_vec_kernel.
+template <int W, bool DROP>
+__global__ void __launch_bounds__(W * 32) ln_bwd_long_kernel(
+    const float* __restrict__ dy, const float* __restrict__ y, const float* __restrict__ rstd,
+    const float* __restrict__ gamma, const float* __restrict__ beta, float* __restrict__ dx,
+    double* __restrict__ ws, int64_t rows, int nch, const uint32_t* __restrict__ mask,
+    double scale, float* __restrict__ dproj) {
+    grid_dep_wait();  // PDL: predecessor complete and visible
+    grid_dep_launch_persistent();
+    constexpr int NT = W * 32;
+    const int cols = nch * 128;
+    extern __shared__ __align__(128) unsigned char dsm[];
+    double* pg = reinterpret_cast<double*>(dsm);  // [cols], lane-transposed
+    double* pb = pg + cols;
+    float4* sg = reinterpret_cast<float4*>(pb + cols);  // [cols/4] gamma
+    float4* sb = sg + cols / 4;                         // beta
+    float4* si = sb + cols / 4;                         // float(1/gamma)
+    __shared__ float red[2][2][W];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (int i = threadIdx.x; i < cols / 4; i += NT) {
+        const float4 g4 = reinterpret_cast<const float4*>(gamma)[i];
+        sg[i] = g4;
+        sb[i] = reinterpret_cast<const float4*>(beta)[i];
+        si[i] = make_float4((float)(1.0 / (double)g4.x), (float)(1.0 / (double)g4.y),
+                            (float)(1.0 / (double)g4.z), (float)(1.0 / (double)g4.w));
+    }
+    for (int i = threadIdx.x; i < 2 * cols; i += NT) pg[i] = 0.0;
+    __syncthreads();
+    const float inv_m = 1.0f / (float)cols;
+    int par = 0;
+    for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
+        const float4* gr = reinterpret_cast<const float4*>(dy + r * cols);
+        const float4* yr = reinterpret_cast<const float4*>(y + r * cols);
+        float4 gv[kLongVPL], yv[kLongVPL];
+        uint32_t nib[kLongVPL];
+#pragma unroll
+        for (int k = 0; k < kLongVPL; ++k) {
+            const int c = w + k * W;
+            if (c < nch) {
+                gv[k] = ld_stream(gr + c * 32 + lane);
+                yv[k] = ld_stream(yr + c * 32 + lane);
+                if (DROP) nib[k] = chunk_nibble(mask + ((r * cols) >> 5) + c * 4, lane);
+            }
+        }
+        const float rs = __ldg(rstd + r);
+        float s1 = 0.0f, s2 = 0.0f;
+#pragma unroll
+        for (int k = 0; k < kLongVPL; ++k) {
+            const int c = w + k * W;
+            if (c >= nch) continue;
+            const float4 gm = sg[c * 32 + lane], bt = sb[c * 32 + lane], ig = si[c * 32 + lane];
+            const float g0 = gv[k].x * gm.x, g1 = gv[k].y * gm.y, g2 = gv[k].z * gm.z,
+                        g3 = gv[k].w * gm.w;
+            s1 += g0;
+            s2 = fmaf(g0, (yv[k].x - bt.x) * ig.x, s2);
+            s1 += g1;
+            s2 = fmaf(g1, (yv[k].y - bt.y) * ig.y, s2);
+            s1 += g2;
+            s2 = fmaf(g2, (yv[k].z - bt.z) * ig.z, s2);
+            s1 += g3;
+            s2 = fmaf(g3, (yv[k].w - bt.w) * ig.w, s2);
+        }
+        s1 = warp_sumf(s1);
+        s2 = warp_sumf(s2);
+        if (lane == 0) {
+            red[par][0][w] = s1;
+            red[par][1][w] = s2;
+        }
+        __syncthreads();
+        s1 = red[par][0][0];
+        s2 = red[par][1][0];
+#pragma unroll
+        for (int i = 1; i < W; ++i) {
+            s1 += red[par][0][i];
+            s2 += red[par][1][i];
+        }
+        par ^= 1;
+        const float c1 = s1 * inv_m, c2 = s2 * inv_m;
+#pragma unroll
+        for (int k = 0; k < kLongVPL; ++k) {
+            const int c = w + k * W;
+            if (c >= nch) continue;
+            const float4 gm4 = sg[c * 32 + lane], bt4 = sb[c * 32 + lane], ig4 = si[c * 32 + lane];
+            const float ga[4] = {gv[k].x, gv[k].y, gv[k].z, gv[k].w};
+            const float ya[4] = {yv[k].x, yv[k].y, yv[k].z, yv[k].w};
+            const float gm[4] = {gm4.x, gm4.y, gm4.z, gm4.w};
+            const float bt[4] = {bt4.x, bt4.y, bt4.z, bt4.w};
+            const float ig[4] = {ig4.x, ig4.y, ig4.z, ig4.w};
+            float o[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const float xh = (ya[j] - bt[j]) * ig[j];
+                o[j] = (fmaf(ga[j], gm[j], -c1) - xh * c2) * rs;
+                const int pi = (c * 4 + j) * 32 + lane;  // column c*128 + 4*lane + j
+                const double gd = (double)ga[j];
+                pg[pi] = fma(gd, (double)ya[j], pg[pi]);
+                pb[pi] += gd;
+            }
+            st_stream(reinterpret_cast<float4*>(dx + r * cols) + c * 32 + lane,
+                      make_float4(o[0], o[1], o[2], o[3]));
+            if (DROP) {
+                float4 dp;
+                dp.x = (nib[k] & 1u) ? (float)((double)o[0] * scale) : 0.0f;
+                dp.y = (nib[k] & 2u) ? (float)((double)o[1] * scale) : 0.0f;
+                dp.z = (nib[k] & 4u) ? (float)((double)o[2] * scale) : 0.0f;
+                dp.w = (nib[k] & 8u) ? (float)((double)o[3] * scale) : 0.0f;
+                st_stream(reinterpret_cast<float4*>(dproj + r * cols) + c * 32 + lane, dp);
+            }
+        }
+    }
+    // sum g*xhat = (sum g*y - beta * sum g) / gamma per column (as ln_bwd_vec_kernel)
+    double* wg = ws + (size_t)blockIdx.x * 2 * cols;
+    for (int k = 0; k < kLongVPL; ++k) {
+        const int c = w + k * W;
+        if (c >= nch) continue;
+        const float4 gm4 = sg[c * 32 + lane], bt4 = sb[c * 32 + lane];
+        const float gm[4] = {gm4.x, gm4.y, gm4.z, gm4.w};
+        const float bt[4] = {bt4.x, bt4.y, bt4.z, bt4.w};
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int pi = (c * 4 + j) * 32 + lane;
+            const int col = c * 128 + lane * 4 + j;
+            wg[col] = fma(-(double)bt[j], pb[pi], pg[pi]) * (1.0 / (double)gm[j]);
+            wg[cols + col] = pb[pi];
+        }
+    }
+}
+
+size_t bwd_long_smem(int64_t cols) { return (size_t)cols * (2 * sizeof(double) + 3 * sizeof(float)); }
 
 // Stage 2: out[j] = sum over CTAs c (fixed order) of ws[c][j], j < 2*cols.
 // A 32 x 32 block: column lane tx owns output j0 + tx, slice ty sums the
@@ -975,12 +1291,64 @@ const void* bwd_vec_fn(int64_t cols, bool drop = false) {
 size_t fwd_smem(int64_t cols) { return 128 + (size_t)kStages * kRows * cols * sizeof(float); }
 size_t bwd_smem(int64_t cols) { return 128 + (size_t)kStagesB * 2 * kRowsB * cols * sizeof(float); }
 
+// long-row paths (cols % 128 == 0): forward 2048 < cols <= 16384 (the fused
+// dropout -> add -> LayerNorm forward from 1024), backward up to 8192
+bool long_fwd_ok(int64_t cols, int64_t min_cols) {
+    return cols % 128 == 0 && cols > min_cols && cols <= 16 * kLongVPL * 128;
+}
+bool long_bwd_ok(int64_t cols) { return cols % 128 == 0 && cols > 4 * kMaxThreads && cols <= 8 * kLongVPL * 128; }
+const void* bwd_long_fn(int64_t cols, bool drop) {
+    if (long_warps(cols / 128) == 4)
+        return drop ? (const void*)ln_bwd_long_kernel<4, true> : (const void*)ln_bwd_long_kernel<4, false>;
+    return drop ? (const void*)ln_bwd_long_kernel<8, true> : (const void*)ln_bwd_long_kernel<8, false>;
+}
+int bwd_long_grid(int64_t rows, int64_t cols) {
+    return grid_for(bwd_long_fn(cols, false), long_warps(cols / 128) * 32, bwd_long_smem(cols), rows);
+}
+
+// generic backward: partials in smem up to this many bytes, else in the
+// CTA's own workspace row (global, L2-resident)
+constexpr size_t kGenericPartSmem = 160 * 1024;
+size_t generic_bwd_smem(int64_t cols) {
+    const size_t b = (size_t)2 * cols * sizeof(double);
+    return b <= kGenericPartSmem ? b : 0;
+}
+
 int bwd_grid(int64_t rows, int64_t cols, bool vec) {
     int64_t work = vec ? (rows + kRowsB - 1) / kRowsB : rows;
     const void* k = !vec ? (const void*)ln_bwd_generic_kernel : bwd_vec_fn(cols);
     int block = vec ? bwd_threads(cols) : 256;
-    size_t smem = vec ? bwd_smem(cols) : (size_t)2 * cols * sizeof(double);
+    size_t smem = vec ? bwd_smem(cols) : generic_bwd_smem(cols);
     return grid_for(k, block, smem, work);
+}
+
+template <int MODE>
+cudaError_t launch_ln_long_fwd(const float* x, const float* res, uint32_t* mask, double scale,
+                               uint64_t thresh, uint64_t seed, uint64_t offset,
+                               const float* gamma, const float* beta, double eps, float* y,
+                               float* rstd, int64_t rows, int64_t cols, int32_t* dev_status,
+                               cudaStream_t st) {
+    const int nch = (int)(cols / 128);
+    const int T = MODE == 0 ? 1 : 2;
+    const size_t smem = lnl_smem(cols, T);
+    const int ns = lnl_stages(cols, T);
+#define TB_LNL(W)                                                                            \
+    case W: {                                                                                \
+        auto k = ln_fwd_long_kernel<W, MODE>;                                                \
+        int grid = grid_for((const void*)k, W * 32, smem, rows);                             \
+        launch(k, grid, W * 32, smem, st)(x, res, mask, scale, thresh, seed, offset, gamma, beta, \
+                                          eps, y, rstd, rows, nch, ns, dev_status);          \
+        break;                                                                               \
+    }
+    switch (lnl_fwd_warps(nch)) {
+        TB_LNL(2)
+        TB_LNL(4)
+        TB_LNL(8)
+        TB_LNL(16)
+        default: return cudaErrorInvalidValue;
+    }
+#undef TB_LNL
+    return cudaGetLastError();
 }
 
 }  // namespace
@@ -1009,6 +1377,10 @@ cudaError_t launch_ln_fwd(const float* x, const float* gamma, const float* beta,
 #undef TB_LNW
         return cudaGetLastError();
     }
+    if (long_fwd_ok(cols, 1024) && aligned16(x) && aligned16(y) && aligned16(gamma) &&
+        aligned16(beta))
+        return launch_ln_long_fwd<0>(x, nullptr, nullptr, 1.0, 0, 0, 0, gamma, beta, eps, y, rstd,
+                                     rows, cols, dev_status, st);
     if (use_vec(cols, x, y, gamma, beta, x)) {
         int block = vec_threads(cols);
         size_t smem = fwd_smem(cols);
@@ -1050,7 +1422,9 @@ size_t ln_bwd_workspace(int64_t rows, int64_t cols) {
     // the larger of the two grids.
     int gv = (cols % 4 == 0 && cols <= 4 * kMaxThreads) ? bwd_grid(rows, cols, true) : 0;
     int gg = bwd_grid(rows, cols, false);
+    int gl = long_bwd_ok(cols) ? bwd_long_grid(rows, cols) : 0;
     int g = gv > gg ? gv : gg;
+    g = gl > g ? gl : g;
     return (size_t)g * 2 * (size_t)cols * sizeof(double);
 }
 
@@ -1066,12 +1440,24 @@ cudaError_t launch_ln_bwd(const float* dy, const float* y, const float* rstd, co
         return cudaGetLastError();
     }
     const bool drop = dproj != nullptr;
-    const bool vec = use_vec(cols, dy, y, dx, gamma, beta) && (!drop || aligned16(dproj));
+    const bool aligned = aligned16(dy) && aligned16(y) && aligned16(dx) && aligned16(gamma) &&
+                         aligned16(beta) && (!drop || aligned16(dproj));
+    const bool lng = long_bwd_ok(cols) && aligned;
+    const bool vec = !lng && use_vec(cols, dy, y, dx, gamma, beta) && (!drop || aligned16(dproj));
     // the grid (= the workspace's partial rows) is the plain kernel's, also
     // for the fused variant, so one workspace query serves both
-    const int grid = bwd_grid(rows, cols, vec);
+    const int grid = lng ? bwd_long_grid(rows, cols) : bwd_grid(rows, cols, vec);
     double* w = static_cast<double*>(ws);
-    if (vec) {
+    if (lng) {
+        using KFn = void (*)(const float*, const float*, const float*, const float*,
+                             const float*, float*, double*, int64_t, int, const uint32_t*, double,
+                             float*);
+        KFn k = reinterpret_cast<KFn>(const_cast<void*>(bwd_long_fn(cols, drop)));
+        const int nt = long_warps(cols / 128) * 32;
+        if (drop) (void)grid_for((const void*)k, nt, bwd_long_smem(cols), grid);  // smem opt-in
+        launch(k, grid, nt, bwd_long_smem(cols), st)(dy, y, rstd, gamma, beta, dx, w, rows,
+                                                     (int)(cols / 128), mask, scale, dproj);
+    } else if (vec) {
         using KFn = void (*)(const float*, const float*, const float*, const float*,
                              const float*, float*, double*, int64_t, int, const uint32_t*, double,
                              float*);
@@ -1081,9 +1467,10 @@ cudaError_t launch_ln_bwd(const float* dy, const float* y, const float* rstd, co
         launch(k, grid, bwd_threads(cols), bwd_smem(cols), st)(dy, y, rstd, gamma, beta, dx, w, rows,
                                                            (int)cols, mask, scale, dproj);
     } else {
-        size_t smem = (size_t)2 * cols * sizeof(double);
+        const size_t smem = generic_bwd_smem(cols);
         launch(ln_bwd_generic_kernel, grid, 256, smem, st)(dy, y, rstd, gamma, beta, dx, w, rows,
-                                                       (int)cols, mask, scale, dproj);
+                                                       (int)cols, mask, scale, dproj,
+                                                       smem == 0 ? 1 : 0);
     }
     if (peer) return launch_ln_param_reduce_peer(w, grid, cols, *peer, dgamma, dbeta, st);
     const int rgrid = (int)((2 * cols + 31) / 32);
@@ -1124,11 +1511,19 @@ cudaError_t launch_dal_fwd(const float* proj, const float* res, double scale, ui
 #undef TB_DAL
         return cudaGetLastError();
     }
-    const size_t smem = (size_t)cols * sizeof(float);
+    if (long_fwd_ok(cols, 1024) && aligned16(proj) && aligned16(res) && aligned16(y) &&
+        aligned16(gamma) && aligned16(beta) && (offset & 3u) == 0) {
+        return philox ? launch_ln_long_fwd<2>(proj, res, mask, scale, thresh, seed, offset, gamma,
+                                              beta, eps, y, rstd, rows, cols, dev_status, st)
+                      : launch_ln_long_fwd<1>(proj, res, mask, scale, thresh, seed, offset, gamma,
+                                              beta, eps, y, rstd, rows, cols, dev_status, st);
+    }
+    const size_t smem = (size_t)cols * sizeof(float) <= 160 * 1024 ? (size_t)cols * sizeof(float) : 0;
     int grid = grid_for((const void*)dal_fwd_generic_kernel, 256, smem, rows);
     launch(dal_fwd_generic_kernel, grid, 256, smem, st)(proj, res, mask, philox ? 2 : 1, scale,
                                                         thresh, seed, offset, gamma, beta, eps, y,
-                                                        rstd, rows, (int)cols, dev_status);
+                                                        rstd, rows, (int)cols, dev_status,
+                                                        smem == 0 ? 1 : 0);
     return cudaGetLastError();
 }
 

@@ -20,7 +20,9 @@
 //
 // Layout: one warp per row, VPL float4 per lane (cols = 128*VPL <= 1024),
 // the whole row in registers (one HBM read per element, no smem staging
-// needed at S <= 1024).  Other shapes use the generic warp-per-row kernels.
+// needed at S <= 1024); longer rows (cols % 128 == 0, <= 16384) stream
+// through a TMA ring into a CTA of W warps that shares each row
+// (softmax_*_long_kernel).  Other shapes use the generic warp-per-row kernels.
 #include <initializer_list>
 
 #include "common.cuh"
@@ -35,6 +37,12 @@ constexpr int kBlock = 256;
 #endif
 
 enum FwdMode { kPlain = 0, kSupplied = 1, kPhilox = 2 };
+#ifndef TM_SOFTMAX_LONG_MIN
+#define TM_SOFTMAX_LONG_MIN 1024  // rows longer than this take the TMA row-group kernels
+#endif
+#ifndef TM_SOFTMAX_LONG_MIN_BWD
+#define TM_SOFTMAX_LONG_MIN_BWD 512  // backward: S = 1024 too (vec VPL=8 needs 154+ regs: 0.70 -> 0.84)
+#endif
 
 #ifndef TM_SOFTMAX_TWOSUM
 #define TM_SOFTMAX_TWOSUM 1
@@ -287,6 +295,245 @@ __global__ void __launch_bounds__(kBlock) softmax_bwd_vec_kernel(
     }
 }
 
+// ------------------------------------------------------------- long rows
+// S > 1024 (the paper's sweep reaches S = 3072): one CTA =
+// one row group of W warps, persistent over rows r = blockIdx.x + i*gridDim.x.
+// The rows stream into a shallow shared-memory ring by TMA bulk
+// copies (cp.async.bulk, one mbarrier per stage; thread 0 issues): the bytes
+// in flight per SM are bounded by shared memory, not by the registers that
+// hold a row -- a register-only row group keeps ~64 KB per SM in flight and
+// reaches 0.58-0.75 of the copy peak at S = 2048-8192.  The row's 128-column
+// chunks are dealt round-robin to the warps (warp w: chunks w, w+W, ...; at
+// most VPL each), read from the stage into registers, and the row max / sum /
+// dot are warp shuffles plus ONE exchange of the W warp partials through
+// shared memory (__syncthreads; partials combined in warp order in every
+// thread, slots alternating by row parity).  The first exchange of a row also
+// proves every warp has read the stage, so thread 0 refills it right there.
+// Still one HBM read and one write per element; numerics as the vec kernels
+// (the plain and dropout P are bitwise equal).
+// ring depth per direction (fewer when a row is too long for the smem
+// budget): measured, occupancy (CTAs per SM) is worth more than depth
+#ifndef TM_SMXL_FWD_STAGES
+#define TM_SMXL_FWD_STAGES 2
+#endif
+#ifndef TM_SMXL_BWD_STAGES
+#define TM_SMXL_BWD_STAGES 1  // A/B: 1 stage 0.92/0.86/0.91/0.86 at S = 2048/3072/4096/8192 vs 0.87/0.87/0.87/0.67 with 2
+#endif
+constexpr size_t kLongRingBytes = 192 * 1024;
+
+__device__ __forceinline__ void ring_init(uint64_t* full, int ns) {
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < ns; ++s) mbar_init(&full[s], 1);
+        mbar_fence_init();
+    }
+    __syncthreads();
+}
+
+template <int W, int VPL, int MODE>
+__global__ void __launch_bounds__(W * 32) softmax_fwd_long_kernel(
+    const float* __restrict__ z, float* __restrict__ P, float* __restrict__ D,
+    uint32_t* __restrict__ mask, double scale, uint64_t thresh, uint64_t seed, uint64_t offset,
+    int64_t rows, int nch, int ns) {
+    grid_dep_wait();  // PDL: predecessor complete and visible
+    grid_dep_launch();
+    extern __shared__ __align__(128) unsigned char dsm[];
+    uint64_t* full = reinterpret_cast<uint64_t*>(dsm);
+    const float4* ring = reinterpret_cast<const float4*>(dsm + 128);
+    __shared__ float red[2][2][W];  // [row parity][max, sum][warp]
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int64_t C = (int64_t)nch * 128;
+    const uint32_t row_bytes = (uint32_t)C * 4u;
+    ring_init(full, ns);
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < ns; ++s) {
+            const int64_t r = blockIdx.x + (int64_t)s * gridDim.x;
+            if (r < rows) {
+                mbar_expect_tx(&full[s], row_bytes);
+                bulk_g2s((void*)(ring + (size_t)s * (C / 4)), z + r * C, row_bytes, &full[s]);
+            }
+        }
+    }
+    int it = 0;
+    for (int64_t r = blockIdx.x; r < rows; r += gridDim.x, ++it) {
+        const int st = it % ns;
+        uint32_t nib[VPL];
+        if (MODE == kSupplied) {  // mask words straight from global (1/32 of the bytes)
+#pragma unroll
+            for (int k = 0; k < VPL; ++k)
+                if (w + k * W < nch) nib[k] = chunk_nibble(mask + ((r * C) >> 5) + (w + k * W) * 4, lane);
+        }
+        mbar_wait(&full[st], (uint32_t)((it / ns) & 1));
+        const float4* sp = ring + (size_t)st * (C / 4);
+        float4 v[VPL];
+        float mx = -INFINITY;
+#pragma unroll
+        for (int k = 0; k < VPL; ++k) {
+            const int c = w + k * W;
+            if (c < nch) {
+                v[k] = sp[c * 32 + lane];
+                mx = fmax_nan(mx, fmax_nan(fmax_nan(v[k].x, v[k].y), fmax_nan(v[k].z, v[k].w)));
+            }
+        }
+        const int par = it & 1;
+        mx = warp_max_nan(mx);
+        if (lane == 0) red[par][0][w] = mx;
+        __syncthreads();  // every warp has read stage st: refill it
+        if (threadIdx.x == 0) {
+            const int64_t rn = r + (int64_t)ns * gridDim.x;
+            if (rn < rows) {
+                fence_proxy_async_smem();
+                mbar_expect_tx(&full[st], row_bytes);
+                bulk_g2s((void*)(ring + (size_t)st * (C / 4)), z + rn * C, row_bytes, &full[st]);
+            }
+        }
+        mx = red[par][0][0];
+#pragma unroll
+        for (int i = 1; i < W; ++i) mx = fmax_nan(mx, red[par][0][i]);
+        float acc = 0.0f;
+#pragma unroll
+        for (int k = 0; k < VPL; ++k) {
+            if (w + k * W >= nch) continue;
+#if TM_SOFTMAX_PACKED
+            const float2 lo = exp_shift2(make_float2(v[k].x, v[k].y), mx);
+            const float2 hi = exp_shift2(make_float2(v[k].z, v[k].w), mx);
+            v[k] = make_float4(lo.x, lo.y, hi.x, hi.y);
+#else
+            v[k] = make_float4(exp_shift(v[k].x, mx), exp_shift(v[k].y, mx),
+                               exp_shift(v[k].z, mx), exp_shift(v[k].w, mx));
+#endif
+            acc += (v[k].x + v[k].y) + (v[k].z + v[k].w);
+        }
+        acc = warp_sumf(acc);
+        if (lane == 0) red[par][1][w] = acc;
+        __syncthreads();
+        float sum = red[par][1][0];
+#pragma unroll
+        for (int i = 1; i < W; ++i) sum += red[par][1][i];
+        const float inv = row_inv(sum, mx);
+        float4* Pr = reinterpret_cast<float4*>(P + r * C);
+        float4* Dr = reinterpret_cast<float4*>(D + r * C);
+#pragma unroll
+        for (int k = 0; k < VPL; ++k) {
+            const int c = w + k * W;
+            if (c >= nch) continue;
+            const float4 p = make_float4(v[k].x * inv, v[k].y * inv, v[k].z * inv, v[k].w * inv);
+            st_stream(Pr + c * 32 + lane, p);
+            if (MODE == kPlain) continue;
+            uint32_t bits;
+            if (MODE == kPhilox) {
+                U4 rnd = philox_quad(seed, (offset + (uint64_t)(r * C + c * 128 + lane * 4)) >> 2);
+                bits = nibble4((uint64_t)rnd.x >= thresh, (uint64_t)rnd.y >= thresh,
+                               (uint64_t)rnd.z >= thresh, (uint64_t)rnd.w >= thresh);
+                store_chunk_mask(mask + ((r * C) >> 5) + c * 4, bits, lane);
+            } else {
+                bits = nib[k];
+            }
+            if (D) {
+                float4 d;
+                d.x = (bits & 1u) ? dscale(p.x, scale) : 0.0f;
+                d.y = (bits & 2u) ? dscale(p.y, scale) : 0.0f;
+                d.z = (bits & 4u) ? dscale(p.z, scale) : 0.0f;
+                d.w = (bits & 8u) ? dscale(p.w, scale) : 0.0f;
+                st_stream(Dr + c * 32 + lane, d);
+            }
+        }
+    }
+}
+
+template <int W, int VPL, bool DROP, bool WRITE_D>
+__global__ void __launch_bounds__(W * 32) softmax_bwd_long_kernel(
+    const float* __restrict__ dD, const float* __restrict__ P, const uint32_t* __restrict__ mask,
+    double scale, float* __restrict__ dZ, float* __restrict__ D, int64_t rows, int nch, int ns) {
+    grid_dep_wait();  // PDL: predecessor complete and visible
+    grid_dep_launch();
+    extern __shared__ __align__(128) unsigned char dsm[];
+    uint64_t* full = reinterpret_cast<uint64_t*>(dsm);
+    const float4* ring = reinterpret_cast<const float4*>(dsm + 128);  // [stage][dD, P][C/4]
+    __shared__ double red[2][W];  // [row parity][warp]
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int64_t C = (int64_t)nch * 128;
+    const uint32_t row_bytes = (uint32_t)C * 4u;
+    auto issue = [&](int64_t r, int s) {
+        mbar_expect_tx(&full[s], 2 * row_bytes);
+        bulk_g2s((void*)(ring + (size_t)(2 * s) * (C / 4)), dD + r * C, row_bytes, &full[s]);
+        bulk_g2s((void*)(ring + (size_t)(2 * s + 1) * (C / 4)), P + r * C, row_bytes, &full[s]);
+    };
+    ring_init(full, ns);
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < ns; ++s) {
+            const int64_t r = blockIdx.x + (int64_t)s * gridDim.x;
+            if (r < rows) issue(r, s);
+        }
+    }
+    int it = 0;
+    for (int64_t r = blockIdx.x; r < rows; r += gridDim.x, ++it) {
+        const int st = it % ns;
+        uint32_t nib[VPL];
+        if (DROP) {
+#pragma unroll
+            for (int k = 0; k < VPL; ++k)
+                if (w + k * W < nch) nib[k] = chunk_nibble(mask + ((r * C) >> 5) + (w + k * W) * 4, lane);
+        }
+        mbar_wait(&full[st], (uint32_t)((it / ns) & 1));
+        const float4* gs = ring + (size_t)(2 * st) * (C / 4);
+        const float4* ps = ring + (size_t)(2 * st + 1) * (C / 4);
+        float4 gv[VPL], p[VPL];
+        double acc = 0.0;
+#pragma unroll
+        for (int k = 0; k < VPL; ++k) {
+            const int c = w + k * W;
+            if (c >= nch) continue;
+            gv[k] = gs[c * 32 + lane];
+            p[k] = ps[c * 32 + lane];
+            if (DROP) {  // dropout_backward: F32-stored dP (ops_reference.cpp:155-161)
+                gv[k].x = (nib[k] & 1u) ? dscale(gv[k].x, scale) : 0.0f;
+                gv[k].y = (nib[k] & 2u) ? dscale(gv[k].y, scale) : 0.0f;
+                gv[k].z = (nib[k] & 4u) ? dscale(gv[k].z, scale) : 0.0f;
+                gv[k].w = (nib[k] & 8u) ? dscale(gv[k].w, scale) : 0.0f;
+            }
+            acc = fma((double)gv[k].x, (double)p[k].x, acc);
+            acc = fma((double)gv[k].y, (double)p[k].y, acc);
+            acc = fma((double)gv[k].z, (double)p[k].z, acc);
+            acc = fma((double)gv[k].w, (double)p[k].w, acc);
+        }
+        const int par = it & 1;
+        acc = warp_sum(acc);
+        if (lane == 0) red[par][w] = acc;
+        __syncthreads();  // every warp has read stage st: refill it
+        if (threadIdx.x == 0) {
+            const int64_t rn = r + (int64_t)ns * gridDim.x;
+            if (rn < rows) {
+                fence_proxy_async_smem();
+                issue(rn, st);
+            }
+        }
+        double s = red[par][0];
+#pragma unroll
+        for (int i = 1; i < W; ++i) s += red[par][i];
+        float4* zr = reinterpret_cast<float4*>(dZ + r * C);
+        float4* Dr = reinterpret_cast<float4*>(D + r * C);
+#pragma unroll
+        for (int k = 0; k < VPL; ++k) {
+            const int c = w + k * W;
+            if (c >= nch) continue;
+            float4 o;
+            o.x = (float)((double)p[k].x * ((double)gv[k].x - s));
+            o.y = (float)((double)p[k].y * ((double)gv[k].y - s));
+            o.z = (float)((double)p[k].z * ((double)gv[k].z - s));
+            o.w = (float)((double)p[k].w * ((double)gv[k].w - s));
+            st_stream(zr + c * 32 + lane, o);
+            if (WRITE_D) {
+                float4 d;
+                d.x = (nib[k] & 1u) ? dscale(p[k].x, scale) : 0.0f;
+                d.y = (nib[k] & 2u) ? dscale(p[k].y, scale) : 0.0f;
+                d.z = (nib[k] & 4u) ? dscale(p[k].z, scale) : 0.0f;
+                d.w = (nib[k] & 8u) ? dscale(p[k].w, scale) : 0.0f;
+                st_stream(Dr + c * 32 + lane, d);
+            }
+        }
+    }
+}
+
 // ---------------------------------------------------------------- generic
 __device__ __forceinline__ bool mask_bit(const uint32_t* mask, int64_t i) {
     return (__ldg(mask + (i >> 5)) >> (i & 31)) & 1u;
@@ -314,14 +561,33 @@ __global__ void __launch_bounds__(kBlock) softmax_fwd_generic_kernel(
             float p = (float)((double)exp_shift(zr[j], mx) * inv);
             P[i] = p;
             if (mode == kPlain) continue;
-            bool keep;
-            if (mode == kPhilox) {
-                keep = (uint64_t)philox_at(seed, offset + (uint64_t)i) >= thresh;
-                if (keep) atomicOr(mask + (i >> 5), 1u << (i & 31));
-            } else {
-                keep = mask_bit(mask, i);
-            }
+            const bool keep = mode == kPhilox
+                                  ? (uint64_t)philox_at(seed, offset + (uint64_t)i) >= thresh
+                                  : mask_bit(mask, i);
             if (D) D[i] = keep ? dscale(p, scale) : 0.0f;
+        }
+        if (mode == kPhilox) {
+            // The row's mask words, whole words per lane (no atomics): a word
+            // shared with the neighbouring row is written by both warps with
+            // the same value -- its bits depend only on (seed, index).
+            const int64_t n = rows * C;
+            for (int64_t wd = (r * C) >> 5, w1 = (r * C + C - 1) >> 5; wd <= w1; wd += 32) {
+                if (wd + lane > w1) break;
+                const int64_t i0 = (wd + lane) * 32;
+                uint32_t word = 0;
+                uint64_t qi = ~0ull;
+                U4 q{};
+                for (int b = 0; b < 32 && i0 + b < n; ++b) {
+                    const uint64_t gi = offset + (uint64_t)(i0 + b);
+                    if ((gi >> 2) != qi) {
+                        qi = gi >> 2;
+                        q = philox_quad(seed, qi);
+                    }
+                    const uint32_t x = (gi & 3) == 0 ? q.x : (gi & 3) == 1 ? q.y : (gi & 3) == 2 ? q.z : q.w;
+                    word |= (uint32_t)((uint64_t)x >= thresh) << b;
+                }
+                mask[wd + lane] = word;
+            }
         }
     }
 }
@@ -408,11 +674,112 @@ cudaError_t bwd_vec(int vpl, const float* dD, const float* P, const uint32_t* ma
     return cudaGetLastError();
 }
 
-bool vec_ok(int64_t cols, uint64_t offset, std::initializer_list<const void*> ptrs) {
-    if (cols % 128 != 0 || cols > 1024 || cols == 0 || (offset & 3u)) return false;
+bool vec_ok(int64_t cols, uint64_t offset, std::initializer_list<const void*> ptrs,
+            int64_t max_cols = TM_SOFTMAX_LONG_MIN) {
+    if (cols % 128 != 0 || cols > 1024 || cols > max_cols || cols == 0 || (offset & 3u))
+        return false;
     for (const void* p : ptrs)
         if (p && !aligned16(p)) return false;
     return true;
+}
+
+// long rows: cols % 128 == 0, TM_SOFTMAX_LONG_MIN < cols <= 16384, with
+// VPL = 4 chunks per warp (W = nch/4 rounded up to a power of two, <= 16) or
+// VPL = 8 at W = 16
+constexpr int kLongMaxCols = 16 * 8 * 128;
+bool long_ok(int64_t cols, uint64_t offset, std::initializer_list<const void*> ptrs,
+             int64_t min_cols = TM_SOFTMAX_LONG_MIN) {
+    if (cols % 128 != 0 || cols <= min_cols || cols > kLongMaxCols || (offset & 3u))
+        return false;
+    for (const void* p : ptrs)
+        if (p && !aligned16(p)) return false;
+    return true;
+}
+// (W, VPL) code W*10 + VPL with W*VPL >= nch: VPL (4 or 8) chunks per warp,
+// W the smallest power of two that covers the row (<= 16).  Measured at
+// 2^27 elements (tools/long_rows_bench.py): the forward wants more work per
+// warp between the row's barriers (VPL 8: S = 2048/3072/8192 at 0.90/0.87/
+// 0.86 of the copy peak vs 0.83/0.77/0.80 with VPL 4), the backward -- twice
+// the registers and smem per row -- more CTAs per SM (VPL 4).
+#ifndef TM_SMXL_FWD_VPL
+#define TM_SMXL_FWD_VPL 8
+#endif
+#ifndef TM_SMXL_BWD_VPL
+#define TM_SMXL_BWD_VPL 4
+#endif
+inline int long_cfg(int nch, int vpl) {
+    if (vpl == 8) return nch <= 16 ? 28 : nch <= 32 ? 48 : nch <= 64 ? 88 : 168;
+    return nch <= 8 ? 24 : nch <= 16 ? 44 : nch <= 32 ? 84 : nch <= 64 ? 164 : 168;
+}
+inline int long_stages(int64_t cols, int tensors) {
+    const size_t stage = (size_t)tensors * cols * sizeof(float);
+    const int ns = (int)(kLongRingBytes / stage);
+    const int want = tensors == 1 ? TM_SMXL_FWD_STAGES : TM_SMXL_BWD_STAGES;
+    return ns < 1 ? 1 : ns > want ? want : ns;
+}
+inline size_t long_smem(int64_t cols, int tensors) {
+    return 128 + (size_t)long_stages(cols, tensors) * tensors * cols * sizeof(float);
+}
+
+template <int MODE>
+cudaError_t fwd_long(int nch, const float* z, float* P, float* D, uint32_t* mask, double scale,
+                     uint64_t thresh, uint64_t seed, uint64_t offset, int64_t rows,
+                     cudaStream_t st) {
+    const size_t smem = long_smem((int64_t)nch * 128, 1);
+#define TB_FWDL_CASE(W, V)                                                                    \
+    case W * 10 + V: {                                                                        \
+        auto k = softmax_fwd_long_kernel<W, V, MODE>;                                         \
+        int grid = grid_for((const void*)k, W * 32, smem, rows);                              \
+        launch(k, grid, W * 32, smem, st)(z, P, D, mask, scale, thresh, seed, offset, rows, nch, \
+                                          long_stages((int64_t)nch * 128, 1));                \
+        break;                                                                                \
+    }
+    switch (long_cfg(nch, TM_SMXL_FWD_VPL)) {
+#if TM_SMXL_FWD_VPL == 8
+        TB_FWDL_CASE(2, 8)
+        TB_FWDL_CASE(4, 8)
+        TB_FWDL_CASE(8, 8)
+#else
+        TB_FWDL_CASE(2, 4)
+        TB_FWDL_CASE(4, 4)
+        TB_FWDL_CASE(8, 4)
+        TB_FWDL_CASE(16, 4)
+#endif
+        TB_FWDL_CASE(16, 8)
+        default: return cudaErrorInvalidValue;
+    }
+#undef TB_FWDL_CASE
+    return cudaGetLastError();
+}
+
+template <bool DROP, bool WRITE_D>
+cudaError_t bwd_long(int nch, const float* dD, const float* P, const uint32_t* mask, double scale,
+                     float* dZ, float* D, int64_t rows, cudaStream_t st) {
+    const size_t smem = long_smem((int64_t)nch * 128, 2);
+#define TB_BWDL_CASE(W, V)                                                                    \
+    case W * 10 + V: {                                                                        \
+        auto k = softmax_bwd_long_kernel<W, V, DROP, WRITE_D>;                                \
+        int grid = grid_for((const void*)k, W * 32, smem, rows);                              \
+        launch(k, grid, W * 32, smem, st)(dD, P, mask, scale, dZ, D, rows, nch,               \
+                                          long_stages((int64_t)nch * 128, 2));                \
+        break;                                                                                \
+    }
+    switch (long_cfg(nch, TM_SMXL_BWD_VPL)) {
+#if TM_SMXL_BWD_VPL == 8
+        TB_BWDL_CASE(2, 8)
+        TB_BWDL_CASE(4, 8)
+        TB_BWDL_CASE(8, 8)
+#else
+        TB_BWDL_CASE(2, 4)
+        TB_BWDL_CASE(4, 4)
+        TB_BWDL_CASE(8, 4)
+        TB_BWDL_CASE(16, 4)
+#endif
+        TB_BWDL_CASE(16, 8)
+        default: return cudaErrorInvalidValue;
+    }
+#undef TB_BWDL_CASE
+    return cudaGetLastError();
 }
 
 int generic_grid(const void* k, int64_t rows) {
@@ -426,6 +793,8 @@ cudaError_t launch_softmax_fwd(const float* z, float* P, int64_t rows, int64_t c
     if (rows == 0 || cols == 0) return cudaSuccess;
     if (vec_ok(cols, 0, {z, P}))
         return fwd_vec<kPlain>((int)(cols / 128), z, P, nullptr, nullptr, 1.0, 0, 0, 0, rows, st);
+    if (long_ok(cols, 0, {z, P}))
+        return fwd_long<kPlain>((int)(cols / 128), z, P, nullptr, nullptr, 1.0, 0, 0, 0, rows, st);
     launch(softmax_fwd_generic_kernel, generic_grid((const void*)softmax_fwd_generic_kernel, rows),
                                  kBlock, 0, st)(z, P, nullptr, nullptr, kPlain, 1.0, 0, 0, 0,
                                                   rows, cols);
@@ -435,9 +804,12 @@ cudaError_t launch_softmax_fwd(const float* z, float* P, int64_t rows, int64_t c
 cudaError_t launch_softmax_bwd(const float* dP, const float* P, float* dZ, int64_t rows,
                                int64_t cols, cudaStream_t st) {
     if (rows == 0 || cols == 0) return cudaSuccess;
-    if (vec_ok(cols, 0, {dP, P, dZ}))
+    if (vec_ok(cols, 0, {dP, P, dZ}, TM_SOFTMAX_LONG_MIN_BWD))
         return bwd_vec<false, false>((int)(cols / 128), dP, P, nullptr, 1.0, dZ, nullptr, rows,
                                      st);
+    if (long_ok(cols, 0, {dP, P, dZ}, TM_SOFTMAX_LONG_MIN_BWD))
+        return bwd_long<false, false>((int)(cols / 128), dP, P, nullptr, 1.0, dZ, nullptr, rows,
+                                      st);
     launch(softmax_bwd_generic_kernel, generic_grid((const void*)softmax_bwd_generic_kernel, rows),
                                  kBlock, 0, st)(dP, P, nullptr, 0, 1.0, dZ, nullptr, rows,
                                                   cols);
@@ -454,9 +826,11 @@ cudaError_t launch_softmax_dropout_fwd(const float* z, double scale, uint64_t th
                       : fwd_vec<kSupplied>(vpl, z, P, D, mask, scale, thresh, seed, offset, rows,
                                            st);
     }
-    if (philox) {
-        cudaError_t e = cudaMemsetAsync(mask, 0, (size_t)((rows * cols + 31) / 32) * 4, st);
-        if (e != cudaSuccess) return e;
+    if (long_ok(cols, offset, {z, P, D, mask})) {
+        const int nch = (int)(cols / 128);
+        return philox ? fwd_long<kPhilox>(nch, z, P, D, mask, scale, thresh, seed, offset, rows, st)
+                      : fwd_long<kSupplied>(nch, z, P, D, mask, scale, thresh, seed, offset, rows,
+                                            st);
     }
     launch(softmax_fwd_generic_kernel, generic_grid((const void*)softmax_fwd_generic_kernel, rows),
                                  kBlock, 0, st)(z, P, D, mask, philox ? kPhilox : kSupplied,
@@ -468,10 +842,15 @@ cudaError_t launch_attn_probs_bwd(const float* dD, const float* P, const uint32_
                                   double scale, float* dZ, float* D, int64_t rows, int64_t cols,
                                   cudaStream_t st) {
     if (rows == 0 || cols == 0) return cudaSuccess;
-    if (vec_ok(cols, 0, {dD, P, dZ, D, mask})) {
+    if (vec_ok(cols, 0, {dD, P, dZ, D, mask}, TM_SOFTMAX_LONG_MIN_BWD)) {
         const int vpl = (int)(cols / 128);
         return D ? bwd_vec<true, true>(vpl, dD, P, mask, scale, dZ, D, rows, st)
                  : bwd_vec<true, false>(vpl, dD, P, mask, scale, dZ, nullptr, rows, st);
+    }
+    if (long_ok(cols, 0, {dD, P, dZ, D, mask}, TM_SOFTMAX_LONG_MIN_BWD)) {
+        const int nch = (int)(cols / 128);
+        return D ? bwd_long<true, true>(nch, dD, P, mask, scale, dZ, D, rows, st)
+                 : bwd_long<true, false>(nch, dD, P, mask, scale, dZ, nullptr, rows, st);
     }
     launch(softmax_bwd_generic_kernel, generic_grid((const void*)softmax_bwd_generic_kernel, rows),
                                  kBlock, 0, st)(dD, P, mask, 1, scale, dZ, D, rows, cols);

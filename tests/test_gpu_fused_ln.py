@@ -13,8 +13,9 @@ from test_gpu_parity import bits_to_dev, rel_err, to_dev, unpack
 
 pytestmark = pytest.mark.gpu
 
+# 1536 / 2048 / 3072 / 4096 / 8192 / 16384: the long-row (warp-group) kernels
 SHAPES = [(64, 1024), (333, 768), (7, 512), (5, 128), (9, 1536), (3, 96), (16, 4096),
-          (1, 1024), (40, 384)]
+          (1, 1024), (40, 384), (9, 2048), (5, 3072), (3, 8192), (2, 16384), (3, 2080)]
 
 
 def inputs(rows, cols, seed, p):
@@ -57,7 +58,8 @@ def test_fused_forward_matches_reference_composition(tops, port, cuda, rows, col
 
 
 @pytest.mark.parametrize("rows,cols,offset", [(64, 1024, 0), (33, 768, 4096 * 768),
-                                              (8, 96, 32 * 7), (9, 1536, 128)])
+                                              (8, 96, 32 * 7), (9, 1536, 128),
+                                              (5, 3072, 3072 * 11), (2, 16384, 0)])
 def test_fused_forward_philox_mask_is_dropouts(tops, cuda, rows, cols, offset):
     """Generated masks are the bits tempo_dropout_fwd draws for the same
     global element offsets (so row shards and the unfused path agree)."""
@@ -75,7 +77,8 @@ def test_fused_forward_philox_mask_is_dropouts(tops, cuda, rows, cols, offset):
 
 
 @pytest.mark.parametrize("rows,cols", [(64, 1024), (333, 768), (7, 512), (9, 1536), (3, 96),
-                                       (16, 4096), (2048, 1024)])
+                                       (16, 4096), (2048, 1024), (9, 2048), (5, 3072),
+                                       (300, 4096), (3, 8192), (2, 16384), (3, 2080)])
 def test_fused_backward_matches_reference_composition(tops, port, cuda, rows, cols):
     import torch
     p = 0.1
