@@ -23,10 +23,18 @@
 // walks row tiles with a grid stride; the tiles arrive through a TMA
 // (cp.async.bulk) ring in shared memory, kStages deep.  Row reductions are
 // warp shuffles plus one smem exchange (fixed order, identical in every
-// thread).  Rows longer than 2048 (cols % 128 == 0) are held in the
-// registers of a group of warps (ln_fwd_long_kernel / ln_bwd_long_kernel);
-// cols % 4 != 0, other long rows or unaligned pointers use the generic
-// kernels (one element per thread per pass).
+// thread).  Long rows: the forward (cols % 128 == 0, > 1024) streams whole
+// rows through a TMA ring into a CTA of W warps (ln_fwd_long_kernel); the
+// backward (cols % 4 == 0, 2048 < cols <= 16384) splits the columns over a
+// thread-block cluster whose CTAs exchange the row sums through distributed
+// shared memory (ln_bwd_cluster_kernel).  Other shapes and unaligned
+// pointers use the generic kernels (one element per thread per pass).
+#include <cooperative_groups.h>
+
+#include <algorithm>
+#include <map>
+#include <mutex>
+
 #include "common.cuh"
 #include "tempo_internal.h"
 
@@ -675,10 +683,6 @@ inline size_t lnl_smem(int64_t cols, int tensors) {
 // forward: W * 8 chunks cover the row
 inline int lnl_fwd_warps(int64_t nch) { return nch <= 16 ? 2 : nch <= 32 ? 4 : nch <= 64 ? 8 : 16; }
 
-inline int long_warps(int64_t nch) {
-    return nch <= 4 * kLongVPL ? 4 : nch <= 8 * kLongVPL ? 8 : 16;
-}
-
 size_t warp_fwd_smem(int vpl) {
     return 1024 + 2 * (size_t)vpl * 128 * 4 + (size_t)kWWarps * kWStages * vpl * 128 * 4;
 }
@@ -966,144 +970,207 @@ __global__ void __launch_bounds__(256) ln_bwd_generic_kernel(
     for (int j = threadIdx.x; j < 2 * cols; j += blockDim.x) wg[j] = part[j];
 }
 
-// Stage 1, long rows (cols % 128 == 0, 2048 < cols <= 8192): one CTA = one
-// row group of W warps (W = 4 or 8), the row's 128-column chunks dealt
-// round-robin to its warps and held in registers (dy and y read once from
-// HBM); the two row sums are exchanged through shared memory.  The per-CTA
-// fp64 dgamma/dbeta column partials (too many columns for registers) live in
-// shared memory, lane-transposed ([chunk][k][lane]: conflict-free 64-bit
-// accesses); each column belongs to one thread, so they are updated without
-// synchronisation.  gamma, beta and 1/gamma are staged in shared memory
-// (float4 per lane, conflict-free).  28 B of smem per column.  DROP as in
-// ln_bwd_vec_kernel.
-template <int W, bool DROP>
-__global__ void __launch_bounds__(W * 32) ln_bwd_long_kernel(
+// Stage 1, long rows on a thread-block CLUSTER (2048 < cols <= 16384): the K
+// CTAs of a cluster split the columns (CTA rank q owns the slice [q*sw,
+// q*sw + sw), sw <= 4*NT, thread t the float4 at column q*sw + 4t) and walk the
+// SAME row tiles, so each CTA is ln_bwd_vec_kernel on its slice -- TMA ring of
+// kRowsB-row tiles (one bulk copy per row slice), gamma/beta and the fp64
+// dgamma/dbeta column partials in registers -- and the two row sums of a tile
+// are the fixed-order sum of the K CTAs' block sums, exchanged through
+// distributed shared memory: each CTA stores its 2*kRowsB sums into its own
+// slot, one cluster barrier, every thread reads the K slots (ld.shared::cluster)
+// in rank order.  Slots alternate by tile parity: a CTA reaches tile t+2's
+// store only after the barrier of tile t+1, i.e. after every peer read tile
+// t's slots.  The partial row of cluster c is ws[c] (its K CTAs write
+// disjoint column slices), reduced by the usual stage 2.
+template <int NT, bool DROP>
+__global__ void __launch_bounds__(NT) ln_bwd_cluster_kernel(
     const float* __restrict__ dy, const float* __restrict__ y, const float* __restrict__ rstd,
     const float* __restrict__ gamma, const float* __restrict__ beta, float* __restrict__ dx,
-    double* __restrict__ ws, int64_t rows, int nch, const uint32_t* __restrict__ mask,
+    double* __restrict__ ws, int64_t rows, int cols, int sw, const uint32_t* __restrict__ mask,
     double scale, float* __restrict__ dproj) {
+    namespace cg = cooperative_groups;
+    cg::cluster_group cluster = cg::this_cluster();
     grid_dep_wait();  // PDL: predecessor complete and visible
     grid_dep_launch_persistent();
-    constexpr int NT = W * 32;
-    const int cols = nch * 128;
     extern __shared__ __align__(128) unsigned char dsm[];
-    double* pg = reinterpret_cast<double*>(dsm);  // [cols], lane-transposed
-    double* pb = pg + cols;
-    float4* sg = reinterpret_cast<float4*>(pb + cols);  // [cols/4] gamma
-    float4* sb = sg + cols / 4;                         // beta
-    float4* si = sb + cols / 4;                         // float(1/gamma)
-    __shared__ float red[2][2][W];
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    for (int i = threadIdx.x; i < cols / 4; i += NT) {
-        const float4 g4 = reinterpret_cast<const float4*>(gamma)[i];
-        sg[i] = g4;
-        sb[i] = reinterpret_cast<const float4*>(beta)[i];
-        si[i] = make_float4((float)(1.0 / (double)g4.x), (float)(1.0 / (double)g4.y),
-                            (float)(1.0 / (double)g4.z), (float)(1.0 / (double)g4.w));
+    uint64_t* full = reinterpret_cast<uint64_t*>(dsm);
+    float* ring = reinterpret_cast<float*>(dsm + 128);
+    __shared__ float red[2 * 2 * kRowsB * 32];
+    __shared__ float xch[2][2 * kRowsB];  // [tile parity][s1, s2 per row]
+    __shared__ float xall[8 * 2 * kRowsB];  // the K CTAs' sums of the current tile
+    int phase = 0;
+    const int K = (int)cluster.num_blocks(), q = (int)cluster.block_rank();
+    const int64_t cid = blockIdx.x / K, ncl = gridDim.x / K;
+    const int c0 = q * sw;                        // first column of the slice
+    const int width = max(0, min(sw, cols - c0));  // columns of the slice (% 4 == 0)
+    const int tile_floats = kRowsB * sw;          // per tensor; a stage holds dy then y
+    const int64_t ntiles = (rows + kRowsB - 1) / kRowsB;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kStagesB; ++s) mbar_init(&full[s], 1);
+        mbar_fence_init();
     }
-    for (int i = threadIdx.x; i < 2 * cols; i += NT) pg[i] = 0.0;
     __syncthreads();
-    const float inv_m = 1.0f / (float)cols;
-    int par = 0;
-    for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
-        const float4* gr = reinterpret_cast<const float4*>(dy + r * cols);
-        const float4* yr = reinterpret_cast<const float4*>(y + r * cols);
-        float4 gv[kLongVPL], yv[kLongVPL];
-        uint32_t nib[kLongVPL];
+    auto issue = [&](int64_t t, int s) {
+        const int64_t r0 = t * kRowsB;
+        const int nr = (int)min((int64_t)kRowsB, rows - r0);
+        const uint32_t bytes = (uint32_t)width * 4u;
+        mbar_expect_tx(&full[s], 2 * nr * bytes);
+        for (int i = 0; i < nr; ++i) {
+            bulk_g2s(ring + (2 * s) * tile_floats + i * sw, dy + (r0 + i) * cols + c0, bytes, &full[s]);
+            bulk_g2s(ring + (2 * s + 1) * tile_floats + i * sw, y + (r0 + i) * cols + c0, bytes,
+                     &full[s]);
+        }
+    };
+    if (threadIdx.x == 0 && width > 0) {
+        for (int s = 0; s < kStagesB; ++s) {
+            const int64_t t = cid + (int64_t)s * ncl;
+            if (t < ntiles) issue(t, s);
+        }
+    }
+    const int cg4 = threadIdx.x;  // float4 column group within the slice
+    const bool act = 4 * cg4 < width;
+    const int col = c0 + 4 * cg4;
+    float gm[4], bt[4], igf[4];
+    double pg[4], pb[4];
+    {
+        float4 g = make_float4(1.f, 1.f, 1.f, 1.f), b = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (act) {
+            g = *reinterpret_cast<const float4*>(gamma + col);
+            b = *reinterpret_cast<const float4*>(beta + col);
+        }
+        const float ga[4] = {g.x, g.y, g.z, g.w}, ba[4] = {b.x, b.y, b.z, b.w};
 #pragma unroll
-        for (int k = 0; k < kLongVPL; ++k) {
-            const int c = w + k * W;
-            if (c < nch) {
-                gv[k] = ld_stream(gr + c * 32 + lane);
-                yv[k] = ld_stream(yr + c * 32 + lane);
-                if (DROP) nib[k] = chunk_nibble(mask + ((r * cols) >> 5) + c * 4, lane);
+        for (int k = 0; k < 4; ++k) {
+            gm[k] = ga[k];
+            bt[k] = ba[k];
+            igf[k] = (float)(1.0 / (double)ga[k]);
+            pg[k] = 0.0;
+            pb[k] = 0.0;
+        }
+    }
+    const float inv_m = 1.0f / (float)cols;
+    cluster.sync();  // every CTA of the cluster is running before any DSMEM access
+    int it = 0;
+    for (int64_t tile = cid; tile < ntiles; tile += ncl, ++it) {
+        const int64_t r0 = tile * kRowsB;
+        float rsv[kRowsB];
+        uint32_t mwv[kRowsB];
+#pragma unroll
+        for (int i = 0; i < kRowsB; ++i) {
+            const bool in = r0 + i < rows;
+            rsv[i] = in ? __ldg(rstd + r0 + i) : 0.f;
+            mwv[i] = (DROP && in && act) ? __ldg(mask + (((r0 + i) * cols + col) >> 5)) : 0u;
+        }
+        const int st = it % kStagesB;
+        float4 gv[kRowsB], yv[kRowsB];
+        if (width > 0) mbar_wait(&full[st], (uint32_t)((it / kStagesB) & 1));
+        const float* gs = ring + (2 * st) * tile_floats;
+        const float* ys = ring + (2 * st + 1) * tile_floats;
+#pragma unroll
+        for (int i = 0; i < kRowsB; ++i) {
+            gv[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+            yv[i] = gv[i];
+            if (r0 + i < rows && act) {
+                gv[i] = reinterpret_cast<const float4*>(gs + i * sw)[cg4];
+                yv[i] = reinterpret_cast<const float4*>(ys + i * sw)[cg4];
             }
         }
-        const float rs = __ldg(rstd + r);
-        float s1 = 0.0f, s2 = 0.0f;
+        float s[2 * kRowsB];
 #pragma unroll
-        for (int k = 0; k < kLongVPL; ++k) {
-            const int c = w + k * W;
-            if (c >= nch) continue;
-            const float4 gm = sg[c * 32 + lane], bt = sb[c * 32 + lane], ig = si[c * 32 + lane];
-            const float g0 = gv[k].x * gm.x, g1 = gv[k].y * gm.y, g2 = gv[k].z * gm.z,
-                        g3 = gv[k].w * gm.w;
-            s1 += g0;
-            s2 = fmaf(g0, (yv[k].x - bt.x) * ig.x, s2);
-            s1 += g1;
-            s2 = fmaf(g1, (yv[k].y - bt.y) * ig.y, s2);
-            s1 += g2;
-            s2 = fmaf(g2, (yv[k].z - bt.z) * ig.z, s2);
-            s1 += g3;
-            s2 = fmaf(g3, (yv[k].w - bt.w) * ig.w, s2);
+        for (int i = 0; i < kRowsB; ++i) {
+            const float ga[4] = {gv[i].x, gv[i].y, gv[i].z, gv[i].w};
+            const float ya[4] = {yv[i].x, yv[i].y, yv[i].z, yv[i].w};
+            float s1 = 0.0f, s2 = 0.0f;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const float gg = ga[k] * gm[k];
+                const float xh = (ya[k] - bt[k]) * igf[k];
+                s1 += gg;
+                s2 = fmaf(gg, xh, s2);
+            }
+            s[2 * i] = s1;
+            s[2 * i + 1] = s2;
         }
-        s1 = warp_sumf(s1);
-        s2 = warp_sumf(s2);
-        if (lane == 0) {
-            red[par][0][w] = s1;
-            red[par][1][w] = s2;
+        block_sum<2 * kRowsB>(s, red, phase);
+        if (threadIdx.x == 0 && width > 0) {  // stage consumed by every thread: refill
+            const int64_t nt = tile + (int64_t)kStagesB * ncl;
+            if (nt < ntiles) {
+                fence_proxy_async_smem();
+                issue(nt, st);
+            }
         }
+        const int par = it & 1;
+        if (threadIdx.x == 0) {
+#pragma unroll
+            for (int j = 0; j < 2 * kRowsB; ++j) xch[par][j] = s[j];
+        }
+        cluster.sync();
+        // K*2*kRowsB threads fetch the peers' sums (one remote load each), then
+        // every thread adds them from local smem in rank order
+        if (threadIdx.x < K * 2 * kRowsB)
+            xall[threadIdx.x] =
+                *cluster.map_shared_rank(&xch[par][threadIdx.x % (2 * kRowsB)], threadIdx.x / (2 * kRowsB));
         __syncthreads();
-        s1 = red[par][0][0];
-        s2 = red[par][1][0];
 #pragma unroll
-        for (int i = 1; i < W; ++i) {
-            s1 += red[par][0][i];
-            s2 += red[par][1][i];
+        for (int j = 0; j < 2 * kRowsB; ++j) s[j] = xall[j];
+        for (int p = 1; p < K; ++p) {  // fixed rank order: identical sums in every CTA
+#pragma unroll
+            for (int j = 0; j < 2 * kRowsB; ++j) s[j] += xall[p * 2 * kRowsB + j];
         }
-        par ^= 1;
-        const float c1 = s1 * inv_m, c2 = s2 * inv_m;
 #pragma unroll
-        for (int k = 0; k < kLongVPL; ++k) {
-            const int c = w + k * W;
-            if (c >= nch) continue;
-            const float4 gm4 = sg[c * 32 + lane], bt4 = sb[c * 32 + lane], ig4 = si[c * 32 + lane];
-            const float ga[4] = {gv[k].x, gv[k].y, gv[k].z, gv[k].w};
-            const float ya[4] = {yv[k].x, yv[k].y, yv[k].z, yv[k].w};
-            const float gm[4] = {gm4.x, gm4.y, gm4.z, gm4.w};
-            const float bt[4] = {bt4.x, bt4.y, bt4.z, bt4.w};
-            const float ig[4] = {ig4.x, ig4.y, ig4.z, ig4.w};
+        for (int i = 0; i < kRowsB; ++i) {
+            if (r0 + i >= rows || !act) continue;
+            const float c1 = s[2 * i] * inv_m, c2 = s[2 * i + 1] * inv_m;
+            const float ga[4] = {gv[i].x, gv[i].y, gv[i].z, gv[i].w};
+            const float ya[4] = {yv[i].x, yv[i].y, yv[i].z, yv[i].w};
             float o[4];
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const float xh = (ya[j] - bt[j]) * ig[j];
-                o[j] = (fmaf(ga[j], gm[j], -c1) - xh * c2) * rs;
-                const int pi = (c * 4 + j) * 32 + lane;  // column c*128 + 4*lane + j
-                const double gd = (double)ga[j];
-                pg[pi] = fma(gd, (double)ya[j], pg[pi]);
-                pb[pi] += gd;
+            for (int k = 0; k < 4; ++k) {
+                const float xh = (ya[k] - bt[k]) * igf[k];
+                o[k] = (fmaf(ga[k], gm[k], -c1) - xh * c2) * rsv[i];
+                const double gd = (double)ga[k];
+                pg[k] = fma(gd, (double)ya[k], pg[k]);
+                pb[k] += gd;
             }
-            st_stream(reinterpret_cast<float4*>(dx + r * cols) + c * 32 + lane,
-                      make_float4(o[0], o[1], o[2], o[3]));
+            const int64_t e = (r0 + i) * cols + col;
+            st_stream(reinterpret_cast<float4*>(dx + e), make_float4(o[0], o[1], o[2], o[3]));
             if (DROP) {
+                const uint32_t nb = (mwv[i] >> (e & 31)) & 0xfu;
                 float4 dp;
-                dp.x = (nib[k] & 1u) ? (float)((double)o[0] * scale) : 0.0f;
-                dp.y = (nib[k] & 2u) ? (float)((double)o[1] * scale) : 0.0f;
-                dp.z = (nib[k] & 4u) ? (float)((double)o[2] * scale) : 0.0f;
-                dp.w = (nib[k] & 8u) ? (float)((double)o[3] * scale) : 0.0f;
-                st_stream(reinterpret_cast<float4*>(dproj + r * cols) + c * 32 + lane, dp);
+                dp.x = (nb & 1u) ? (float)((double)o[0] * scale) : 0.0f;
+                dp.y = (nb & 2u) ? (float)((double)o[1] * scale) : 0.0f;
+                dp.z = (nb & 4u) ? (float)((double)o[2] * scale) : 0.0f;
+                dp.w = (nb & 8u) ? (float)((double)o[3] * scale) : 0.0f;
+                st_stream(reinterpret_cast<float4*>(dproj + e), dp);
             }
         }
     }
-    // sum g*xhat = (sum g*y - beta * sum g) / gamma per column (as ln_bwd_vec_kernel)
-    double* wg = ws + (size_t)blockIdx.x * 2 * cols;
-    for (int k = 0; k < kLongVPL; ++k) {
-        const int c = w + k * W;
-        if (c >= nch) continue;
-        const float4 gm4 = sg[c * 32 + lane], bt4 = sb[c * 32 + lane];
-        const float gm[4] = {gm4.x, gm4.y, gm4.z, gm4.w};
-        const float bt[4] = {bt4.x, bt4.y, bt4.z, bt4.w};
+    if (act) {
+        double* wg = ws + (size_t)cid * 2 * cols;
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            const int pi = (c * 4 + j) * 32 + lane;
-            const int col = c * 128 + lane * 4 + j;
-            wg[col] = fma(-(double)bt[j], pb[pi], pg[pi]) * (1.0 / (double)gm[j]);
-            wg[cols + col] = pb[pi];
+        for (int k = 0; k < 4; ++k) {
+            wg[col + k] = fma(-(double)bt[k], pb[k], pg[k]) * (1.0 / (double)gm[k]);
+            wg[cols + col + k] = pb[k];
         }
     }
+    cluster.sync();  // no CTA leaves while a peer may still read its slots
 }
 
-size_t bwd_long_smem(int64_t cols) { return (size_t)cols * (2 * sizeof(double) + 3 * sizeof(float)); }
+#ifndef TM_LN_CLUSTER_NT
+#define TM_LN_CLUSTER_NT 512
+#endif
+constexpr int kClusterNT = TM_LN_CLUSTER_NT;
+// cluster size and slice width for a long row: K = ceil(cols / (4*NT)), the
+// slice rounded up to a multiple of 4 columns
+inline int cluster_k(int64_t cols) { return (int)((cols + 4 * kClusterNT - 1) / (4 * kClusterNT)); }
+inline int cluster_sw(int64_t cols) {
+    const int k = cluster_k(cols);
+    return (int)(((cols + k - 1) / k + 3) / 4 * 4);
+}
+size_t bwd_cluster_smem(int64_t cols) {
+    return 128 + (size_t)kStagesB * 2 * kRowsB * cluster_sw(cols) * sizeof(float);
+}
 
 // Stage 2: out[j] = sum over CTAs c (fixed order) of ws[c][j], j < 2*cols.
 // A 32 x 32 block: column lane tx owns output j0 + tx, slice ty sums the
@@ -1296,14 +1363,49 @@ size_t bwd_smem(int64_t cols) { return 128 + (size_t)kStagesB * 2 * kRowsB * col
 bool long_fwd_ok(int64_t cols, int64_t min_cols) {
     return cols % 128 == 0 && cols > min_cols && cols <= 16 * kLongVPL * 128;
 }
-bool long_bwd_ok(int64_t cols) { return cols % 128 == 0 && cols > 4 * kMaxThreads && cols <= 8 * kLongVPL * 128; }
-const void* bwd_long_fn(int64_t cols, bool drop) {
-    if (long_warps(cols / 128) == 4)
-        return drop ? (const void*)ln_bwd_long_kernel<4, true> : (const void*)ln_bwd_long_kernel<4, false>;
-    return drop ? (const void*)ln_bwd_long_kernel<8, true> : (const void*)ln_bwd_long_kernel<8, false>;
+bool cluster_bwd_ok(int64_t cols) {
+    return cols % 4 == 0 && cols > 4 * kMaxThreads && cluster_k(cols) <= 8;
 }
-int bwd_long_grid(int64_t rows, int64_t cols) {
-    return grid_for(bwd_long_fn(cols, false), long_warps(cols / 128) * 32, bwd_long_smem(cols), rows);
+// CTAs (a multiple of K): as many clusters as can be co-resident -- a
+// persistent grid with clusters waiting for a second wave would serialise
+// (cluster placement is per GPC, so this is below SMs / K)
+int bwd_cluster_grid(int64_t rows, int64_t cols) {
+    static std::mutex mu;
+    static std::map<std::pair<int, int64_t>, int> cache;  // (device, cols) -> max active clusters
+    const int k = cluster_k(cols);
+    const int64_t ntiles = (rows + kRowsB - 1) / kRowsB;
+    const void* kf = (const void*)ln_bwd_cluster_kernel<kClusterNT, false>;
+    const size_t smem = bwd_cluster_smem(cols);
+    (void)grid_for(kf, kClusterNT, smem, 1);  // dynamic smem opt-in
+    int dev = 0;
+    cudaGetDevice(&dev);
+    int maxcl = 0;
+    {
+        std::lock_guard<std::mutex> lock(mu);
+        auto it = cache.find({dev, cols});
+        if (it != cache.end()) {
+            maxcl = it->second;
+        } else {
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3((unsigned)(k * 148));
+            cfg.blockDim = dim3((unsigned)kClusterNT);
+            cfg.dynamicSmemBytes = smem;
+            cudaLaunchAttribute attr[1];
+            attr[0].id = cudaLaunchAttributeClusterDimension;
+            attr[0].val.clusterDim.x = (unsigned)k;
+            attr[0].val.clusterDim.y = 1;
+            attr[0].val.clusterDim.z = 1;
+            cfg.attrs = attr;
+            cfg.numAttrs = 1;
+            if (cudaOccupancyMaxActiveClusters(&maxcl, kf, &cfg) != cudaSuccess || maxcl < 1) {
+                cudaGetLastError();
+                maxcl = 1;
+            }
+            cache[{dev, cols}] = maxcl;
+        }
+    }
+    const int64_t ncl = std::min<int64_t>(maxcl, ntiles);
+    return (int)(ncl < 1 ? 1 : ncl) * k;
 }
 
 // generic backward: partials in smem up to this many bytes, else in the
@@ -1422,7 +1524,7 @@ size_t ln_bwd_workspace(int64_t rows, int64_t cols) {
     // the larger of the two grids.
     int gv = (cols % 4 == 0 && cols <= 4 * kMaxThreads) ? bwd_grid(rows, cols, true) : 0;
     int gg = bwd_grid(rows, cols, false);
-    int gl = long_bwd_ok(cols) ? bwd_long_grid(rows, cols) : 0;
+    int gl = cluster_bwd_ok(cols) ? bwd_cluster_grid(rows, cols) / cluster_k(cols) : 0;
     int g = gv > gg ? gv : gg;
     g = gl > g ? gl : g;
     return (size_t)g * 2 * (size_t)cols * sizeof(double);
@@ -1442,21 +1544,22 @@ cudaError_t launch_ln_bwd(const float* dy, const float* y, const float* rstd, co
     const bool drop = dproj != nullptr;
     const bool aligned = aligned16(dy) && aligned16(y) && aligned16(dx) && aligned16(gamma) &&
                          aligned16(beta) && (!drop || aligned16(dproj));
-    const bool lng = long_bwd_ok(cols) && aligned;
-    const bool vec = !lng && use_vec(cols, dy, y, dx, gamma, beta) && (!drop || aligned16(dproj));
+    const bool clu = cluster_bwd_ok(cols) && aligned;
+    const bool vec = !clu && use_vec(cols, dy, y, dx, gamma, beta) &&
+                     (!drop || aligned16(dproj));
     // the grid (= the workspace's partial rows) is the plain kernel's, also
     // for the fused variant, so one workspace query serves both
-    const int grid = lng ? bwd_long_grid(rows, cols) : bwd_grid(rows, cols, vec);
+    const int grid = clu ? bwd_cluster_grid(rows, cols) / cluster_k(cols) : bwd_grid(rows, cols, vec);
     double* w = static_cast<double*>(ws);
-    if (lng) {
-        using KFn = void (*)(const float*, const float*, const float*, const float*,
-                             const float*, float*, double*, int64_t, int, const uint32_t*, double,
-                             float*);
-        KFn k = reinterpret_cast<KFn>(const_cast<void*>(bwd_long_fn(cols, drop)));
-        const int nt = long_warps(cols / 128) * 32;
-        if (drop) (void)grid_for((const void*)k, nt, bwd_long_smem(cols), grid);  // smem opt-in
-        launch(k, grid, nt, bwd_long_smem(cols), st)(dy, y, rstd, gamma, beta, dx, w, rows,
-                                                     (int)(cols / 128), mask, scale, dproj);
+    if (clu) {
+        const int k = cluster_k(cols);
+        auto kf = drop ? ln_bwd_cluster_kernel<kClusterNT, true> : ln_bwd_cluster_kernel<kClusterNT, false>;
+        const size_t smem = bwd_cluster_smem(cols);
+        (void)grid_for((const void*)kf, kClusterNT, smem, grid * k);  // smem opt-in
+        cudaError_t e = launch(kf, grid * k, kClusterNT, smem, st)
+                            .cluster((unsigned)k)(dy, y, rstd, gamma, beta, dx, w, rows, (int)cols,
+                                                  cluster_sw(cols), mask, scale, dproj);
+        if (e != cudaSuccess) return e;
     } else if (vec) {
         using KFn = void (*)(const float*, const float*, const float*, const float*,
                              const float*, float*, double*, int64_t, int, const uint32_t*, double,

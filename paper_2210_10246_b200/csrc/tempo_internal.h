@@ -154,11 +154,21 @@ template <typename... KArgs>
 struct Launch {
     void (*kernel)(KArgs...);
     cudaLaunchConfig_t cfg;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
+    unsigned nattr = 1;
+    // thread-block clusters of k CTAs along x (grid.x % k == 0)
+    Launch& cluster(unsigned k) {
+        attr[nattr].id = cudaLaunchAttributeClusterDimension;
+        attr[nattr].val.clusterDim.x = k;
+        attr[nattr].val.clusterDim.y = 1;
+        attr[nattr].val.clusterDim.z = 1;
+        ++nattr;
+        return *this;
+    }
     template <typename... A>
     cudaError_t operator()(A&&... a) {
         cfg.attrs = attr;
-        cfg.numAttrs = 1;
+        cfg.numAttrs = nattr;
         return cudaLaunchKernelEx(&cfg, kernel, std::forward<A>(a)...);
     }
 };

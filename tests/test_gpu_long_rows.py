@@ -149,7 +149,8 @@ def test_long_softmax_many_rows(tops, port, cuda):
 
 
 # ------------------------------------------------------------- LayerNorm
-LN_LONG_COLS = [2560, 3072, 4096, 5120, 8192, 12288, 2052, 3000]
+# 2052..16384: the cluster backward (K = 2..8 CTAs); 20000: generic kernels
+LN_LONG_COLS = [2560, 3072, 4096, 5120, 8192, 12288, 2052, 3000, 16384, 20000]
 
 
 @pytest.mark.parametrize("cols", LN_LONG_COLS)
