@@ -545,6 +545,70 @@ def per_config_timings(dev, peak, reps=40):
 
 
 # ------------------------------------- the recompute fused into its consumer
+def row_length_timings(dev, peak, reps=10):
+    """The row kernels across row lengths at a fixed element count (outside
+    the timed region): softmax+dropout fwd / attn-probs bwd over S (2^27
+    elements; S <= 1024 the warp-per-row kernels, longer rows the TMA
+    row-group kernels) and LayerNorm fwd/bwd over H (2^25 elements; H > 2048
+    backward on a thread-block cluster).  Each op alone, L2 cleaned by a 512 MB
+    read before every rep, median device time, algorithmic bytes."""
+    import statistics
+    import torch
+    from paper_2210_10246_b200 import ops
+    fb = torch.empty(128 * 1024 * 1024, device=dev).fill_(1.0)
+    sink = torch.empty((), device=dev)
+
+    def timeit(fn):
+        fn()
+        ts = []
+        for _ in range(reps):
+            torch.sum(fb, dim=0, out=sink)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            fn()
+            b.record()
+            b.synchronize()
+            ts.append(a.elapsed_time(b))
+        return statistics.median(ts)
+
+    def frac(nbytes, ms):
+        return round(nbytes / (ms * 1e-3) / 1e9 / peak, 4)
+
+    out = {"softmax": [], "layernorm": []}
+    g = torch.Generator(device=dev)
+    g.manual_seed(3)
+    for S in (512, 1024, 2048, 3072, 4096):
+        rows = (1 << 27) // S
+        n = rows * S
+        z, dD = torch.randn(rows, S, device=dev, generator=g), torch.randn(rows, S, device=dev, generator=g)
+        P, D, dZ = torch.empty_like(z), torch.empty_like(z), torch.empty_like(z)
+        m = torch.empty(ops.mask_words(n), dtype=torch.int32, device=dev)
+        tf = timeit(lambda: ops.softmax_dropout_fwd(z, P_DROP, mask=m, seed=1, P=P, D=D, generate=True))
+        tb = timeit(lambda: ops.attn_probs_bwd(dD, P, m, P_DROP, dZ=dZ))
+        out["softmax"].append({"S": S, "rows": rows, "fwd_ms": round(tf, 4),
+                               "fwd_frac": frac(n * 12.125, tf), "bwd_ms": round(tb, 4),
+                               "bwd_frac": frac(n * 12.125, tb)})
+        del z, dD, P, D, dZ, m
+    for H in (1024, 2048, 4096, 8192):
+        rows = (1 << 25) // H
+        n = rows * H
+        x, dy = torch.randn(rows, H, device=dev, generator=g), torch.randn(rows, H, device=dev, generator=g)
+        ga = (1 + 0.1 * torch.randn(H, device=dev, generator=g)).contiguous()
+        be = (0.1 * torch.randn(H, device=dev, generator=g)).contiguous()
+        y, dx, rs = torch.empty_like(x), torch.empty_like(x), torch.empty(rows, device=dev)
+        dg, db = torch.empty(H, device=dev), torch.empty(H, device=dev)
+        ws = torch.empty(max(16, int(ops.lib().tempo_ln_ip_bwd_workspace_size(rows, H))),
+                         dtype=torch.uint8, device=dev)
+        tf = timeit(lambda: ops.layernorm_ip_fwd(x, ga, be, check_gamma=False, y=y, rstd=rs))
+        tb = timeit(lambda: ops.layernorm_ip_bwd(dy, y, rs, ga, be, dx=dx, dgamma=dg, dbeta=db,
+                                                 workspace=ws))
+        out["layernorm"].append({"H": H, "rows": rows, "fwd_ms": round(tf, 4),
+                                 "fwd_frac": frac(n * 8, tf), "bwd_ms": round(tb, 4),
+                                 "bwd_frac": frac(n * 12, tb)})
+        del x, dy, y, dx
+    return out
+
+
 def dv_consumer_timings(chain, peak, reps=11, flush=None):
     """the attention-probability backward plus the
     consumer of the dropped-out map D, the dV GEMM (dV = D^T dO per head,
@@ -887,6 +951,12 @@ def main():
 
     # ---- configs[0..2] at their own shapes (outside the timed region) -------
     per_config = per_config_timings(dev, peak) if rank == 0 else None
+    per_row_length = None
+    if rank == 0:
+        try:
+            per_row_length = row_length_timings(dev, peak)
+        except Exception as ex:  # noqa: BLE001  (report, do not fail the bench)
+            per_row_length = {"unavailable": str(ex)[:200]}
     # ---- the dropout recompute fused into the dV GEMM ----
     dv_consumer = None
     if rank == 0:
@@ -986,6 +1056,7 @@ def main():
             "clocks": clk,
             "per_op": per_op_rows,
             "per_config": per_config,
+            "per_row_length": per_row_length,
             "dv_consumer": dv_consumer,
             "frac_of_peak": round(value / world / peak, 4),
             "unfused_equivalent": ({
