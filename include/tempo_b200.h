@@ -264,7 +264,7 @@ int tempo_attn_dropout_dv(const float* P, const uint32_t* mask, double p, const 
  * without storing the dropout output or r.  SUPPLIED reads `mask`, PHILOX
  * writes it (the same bits tempo_dropout_fwd generates for these global
  * element offsets).  cols % 32 == 0 (else TEMPO_ERR_UNSUPPORTED: use the
- * separate ops); cols <= 16384.  HBM: 12.125 B/element. */
+ * separate ops).  HBM: 12.125 B/element. */
 int tempo_dropout_add_ln_fwd(const float* proj, const float* residual, double p,
                              tempo_mask_mode_t mode, uint32_t* mask, uint64_t seed,
                              uint64_t offset, const float* gamma, const float* beta, double eps,

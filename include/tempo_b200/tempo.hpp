@@ -331,6 +331,19 @@ NodeId softmax_dropout(Graph& g, NodeId z, double p, BoolMask mask, std::uint64_
                        std::uint64_t offset, const std::string& probs_tag,
                        const std::string& drop_tag, const std::string& mask_tag,
                        NodeId* probs_out);
+// The reference layer's hidden dropout -> residual add -> layernorm
+// (encoder.cpp:180-191, 198-210: ref_ops::dropout(proj) -> Graph::add ->
+// tempo_ops::layernorm) as ONE node: y = LN(residual + dropout(proj)), stash
+// = y + rstd + the mask bits (neither the dropout output nor the sum is
+// stored); its backward returns {d_proj, d_residual, dgamma, dbeta} in one
+// pass (tempo_dropout_add_ln_fwd/bwd).  A Philox mask is generated when
+// `mask` is undefined (seed/offset: the bits ref_ops::dropout would read from
+// tempo_dropout_fwd's Philox stream), else it is read.  Inputs of the node:
+// {proj, residual, gamma, beta}.
+NodeId dropout_add_layernorm(Graph& g, NodeId proj, NodeId residual, double p, BoolMask mask,
+                             std::uint64_t seed, std::uint64_t offset, NodeId gamma,
+                             NodeId beta, double epsilon, std::string tag, std::string rstd_tag,
+                             std::string mask_tag);
 void ensure_recompute_rules();
 // ops_tempo.cpp:196-210: q k^T -> scale 1/sqrt(d) -> softmax-ip ->
 // dropout_recompute -> x v, on [B, A, S, d] inputs (DimensionError otherwise).

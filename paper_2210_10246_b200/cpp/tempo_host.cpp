@@ -874,6 +874,66 @@ NodeId layernorm(Graph& g, NodeId x, NodeId gamma, NodeId beta, double epsilon, 
         });
 }
 
+NodeId dropout_add_layernorm(Graph& g, NodeId proj, NodeId residual, double p, BoolMask mask,
+                             std::uint64_t seed, std::uint64_t offset, NodeId gamma,
+                             NodeId beta, double epsilon, std::string tag, std::string rstd_tag,
+                             std::string mask_tag) {  // encoder.cpp:180-191, 198-210
+    StreamScope scope_(g.stream);
+    const Tensor& vp = g.value(proj);
+    const Tensor& vr = g.value(residual);
+    const Tensor& vg = g.value(gamma);
+    const Tensor& vb = g.value(beta);
+    require_same_shape(vp.shape(), vr.shape(), "add");
+    const std::int64_t m = last_dim(vp.shape());
+    if (vg.shape() != Shape{m} || vb.shape() != Shape{m})
+        throw DimensionError("layernorm affine params " + shape_str(vg.shape()) + ", " +
+                             shape_str(vb.shape()) + " do not match " + shape_str(vp.shape()));
+    {  // as tempo_ops::layernorm: checked once per (immutable) gamma storage
+        std::shared_ptr<Tensor::Storage> gs = vg.weak_storage().lock();
+        if (!gs || !gs->gamma_ok.load(std::memory_order_acquire)) {
+            check(tempo_ln_check_gamma(vg.data(), m, g.stream));
+            if (gs) gs->gamma_ok.store(true, std::memory_order_release);
+        }
+    }
+    const bool generate = !mask.defined();
+    if (generate) mask = BoolMask::empty(vp.shape());
+    require_same_shape(vp.shape(), mask.shape(), "mask_scale");
+    const std::int64_t rows = m ? vp.numel() / m : 0;
+    Shape rshape(vp.shape().begin(), vp.shape().end() - 1);
+    Tensor y = Tensor::empty(vp.shape());
+    Tensor rstd = Tensor::empty(rshape);
+    check(tempo_dropout_add_ln_fwd(vp.data(), vr.data(), p,
+                                   generate ? TEMPO_MASK_PHILOX : TEMPO_MASK_SUPPLIED,
+                                   mask.words(), seed, offset, vg.data(), vb.data(), epsilon,
+                                   y.data(), rstd.data(), rows, m, nullptr, g.stream));
+    std::vector<LazyStash> stashes;
+    stashes.push_back(LazyStash::materialized(tag, StashRole::OpOwnStash, y));
+    stashes.push_back(LazyStash::materialized(rstd_tag, StashRole::Statistic, rstd));
+    tempo_stream_t st = g.stream;
+    NodeId id = g.tape.record(
+        "dropout_add_layernorm", tag, {proj, residual, gamma, beta}, y, std::move(stashes),
+        [st, rows, m, mask, p](BackwardCtx& ctx) -> std::vector<Tensor> {
+            const Tensor& gy = ctx.grad_out();
+            const Tensor& yv = ctx.stash(0);
+            const Tensor& rs = ctx.stash(1);
+            const Tensor& gv = ctx.input_value(2);
+            const Tensor& bv = ctx.input_value(3);
+            Tensor d_res = Tensor::empty(yv.shape()), d_proj = Tensor::empty(yv.shape());
+            Tensor dg = Tensor::empty({m}), db = Tensor::empty({m});
+            size_t ws_bytes = tempo_ln_ip_bwd_workspace_size(rows, m);
+            void* ws = ws_bytes ? dev_alloc(ws_bytes, st) : nullptr;
+            int rc = tempo_dropout_add_ln_bwd(gy.data(), yv.data(), rs.data(), gv.data(),
+                                              bv.data(), mask.words(), p, d_res.data(),
+                                              d_proj.data(), dg.data(), db.data(), ws, ws_bytes,
+                                              rows, m, nullptr, st);
+            dev_free(ws, st);
+            check(rc);
+            return {d_proj, d_res, dg, db};
+        });
+    g.tape.charge(id, mask_tag, StashRole::OpOwnStash, mask);
+    return id;
+}
+
 NodeId softmax(Graph& g, NodeId z, std::string tag) {  // ops_tempo.cpp:158-166
     StreamScope scope_(g.stream);
     const Tensor& vz = g.value(z);

@@ -313,6 +313,59 @@ static void test_hidden_dropout() {
     CHECK(throws<ParamError>([&] { ref_ops::dropout(g, x, 1.0, mask, "d2", "m2"); }));
 }
 
+// tempo_ops::dropout_add_layernorm against the reference layer's own
+// composition ref_ops::dropout -> Graph::add -> tempo_ops::layernorm
+// (encoder.cpp:180-191) on the same mask: y, rstd and all four input
+// gradients within 1e-5, d_proj bit-consistent with d_residual, mask-only +
+// y + rstd stash.
+static void test_dropout_add_layernorm() {
+    for (std::int64_t H : {1024, 768, 3072, 96}) {
+        const std::int64_t R = 37, n = R * H;
+        const double p = 0.1;
+        std::vector<float> ph = randn(n, 31), rh = randn(n, 32), gh = randn(n, 33);
+        std::vector<float> gam = randn(H, 34, 0.2), bet = randn(H, 35, 0.1);
+        for (auto& v : gam) v += 1.0f;
+        BoolMask mask = BoolMask::bernoulli_keep({R, H}, p, 36);
+        auto build = [&](bool fused, Graph& g, NodeId& pn, NodeId& rn, NodeId& gn, NodeId& bn) {
+            pn = g.leaf(Tensor::from_host({R, H}, ph), "proj");
+            rn = g.leaf(Tensor::from_host({R, H}, rh), "res");
+            gn = g.leaf(Tensor::from_host({H}, gam), "gamma");
+            bn = g.leaf(Tensor::from_host({H}, bet), "beta");
+            if (fused)
+                return tempo_ops::dropout_add_layernorm(g, pn, rn, p, mask, 0, 0, gn, bn, 1e-5, "ln",
+                                                        "ln_rstd", "drop_mask");
+            NodeId d = ref_ops::dropout(g, pn, p, mask, "drop", "drop_mask");
+            NodeId r = g.add(rn, d, "sum");
+            return tempo_ops::layernorm(g, r, gn, bn, 1e-5, "ln", "ln_rstd");
+        };
+        Graph ga, gb;
+        NodeId pa, ra, gaa, ba, pb, rb, gbb, bb;
+        NodeId ya = build(true, ga, pa, ra, gaa, ba), yb = build(false, gb, pb, rb, gbb, bb);
+        auto tags = ga.ledger.live_by_tag();
+        CHECK(tags.at("ln") == n * 4 && tags.at("ln_rstd") == R * 4);
+        CHECK(tags.at("drop_mask") == (n + 31) / 32 * 4);
+        CHECK(tags.count("drop") == 0 && tags.count("sum") == 0);
+        std::vector<float> y1 = ga.value(ya).to_host(), y2 = gb.value(yb).to_host();
+        double worst = 0;
+        for (std::int64_t i = 0; i < n; ++i) worst = std::max(worst, rel_err(y1[i], y2[i]));
+        GradientMap g1 = ga.tape.backward(ya, Tensor::from_host({R, H}, gh));
+        GradientMap g2 = gb.tape.backward(yb, Tensor::from_host({R, H}, gh));
+        const std::pair<NodeId, NodeId> pairs[4] = {{pa, pb}, {ra, rb}, {gaa, gbb}, {ba, bb}};
+        for (const auto& pr : pairs) {
+            std::vector<float> a = g1.at(pr.first).to_host(), b = g2.at(pr.second).to_host();
+            CHECK(a.size() == b.size());
+            for (std::size_t i = 0; i < a.size(); ++i) worst = std::max(worst, rel_err(a[i], b[i]));
+        }
+        std::vector<float> dres = g1.at(ra).to_host(), dproj = g1.at(pa).to_host();
+        std::vector<std::uint8_t> keep = mask.to_bytes();
+        for (std::int64_t i = 0; i < n; ++i)
+            CHECK(dproj[i] == (keep[i] ? (float)((double)dres[i] * (1.0 / (1.0 - p))) : 0.0f));
+        std::printf("  H=%lld fused vs composed max rel_err %.3g\n", (long long)H, worst);
+        CHECK(worst <= 1e-5);
+        CHECK(ga.ledger.current_bytes() == 0);
+    }
+}
+
 // tempo_ops::sdpa (ops_tempo.cpp:196-210): cuBLAS GEMMs around the Tempo
 // softmax + dropout_recompute, forward and all three input gradients against
 // a host fp64 restatement; the dropped-out map is recomputed, not stashed.
@@ -492,6 +545,7 @@ int main() {
     run("dropout recompute + lazy stash", test_dropout_recompute);
     run("fused softmax+dropout", test_softmax_dropout_fused);
     run("hidden dropout", test_hidden_dropout);
+    run("fused dropout -> add -> layernorm vs the composed layer", test_dropout_add_layernorm);
     run("large mask: device reference stream", test_large_mask_device_stream);
     run("sdpa (cuBLAS GEMMs + Tempo softmax/dropout)", test_sdpa);
     run("graph on a non-blocking stream", test_graph_on_stream);

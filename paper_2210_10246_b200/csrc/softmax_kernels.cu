@@ -707,9 +707,19 @@ bool long_ok(int64_t cols, uint64_t offset, std::initializer_list<const void*> p
 #ifndef TM_SMXL_BWD_VPL
 #define TM_SMXL_BWD_VPL 4
 #endif
-inline int long_cfg(int nch, int vpl) {
-    if (vpl == 8) return nch <= 16 ? 28 : nch <= 32 ? 48 : nch <= 64 ? 88 : 168;
-    return nch <= 8 ? 24 : nch <= 16 ? 44 : nch <= 32 ? 84 : nch <= 64 ? 164 : 168;
+// W from {2, 3, 4, 6, 8, 12, 16}: the common S (1536, 2048, 3072, 4096, 6144,
+// 8192, 12288) fill every chunk slot of every warp.  A/B (2^27 elements):
+// backward S = 1536/3072/6144 at 0.89/0.88/0.89 vs 0.88/0.86/0.80 with
+// W in {2,4,8,16}; forward S = 6144/12288 0.87/0.80 vs 0.80/0.76, but S =
+// 3072 0.83 with W = 3 vs 0.86 with W = 4 (6 of 8 slots): the forward skips
+// W = 3 (its CTAs are smem-limited per SM, so more warps per CTA win).
+inline int long_cfg(int nch, int vpl, bool allow3) {
+    static const int kW[] = {2, 3, 4, 6, 8, 12, 16};
+    for (int w : kW) {
+        if (w == 3 && !allow3) continue;
+        if (w * vpl >= nch) return w * 10 + vpl;
+    }
+    return 168;  // 16 warps x 8 chunks: S <= 16384
 }
 inline int long_stages(int64_t cols, int tensors) {
     const size_t stage = (size_t)tensors * cols * sizeof(float);
@@ -734,15 +744,20 @@ cudaError_t fwd_long(int nch, const float* z, float* P, float* D, uint32_t* mask
                                           long_stages((int64_t)nch * 128, 1));                \
         break;                                                                                \
     }
-    switch (long_cfg(nch, TM_SMXL_FWD_VPL)) {
+    switch (long_cfg(nch, TM_SMXL_FWD_VPL, false)) {
 #if TM_SMXL_FWD_VPL == 8
         TB_FWDL_CASE(2, 8)
         TB_FWDL_CASE(4, 8)
+        TB_FWDL_CASE(6, 8)
         TB_FWDL_CASE(8, 8)
+        TB_FWDL_CASE(12, 8)
 #else
         TB_FWDL_CASE(2, 4)
+        TB_FWDL_CASE(3, 4)
         TB_FWDL_CASE(4, 4)
+        TB_FWDL_CASE(6, 4)
         TB_FWDL_CASE(8, 4)
+        TB_FWDL_CASE(12, 4)
         TB_FWDL_CASE(16, 4)
 #endif
         TB_FWDL_CASE(16, 8)
@@ -764,15 +779,21 @@ cudaError_t bwd_long(int nch, const float* dD, const float* P, const uint32_t* m
                                           long_stages((int64_t)nch * 128, 2));                \
         break;                                                                                \
     }
-    switch (long_cfg(nch, TM_SMXL_BWD_VPL)) {
+    switch (long_cfg(nch, TM_SMXL_BWD_VPL, true)) {
 #if TM_SMXL_BWD_VPL == 8
         TB_BWDL_CASE(2, 8)
+        TB_BWDL_CASE(3, 8)
         TB_BWDL_CASE(4, 8)
+        TB_BWDL_CASE(6, 8)
         TB_BWDL_CASE(8, 8)
+        TB_BWDL_CASE(12, 8)
 #else
         TB_BWDL_CASE(2, 4)
+        TB_BWDL_CASE(3, 4)
         TB_BWDL_CASE(4, 4)
+        TB_BWDL_CASE(6, 4)
         TB_BWDL_CASE(8, 4)
+        TB_BWDL_CASE(12, 4)
         TB_BWDL_CASE(16, 4)
 #endif
         TB_BWDL_CASE(16, 8)

@@ -14,10 +14,12 @@ from test_gpu_parity import (_close_nan, _masked_scores, bits_to_dev, rel_err, t
 
 pytestmark = pytest.mark.gpu
 
-# 1152: W=2 with 9 of 16 chunk slots; 2176: W=4 ragged (17 chunks); 3072: W=4,
-# 6 chunks per warp; 6144/8192: W=8; 16384: W=16 (512-thread CTAs); 2050 and
-# 20000: the generic kernel (not a multiple of 128 / longer than 16384).
-LONG_COLS = [1152, 2048, 2176, 3072, 4096, 6144, 8192, 16384, 2050, 20000]
+# Forward 8 / backward 4 chunks per warp, W from {2,3,4,6,8,12,16}: 1152
+# (9 chunks: W=2 fwd with 9 of 16 slots), 1536 (W=2 fwd / 3 bwd), 2176
+# (17 chunks, ragged), 3072 (W=3 / 6), 6144 (W=6 / 12), 12288 (W=12 / 16x8),
+# 16384 (W=16, 512-thread CTAs); 2050 and 20000: the generic kernel (not a
+# multiple of 128 / longer than 16384).
+LONG_COLS = [1152, 1536, 2048, 2176, 3072, 4096, 6144, 8192, 12288, 16384, 2050, 20000]
 
 
 @pytest.mark.parametrize("cols", LONG_COLS)
