@@ -977,14 +977,47 @@ __global__ void __launch_bounds__(256) ln_bwd_generic_kernel(
 // kRowsB-row tiles (one bulk copy per row slice), gamma/beta and the fp64
 // dgamma/dbeta column partials in registers -- and the two row sums of a tile
 // are the fixed-order sum of the K CTAs' block sums, exchanged through
-// distributed shared memory: each CTA stores its 2*kRowsB sums into its own
-// slot, one cluster barrier, every thread reads the K slots (ld.shared::cluster)
-// in rank order.  Slots alternate by tile parity: a CTA reaches tile t+2's
-// store only after the barrier of tile t+1, i.e. after every peer read tile
-// t's slots.  The partial row of cluster c is ws[c] (its K CTAs write
-// disjoint column slices), reduced by the usual stage 2.
+// distributed shared memory.  The exchange is decoupled, one tile ahead: in
+// iteration i a CTA (A) computes its block sums of tile i+1 and PUSHES them
+// into slot (i+1)%4 of every cluster CTA's inbox (st.shared::cluster, then a
+// release-arrive on that CTA's inbox mbarrier, K arrivals per phase), then
+// (B) waits for its own inbox slot i%4 -- filled by the peers one iteration
+// earlier -- and produces tile i's dx and partials from the stage still in
+// smem.  No cluster-wide barrier per tile: a CTA waits only for the peers'
+// sums of a tile it has not computed on yet.  Slots: a peer pushes tile i+4
+// into slot i%4 only after its B(i+2), which needs this CTA's push of tile
+// i+2, made after this CTA's B(i) -- so 4 slots never overwrite unread sums.
+// Stages: tile i (B), i+1 (A), i+2 in flight: 3-deep ring; stage i%3 is
+// refilled with tile i+3 after the next iteration's first block barrier.
+// The partial row of cluster c is ws[c] (its K CTAs write disjoint column
+// slices), reduced by the usual stage 2.
+constexpr int kStagesC = 3;
+constexpr int kInbox = 4;
+
+__device__ __forceinline__ uint32_t mapa_u32(uint32_t addr, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void st_cluster_f32(uint32_t addr, float v) {
+    asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(addr), "f"(v) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "TB_WAITC_%=:\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra TB_WAITC_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
 template <int NT, bool DROP>
-__global__ void __launch_bounds__(NT) ln_bwd_cluster_kernel(
+__global__ void __launch_bounds__(NT, 1) ln_bwd_cluster_kernel(
     const float* __restrict__ dy, const float* __restrict__ y, const float* __restrict__ rstd,
     const float* __restrict__ gamma, const float* __restrict__ beta, float* __restrict__ dx,
     double* __restrict__ ws, int64_t rows, int cols, int sw, const uint32_t* __restrict__ mask,
@@ -994,11 +1027,11 @@ __global__ void __launch_bounds__(NT) ln_bwd_cluster_kernel(
     grid_dep_wait();  // PDL: predecessor complete and visible
     grid_dep_launch_persistent();
     extern __shared__ __align__(128) unsigned char dsm[];
-    uint64_t* full = reinterpret_cast<uint64_t*>(dsm);
+    uint64_t* full = reinterpret_cast<uint64_t*>(dsm);           // [kStagesC]
+    uint64_t* inbar = full + kStagesC;                            // [kInbox]
     float* ring = reinterpret_cast<float*>(dsm + 128);
     __shared__ float red[2 * 2 * kRowsB * 32];
-    __shared__ float xch[2][2 * kRowsB];  // [tile parity][s1, s2 per row]
-    __shared__ float xall[8 * 2 * kRowsB];  // the K CTAs' sums of the current tile
+    __shared__ __align__(16) float inbox[kInbox][8][2 * kRowsB];  // [slot][rank][s1, s2 per row]
     int phase = 0;
     const int K = (int)cluster.num_blocks(), q = (int)cluster.block_rank();
     const int64_t cid = blockIdx.x / K, ncl = gridDim.x / K;
@@ -1006,27 +1039,26 @@ __global__ void __launch_bounds__(NT) ln_bwd_cluster_kernel(
     const int width = max(0, min(sw, cols - c0));  // columns of the slice (% 4 == 0)
     const int tile_floats = kRowsB * sw;          // per tensor; a stage holds dy then y
     const int64_t ntiles = (rows + kRowsB - 1) / kRowsB;
+    const int n = cid < ntiles ? (int)((ntiles - 1 - cid) / ncl + 1) : 0;  // this cluster's tiles
     if (threadIdx.x == 0) {
-        for (int s = 0; s < kStagesB; ++s) mbar_init(&full[s], 1);
+        for (int s = 0; s < kStagesC; ++s) mbar_init(&full[s], 1);
+        for (int s = 0; s < kInbox; ++s) mbar_init(&inbar[s], (uint32_t)K);
         mbar_fence_init();
     }
     __syncthreads();
-    auto issue = [&](int64_t t, int s) {
-        const int64_t r0 = t * kRowsB;
+    auto issue = [&](int i, int s) {  // local tile i into stage s
+        const int64_t r0 = (cid + (int64_t)i * ncl) * kRowsB;
         const int nr = (int)min((int64_t)kRowsB, rows - r0);
         const uint32_t bytes = (uint32_t)width * 4u;
         mbar_expect_tx(&full[s], 2 * nr * bytes);
-        for (int i = 0; i < nr; ++i) {
-            bulk_g2s(ring + (2 * s) * tile_floats + i * sw, dy + (r0 + i) * cols + c0, bytes, &full[s]);
-            bulk_g2s(ring + (2 * s + 1) * tile_floats + i * sw, y + (r0 + i) * cols + c0, bytes,
+        for (int j = 0; j < nr; ++j) {
+            bulk_g2s(ring + (2 * s) * tile_floats + j * sw, dy + (r0 + j) * cols + c0, bytes, &full[s]);
+            bulk_g2s(ring + (2 * s + 1) * tile_floats + j * sw, y + (r0 + j) * cols + c0, bytes,
                      &full[s]);
         }
     };
     if (threadIdx.x == 0 && width > 0) {
-        for (int s = 0; s < kStagesB; ++s) {
-            const int64_t t = cid + (int64_t)s * ncl;
-            if (t < ntiles) issue(t, s);
-        }
+        for (int i = 0; i < kStagesC && i < n; ++i) issue(i, i);
     }
     const int cg4 = threadIdx.x;  // float4 column group within the slice
     const bool act = 4 * cg4 < width;
@@ -1050,93 +1082,113 @@ __global__ void __launch_bounds__(NT) ln_bwd_cluster_kernel(
         }
     }
     const float inv_m = 1.0f / (float)cols;
-    cluster.sync();  // every CTA of the cluster is running before any DSMEM access
-    int it = 0;
-    for (int64_t tile = cid; tile < ntiles; tile += ncl, ++it) {
-        const int64_t r0 = tile * kRowsB;
+    cluster.sync();  // every CTA's inbox barriers are initialised before the first push
+    // A(i): block sums of local tile i from its stage, pushed to every CTA's inbox
+    auto phase_a = [&](int i) {
+        const int st = i % kStagesC;
+        const int64_t r0 = (cid + (int64_t)i * ncl) * kRowsB;
+        if (width > 0) mbar_wait(&full[st], (uint32_t)((i / kStagesC) & 1));
+        const float* gs = ring + (2 * st) * tile_floats;
+        const float* ys = ring + (2 * st + 1) * tile_floats;
+        float s[2 * kRowsB];
+#pragma unroll
+        for (int j = 0; j < kRowsB; ++j) {
+            float s1 = 0.0f, s2 = 0.0f;
+            if (r0 + j < rows && act) {
+                const float4 gv = reinterpret_cast<const float4*>(gs + j * sw)[cg4];
+                const float4 yv = reinterpret_cast<const float4*>(ys + j * sw)[cg4];
+                const float ga[4] = {gv.x, gv.y, gv.z, gv.w}, ya[4] = {yv.x, yv.y, yv.z, yv.w};
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const float gg = ga[k] * gm[k];
+                    const float xh = (ya[k] - bt[k]) * igf[k];
+                    s1 += gg;
+                    s2 = fmaf(gg, xh, s2);
+                }
+            }
+            s[2 * j] = s1;
+            s[2 * j + 1] = s2;
+        }
+        block_sum<2 * kRowsB>(s, red, phase);  // (its barrier also ends the previous B)
+        // lane p of warp 1 pushes to cluster CTA p (in parallel: one remote
+        // round trip, not K; the release-arrive waits for its own stores only)
+        if ((threadIdx.x >> 5) == 1 && (threadIdx.x & 31) < K) {
+            const uint32_t p = threadIdx.x & 31;
+            const int slot = i % kInbox;
+            const uint32_t ra = mapa_u32(smem_u32(&inbox[slot][q][0]), p);
+#pragma unroll
+            for (int j = 0; j < 2 * kRowsB; ++j) st_cluster_f32(ra + 4 * j, s[j]);
+            mbar_arrive_remote(mapa_u32(smem_u32(&inbar[slot]), p));
+        }
+        if (threadIdx.x == 0 && i >= 1 && i + 2 < n && width > 0) {
+            fence_proxy_async_smem();  // stage of tile i-1 is free: tile i+2
+            issue(i + 2, (i - 1) % kStagesC);
+        }
+    };
+    float rs_nx[kRowsB];
+    uint32_t mw_nx[kRowsB];
+    auto prefetch = [&](int i) {
+        const int64_t r0 = (cid + (int64_t)i * ncl) * kRowsB;
+#pragma unroll
+        for (int j = 0; j < kRowsB; ++j) {
+            const bool in = i < n && r0 + j < rows;
+            rs_nx[j] = in ? __ldg(rstd + r0 + j) : 0.f;
+            mw_nx[j] = (DROP && in && act) ? __ldg(mask + (((r0 + j) * cols + col) >> 5)) : 0u;
+        }
+    };
+    if (n > 0) {
+        phase_a(0);
+        prefetch(0);
+    }
+    for (int i = 0; i < n; ++i) {
         float rsv[kRowsB];
         uint32_t mwv[kRowsB];
 #pragma unroll
-        for (int i = 0; i < kRowsB; ++i) {
-            const bool in = r0 + i < rows;
-            rsv[i] = in ? __ldg(rstd + r0 + i) : 0.f;
-            mwv[i] = (DROP && in && act) ? __ldg(mask + (((r0 + i) * cols + col) >> 5)) : 0u;
+        for (int j = 0; j < kRowsB; ++j) {
+            rsv[j] = rs_nx[j];
+            mwv[j] = mw_nx[j];
         }
-        const int st = it % kStagesB;
-        float4 gv[kRowsB], yv[kRowsB];
-        if (width > 0) mbar_wait(&full[st], (uint32_t)((it / kStagesB) & 1));
+        if (i + 1 < n) {
+            prefetch(i + 1);
+            phase_a(i + 1);
+        }
+        // B(i): the K CTAs' sums of tile i, then dx / d(proj) / partials
+        const int slot = i % kInbox;
+        // one acquiring waiter per warp (a cluster-scope acquire invalidates
+        // L1: once per warp, not per thread); __syncwarp orders its lanes after it
+        if ((threadIdx.x & 31) == 0) mbar_wait_cluster(&inbar[slot], (uint32_t)((i / kInbox) & 1));
+        __syncwarp();
+        float s[2 * kRowsB];
+#pragma unroll
+        for (int j = 0; j < 2 * kRowsB; ++j) s[j] = inbox[slot][0][j];
+        for (int p = 1; p < K; ++p) {  // fixed rank order: identical sums in every CTA
+#pragma unroll
+            for (int j = 0; j < 2 * kRowsB; ++j) s[j] += inbox[slot][p][j];
+        }
+        const int st = i % kStagesC;
+        const int64_t r0 = (cid + (int64_t)i * ncl) * kRowsB;
         const float* gs = ring + (2 * st) * tile_floats;
         const float* ys = ring + (2 * st + 1) * tile_floats;
 #pragma unroll
-        for (int i = 0; i < kRowsB; ++i) {
-            gv[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-            yv[i] = gv[i];
-            if (r0 + i < rows && act) {
-                gv[i] = reinterpret_cast<const float4*>(gs + i * sw)[cg4];
-                yv[i] = reinterpret_cast<const float4*>(ys + i * sw)[cg4];
-            }
-        }
-        float s[2 * kRowsB];
-#pragma unroll
-        for (int i = 0; i < kRowsB; ++i) {
-            const float ga[4] = {gv[i].x, gv[i].y, gv[i].z, gv[i].w};
-            const float ya[4] = {yv[i].x, yv[i].y, yv[i].z, yv[i].w};
-            float s1 = 0.0f, s2 = 0.0f;
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const float gg = ga[k] * gm[k];
-                const float xh = (ya[k] - bt[k]) * igf[k];
-                s1 += gg;
-                s2 = fmaf(gg, xh, s2);
-            }
-            s[2 * i] = s1;
-            s[2 * i + 1] = s2;
-        }
-        block_sum<2 * kRowsB>(s, red, phase);
-        if (threadIdx.x == 0 && width > 0) {  // stage consumed by every thread: refill
-            const int64_t nt = tile + (int64_t)kStagesB * ncl;
-            if (nt < ntiles) {
-                fence_proxy_async_smem();
-                issue(nt, st);
-            }
-        }
-        const int par = it & 1;
-        if (threadIdx.x == 0) {
-#pragma unroll
-            for (int j = 0; j < 2 * kRowsB; ++j) xch[par][j] = s[j];
-        }
-        cluster.sync();
-        // K*2*kRowsB threads fetch the peers' sums (one remote load each), then
-        // every thread adds them from local smem in rank order
-        if (threadIdx.x < K * 2 * kRowsB)
-            xall[threadIdx.x] =
-                *cluster.map_shared_rank(&xch[par][threadIdx.x % (2 * kRowsB)], threadIdx.x / (2 * kRowsB));
-        __syncthreads();
-#pragma unroll
-        for (int j = 0; j < 2 * kRowsB; ++j) s[j] = xall[j];
-        for (int p = 1; p < K; ++p) {  // fixed rank order: identical sums in every CTA
-#pragma unroll
-            for (int j = 0; j < 2 * kRowsB; ++j) s[j] += xall[p * 2 * kRowsB + j];
-        }
-#pragma unroll
-        for (int i = 0; i < kRowsB; ++i) {
-            if (r0 + i >= rows || !act) continue;
-            const float c1 = s[2 * i] * inv_m, c2 = s[2 * i + 1] * inv_m;
-            const float ga[4] = {gv[i].x, gv[i].y, gv[i].z, gv[i].w};
-            const float ya[4] = {yv[i].x, yv[i].y, yv[i].z, yv[i].w};
+        for (int j = 0; j < kRowsB; ++j) {
+            if (r0 + j >= rows || !act) continue;
+            const float c1 = s[2 * j] * inv_m, c2 = s[2 * j + 1] * inv_m;
+            const float4 gv = reinterpret_cast<const float4*>(gs + j * sw)[cg4];
+            const float4 yv = reinterpret_cast<const float4*>(ys + j * sw)[cg4];
+            const float ga[4] = {gv.x, gv.y, gv.z, gv.w}, ya[4] = {yv.x, yv.y, yv.z, yv.w};
             float o[4];
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
                 const float xh = (ya[k] - bt[k]) * igf[k];
-                o[k] = (fmaf(ga[k], gm[k], -c1) - xh * c2) * rsv[i];
+                o[k] = (fmaf(ga[k], gm[k], -c1) - xh * c2) * rsv[j];
                 const double gd = (double)ga[k];
                 pg[k] = fma(gd, (double)ya[k], pg[k]);
                 pb[k] += gd;
             }
-            const int64_t e = (r0 + i) * cols + col;
+            const int64_t e = (r0 + j) * cols + col;
             st_stream(reinterpret_cast<float4*>(dx + e), make_float4(o[0], o[1], o[2], o[3]));
             if (DROP) {
-                const uint32_t nb = (mwv[i] >> (e & 31)) & 0xfu;
+                const uint32_t nb = (mwv[j] >> (e & 31)) & 0xfu;
                 float4 dp;
                 dp.x = (nb & 1u) ? (float)((double)o[0] * scale) : 0.0f;
                 dp.y = (nb & 2u) ? (float)((double)o[1] * scale) : 0.0f;
@@ -1154,7 +1206,9 @@ __global__ void __launch_bounds__(NT) ln_bwd_cluster_kernel(
             wg[cols + col + k] = pb[k];
         }
     }
-    cluster.sync();  // no CTA leaves while a peer may still read its slots
+    // every push into this CTA's inbox was consumed above (B(n-1) waited for
+    // the last), and this CTA's own pushes completed before its arrives: no
+    // DSMEM access can target an exited CTA
 }
 
 #ifndef TM_LN_CLUSTER_NT
@@ -1169,7 +1223,7 @@ inline int cluster_sw(int64_t cols) {
     return (int)(((cols + k - 1) / k + 3) / 4 * 4);
 }
 size_t bwd_cluster_smem(int64_t cols) {
-    return 128 + (size_t)kStagesB * 2 * kRowsB * cluster_sw(cols) * sizeof(float);
+    return 128 + (size_t)kStagesC * 2 * kRowsB * cluster_sw(cols) * sizeof(float);
 }
 
 // Stage 2: out[j] = sum over CTAs c (fixed order) of ws[c][j], j < 2*cols.
