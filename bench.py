@@ -223,6 +223,9 @@ class Chain:
         self.status = torch.zeros(1, dtype=torch.int32, device=dev)
         self.step_idx = 0
         self.mask_mode = "philox"  # or "reference" (bench.py --masks reference)
+        # --masks reference: the attention mask generated inside the softmax
+        # kernel (False: a separate generation pass, TEMPO_REFMASK_FUSED=0)
+        self.refmask_fused = os.environ.get("TEMPO_REFMASK_FUSED", "1") != "0"
         # global element offsets: rank shards reproduce the unsharded masks
         self.off_att = rank * ATT_ROWS * S
         self.off_h = rank * T * H
@@ -258,37 +261,63 @@ class Chain:
         for site, (m, n, off) in enumerate([(self.m_att, ATT_ROWS * S, self.off_att),
                                             (self.m1, T * H, self.off_h),
                                             (self.m2, T * H, self.off_h)]):
+            if site == 0 and self.refmask_fused:
+                continue  # generated inside the softmax forward (forward())
             s_ = self._mask_streams[site]
             s_.wait_stream(main)  # the previous step is done with this mask
             with torch.cuda.stream(s_):
                 o.bernoulli_keep_bits_device(n, P_DROP, o.mask_stream_seed(1234, step, site),
                                              offset=off, out=m)
-        for s_ in self._mask_streams:
-            main.wait_stream(s_)
+        if not self.refmask_fused:
+            for s_ in self._mask_streams:
+                main.wait_stream(s_)
+        # else: the hidden masks' generation overlaps the attention mask's
+        # jump and the fused softmax forward; each consumer waits for its own
+        # mask (_mask_ready)
+
+    def _mask_ready(self, site):
+        if self.mask_mode == "reference" and self.refmask_fused:
+            self.torch.cuda.current_stream().wait_stream(self._mask_streams[site])
 
     def forward(self, seed):
         o = self.ops
         gen = self.mask_mode != "reference"
         if not gen:
             self.reference_masks(seed)
-        o.softmax_dropout_fwd(self.z, P_DROP, mask=self.m_att, generate=gen, seed=seed,
-                              offset=self.off_att, P=self.P, D=self.D)
+        if not gen and self.refmask_fused:
+            # the attention mask = the reference's stream, generated inside the
+            # softmax kernel (tempo_softmax_dropout_fwd_refmask)
+            if getattr(self, "_ws_att", None) is None:
+                nb = int(o.lib().tempo_bernoulli_keep_bits_workspace_size(self.off_att,
+                                                                          self.ATT_ROWS * S))
+                self._ws_att = self.torch.empty(max(nb, 1), dtype=self.torch.uint8,
+                                                device=self.z.device)
+            o.softmax_dropout_fwd_refmask(self.z, P_DROP, o.mask_stream_seed(1234, seed, 0),
+                                          offset=self.off_att, mask=self.m_att, P=self.P,
+                                          D=self.D, workspace=self._ws_att)
+        else:
+            o.softmax_dropout_fwd(self.z, P_DROP, mask=self.m_att, generate=gen, seed=seed,
+                                  offset=self.off_att, P=self.P, D=self.D)
         if self.fused:  # encoder.cpp:180-191, 198-210 as two fused passes
+            self._mask_ready(1)
             o.dropout_add_layernorm_fwd(self.x_attn_out, self.x_res, self.g1, self.b1, P_DROP,
                                         mask=self.m1, generate=gen, seed=seed + 1,
                                         offset=self.off_h, check_gamma=False, y=self.y_ln1,
                                         rstd=self.rs1, dev_status=self.status)
             o.gelu_ip_fwd(self.x_ffn1, self.table, y=self.y_g, mask=self.m_g)
+            self._mask_ready(2)
             o.dropout_add_layernorm_fwd(self.x_ffn2, self.y_ln1, self.g2, self.b2, P_DROP,
                                         mask=self.m2, generate=gen, seed=seed + 2,
                                         offset=self.off_h, check_gamma=False, y=self.y_ln2,
                                         rstd=self.rs2, dev_status=self.status)
             return
+        self._mask_ready(1)
         o.dropout_fwd(self.x_attn_out, P_DROP, mask=self.m1, generate=gen, seed=seed + 1,
                       offset=self.off_h, y=self.d1)
         o.layernorm_ip_fwd(self.d1, self.g1, self.b1, check_gamma=False, y=self.y_ln1,
                            rstd=self.rs1, dev_status=self.status)
         o.gelu_ip_fwd(self.x_ffn1, self.table, y=self.y_g, mask=self.m_g)
+        self._mask_ready(2)
         o.dropout_fwd(self.x_ffn2, P_DROP, mask=self.m2, generate=gen, seed=seed + 2,
                       offset=self.off_h, y=self.d2)
         o.layernorm_ip_fwd(self.d2, self.g2, self.b2, check_gamma=False, y=self.y_ln2,

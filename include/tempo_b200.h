@@ -319,6 +319,20 @@ size_t tempo_bernoulli_keep_bits_workspace_size(uint64_t offset, int64_t n);
 int tempo_bernoulli_keep_bits(int64_t n, double p, uint64_t seed, uint64_t offset,
                               uint32_t* bits, void* workspace, size_t workspace_bytes,
                               tempo_stream_t stream);
+/* softmax -> dropout_recompute forward (as tempo_softmax_dropout_fwd) whose
+ * mask is the reference's OWN stream: elements [offset, offset + rows*cols)
+ * of BoolMask::bernoulli_keep(shape, p, seed), generated on the device INSIDE
+ * the softmax kernel (warp-specialised: generator warps run the jumped chunk
+ * recurrence, consumer warps the softmax rows) and written to `mask` (the
+ * stash), bit-identical to tempo_bernoulli_keep_bits followed by the
+ * supplied-mask forward -- which is what runs when the shape does not fit
+ * the fused kernel (cols not in {128, 256, 512, 1024}, offset % 2^19 != 0 or
+ * rows*cols % 8192 != 0).  Workspace: tempo_bernoulli_keep_bits_workspace_size(
+ * offset, rows*cols).  offset % 32 != 0 -> TEMPO_ERR_PARAM. */
+int tempo_softmax_dropout_fwd_refmask(const float* z, double p, uint64_t seed, uint64_t offset,
+                                      uint32_t* mask, float* P, float* D, int64_t rows,
+                                      int64_t cols, void* workspace, size_t workspace_bytes,
+                                      tempo_stream_t stream);
 /* Host reference of the jump construction (test helper): `count` outputs of
  * std::mt19937_64(seed) after discard(steps), via x^steps mod P.  0 = ok. */
 int tempo_mt_outputs_after_host(uint64_t seed, uint64_t steps, int64_t count, uint64_t* out);

@@ -88,6 +88,8 @@ SIGNATURES = {
     "tempo_bernoulli_keep_bits_host": (C.c_int, [_i64, _dbl, _u64, _vp]),
     "tempo_bernoulli_keep_bits_workspace_size": (_sz, [_u64, _i64]),
     "tempo_bernoulli_keep_bits": (C.c_int, [_i64, _dbl, _u64, _u64, _vp, _vp, _sz, _vp]),
+    "tempo_softmax_dropout_fwd_refmask": (C.c_int, [_vp, _dbl, _u64, _u64, _vp, _vp, _vp, _i64,
+                                                    _i64, _vp, _sz, _vp]),
     "tempo_mt_outputs_after_host": (C.c_int, [_u64, _u64, _i64, _vp]),
     "tempo_mask_stream_seed": (_u64, [_u64, _u64, C.c_int]),
     "tempo_layer_stash_bytes_per_token": (_i64, [_i64, _i64, _i64, C.c_int, C.c_int]),

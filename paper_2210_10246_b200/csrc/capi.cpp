@@ -969,6 +969,26 @@ int tempo_bernoulli_keep_bits(int64_t n, double p, uint64_t seed, uint64_t offse
                        "tempo_bernoulli_keep_bits");
 }
 
+int tempo_softmax_dropout_fwd_refmask(const float* z, double p, uint64_t seed, uint64_t offset,
+                                      uint32_t* mask, float* P, float* D, int64_t rows,
+                                      int64_t cols, void* workspace, size_t workspace_bytes,
+                                      tempo_stream_t stream) {
+    if (int rc = check_rows(rows, cols, "softmax")) return rc;
+    if (int rc = check_p(p)) return rc;
+    if (offset % 32 != 0)
+        return fail(TEMPO_ERR_PARAM, "offset must be a multiple of 32 (whole mask words)");
+    if (rows == 0 || cols == 0) return TEMPO_OK;
+    if (!z || !P || !mask) return fail(TEMPO_ERR_PARAM, "softmax: null pointer");
+    const size_t need = tb::mt_keep_workspace(offset, rows * cols);
+    if (workspace_bytes < need || (need && !workspace))
+        return fail(TEMPO_ERR_PARAM, "workspace too small: need " + std::to_string(need) +
+                                         " bytes");
+    return cuda_status(tb::launch_softmax_dropout_fwd_mt(z, p, seed, offset, mask, P, D, rows,
+                                                         cols, workspace, workspace_bytes,
+                                                         S(stream)),
+                       "tempo_softmax_dropout_fwd_refmask");
+}
+
 uint64_t tempo_mask_stream_seed(uint64_t mask_seed, uint64_t salt, int site) {
     // encoder.cpp:39-46 (splitmix64 over a site-salted input)
     uint64_t z = mask_seed + 0x9E3779B97F4A7C15ull * (salt * 3 + (uint64_t)site + 1);

@@ -256,11 +256,10 @@ size_t mt_keep_workspace(uint64_t e_begin, int64_t n) {
     return mt_ws_layout(e_begin, n).total;
 }
 
-cudaError_t launch_mt_keep_bits(uint64_t seed, double p, uint64_t e_begin, int64_t n,
-                                uint32_t* mask, void* ws, size_t ws_bytes, cudaStream_t st) {
-    if (n <= 0) return cudaSuccess;
+cudaError_t launch_mt_chunk_states(uint64_t seed, uint64_t e_begin, int64_t n, void* ws,
+                                   size_t ws_bytes, const uint64_t** states, cudaStream_t st) {
     const MtWs L = mt_ws_layout(e_begin, n);
-    if (ws_bytes < L.total || (e_begin & 31u)) return cudaErrorInvalidValue;
+    if (n <= 0 || ws_bytes < L.total || (e_begin & 31u)) return cudaErrorInvalidValue;
     const uint16_t* jidx = nullptr;
     const int32_t* joff = nullptr;
     cudaError_t err = device_index(&jidx, &joff);
@@ -306,6 +305,18 @@ cudaError_t launch_mt_keep_bits(uint64_t seed, double p, uint64_t e_begin, int64
         lo = clo;
         hi = chi;
     }
+    *states = cur;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_mt_keep_bits(uint64_t seed, double p, uint64_t e_begin, int64_t n,
+                                uint32_t* mask, void* ws, size_t ws_bytes, cudaStream_t st) {
+    if (n <= 0) return cudaSuccess;
+    const uint64_t* cur = nullptr;
+    cudaError_t err = launch_mt_chunk_states(seed, e_begin, n, ws, ws_bytes, &cur, st);
+    if (err != cudaSuccess) return err;
+    const int64_t k0 = (int64_t)(e_begin / kMtChunk);
+    const int64_t k1 = (int64_t)((e_begin + (uint64_t)n - 1) / kMtChunk);
     const uint64_t xmin = mt_keep_threshold(p);
     launch(mt_keep_kernel, (unsigned)(k1 - k0 + 1), kGenThreads, 0, st)(cur, k0, e_begin,
                                                                    e_begin + (uint64_t)n, xmin,

@@ -26,6 +26,7 @@
 #include <initializer_list>
 
 #include "common.cuh"
+#include "mt19937.h"
 #include "tempo_internal.h"
 
 namespace tb {
@@ -534,6 +535,156 @@ __global__ void __launch_bounds__(W * 32) softmax_bwd_long_kernel(
     }
 }
 
+// ------------------------------------- the reference's mask stream, fused
+// softmax -> dropout_recompute forward whose mask is the reference's own
+// BoolMask::bernoulli_keep stream (std::mt19937_64, tensor.cpp:186-203)
+// GENERATED INSIDE the kernel instead of by a separate pass (§3a computes
+// the same bits in mt_keep_kernel).  One CTA per 2^19-output chunk of the
+// stream, warp-specialised:
+//   * 4 generator warps run the chunk's recurrence from its jumped start
+//     state (128 outputs per step, 312-word ring in smem, a named barrier
+//     of the 128 generator threads per step), temper, compare with the
+//     integer threshold and ballot one mask word per warp and step into a
+//     kMtSlots-deep smem ring of slots of 4 rows (4C outputs, C/32 steps);
+//   * 4 consumer warps, one row of the slot each, run softmax_fwd_vec_kernel's
+//     per-row math (the row's loads issued before the slot wait), read their
+//     mask nibbles from the ring, store P, D and the row's mask words (the
+//     stash) to HBM;
+//   * full[s] (4 generator arrivals) / empty[s] (4 consumer arrivals)
+//     mbarriers hand the slots over.
+// The chunk's generation is sequential (2^19 / 128 steps), so the kernel is
+// only as fast as the chunks that run CONCURRENTLY: 256-thread CTAs within
+// 64 registers give 4 CTAs per SM, i.e. all 512 chunks of a 2^28-element
+// mask resident at once (2 per SM -- the first version's 384-thread CTAs at
+// 80 registers -- ran two waves: 1.07 ms vs 0.58 + 0.47 for the passes).
+// Needs C in {128, 256, 512, 1024}, e_begin % 2^19 == 0 and rows*C % 4C
+// == 0 (the launcher falls back to the separate passes otherwise).  Bits, P
+// and D are exactly those of mt_keep_kernel + the supplied-mask forward.
+constexpr int kMtGenWarps = 4, kMtConsWarps = 4;
+constexpr int kMtThreads = 32 * (kMtGenWarps + kMtConsWarps);
+constexpr int kMtSlots = 8;
+#ifndef TM_MTGEN_MINB
+#define TM_MTGEN_MINB 4
+#endif
+
+template <int VPL>
+__global__ void __launch_bounds__(kMtThreads, TM_MTGEN_MINB) softmax_fwd_mtgen_kernel(
+    const float* __restrict__ z, float* __restrict__ P, float* __restrict__ D,
+    uint32_t* __restrict__ mask, const uint64_t* __restrict__ states, double scale,
+    uint64_t xmin, int64_t rows) {
+    grid_dep_wait();  // PDL: predecessor (the chunk-state jump) complete and visible
+    grid_dep_launch();
+    constexpr int C = VPL * 128;
+    constexpr int kSlotSteps = kMtConsWarps * C / 128;  // steps per slot (one row per consumer)
+    constexpr int kSlotWords = kSlotSteps * 4;
+    constexpr int kRowsPerChunk = (int)(kMtChunk / C);
+    __shared__ uint64_t ring[512];
+    __shared__ uint32_t mring[kMtSlots * kSlotWords];
+    __shared__ __align__(8) uint64_t full[kMtSlots], empty[kMtSlots];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t r_begin = (int64_t)blockIdx.x * kRowsPerChunk;
+    const int64_t r_end = min(rows, r_begin + kRowsPerChunk);
+    const int nslots = (int)((r_end - r_begin) / kMtConsWarps);
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kMtSlots; ++s) {
+            mbar_init(&full[s], kMtGenWarps);
+            mbar_init(&empty[s], kMtConsWarps);
+        }
+        mbar_fence_init();
+    }
+    if (warp < kMtGenWarps) {
+        const uint64_t* st = states + (size_t)blockIdx.x * kMtN;
+        for (int i = threadIdx.x; i < (int)kMtN; i += 32 * kMtGenWarps) ring[i] = st[i];
+    }
+    __syncthreads();
+    if (warp < kMtGenWarps) {
+        // ---- generator: as mt_keep_kernel, one ballot word per warp and step
+        const int tid = threadIdx.x;
+        int a312[4], a311[4], a156[4], aw[4];
+#pragma unroll
+        for (int ph = 0; ph < 4; ++ph) {
+            const int j = ph * 128 + kMtN + tid;  // sequence index mod 512
+            a312[ph] = (j - 312) & 511;
+            a311[ph] = (j - 311) & 511;
+            a156[ph] = (j - 156) & 511;
+            aw[ph] = j & 511;
+        }
+        for (int sl = 0; sl < nslots; ++sl) {
+            const int s = sl % kMtSlots;
+            if (sl >= kMtSlots) {  // the consumers are done with this slot's previous use
+                if (lane == 0) mbar_wait(&empty[s], (uint32_t)(((sl / kMtSlots) - 1) & 1));
+                __syncwarp();
+            }
+            uint32_t* words = mring + s * kSlotWords;
+#pragma unroll 1
+            for (int t4 = 0; t4 < kSlotSteps; t4 += 4) {  // kSlotSteps % 4 == 0
+#pragma unroll
+                for (int ph = 0; ph < 4; ++ph) {
+                    const uint64_t w = mt_next_word(ring[a312[ph]], ring[a311[ph]], ring[a156[ph]]);
+                    ring[aw[ph]] = w;
+                    group_bar(1, 32 * kMtGenWarps);  // w visible to the next step
+                    const uint32_t word = __ballot_sync(kFull, mt_temper(w) >= xmin);
+                    if (lane == 0) words[(t4 + ph) * 4 + warp] = word;
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&full[s]);
+        }
+        return;
+    }
+    // ---- consumers: warp cw takes row cw of every slot
+    const int cw = warp - kMtGenWarps;
+    for (int sl = 0; sl < nslots; ++sl) {
+        const int s = sl % kMtSlots;
+        const int64_t r = r_begin + (int64_t)sl * kMtConsWarps + cw;
+        float4 v[VPL];
+        const float4* zr = reinterpret_cast<const float4*>(z + r * C);
+#pragma unroll
+        for (int k = 0; k < VPL; ++k) v[k] = ld_stream(zr + k * 32 + lane);
+        if (lane == 0) mbar_wait(&full[s], (uint32_t)((sl / kMtSlots) & 1));
+        __syncwarp();
+        const uint32_t* words = mring + s * kSlotWords + cw * (C / 32);  // this row's words
+        float mx = v[0].x;
+#pragma unroll
+        for (int k = 0; k < VPL; ++k)
+            mx = fmax_nan(mx, fmax_nan(fmax_nan(v[k].x, v[k].y), fmax_nan(v[k].z, v[k].w)));
+        mx = warp_max_nan(mx);
+        float acc = 0.0f;
+#pragma unroll
+        for (int k = 0; k < VPL; ++k) {
+#if TM_SOFTMAX_PACKED
+            const float2 lo = exp_shift2(make_float2(v[k].x, v[k].y), mx);
+            const float2 hi = exp_shift2(make_float2(v[k].z, v[k].w), mx);
+            v[k] = make_float4(lo.x, lo.y, hi.x, hi.y);
+#else
+            v[k] = make_float4(exp_shift(v[k].x, mx), exp_shift(v[k].y, mx),
+                               exp_shift(v[k].z, mx), exp_shift(v[k].w, mx));
+#endif
+            acc += (v[k].x + v[k].y) + (v[k].z + v[k].w);
+        }
+        const float inv = row_inv(warp_sumf(acc), mx);
+        float4* Pr = reinterpret_cast<float4*>(P + r * C);
+        float4* Dr = reinterpret_cast<float4*>(D + r * C);
+#pragma unroll
+        for (int k = 0; k < VPL; ++k) {
+            const float4 p = make_float4(v[k].x * inv, v[k].y * inv, v[k].z * inv, v[k].w * inv);
+            st_stream(Pr + k * 32 + lane, p);
+            if (D) {  // the chunk_nibble layout: word k*4 + lane/8, nibble lane%8
+                const uint32_t bits = (words[k * 4 + (lane >> 3)] >> (4 * (lane & 7))) & 0xfu;
+                float4 d;
+                d.x = (bits & 1u) ? dscale(p.x, scale) : 0.0f;
+                d.y = (bits & 2u) ? dscale(p.y, scale) : 0.0f;
+                d.z = (bits & 4u) ? dscale(p.z, scale) : 0.0f;
+                d.w = (bits & 8u) ? dscale(p.w, scale) : 0.0f;
+                st_stream(Dr + k * 32 + lane, d);
+            }
+        }
+        if (lane < C / 32) st_stream(mask + ((r * C) >> 5) + lane, words[lane]);  // the stash
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+    }
+}
+
 // ---------------------------------------------------------------- generic
 __device__ __forceinline__ bool mask_bit(const uint32_t* mask, int64_t i) {
     return (__ldg(mask + (i >> 5)) >> (i & 31)) & 1u;
@@ -856,6 +1007,42 @@ cudaError_t launch_softmax_dropout_fwd(const float* z, double scale, uint64_t th
     launch(softmax_fwd_generic_kernel, generic_grid((const void*)softmax_fwd_generic_kernel, rows),
                                  kBlock, 0, st)(z, P, D, mask, philox ? kPhilox : kSupplied,
                                                   scale, thresh, seed, offset, rows, cols);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_softmax_dropout_fwd_mt(const float* z, double p, uint64_t seed,
+                                          uint64_t e_begin, uint32_t* mask, float* P, float* D,
+                                          int64_t rows, int64_t cols, void* ws, size_t ws_bytes,
+                                          cudaStream_t st) {
+    if (rows == 0 || cols == 0) return cudaSuccess;
+    const int64_t n = rows * cols;
+    const double scale = 1.0 / (1.0 - p);
+    const bool fused = (cols == 128 || cols == 256 || cols == 512 || cols == 1024) &&
+                       e_begin % (uint64_t)kMtChunk == 0 && rows % kMtConsWarps == 0 &&
+                       vec_ok(cols, 0, {z, P, D, mask});
+    if (!fused) {  // the separate passes: generation, then the supplied-mask forward
+        cudaError_t e = launch_mt_keep_bits(seed, p, e_begin, n, mask, ws, ws_bytes, st);
+        if (e != cudaSuccess) return e;
+        return launch_softmax_dropout_fwd(z, scale, 0, 0, mask, 0, 0, P, D, rows, cols, st);
+    }
+    const uint64_t* states = nullptr;
+    cudaError_t e = launch_mt_chunk_states(seed, e_begin, n, ws, ws_bytes, &states, st);
+    if (e != cudaSuccess) return e;
+    const unsigned nchunks = (unsigned)((n + kMtChunk - 1) / kMtChunk);
+    const uint64_t xmin = mt_keep_threshold(p);
+#define TB_MTG_CASE(V)                                                                         \
+    case V:                                                                                    \
+        launch(softmax_fwd_mtgen_kernel<V>, nchunks, kMtThreads, 0, st)(z, P, D, mask, states,  \
+                                                                     scale, xmin, rows);       \
+        break;
+    switch (cols / 128) {
+        TB_MTG_CASE(1)
+        TB_MTG_CASE(2)
+        TB_MTG_CASE(4)
+        TB_MTG_CASE(8)
+        default: return cudaErrorInvalidValue;
+    }
+#undef TB_MTG_CASE
     return cudaGetLastError();
 }
 

@@ -137,6 +137,18 @@ cudaError_t launch_pdl(const void* kernel, int grid, int block, size_t smem, cud
 // The reference's mask stream (std::mt19937_64, tensor.cpp:186-203) on the
 // device: keep bits of elements [e_begin, e_begin + n), e_begin % 32 == 0.
 size_t mt_keep_workspace(uint64_t e_begin, int64_t n);
+// The chunk start states (kMtN words each) of the chunks covering elements
+// [e_begin, e_begin + n) of the stream, computed into the workspace
+// (mt_keep_workspace bytes); *states = chunk e_begin / kMtChunk's state.
+cudaError_t launch_mt_chunk_states(uint64_t seed, uint64_t e_begin, int64_t n, void* ws,
+                                   size_t ws_bytes, const uint64_t** states, cudaStream_t st);
+// Softmax + dropout forward with the reference's mask stream generated inside
+// the kernel (softmax_kernels.cu); falls back to launch_mt_keep_bits + the
+// supplied-mask forward when the shape does not fit the fused kernel.
+cudaError_t launch_softmax_dropout_fwd_mt(const float* z, double p, uint64_t seed,
+                                          uint64_t e_begin, uint32_t* mask, float* P, float* D,
+                                          int64_t rows, int64_t cols, void* ws, size_t ws_bytes,
+                                          cudaStream_t st);
 cudaError_t launch_mt_keep_bits(uint64_t seed, double p, uint64_t e_begin, int64_t n,
                                 uint32_t* mask, void* ws, size_t ws_bytes, cudaStream_t st);
 

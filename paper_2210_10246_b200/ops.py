@@ -668,6 +668,34 @@ def bernoulli_keep_bits_device(n: int, p: float, seed: int, offset: int = 0,
     return out
 
 
+def softmax_dropout_fwd_refmask(z: torch.Tensor, p: float, seed: int, offset: int = 0,
+                                mask: torch.Tensor = None, P: torch.Tensor = None,
+                                D: torch.Tensor = None, write_d: bool = True,
+                                workspace: torch.Tensor = None):
+    """softmax_dropout_fwd with the reference's own mask stream
+    (BoolMask::bernoulli_keep(shape, p, seed), elements [offset, offset + n))
+    generated inside the softmax kernel; the mask is written to ``mask``.
+    Returns (P, D, mask): bitwise the supplied-mask forward on
+    bernoulli_keep_bits_device(n, p, seed, offset)."""
+    z = _f32(z, "z")
+    rows, cols = _rows_cols(z)
+    mask = _mask(mask, "mask", z.numel(), z.device)
+    P = _out(P, "P", z)
+    D = _out(D, "D", z) if write_d else None
+    nbytes = int(lib().tempo_bernoulli_keep_bits_workspace_size(int(offset), z.numel()))
+    if workspace is None:
+        workspace = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=z.device)
+    else:
+        _dev(workspace, "workspace", workspace.dtype, z.device, min_numel=None)
+        if workspace.numel() * workspace.element_size() < nbytes:
+            raise TempoError(2, f"workspace: need {nbytes} bytes")
+    check(lib().tempo_softmax_dropout_fwd_refmask(
+        _ptr(z), float(p), int(seed), int(offset), _ptr(mask), _ptr(P),
+        _ptr(D if write_d else None), rows, cols, _ptr(workspace),
+        workspace.numel() * workspace.element_size(), _stream()))
+    return P, (D if write_d else None), mask
+
+
 def mt_outputs_after(seed: int, steps: int, count: int):
     """Host reference of the jump-ahead: `count` outputs of
     std::mt19937_64(seed) after discard(steps) (numpy uint64)."""
