@@ -45,6 +45,27 @@ TB_HD uint64_t mt_temper(uint64_t z) {
     return z;
 }
 
+#ifdef __CUDACC__
+// keep <=> mt_temper(w) >= xmin, from the HIGH word of the tempered output
+// alone except on a tie of the high words (probability 2^-32 per output):
+// tempering is linear over GF(2), and its last step (z ^= z >> 43) and the
+// low half of the third never reach the high word, so hi(temper(w)) =
+// hi(y2) ^ ((lo(y2) << 5) & 0xFFF7EEE0) with y1, y2 the first two steps on
+// 32-bit halves -- about half the integer work of the full 64-bit temper
+// (the generators are issue-bound on it).
+__device__ __forceinline__ bool mt_keep(uint64_t w, uint64_t xmin) {
+    const uint32_t zl = (uint32_t)w, zh = (uint32_t)(w >> 32);
+    const uint32_t y1l = zl ^ (__funnelshift_r(zl, zh, 29) & 0x55555555u);
+    const uint32_t y1h = zh ^ ((zh >> 29) & 0x55555555u);
+    const uint32_t y2l = y1l ^ ((y1l << 17) & 0xEDA60000u);
+    const uint32_t y2h = y1h ^ (__funnelshift_l(y1l, y1h, 17) & 0x71D67FFFu);
+    const uint32_t th = y2h ^ ((y2l << 5) & 0xFFF7EEE0u);
+    const uint32_t xh = (uint32_t)(xmin >> 32);
+    if (th != xh) return th > xh;
+    return mt_temper(w) >= xmin;  // tie of the high words
+}
+#endif
+
 // Host only.
 void mt_seed_state(uint64_t seed, uint64_t* st312);
 // Jump polynomials x^(d * 32^l * kMtChunk) mod P, layout [l][d-1][kMtPolyWords]

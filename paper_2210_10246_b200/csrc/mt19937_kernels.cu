@@ -156,7 +156,7 @@ __global__ void __launch_bounds__(kGenThreads) mt_keep_kernel(const uint64_t* __
                     const uint64_t w = mt_next_word(ring[a312[ph]], ring[a311[ph]], ring[a156[ph]]);
                     ring[aw[ph]] = w;
                     __syncthreads();  // w is visible: the next step's loads overlap the tempering
-                    const uint32_t word = __ballot_sync(kFull, mt_temper(w) >= xmin);
+                    const uint32_t word = __ballot_sync(kFull, mt_keep(w, xmin));
                     if (lane == s4 + ph) mine = word;
                 }
             }

@@ -623,7 +623,7 @@ __global__ void __launch_bounds__(kMtThreads, TM_MTGEN_MINB) softmax_fwd_mtgen_k
                     const uint64_t w = mt_next_word(ring[a312[ph]], ring[a311[ph]], ring[a156[ph]]);
                     ring[aw[ph]] = w;
                     group_bar(1, 32 * kMtGenWarps);  // w visible to the next step
-                    const uint32_t word = __ballot_sync(kFull, mt_temper(w) >= xmin);
+                    const uint32_t word = __ballot_sync(kFull, mt_keep(w, xmin));
                     if (lane == 0) words[(t4 + ph) * 4 + warp] = word;
                 }
             }
