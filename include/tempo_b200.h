@@ -125,6 +125,20 @@ int tempo_ln_ip_bwd(const float* dy, const float* y, const float* rstd, const fl
                     const float* beta, float* dx, float* dgamma, float* dbeta, void* workspace,
                     size_t workspace_bytes, int64_t rows, int64_t cols, tempo_stream_t stream);
 
+/* The two stages separately (SURVEY 8b's split form), for callers that
+ * combine partials themselves: stage 1 writes dx and leaves the per-CTA
+ * fp64 partial rows in `workspace` ([*nparts][2*cols]: dgamma partials, then
+ * dbeta partials; *nparts is set); tempo_ln_param_reduce sums nparts such
+ * rows (any producer: stage 1 here, or partial rows gathered from several
+ * ranks) in a fixed order into dgamma/dbeta -- tempo_ln_ip_bwd is exactly
+ * stage 1 then stage 2 on the same workspace. */
+int tempo_ln_ip_bwd_partials(const float* dy, const float* y, const float* rstd,
+                             const float* gamma, const float* beta, float* dx, void* workspace,
+                             size_t workspace_bytes, int64_t rows, int64_t cols, int64_t* nparts,
+                             tempo_stream_t stream);
+int tempo_ln_param_reduce(const double* partials, int64_t nparts, int64_t cols, float* dgamma,
+                          float* dbeta, tempo_stream_t stream);
+
 /* Multi-GPU: the path's one collective -- the sum of every
  * rank's LayerNorm dgamma/dbeta -- fused into the backward's stage 2 over
  * peer memory instead of a separate all-reduce (replaces the reference's
@@ -232,6 +246,12 @@ int tempo_attn_probs_bwd(const float* dD, const float* P, const uint32_t* mask, 
  * Also the recompute rule "dropout-rescale" (ops_tempo.cpp:17-26). */
 int tempo_dropout_fwd(const float* x, double p, tempo_mask_mode_t mode, uint32_t* mask,
                       uint64_t seed, uint64_t offset, float* y, int64_t n, tempo_stream_t stream);
+/* The recompute rule "dropout-rescale" (ops_tempo.cpp:17-26, run from the
+ * consumer's BackwardCtx::stash, tape.cpp:244-264): D = mask ? P*(1/(1-p)) :
+ * 0, bitwise the forward's D (the same kernel as tempo_dropout_fwd with a
+ * SUPPLIED mask; the mask is only read). */
+int tempo_dropout_recompute(const float* P, const uint32_t* mask, double p, float* D, int64_t n,
+                            tempo_stream_t stream);
 /* dx = mask ? dy*(1/(1-p)) : 0.  dx may alias dy. */
 int tempo_dropout_bwd(const float* dy, const uint32_t* mask, double p, float* dx, int64_t n,
                       tempo_stream_t stream);

@@ -589,6 +589,39 @@ int tempo_ln_ip_bwd(const float* dy, const float* y, const float* rstd, const fl
                        "tempo_ln_ip_bwd");
 }
 
+int tempo_ln_ip_bwd_partials(const float* dy, const float* y, const float* rstd,
+                             const float* gamma, const float* beta, float* dx, void* workspace,
+                             size_t workspace_bytes, int64_t rows, int64_t cols, int64_t* nparts,
+                             tempo_stream_t stream) {
+    if (!nparts) return fail(TEMPO_ERR_PARAM, "layernorm: null nparts");
+    *nparts = 0;
+    if (int rc = check_rows(rows, cols, "layernorm backward")) return rc;
+    if (cols > std::numeric_limits<int>::max())
+        return fail(TEMPO_ERR_DIMENSION, "layernorm: row too long");
+    if (cols > 0 && (!gamma || !beta)) return fail(TEMPO_ERR_PARAM, "layernorm: null parameter pointer");
+    if (rows > 0 && (!dy || !y || !rstd || !dx))
+        return fail(TEMPO_ERR_PARAM, "layernorm: null tensor pointer");
+    size_t need = tempo_ln_ip_bwd_workspace_size(rows, cols);
+    if (workspace_bytes < need || (need > 0 && !workspace))
+        return fail(TEMPO_ERR_PARAM, "layernorm backward workspace too small: need " +
+                                         std::to_string(need) + " bytes");
+    return cuda_status(tb::launch_ln_bwd(dy, y, rstd, gamma, beta, dx, nullptr, nullptr, workspace,
+                                         rows, cols, S(stream), nullptr, nullptr, 1.0, nullptr,
+                                         nparts),
+                       "tempo_ln_ip_bwd_partials");
+}
+
+int tempo_ln_param_reduce(const double* partials, int64_t nparts, int64_t cols, float* dgamma,
+                          float* dbeta, tempo_stream_t stream) {
+    if (nparts < 0 || cols < 0) return fail(TEMPO_ERR_DIMENSION, "ln_param_reduce: negative size");
+    if (cols > std::numeric_limits<int>::max() / 2 || nparts > std::numeric_limits<int>::max())
+        return fail(TEMPO_ERR_DIMENSION, "ln_param_reduce: too large");
+    if (cols > 0 && (!dgamma || !dbeta || (nparts > 0 && !partials)))
+        return fail(TEMPO_ERR_PARAM, "ln_param_reduce: null pointer");
+    return cuda_status(tb::launch_ln_param_reduce(partials, nparts, cols, dgamma, dbeta, S(stream)),
+                       "tempo_ln_param_reduce");
+}
+
 // ---- multi-GPU: stage 2 fused with the cross-rank sum --------------------------------
 size_t tempo_ln_peer_inbox_bytes(int32_t world, int64_t cols) {
     return world > 0 && cols > 0 ? tb::ln_peer_inbox_bytes(world, cols) : 0;
@@ -889,6 +922,16 @@ int tempo_dropout_fwd(const float* x, double p, tempo_mask_mode_t mode, uint32_t
                                               mode == TEMPO_MASK_PHILOX, mask, seed, offset, y, n,
                                               S(stream)),
                        "tempo_dropout_fwd");
+}
+
+int tempo_dropout_recompute(const float* P, const uint32_t* mask, double p, float* D, int64_t n,
+                            tempo_stream_t stream) {
+    if (int rc = check_n(n, "dropout recompute")) return rc;
+    if (int rc = check_p(p)) return rc;
+    if (n > 0 && (!P || !D || !mask)) return fail(TEMPO_ERR_PARAM, "dropout recompute: null pointer");
+    return cuda_status(tb::launch_dropout_fwd(P, 1.0 / (1.0 - p), philox_threshold(p), 0,
+                                              const_cast<uint32_t*>(mask), 0, 0, D, n, S(stream)),
+                       "tempo_dropout_recompute");
 }
 
 int tempo_dropout_bwd(const float* dy, const uint32_t* mask, double p, float* dx, int64_t n,

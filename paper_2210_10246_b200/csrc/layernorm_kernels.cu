@@ -343,7 +343,10 @@ __global__ void __launch_bounds__(kWWarps * 32, 2) ln_fwd_warp_kernel(
 constexpr int kDStages = TM_DAL_STAGES;
 
 template <int VPL, int MODE>
-__global__ void __launch_bounds__(kWWarps * 32, 2) dal_fwd_warp_kernel(
+#ifndef TM_DAL_MINB
+#define TM_DAL_MINB 2
+#endif
+__global__ void __launch_bounds__(kWWarps * 32, TM_DAL_MINB) dal_fwd_warp_kernel(
     const float* __restrict__ proj, const float* __restrict__ res, uint32_t* __restrict__ mask,
     double scale, uint64_t thresh, uint64_t seed, uint64_t offset,
     const float* __restrict__ gamma, const float* __restrict__ beta, double eps,
@@ -1587,8 +1590,10 @@ size_t ln_bwd_workspace(int64_t rows, int64_t cols) {
 cudaError_t launch_ln_bwd(const float* dy, const float* y, const float* rstd, const float* gamma,
                           const float* beta, float* dx, float* dgamma, float* dbeta, void* ws,
                           int64_t rows, int64_t cols, cudaStream_t st, const LnPeer* peer,
-                          const uint32_t* mask, double scale, float* dproj) {
+                          const uint32_t* mask, double scale, float* dproj, int64_t* nparts_out) {
+    if (nparts_out) *nparts_out = 0;
     if (cols == 0) return cudaSuccess;
+    if (rows == 0 && nparts_out) return cudaSuccess;  // no partial rows
     if (rows == 0) {
         if (peer) return launch_ln_param_reduce_peer(nullptr, 0, cols, *peer, dgamma, dbeta, st);
         cudaMemsetAsync(dgamma, 0, cols * sizeof(float), st);
@@ -1629,10 +1634,25 @@ cudaError_t launch_ln_bwd(const float* dy, const float* y, const float* rstd, co
                                                        (int)cols, mask, scale, dproj,
                                                        smem == 0 ? 1 : 0);
     }
+    if (nparts_out) {
+        *nparts_out = grid;
+        return cudaGetLastError();
+    }
     if (peer) return launch_ln_param_reduce_peer(w, grid, cols, *peer, dgamma, dbeta, st);
+    return launch_ln_param_reduce(w, grid, cols, dgamma, dbeta, st);
+}
+
+cudaError_t launch_ln_param_reduce(const double* partials, int64_t nparts, int64_t cols,
+                                   float* dgamma, float* dbeta, cudaStream_t st) {
+    if (cols == 0) return cudaSuccess;
+    if (nparts == 0) {
+        cudaMemsetAsync(dgamma, 0, cols * sizeof(float), st);
+        cudaMemsetAsync(dbeta, 0, cols * sizeof(float), st);
+        return cudaGetLastError();
+    }
     const int rgrid = (int)((2 * cols + 31) / 32);
-    return launch_pdl((const void*)ln_param_reduce_kernel, rgrid, 1024, 0, st,
-                      (const double*)w, grid, (int)cols, dgamma, dbeta);
+    return launch_pdl((const void*)ln_param_reduce_kernel, rgrid, 1024, 0, st, partials,
+                      (int)nparts, (int)cols, dgamma, dbeta);
 }
 
 cudaError_t launch_dal_fwd(const float* proj, const float* res, double scale, uint64_t thresh,

@@ -72,11 +72,17 @@ size_t ln_peer_flag_bytes(int world, int64_t cols);
 cudaError_t launch_ln_param_reduce_peer(const double* partials, int64_t nparts, int64_t cols,
                                         const LnPeer& peer, float* dgamma, float* dbeta,
                                         cudaStream_t st);
+// nparts_out != nullptr: stage 1 only -- the fp64 partial rows stay in ws
+// ([nparts][2*cols]: dgamma partials, then dbeta) and their count is returned
 cudaError_t launch_ln_bwd(const float* dy, const float* y, const float* rstd, const float* gamma,
                           const float* beta, float* dx, float* dgamma, float* dbeta, void* ws,
                           int64_t rows, int64_t cols, cudaStream_t st,
                           const LnPeer* peer = nullptr, const uint32_t* mask = nullptr,
-                          double scale = 1.0, float* dproj = nullptr);
+                          double scale = 1.0, float* dproj = nullptr,
+                          int64_t* nparts_out = nullptr);
+// stage 2 alone: dgamma/dbeta = the fixed-order sum of nparts partial rows
+cudaError_t launch_ln_param_reduce(const double* partials, int64_t nparts, int64_t cols,
+                                   float* dgamma, float* dbeta, cudaStream_t st);
 // hidden dropout -> residual add -> LayerNorm forward, fused (cols % 32 == 0)
 cudaError_t launch_dal_fwd(const float* proj, const float* res, double scale, uint64_t thresh,
                            int philox, uint32_t* mask, uint64_t seed, uint64_t offset,

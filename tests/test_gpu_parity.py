@@ -578,3 +578,74 @@ def test_vector_paths_agree_bitwise(tops, table_text, cuda, n):
     for other in res[1:]:
         for a, b in zip(res[0], other):
             assert torch.equal(a, b)
+
+
+# ------------------------------------------- the split LN backward, recompute
+@pytest.mark.parametrize("rows,cols", [(64, 1024), (33, 3000), (16, 4096), (7, 768)])
+def test_ln_bwd_split_stages(tops, port, cuda, rows, cols):
+    """tempo_ln_ip_bwd_partials + tempo_ln_param_reduce (SURVEY 8b's split
+    form) equal tempo_ln_ip_bwd bitwise; partial rows of two row shards
+    reduced together give the unsharded dgamma/dbeta (F64 oracle, 1e-5)."""
+    import ctypes as C
+    import torch
+    from paper_2210_10246_b200._capi import lib
+    L = lib()
+    g = np.random.default_rng(rows + cols)
+    x = g.standard_normal((rows, cols)).astype(np.float32)
+    gam = (1 + 0.2 * g.standard_normal(cols)).astype(np.float32)
+    bet = (0.1 * g.standard_normal(cols)).astype(np.float32)
+    dy = g.standard_normal((rows, cols)).astype(np.float32)
+    T = lambda a: to_dev(a, cuda)  # noqa: E731
+    y, rs = tops.layernorm_ip_fwd(T(x), T(gam), T(bet))
+    dx, dg, db = tops.layernorm_ip_bwd(T(dy), y, rs, T(gam), T(bet))
+    st = torch.cuda.current_stream().cuda_stream
+
+    def stage1(dy_t, y_t, rs_t):
+        r = y_t.shape[0]
+        nb = int(L.tempo_ln_ip_bwd_workspace_size(r, cols))
+        ws = torch.empty(max(nb, 16), dtype=torch.uint8, device=cuda)
+        dx_t = torch.empty_like(y_t)
+        npart = C.c_int64(-1)
+        assert L.tempo_ln_ip_bwd_partials(dy_t.data_ptr(), y_t.data_ptr(), rs_t.data_ptr(),
+                                          T(gam).data_ptr(), T(bet).data_ptr(), dx_t.data_ptr(),
+                                          ws.data_ptr(), nb, r, cols, C.byref(npart), st) == 0
+        return dx_t, ws.view(torch.float64)[: npart.value * 2 * cols].view(npart.value, 2 * cols)
+
+    def reduce(parts):
+        dg2 = torch.empty(cols, device=cuda)
+        db2 = torch.empty(cols, device=cuda)
+        parts = parts.contiguous()
+        assert L.tempo_ln_param_reduce(parts.data_ptr(), parts.shape[0], cols, dg2.data_ptr(),
+                                       db2.data_ptr(), st) == 0
+        return dg2, db2
+
+    dy_t = T(dy)
+    dx1, parts = stage1(dy_t, y, rs)
+    dg1, db1 = reduce(parts)
+    torch.cuda.synchronize()
+    assert torch.equal(dx1, dx) and torch.equal(dg1, dg) and torch.equal(db1, db)
+    # two row shards: their partial rows stacked and reduced once
+    h = rows // 2
+    _, pa = stage1(dy_t[:h].contiguous(), y[:h].contiguous(), rs[:h].contiguous())
+    pa = pa.clone()
+    _, pb = stage1(dy_t[h:].contiguous(), y[h:].contiguous(), rs[h:].contiguous())
+    dg3, db3 = reduce(torch.cat([pa, pb.clone()]))
+    torch.cuda.synchronize()
+    _, rdg, rdb = port.ln_bwd(dy, y.cpu().numpy(), rs.cpu().numpy(), gam, bet, True)
+    assert rel_err(dg3.cpu().numpy(), rdg) <= 1e-5
+    assert rel_err(db3.cpu().numpy(), rdb) <= 1e-5
+
+
+def test_dropout_recompute_entry(tops, cuda):
+    """tempo_dropout_recompute: the recompute rule, bitwise the forward D."""
+    import torch
+    from paper_2210_10246_b200._capi import lib
+    z = torch.randn(333, 512, device=cuda)
+    P, D, m = tops.softmax_dropout_fwd(z, 0.1, seed=4)
+    D2 = torch.empty_like(D)
+    assert lib().tempo_dropout_recompute(P.data_ptr(), m.data_ptr(), 0.1, D2.data_ptr(), P.numel(),
+                                         torch.cuda.current_stream().cuda_stream) == 0
+    torch.cuda.synchronize()
+    assert torch.equal(D2, D)
+    assert lib().tempo_dropout_recompute(P.data_ptr(), m.data_ptr(), 1.0, D2.data_ptr(), 4,
+                                         torch.cuda.current_stream().cuda_stream) == 3
