@@ -808,6 +808,53 @@ def cpu_reference_sample(frac_rows: int, threads: int, steps: int, warmup: int, 
     return nbytes / dt / 1e9, dt, sample
 
 
+def cpu_reference_configs(threads: int, reps: int = 2):
+    """BASELINE configs[0..2] on the reference's own CPU implementation
+    (oracle/_ref: ref_op_create / ref_op_run -- the reference's builders and
+    Tape::backward) at their FULL shapes, rows sharded over `threads` host
+    threads (one Graph per thread), inputs built outside the
+    timed region: the CPU column beside per_config (SURVEY 8d "full shapes
+    for cfg1-3").  Returns {config index: {ms, gbs, threads}}."""
+    import oracle
+    ref = oracle.Ref()
+    table = open(os.path.join(ROOT, "tests", "golden", "gelu_table_default_v1.txt")).read()
+    bits = 1.0 / 8
+    cfgs = [(0, 1024, 3072, 8 + bits + 12 + bits),
+            (1, 32 * 512, 768, 8 + 12),
+            (2, 32 * 12 * 512, 512, 12 + bits + 16 + bits)]
+    out = {}
+    for kind, rows, cols, bpe in cfgs:
+        handles = [None] * threads
+
+        def create(k):
+            r = (k + 1) * rows // threads - k * rows // threads
+            handles[k] = ref.op_create(kind, table, P_DROP, r, cols, 500 + k) if r else None
+
+        def run_all(fn):
+            ths = [threading.Thread(target=fn, args=(k,)) for k in range(threads)]
+            for t in ths:
+                t.start()
+            for t in ths:
+                t.join()
+
+        run_all(create)
+        try:
+            run = lambda k: handles[k] and ref.op_run(handles[k])  # noqa: E731
+            run_all(run)  # warm-up
+            t0 = time.perf_counter()
+            for _ in range(reps):
+                run_all(run)
+            dt = (time.perf_counter() - t0) / reps
+        finally:
+            for h in handles:
+                if h:
+                    ref.op_destroy(h)
+        out[kind] = {"ms": round(dt * 1e3, 2), "gbs": round(rows * cols * bpe / dt / 1e9, 3),
+                     "threads": threads, "kind": "reference",
+                     "what": "fwd + Tape::backward of the op pair at the config's full shape"}
+    return out
+
+
 def reference_frac(steps: int, warmup: int, budget_steps: int = 40) -> int:
     """Row fraction of the reference arm's step: the whole chain (1) while
     steps + warmup full steps (~2.5 s each on 16 host threads) fit the time
@@ -968,7 +1015,9 @@ def main():
                 "share_of_step": round(k_ms / ms, 4),
                 "isolated": {"ms": next(r["ms"] for r in per_op_rows if r["op"] == "attn_probs_bwd"),
                              "frac": next(r["frac"] for r in per_op_rows if r["op"] == "attn_probs_bwd")},
-                "per_unit": "16.125 B/element: dD, P (4+4) + mask bit + dZ, D (4+4); SURVEY 8d"}
+                "per_unit": "16.125 B/element: dD, P (4+4) + mask bit + dZ, D (4+4); SURVEY 8d",
+                # also against the 8 TB/s HBM3e specification
+                "frac_of_hbm_spec": round(k_gbs / 8000.0, 4)}
     prof_traffic = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(prof_traffic) and batch == B:  # captured at the configs[3] shapes
         try:
@@ -980,6 +1029,16 @@ def main():
 
     # ---- configs[0..2] at their own shapes (outside the timed region) -------
     per_config = per_config_timings(dev, peak) if rank == 0 else None
+    if per_config and world == 1 and not args.no_cpu_baseline:
+        try:  # the reference's CPU path beside each config
+            cpu_cfg = cpu_reference_configs(len(os.sched_getaffinity(0)))
+            for c in per_config:
+                for i in range(3):
+                    if c["config"].startswith(f"configs[{i}]"):
+                        c["cpu_reference"] = cpu_cfg[i]
+                        c["gpu_vs_cpu_reference"] = round(c["ms"] and cpu_cfg[i]["ms"] / c["ms"], 1)
+        except Exception as ex:  # noqa: BLE001  (report, do not fail the bench)
+            per_config.append({"cpu_reference": f"unavailable: {str(ex)[:160]}"})
     per_row_length = None
     if rank == 0:
         try:

@@ -264,6 +264,10 @@ class Ref:
         L.ref_chain_create.restype = C.c_void_p
         L.ref_chain_run.argtypes = [C.c_void_p]
         L.ref_chain_destroy.argtypes = [C.c_void_p]
+        L.ref_op_create.argtypes = [C.c_int, C.c_char_p, C.c_double, _i64, _i64, C.c_uint64]
+        L.ref_op_create.restype = C.c_void_p
+        L.ref_op_run.argtypes = [C.c_void_p]
+        L.ref_op_destroy.argtypes = [C.c_void_p]
 
     def _check(self, rc: int) -> None:
         if rc:
@@ -283,6 +287,22 @@ class Ref:
         if not h:
             raise OracleError(1, self.L.ref_last_error().decode())
         return h
+
+    def op_create(self, kind: int, table_text: str, p: float, rows: int, cols: int, seed: int):
+        """One op pair of BASELINE configs[0..2] (kind 0 GELU, 1 LayerNorm, 2
+        softmax -> dropout_recompute) on [rows, cols], inputs built once by the
+        reference's generators (ref_harness.cpp ref_op_create)."""
+        h = self.L.ref_op_create(kind, table_text.encode(), p, rows, cols, seed)
+        if not h:
+            raise OracleError(1, self.L.ref_last_error().decode())
+        return h
+
+    def op_run(self, h) -> None:
+        """Forward + Tape::backward of the op pair (the timed step)."""
+        self._check(self.L.ref_op_run(h))
+
+    def op_destroy(self, h) -> None:
+        self.L.ref_op_destroy(h)
 
     def chain_run(self, h) -> None:
         """One forward + Tape::backward of the chain shard (the timed step)."""

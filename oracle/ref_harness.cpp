@@ -438,5 +438,71 @@ int ref_chain_run(void* handle) {
 
 void ref_chain_destroy(void* handle) { delete static_cast<RefChain*>(handle); }
 
+// BASELINE configs[0..2] one op pair at a time (bench.py per_config's CPU
+// column): kind 0 = GELU-ip fwd + Tape::backward on [rows, cols] (configs[0]),
+// 1 = LayerNorm-ip fwd + backward incl. dgamma/dbeta (configs[1]), 2 =
+// softmax -> dropout_recompute fwd + backward + the consumer's recompute of D
+// (configs[2]); inputs built once by the reference's own generators.
+struct RefOp {
+    int kind;
+    GeluPolyTable table;
+    double p;
+    Tensor x, dy, g, b;
+    BoolMask keep;
+};
+
+void* ref_op_create(int kind, const char* table_text, double p, std::int64_t rows,
+                    std::int64_t cols, std::uint64_t seed) {
+    RefOp* c = nullptr;
+    int rc = guarded([&] {
+        c = new RefOp{kind, GeluPolyTable::parse_string(table_text), p};
+        Shape sh{rows, cols};
+        c->x = Tensor::randn(sh, seed * 16 + 1, Dtype::F32);
+        c->dy = Tensor::randn(sh, seed * 16 + 2, Dtype::F32);
+        if (kind == 1) {
+            Tensor n1 = Tensor::randn({cols}, seed * 16 + 3, Dtype::F64);
+            c->g = Tensor::zeros({cols}, Dtype::F32);
+            c->b = Tensor::zeros({cols}, Dtype::F32);
+            for (std::int64_t j = 0; j < cols; ++j) {
+                c->g.set(j, 1 + 0.2 * n1.get(j));
+                c->b.set(j, 0.1 * n1.get(j));
+            }
+        }
+        if (kind == 2) c->keep = BoolMask::bernoulli_keep(sh, p, seed * 16 + 4);
+    });
+    if (rc != 0) {
+        delete c;
+        return nullptr;
+    }
+    return c;
+}
+
+int ref_op_run(void* handle) {
+    return guarded([&] {
+        RefOp& c = *static_cast<RefOp*>(handle);
+        Graph g;
+        NodeId xn = g.leaf(c.x, "x");
+        if (c.kind == 0) {
+            NodeId yn = tempo_ops::gelu(g, xn, &c.table, "y", "y_mask");
+            GradientMap gm = g.tape.backward(yn, c.dy);
+            (void)gm.at(xn);
+        } else if (c.kind == 1) {
+            NodeId gn = g.param(c.g, "gamma");
+            NodeId bn = g.param(c.b, "beta");
+            NodeId yn = tempo_ops::layernorm(g, xn, gn, bn, 1e-5, "y", "y_rstd");
+            GradientMap gm = g.tape.backward(yn, c.dy);
+            (void)gm.at(xn);
+        } else {
+            NodeId pn = tempo_ops::softmax(g, xn, "probs");
+            NodeId dn = tempo_ops::dropout_recompute(g, pn, c.p, c.keep, "drop", "drop_mask");
+            GradientMap gm = g.tape.backward(dn, c.dy);
+            Tensor d_rec = dropout_apply(g.value(pn), c.keep, c.p);  // the dV GEMM's recompute
+            (void)gm.at(xn);
+        }
+    });
+}
+
+void ref_op_destroy(void* handle) { delete static_cast<RefOp*>(handle); }
+
 }  // extern "C"
 
