@@ -1,0 +1,70 @@
+"""One launch of each round-2 kernel family at a representative shape, for an
+`ncu --set full` capture (tools/profile_round.sh profiles the bench chain):
+long-row softmax fwd/bwd (S = 2048, 3072), long-row LayerNorm fwd / cluster
+backward (H = 4096), the fused dropout -> add -> LN at H = 4096, the softmax
+forward with the in-kernel reference mask stream (2^28 elements) and the
+tcgen05 dV GEMM (BERT-large heads).  Every op runs once as a warm-up, then
+once more inside the NVTX range "capture" (ncu --nvtx --nvtx-include
+"capture/" profiles only that pass)."""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+
+def main():
+    import torch
+    from paper_2210_10246_b200 import ops
+    dev = torch.device("cuda:0")
+    p = 0.1
+    ops_list = []
+    for S in (2048, 3072):
+        rows = (1 << 27) // S
+        z, dD = torch.randn(rows, S, device=dev), torch.randn(rows, S, device=dev)
+        P, D, dZ = torch.empty_like(z), torch.empty_like(z), torch.empty_like(z)
+        m = torch.empty(ops.mask_words(rows * S), dtype=torch.int32, device=dev)
+        ops_list.append(lambda z=z, P=P, D=D, m=m: ops.softmax_dropout_fwd(
+            z, p, mask=m, seed=1, P=P, D=D, generate=True))
+        ops_list.append(lambda dD=dD, P=P, m=m, dZ=dZ: ops.attn_probs_bwd(dD, P, m, p, dZ=dZ))
+    H, R = 4096, 8192
+    x, r, dy = (torch.randn(R, H, device=dev) for _ in range(3))
+    g = (1 + 0.1 * torch.randn(H, device=dev)).contiguous()
+    b = (0.1 * torch.randn(H, device=dev)).contiguous()
+    y, dx, dp = torch.empty_like(x), torch.empty_like(x), torch.empty_like(x)
+    rs = torch.empty(R, device=dev)
+    dg, db = torch.empty(H, device=dev), torch.empty(H, device=dev)
+    mh = torch.empty(ops.mask_words(R * H), dtype=torch.int32, device=dev)
+    ws = ops.ln_workspace(R, H, dev)
+    ops_list.append(lambda: ops.layernorm_ip_fwd(x, g, b, y=y, rstd=rs, check_gamma=False))
+    ops_list.append(lambda: ops.layernorm_ip_bwd(dy, y, rs, g, b, dx=dx, dgamma=dg, dbeta=db,
+                                                 workspace=ws))
+    ops_list.append(lambda: ops.dropout_add_layernorm_fwd(x, r, g, b, p, mask=mh, seed=3, y=y,
+                                                          rstd=rs, generate=True,
+                                                          check_gamma=False))
+    ops_list.append(lambda: ops.dropout_add_layernorm_bwd(dy, y, rs, g, b, mh, p, d_residual=dx,
+                                                          d_proj=dp, dgamma=dg, dbeta=db,
+                                                          workspace=ws))
+    rows, S = 64 * 16 * 512, 512
+    za = torch.randn(rows, S, device=dev)
+    Pa, Da = torch.empty_like(za), torch.empty_like(za)
+    ma = torch.empty(ops.mask_words(rows * S), dtype=torch.int32, device=dev)
+    nb = int(ops.lib().tempo_bernoulli_keep_bits_workspace_size(0, rows * S))
+    wsa = torch.empty(nb, dtype=torch.uint8, device=dev)
+    ops_list.append(lambda: ops.softmax_dropout_fwd_refmask(za, p, 5, mask=ma, P=Pa, D=Da,
+                                                            workspace=wsa))
+    dO = torch.randn(64 * 16, S, 64, device=dev)
+    dV = torch.empty(64 * 16, S, 64, device=dev)
+    ops_list.append(lambda: ops.attn_dropout_dv(Pa.view(64 * 16, S, S), ma, p, dO, dV=dV))
+    for fn in ops_list:  # warm-up pass
+        fn()
+    torch.cuda.synchronize()
+    torch.cuda.nvtx.range_push("capture")  # ncu --nvtx --nvtx-include "capture/"
+    for fn in ops_list:  # the captured pass
+        fn()
+        torch.cuda.synchronize()
+    torch.cuda.nvtx.range_pop()
+    print("profile_new done")
+
+
+if __name__ == "__main__":
+    main()
