@@ -15,8 +15,10 @@ timeout 1800 $CS --tool memcheck python -m pytest tests/test_gpu_parity.py tests
 # round 2: the long-row kernels (TMA row groups, the cluster LN backward with
 # its DSMEM exchange), the fused dropout -> add -> LN and the tcgen05 dV GEMM
 timeout 1800 $CS --tool memcheck python -m pytest tests/test_gpu_long_rows.py \
-    tests/test_gpu_fused_ln.py tests/test_gpu_dv_gemm.py -m gpu -q -x \
+    tests/test_gpu_fused_ln.py tests/test_gpu_dv_gemm.py tests/test_gpu_refmask.py -m gpu -q -x \
     > $O/pytest_long_fused_dv_memcheck.log 2>&1
+timeout 1800 $CS --tool racecheck python -m pytest tests/test_gpu_refmask.py -m gpu -q -x \
+    -k "fused_shapes" > $O/pytest_refmask_racecheck.log 2>&1
 for t in racecheck synccheck; do
     timeout 1800 $CS --tool $t python -m pytest tests/test_gpu_long_rows.py -m gpu -q -x \
         -k "supplied_mask or long_layernorm" > $O/pytest_long_$t.log 2>&1
