@@ -102,7 +102,11 @@ __device__ __forceinline__ void refine_moments(float m0, float t, float q, float
                                                float& mean, float& var) {
     const double delta = (double)t * (double)inv_m;
     mean = (float)((double)m0 + delta);
-    var = fmaxf(fmaf(-(float)delta, (float)delta, q * inv_m), 0.0f);
+    // clamp rounding-negative variances to 0 but keep a NaN (a NaN in the
+    // row makes the reference's var and rstd NaN; fmaxf would turn it into 0
+    // and rstd into 1/sqrt(eps))
+    const float v = fmaf(-(float)delta, (float)delta, q * inv_m);
+    var = v < 0.0f ? 0.0f : v;
 }
 
 __device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }

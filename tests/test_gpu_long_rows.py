@@ -178,3 +178,49 @@ def test_long_layernorm(tops, port, cuda, cols):
     assert rel_err(dx.cpu().numpy(), rdx) <= 1e-5
     assert rel_err(dg.cpu().numpy(), rdg) <= 1e-5
     assert rel_err(db.cpu().numpy(), rdb) <= 1e-5
+
+
+@pytest.mark.parametrize("cols", [2048, 3072, 8192])
+def test_long_softmax_special_rows(tops, port, cuda, cols):
+    """NaN anywhere -> NaN row, +inf -> NaN row, one finite score among -inf
+    (P = 1 there), huge logits, masked halves: as the oracle, on the
+    row-group kernels (the chunk holding the special value belongs to a
+    different warp of the group than the row's max)."""
+    import torch
+    from test_gpu_parity import _close_nan
+    inf, nan, big = np.inf, np.nan, float(np.finfo(np.float32).max)
+    rows = []
+    r = np.zeros(cols, np.float32); r[cols - 3] = nan; rows.append(r)
+    r = np.zeros(cols, np.float32); r[130] = inf; rows.append(r)
+    r = np.full(cols, -inf, np.float32); r[cols // 2 + 5] = 2.0; rows.append(r)
+    r = np.full(cols, -big, np.float32); r[777] = big; rows.append(r)
+    r = np.linspace(-100, 0, cols).astype(np.float32); rows.append(r)
+    r = np.random.default_rng(cols).standard_normal(cols).astype(np.float32); r[: cols // 2] = -inf
+    rows.append(r)
+    z = np.stack(rows)
+    P = tops.softmax_ip_fwd(to_dev(z, cuda))
+    Pd, D, m = tops.softmax_dropout_fwd(to_dev(z, cuda), 0.1, seed=2)
+    torch.cuda.synchronize()
+    rP = port.softmax_fwd(z)
+    assert _close_nan(P.cpu().numpy(), rP, 1e-5, 1e-9)
+    assert np.array_equal(Pd.cpu().numpy(), P.cpu().numpy(), equal_nan=True)
+
+
+@pytest.mark.parametrize("cols", [3072, 8192])
+def test_long_layernorm_special_rows(tops, port, cuda, cols):
+    """A NaN in a row makes that row's y and rstd NaN (the reference's double
+    sums propagate it) and leaves the other rows -- on the same row group /
+    cluster tile -- untouched; a constant row has var 0 -> rstd = 1/sqrt(eps)."""
+    import torch
+    from test_gpu_parity import _close_nan
+    g = np.random.default_rng(cols)
+    x = g.standard_normal((6, cols)).astype(np.float32)
+    x[1, cols // 3] = np.nan
+    x[3, :] = 2.5
+    gam = (1 + 0.2 * g.standard_normal(cols)).astype(np.float32)
+    bet = (0.1 * g.standard_normal(cols)).astype(np.float32)
+    y, rstd = tops.layernorm_ip_fwd(to_dev(x, cuda), to_dev(gam, cuda), to_dev(bet, cuda))
+    torch.cuda.synchronize()
+    ry, rrs, _ = port.ln_fwd(x, gam, bet, 1e-5)
+    assert _close_nan(y.cpu().numpy(), ry, 1e-5, 1e-5)
+    assert _close_nan(rstd.cpu().numpy(), rrs, 1e-6, 0)

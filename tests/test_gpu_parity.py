@@ -649,3 +649,27 @@ def test_dropout_recompute_entry(tops, cuda):
     assert torch.equal(D2, D)
     assert lib().tempo_dropout_recompute(P.data_ptr(), m.data_ptr(), 1.0, D2.data_ptr(), 4,
                                          torch.cuda.current_stream().cuda_stream) == 3
+
+
+@pytest.mark.parametrize("rows,cols", [(8, 1024), (8, 768), (8, 1000), (8, 2048)])
+def test_layernorm_nan_row(tops, port, cuda, rows, cols):
+    """A NaN in a row: that row's y and rstd are NaN as in the reference (its
+    double variance propagates the NaN), the other rows are untouched."""
+    import torch
+    g = np.random.default_rng(cols)
+    x = g.standard_normal((rows, cols)).astype(np.float32)
+    x[2, 5] = np.nan
+    gam = (1 + 0.2 * g.standard_normal(cols)).astype(np.float32)
+    bet = (0.1 * g.standard_normal(cols)).astype(np.float32)
+    y, rstd = tops.layernorm_ip_fwd(to_dev(x, cuda), to_dev(gam, cuda), to_dev(bet, cuda))
+    torch.cuda.synchronize()
+    ry, rrs, _ = port.ln_fwd(x, gam, bet, 1e-5)
+    assert _close_nan(y.cpu().numpy(), ry, 1e-5, 1e-5)
+    assert _close_nan(rstd.cpu().numpy(), rrs, 1e-6, 0)
+    if cols % 32 == 0:  # the fused dropout -> add -> LN forward (cols % 32 == 0)
+        yd, rsd, _ = tops.dropout_add_layernorm_fwd(to_dev(np.zeros_like(x), cuda),
+                                                    to_dev(x, cuda), to_dev(gam, cuda),
+                                                    to_dev(bet, cuda), 0.1, seed=1)
+        torch.cuda.synchronize()
+        assert _close_nan(yd.cpu().numpy(), ry, 1e-5, 1e-5)
+        assert _close_nan(rsd.cpu().numpy(), rrs, 1e-6, 0)
