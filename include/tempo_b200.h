@@ -125,8 +125,10 @@ int tempo_ln_ip_bwd(const float* dy, const float* y, const float* rstd, const fl
                     const float* beta, float* dx, float* dgamma, float* dbeta, void* workspace,
                     size_t workspace_bytes, int64_t rows, int64_t cols, tempo_stream_t stream);
 
-/* The two stages separately (SURVEY 8b's split form), for callers that
- * combine partials themselves: stage 1 writes dx and leaves the per-CTA
+/* The two stages separately (SURVEY 8b's split form of the backward
+ * closure, ops_tempo.cpp:121-155, whose dgamma/dbeta accumulation :150-151
+ * becomes stage 2), for callers that combine partials themselves: stage 1
+ * writes dx and leaves the per-CTA
  * fp64 partial rows in `workspace` ([*nparts][2*cols]: dgamma partials, then
  * dbeta partials; *nparts is set); tempo_ln_param_reduce sums nparts such
  * rows (any producer: stage 1 here, or partial rows gathered from several
