@@ -688,7 +688,22 @@ inline size_t lnl_smem(int64_t cols, int tensors) {
     return 128 + (size_t)lnl_stages(cols, tensors) * tensors * cols * 4;
 }
 // forward: W * 8 chunks cover the row
-inline int lnl_fwd_warps(int64_t nch) { return nch <= 16 ? 2 : nch <= 32 ? 4 : nch <= 64 ? 8 : 16; }
+inline int lnl_fwd_warps(int64_t nch) {
+    return nch <= 8 ? 1 : nch <= 16 ? 2 : nch <= 32 ? 4 : nch <= 64 ? 8 : 16;
+}
+#ifndef TM_LN_LONG_MIN
+#define TM_LN_LONG_MIN 1024  // LN forward: rows longer than this take ln_fwd_long_kernel
+#endif
+#ifndef TM_DAL_LONG_MIN
+#define TM_DAL_LONG_MIN 1024  // fused dropout -> add -> LN forward: likewise
+#endif
+// Small LN forwards (configs[1]: 16384 x 768 = 12.6 M elements) take the TMA
+// row-group kernel at any row length (one-warp CTAs for H <= 1024): A/B
+// configs[1] fwd+bwd 57.3 -> 52.9 us; at 32768 x 1024 the warp kernel stays
+// ahead (0.88 vs 0.86 of the copy peak), hence the size switch.
+#ifndef TM_LN_LONG_SMALL_N
+#define TM_LN_LONG_SMALL_N (int64_t(1) << 24)
+#endif
 
 size_t warp_fwd_smem(int vpl) {
     return 1024 + 2 * (size_t)vpl * 128 * 4 + (size_t)kWWarps * kWStages * vpl * 128 * 4;
@@ -1504,6 +1519,7 @@ cudaError_t launch_ln_long_fwd(const float* x, const float* res, uint32_t* mask,
         break;                                                                               \
     }
     switch (lnl_fwd_warps(nch)) {
+        TB_LNL(1)
         TB_LNL(2)
         TB_LNL(4)
         TB_LNL(8)
@@ -1521,8 +1537,9 @@ cudaError_t launch_ln_fwd(const float* x, const float* gamma, const float* beta,
                           cudaStream_t st) {
     if (rows == 0) return cudaSuccess;
     const int vpl = (int)(cols / 128);
+    const int64_t long_min = rows * cols < TM_LN_LONG_SMALL_N ? 0 : TM_LN_LONG_MIN;
     if (cols % 128 == 0 && (vpl == 6 || vpl == 8 || vpl == 4 || vpl == 2) &&
-        use_vec(cols, x, y, gamma, beta, x)) {
+        cols <= long_min && use_vec(cols, x, y, gamma, beta, x)) {
         const size_t smem = warp_fwd_smem(vpl);
 #define TB_LNW(V)                                                                            \
     case V: {                                                                                \
@@ -1540,7 +1557,7 @@ cudaError_t launch_ln_fwd(const float* x, const float* gamma, const float* beta,
 #undef TB_LNW
         return cudaGetLastError();
     }
-    if (long_fwd_ok(cols, 1024) && aligned16(x) && aligned16(y) && aligned16(gamma) &&
+    if (long_fwd_ok(cols, long_min) && aligned16(x) && aligned16(y) && aligned16(gamma) &&
         aligned16(beta))
         return launch_ln_long_fwd<0>(x, nullptr, nullptr, 1.0, 0, 0, 0, gamma, beta, eps, y, rstd,
                                      rows, cols, dev_status, st);
@@ -1666,7 +1683,8 @@ cudaError_t launch_dal_fwd(const float* proj, const float* res, double scale, ui
                            cudaStream_t st) {
     if (rows == 0) return cudaSuccess;
     const int vpl = (int)(cols / 128);
-    const bool warp_ok = cols % 128 == 0 && vpl >= 1 && vpl <= 8 && aligned16(proj) &&
+    const bool warp_ok = cols % 128 == 0 && vpl >= 1 && vpl <= 8 && cols <= TM_DAL_LONG_MIN &&
+                         aligned16(proj) &&
                          aligned16(res) && aligned16(y) && aligned16(gamma) && aligned16(beta) &&
                          (offset & 3u) == 0;
     if (warp_ok) {
@@ -1692,7 +1710,7 @@ cudaError_t launch_dal_fwd(const float* proj, const float* res, double scale, ui
 #undef TB_DAL
         return cudaGetLastError();
     }
-    if (long_fwd_ok(cols, 1024) && aligned16(proj) && aligned16(res) && aligned16(y) &&
+    if (long_fwd_ok(cols, TM_DAL_LONG_MIN) && aligned16(proj) && aligned16(res) && aligned16(y) &&
         aligned16(gamma) && aligned16(beta) && (offset & 3u) == 0) {
         return philox ? launch_ln_long_fwd<2>(proj, res, mask, scale, thresh, seed, offset, gamma,
                                               beta, eps, y, rstd, rows, cols, dev_status, st)
