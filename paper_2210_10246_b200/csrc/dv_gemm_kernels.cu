@@ -58,10 +58,33 @@ constexpr int kStagesG = 2;
 constexpr int kProducers = 256;      // 8 warps
 constexpr int kThreadsG = kProducers + 32;
 
+#ifndef TM_DV_FAST_RNA
+#define TM_DV_FAST_RNA 1
+#endif
+// Round to TF32 (10 explicit mantissa bits), nearest, ties away from zero:
+// cvt.rna.tf32.f32.  On sm_100 that conversion is a multi-instruction
+// sequence (inf/NaN check, integer rounding, mask), the producers' largest
+// ALU cost (ncu).  On the sign-magnitude bit pattern, adding half a TF32 ulp
+// (bit 12) and clearing the 13 low bits IS that rounding for finite values;
+// inf/NaN keep their bits (a NaN payload could carry into the sign).  The
+// split's low part x - hi is always finite and small, so it skips the check.
 __device__ __forceinline__ float tf32_rna(float x) {
+#if TM_DV_FAST_RNA
+    const uint32_t u = __float_as_uint(x);
+    const uint32_t r = (u + 0x1000u) & 0xffffe000u;
+    return __uint_as_float((u & 0x7f800000u) == 0x7f800000u ? u : r);
+#else
     uint32_t r;
     asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
     return __uint_as_float(r);
+#endif
+}
+__device__ __forceinline__ float tf32_rna_finite(float x) {  // x finite
+#if TM_DV_FAST_RNA
+    return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xffffe000u);
+#else
+    return tf32_rna(x);
+#endif
 }
 
 __device__ __forceinline__ uint32_t sw128_k_offset(int mn, int kchunk) {
@@ -223,7 +246,7 @@ __global__ void __launch_bounds__(kThreadsG, 1) dv_recompute_gemm_kernel(
                     // D exactly as dropout_apply / the forward's D (one fp64 rounding)
                     const float d = ((w >> lane) & 1u) ? (float)((double)pv[k] * scale) : 0.0f;
                     hi[u] = tf32_rna(d);
-                    lo[u] = tf32_rna(d - hi[u]);
+                    lo[u] = isfinite(d) ? tf32_rna_finite(d - hi[u]) : d - hi[u];
                 }
                 const uint32_t off = sw128_k_offset(t, q);
                 *reinterpret_cast<float4*>(a_hi + off) = make_float4(hi[0], hi[1], hi[2], hi[3]);
@@ -236,7 +259,7 @@ __global__ void __launch_bounds__(kThreadsG, 1) dv_recompute_gemm_kernel(
                 for (int u = 0; u < 4; ++u) {
                     const float o = ov[4 * q + u];
                     hi[u] = tf32_rna(o);
-                    lo[u] = tf32_rna(o - hi[u]);
+                    lo[u] = isfinite(o) ? tf32_rna_finite(o - hi[u]) : o - hi[u];
                 }
                 const uint32_t off = sw128_k_offset(bn, (bk0 >> 2) + q);
                 *reinterpret_cast<float4*>(b_hi + off) = make_float4(hi[0], hi[1], hi[2], hi[3]);
@@ -361,10 +384,16 @@ __device__ __forceinline__ uint32_t ldsu32(uint32_t addr) {
     return v;
 }
 
+#ifndef TM_DV_SS
+#define TM_DV_SS 5
+#endif
+#ifndef TM_DV_OS
+#define TM_DV_OS 3
+#endif
 template <int N>
 struct StagedCfg {
-    static constexpr int kSS = 5;                                  // staging slices in flight
-    static constexpr int kOS = 3;                                  // operand stages
+    static constexpr int kSS = TM_DV_SS;                           // staging slices in flight
+    static constexpr int kOS = TM_DV_OS;                           // operand stages
     static constexpr int kPbytes = kBKs * kBM * 4;                 // 16 KB
     static constexpr int kObytes = kBKs * N * 4;                   // 2 / 4 KB
     static constexpr int kMbytes = kBKs * (kBM / 32) * 4;          // 512 B of mask words
@@ -412,12 +441,12 @@ __global__ void __launch_bounds__(kSP + 64, 1) dv_recompute_gemm_staged_kernel(
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < kOS; ++s) {
-            mbar_init(&full[s], kSP);
+            mbar_init(&full[s], kSP / 32);  // one arrival per producer warp
             mbar_init(&empty[s], 1);
         }
         for (int s = 0; s < kSS; ++s) {
             mbar_init(&sfull[s], 1);
-            mbar_init(&sempty[s], kSP);
+            mbar_init(&sempty[s], kSP / 32);
         }
         mbar_init(&acc_full, 1);
         mbar_fence_init();
@@ -458,7 +487,8 @@ __global__ void __launch_bounds__(kSP + 64, 1) dv_recompute_gemm_staged_kernel(
             float ov[kOPT];
 #pragma unroll
             for (int k = 0; k < kOPT; ++k) ov[k] = lds32(sp + Cfg::kPbytes + (uint32_t)(((bk + k) * N + bn) * 4));
-            mbar_arrive(&sempty[ss]);  // this thread is done reading slice ss
+            __syncwarp();  // the warp is done reading slice ss: one arrival for it
+            if (lane == 0) mbar_arrive(&sempty[ss]);
             if (sl >= kOS) mbar_wait(&empty[s], (uint32_t)(((sl / kOS) + 1) & 1));
             const uint32_t a_hi = base + s * Cfg::kOpStage, a_lo = a_hi + Cfg::kAbytes;
             const uint32_t b_hi = a_lo + Cfg::kAbytes, b_lo = b_hi + Cfg::kBbytes;
@@ -470,7 +500,7 @@ __global__ void __launch_bounds__(kSP + 64, 1) dv_recompute_gemm_staged_kernel(
                     const int k = 4 * q + u;
                     const float d = ((w[k] >> lane) & 1u) ? pv[k] : 0.0f;
                     hi[u] = tf32_rna(d);
-                    lo[u] = tf32_rna(d - hi[u]);
+                    lo[u] = isfinite(d) ? tf32_rna_finite(d - hi[u]) : d - hi[u];
                 }
                 const uint32_t off = sw64_k_offset(m, kh * 2 + q);
                 sts128(a_hi + off, hi[0], hi[1], hi[2], hi[3]);
@@ -481,7 +511,7 @@ __global__ void __launch_bounds__(kSP + 64, 1) dv_recompute_gemm_staged_kernel(
 #pragma unroll
                 for (int u = 0; u < kOPT; ++u) {
                     hi[u] = tf32_rna(ov[u]);
-                    lo[u] = tf32_rna(ov[u] - hi[u]);
+                    lo[u] = isfinite(ov[u]) ? tf32_rna_finite(ov[u] - hi[u]) : ov[u] - hi[u];
                 }
                 const uint32_t off = sw64_k_offset(bn, bk >> 2) + (uint32_t)((bk & 3) * 4);
                 if (kOPT == 2) {
@@ -493,7 +523,8 @@ __global__ void __launch_bounds__(kSP + 64, 1) dv_recompute_gemm_staged_kernel(
                 }
             }
             fence_proxy_async_smem();
-            mbar_arrive(&full[s]);
+            __syncwarp();  // every lane fenced its operand stores: one arrival per warp
+            if (lane == 0) mbar_arrive(&full[s]);
         }
         // ---------------- epilogue: dV = (1/(1-p)) * sum of the sets ----------
         mbar_wait(&acc_full, 0);

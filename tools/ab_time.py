@@ -56,6 +56,7 @@ def main():
         "dal_bwd": (lambda: o.dropout_add_layernorm_bwd(c.dy_ln2, c.y_ln2, c.rs2, c.g2, c.b2, c.m2, bench.P_DROP, d_residual=c.dx_ln2, d_proj=c.dx_d2, dgamma=dp[:H], dbeta=dp[H:2 * H], workspace=c.ws), [c.dx_ln2, c.dx_d2, dp[:2 * H]]),
     }
     heads = bench.B * bench.A
+    torch.manual_seed(59)  # fixed dO: the output checksums compare across builds
     dO = torch.randn(heads, bench.S, 64, device=dev)
     dV = torch.empty(heads, bench.S, 64, device=dev)
     torch.backends.cuda.matmul.allow_tf32 = False
