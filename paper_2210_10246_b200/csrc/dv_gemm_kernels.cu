@@ -390,19 +390,27 @@ __device__ __forceinline__ uint32_t ldsu32(uint32_t addr) {
 #ifndef TM_DV_OS
 #define TM_DV_OS 3
 #endif
-template <int N>
+#ifndef TM_DV_BM
+// dV rows per CTA: 256 (1 CTA/SM) or 128 (2 CTAs/SM, 8 producer warps each).
+// A/B at BERT-large: 414 vs 449 us, bit-identical -- two CTAs per SM hide no
+// latency that matters and each loads the head's dO slices once per 128
+// rows (twice the dO traffic): the producers' issue rate is the limit.
+#define TM_DV_BM 256
+#endif
+template <int N, int BM>
 struct StagedCfg {
-    static constexpr int kSS = TM_DV_SS;                           // staging slices in flight
-    static constexpr int kOS = TM_DV_OS;                           // operand stages
-    static constexpr int kPbytes = kBKs * kBM * 4;                 // 16 KB
+    static constexpr int kSS = BM == 256 ? TM_DV_SS : 4;           // staging slices in flight
+    static constexpr int kOS = BM == 256 ? TM_DV_OS : 2;           // operand stages
+    static constexpr int kSP = 2 * BM;                             // producer threads
+    static constexpr int kPbytes = kBKs * BM * 4;                  // 16 / 8 KB
     static constexpr int kObytes = kBKs * N * 4;                   // 2 / 4 KB
-    static constexpr int kMbytes = kBKs * (kBM / 32) * 4;          // 512 B of mask words
+    static constexpr int kMbytes = kBKs * (BM / 32) * 4;           // 512 / 256 B of mask words
     static constexpr int kSlice = kPbytes + kObytes + kMbytes;
-    static constexpr int kAbytes = kBM * kBKs * 4;                 // 16 KB
+    static constexpr int kAbytes = BM * kBKs * 4;                  // 16 / 8 KB
     static constexpr int kBbytes = N * kBKs * 4;
     static constexpr int kOpStage = 2 * kAbytes + 2 * kBbytes;
     static constexpr size_t kSmem = 1024 + (size_t)kOS * kOpStage + (size_t)kSS * kSlice;
-    static_assert(kSmem <= 227 * 1024, "smem");
+    static_assert(kSmem <= (BM == 256 ? 227 : 110) * 1024, "smem");
 };
 
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y,
@@ -414,14 +422,16 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
         : "memory");
 }
 
-template <int N>
-__global__ void __launch_bounds__(kSP + 64, 1) dv_recompute_gemm_staged_kernel(
+template <int N, int BM>
+__global__ void __launch_bounds__(2 * BM + 64, BM == 256 ? 1 : 2) dv_recompute_gemm_staged_kernel(
     const __grid_constant__ CUtensorMap tm_p, const __grid_constant__ CUtensorMap tm_m,
     const __grid_constant__ CUtensorMap tm_o, double scale, float* __restrict__ dV, int s_q,
     int s_k) {
-    using Cfg = StagedCfg<N>;
+    using Cfg = StagedCfg<N, BM>;
+    constexpr int kSP = Cfg::kSP;
+    constexpr int kMB = BM / 128;  // M = 128 blocks (TMEM accumulators per set)
     constexpr int kSets = 512 / (2 * N) >= 4 ? 4 : 512 / (2 * N);
-    constexpr int kTmemCols = kSets * 2 * N;
+    constexpr int kTmemCols = kSets * kMB * N < 32 ? 32 : kSets * kMB * N;
     constexpr int kSS = Cfg::kSS, kOS = Cfg::kOS;
     grid_dep_wait();
     grid_dep_launch();
@@ -433,9 +443,9 @@ __global__ void __launch_bounds__(kSP + 64, 1) dv_recompute_gemm_staged_kernel(
     __shared__ uint32_t tmem_base_sh;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int jblocks = s_k / kBM;
+    const int jblocks = s_k / BM;
     const int64_t head = blockIdx.x / jblocks;
-    const int j0 = (blockIdx.x % jblocks) * kBM;
+    const int j0 = (blockIdx.x % jblocks) * BM;
     const int nsl = s_q / kBKs;  // slices = operand stages
     constexpr int kMMAWarp = kSP / 32, kLoadWarp = kSP / 32 + 1;
 
@@ -469,9 +479,9 @@ __global__ void __launch_bounds__(kSP + 64, 1) dv_recompute_gemm_staged_kernel(
         //    slice: D' = keep ? P : 0, split hi/lo TF32.  B: dO column
         //    bn = t % N, K-rows bk.. (1 or 2 per thread).
         const int t = threadIdx.x;
-        const int m = t % kBM, kh = t / kBM;
-        constexpr int kOPT = kBKs * N / kSP;  // 1 (N = 32) or 2 (N = 64)
-        static_assert(kOPT == 1 || kOPT == 2, "dO slice split");
+        const int m = t % BM, kh = t / BM;
+        constexpr int kOPT = kBKs * N / kSP;  // 1, 2 or 4 dO values per thread
+        static_assert(kOPT == 1 || kOPT == 2 || kOPT == 4, "dO slice split");
         const int bn = t % N, bk = (t / N) * kOPT;
         for (int sl = 0; sl < nsl; ++sl) {
             const int ss = sl % kSS, s = sl % kOS;
@@ -481,8 +491,8 @@ __global__ void __launch_bounds__(kSP + 64, 1) dv_recompute_gemm_staged_kernel(
             uint32_t w[8];
 #pragma unroll
             for (int k = 0; k < 8; ++k) {
-                pv[k] = lds32(sp + (uint32_t)(((kh * 8 + k) * kBM + m) * 4));
-                w[k] = ldsu32(sp + Cfg::kPbytes + Cfg::kObytes + (uint32_t)(((kh * 8 + k) * (kBM / 32) + (m >> 5)) * 4));
+                pv[k] = lds32(sp + (uint32_t)(((kh * 8 + k) * BM + m) * 4));
+                w[k] = ldsu32(sp + Cfg::kPbytes + Cfg::kObytes + (uint32_t)(((kh * 8 + k) * (BM / 32) + (m >> 5)) * 4));
             }
             float ov[kOPT];
 #pragma unroll
@@ -514,7 +524,10 @@ __global__ void __launch_bounds__(kSP + 64, 1) dv_recompute_gemm_staged_kernel(
                     lo[u] = isfinite(ov[u]) ? tf32_rna_finite(ov[u] - hi[u]) : ov[u] - hi[u];
                 }
                 const uint32_t off = sw64_k_offset(bn, bk >> 2) + (uint32_t)((bk & 3) * 4);
-                if (kOPT == 2) {
+                if (kOPT == 4) {
+                    sts128(b_hi + off, hi[0], hi[1 % kOPT], hi[2 % kOPT], hi[3 % kOPT]);
+                    sts128(b_lo + off, lo[0], lo[1 % kOPT], lo[2 % kOPT], lo[3 % kOPT]);
+                } else if (kOPT == 2) {
                     sts64(b_hi + off, hi[0], hi[kOPT - 1]);
                     sts64(b_lo + off, lo[0], lo[kOPT - 1]);
                 } else {
@@ -529,7 +542,7 @@ __global__ void __launch_bounds__(kSP + 64, 1) dv_recompute_gemm_staged_kernel(
         // ---------------- epilogue: dV = (1/(1-p)) * sum of the sets ----------
         mbar_wait(&acc_full, 0);
         tc_fence_after();
-        const int quad = warp % 4, mb = (warp / 4) % 2, half = warp / 8;  // warp w, w+8: column halves
+        const int quad = warp % 4, mb = (warp / 4) % kMB, half = warp / (4 * kMB);  // 2 column halves
         const int row = j0 + mb * 128 + quad * 32 + lane;
         float* out = dV + head * (int64_t)s_k * N + (int64_t)row * N;
         const float sc = (float)scale;
@@ -537,11 +550,12 @@ __global__ void __launch_bounds__(kSP + 64, 1) dv_recompute_gemm_staged_kernel(
         for (int c0 = half * (N / 2); c0 < (half + 1) * (N / 2); c0 += 16) {
             float v[16];
             const uint32_t ta = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(mb * N + c0);
+            static_assert(kSP / 32 == 8 * kMB, "two warps per (TMEM lane quadrant, M-block)");
             tmem_ld16(ta, v);
 #pragma unroll
             for (int set = 1; set < kSets; ++set) {
                 float wv[16];
-                tmem_ld16(ta + (uint32_t)(set * 2 * N), wv);
+                tmem_ld16(ta + (uint32_t)(set * kMB * N), wv);
 #pragma unroll
                 for (int i = 0; i < 16; ++i) v[i] += wv[i];
             }
@@ -566,11 +580,11 @@ __global__ void __launch_bounds__(kSP + 64, 1) dv_recompute_gemm_staged_kernel(
                 const int gk = sl * (kBKs / 8) + kk;  // global K-step
                 const int set = gk % kSets;
 #pragma unroll
-                for (int mb = 0; mb < 2; ++mb) {
+                for (int mb = 0; mb < kMB; ++mb) {
                     const uint32_t ao = mb * 128 * 64 + kk * 32;  // 128 rows x 64 B per M-block
                     const uint64_t ah = umma_desc_sw64(a_hi + ao, 512);
                     const uint64_t al = umma_desc_sw64(a_lo + ao, 512);
-                    const uint32_t acc = tmem + (uint32_t)(set * 2 * N + mb * N);
+                    const uint32_t acc = tmem + (uint32_t)(set * kMB * N + mb * N);
                     mma_tf32(acc, al, bh, idesc, gk >= kSets);
                     mma_tf32(acc, ah, bl, idesc, 1);
                     mma_tf32(acc, ah, bh, idesc, 1);
@@ -651,18 +665,20 @@ bool make_tmap_2d(CUtensorMap* map, CUtensorMapDataType dt, const void* ptr, uin
 template <int N>
 cudaError_t launch_dv_staged(const float* P, const uint32_t* mask, double scale, const float* dO,
                              float* dV, int64_t heads, int64_t s_q, int64_t s_k, cudaStream_t st) {
+    constexpr int BM = TM_DV_BM;
     CUtensorMap tp, tmk, to;
     const uint64_t rows = (uint64_t)(heads * s_q);
-    if (!make_tmap_2d(&tp, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, P, rows, (uint64_t)s_k, kBKs, kBM) ||
+    if (!make_tmap_2d(&tp, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, P, rows, (uint64_t)s_k, kBKs, BM) ||
         !make_tmap_2d(&tmk, CU_TENSOR_MAP_DATA_TYPE_UINT32, mask, rows, (uint64_t)(s_k / 32), kBKs,
-                      kBM / 32) ||
+                      BM / 32) ||
         !make_tmap_2d(&to, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, dO, rows, (uint64_t)N, kBKs, N))
         return launch_dv<N>(P, mask, scale, dO, dV, heads, s_q, s_k, st);  // no tensor maps
-    auto k = dv_recompute_gemm_staged_kernel<N>;
-    const size_t smem = StagedCfg<N>::kSmem;
-    (void)grid_for((const void*)k, kSP + 64, smem, 1);
-    const int64_t grid = heads * (s_k / kBM);
-    launch(k, (int)grid, kSP + 64, smem, st)(tp, tmk, to, scale, dV, (int)s_q, (int)s_k);
+    auto k = dv_recompute_gemm_staged_kernel<N, BM>;
+    const size_t smem = StagedCfg<N, BM>::kSmem;
+    constexpr int threads = StagedCfg<N, BM>::kSP + 64;
+    (void)grid_for((const void*)k, threads, smem, 1);
+    const int64_t grid = heads * (s_k / BM);
+    launch(k, (int)grid, threads, smem, st)(tp, tmk, to, scale, dV, (int)s_q, (int)s_k);
     return cudaGetLastError();
 }
 
