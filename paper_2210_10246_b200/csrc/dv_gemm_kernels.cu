@@ -345,7 +345,6 @@ __global__ void __launch_bounds__(kThreadsG, 1) dv_recompute_gemm_kernel(
 // 1/(1-p) is applied to dV in the epilogue, so staging D' = keep ? P : 0 is
 // a select.
 constexpr int kBKs = 16;  // K rows per staging slice = per operand stage
-constexpr int kSP = 512;  // 16 producer warps: 2 per dV row, 8 K-rows each
 
 __device__ __forceinline__ uint32_t sw64_k_offset(int mn, int kchunk) {
     // byte offset of 16-byte K-chunk `kchunk` (< 4) of row mn, K-major
