@@ -1009,8 +1009,9 @@ __global__ void __launch_bounds__(256) ln_bwd_generic_kernel(
 // sums of a tile it has not computed on yet.  Slots: a peer pushes tile i+4
 // into slot i%4 only after its B(i+2), which needs this CTA's push of tile
 // i+2, made after this CTA's B(i) -- so 4 slots never overwrite unread sums.
-// Stages: tile i (B), i+1 (A), i+2 in flight: 3-deep ring; stage i%3 is
-// refilled with tile i+3 after the next iteration's first block barrier.
+// Stages: tile i (B), i+1 (A), i+2 in flight: 3-deep ring; tile t lives in
+// stage t%3, and tile i+2 is loaded once B(i-1) has released its stage (at
+// A(i+1)'s block barrier).
 // The partial row of cluster c is ws[c] (its K CTAs write disjoint column
 // slices), reduced by the usual stage 2.
 constexpr int kStagesC = 3;
@@ -1142,9 +1143,12 @@ __global__ void __launch_bounds__(NT, 1) ln_bwd_cluster_kernel(
             for (int j = 0; j < 2 * kRowsB; ++j) st_cluster_f32(ra + 4 * j, s[j]);
             mbar_arrive_remote(mapa_u32(smem_u32(&inbar[slot]), p));
         }
-        if (threadIdx.x == 0 && i >= 1 && i + 2 < n && width > 0) {
-            fence_proxy_async_smem();  // stage of tile i-1 is free: tile i+2
-            issue(i + 2, (i - 1) % kStagesC);
+        // phase_a(i) runs in iteration i-1, BEFORE B(i-1): the stage that is
+        // free here is tile i-2's (read by B(i-2) in the previous iteration;
+        // the block barrier above orders every thread's reads of it) -> tile i+1
+        if (threadIdx.x == 0 && i >= 2 && i + 1 < n && width > 0) {
+            fence_proxy_async_smem();
+            issue(i + 1, (i - 2) % kStagesC);
         }
     };
     float rs_nx[kRowsB];

@@ -118,12 +118,15 @@ def test_concurrent_layernorm_backwards_on_two_streams(tops, cuda):
                 assert torch.equal(a, b)
 
 
-def test_sharded_layernorm_backward(tops, cuda):
+@pytest.mark.parametrize("rows,cols", [(4096, 1024), (1024, 4096)])
+def test_sharded_layernorm_backward(tops, cuda, rows, cols):
     """Row shards + the fused exchange == the unsharded backward: dx bit for
     bit, dgamma/dbeta identical on every rank and equal to the single-GPU
-    values up to the summation order (fp64 partials, one float rounding)."""
+    values up to the summation order (fp64 partials, one float rounding).
+    cols = 4096: stage 1 is the thread-block-cluster kernel (its partial rows
+    = co-resident clusters) feeding the same fused exchange."""
     import torch
-    rows, cols, world = 4096, 1024, 2
+    world = 2
     g = np.random.default_rng(7)
     x = torch.from_numpy(g.standard_normal((rows, cols)).astype(np.float32)).to(cuda)
     gam = torch.from_numpy((1 + 0.2 * g.standard_normal(cols)).astype(np.float32)).to(cuda)
@@ -136,10 +139,39 @@ def test_sharded_layernorm_backward(tops, cuda):
     from paper_2210_10246_b200.dist import shard_rows
     streams = [torch.cuda.Stream() for _ in range(world)]
     outs = []
-    for r, st in zip(ranks, streams):
-        b, e = shard_rows(rows, r.rank, world)
-        with torch.cuda.stream(st):
-            outs.append((b, e) + tops.layernorm_ip_bwd_peer(dy[b:e], y[b:e], rstd[b:e], gam, bet, r))
+    if cols <= 2048:
+        for r, st in zip(ranks, streams):
+            b, e = shard_rows(rows, r.rank, world)
+            with torch.cuda.stream(st):
+                outs.append((b, e) + tops.layernorm_ip_bwd_peer(dy[b:e], y[b:e], rstd[b:e], gam,
+                                                                 bet, r))
+    else:
+        # The simulated ranks share ONE GPU: a rank's exchange kernel, spinning
+        # for its peer, can hold the registers the peer's 512-thread cluster
+        # stage 1 needs (on separate GPUs each rank's stage 1 precedes its own
+        # exchange).  So here: stage 1 of every rank (tempo_ln_ip_bwd_partials,
+        # the cluster kernel), then the fused exchange of every rank on the
+        # partial rows -- the same two kernels tempo_ln_ip_bwd_peer runs.
+        import ctypes as C
+        from paper_2210_10246_b200._capi import lib
+        parts = []
+        for r, st in zip(ranks, streams):
+            b, e = shard_rows(rows, r.rank, world)
+            nb = int(lib().tempo_ln_ip_bwd_workspace_size(e - b, cols))
+            ws = torch.empty(nb, dtype=torch.uint8, device=cuda)
+            dx = torch.empty(e - b, cols, device=cuda)
+            npart = C.c_int64()
+            with torch.cuda.stream(st):
+                assert lib().tempo_ln_ip_bwd_partials(
+                    dy[b:e].data_ptr(), y[b:e].data_ptr(), rstd[b:e].data_ptr(), gam.data_ptr(),
+                    bet.data_ptr(), dx.data_ptr(), ws.data_ptr(), nb, e - b, cols,
+                    C.byref(npart), st.cuda_stream) == 0
+            parts.append((b, e, dx, ws.view(torch.float64)[: npart.value * 2 * cols]
+                          .view(npart.value, 2 * cols)))
+        torch.cuda.synchronize()
+        for r, st, (b, e, dx, pr) in zip(ranks, streams, parts):
+            with torch.cuda.stream(st):
+                outs.append((b, e, dx) + tops.ln_param_reduce_peer(pr, cols, r))
     torch.cuda.synchronize()
     for r in ranks:
         r.check_status()
