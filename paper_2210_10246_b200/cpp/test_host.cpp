@@ -165,8 +165,13 @@ static void test_layernorm() {
 
 // Wide rows take the TMA (cp.async.bulk) kernels: warp-per-row forward,
 // CTA-per-row backward with the two-stage dgamma/dbeta reduction.
+static void layernorm_wide_case(std::int64_t m);
 static void test_layernorm_wide() {
-    const std::int64_t rows = 37, m = 1024;
+    layernorm_wide_case(1024);  // the TMA warp / vector kernels
+    layernorm_wide_case(4096);  // the row-group forward, the cluster backward
+}
+static void layernorm_wide_case(std::int64_t m) {
+    const std::int64_t rows = 37;
     std::vector<float> xh = randn(rows * m, 21), gam = randn(m, 22, 0.2), bet = randn(m, 23, 0.1),
                        gh = randn(rows * m, 24);
     for (auto& v : gam) v += 1.0f;
