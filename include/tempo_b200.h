@@ -94,6 +94,15 @@ int tempo_gelu_table_eval_host(tempo_gelu_table_t table, const double* y, const 
  * Refuses a NULL/empty table (ConfigError, ops_tempo.cpp:91-94). */
 int tempo_gelu_ip_fwd(const float* x, float* y, uint32_t* mask, int64_t n,
                       tempo_gelu_table_t table, tempo_stream_t stream);
+/* Reference-exact mode of the forward: y = float(x*0.5*erfc(-x/sqrt2))
+ * evaluated in fp64 for EVERY element (math.hpp:17-28, one rounding) instead
+ * of the fp32 fast path -- the survey's <= 2-ulp contract with room (it
+ * differs from the reference only where CUDA's and glibc's double erfc
+ * straddle a float rounding boundary), at several times the FP64 cost (the
+ * default forward is <= 6 ulp, 14x inside the 1e-5 relative contract).  Same
+ * mask bits, same stash, same backward. */
+int tempo_gelu_ip_fwd_exact(const float* x, float* y, uint32_t* mask, int64_t n,
+                            tempo_gelu_table_t table, tempo_stream_t stream);
 /* Backward closure (ops_tempo.cpp:59-68 + gelu_spec :79-85):
  * dx = dy * table.eval(y, m).  Refuses an unverified table with ConfigError
  * (ops_tempo.cpp:80-83).  dx may alias dy (in place). */

@@ -49,6 +49,7 @@ SIGNATURES = {
     "tempo_gelu_default_table_v1": (C.c_char_p, []),
     "tempo_gelu_table_eval_host": (C.c_int, [_vp, _vp, _vp, _vp, _i64]),
     "tempo_gelu_ip_fwd": (C.c_int, [_vp, _vp, _vp, _i64, _vp, _vp]),
+    "tempo_gelu_ip_fwd_exact": (C.c_int, [_vp, _vp, _vp, _i64, _vp, _vp]),
     "tempo_gelu_ip_bwd": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _i64, _vp]),
     "tempo_ln_ip_fwd": (C.c_int, [_vp, _vp, _vp, _dbl, _vp, _vp, _i64, _i64, _vp, _vp]),
     "tempo_ln_check_gamma": (C.c_int, [_vp, _i64, _vp]),

@@ -519,6 +519,15 @@ int tempo_gelu_ip_fwd(const float* x, float* y, uint32_t* mask, int64_t n,
                        "tempo_gelu_ip_fwd");
 }
 
+int tempo_gelu_ip_fwd_exact(const float* x, float* y, uint32_t* mask, int64_t n,
+                            tempo_gelu_table_t table, tempo_stream_t stream) {
+    if (!table) return fail(TEMPO_ERR_CONFIG, "in-place gelu needs a fitted table");
+    if (int rc = check_n(n, "gelu")) return rc;
+    if (n > 0 && (!x || !y || !mask)) return fail(TEMPO_ERR_PARAM, "gelu: null tensor pointer");
+    return cuda_status(tb::launch_gelu_fwd_exact(x, y, mask, n, table->dev.xstar_gt, S(stream)),
+                       "tempo_gelu_ip_fwd_exact");
+}
+
 int tempo_gelu_ip_bwd(const float* dy, const float* y, const uint32_t* mask,
                       tempo_gelu_table_t table, float* dx, int64_t n, tempo_stream_t stream) {
     if (!table) return fail(TEMPO_ERR_CONFIG, "in-place gelu needs a fitted table");

@@ -203,6 +203,51 @@ __global__ void __launch_bounds__(kBlock) gelu_fwd_scalar_kernel(const float* __
     gelu_fwd_scalar_words(x, y, mask, n, xstar_gt, xs_lo, warp, nwarps, lane);
 }
 
+// ---- forward, reference-exact mode ----------------------------------------
+// y = float(x * 0.5 * erfc(-x / sqrt2)) evaluated in fp64 for EVERY element --
+// the reference's own formula (math.hpp:17-28, one rounding to float) instead
+// of the fp32 fast path (<= 6 ulp): the survey's <= 2 ulp contract is met
+// with room (the only differences from the reference are the rare inputs
+// where CUDA's and glibc's double erfc straddle a float rounding boundary).
+// Same lanes and mask bytes as gelu_fwd8_kernel (the mask bit is the sign
+// bit of xs_lo - x); the fp64 erfc makes it FP64-pipe bound.
+// vec = 0 (pointers not 32-byte aligned): every element takes the word loop.
+__global__ void __launch_bounds__(kBlock) gelu_fwd_exact_kernel(const float* __restrict__ x,
+                                                                float* __restrict__ y,
+                                                                uint32_t* __restrict__ mask,
+                                                                int64_t n, float xstar_gt,
+                                                                float xs_lo, int vec) {
+    grid_dep_wait();  // PDL: predecessor complete and visible
+    grid_dep_launch();
+    const int lane = threadIdx.x & 31;
+    uint8_t* mask8 = reinterpret_cast<uint8_t*>(mask);
+    const int64_t warp = ((int64_t)blockIdx.x * kBlock + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * kBlock) >> 5;
+    const int64_t nchunks = vec ? n >> 8 : 0;
+    for (int64_t c = warp; c < nchunks; c += nwarps) {
+        const F8 v = ld_stream8(x + (c << 8) + 8 * lane);
+        F8 o;
+        uint32_t mb = 0;
+#pragma unroll
+        for (int k = 7; k >= 0; --k) {
+            o.v[k] = (float)tm_gelu_exact(v.v[k]);
+            mb = push_sign(mb, xs_lo - v.v[k]);  // x > x*  <=>  x > xs_lo (NaN -> 0)
+        }
+        st_stream8(y + (c << 8) + 8 * lane, o);
+        st_stream(mask8 + (c << 5) + lane, mb);
+    }
+    // the rest by mask words [8*nchunks, ceil(n/32)), one word per warp step
+    const int64_t nwords = (n + 31) >> 5;
+    for (int64_t w = (nchunks << 3) + warp; w < nwords; w += nwarps) {
+        const int64_t i = (w << 5) + lane;
+        const bool in = i < n;
+        const float xv = in ? x[i] : 0.0f;
+        const uint32_t bits = __ballot_sync(kFull, in && xv >= xstar_gt);
+        if (in) y[i] = (float)tm_gelu_exact(xv);
+        if (lane == 0) mask[w] = bits;
+    }
+}
+
 // --------------------------------------------------------------- backward
 // Shared-memory copy of the table: per-segment parameters and the padded
 // coefficient matrix with an odd stride, so lanes on different segments
@@ -629,6 +674,18 @@ cudaError_t launch_gelu_fwd(const float* x, float* y, uint32_t* mask, int64_t n,
                             (((n + 31) >> 5) * 32 + kBlock - 1) / kBlock);
         launch(gelu_fwd_scalar_kernel, grid, kBlock, 0, st)(x, y, mask, n, xstar_gt, xs_lo);
     }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_gelu_fwd_exact(const float* x, float* y, uint32_t* mask, int64_t n,
+                                  float xstar_gt, cudaStream_t st) {
+    if (n == 0) return cudaSuccess;
+    const float xs_lo = std::nextafter(xstar_gt, -std::numeric_limits<float>::infinity());
+    const int vec = aligned32(x) && aligned32(y) && aligned16(mask);
+    const int64_t warps_needed = vec ? (n >> 8) + 1 : (n + 31) >> 5;
+    int grid = grid_for((const void*)gelu_fwd_exact_kernel, kBlock, 0,
+                        (warps_needed * 32 + kBlock - 1) / kBlock, 0, 4);
+    launch(gelu_fwd_exact_kernel, grid, kBlock, 0, st)(x, y, mask, n, xstar_gt, xs_lo, vec);
     return cudaGetLastError();
 }
 

@@ -48,6 +48,9 @@ struct GeluDevTable {
 };
 
 // Kernel launchers (defined in the .cu files; return cudaGetLastError()).
+// reference-exact forward: the fp64 formula for every element
+cudaError_t launch_gelu_fwd_exact(const float* x, float* y, uint32_t* mask, int64_t n,
+                                  float xstar_gt, cudaStream_t st);
 cudaError_t launch_gelu_fwd(const float* x, float* y, uint32_t* mask, int64_t n, float xstar_gt,
                             cudaStream_t st);
 cudaError_t launch_gelu_bwd(const float* dy, const float* y, const uint32_t* mask,

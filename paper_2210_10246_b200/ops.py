@@ -157,15 +157,17 @@ class GeluTable:
 # In-Place GELU (tempo_ops::gelu, ops_tempo.cpp:89-96)
 # --------------------------------------------------------------------------
 def gelu_ip_fwd(x: torch.Tensor, table: GeluTable, y: torch.Tensor = None,
-                mask: torch.Tensor = None):
-    """Returns (y, mask_bits).  Stash = y + mask (the input is not kept)."""
+                mask: torch.Tensor = None, exact: bool = False):
+    """Returns (y, mask_bits).  Stash = y + mask (the input is not kept).
+    exact=True: the reference formula in fp64 for every element
+    (tempo_gelu_ip_fwd_exact, <= 2 ulp) instead of the fp32 fast path."""
     if table is None:
         raise TempoError(5, "in-place gelu needs a fitted table")
     x = _f32(x, "x")
     y = _out(y, "y", x)
     mask = _mask(mask, "mask", x.numel(), x.device)
-    check(lib().tempo_gelu_ip_fwd(_ptr(x), _ptr(y), _ptr(mask), x.numel(), table.handle,
-                                  _stream()))
+    fn = lib().tempo_gelu_ip_fwd_exact if exact else lib().tempo_gelu_ip_fwd
+    check(fn(_ptr(x), _ptr(y), _ptr(mask), x.numel(), table.handle, _stream()))
     return y, mask
 
 

@@ -64,6 +64,37 @@ def gelu_inputs(n, seed):
     return x
 
 
+@pytest.mark.parametrize("n,shift", [(1, 0), (31, 0), (129, 0), (4101, 0), (1024 * 3072, 0),
+                                     (4101, 1), (70000, 3)])
+def test_gelu_forward_exact(tops, port, table_text, cuda, n, shift):
+    """The reference-exact forward (tempo_gelu_ip_fwd_exact: the reference's
+    fp64 formula for every element) against the oracle (the same formula with
+    glibc's erfc): <= 1 ulp, in practice bitwise (CUDA's and glibc's double
+    erfc agree to ~1 double ulp); mask bit-exact; unaligned views (shift)
+    take the word loop."""
+    import torch
+    table = tops.GeluTable(table_text)
+    x = gelu_inputs(n + shift, n)
+    xt = to_dev(x, cuda)[shift:]
+    y, mask = tops.gelu_ip_fwd(xt, table, exact=True)
+    torch.cuda.synchronize()
+    xs = x[shift:]
+    ry, rm = port.gelu_fwd(xs, table.info()["x_star"])
+    assert np.array_equal(unpack(mask, n), rm)
+    yg = y.cpu().numpy()
+    assert np.array_equal(np.isnan(yg), np.isnan(ry))
+    fin = np.isfinite(ry)
+    d = ulp_diff(yg[fin], ry[fin])
+    assert d.max(initial=0) <= 1
+    assert (d > 0).mean() <= 1e-5 if d.size > 10000 else True
+    # the backward of the exact forward's stash, as for the fast one
+    dy = np.random.default_rng(n).standard_normal(n).astype(np.float32)
+    dx = tops.gelu_ip_bwd(to_dev(dy, cuda), y, mask, table)
+    torch.cuda.synchronize()
+    pt = port.table(table_text)
+    assert rel_err(dx.cpu().numpy(), pt.gelu_bwd(dy, ry, rm)) <= 1e-5
+
+
 @pytest.mark.parametrize("n", [1, 31, 32, 127, 128, 129, 1000, 4101, 1024 * 3072])
 def test_gelu_forward(tops, port, table_text, cuda, n):
     import torch

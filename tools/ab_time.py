@@ -43,6 +43,7 @@ def main():
         "softmax_dropout_fwd": (lambda: o.softmax_dropout_fwd(c.z, bench.P_DROP, mask=c.m_att, generate=True, seed=7, P=c.P, D=c.D), [c.P, c.D, c.m_att]),
         "attn_probs_bwd": (lambda: o.attn_probs_bwd(c.dD, c.P, c.m_att, bench.P_DROP, write_d=True, dZ=c.dZ, D=c.Drec), [c.dZ, c.Drec]),
         "gelu_fwd": (lambda: o.gelu_ip_fwd(c.x_ffn1, c.table, y=c.y_g, mask=c.m_g), [c.y_g, c.m_g]),
+        "gelu_fwd_exact": (lambda: o.gelu_ip_fwd(c.x_ffn1, c.table, y=c.y_g, mask=c.m_g, exact=True), [c.y_g, c.m_g]),
         "gelu_bwd": (lambda: o.gelu_ip_bwd(c.dy_gelu, c.y_g, c.m_g, c.table, dx=c.dx_g), [c.dx_g]),
         "ln_fwd": (lambda: o.layernorm_ip_fwd(c.d1, c.g1, c.b1, check_gamma=False, y=c.y_ln1, rstd=c.rs1), [c.y_ln1, c.rs1]),
         "ln_bwd": (lambda: o.layernorm_ip_bwd(c.dy_ln1, c.y_ln1, c.rs1, c.g1, c.b1, dx=c.dx_ln1, dgamma=dp[:H], dbeta=dp[H:2 * H], workspace=c.ws), [c.dx_ln1, dp[:2 * H]]),
@@ -88,7 +89,7 @@ def main():
     ob["mt_mask"] = c.z.numel() / 8
     ob["mt_mask_h"] = c.x_ffn2.numel() / 8
     ob["copy_h"] = 2 * 8 * c.x_ffn2.numel()
-    names = {"ln_fwd": "layernorm_fwd", "ln_bwd": "layernorm_bwd"}
+    names = {"ln_fwd": "layernorm_fwd", "ln_bwd": "layernorm_bwd", "gelu_fwd_exact": "gelu_fwd"}
     reps = int(os.environ.get("REPS", "20"))
     st = torch.cuda.current_stream()
     for name in sys.argv[1:]:
