@@ -1237,19 +1237,34 @@ __global__ void __launch_bounds__(NT, 1) ln_bwd_cluster_kernel(
     // DSMEM access can target an exited CTA
 }
 
-#ifndef TM_LN_CLUSTER_NT
-#define TM_LN_CLUSTER_NT 512
+// CTA size of the cluster backward: 256 threads (1024 columns per CTA, two
+// CTAs per SM) while K <= 8 covers the row, 512 beyond (A/B with the
+// decoupled exchange: H = 4096 / 8192 at 0.56 / 0.50 vs 0.53 / 0.48)
+#ifndef TM_LN_CLUSTER_NT_MAX
+#define TM_LN_CLUSTER_NT_MAX 512
 #endif
-constexpr int kClusterNT = TM_LN_CLUSTER_NT;
+inline int cluster_nt(int64_t cols) {
+    return cols <= 8 * 4 * 256 ? 256 : TM_LN_CLUSTER_NT_MAX;
+}
 // cluster size and slice width for a long row: K = ceil(cols / (4*NT)), the
 // slice rounded up to a multiple of 4 columns
-inline int cluster_k(int64_t cols) { return (int)((cols + 4 * kClusterNT - 1) / (4 * kClusterNT)); }
+inline int cluster_k(int64_t cols) {
+    const int nt = cluster_nt(cols);
+    return (int)((cols + 4 * nt - 1) / (4 * nt));
+}
 inline int cluster_sw(int64_t cols) {
     const int k = cluster_k(cols);
     return (int)(((cols + k - 1) / k + 3) / 4 * 4);
 }
 size_t bwd_cluster_smem(int64_t cols) {
     return 128 + (size_t)kStagesC * 2 * kRowsB * cluster_sw(cols) * sizeof(float);
+}
+const void* bwd_cluster_fn(int64_t cols, bool drop) {
+    if (cluster_nt(cols) == 256)
+        return drop ? (const void*)ln_bwd_cluster_kernel<256, true>
+                    : (const void*)ln_bwd_cluster_kernel<256, false>;
+    return drop ? (const void*)ln_bwd_cluster_kernel<512, true>
+                : (const void*)ln_bwd_cluster_kernel<512, false>;
 }
 
 // Stage 2: out[j] = sum over CTAs c (fixed order) of ws[c][j], j < 2*cols.
@@ -1454,9 +1469,10 @@ int bwd_cluster_grid(int64_t rows, int64_t cols) {
     static std::map<std::pair<int, int64_t>, int> cache;  // (device, cols) -> max active clusters
     const int k = cluster_k(cols);
     const int64_t ntiles = (rows + kRowsB - 1) / kRowsB;
-    const void* kf = (const void*)ln_bwd_cluster_kernel<kClusterNT, false>;
+    const void* kf = bwd_cluster_fn(cols, false);
+    const int nt = cluster_nt(cols);
     const size_t smem = bwd_cluster_smem(cols);
-    (void)grid_for(kf, kClusterNT, smem, 1);  // dynamic smem opt-in
+    (void)grid_for(kf, nt, smem, 1);  // dynamic smem opt-in
     int dev = 0;
     cudaGetDevice(&dev);
     int maxcl = 0;
@@ -1468,7 +1484,7 @@ int bwd_cluster_grid(int64_t rows, int64_t cols) {
         } else {
             cudaLaunchConfig_t cfg = {};
             cfg.gridDim = dim3((unsigned)(k * 148));
-            cfg.blockDim = dim3((unsigned)kClusterNT);
+            cfg.blockDim = dim3((unsigned)nt);
             cfg.dynamicSmemBytes = smem;
             cudaLaunchAttribute attr[1];
             attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -1637,10 +1653,14 @@ cudaError_t launch_ln_bwd(const float* dy, const float* y, const float* rstd, co
     double* w = static_cast<double*>(ws);
     if (clu) {
         const int k = cluster_k(cols);
-        auto kf = drop ? ln_bwd_cluster_kernel<kClusterNT, true> : ln_bwd_cluster_kernel<kClusterNT, false>;
+        using KFn = void (*)(const float*, const float*, const float*, const float*,
+                             const float*, float*, double*, int64_t, int, int, const uint32_t*,
+                             double, float*);
+        KFn kf = reinterpret_cast<KFn>(const_cast<void*>(bwd_cluster_fn(cols, drop)));
+        const int nt = cluster_nt(cols);
         const size_t smem = bwd_cluster_smem(cols);
-        (void)grid_for((const void*)kf, kClusterNT, smem, grid * k);  // smem opt-in
-        cudaError_t e = launch(kf, grid * k, kClusterNT, smem, st)
+        (void)grid_for((const void*)kf, nt, smem, grid * k);  // smem opt-in
+        cudaError_t e = launch(kf, grid * k, nt, smem, st)
                             .cluster((unsigned)k)(dy, y, rstd, gamma, beta, dx, w, rows, (int)cols,
                                                   cluster_sw(cols), mask, scale, dproj);
         if (e != cudaSuccess) return e;
