@@ -11,7 +11,7 @@ O=gpurun_out/${R}_sanitizer
 mkdir -p $O
 CS="compute-sanitizer --error-exitcode 9"
 timeout 1800 $CS --tool memcheck python -m pytest tests/test_gpu_parity.py tests/test_mt_jump.py \
-    -m gpu -q -x > $O/pytest_parity_memcheck.log 2>&1
+    tests/test_gpu_peer.py -m gpu -q -x > $O/pytest_parity_memcheck.log 2>&1
 # round 2: the long-row kernels (TMA row groups, the cluster LN backward with
 # its DSMEM exchange), the fused dropout -> add -> LN and the tcgen05 dV GEMM
 timeout 1800 $CS --tool memcheck python -m pytest tests/test_gpu_long_rows.py \
