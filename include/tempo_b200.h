@@ -283,6 +283,18 @@ int tempo_dropout_bwd(const float* dy, const uint32_t* mask, double p, float* dx
 int tempo_attn_dropout_dv(const float* P, const uint32_t* mask, double p, const float* dO,
                           float* dV, int64_t heads, int64_t s_q, int64_t s_k, int64_t d,
                           tempo_stream_t stream);
+/* The FORWARD consumer of the recomputed map: ctx = D @ V per (batch, head),
+ * D = keep ? P/(1-p) : 0 rebuilt inside a tcgen05 (3xTF32) GEMM from P and
+ * the mask -- tempo_ops::sdpa's matmul(dropout_recompute(probs), v)
+ * (ops_tempo.cpp:196-210) without D in HBM: pair with
+ * tempo_softmax_dropout_fwd(..., D = NULL), so the forward writes P and the
+ * bits only.  P: [heads][s_q][s_k], V: [heads][s_k][d], ctx: [heads][s_q][d],
+ * fp32, within 1e-6 relative of the fp64 product.  Needs s_k % 32 == 0,
+ * d in {32, 64} (else TEMPO_ERR_UNSUPPORTED), 16-byte aligned
+ * P, V, ctx. */
+int tempo_attn_dropout_ctx(const float* P, const uint32_t* mask, double p, const float* V,
+                           float* ctx, int64_t heads, int64_t s_q, int64_t s_k, int64_t d,
+                           tempo_stream_t stream);
 
 /* ---------------------------------------------------------------------- */
 /* Hidden dropout -> residual add -> In-Place LayerNorm, fused             */

@@ -81,6 +81,7 @@ SIGNATURES = {
     "tempo_ln_param_reduce": (C.c_int, [_vp, _i64, _i64, _vp, _vp, _vp]),
     "tempo_dropout_fwd": (C.c_int, [_vp, _dbl, C.c_int, _vp, _u64, _u64, _vp, _i64, _vp]),
     "tempo_attn_dropout_dv": (C.c_int, [_vp, _vp, _dbl, _vp, _vp, _i64, _i64, _i64, _i64, _vp]),
+    "tempo_attn_dropout_ctx": (C.c_int, [_vp, _vp, _dbl, _vp, _vp, _i64, _i64, _i64, _i64, _vp]),
     "tempo_dropout_add_ln_fwd": (C.c_int, [_vp, _vp, _dbl, C.c_int, _vp, _u64, _u64, _vp, _vp,
                                            _dbl, _vp, _vp, _i64, _i64, _vp, _vp]),
     "tempo_dropout_add_ln_bwd": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _dbl, _vp, _vp, _vp,

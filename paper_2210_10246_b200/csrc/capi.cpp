@@ -851,6 +851,25 @@ int tempo_attn_probs_bwd(const float* dD, const float* P, const uint32_t* mask, 
 }
 
 // ---- dropout -------------------------------------------------------------------
+int tempo_attn_dropout_ctx(const float* P, const uint32_t* mask, double p, const float* V,
+                           float* ctx, int64_t heads, int64_t s_q, int64_t s_k, int64_t d,
+                           tempo_stream_t stream) {
+    if (heads < 0 || s_q < 0 || s_k < 0 || d < 0)
+        return fail(TEMPO_ERR_DIMENSION, "attn_dropout_ctx: negative shape");
+    if (int rc = check_p(p)) return rc;
+    if (heads == 0) return TEMPO_OK;
+    if (!tb::ctx_gemm_supported(s_q, s_k, d))
+        return fail(TEMPO_ERR_UNSUPPORTED,
+                    "attn_dropout_ctx needs s_k % 32 == 0 and d in {32, 64}; "
+                    "use tempo_softmax_dropout_fwd with D and a GEMM");
+    if (!P || !mask || !V || !ctx) return fail(TEMPO_ERR_PARAM, "attn_dropout_ctx: null pointer");
+    if (((uintptr_t)P | (uintptr_t)V | (uintptr_t)ctx) & 15u)
+        return fail(TEMPO_ERR_ALIGNMENT, "attn_dropout_ctx: P, V and ctx must be 16-byte aligned");
+    return cuda_status(tb::launch_ctx_recompute_gemm(P, mask, 1.0 / (1.0 - p), V, ctx, heads, s_q,
+                                                     s_k, d, S(stream)),
+                       "tempo_attn_dropout_ctx");
+}
+
 int tempo_attn_dropout_dv(const float* P, const uint32_t* mask, double p, const float* dO,
                           float* dV, int64_t heads, int64_t s_q, int64_t s_k, int64_t d,
                           tempo_stream_t stream) {

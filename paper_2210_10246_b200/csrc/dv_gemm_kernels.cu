@@ -649,7 +649,8 @@ PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
 
 // 2D row-major tensor [rows][cols] of 4-byte elements, box [box_rows][box_cols]
 bool make_tmap_2d(CUtensorMap* map, CUtensorMapDataType dt, const void* ptr, uint64_t rows,
-                  uint64_t cols, uint32_t box_rows, uint32_t box_cols) {
+                  uint64_t cols, uint32_t box_rows, uint32_t box_cols,
+                  CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_NONE) {
     auto enc = tmap_encoder();
     if (!enc) return false;
     const cuuint64_t dims[2] = {cols, rows};
@@ -657,7 +658,7 @@ bool make_tmap_2d(CUtensorMap* map, CUtensorMapDataType dt, const void* ptr, uin
     const cuuint32_t box[2] = {box_cols, box_rows};
     const cuuint32_t estr[2] = {1, 1};
     return enc(map, dt, 2, const_cast<void*>(ptr), dims, strides, box, estr,
-               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
@@ -681,7 +682,269 @@ cudaError_t launch_dv_staged(const float* P, const uint32_t* mask, double scale,
     return cudaGetLastError();
 }
 
+// ---- the FORWARD consumer: ctx = D @ V with D rebuilt from P + mask -------
+// The attention forward's consumer of the dropped-out map (tempo_ops::sdpa,
+// ops_tempo.cpp:196-210: matmul(dropout_recompute(probs), v)) as one tcgen05
+// GEMM that never reads D: per (head, 128-query block), ctx[i, c] = (1/(1-p))
+// * sum_j keep[i, j] P[i, j] V[j, c] -- M = s_q (i), N = d (c), K = s_k (j).
+// Here P's rows are already K-major, so the loader's 2D TMA stages each
+// 256 x 16 P tile with SWIZZLE_64B, which IS the UMMA K-major SWIZZLE_64B
+// operand layout: the producers split every element in place (select on the
+// keep bit, 3xTF32 hi/lo) at the same smem offset, vectorised and
+// conflict-free; only V (row-major [j][c], MN-major) is transposed by the
+// producers, as dO is in the dV GEMM.  (A first version with 128-row CTAs and
+// 32-column SWIZZLE_128B slices took 0.53 ms at BERT-large: each head's V was
+// read by four CTAs.)  With the dV GEMM, D exists in neither
+// pass: the softmax forward writes P and the mask bits only (8.125 B/elem
+// instead of 12.125).
+constexpr int kCM = 256;        // query rows per CTA (two M = 128 accumulators)
+constexpr int kCK = 16;         // key columns per slice (64-byte operand rows, SWIZZLE_64B)
+constexpr int kCSP = 512;       // 16 producer warps: 2 per query row
+constexpr int kCThreads = kCSP + 64;
+
+template <int N>
+struct CtxCfg {
+    static constexpr int kSS = 4, kOS = 3;
+    static constexpr int kPbytes = kCM * kCK * 4;   // 16 KB, swizzled
+    static constexpr int kVbytes = kCK * N * 4;     // 4 KB (N = 64)
+    static constexpr int kSlice = kPbytes + kVbytes;
+    static constexpr int kAbytes = kCM * kCK * 4;
+    static constexpr int kBbytes = N * kCK * 4;
+    static constexpr int kOpStage = 2 * kAbytes + 2 * kBbytes;
+    static constexpr size_t kSmem = 1024 + (size_t)kOS * kOpStage + (size_t)kSS * kSlice;
+    static_assert(kSmem <= 227 * 1024, "smem");
+};
+
+template <int N>
+__global__ void __launch_bounds__(kCThreads, 1) ctx_recompute_gemm_kernel(
+    const __grid_constant__ CUtensorMap tm_p, const __grid_constant__ CUtensorMap tm_v,
+    const uint32_t* __restrict__ mask, double scale, float* __restrict__ ctx, int s_q, int s_k) {
+    using Cfg = CtxCfg<N>;
+    constexpr int kSets = 512 / (2 * N) >= 4 ? 4 : 512 / (2 * N);
+    constexpr int kTmemCols = kSets * 2 * N;
+    constexpr int kSS = Cfg::kSS, kOS = Cfg::kOS;
+    grid_dep_wait();
+    grid_dep_launch();
+    extern __shared__ __align__(1024) unsigned char gsm[];
+    const uint32_t base = (smem_u32(gsm) + 1023u) & ~1023u;
+    const uint32_t stage_base = base + kOS * Cfg::kOpStage;
+    unsigned char* stage_ptr = gsm + (stage_base - smem_u32(gsm));
+    __shared__ uint64_t full[kOS], empty[kOS], acc_full, sfull[kSS], sempty[kSS];
+    __shared__ uint32_t tmem_base_sh;
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int iblocks = (s_q + kCM - 1) / kCM;  // a ragged last block: rows >= s_q are
+    const int64_t head = blockIdx.x / iblocks;  // computed on the next head's (or zero-
+    const int i0 = (blockIdx.x % iblocks) * kCM;  // filled) P rows and not stored
+    const int nsl = s_k / kCK;
+    constexpr int kMMAWarp = kCSP / 32, kLoadWarp = kCSP / 32 + 1;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kOS; ++s) {
+            mbar_init(&full[s], kCSP / 32);
+            mbar_init(&empty[s], 1);
+        }
+        for (int s = 0; s < kSS; ++s) {
+            mbar_init(&sfull[s], 1);
+            mbar_init(&sempty[s], kCSP / 32);
+        }
+        mbar_init(&acc_full, 1);
+        mbar_fence_init();
+    }
+    if (warp == kMMAWarp) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         smem_u32(&tmem_base_sh)),
+                     "n"(kTmemCols)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = tmem_base_sh;
+
+    if (warp < kMMAWarp) {
+        // ---------------- producers ----------------
+        // A: thread t owns query row m = t % 256 and the two 16-byte K-chunks
+        //    2h, 2h+1 (h = t / 256) of the slice, at the same swizzled offset
+        //    in staging and operand.
+        // B: thread t owns V column n = t % N, K-rows kq*KV..+KV-1.
+        const int t = threadIdx.x;
+        const int m = t % kCM, h = t / kCM;
+        constexpr int kKV = kCK * N / kCSP;  // V values per thread per slice (2 for N = 64)
+        static_assert(kKV == 1 || kKV == 2, "V chunk");
+        const int bn = t % N, bk = (t / N) * kKV;
+        const bool row_in = i0 + m < s_q;
+        const uint32_t* mrow = mask + (((head * (int64_t)s_q + i0 + m) * s_k) >> 5);
+        uint32_t w = 0;
+        for (int sl = 0; sl < nsl; ++sl) {
+            const int ss = sl % kSS, s = sl % kOS;
+            if ((sl & 1) == 0) w = row_in ? __ldg(mrow + (sl >> 1)) : 0u;  // columns 32*(sl/2) ..
+            mbar_wait(&sfull[ss], (uint32_t)((sl / kSS) & 1));
+            const uint32_t sp = stage_base + ss * Cfg::kSlice;
+            float4 pv[2];
+#pragma unroll
+            for (int c = 0; c < 2; ++c)
+                asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
+                             : "=f"(pv[c].x), "=f"(pv[c].y), "=f"(pv[c].z), "=f"(pv[c].w)
+                             : "r"(sp + sw64_k_offset(m, 2 * h + c)));
+            float ov[kKV];
+#pragma unroll
+            for (int k = 0; k < kKV; ++k)
+                ov[k] = lds32(sp + Cfg::kPbytes + (uint32_t)(((bk + k) * N + bn) * 4));
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&sempty[ss]);
+            if (sl >= kOS) mbar_wait(&empty[s], (uint32_t)(((sl / kOS) + 1) & 1));
+            const uint32_t a_hi = base + s * Cfg::kOpStage, a_lo = a_hi + Cfg::kAbytes;
+            const uint32_t b_hi = a_lo + Cfg::kAbytes, b_lo = b_hi + Cfg::kBbytes;
+            const uint32_t wsl = w >> (16 * (sl & 1));  // this slice's 16 keep bits
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+                const float e[4] = {pv[c].x, pv[c].y, pv[c].z, pv[c].w};
+                float hi[4], lo[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int k = 4 * (2 * h + c) + u;  // column 16*sl + k
+                    const float d = ((wsl >> k) & 1u) ? e[u] : 0.0f;
+                    hi[u] = tf32_rna(d);
+                    lo[u] = isfinite(d) ? tf32_rna_finite(d - hi[u]) : d - hi[u];
+                }
+                const uint32_t off = sw64_k_offset(m, 2 * h + c);
+                sts128(a_hi + off, hi[0], hi[1], hi[2], hi[3]);
+                sts128(a_lo + off, lo[0], lo[1], lo[2], lo[3]);
+            }
+            {
+                float hi[kKV], lo[kKV];
+#pragma unroll
+                for (int u = 0; u < kKV; ++u) {
+                    hi[u] = tf32_rna(ov[u]);
+                    lo[u] = isfinite(ov[u]) ? tf32_rna_finite(ov[u] - hi[u]) : ov[u] - hi[u];
+                }
+                const uint32_t off = sw64_k_offset(bn, bk >> 2) + (uint32_t)((bk & 3) * 4);
+                if (kKV == 2) {
+                    sts64(b_hi + off, hi[0], hi[kKV - 1]);
+                    sts64(b_lo + off, lo[0], lo[kKV - 1]);
+                } else {
+                    sts32(b_hi + off, hi[0]);
+                    sts32(b_lo + off, lo[0]);
+                }
+            }
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&full[s]);
+        }
+        // ---------------- epilogue: ctx = (1/(1-p)) * sum of the sets ------
+        mbar_wait(&acc_full, 0);
+        tc_fence_after();
+        const int quad = warp % 4, mb = (warp / 4) % 2, half = warp / 8;
+        const int row = i0 + mb * 128 + quad * 32 + lane;
+        float* out = ctx + (head * (int64_t)s_q + row) * N;
+        const float sc = (float)scale;
+        const bool store = row < s_q;
+#pragma unroll
+        for (int c0 = half * (N / 2); c0 < (half + 1) * (N / 2); c0 += 16) {
+            float v[16];
+            const uint32_t ta = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(mb * N + c0);
+            tmem_ld16(ta, v);
+#pragma unroll
+            for (int set = 1; set < kSets; ++set) {
+                float wv[16];
+                tmem_ld16(ta + (uint32_t)(set * 2 * N), wv);
+#pragma unroll
+                for (int i = 0; i < 16; ++i) v[i] += wv[i];
+            }
+            if (store) {  // (the tcgen05.ld above stays warp-uniform)
+#pragma unroll
+                for (int i = 0; i < 16; i += 4)
+                    st_stream(reinterpret_cast<float4*>(out + c0 + i),
+                              make_float4(v[i] * sc, v[i + 1] * sc, v[i + 2] * sc, v[i + 3] * sc));
+            }
+        }
+    } else if (warp == kMMAWarp && lane == 0) {
+        // ---------------- MMA issuer ----------------
+        constexpr uint32_t idesc = idesc_tf32_k(128, N);
+        for (int sl = 0; sl < nsl; ++sl) {
+            const int s = sl % kOS;
+            mbar_wait(&full[s], (uint32_t)((sl / kOS) & 1));
+            tc_fence_after();
+            const uint32_t a_hi = base + s * Cfg::kOpStage, a_lo = a_hi + Cfg::kAbytes;
+            const uint32_t b_hi = a_lo + Cfg::kAbytes, b_lo = b_hi + Cfg::kBbytes;
+#pragma unroll
+            for (int kk = 0; kk < kCK / 8; ++kk) {  // K = 8 per MMA: +32 bytes along 64-byte rows
+                const uint64_t bh = umma_desc_sw64(b_hi + kk * 32, 512);
+                const uint64_t bl = umma_desc_sw64(b_lo + kk * 32, 512);
+                const int gk = sl * (kCK / 8) + kk;
+                const int set = gk % kSets;
+#pragma unroll
+                for (int mb = 0; mb < 2; ++mb) {
+                    const uint32_t ao = mb * 128 * 64 + kk * 32;  // 128 rows x 64 B per M-block
+                    const uint64_t ah = umma_desc_sw64(a_hi + ao, 512);
+                    const uint64_t al = umma_desc_sw64(a_lo + ao, 512);
+                    const uint32_t acc = tmem + (uint32_t)(set * 2 * N + mb * N);
+                    mma_tf32(acc, al, bh, idesc, gk >= kSets);  // small terms first
+                    mma_tf32(acc, ah, bl, idesc, 1);
+                    mma_tf32(acc, ah, bh, idesc, 1);
+                }
+            }
+            mma_commit(&empty[s]);
+        }
+        mma_commit(&acc_full);
+    } else if (warp == kLoadWarp && lane == 0) {
+        // ---------------- loader: the P tile (swizzled) and the V rows ------
+        const int y_p = (int)(head * s_q + i0), y_v0 = (int)(head * s_k);
+        for (int sl = 0; sl < nsl; ++sl) {
+            const int ss = sl % kSS;
+            if (sl >= kSS) mbar_wait(&sempty[ss], (uint32_t)(((sl / kSS) + 1) & 1));
+            unsigned char* sp = stage_ptr + ss * Cfg::kSlice;
+            mbar_expect_tx(&sfull[ss], Cfg::kSlice);
+            tma_load_2d(sp, &tm_p, sl * kCK, y_p, &sfull[ss]);
+            tma_load_2d(sp + Cfg::kPbytes, &tm_v, 0, y_v0 + sl * kCK, &sfull[ss]);
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (warp == kMMAWarp) {
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                     "n"(kTmemCols)
+                     : "memory");
+    }
+}
+
+template <int N>
+cudaError_t launch_ctx(const float* P, const uint32_t* mask, double scale, const float* V,
+                       float* ctx, int64_t heads, int64_t s_q, int64_t s_k, cudaStream_t st) {
+    CUtensorMap tp, tv;
+    if (!make_tmap_2d(&tp, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, P, (uint64_t)(heads * s_q),
+                      (uint64_t)s_k, kCM, kCK, CU_TENSOR_MAP_SWIZZLE_64B) ||
+        !make_tmap_2d(&tv, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, V, (uint64_t)(heads * s_k),
+                      (uint64_t)N, kCK, N))
+        return cudaErrorNotSupported;
+    auto k = ctx_recompute_gemm_kernel<N>;
+    const size_t smem = CtxCfg<N>::kSmem;
+    (void)grid_for((const void*)k, kCThreads, smem, 1);
+    const int64_t grid = heads * ((s_q + kCM - 1) / kCM);
+    launch(k, (int)grid, kCThreads, smem, st)(tp, tv, mask, scale, ctx, (int)s_q, (int)s_k);
+    return cudaGetLastError();
+}
+
 }  // namespace
+
+bool ctx_gemm_supported(int64_t s_q, int64_t s_k, int64_t d) {
+    return s_q > 0 && s_k > 0 && s_k % 32 == 0 && (d == 32 || d == 64) &&
+           s_q <= (1 << 20) && s_k <= (1 << 20);
+}
+
+cudaError_t launch_ctx_recompute_gemm(const float* P, const uint32_t* mask, double scale,
+                                      const float* V, float* ctx, int64_t heads, int64_t s_q,
+                                      int64_t s_k, int64_t d, cudaStream_t st) {
+    if (heads == 0) return cudaSuccess;
+    switch (d) {
+        case 32: return launch_ctx<32>(P, mask, scale, V, ctx, heads, s_q, s_k, st);
+        case 64: return launch_ctx<64>(P, mask, scale, V, ctx, heads, s_q, s_k, st);
+        default: return cudaErrorInvalidValue;
+    }
+}
 
 bool dv_gemm_supported(int64_t s_q, int64_t s_k, int64_t d) {
     return s_q > 0 && s_k > 0 && s_q % kBK == 0 && s_k % kBM == 0 && (d == 32 || d == 64 || d == 128) &&

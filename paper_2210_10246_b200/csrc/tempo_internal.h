@@ -107,6 +107,11 @@ cudaError_t launch_attn_probs_bwd(const float* dD, const float* P, const uint32_
 // dV = D^T dO with D rebuilt from P and the mask in the GEMM's operand
 // staging (dv_gemm_kernels.cu; tcgen05, 3xTF32)
 bool dv_gemm_supported(int64_t s_q, int64_t s_k, int64_t d);
+// the forward consumer: ctx = dropout(P) @ V, D rebuilt inside the tcgen05 GEMM
+bool ctx_gemm_supported(int64_t s_q, int64_t s_k, int64_t d);
+cudaError_t launch_ctx_recompute_gemm(const float* P, const uint32_t* mask, double scale,
+                                      const float* V, float* ctx, int64_t heads, int64_t s_q,
+                                      int64_t s_k, int64_t d, cudaStream_t st);
 cudaError_t launch_dv_recompute_gemm(const float* P, const uint32_t* mask, double scale,
                                      const float* dO, float* dV, int64_t heads, int64_t s_q,
                                      int64_t s_k, int64_t d, cudaStream_t st);

@@ -22,7 +22,7 @@ import torch
 from ._capi import MASK_PHILOX, MASK_SUPPLIED, TempoError, check, lib
 
 __all__ = [
-    "GeluTable", "TempoError", "gelu_ip_fwd", "gelu_ip_bwd", "layernorm_ip_fwd",
+    "GeluTable", "TempoError", "gelu_ip_fwd", "gelu_ip_bwd", "layernorm_ip_fwd", "attn_dropout_ctx",
     "layernorm_ip_bwd", "ln_check_gamma", "softmax_ip_fwd", "softmax_ip_bwd",
     "softmax_dropout_fwd", "attn_probs_bwd", "dropout_fwd", "dropout_bwd", "mask_words",
     "pack_mask", "unpack_mask", "bernoulli_keep_bits", "bernoulli_keep_bits_device",
@@ -551,6 +551,35 @@ def attn_dropout_dv(P: torch.Tensor, mask: torch.Tensor, p: float, dO: torch.Ten
     check(lib().tempo_attn_dropout_dv(_ptr(P), _ptr(mask), float(p), _ptr(dO), _ptr(dV), heads,
                                       s_q, s_k, d, _stream()))
     return dV
+
+
+def attn_dropout_ctx(P: torch.Tensor, mask: torch.Tensor, p: float, V: torch.Tensor,
+                     ctx: torch.Tensor = None) -> torch.Tensor:
+    """ctx = D @ V per (batch, head) with D = mask ? P/(1-p) : 0 rebuilt inside
+    the tcgen05 GEMM (the forward consumer of Sub-Layer Dropout
+    Recomputation, tempo_ops::sdpa ops_tempo.cpp:196-210): with
+    softmax_dropout_fwd(..., write_d=False) D never reaches HBM.
+    P [..., s_q, s_k], V [..., s_k, d] -> ctx [..., s_q, d]."""
+    P = _f32(P, "P")
+    if P.dim() < 2:
+        raise TempoError(2, "P: expected [..., s_q, s_k]")
+    s_q, s_k = P.shape[-2], P.shape[-1]
+    heads = P.numel() // max(1, s_q * s_k)
+    V = _f32(V, "V", P.device)
+    if V.dim() != P.dim() or V.shape[:-2] != P.shape[:-2] or V.shape[-2] != s_k:
+        raise TempoError(2, f"V {tuple(V.shape)} does not match P {tuple(P.shape)}")
+    d = V.shape[-1]
+    if mask is None:
+        raise TempoError(2, "mask: the forward's bit mask is required")
+    mask = _mask(mask, "mask", P.numel(), P.device)
+    shape = tuple(P.shape[:-1]) + (d,)
+    if ctx is None:
+        ctx = torch.empty(shape, dtype=torch.float32, device=P.device)
+    else:
+        _f32(ctx, "ctx", P.device, heads * s_q * d)
+    check(lib().tempo_attn_dropout_ctx(_ptr(P), _ptr(mask), float(p), _ptr(V), _ptr(ctx), heads,
+                                       s_q, s_k, d, _stream()))
+    return ctx
 
 
 def dropout_add_layernorm_fwd(proj: torch.Tensor, residual: torch.Tensor, gamma: torch.Tensor,

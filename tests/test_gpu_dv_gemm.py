@@ -90,3 +90,63 @@ def test_umma_probe_layouts():
     out = subprocess.run([exe], capture_output=True, text=True, timeout=120).stdout
     lines = {int(l.split()[1]): l for l in out.splitlines() if l.startswith("variant")}
     assert "max|err|=0 " in lines[0]
+
+
+# ------------------------------------------------ the forward consumer (ctx)
+@pytest.mark.parametrize("heads,s_q,s_k,d,p", [(3, 512, 512, 64, 0.1), (2, 512, 512, 32, 0.1),
+                                               (1, 128, 32, 64, 0.5), (5, 384, 256, 64, 0.0),
+                                               (2, 256, 1024, 64, 0.1), (1, 128, 96, 32, 0.3),
+                                               (3, 100, 64, 64, 0.1), (2, 300, 128, 32, 0.2)])
+def test_ctx_matches_oracle_composition(tops, port, cuda, heads, s_q, s_k, d, p):
+    """tempo_attn_dropout_ctx: ctx = D @ V with D rebuilt inside the tcgen05
+    GEMM (P's tile staged with TMA SWIZZLE_128B = the K-major operand layout)
+    against the oracle composition dropout_apply -> fp64 D @ V."""
+    import torch
+    g = np.random.default_rng(heads * s_q + s_k + d)
+    z = g.standard_normal((heads, s_q, s_k)) * 2
+    P = np.exp(z - z.max(-1, keepdims=True))
+    P = (P / P.sum(-1, keepdims=True)).astype(np.float32)
+    V = g.standard_normal((heads, s_k, d)).astype(np.float32)
+    keep = (g.random(heads * s_q * s_k) >= p).astype(np.uint8)
+    ctx = tops.attn_dropout_ctx(to_dev(P, cuda), bits_to_dev(pack(keep), cuda), p, to_dev(V, cuda))
+    torch.cuda.synchronize()
+    D = port.dropout_apply(P.reshape(-1), keep, p).reshape(P.shape).astype(np.float64)
+    ref = np.einsum("hij,hjc->hic", D, V.astype(np.float64))
+    mag = np.einsum("hij,hjc->hic", np.abs(D), np.abs(V.astype(np.float64)))
+    got = ctx.cpu().numpy().astype(np.float64)
+    assert rel_err(got, ref.astype(np.float32)) <= 1e-5
+    assert np.all(np.abs(got - ref) <= 1e-5 * (np.abs(ref) + mag))
+
+
+def test_ctx_equals_materialised_d_gemm(tops, cuda):
+    """The D-free forward (softmax_dropout_fwd without D + the fused ctx GEMM)
+    against the materialised path (the forward's D + an fp32 cuBLAS GEMM)."""
+    import torch
+    heads, s, d, p = 4, 512, 64, 0.1
+    g = torch.Generator(device=cuda)
+    g.manual_seed(12)
+    z = torch.randn(heads * s, s, device=cuda, generator=g)
+    P, D, m = tops.softmax_dropout_fwd(z, p, seed=4)
+    P2, none, m2 = tops.softmax_dropout_fwd(z, p, seed=4, write_d=False)
+    V = torch.randn(heads, s, d, device=cuda, generator=g)
+    ctx = tops.attn_dropout_ctx(P2.view(heads, s, s), m2, p, V)
+    prev = torch.backends.cuda.matmul.allow_tf32
+    torch.backends.cuda.matmul.allow_tf32 = False
+    try:
+        ref = torch.matmul(D.view(heads, s, s), V)
+    finally:
+        torch.backends.cuda.matmul.allow_tf32 = prev
+    torch.cuda.synchronize()
+    assert none is None and torch.equal(P, P2) and torch.equal(m, m2)
+    assert rel_err(ctx.cpu().numpy(), ref.cpu().numpy()) <= 1e-5
+
+
+def test_ctx_refusals(tops, cuda):
+    import torch
+    from paper_2210_10246_b200 import TempoError
+    P = torch.rand(1, 100, 48, device=cuda)
+    V = torch.rand(1, 48, 64, device=cuda)
+    m = torch.zeros(100 * 48 // 32 + 1, dtype=torch.int32, device=cuda)
+    with pytest.raises(TempoError) as e:
+        tops.attn_dropout_ctx(P, m, 0.1, V)  # s_k % 32 != 0
+    assert e.value.kind == "Unsupported"

@@ -70,6 +70,20 @@ def main():
         o.attn_probs_bwd(c.dD, c.P, c.m_att, bench.P_DROP, write_d=False, dZ=c.dZ)
         o.attn_dropout_dv(c.P.view(heads, bench.S, bench.S), c.m_att, bench.P_DROP, dO, dV=dV)
 
+    ctx = torch.empty(heads, bench.S, 64, device=dev)
+
+    def ctx_unfused():  # D written by the softmax forward, then an fp32 cuBLAS GEMM
+        o.softmax_dropout_fwd(c.z, bench.P_DROP, mask=c.m_att, generate=True, seed=7, P=c.P, D=c.D)
+        torch.matmul(c.D.view(heads, bench.S, bench.S), dO, out=ctx)
+
+    def ctx_fused():  # no D: P + bits, then the tcgen05 GEMM rebuilds D
+        o.softmax_dropout_fwd(c.z, bench.P_DROP, mask=c.m_att, generate=True, seed=7, P=c.P,
+                              write_d=False)
+        o.attn_dropout_ctx(c.P.view(heads, bench.S, bench.S), c.m_att, bench.P_DROP, dO, ctx=ctx)
+
+    calls["ctx_unfused"] = (ctx_unfused, [ctx])
+    calls["ctx_fused"] = (ctx_fused, [ctx])
+    calls["ctx_gemm_only"] = (lambda: o.attn_dropout_ctx(c.P.view(heads, bench.S, bench.S), c.m_att, bench.P_DROP, dO, ctx=ctx), [ctx])
     calls["dv_unfused"] = (dv_unfused, [dV])
     calls["dv_fused"] = (dv_fused, [dV])
     calls["dv_gemm_only"] = (lambda: o.attn_dropout_dv(c.P.view(heads, bench.S, bench.S), c.m_att, bench.P_DROP, dO, dV=dV), [dV])
@@ -82,6 +96,9 @@ def main():
     ob["dv_gemm_only"] = n_a * 4.125 + dO.numel() * 8
     ob["cublas_dv_only"] = n_a * 4 + dO.numel() * 8
     ob["attn_bwd_noD"] = n_a * 12.125
+    ob["ctx_unfused"] = n_a * 12.125 + n_a * 4 + dO.numel() * 8
+    ob["ctx_fused"] = n_a * 8.125 + n_a * 4.125 + dO.numel() * 8
+    ob["ctx_gemm_only"] = n_a * 4.125 + dO.numel() * 8
     obf = bench.op_bytes(fused=True)
     ob["dal_fwd"] = obf["dropout_add_layernorm_fwd"]
     ob["dal_bwd"] = obf["dropout_add_layernorm_bwd"]
