@@ -638,6 +638,30 @@ def row_length_timings(dev, peak, reps=10):
     return out
 
 
+def _time_cases(torch, cases, peak, reps, flush):
+    """Device time of each {name: (fn, algorithmic bytes)} case: CUDA events on
+    the current stream, L2 read-flushed before each rep, trimmed mean."""
+    st = torch.cuda.current_stream()
+    out = {}
+    for name, (fn, nbytes) in cases.items():
+        fn()
+        ts = []
+        for _ in range(reps):
+            if flush is not None:
+                flush()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(st)
+            fn()
+            b.record(st)
+            b.synchronize()
+            ts.append(a.elapsed_time(b))
+        t_ms = trimmed_mean(ts)
+        gbs = nbytes / (t_ms * 1e-3) / 1e9
+        out[name] = {"ms": round(t_ms, 4), "bytes": int(nbytes), "gbs": round(gbs, 1),
+                     "frac": round(gbs / peak, 4)}
+    return out
+
+
 def dv_consumer_timings(chain, peak, reps=11, flush=None):
     """the attention-probability backward plus the
     consumer of the dropped-out map D, the dV GEMM (dV = D^T dO per head,
@@ -655,8 +679,6 @@ def dv_consumer_timings(chain, peak, reps=11, flush=None):
     dO = torch.randn(heads, S, 64, device=dev, generator=g)
     dV = torch.empty(heads, S, 64, device=dev)
     P3 = chain.P.view(heads, S, S)
-    prev = torch.backends.cuda.matmul.allow_tf32
-    torch.backends.cuda.matmul.allow_tf32 = False
 
     def unfused():
         o.attn_probs_bwd(chain.dD, chain.P, chain.m_att, P_DROP, write_d=True, dZ=chain.dZ,
@@ -675,30 +697,63 @@ def dv_consumer_timings(chain, peak, reps=11, flush=None):
     cases = {"unfused": (unfused, n_a * (16 + 1 / 8) + n_a * 4 + 2 * nb_o),
              "fused": (fused, n_a * (12 + 1 / 8) + n_a * (4 + 1 / 8) + 2 * nb_o),
              "dv_gemm_only": (gemm_only, n_a * (4 + 1 / 8) + 2 * nb_o)}
-    st = torch.cuda.current_stream()
-    out = {}
+    prev = torch.backends.cuda.matmul.allow_tf32
+    torch.backends.cuda.matmul.allow_tf32 = False
     try:
-        for name, (fn, nbytes) in cases.items():
-            fn()
-            ts = []
-            for _ in range(reps):
-                if flush is not None:
-                    flush()
-                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                a.record(st)
-                fn()
-                b.record(st)
-                b.synchronize()
-                ts.append(a.elapsed_time(b))
-            t_ms = trimmed_mean(ts)
-            gbs = nbytes / (t_ms * 1e-3) / 1e9
-            out[name] = {"ms": round(t_ms, 4), "bytes": int(nbytes), "gbs": round(gbs, 1),
-                         "frac": round(gbs / peak, 4)}
+        out = _time_cases(torch, cases, peak, reps, flush)
     finally:
         torch.backends.cuda.matmul.allow_tf32 = prev
     out["speedup_fused_vs_unfused"] = round(out["unfused"]["ms"] / out["fused"]["ms"], 3)
     out["what"] = ("attn_probs_bwd + dV = D^T dO (d=64): D written + fp32 cuBLAS GEMM vs "
                    "D rebuilt inside the tcgen05 3xTF32 GEMM (tempo_attn_dropout_dv)")
+    return out
+
+
+def ctx_consumer_timings(chain, peak, reps=11, flush=None):
+    """The forward side of the same fusion: softmax + dropout forward plus the
+    consumer of D, ctx = D @ V per head (d = 64), at the configs[3] shape:
+      unfused: softmax_dropout_fwd writes P and D (12.125 B/elem), then an
+               fp32 cuBLAS GEMM reads D (TF32 off);
+      fused:   softmax_dropout_fwd without D (8.125 B/elem), then
+               tempo_attn_dropout_ctx rebuilds D from P + mask inside its
+               tcgen05 3xTF32 GEMM (4.125 B/elem + V + ctx).
+    The mask is regenerated (Philox, seed 7) by each forward, as in the
+    bench step's breakdown."""
+    torch, o = chain.torch, chain.ops
+    heads, dev = chain.batch * A, chain.dev
+    g = torch.Generator(device=dev)
+    g.manual_seed(98)
+    V = torch.randn(heads, S, 64, device=dev, generator=g)
+    ctx = torch.empty(heads, S, 64, device=dev)
+    P3 = chain.P.view(heads, S, S)
+
+    def unfused():
+        o.softmax_dropout_fwd(chain.z, P_DROP, mask=chain.m_att, generate=True, seed=7,
+                              P=chain.P, D=chain.D)
+        torch.matmul(chain.D.view(heads, S, S), V, out=ctx)
+
+    def fused():
+        o.softmax_dropout_fwd(chain.z, P_DROP, mask=chain.m_att, generate=True, seed=7,
+                              P=chain.P, write_d=False)
+        o.attn_dropout_ctx(P3, chain.m_att, P_DROP, V, ctx=ctx)
+
+    def gemm_only():
+        o.attn_dropout_ctx(P3, chain.m_att, P_DROP, V, ctx=ctx)
+
+    n_a = chain.P.numel()
+    nb_v = V.numel() * 4
+    cases = {"unfused": (unfused, n_a * (12 + 1 / 8) + n_a * 4 + 2 * nb_v),
+             "fused": (fused, n_a * (8 + 1 / 8) + n_a * (4 + 1 / 8) + 2 * nb_v),
+             "ctx_gemm_only": (gemm_only, n_a * (4 + 1 / 8) + 2 * nb_v)}
+    prev = torch.backends.cuda.matmul.allow_tf32
+    torch.backends.cuda.matmul.allow_tf32 = False
+    try:
+        out = _time_cases(torch, cases, peak, reps, flush)
+    finally:
+        torch.backends.cuda.matmul.allow_tf32 = prev
+    out["speedup_fused_vs_unfused"] = round(out["unfused"]["ms"] / out["fused"]["ms"], 3)
+    out["what"] = ("softmax_dropout_fwd + ctx = D V (d=64): D written + fp32 cuBLAS GEMM vs "
+                   "D rebuilt inside the tcgen05 3xTF32 GEMM (tempo_attn_dropout_ctx)")
     return out
 
 
@@ -1052,6 +1107,12 @@ def main():
             dv_consumer = dv_consumer_timings(chain, peak, flush=flush)
         except Exception as ex:  # noqa: BLE001  (report, do not fail the bench)
             dv_consumer = {"unavailable": str(ex)[:200]}
+    ctx_consumer = None
+    if rank == 0:
+        try:
+            ctx_consumer = ctx_consumer_timings(chain, peak, flush=flush)
+        except Exception as ex:  # noqa: BLE001  (report, do not fail the bench)
+            ctx_consumer = {"unavailable": str(ex)[:200]}
 
     # ---- the reference mask stream on the device (outside the timed region) --
     ref_mask = None
@@ -1146,6 +1207,7 @@ def main():
             "per_config": per_config,
             "per_row_length": per_row_length,
             "dv_consumer": dv_consumer,
+            "ctx_consumer": ctx_consumer,
             "frac_of_peak": round(value / world / peak, 4),
             "unfused_equivalent": ({
                 "what": "the same step's work as separate ops incl. the residual adds "
