@@ -68,6 +68,10 @@ constexpr int kThreadsG = kProducers + 32;
 // (bit 12) and clearing the 13 low bits IS that rounding for finite values;
 // inf/NaN keep their bits (a NaN payload could carry into the sign).  The
 // split's low part x - hi is always finite and small, so it skips the check.
+#ifndef TM_DV_SPLIT
+#define TM_DV_SPLIT 1
+#endif
+#if !TM_DV_SPLIT
 __device__ __forceinline__ float tf32_rna(float x) {
 #if TM_DV_FAST_RNA
     const uint32_t u = __float_as_uint(x);
@@ -84,6 +88,25 @@ __device__ __forceinline__ float tf32_rna_finite(float x) {  // x finite
     return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xffffe000u);
 #else
     return tf32_rna(x);
+#endif
+}
+#endif
+
+// 3xTF32 operand split x = hi + lo.  hi = x rounded to TF32 (nearest, ties
+// away: the integer form, which keeps +-inf and turns a NaN into a NaN or, for
+// a NaN with the top mantissa bits set, -0 -- its lo is then NaN, so NaN still
+// propagates through the hi*lo products); lo = x - hi is exact and left
+// unrounded: the tensor core reads the top 19 bits of an fp32 TF32 operand,
+// so lo is truncated there (error < 2^-21 |x| per element, vs 2^-22 with a
+// rounded lo) at 3 instructions instead of ~10.  TM_DV_SPLIT=0: both parts
+// rounded with the inf/NaN guards.
+__device__ __forceinline__ void split_tf32(float x, float& hi, float& lo) {
+#if TM_DV_SPLIT
+    hi = __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xffffe000u);
+    lo = x - hi;
+#else
+    hi = tf32_rna(x);
+    lo = isfinite(x) ? tf32_rna_finite(x - hi) : x - hi;
 #endif
 }
 
@@ -245,8 +268,7 @@ __global__ void __launch_bounds__(kThreadsG, 1) dv_recompute_gemm_kernel(
                     const uint32_t w = __shfl_sync(kFull, mword, k);
                     // D exactly as dropout_apply / the forward's D (one fp64 rounding)
                     const float d = ((w >> lane) & 1u) ? (float)((double)pv[k] * scale) : 0.0f;
-                    hi[u] = tf32_rna(d);
-                    lo[u] = isfinite(d) ? tf32_rna_finite(d - hi[u]) : d - hi[u];
+                    split_tf32(d, hi[u], lo[u]);
                 }
                 const uint32_t off = sw128_k_offset(t, q);
                 *reinterpret_cast<float4*>(a_hi + off) = make_float4(hi[0], hi[1], hi[2], hi[3]);
@@ -258,8 +280,7 @@ __global__ void __launch_bounds__(kThreadsG, 1) dv_recompute_gemm_kernel(
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
                     const float o = ov[4 * q + u];
-                    hi[u] = tf32_rna(o);
-                    lo[u] = isfinite(o) ? tf32_rna_finite(o - hi[u]) : o - hi[u];
+                    split_tf32(o, hi[u], lo[u]);
                 }
                 const uint32_t off = sw128_k_offset(bn, (bk0 >> 2) + q);
                 *reinterpret_cast<float4*>(b_hi + off) = make_float4(hi[0], hi[1], hi[2], hi[3]);
@@ -508,8 +529,7 @@ __global__ void __launch_bounds__(2 * BM + 64, BM == 256 ? 1 : 2) dv_recompute_g
                 for (int u = 0; u < 4; ++u) {
                     const int k = 4 * q + u;
                     const float d = ((w[k] >> lane) & 1u) ? pv[k] : 0.0f;
-                    hi[u] = tf32_rna(d);
-                    lo[u] = isfinite(d) ? tf32_rna_finite(d - hi[u]) : d - hi[u];
+                    split_tf32(d, hi[u], lo[u]);
                 }
                 const uint32_t off = sw64_k_offset(m, kh * 2 + q);
                 sts128(a_hi + off, hi[0], hi[1], hi[2], hi[3]);
@@ -519,8 +539,7 @@ __global__ void __launch_bounds__(2 * BM + 64, BM == 256 ? 1 : 2) dv_recompute_g
                 float hi[kOPT], lo[kOPT];
 #pragma unroll
                 for (int u = 0; u < kOPT; ++u) {
-                    hi[u] = tf32_rna(ov[u]);
-                    lo[u] = isfinite(ov[u]) ? tf32_rna_finite(ov[u] - hi[u]) : ov[u] - hi[u];
+                    split_tf32(ov[u], hi[u], lo[u]);
                 }
                 const uint32_t off = sw64_k_offset(bn, bk >> 2) + (uint32_t)((bk & 3) * 4);
                 if (kOPT == 4) {
@@ -776,10 +795,15 @@ __global__ void __launch_bounds__(kCThreads, 1) ctx_recompute_gemm_kernel(
         const int bn = t % N, bk = (t / N) * kKV;
         const bool row_in = i0 + m < s_q;
         const uint32_t* mrow = mask + (((head * (int64_t)s_q + i0 + m) * s_k) >> 5);
-        uint32_t w = 0;
+        // the mask word of columns 32*(sl/2).. serves two slices; the next
+        // one is loaded a slice pair ahead (a per-row word: 32 sectors/warp)
+        uint32_t w = 0, w_next = row_in ? __ldg(mrow) : 0u;
         for (int sl = 0; sl < nsl; ++sl) {
             const int ss = sl % kSS, s = sl % kOS;
-            if ((sl & 1) == 0) w = row_in ? __ldg(mrow + (sl >> 1)) : 0u;  // columns 32*(sl/2) ..
+            if ((sl & 1) == 0) {
+                w = w_next;
+                if (row_in && sl + 2 < nsl) w_next = __ldg(mrow + (sl >> 1) + 1);
+            }
             mbar_wait(&sfull[ss], (uint32_t)((sl / kSS) & 1));
             const uint32_t sp = stage_base + ss * Cfg::kSlice;
             float4 pv[2];
@@ -806,8 +830,7 @@ __global__ void __launch_bounds__(kCThreads, 1) ctx_recompute_gemm_kernel(
                 for (int u = 0; u < 4; ++u) {
                     const int k = 4 * (2 * h + c) + u;  // column 16*sl + k
                     const float d = ((wsl >> k) & 1u) ? e[u] : 0.0f;
-                    hi[u] = tf32_rna(d);
-                    lo[u] = isfinite(d) ? tf32_rna_finite(d - hi[u]) : d - hi[u];
+                    split_tf32(d, hi[u], lo[u]);
                 }
                 const uint32_t off = sw64_k_offset(m, 2 * h + c);
                 sts128(a_hi + off, hi[0], hi[1], hi[2], hi[3]);
@@ -817,8 +840,7 @@ __global__ void __launch_bounds__(kCThreads, 1) ctx_recompute_gemm_kernel(
                 float hi[kKV], lo[kKV];
 #pragma unroll
                 for (int u = 0; u < kKV; ++u) {
-                    hi[u] = tf32_rna(ov[u]);
-                    lo[u] = isfinite(ov[u]) ? tf32_rna_finite(ov[u] - hi[u]) : ov[u] - hi[u];
+                    split_tf32(ov[u], hi[u], lo[u]);
                 }
                 const uint32_t off = sw64_k_offset(bn, bk >> 2) + (uint32_t)((bk & 3) * 4);
                 if (kKV == 2) {

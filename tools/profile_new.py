@@ -3,7 +3,7 @@
 long-row softmax fwd/bwd (S = 2048, 3072), long-row LayerNorm fwd / cluster
 backward (H = 4096), the fused dropout -> add -> LN at H = 4096, the softmax
 forward with the in-kernel reference mask stream (2^28 elements) and the
-tcgen05 dV GEMM (BERT-large heads).  Every op runs once as a warm-up, then
+tcgen05 dV and ctx GEMMs (BERT-large heads).  Every op runs once as a warm-up, then
 once more inside the NVTX range "capture" (ncu --nvtx --nvtx-include
 "capture/" profiles only that pass)."""
 import os
@@ -55,6 +55,7 @@ def main():
     dO = torch.randn(64 * 16, S, 64, device=dev)
     dV = torch.empty(64 * 16, S, 64, device=dev)
     ops_list.append(lambda: ops.attn_dropout_dv(Pa.view(64 * 16, S, S), ma, p, dO, dV=dV))
+    ops_list.append(lambda: ops.attn_dropout_ctx(Pa.view(64 * 16, S, S), ma, p, dO, ctx=dV))
     for fn in ops_list:  # warm-up pass
         fn()
     torch.cuda.synchronize()
