@@ -933,17 +933,355 @@ __global__ void __launch_bounds__(kCThreads, 1) ctx_recompute_gemm_kernel(
     }
 }
 
+// ---- ctx with the A operand in TMEM ----------------------------------------
+// The producers above write every A element twice to shared memory (hi, lo),
+// fence the generic->async proxy per slice, and the MMA reads A back from smem
+// three times (al.bh, ah.bl, ah.bh): ~34 B of smem traffic per P element.
+// tcgen05.mma also takes A from TMEM (tests/tools/tmem_a_probe.cu: exact for
+// kind::tf32, lane = row, one column per K element), and a producer thread
+// owns one query row = one TMEM lane: it splits its 8 P values of the slice
+// and tcgen05.st's them (hi, lo: 8 columns each) straight into the A stage.
+// Only V's K-major B tile still goes through smem, written by warps 0-3 (the
+// only ones that fence the async proxy).  TMEM: kSets accumulator sets x 2
+// M-blocks x N columns + kAS A stages x 2 M-blocks x 32 columns = 512.
+#ifndef TM_CTX_TA
+#define TM_CTX_TA 1
+#endif
+#ifndef TM_CTX_TA_SS
+#define TM_CTX_TA_SS 4
+#endif
+#ifndef TM_CTX_TA_SETS
+#define TM_CTX_TA_SETS 2
+#endif
+#ifndef TM_CTX_TA_K
+#define TM_CTX_TA_K 32   // key columns per slice: 32 (SWIZZLE_128B) or 16 (SWIZZLE_64B)
+#endif
+#ifndef TM_CTX_DRAIN
+#define TM_CTX_DRAIN 8   // slices per drained segment of the drained instantiation
+#endif
+#ifndef TM_CTX_DRAIN_MIN_SK
+#define TM_CTX_DRAIN_MIN_SK 1024  // s_k above which the drained instantiation runs
+#endif
+#ifndef TM_CTX_DBG_NOMMA  // timing experiments only: issue no MMAs (producer-bound time)
+#define TM_CTX_DBG_NOMMA 0
+#endif
+#ifndef TM_CTX_TA_AS
+#define TM_CTX_TA_AS 2
+#endif
+#ifndef TM_CTX_A_FIRST
+#define TM_CTX_A_FIRST 1
+#endif
+template <int N, bool DRAIN>
+struct CtxTaCfg {
+    static constexpr int kTK = TM_CTX_TA_K;             // key columns per slice
+    static constexpr int kCh = kTK / 8;                 // 16-byte chunks per thread (2 per row half)
+    // kG > 0: the accumulation runs in segments of kG slices into two
+    // ping-pong TMEM accumulators; the producers drain each finished segment
+    // into fp32 registers (round-to-nearest adds), so the tensor core's
+    // truncating accumulation spans at most 3 * kTK/8 * kG products whatever
+    // s_k is.  kG = 0: kSets accumulator sets in rotation.
+    static constexpr int kG = DRAIN ? TM_CTX_DRAIN : 0;
+    static constexpr int kSets = kG > 0 ? 2 : (N == 64 ? TM_CTX_TA_SETS : 4);
+    static constexpr int kAcc = kSets * 2 * N;         // accumulator columns
+    static constexpr int kAcols = 2 * 2 * kTK;         // one A stage: 2 M-blocks x (hi, lo)
+    static constexpr int kASmax = (512 - kAcc) / kAcols > 4 ? 4 : (512 - kAcc) / kAcols;
+    static constexpr int kAS = TM_CTX_TA_AS < kASmax ? TM_CTX_TA_AS : kASmax;
+    static_assert(kAS >= 2, "TMEM columns");
+    // TMEM column map: A stages first, the accumulators at the top
+    static constexpr int kA0 = TM_CTX_A_FIRST ? 0 : kAcc;
+    static constexpr int kAcc0 = TM_CTX_A_FIRST ? 512 - kAcc : 0;
+    static constexpr int kSS = TM_CTX_TA_SS;
+    static constexpr int kPbytes = kCM * kTK * 4;      // 16 / 32 KB, swizzled
+    static constexpr int kVbytes = kTK * N * 4;
+    static constexpr int kSlice = kPbytes + kVbytes;
+    static constexpr int kBbytes = N * kTK * 4;
+    static constexpr int kOpStage = 2 * kBbytes;       // B hi, lo
+    static constexpr size_t kSmem = 1024 + (size_t)kAS * kOpStage + (size_t)kSS * kSlice;
+    static_assert(kSmem <= 227 * 1024, "smem");
+};
+
+__device__ __forceinline__ void mma_tf32_ta(uint32_t tmem_d, uint32_t tmem_a, uint64_t b,
+                                            uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+        "r"(tmem_a), "l"(b), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const float* v) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr),
+                 "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]),
+                 "f"(v[7])
+                 : "memory");
+}
+template <int TK>
+__device__ __forceinline__ uint32_t swz_k_offset(int mn, int kchunk) {
+    return TK == 32 ? sw128_k_offset(mn, kchunk) : sw64_k_offset(mn, kchunk);
+}
+template <int TK>
+__device__ __forceinline__ uint64_t umma_desc_k(uint32_t addr) {
+    return TK == 32 ? umma_desc_sw128(addr, 16, 1024) : umma_desc_sw64(addr, 512);
+}
+
+template <int N, bool DRAIN>
+__global__ void __launch_bounds__(kCThreads, 1) ctx_recompute_gemm_ta_kernel(
+    const __grid_constant__ CUtensorMap tm_p, const __grid_constant__ CUtensorMap tm_v,
+    const uint32_t* __restrict__ mask, double scale, float* __restrict__ ctx, int s_q, int s_k) {
+    using Cfg = CtxTaCfg<N, DRAIN>;
+    constexpr int kSets = Cfg::kSets, kSS = Cfg::kSS, kAS = Cfg::kAS, kG = Cfg::kG;
+    constexpr int kTK = Cfg::kTK, kCh = Cfg::kCh;
+    constexpr int kGd = kG > 0 ? kG : 1;  // (division-safe)
+    grid_dep_wait();
+    grid_dep_launch();
+    extern __shared__ __align__(1024) unsigned char gsm[];
+    const uint32_t base = (smem_u32(gsm) + 1023u) & ~1023u;
+    const uint32_t stage_base = base + kAS * Cfg::kOpStage;
+    unsigned char* stage_ptr = gsm + (stage_base - smem_u32(gsm));
+    __shared__ uint64_t full[kAS], empty[kAS], acc_full, sfull[kSS], sempty[kSS];
+    __shared__ uint64_t seg_full[2], seg_empty[2];  // kG > 0: segment accumulators
+    __shared__ uint32_t tmem_base_sh;
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int iblocks = (s_q + kCM - 1) / kCM;
+    const int64_t head = blockIdx.x / iblocks;
+    const int i0 = (blockIdx.x % iblocks) * kCM;
+    const int nsl = s_k / kTK;
+    constexpr int kMMAWarp = kCSP / 32, kLoadWarp = kCSP / 32 + 1;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kAS; ++s) {
+            mbar_init(&full[s], kCSP / 32);
+            mbar_init(&empty[s], 1);
+        }
+        for (int s = 0; s < kSS; ++s) {
+            mbar_init(&sfull[s], 1);
+            mbar_init(&sempty[s], kCSP / 32);
+        }
+        mbar_init(&acc_full, 1);
+        for (int g = 0; g < 2; ++g) {
+            mbar_init(&seg_full[g], 1);
+            mbar_init(&seg_empty[g], kCSP / 32);
+        }
+        mbar_fence_init();
+    }
+    if (warp == kMMAWarp) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                         smem_u32(&tmem_base_sh))
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = tmem_base_sh;
+
+    if (warp < kMMAWarp) {
+        // ---------------- producers ----------------
+        // A: thread t owns query row m = t % 256 (TMEM lane 32*(warp%4) + lane
+        //    of M-block m / 128) and the K columns h*kTK/2.. (h = t / 256).
+        // B: warps 0-3, thread t owns V column n = t % N, K-rows kb..kb+kKV-1.
+        const int t = threadIdx.x;
+        const int m = t % kCM, h = t / kCM, mb = m >> 7;
+        const bool bwarp = warp < 4;
+        constexpr int kKV = kTK * N / 128;  // 16 / 8 (N = 64) or 8 / 4
+        const int bn = t % N, kb = (t / N) * kKV;
+        const bool row_in = i0 + m < s_q;
+        const uint32_t lane_base = tmem + ((uint32_t)((warp & 3) * 32) << 16);
+        const uint32_t* mrow = mask + (((head * (int64_t)s_q + i0 + m) * s_k) >> 5);
+        constexpr int kSlPerWord = 32 / kTK;  // slices per mask word (2 or 1)
+        uint32_t w = 0, w_next = row_in ? __ldg(mrow) : 0u;
+        // segment drains (kG > 0): this thread's N/2 accumulator columns
+        const int quad = warp % 4, emb = (warp / 4) % 2, half = warp / 8;
+        const uint32_t acc_lane = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(Cfg::kAcc0 + emb * N + half * (N / 2));
+        float racc[N / 2];
+#pragma unroll
+        for (int i = 0; i < N / 2; ++i) racc[i] = 0.0f;
+        auto drain = [&](int j) {  // segment j: wait for its MMAs, add, free the buffer
+            mbar_wait(&seg_full[j & 1], (uint32_t)((j >> 1) & 1));
+            tc_fence_after();
+#pragma unroll
+            for (int c0 = 0; c0 < N / 2; c0 += 16) {
+                float v[16];
+                tmem_ld16(acc_lane + (uint32_t)((j & 1) * 2 * N + c0), v);
+#pragma unroll
+                for (int i = 0; i < 16; ++i) racc[c0 + i] += v[i];
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&seg_empty[j & 1]);
+        };
+        constexpr int kLag = 2;  // drain segment j while producing slice (j+1)*kG + kLag
+        int drained = 0;
+        for (int sl = 0; sl < nsl; ++sl) {
+            const int ss = sl % kSS, s = sl % kAS;
+            if (kG > 0 && sl >= kG + kLag && (sl - kLag) % kGd == 0) drain(drained++);
+            if (sl % kSlPerWord == 0) {
+                w = w_next;
+                if (row_in && sl + kSlPerWord < nsl) w_next = __ldg(mrow + sl / kSlPerWord + 1);
+            }
+            mbar_wait(&sfull[ss], (uint32_t)((sl / kSS) & 1));
+            const uint32_t sp = stage_base + ss * Cfg::kSlice;
+            float e[4 * kCh];
+#pragma unroll
+            for (int c = 0; c < kCh; ++c)
+                asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
+                             : "=f"(e[4 * c]), "=f"(e[4 * c + 1]), "=f"(e[4 * c + 2]), "=f"(e[4 * c + 3])
+                             : "r"(sp + swz_k_offset<kTK>(m, kCh * h + c)));
+            float ov[kKV];
+            if (bwarp) {
+#pragma unroll
+                for (int k = 0; k < kKV; ++k)
+                    ov[k] = lds32(sp + Cfg::kPbytes + (uint32_t)(((kb + k) * N + bn) * 4));
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&sempty[ss]);
+            if (sl >= kAS) mbar_wait(&empty[s], (uint32_t)(((sl / kAS) + 1) & 1));
+            tc_fence_after();
+            // this thread's keep bits: columns kTK*sl + h*kTK/2 ..
+            const uint32_t wsl = w >> (kTK * (sl % kSlPerWord) + (kTK / 2) * h);
+            float hi[4 * kCh], lo[4 * kCh];
+#pragma unroll
+            for (int k = 0; k < 4 * kCh; ++k) split_tf32(((wsl >> k) & 1u) ? e[k] : 0.0f, hi[k], lo[k]);
+            const uint32_t ta = lane_base + (uint32_t)(Cfg::kA0 + s * Cfg::kAcols + mb * 2 * kTK + (kTK / 2) * h);
+#pragma unroll
+            for (int c = 0; c < kCh / 2; ++c) {
+                tmem_st8(ta + 8 * c, hi + 8 * c);
+                tmem_st8(ta + kTK + 8 * c, lo + 8 * c);
+            }
+            if (bwarp) {
+                const uint32_t b_hi = base + s * Cfg::kOpStage, b_lo = b_hi + Cfg::kBbytes;
+                float bh[kKV], bl[kKV];
+#pragma unroll
+                for (int u = 0; u < kKV; ++u) split_tf32(ov[u], bh[u], bl[u]);
+#pragma unroll
+                for (int c = 0; c < kKV / 4; ++c) {
+                    const uint32_t off = swz_k_offset<kTK>(bn, (kb >> 2) + c);
+                    sts128(b_hi + off, bh[4 * c], bh[4 * c + 1], bh[4 * c + 2], bh[4 * c + 3]);
+                    sts128(b_lo + off, bl[4 * c], bl[4 * c + 1], bl[4 * c + 2], bl[4 * c + 3]);
+                }
+                fence_proxy_async_smem();
+            }
+            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&full[s]);
+        }
+        // ---------------- epilogue: ctx = (1/(1-p)) * the accumulation -----
+        const int row = i0 + emb * 128 + quad * 32 + lane;
+        float* out = ctx + (head * (int64_t)s_q + row) * N;
+        const float sc = (float)scale;
+        const bool store = row < s_q;
+        if (kG > 0) {
+            const int nseg = (nsl + kGd - 1) / kGd;
+            while (drained < nseg) drain(drained++);
+            if (store) {
+#pragma unroll
+                for (int i = 0; i < N / 2; i += 4)
+                    st_stream(reinterpret_cast<float4*>(out + half * (N / 2) + i),
+                              make_float4(racc[i] * sc, racc[i + 1] * sc, racc[i + 2] * sc,
+                                          racc[i + 3] * sc));
+            }
+        } else {
+            mbar_wait(&acc_full, 0);
+            tc_fence_after();
+#pragma unroll
+            for (int c0 = half * (N / 2); c0 < (half + 1) * (N / 2); c0 += 16) {
+                float v[16];
+                const uint32_t ta = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(Cfg::kAcc0 + emb * N + c0);
+                tmem_ld16(ta, v);
+#pragma unroll
+                for (int set = 1; set < kSets; ++set) {
+                    float wv[16];
+                    tmem_ld16(ta + (uint32_t)(set * 2 * N), wv);
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) v[i] += wv[i];
+                }
+                if (store) {
+#pragma unroll
+                    for (int i = 0; i < 16; i += 4)
+                        st_stream(reinterpret_cast<float4*>(out + c0 + i),
+                                  make_float4(v[i] * sc, v[i + 1] * sc, v[i + 2] * sc, v[i + 3] * sc));
+                }
+            }
+        }
+    } else if (warp == kMMAWarp && lane == 0) {
+        // ---------------- MMA issuer: A from TMEM, B from smem ----------
+        constexpr uint32_t idesc = idesc_tf32_k(128, N);
+        for (int sl = 0; sl < nsl; ++sl) {
+            const int s = sl % kAS;
+            const int seg = sl / kGd;
+            const bool seg_first = kG > 0 && sl % kGd == 0;
+            if (seg_first && seg >= 2) {  // the producers drained segment seg - 2
+                mbar_wait(&seg_empty[seg & 1], (uint32_t)(((seg >> 1) + 1) & 1));
+            }
+            mbar_wait(&full[s], (uint32_t)((sl / kAS) & 1));
+            tc_fence_after();
+            const uint32_t b_hi = base + s * Cfg::kOpStage, b_lo = b_hi + Cfg::kBbytes;
+#pragma unroll
+            for (int kk = 0; kk < kTK / 8; ++kk) {  // K = 8 per MMA: +32 bytes along the rows
+                const uint64_t bh = umma_desc_k<kTK>(b_hi + kk * 32);
+                const uint64_t bl = umma_desc_k<kTK>(b_lo + kk * 32);
+                const int gk = sl * (kTK / 8) + kk;
+                const int set = kG > 0 ? (seg & 1) : gk % kSets;
+                const bool fresh = kG > 0 ? (seg_first && kk == 0) : (gk < kSets);
+#pragma unroll
+                for (int mb = 0; mb < 2; ++mb) {
+                    const uint32_t ah = tmem + (uint32_t)(Cfg::kA0 + s * Cfg::kAcols + mb * 2 * kTK + kk * 8);
+                    const uint32_t acc = tmem + (uint32_t)(Cfg::kAcc0 + set * 2 * N + mb * N);
+#if !TM_CTX_DBG_NOMMA
+                    mma_tf32_ta(acc, ah + kTK, bh, idesc, !fresh);  // small terms first
+                    mma_tf32_ta(acc, ah, bl, idesc, 1);
+                    mma_tf32_ta(acc, ah, bh, idesc, 1);
+#else
+                    (void)acc; (void)ah; (void)bh; (void)bl; (void)fresh;
+#endif
+                }
+            }
+            mma_commit(&empty[s]);
+            if (kG > 0 && (sl % kGd == kGd - 1 || sl == nsl - 1)) mma_commit(&seg_full[seg & 1]);
+        }
+        mma_commit(&acc_full);
+    } else if (warp == kLoadWarp && lane == 0) {
+        // ---------------- loader: the P tile (swizzled) and the V rows ------
+        const int y_p = (int)(head * s_q + i0), y_v0 = (int)(head * s_k);
+        for (int sl = 0; sl < nsl; ++sl) {
+            const int ss = sl % kSS;
+            if (sl >= kSS) mbar_wait(&sempty[ss], (uint32_t)(((sl / kSS) + 1) & 1));
+            unsigned char* sp = stage_ptr + ss * Cfg::kSlice;
+            mbar_expect_tx(&sfull[ss], Cfg::kSlice);
+            tma_load_2d(sp, &tm_p, sl * kTK, y_p, &sfull[ss]);
+            tma_load_2d(sp + Cfg::kPbytes, &tm_v, 0, y_v0 + sl * kTK, &sfull[ss]);
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (warp == kMMAWarp) {
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem)
+                     : "memory");
+    }
+}
+
 template <int N>
 cudaError_t launch_ctx(const float* P, const uint32_t* mask, double scale, const float* V,
                        float* ctx, int64_t heads, int64_t s_q, int64_t s_k, cudaStream_t st) {
     CUtensorMap tp, tv;
+    constexpr int tk = TM_CTX_TA ? CtxTaCfg<N, false>::kTK : kCK;
     if (!make_tmap_2d(&tp, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, P, (uint64_t)(heads * s_q),
-                      (uint64_t)s_k, kCM, kCK, CU_TENSOR_MAP_SWIZZLE_64B) ||
+                      (uint64_t)s_k, kCM, tk,
+                      tk == 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B) ||
         !make_tmap_2d(&tv, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, V, (uint64_t)(heads * s_k),
-                      (uint64_t)N, kCK, N))
+                      (uint64_t)N, tk, N))
         return cudaErrorNotSupported;
-    auto k = ctx_recompute_gemm_kernel<N>;
-    const size_t smem = CtxCfg<N>::kSmem;
+    // long rows: the drained accumulation (bounded truncation error); up to
+    // TM_CTX_DRAIN_MIN_SK the set rotation, ~10 % faster (see CtxTaCfg)
+    const bool drain = s_k > TM_CTX_DRAIN_MIN_SK;
+    auto k = !TM_CTX_TA ? ctx_recompute_gemm_kernel<N>
+             : drain    ? ctx_recompute_gemm_ta_kernel<N, true>
+                        : ctx_recompute_gemm_ta_kernel<N, false>;
+    const size_t smem = !TM_CTX_TA ? CtxCfg<N>::kSmem
+                        : drain    ? CtxTaCfg<N, true>::kSmem
+                                   : CtxTaCfg<N, false>::kSmem;
     (void)grid_for((const void*)k, kCThreads, smem, 1);
     const int64_t grid = heads * ((s_q + kCM - 1) / kCM);
     launch(k, (int)grid, kCThreads, smem, st)(tp, tv, mask, scale, ctx, (int)s_q, (int)s_k);

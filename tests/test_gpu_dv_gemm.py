@@ -96,11 +96,18 @@ def test_umma_probe_layouts():
 @pytest.mark.parametrize("heads,s_q,s_k,d,p", [(3, 512, 512, 64, 0.1), (2, 512, 512, 32, 0.1),
                                                (1, 128, 32, 64, 0.5), (5, 384, 256, 64, 0.0),
                                                (2, 256, 1024, 64, 0.1), (1, 128, 96, 32, 0.3),
-                                               (3, 100, 64, 64, 0.1), (2, 300, 128, 32, 0.2)])
+                                               (3, 100, 64, 64, 0.1), (2, 300, 128, 32, 0.2),
+                                               # long rows: the drained accumulation
+                                               # (s_k > 1024), incl. a 1-slice last segment
+                                               (1, 256, 2048, 64, 0.1), (1, 128, 8192, 64, 0.1),
+                                               (1, 200, 4096, 32, 0.1), (2, 128, 1056, 64, 0.2)])
 def test_ctx_matches_oracle_composition(tops, port, cuda, heads, s_q, s_k, d, p):
     """tempo_attn_dropout_ctx: ctx = D @ V with D rebuilt inside the tcgen05
     GEMM (P's tile staged with TMA SWIZZLE_128B = the K-major operand layout)
-    against the oracle composition dropout_apply -> fp64 D @ V."""
+    against the oracle composition dropout_apply -> fp64 D @ V.  The bound
+    holds at any s_k: beyond s_k = 1024 the kernel drains its TMEM
+    accumulators into fp32 registers every 256 key columns, so the tensor
+    core's truncating accumulation never spans more than 48 products."""
     import torch
     g = np.random.default_rng(heads * s_q + s_k + d)
     z = g.standard_normal((heads, s_q, s_k)) * 2
