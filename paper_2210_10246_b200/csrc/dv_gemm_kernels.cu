@@ -971,7 +971,7 @@ __global__ void __launch_bounds__(kCThreads, 1) ctx_recompute_gemm_kernel(
 #ifndef TM_CTX_A_FIRST
 #define TM_CTX_A_FIRST 1
 #endif
-template <int N, bool DRAIN>
+template <int N, bool DRAIN, bool DV = false>
 struct CtxTaCfg {
     static constexpr int kTK = TM_CTX_TA_K;             // key columns per slice
     static constexpr int kCh = kTK / 8;                 // 16-byte chunks per thread (2 per row half)
@@ -992,8 +992,9 @@ struct CtxTaCfg {
     static constexpr int kAcc0 = TM_CTX_A_FIRST ? 512 - kAcc : 0;
     static constexpr int kSS = TM_CTX_TA_SS;
     static constexpr int kPbytes = kCM * kTK * 4;      // 16 / 32 KB, swizzled
-    static constexpr int kVbytes = kTK * N * 4;
-    static constexpr int kSlice = kPbytes + kVbytes;
+    static constexpr int kVbytes = kTK * N * 4;        // V (ctx) / dO (dV) rows
+    static constexpr int kMbytes = DV ? kTK * (kCM / 32) * 4 : 0;  // dV: the slice's mask words
+    static constexpr int kSlice = (kPbytes + kVbytes + kMbytes + 1023) / 1024 * 1024;
     static constexpr int kBbytes = N * kTK * 4;
     static constexpr int kOpStage = 2 * kBbytes;       // B hi, lo
     static constexpr size_t kSmem = 1024 + (size_t)kAS * kOpStage + (size_t)kSS * kSlice;
@@ -1023,11 +1024,18 @@ __device__ __forceinline__ uint64_t umma_desc_k(uint32_t addr) {
     return TK == 32 ? umma_desc_sw128(addr, 16, 1024) : umma_desc_sw64(addr, 512);
 }
 
-template <int N, bool DRAIN>
+// DV = true: the same pipeline for dV = D^T dO (M = s_k, N = d, K = s_q):
+// the loader stages [kTK query rows x 256 key columns] of P row-major, their
+// mask words and the dO rows; a producer thread owns key column m = one TMEM
+// lane and reads its kTK/2 values down the slice (a warp reads 32 consecutive
+// floats of a row: conflict-free) -- the transpose happens on the way into
+// TMEM.  B = dO's K-major tile, exactly as V's for ctx.
+template <int N, bool DRAIN, bool DV>
 __global__ void __launch_bounds__(kCThreads, 1) ctx_recompute_gemm_ta_kernel(
     const __grid_constant__ CUtensorMap tm_p, const __grid_constant__ CUtensorMap tm_v,
-    const uint32_t* __restrict__ mask, double scale, float* __restrict__ ctx, int s_q, int s_k) {
-    using Cfg = CtxTaCfg<N, DRAIN>;
+    const __grid_constant__ CUtensorMap tm_m, const uint32_t* __restrict__ mask, double scale,
+    float* __restrict__ ctx, int s_q, int s_k) {
+    using Cfg = CtxTaCfg<N, DRAIN, DV>;
     constexpr int kSets = Cfg::kSets, kSS = Cfg::kSS, kAS = Cfg::kAS, kG = Cfg::kG;
     constexpr int kTK = Cfg::kTK, kCh = Cfg::kCh;
     constexpr int kGd = kG > 0 ? kG : 1;  // (division-safe)
@@ -1042,10 +1050,12 @@ __global__ void __launch_bounds__(kCThreads, 1) ctx_recompute_gemm_ta_kernel(
     __shared__ uint32_t tmem_base_sh;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int iblocks = (s_q + kCM - 1) / kCM;
+    // output rows: ctx's query rows (ragged s_q allowed) / dV's key rows
+    const int n_rows = DV ? s_k : s_q;
+    const int iblocks = (n_rows + kCM - 1) / kCM;
     const int64_t head = blockIdx.x / iblocks;
     const int i0 = (blockIdx.x % iblocks) * kCM;
-    const int nsl = s_k / kTK;
+    const int nsl = (DV ? s_q : s_k) / kTK;
     constexpr int kMMAWarp = kCSP / 32, kLoadWarp = kCSP / 32 + 1;
 
     if (threadIdx.x == 0) {
@@ -1085,7 +1095,7 @@ __global__ void __launch_bounds__(kCThreads, 1) ctx_recompute_gemm_ta_kernel(
         const bool bwarp = warp < 4;
         constexpr int kKV = kTK * N / 128;  // 16 / 8 (N = 64) or 8 / 4
         const int bn = t % N, kb = (t / N) * kKV;
-        const bool row_in = i0 + m < s_q;
+        const bool row_in = !DV && i0 + m < s_q;
         const uint32_t lane_base = tmem + ((uint32_t)((warp & 3) * 32) << 16);
         const uint32_t* mrow = mask + (((head * (int64_t)s_q + i0 + m) * s_k) >> 5);
         constexpr int kSlPerWord = 32 / kTK;  // slices per mask word (2 or 1)
@@ -1115,18 +1125,30 @@ __global__ void __launch_bounds__(kCThreads, 1) ctx_recompute_gemm_ta_kernel(
         for (int sl = 0; sl < nsl; ++sl) {
             const int ss = sl % kSS, s = sl % kAS;
             if (kG > 0 && sl >= kG + kLag && (sl - kLag) % kGd == 0) drain(drained++);
-            if (sl % kSlPerWord == 0) {
+            if (!DV && sl % kSlPerWord == 0) {
                 w = w_next;
                 if (row_in && sl + kSlPerWord < nsl) w_next = __ldg(mrow + sl / kSlPerWord + 1);
             }
             mbar_wait(&sfull[ss], (uint32_t)((sl / kSS) & 1));
             const uint32_t sp = stage_base + ss * Cfg::kSlice;
             float e[4 * kCh];
+            uint32_t dvw[DV ? 4 * kCh : 1];
+            if (!DV) {
 #pragma unroll
-            for (int c = 0; c < kCh; ++c)
-                asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
-                             : "=f"(e[4 * c]), "=f"(e[4 * c + 1]), "=f"(e[4 * c + 2]), "=f"(e[4 * c + 3])
-                             : "r"(sp + swz_k_offset<kTK>(m, kCh * h + c)));
+                for (int c = 0; c < kCh; ++c)
+                    asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
+                                 : "=f"(e[4 * c]), "=f"(e[4 * c + 1]), "=f"(e[4 * c + 2]), "=f"(e[4 * c + 3])
+                                 : "r"(sp + swz_k_offset<kTK>(m, kCh * h + c)));
+            } else {
+                // query rows h*kTK/2 + k of key column m, and their mask words
+#pragma unroll
+                for (int k = 0; k < 4 * kCh; ++k) {
+                    const int r = h * (kTK / 2) + k;
+                    e[k] = lds32(sp + (uint32_t)((r * kCM + m) * 4));
+                    dvw[k % (DV ? 4 * kCh : 1)] =
+                        ldsu32(sp + Cfg::kPbytes + Cfg::kVbytes + (uint32_t)((r * (kCM / 32) + (m >> 5)) * 4));
+                }
+            }
             float ov[kKV];
             if (bwarp) {
 #pragma unroll
@@ -1141,7 +1163,10 @@ __global__ void __launch_bounds__(kCThreads, 1) ctx_recompute_gemm_ta_kernel(
             const uint32_t wsl = w >> (kTK * (sl % kSlPerWord) + (kTK / 2) * h);
             float hi[4 * kCh], lo[4 * kCh];
 #pragma unroll
-            for (int k = 0; k < 4 * kCh; ++k) split_tf32(((wsl >> k) & 1u) ? e[k] : 0.0f, hi[k], lo[k]);
+            for (int k = 0; k < 4 * kCh; ++k) {
+                const bool keep = DV ? ((dvw[k % (DV ? 4 * kCh : 1)] >> lane) & 1u) : ((wsl >> k) & 1u);
+                split_tf32(keep ? e[k] : 0.0f, hi[k], lo[k]);
+            }
             const uint32_t ta = lane_base + (uint32_t)(Cfg::kA0 + s * Cfg::kAcols + mb * 2 * kTK + (kTK / 2) * h);
 #pragma unroll
             for (int c = 0; c < kCh / 2; ++c) {
@@ -1168,9 +1193,9 @@ __global__ void __launch_bounds__(kCThreads, 1) ctx_recompute_gemm_ta_kernel(
         }
         // ---------------- epilogue: ctx = (1/(1-p)) * the accumulation -----
         const int row = i0 + emb * 128 + quad * 32 + lane;
-        float* out = ctx + (head * (int64_t)s_q + row) * N;
+        float* out = ctx + (head * (int64_t)n_rows + row) * N;
         const float sc = (float)scale;
-        const bool store = row < s_q;
+        const bool store = row < n_rows;
         if (kG > 0) {
             const int nseg = (nsl + kGd - 1) / kGd;
             while (drained < nseg) drain(drained++);
@@ -1248,9 +1273,16 @@ __global__ void __launch_bounds__(kCThreads, 1) ctx_recompute_gemm_ta_kernel(
             const int ss = sl % kSS;
             if (sl >= kSS) mbar_wait(&sempty[ss], (uint32_t)(((sl / kSS) + 1) & 1));
             unsigned char* sp = stage_ptr + ss * Cfg::kSlice;
-            mbar_expect_tx(&sfull[ss], Cfg::kSlice);
-            tma_load_2d(sp, &tm_p, sl * kTK, y_p, &sfull[ss]);
-            tma_load_2d(sp + Cfg::kPbytes, &tm_v, 0, y_v0 + sl * kTK, &sfull[ss]);
+            mbar_expect_tx(&sfull[ss], Cfg::kPbytes + Cfg::kVbytes + Cfg::kMbytes);
+            if (!DV) {
+                tma_load_2d(sp, &tm_p, sl * kTK, y_p, &sfull[ss]);
+                tma_load_2d(sp + Cfg::kPbytes, &tm_v, 0, y_v0 + sl * kTK, &sfull[ss]);
+            } else {  // P rows [kTK x 256], dO rows [kTK x N], mask words [kTK x 8]
+                const int y = (int)(head * s_q) + sl * kTK;
+                tma_load_2d(sp, &tm_p, i0, y, &sfull[ss]);
+                tma_load_2d(sp + Cfg::kPbytes, &tm_v, 0, y, &sfull[ss]);
+                tma_load_2d(sp + Cfg::kPbytes + Cfg::kVbytes, &tm_m, i0 / 32, y, &sfull[ss]);
+            }
         }
     }
     tc_fence_before();
@@ -1276,15 +1308,44 @@ cudaError_t launch_ctx(const float* P, const uint32_t* mask, double scale, const
     // long rows: the drained accumulation (bounded truncation error); up to
     // TM_CTX_DRAIN_MIN_SK the set rotation, ~10 % faster (see CtxTaCfg)
     const bool drain = s_k > TM_CTX_DRAIN_MIN_SK;
-    auto k = !TM_CTX_TA ? ctx_recompute_gemm_kernel<N>
-             : drain    ? ctx_recompute_gemm_ta_kernel<N, true>
-                        : ctx_recompute_gemm_ta_kernel<N, false>;
-    const size_t smem = !TM_CTX_TA ? CtxCfg<N>::kSmem
-                        : drain    ? CtxTaCfg<N, true>::kSmem
-                                   : CtxTaCfg<N, false>::kSmem;
-    (void)grid_for((const void*)k, kCThreads, smem, 1);
     const int64_t grid = heads * ((s_q + kCM - 1) / kCM);
-    launch(k, (int)grid, kCThreads, smem, st)(tp, tv, mask, scale, ctx, (int)s_q, (int)s_k);
+    if (!TM_CTX_TA) {
+        auto k = ctx_recompute_gemm_kernel<N>;
+        const size_t smem = CtxCfg<N>::kSmem;
+        (void)grid_for((const void*)k, kCThreads, smem, 1);
+        launch(k, (int)grid, kCThreads, smem, st)(tp, tv, mask, scale, ctx, (int)s_q, (int)s_k);
+        return cudaGetLastError();
+    }
+    auto k = drain ? ctx_recompute_gemm_ta_kernel<N, true, false>
+                   : ctx_recompute_gemm_ta_kernel<N, false, false>;
+    const size_t smem = drain ? CtxTaCfg<N, true>::kSmem : CtxTaCfg<N, false>::kSmem;
+    (void)grid_for((const void*)k, kCThreads, smem, 1);
+    launch(k, (int)grid, kCThreads, smem, st)(tp, tv, tv, mask, scale, ctx, (int)s_q, (int)s_k);
+    return cudaGetLastError();
+}
+
+// dV = D^T dO through the TMEM-A pipeline (DV instantiation above)
+#ifndef TM_DV_TA
+#define TM_DV_TA 1
+#endif
+template <int N>
+cudaError_t launch_dv_ta(const float* P, const uint32_t* mask, double scale, const float* dO,
+                         float* dV, int64_t heads, int64_t s_q, int64_t s_k, cudaStream_t st) {
+    constexpr int tk = CtxTaCfg<N, false, true>::kTK;
+    CUtensorMap tp, tmk, to;
+    const uint64_t rows = (uint64_t)(heads * s_q);
+    if (!make_tmap_2d(&tp, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, P, rows, (uint64_t)s_k, tk, kCM) ||
+        !make_tmap_2d(&tmk, CU_TENSOR_MAP_DATA_TYPE_UINT32, mask, rows, (uint64_t)(s_k / 32), tk,
+                      kCM / 32) ||
+        !make_tmap_2d(&to, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, dO, rows, (uint64_t)N, tk, N))
+        return launch_dv<N>(P, mask, scale, dO, dV, heads, s_q, s_k, st);  // no tensor maps
+    const bool drain = s_q > TM_CTX_DRAIN_MIN_SK;
+    auto k = drain ? ctx_recompute_gemm_ta_kernel<N, true, true>
+                   : ctx_recompute_gemm_ta_kernel<N, false, true>;
+    const size_t smem = drain ? CtxTaCfg<N, true, true>::kSmem : CtxTaCfg<N, false, true>::kSmem;
+    (void)grid_for((const void*)k, kCThreads, smem, 1);
+    const int64_t grid = heads * (s_k / kCM);
+    launch(k, (int)grid, kCThreads, smem, st)(tp, to, tmk, mask, scale, dV, (int)s_q, (int)s_k);
     return cudaGetLastError();
 }
 
@@ -1319,9 +1380,11 @@ cudaError_t launch_dv_recompute_gemm(const float* P, const uint32_t* mask, doubl
 #ifndef TM_DV_STAGED
 #define TM_DV_STAGED 1
 #endif
-        case 32: return TM_DV_STAGED ? launch_dv_staged<32>(P, mask, scale, dO, dV, heads, s_q, s_k, st)
+        case 32: return TM_DV_TA ? launch_dv_ta<32>(P, mask, scale, dO, dV, heads, s_q, s_k, st)
+                      : TM_DV_STAGED ? launch_dv_staged<32>(P, mask, scale, dO, dV, heads, s_q, s_k, st)
                                      : launch_dv<32>(P, mask, scale, dO, dV, heads, s_q, s_k, st);
-        case 64: return TM_DV_STAGED ? launch_dv_staged<64>(P, mask, scale, dO, dV, heads, s_q, s_k, st)
+        case 64: return TM_DV_TA ? launch_dv_ta<64>(P, mask, scale, dO, dV, heads, s_q, s_k, st)
+                      : TM_DV_STAGED ? launch_dv_staged<64>(P, mask, scale, dO, dV, heads, s_q, s_k, st)
                                      : launch_dv<64>(P, mask, scale, dO, dV, heads, s_q, s_k, st);
         case 128: return launch_dv<128>(P, mask, scale, dO, dV, heads, s_q, s_k, st);
         default: return cudaErrorInvalidValue;

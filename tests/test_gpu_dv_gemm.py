@@ -34,7 +34,9 @@ def pack(keep):
 
 @pytest.mark.parametrize("heads,s_q,s_k,d,p", [(3, 512, 512, 64, 0.1), (2, 512, 512, 32, 0.1),
                                                (2, 256, 512, 128, 0.1), (1, 32, 256, 64, 0.5),
-                                               (5, 384, 256, 64, 0.0), (2, 1024, 512, 64, 0.1)])
+                                               (5, 384, 256, 64, 0.0), (2, 1024, 512, 64, 0.1),
+                                               # long K = s_q: the drained accumulation
+                                               (1, 8192, 256, 64, 0.1), (1, 2080, 256, 32, 0.2)])
 def test_dv_matches_oracle_composition(tops, port, cuda, heads, s_q, s_k, d, p):
     import torch
     P, dO, keep = case(heads, s_q, s_k, d, p, heads * s_q + d)

@@ -25,7 +25,7 @@ def main():
         mag = torch.matmul(Dd.abs(), V.double().abs())
         e = (ctx.double() - ref).abs() / (ref.abs() + mag)
         r = {"max": float(e.max()), "mean": float(e.mean())}
-        if s_k <= 2048:
+        if True:
             dO = torch.randn(heads, s_q, d, device=dev)
             Pq = P.view(heads, s_q, s_k)
             if s_k % 256 == 0:
@@ -35,6 +35,17 @@ def main():
                 ev = (dV.double() - refv).abs() / (refv.abs() + magv)
                 r["dv_max"], r["dv_mean"] = float(ev.max()), float(ev.mean())
         out[f"s_k={s_k}"] = r
+    # dV's reduction runs over s_q: a long-K case for it
+    heads, s_q, s_k, d, p = 1, 8192, 256, 64, 0.1
+    z = torch.randn(heads * s_q, s_k, device=dev) * 3
+    P, D, m = ops.softmax_dropout_fwd(z, p, seed=5)
+    dO = torch.randn(heads, s_q, d, device=dev)
+    dV = ops.attn_dropout_dv(P.view(heads, s_q, s_k), m, p, dO)
+    Dd = D.view(heads, s_q, s_k).double()
+    refv = torch.matmul(Dd.transpose(1, 2), dO.double())
+    magv = torch.matmul(Dd.abs().transpose(1, 2), dO.double().abs())
+    ev = (dV.double() - refv).abs() / (refv.abs() + magv)
+    out["dv_s_q=8192"] = {"max": float(ev.max()), "mean": float(ev.mean())}
     print(json.dumps(out))
 
 
