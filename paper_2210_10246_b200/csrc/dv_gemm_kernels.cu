@@ -965,16 +965,24 @@ __global__ void __launch_bounds__(kCThreads, 1) ctx_recompute_gemm_kernel(
 #ifndef TM_CTX_DBG_NOMMA  // timing experiments only: issue no MMAs (producer-bound time)
 #define TM_CTX_DBG_NOMMA 0
 #endif
+#ifndef TM_CTX_DBG_NOPROD  // timing experiments only: no A split / TMEM stores
+#define TM_CTX_DBG_NOPROD 0
+#endif
 #ifndef TM_CTX_TA_AS
 #define TM_CTX_TA_AS 2
 #endif
 #ifndef TM_CTX_A_FIRST
 #define TM_CTX_A_FIRST 1
 #endif
+#ifndef TM_GEMM_PERSIST
+#define TM_GEMM_PERSIST 1  // undrained instantiation: one CTA per SM looping over tiles
+#endif
+#ifndef TM_GEMM_ALT
+#define TM_GEMM_ALT 1  // undrained instantiation: the producer halves alternate slices
+#endif
 template <int N, bool DRAIN, bool DV = false>
 struct CtxTaCfg {
     static constexpr int kTK = TM_CTX_TA_K;             // key columns per slice
-    static constexpr int kCh = kTK / 8;                 // 16-byte chunks per thread (2 per row half)
     // kG > 0: the accumulation runs in segments of kG slices into two
     // ping-pong TMEM accumulators; the producers drain each finished segment
     // into fp32 registers (round-to-nearest adds), so the tensor core's
@@ -1034,40 +1042,47 @@ template <int N, bool DRAIN, bool DV>
 __global__ void __launch_bounds__(kCThreads, 1) ctx_recompute_gemm_ta_kernel(
     const __grid_constant__ CUtensorMap tm_p, const __grid_constant__ CUtensorMap tm_v,
     const __grid_constant__ CUtensorMap tm_m, const uint32_t* __restrict__ mask, double scale,
-    float* __restrict__ ctx, int s_q, int s_k) {
+    float* __restrict__ ctx, int s_q, int s_k, int ntiles) {
     using Cfg = CtxTaCfg<N, DRAIN, DV>;
     constexpr int kSets = Cfg::kSets, kSS = Cfg::kSS, kAS = Cfg::kAS, kG = Cfg::kG;
-    constexpr int kTK = Cfg::kTK, kCh = Cfg::kCh;
+    constexpr int kTK = Cfg::kTK;
     constexpr int kGd = kG > 0 ? kG : 1;  // (division-safe)
+    constexpr bool kAlt = TM_GEMM_ALT && kG == 0 && kTK == 32;
     grid_dep_wait();
     grid_dep_launch();
     extern __shared__ __align__(1024) unsigned char gsm[];
     const uint32_t base = (smem_u32(gsm) + 1023u) & ~1023u;
     const uint32_t stage_base = base + kAS * Cfg::kOpStage;
     unsigned char* stage_ptr = gsm + (stage_base - smem_u32(gsm));
-    __shared__ uint64_t full[kAS], empty[kAS], acc_full, sfull[kSS], sempty[kSS];
+    __shared__ uint64_t full[kAS], empty[kAS], acc_full, acc_empty, sfull[kSS], sempty[kSS];
     __shared__ uint64_t seg_full[2], seg_empty[2];  // kG > 0: segment accumulators
     __shared__ uint32_t tmem_base_sh;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    // output rows: ctx's query rows (ragged s_q allowed) / dV's key rows
+    // Tiles = (head, 256 output rows): ctx's query rows (ragged s_q allowed)
+    // / dV's key rows.  Persistent: CTA b takes tiles b, b + grid, ...; the
+    // slice ring, the operand stages and their barrier phases run on across
+    // tiles (slice counter gs), so the next tile's loads stream in under the
+    // current tile's epilogue.  (The drained instantiation is launched with
+    // one tile per CTA.)
     const int n_rows = DV ? s_k : s_q;
     const int iblocks = (n_rows + kCM - 1) / kCM;
-    const int64_t head = blockIdx.x / iblocks;
-    const int i0 = (blockIdx.x % iblocks) * kCM;
     const int nsl = (DV ? s_q : s_k) / kTK;
+    const int myn = (ntiles - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
     constexpr int kMMAWarp = kCSP / 32, kLoadWarp = kCSP / 32 + 1;
+    constexpr int kArrive = kCSP / 32 / (kAlt ? 2 : 1);  // producer warps per slice
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < kAS; ++s) {
-            mbar_init(&full[s], kCSP / 32);
+            mbar_init(&full[s], kArrive);
             mbar_init(&empty[s], 1);
         }
         for (int s = 0; s < kSS; ++s) {
             mbar_init(&sfull[s], 1);
-            mbar_init(&sempty[s], kCSP / 32);
+            mbar_init(&sempty[s], kArrive);
         }
         mbar_init(&acc_full, 1);
+        mbar_init(&acc_empty, kCSP / 32);
         for (int g = 0; g < 2; ++g) {
             mbar_init(&seg_full[g], 1);
             mbar_init(&seg_empty[g], kCSP / 32);
@@ -1087,25 +1102,30 @@ __global__ void __launch_bounds__(kCThreads, 1) ctx_recompute_gemm_ta_kernel(
 
     if (warp < kMMAWarp) {
         // ---------------- producers ----------------
-        // A: thread t owns query row m = t % 256 (TMEM lane 32*(warp%4) + lane
-        //    of M-block m / 128) and the K columns h*kTK/2.. (h = t / 256).
-        // B: warps 0-3, thread t owns V column n = t % N, K-rows kb..kb+kKV-1.
+        // A: thread t owns output row m = t % 256 of the tile (TMEM lane
+        //    32*(warp%4) + lane of M-block m / 128).  ALT (the undrained
+        //    instantiation): the two 8-warp halves take alternate slices
+        //    (slice counter parity), a thread covering all kTK K values of
+        //    its row; else both halves share every slice, half the K values
+        //    each (h = t / 256).
+        // B: 4 warps per half, thread tb < 128 owns V / dO column n = tb % N,
+        //    K-rows kb..kb+kKV-1.
+        constexpr int kGrp = kAlt ? 2 : 1;
+        constexpr int kColsT = (kTK / 2) * kGrp;  // K values per thread per slice
         const int t = threadIdx.x;
-        const int m = t % kCM, h = t / kCM, mb = m >> 7;
-        const bool bwarp = warp < 4;
+        const int m = t % kCM, mb = m >> 7;
+        const int grp = kAlt ? t / kCM : 0, h = kAlt ? 0 : t / kCM;
+        const int tb = kAlt ? t % kCM : t;
+        const bool bwarp = tb < 128;
         constexpr int kKV = kTK * N / 128;  // 16 / 8 (N = 64) or 8 / 4
-        const int bn = t % N, kb = (t / N) * kKV;
-        const bool row_in = !DV && i0 + m < s_q;
+        const int bn = tb % N, kb = (tb / N) * kKV;
         const uint32_t lane_base = tmem + ((uint32_t)((warp & 3) * 32) << 16);
-        const uint32_t* mrow = mask + (((head * (int64_t)s_q + i0 + m) * s_k) >> 5);
         constexpr int kSlPerWord = 32 / kTK;  // slices per mask word (2 or 1)
-        uint32_t w = 0, w_next = row_in ? __ldg(mrow) : 0u;
-        // segment drains (kG > 0): this thread's N/2 accumulator columns
+        static_assert(!kAlt || kSlPerWord == 1, "alternating halves need a mask word per slice");
         const int quad = warp % 4, emb = (warp / 4) % 2, half = warp / 8;
         const uint32_t acc_lane = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(Cfg::kAcc0 + emb * N + half * (N / 2));
+        const float sc = (float)scale;
         float racc[N / 2];
-#pragma unroll
-        for (int i = 0; i < N / 2; ++i) racc[i] = 0.0f;
         auto drain = [&](int j) {  // segment j: wait for its MMAs, add, free the buffer
             mbar_wait(&seg_full[j & 1], (uint32_t)((j >> 1) & 1));
             tc_fence_after();
@@ -1120,168 +1140,203 @@ __global__ void __launch_bounds__(kCThreads, 1) ctx_recompute_gemm_ta_kernel(
             __syncwarp();
             if (lane == 0) mbar_arrive(&seg_empty[j & 1]);
         };
-        constexpr int kLag = 2;  // drain segment j while producing slice (j+1)*kG + kLag
-        int drained = 0;
-        for (int sl = 0; sl < nsl; ++sl) {
-            const int ss = sl % kSS, s = sl % kAS;
-            if (kG > 0 && sl >= kG + kLag && (sl - kLag) % kGd == 0) drain(drained++);
-            if (!DV && sl % kSlPerWord == 0) {
-                w = w_next;
-                if (row_in && sl + kSlPerWord < nsl) w_next = __ldg(mrow + sl / kSlPerWord + 1);
-            }
-            mbar_wait(&sfull[ss], (uint32_t)((sl / kSS) & 1));
-            const uint32_t sp = stage_base + ss * Cfg::kSlice;
-            float e[4 * kCh];
-            uint32_t dvw[DV ? 4 * kCh : 1];
-            if (!DV) {
+        for (int k = 0; k < myn; ++k) {
+            const int tile = (int)blockIdx.x + k * (int)gridDim.x;
+            const int64_t head = tile / iblocks;
+            const int i0 = (tile % iblocks) * kCM;
+            const int64_t gs0 = (int64_t)k * nsl;
+            const bool row_in = !DV && i0 + m < s_q;
+            const uint32_t* mrow = mask + (((head * (int64_t)s_q + i0 + m) * s_k) >> 5);
+            // this thread's first slice of the tile (ALT: slice-counter parity)
+            const int sl0 = kAlt ? (int)((grp + gs0) & 1) : 0;
+            uint32_t w = 0, w_next = (row_in && sl0 < nsl) ? __ldg(mrow + sl0 / kSlPerWord) : 0u;
 #pragma unroll
-                for (int c = 0; c < kCh; ++c)
-                    asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
-                                 : "=f"(e[4 * c]), "=f"(e[4 * c + 1]), "=f"(e[4 * c + 2]), "=f"(e[4 * c + 3])
-                                 : "r"(sp + swz_k_offset<kTK>(m, kCh * h + c)));
-            } else {
-                // query rows h*kTK/2 + k of key column m, and their mask words
-#pragma unroll
-                for (int k = 0; k < 4 * kCh; ++k) {
-                    const int r = h * (kTK / 2) + k;
-                    e[k] = lds32(sp + (uint32_t)((r * kCM + m) * 4));
-                    dvw[k % (DV ? 4 * kCh : 1)] =
-                        ldsu32(sp + Cfg::kPbytes + Cfg::kVbytes + (uint32_t)((r * (kCM / 32) + (m >> 5)) * 4));
+            for (int i = 0; i < N / 2; ++i) racc[i] = 0.0f;
+            constexpr int kLag = 2;  // drain segment j while producing slice (j+1)*kG + kLag
+            int drained = 0;
+            for (int sl = sl0; sl < nsl; sl += kGrp) {
+                const int64_t gs = gs0 + sl;
+                const int ss = (int)(gs % kSS), s = (int)(gs % kAS);
+                if (kG > 0 && sl >= kG + kLag && (sl - kLag) % kGd == 0) drain(drained++);
+                if (!DV && sl % kSlPerWord == 0) {
+                    w = w_next;
+                    const int nx = sl / kSlPerWord + kGrp;  // this thread's next mask word
+                    if (row_in && nx * kSlPerWord < nsl) w_next = __ldg(mrow + nx);
                 }
-            }
-            float ov[kKV];
-            if (bwarp) {
+                mbar_wait(&sfull[ss], (uint32_t)((gs / kSS) & 1));
+                const uint32_t sp = stage_base + ss * Cfg::kSlice;
+                float e[kColsT];
+                uint32_t dvw[DV ? kColsT : 1];
+                if (!DV) {
 #pragma unroll
-                for (int k = 0; k < kKV; ++k)
-                    ov[k] = lds32(sp + Cfg::kPbytes + (uint32_t)(((kb + k) * N + bn) * 4));
-            }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&sempty[ss]);
-            if (sl >= kAS) mbar_wait(&empty[s], (uint32_t)(((sl / kAS) + 1) & 1));
-            tc_fence_after();
-            // this thread's keep bits: columns kTK*sl + h*kTK/2 ..
-            const uint32_t wsl = w >> (kTK * (sl % kSlPerWord) + (kTK / 2) * h);
-            float hi[4 * kCh], lo[4 * kCh];
+                    for (int c = 0; c < kColsT / 4; ++c)
+                        asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
+                                     : "=f"(e[4 * c]), "=f"(e[4 * c + 1]), "=f"(e[4 * c + 2]), "=f"(e[4 * c + 3])
+                                     : "r"(sp + swz_k_offset<kTK>(m, (kColsT / 4) * h + c)));
+                } else {
+                    // query rows h*kColsT + k of key column m, and their mask words
 #pragma unroll
-            for (int k = 0; k < 4 * kCh; ++k) {
-                const bool keep = DV ? ((dvw[k % (DV ? 4 * kCh : 1)] >> lane) & 1u) : ((wsl >> k) & 1u);
-                split_tf32(keep ? e[k] : 0.0f, hi[k], lo[k]);
-            }
-            const uint32_t ta = lane_base + (uint32_t)(Cfg::kA0 + s * Cfg::kAcols + mb * 2 * kTK + (kTK / 2) * h);
-#pragma unroll
-            for (int c = 0; c < kCh / 2; ++c) {
-                tmem_st8(ta + 8 * c, hi + 8 * c);
-                tmem_st8(ta + kTK + 8 * c, lo + 8 * c);
-            }
-            if (bwarp) {
-                const uint32_t b_hi = base + s * Cfg::kOpStage, b_lo = b_hi + Cfg::kBbytes;
-                float bh[kKV], bl[kKV];
-#pragma unroll
-                for (int u = 0; u < kKV; ++u) split_tf32(ov[u], bh[u], bl[u]);
-#pragma unroll
-                for (int c = 0; c < kKV / 4; ++c) {
-                    const uint32_t off = swz_k_offset<kTK>(bn, (kb >> 2) + c);
-                    sts128(b_hi + off, bh[4 * c], bh[4 * c + 1], bh[4 * c + 2], bh[4 * c + 3]);
-                    sts128(b_lo + off, bl[4 * c], bl[4 * c + 1], bl[4 * c + 2], bl[4 * c + 3]);
+                    for (int q = 0; q < kColsT; ++q) {
+                        const int r = h * kColsT + q;
+                        e[q] = lds32(sp + (uint32_t)((r * kCM + m) * 4));
+                        dvw[q % (DV ? kColsT : 1)] =
+                            ldsu32(sp + Cfg::kPbytes + Cfg::kVbytes + (uint32_t)((r * (kCM / 32) + (m >> 5)) * 4));
+                    }
                 }
-                fence_proxy_async_smem();
-            }
-            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&full[s]);
-        }
-        // ---------------- epilogue: ctx = (1/(1-p)) * the accumulation -----
-        const int row = i0 + emb * 128 + quad * 32 + lane;
-        float* out = ctx + (head * (int64_t)n_rows + row) * N;
-        const float sc = (float)scale;
-        const bool store = row < n_rows;
-        if (kG > 0) {
-            const int nseg = (nsl + kGd - 1) / kGd;
-            while (drained < nseg) drain(drained++);
-            if (store) {
+                float ov[kKV];
+                if (bwarp) {
 #pragma unroll
-                for (int i = 0; i < N / 2; i += 4)
-                    st_stream(reinterpret_cast<float4*>(out + half * (N / 2) + i),
-                              make_float4(racc[i] * sc, racc[i + 1] * sc, racc[i + 2] * sc,
-                                          racc[i + 3] * sc));
-            }
-        } else {
-            mbar_wait(&acc_full, 0);
-            tc_fence_after();
-#pragma unroll
-            for (int c0 = half * (N / 2); c0 < (half + 1) * (N / 2); c0 += 16) {
-                float v[16];
-                const uint32_t ta = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(Cfg::kAcc0 + emb * N + c0);
-                tmem_ld16(ta, v);
-#pragma unroll
-                for (int set = 1; set < kSets; ++set) {
-                    float wv[16];
-                    tmem_ld16(ta + (uint32_t)(set * 2 * N), wv);
-#pragma unroll
-                    for (int i = 0; i < 16; ++i) v[i] += wv[i];
+                    for (int q = 0; q < kKV; ++q)
+                        ov[q] = lds32(sp + Cfg::kPbytes + (uint32_t)(((kb + q) * N + bn) * 4));
                 }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&sempty[ss]);
+                if (gs >= kAS) mbar_wait(&empty[s], (uint32_t)(((gs / kAS) + 1) & 1));
+                tc_fence_after();
+                // this thread's keep bits: columns kTK*sl + h*kColsT ..
+                const uint32_t wsl = w >> (kTK * (sl % kSlPerWord) + kColsT * h);
+                const uint32_t ta = lane_base + (uint32_t)(Cfg::kA0 + s * Cfg::kAcols + mb * 2 * kTK + kColsT * h);
+#pragma unroll
+                for (int q = 0; q < (TM_CTX_DBG_NOPROD ? 0 : kColsT / 16); ++q) {  // 16 values: hi, lo -> TMEM
+                    float hi[16], lo[16];
+#pragma unroll
+                    for (int u = 0; u < 16; ++u) {
+                        const int kk = 16 * q + u;
+                        const bool keep = DV ? ((dvw[kk % (DV ? kColsT : 1)] >> lane) & 1u) : ((wsl >> kk) & 1u);
+                        split_tf32(keep ? e[kk] : 0.0f, hi[u], lo[u]);
+                    }
+#pragma unroll
+                    for (int c = 0; c < 2; ++c) {
+                        tmem_st8(ta + 16 * q + 8 * c, hi + 8 * c);
+                        tmem_st8(ta + kTK + 16 * q + 8 * c, lo + 8 * c);
+                    }
+                }
+                if (bwarp) {
+                    const uint32_t b_hi = base + s * Cfg::kOpStage, b_lo = b_hi + Cfg::kBbytes;
+                    float bh[kKV], bl[kKV];
+#pragma unroll
+                    for (int u = 0; u < kKV; ++u) split_tf32(ov[u], bh[u], bl[u]);
+#pragma unroll
+                    for (int c = 0; c < kKV / 4; ++c) {
+                        const uint32_t off = swz_k_offset<kTK>(bn, (kb >> 2) + c);
+                        sts128(b_hi + off, bh[4 * c], bh[4 * c + 1], bh[4 * c + 2], bh[4 * c + 3]);
+                        sts128(b_lo + off, bl[4 * c], bl[4 * c + 1], bl[4 * c + 2], bl[4 * c + 3]);
+                    }
+                    fence_proxy_async_smem();
+                }
+                asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&full[s]);
+            }
+            // ---------------- epilogue: out = (1/(1-p)) * the accumulation ----
+            const int row = i0 + emb * 128 + quad * 32 + lane;
+            float* out = ctx + (head * (int64_t)n_rows + row) * N;
+            const bool store = row < n_rows;
+            if (kG > 0) {  // (one tile per CTA)
+                const int nseg = (nsl + kGd - 1) / kGd;
+                while (drained < nseg) drain(drained++);
                 if (store) {
 #pragma unroll
-                    for (int i = 0; i < 16; i += 4)
-                        st_stream(reinterpret_cast<float4*>(out + c0 + i),
-                                  make_float4(v[i] * sc, v[i + 1] * sc, v[i + 2] * sc, v[i + 3] * sc));
+                    for (int i = 0; i < N / 2; i += 4)
+                        st_stream(reinterpret_cast<float4*>(out + half * (N / 2) + i),
+                                  make_float4(racc[i] * sc, racc[i + 1] * sc, racc[i + 2] * sc,
+                                              racc[i + 3] * sc));
                 }
+            } else {
+                mbar_wait(&acc_full, (uint32_t)(k & 1));
+                tc_fence_after();
+#pragma unroll
+                for (int c0 = half * (N / 2); c0 < (half + 1) * (N / 2); c0 += 16) {
+                    float v[16];
+                    const uint32_t ta = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(Cfg::kAcc0 + emb * N + c0);
+                    tmem_ld16(ta, v);
+#pragma unroll
+                    for (int set = 1; set < kSets; ++set) {
+                        float wv[16];
+                        tmem_ld16(ta + (uint32_t)(set * 2 * N), wv);
+#pragma unroll
+                        for (int i = 0; i < 16; ++i) v[i] += wv[i];
+                    }
+                    if (store) {
+#pragma unroll
+                        for (int i = 0; i < 16; i += 4)
+                            st_stream(reinterpret_cast<float4*>(out + c0 + i),
+                                      make_float4(v[i] * sc, v[i + 1] * sc, v[i + 2] * sc, v[i + 3] * sc));
+                    }
+                }
+                // accumulators read: the MMA lane may start the next tile
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&acc_empty);
             }
         }
     } else if (warp == kMMAWarp && lane == 0) {
         // ---------------- MMA issuer: A from TMEM, B from smem ----------
         constexpr uint32_t idesc = idesc_tf32_k(128, N);
-        for (int sl = 0; sl < nsl; ++sl) {
-            const int s = sl % kAS;
-            const int seg = sl / kGd;
-            const bool seg_first = kG > 0 && sl % kGd == 0;
-            if (seg_first && seg >= 2) {  // the producers drained segment seg - 2
-                mbar_wait(&seg_empty[seg & 1], (uint32_t)(((seg >> 1) + 1) & 1));
+        for (int k = 0; k < myn; ++k) {
+            if (kG == 0 && k > 0) {  // the producers have read the previous tile's sums
+                mbar_wait(&acc_empty, (uint32_t)((k - 1) & 1));
+                tc_fence_after();
             }
-            mbar_wait(&full[s], (uint32_t)((sl / kAS) & 1));
-            tc_fence_after();
-            const uint32_t b_hi = base + s * Cfg::kOpStage, b_lo = b_hi + Cfg::kBbytes;
-#pragma unroll
-            for (int kk = 0; kk < kTK / 8; ++kk) {  // K = 8 per MMA: +32 bytes along the rows
-                const uint64_t bh = umma_desc_k<kTK>(b_hi + kk * 32);
-                const uint64_t bl = umma_desc_k<kTK>(b_lo + kk * 32);
-                const int gk = sl * (kTK / 8) + kk;
-                const int set = kG > 0 ? (seg & 1) : gk % kSets;
-                const bool fresh = kG > 0 ? (seg_first && kk == 0) : (gk < kSets);
-#pragma unroll
-                for (int mb = 0; mb < 2; ++mb) {
-                    const uint32_t ah = tmem + (uint32_t)(Cfg::kA0 + s * Cfg::kAcols + mb * 2 * kTK + kk * 8);
-                    const uint32_t acc = tmem + (uint32_t)(Cfg::kAcc0 + set * 2 * N + mb * N);
-#if !TM_CTX_DBG_NOMMA
-                    mma_tf32_ta(acc, ah + kTK, bh, idesc, !fresh);  // small terms first
-                    mma_tf32_ta(acc, ah, bl, idesc, 1);
-                    mma_tf32_ta(acc, ah, bh, idesc, 1);
-#else
-                    (void)acc; (void)ah; (void)bh; (void)bl; (void)fresh;
-#endif
+            for (int sl = 0; sl < nsl; ++sl) {
+                const int64_t gs = (int64_t)k * nsl + sl;
+                const int s = (int)(gs % kAS);
+                const int seg = sl / kGd;
+                const bool seg_first = kG > 0 && sl % kGd == 0;
+                if (seg_first && seg >= 2) {  // the producers drained segment seg - 2
+                    mbar_wait(&seg_empty[seg & 1], (uint32_t)(((seg >> 1) + 1) & 1));
                 }
+                mbar_wait(&full[s], (uint32_t)((gs / kAS) & 1));
+                tc_fence_after();
+                const uint32_t b_hi = base + s * Cfg::kOpStage, b_lo = b_hi + Cfg::kBbytes;
+#pragma unroll
+                for (int kk = 0; kk < kTK / 8; ++kk) {  // K = 8 per MMA: +32 bytes along the rows
+                    const uint64_t bh = umma_desc_k<kTK>(b_hi + kk * 32);
+                    const uint64_t bl = umma_desc_k<kTK>(b_lo + kk * 32);
+                    const int gk = sl * (kTK / 8) + kk;
+                    const int set = kG > 0 ? (seg & 1) : gk % kSets;
+                    const bool fresh = kG > 0 ? (seg_first && kk == 0) : (gk < kSets);
+#pragma unroll
+                    for (int mbk = 0; mbk < 2; ++mbk) {
+                        const uint32_t ah = tmem + (uint32_t)(Cfg::kA0 + s * Cfg::kAcols + mbk * 2 * kTK + kk * 8);
+                        const uint32_t acc = tmem + (uint32_t)(Cfg::kAcc0 + set * 2 * N + mbk * N);
+#if !TM_CTX_DBG_NOMMA
+                        mma_tf32_ta(acc, ah + kTK, bh, idesc, !fresh);  // small terms first
+                        mma_tf32_ta(acc, ah, bl, idesc, 1);
+                        mma_tf32_ta(acc, ah, bh, idesc, 1);
+#else
+                        (void)acc; (void)ah; (void)bh; (void)bl; (void)fresh;
+#endif
+                    }
+                }
+                mma_commit(&empty[s]);
+                if (kG > 0 && (sl % kGd == kGd - 1 || sl == nsl - 1)) mma_commit(&seg_full[seg & 1]);
             }
-            mma_commit(&empty[s]);
-            if (kG > 0 && (sl % kGd == kGd - 1 || sl == nsl - 1)) mma_commit(&seg_full[seg & 1]);
+            mma_commit(&acc_full);
         }
-        mma_commit(&acc_full);
     } else if (warp == kLoadWarp && lane == 0) {
-        // ---------------- loader: the P tile (swizzled) and the V rows ------
-        const int y_p = (int)(head * s_q + i0), y_v0 = (int)(head * s_k);
-        for (int sl = 0; sl < nsl; ++sl) {
-            const int ss = sl % kSS;
-            if (sl >= kSS) mbar_wait(&sempty[ss], (uint32_t)(((sl / kSS) + 1) & 1));
-            unsigned char* sp = stage_ptr + ss * Cfg::kSlice;
-            mbar_expect_tx(&sfull[ss], Cfg::kPbytes + Cfg::kVbytes + Cfg::kMbytes);
-            if (!DV) {
-                tma_load_2d(sp, &tm_p, sl * kTK, y_p, &sfull[ss]);
-                tma_load_2d(sp + Cfg::kPbytes, &tm_v, 0, y_v0 + sl * kTK, &sfull[ss]);
-            } else {  // P rows [kTK x 256], dO rows [kTK x N], mask words [kTK x 8]
-                const int y = (int)(head * s_q) + sl * kTK;
-                tma_load_2d(sp, &tm_p, i0, y, &sfull[ss]);
-                tma_load_2d(sp + Cfg::kPbytes, &tm_v, 0, y, &sfull[ss]);
-                tma_load_2d(sp + Cfg::kPbytes + Cfg::kVbytes, &tm_m, i0 / 32, y, &sfull[ss]);
+        // ---------------- loader: the P tile and the V / dO rows -------------
+        for (int k = 0; k < myn; ++k) {
+            const int tile = (int)blockIdx.x + k * (int)gridDim.x;
+            const int64_t head = tile / iblocks;
+            const int i0 = (tile % iblocks) * kCM;
+            const int y_p = (int)(head * s_q + i0), y_v0 = (int)(head * s_k);
+            for (int sl = 0; sl < nsl; ++sl) {
+                const int64_t gs = (int64_t)k * nsl + sl;
+                const int ss = (int)(gs % kSS);
+                if (gs >= kSS) mbar_wait(&sempty[ss], (uint32_t)(((gs / kSS) + 1) & 1));
+                unsigned char* sp = stage_ptr + ss * Cfg::kSlice;
+                mbar_expect_tx(&sfull[ss], Cfg::kPbytes + Cfg::kVbytes + Cfg::kMbytes);
+                if (!DV) {
+                    tma_load_2d(sp, &tm_p, sl * kTK, y_p, &sfull[ss]);
+                    tma_load_2d(sp + Cfg::kPbytes, &tm_v, 0, y_v0 + sl * kTK, &sfull[ss]);
+                } else {  // P rows [kTK x 256], dO rows [kTK x N], mask words [kTK x 8]
+                    const int y = (int)(head * s_q) + sl * kTK;
+                    tma_load_2d(sp, &tm_p, i0, y, &sfull[ss]);
+                    tma_load_2d(sp + Cfg::kPbytes, &tm_v, 0, y, &sfull[ss]);
+                    tma_load_2d(sp + Cfg::kPbytes + Cfg::kVbytes, &tm_m, i0 / 32, y, &sfull[ss]);
+                }
             }
         }
     }
@@ -1319,8 +1374,10 @@ cudaError_t launch_ctx(const float* P, const uint32_t* mask, double scale, const
     auto k = drain ? ctx_recompute_gemm_ta_kernel<N, true, false>
                    : ctx_recompute_gemm_ta_kernel<N, false, false>;
     const size_t smem = drain ? CtxTaCfg<N, true>::kSmem : CtxTaCfg<N, false>::kSmem;
+    // persistent (one CTA per SM) unless drained (one tile per CTA)
+    const int g = drain || !TM_GEMM_PERSIST ? (int)grid : grid_for((const void*)k, kCThreads, smem, grid);
     (void)grid_for((const void*)k, kCThreads, smem, 1);
-    launch(k, (int)grid, kCThreads, smem, st)(tp, tv, tv, mask, scale, ctx, (int)s_q, (int)s_k);
+    launch(k, g, kCThreads, smem, st)(tp, tv, tv, mask, scale, ctx, (int)s_q, (int)s_k, (int)grid);
     return cudaGetLastError();
 }
 
@@ -1343,9 +1400,10 @@ cudaError_t launch_dv_ta(const float* P, const uint32_t* mask, double scale, con
     auto k = drain ? ctx_recompute_gemm_ta_kernel<N, true, true>
                    : ctx_recompute_gemm_ta_kernel<N, false, true>;
     const size_t smem = drain ? CtxTaCfg<N, true, true>::kSmem : CtxTaCfg<N, false, true>::kSmem;
-    (void)grid_for((const void*)k, kCThreads, smem, 1);
     const int64_t grid = heads * (s_k / kCM);
-    launch(k, (int)grid, kCThreads, smem, st)(tp, to, tmk, mask, scale, dV, (int)s_q, (int)s_k);
+    const int g = drain || !TM_GEMM_PERSIST ? (int)grid : grid_for((const void*)k, kCThreads, smem, grid);
+    (void)grid_for((const void*)k, kCThreads, smem, 1);
+    launch(k, g, kCThreads, smem, st)(tp, to, tmk, mask, scale, dV, (int)s_q, (int)s_k, (int)grid);
     return cudaGetLastError();
 }
 

@@ -159,3 +159,30 @@ def test_ctx_refusals(tops, cuda):
     with pytest.raises(TempoError) as e:
         tops.attn_dropout_ctx(P, m, 0.1, V)  # s_k % 32 != 0
     assert e.value.kind == "Unsupported"
+
+
+@pytest.mark.parametrize("heads,s_q,s_k,d", [(300, 256, 256, 64), (200, 300, 128, 64),
+                                             (333, 256, 512, 32)])
+def test_persistent_many_tiles(tops, cuda, heads, s_q, s_k, d):
+    """More (head, 256-row) tiles than SMs: each persistent CTA loops over
+    several tiles, its slice ring and accumulator hand-off running on across
+    tile boundaries (incl. ragged query blocks).  ctx and dV against the fp64
+    product of the forward's D."""
+    import torch
+    p = 0.1
+    g = torch.Generator(device=cuda)
+    g.manual_seed(heads + s_q + d)
+    z = torch.randn(heads * s_q, s_k, device=cuda, generator=g) * 2
+    P, D, m = tops.softmax_dropout_fwd(z, p, seed=heads)
+    V = torch.randn(heads, s_k, d, device=cuda, generator=g)
+    dO = torch.randn(heads, s_q, d, device=cuda, generator=g)
+    Dd = D.view(heads, s_q, s_k).double()
+    ctx = tops.attn_dropout_ctx(P.view(heads, s_q, s_k), m, p, V)
+    ref = torch.matmul(Dd, V.double())
+    mag = torch.matmul(Dd.abs(), V.double().abs())
+    assert bool(((ctx.double() - ref).abs() <= 1e-5 * (ref.abs() + mag)).all())
+    if s_q % 32 == 0 and s_k % 256 == 0:
+        dV = tops.attn_dropout_dv(P.view(heads, s_q, s_k), m, p, dO)
+        refv = torch.matmul(Dd.transpose(1, 2), dO.double())
+        magv = torch.matmul(Dd.abs().transpose(1, 2), dO.double().abs())
+        assert bool(((dV.double() - refv).abs() <= 1e-5 * (refv.abs() + magv)).all())
