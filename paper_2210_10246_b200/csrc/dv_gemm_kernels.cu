@@ -1246,29 +1246,34 @@ __global__ void __launch_bounds__(kCThreads, 1) ctx_recompute_gemm_ta_kernel(
             } else {
                 mbar_wait(&acc_full, (uint32_t)(k & 1));
                 tc_fence_after();
+                // all of this thread's sums into registers first, then free
+                // the accumulators (the MMA lane starts the next tile) and
+                // store while it runs
+                float* v = racc;  // N/2 columns
 #pragma unroll
-                for (int c0 = half * (N / 2); c0 < (half + 1) * (N / 2); c0 += 16) {
-                    float v[16];
-                    const uint32_t ta = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(Cfg::kAcc0 + emb * N + c0);
-                    tmem_ld16(ta, v);
+                for (int c0 = 0; c0 < N / 2; c0 += 16) {
+                    float w16[16];
+                    const uint32_t ta = tmem + ((uint32_t)(quad * 32) << 16) +
+                                        (uint32_t)(Cfg::kAcc0 + emb * N + half * (N / 2) + c0);
+                    tmem_ld16(ta, w16);
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) v[c0 + i] = w16[i];
 #pragma unroll
                     for (int set = 1; set < kSets; ++set) {
-                        float wv[16];
-                        tmem_ld16(ta + (uint32_t)(set * 2 * N), wv);
+                        tmem_ld16(ta + (uint32_t)(set * 2 * N), w16);
 #pragma unroll
-                        for (int i = 0; i < 16; ++i) v[i] += wv[i];
-                    }
-                    if (store) {
-#pragma unroll
-                        for (int i = 0; i < 16; i += 4)
-                            st_stream(reinterpret_cast<float4*>(out + c0 + i),
-                                      make_float4(v[i] * sc, v[i + 1] * sc, v[i + 2] * sc, v[i + 3] * sc));
+                        for (int i = 0; i < 16; ++i) v[c0 + i] += w16[i];
                     }
                 }
-                // accumulators read: the MMA lane may start the next tile
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&acc_empty);
+                if (store) {
+#pragma unroll
+                    for (int i = 0; i < N / 2; i += 4)
+                        st_stream(reinterpret_cast<float4*>(out + half * (N / 2) + i),
+                                  make_float4(v[i] * sc, v[i + 1] * sc, v[i + 2] * sc, v[i + 3] * sc));
+                }
             }
         }
     } else if (warp == kMMAWarp && lane == 0) {
