@@ -219,9 +219,10 @@ struct TapeNode {
     std::vector<NodeId> inputs;
     std::vector<LazyStash> stashes;
     BackwardFn backward;
-    Tensor value;
+    Tensor value;  // undefined while a lazy node's value is not yet needed
     std::vector<const void*> charged;
     std::optional<RecomputeRecipe> output_recipe;
+    bool lazy = false;  // value = run_recompute_rule(*output_recipe), built on first read
 };
 
 class GradientMap {
@@ -244,8 +245,17 @@ public:
     void charge(NodeId id, const std::string& tag, StashRole role, const BoolMask& m);
     void charge(NodeId id, const std::string& tag, StashRole role, const Tensor& t);
     void set_output_recipe(NodeId id, RecomputeRecipe recipe);
+    // A node whose forward value is its output recipe, built only when read
+    // (Tape::value): a consumer that can fuse the recipe into its own kernel
+    // (Graph::matmul with a dropout-rescale left operand: the tcgen05 ctx
+    // GEMM) never materialises it.  The recipe's result_shape is the shape.
+    NodeId record_lazy(std::string op, std::string tag, std::vector<NodeId> inputs,
+                       RecomputeRecipe recipe, std::vector<LazyStash> stashes,
+                       BackwardFn backward);
     const TapeNode& node(NodeId id) const;
-    const Tensor& value(NodeId id) const;
+    const Tensor& value(NodeId id) const;  // materialises a lazy node's value
+    bool value_pending(NodeId id) const;   // lazy and not yet materialised
+    const Shape& value_shape(NodeId id) const;
     std::size_t size() const { return nodes_.size(); }
     // tape.hpp:139.  Like the reference's (synchronous, CPU) backward it
     // returns with every gradient computed: it synchronizes the graph's

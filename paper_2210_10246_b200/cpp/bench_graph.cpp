@@ -101,12 +101,14 @@ int main(int argc, char** argv) {
     cudaEventElapsedTime(&ms, e0, e1);
     ms /= steps;
     const double wall_ms = std::chrono::duration<double, std::milli>(h1 - h0).count() / steps;
-    // algorithmic bytes moved, this chain: attention fwd writes
-    // P, D, reads z (12 B + 1 bit read); its fused bwd reads dD, P, bits and
-    // writes dZ (12.125); GELU 8.125 + 12.125; each hidden dropout 8.125
-    // fwd + 8.125 bwd; each LN 8 + 12 (+ rows/cols terms)
+    // algorithmic bytes moved, this chain: attention fwd reads
+    // z and the bits and writes P (8.125 B: the dropout output D is the
+    // node's lazy value and nothing here reads it -- a ctx GEMM consumer
+    // would rebuild it in its tcgen05 kernel); its fused bwd reads dD, P,
+    // bits and writes dZ (12.125); GELU 8.125 + 12.125; each hidden dropout
+    // 8.125 fwd + 8.125 bwd; each LN 8 + 12 (+ rows/cols terms)
     const double na = (double)R * S, nh = (double)T * H, ng = (double)T * 4 * H;
-    const double bytes = na * (12.125 + 12.125) + ng * (8.125 + 12.125) +
+    const double bytes = na * (8.125 + 12.125) + ng * (8.125 + 12.125) +
                          2 * nh * (8.125 + 8.125) + 2 * (8 * nh + 4 * T + 8 * H) +
                          2 * (12 * nh + 4 * T + 16 * H);
     std::printf("{\"what\": \"bench.py op chain through the C++ operator API (Graph/Tape, "

@@ -481,16 +481,56 @@ const TapeNode& Tape::node(NodeId id) const {
     check_node_id(id);
     return nodes_[id];
 }
-const Tensor& Tape::value(NodeId id) const { return node(id).value; }
+NodeId Tape::record_lazy(std::string op, std::string tag, std::vector<NodeId> inputs,
+                         RecomputeRecipe recipe, std::vector<LazyStash> stashes,
+                         BackwardFn backward) {
+    if (backward_done_) throw StateError("record on a tape whose backward already ran");
+    for (NodeId in : inputs) check_node_id(in);
+    TapeNode node;
+    node.op = std::move(op);
+    node.tag = std::move(tag);
+    node.inputs = std::move(inputs);
+    node.backward = std::move(backward);
+    node.stashes = std::move(stashes);
+    node.output_recipe = std::move(recipe);
+    node.lazy = true;
+    if (ledger_) {
+        for (const LazyStash& s : node.stashes) {
+            if (s.is_materialized() && s.charged()) {
+                ledger_->record(s.tag(), s.role(), s.stored());
+                node.charged.push_back(s.stored().ident());
+            }
+        }
+    }
+    nodes_.push_back(std::move(node));
+    return (NodeId)(nodes_.size() - 1);
+}
+
+const Tensor& Tape::value(NodeId id) const {
+    const TapeNode& nd = node(id);
+    if (nd.lazy && !nd.value.defined()) {  // first read: run the recipe on the tape's stream
+        StreamScope scope(stream_ ? *stream_ : current_stream());
+        const_cast<TapeNode&>(nd).value = run_recompute_rule(*nd.output_recipe);
+    }
+    return nd.value;
+}
+bool Tape::value_pending(NodeId id) const {
+    const TapeNode& nd = node(id);
+    return nd.lazy && !nd.value.defined();
+}
+const Shape& Tape::value_shape(NodeId id) const {
+    const TapeNode& nd = node(id);
+    return value_pending(id) ? nd.output_recipe->result_shape : nd.value.shape();
+}
 
 GradientMap Tape::backward(NodeId root, Tensor seed, bool synchronize) {
     check_node_id(root);
     if (backward_done_) throw StateError("backward already ran on this tape");
     if (!seed.defined()) throw ParamError("backward needs a seed gradient");
-    if (seed.shape() != nodes_[root].value.shape())
+    if (seed.shape() != value_shape(root))
         throw DimensionError("seed shape " + shape_str(seed.shape()) +
                              " does not match root value shape " +
-                             shape_str(nodes_[root].value.shape()));
+                             shape_str(value_shape(root)));
     backward_done_ = true;
     const tempo_stream_t st = stream_ ? *stream_ : nullptr;
     StreamScope scope(st);
@@ -510,7 +550,7 @@ GradientMap Tape::backward(NodeId root, Tensor seed, bool synchronize) {
         for (std::size_t j = 0; j < gin.size(); ++j) {
             if (!gin[j].defined()) continue;
             NodeId in = nd.inputs[j];
-            if (gin[j].shape() != nodes_[in].value.shape())
+            if (gin[j].shape() != value_shape(in))
                 throw InvariantError("op '" + nd.op + "' gradient " + std::to_string(j) +
                                      " has shape " + shape_str(gin[j].shape()));
             if (grads[in].defined()) {  // fan-out accumulation (tape.cpp:225-226)
@@ -572,7 +612,7 @@ const Tensor& BackwardCtx::input_value(std::size_t i) const {
     if (i >= nd.inputs.size())
         throw ParamError("input index " + std::to_string(i) + " out of range for op '" + nd.op +
                          "'");
-    return tape_->nodes_[nd.inputs[i]].value;
+    return tape_->value(nd.inputs[i]);
 }
 
 void BackwardCtx::release_temps() {
@@ -697,14 +737,48 @@ Tensor fused_dropout_dv(tempo_stream_t st, const RecomputeRecipe& recipe, const 
     return dv;
 }
 
+// ctx = D V for D = the (unmaterialised) output of a dropout-rescale recipe:
+// the forward consumer of the recompute, fused into the tcgen05 GEMM
+// (tempo_attn_dropout_ctx).  Undefined Tensor outside the kernel's envelope.
+Tensor fused_dropout_ctx(tempo_stream_t st, const RecomputeRecipe& recipe, const Tensor& v) {
+    if (recipe.rule != "dropout-rescale" || recipe.masks.size() != 1) return Tensor();
+    std::vector<Tensor> src = recipe.lock_sources();
+    if (src.size() != 1) return Tensor();
+    const Tensor& P = src[0];
+    const Shape& ps = P.shape();
+    const Shape& vs = v.shape();
+    if (ps.size() < 2 || vs.size() != ps.size() ||
+        !std::equal(ps.begin(), ps.end() - 2, vs.begin()))
+        return Tensor();
+    const MatDims dp = mat_dims(ps, "matmul"), dv = mat_dims(vs, "matmul");
+    if (dv.r != dp.c) return Tensor();
+    Tensor ctx = Tensor::empty(with_last2(ps, dp.r, dv.c));
+    const int rc = tempo_attn_dropout_ctx(P.data(), recipe.masks[0].words(), recipe.scalars.at("p"),
+                                          v.data(), ctx.data(), dp.batch, dp.r, dp.c, dv.c, st);
+    if (rc == TEMPO_ERR_UNSUPPORTED || rc == TEMPO_ERR_ALIGNMENT) return Tensor();
+    check(rc);
+    return ctx;
+}
+
 NodeId Graph::matmul(NodeId a, NodeId b, std::string tag) {  // graph.cpp:32-51
     StreamScope scope_(stream);
-    const Tensor& va = tape.value(a);
     const Tensor& vb = tape.value(b);
-    if (va.shape().size() != vb.shape().size())
-        throw DimensionError("graph matmul needs equal-rank operands, got " +
-                             shape_str(va.shape()) + " and " + shape_str(vb.shape()));
-    Tensor out = mm(stream, va, vb, false, false);
+    // a dropout_recompute left operand not yet materialised: D never is
+    Tensor out;
+    if (tape.value_pending(a)) {
+        if (tape.value_shape(a).size() != vb.shape().size())
+            throw DimensionError("graph matmul needs equal-rank operands, got " +
+                                 shape_str(tape.value_shape(a)) + " and " + shape_str(vb.shape()));
+        same_batch(tape.value_shape(a), vb.shape(), "matmul");
+        out = fused_dropout_ctx(stream, *tape.node(a).output_recipe, vb);
+    }
+    if (!out.defined()) {
+        const Tensor& va = tape.value(a);
+        if (va.shape().size() != vb.shape().size())
+            throw DimensionError("graph matmul needs equal-rank operands, got " +
+                                 shape_str(va.shape()) + " and " + shape_str(vb.shape()));
+        out = mm(stream, va, vb, false, false);
+    }
     tag = fallback_tag(std::move(tag), "matmul", tape.size());
     tempo_stream_t st = stream;
     return tape.record("matmul", tag, {a, b}, out,
@@ -953,27 +1027,31 @@ NodeId softmax(Graph& g, NodeId z, std::string tag) {  // ops_tempo.cpp:158-166
                          });
 }
 
-static NodeId record_dropout_recompute(Graph& g, NodeId x, const Tensor& y, double p,
-                                       const BoolMask& mask, std::string tag,
-                                       const std::string& mask_tag) {
+// The dropout_recompute node (ops_tempo.cpp:168-194) with a LAZY value: its
+// output D = mask ? x / (1-p) : 0 is the node's recipe ("dropout-rescale"
+// over x and the mask) and is built only when someone reads it; the
+// attention context GEMM (Graph::matmul) consumes the recipe directly, so in
+// tempo_ops::sdpa D is materialised in neither pass.  Reading g.value(d)
+// gives the same bits as the eager dropout (the recipe IS that kernel).
+static NodeId record_dropout_recompute(Graph& g, NodeId x, double p, const BoolMask& mask,
+                                       std::string tag, const std::string& mask_tag) {
     const Tensor& vx = g.value(x);
     RecomputeRecipe recipe;
     recipe.rule = "dropout-rescale";
     recipe.sources = {vx.weak_storage()};
     recipe.masks = {mask};
     recipe.scalars["p"] = p;
-    recipe.result_shape = y.shape();
+    recipe.result_shape = vx.shape();
     tempo_stream_t st = g.stream;
-    NodeId id = g.tape.record("dropout_recompute", std::move(tag), {x}, y, {},
-                              [mask, p, st](BackwardCtx& ctx) -> std::vector<Tensor> {
-                                  const Tensor& gy = ctx.grad_out();
-                                  Tensor dx = Tensor::empty(gy.shape());
-                                  check(tempo_dropout_bwd(gy.data(), mask.words(), p, dx.data(),
-                                                          gy.numel(), st));
-                                  return {dx};
-                              });
+    NodeId id = g.tape.record_lazy("dropout_recompute", std::move(tag), {x}, std::move(recipe), {},
+                                   [mask, p, st](BackwardCtx& ctx) -> std::vector<Tensor> {
+                                       const Tensor& gy = ctx.grad_out();
+                                       Tensor dx = Tensor::empty(gy.shape());
+                                       check(tempo_dropout_bwd(gy.data(), mask.words(), p, dx.data(),
+                                                               gy.numel(), st));
+                                       return {dx};
+                                   });
     g.tape.charge(id, mask_tag, StashRole::OpOwnStash, mask);
-    g.tape.set_output_recipe(id, std::move(recipe));
     return id;
 }
 
@@ -985,10 +1063,8 @@ NodeId dropout_recompute(Graph& g, NodeId x, double p, BoolMask mask, std::strin
     if (!g.ledger.is_live(vx.ident()))
         throw ConfigError("dropout_recompute requires its input to be retained upstream");
     require_same_shape(vx.shape(), mask.shape(), "mask_scale");
-    Tensor y = Tensor::empty(vx.shape());
-    check(tempo_dropout_fwd(vx.data(), p, TEMPO_MASK_SUPPLIED, mask.words(), 0, 0, y.data(),
-                            vx.numel(), g.stream));
-    return record_dropout_recompute(g, x, y, p, mask, std::move(tag), mask_tag);
+    if (!(p >= 0.0 && p < 1.0)) throw ParamError("dropout p must be in [0, 1)");
+    return record_dropout_recompute(g, x, p, mask, std::move(tag), mask_tag);
 }
 
 NodeId softmax_dropout(Graph& g, NodeId z, double p, BoolMask mask, std::uint64_t seed,
@@ -1003,10 +1079,11 @@ NodeId softmax_dropout(Graph& g, NodeId z, double p, BoolMask mask, std::uint64_
     const bool generate = !mask.defined();
     if (generate) mask = BoolMask::empty(vz.shape());
     require_same_shape(vz.shape(), mask.shape(), "mask_scale");
-    Tensor P = Tensor::empty(vz.shape()), D = Tensor::empty(vz.shape());
+    // P and the mask bits only: D is the lazy value of the dropout node
+    Tensor P = Tensor::empty(vz.shape());
     check(tempo_softmax_dropout_fwd(vz.data(), p,
                                     generate ? TEMPO_MASK_PHILOX : TEMPO_MASK_SUPPLIED,
-                                    mask.words(), seed, offset, P.data(), D.data(), rows, c,
+                                    mask.words(), seed, offset, P.data(), nullptr, rows, c,
                                     g.stream));
     tempo_stream_t st = g.stream;
     if (!probs_out) {
@@ -1018,9 +1095,9 @@ NodeId softmax_dropout(Graph& g, NodeId z, double p, BoolMask mask, std::uint64_
         recipe.sources = {P.weak_storage()};
         recipe.masks = {mask};
         recipe.scalars["p"] = p;
-        recipe.result_shape = D.shape();
-        NodeId id = g.tape.record(
-            "softmax_dropout", drop_tag, {z}, D,
+        recipe.result_shape = P.shape();
+        NodeId id = g.tape.record_lazy(
+            "softmax_dropout", drop_tag, {z}, std::move(recipe),
             {LazyStash::materialized(probs_tag, StashRole::OpOwnStash, P)},
             [st, rows, c, mask, p](BackwardCtx& ctx) -> std::vector<Tensor> {
                 const Tensor& pv = ctx.stash(0);
@@ -1030,7 +1107,6 @@ NodeId softmax_dropout(Graph& g, NodeId z, double p, BoolMask mask, std::uint64_
                 return {dz};
             });
         g.tape.charge(id, mask_tag, StashRole::OpOwnStash, mask);
-        g.tape.set_output_recipe(id, std::move(recipe));
         return id;
     }
     NodeId pn = g.tape.record("softmax_ip", probs_tag, {z}, P,
@@ -1043,7 +1119,7 @@ NodeId softmax_dropout(Graph& g, NodeId z, double p, BoolMask mask, std::uint64_
                                   return {dz};
                               });
     if (probs_out) *probs_out = pn;
-    return record_dropout_recompute(g, pn, D, p, mask, drop_tag, mask_tag);
+    return record_dropout_recompute(g, pn, p, mask, drop_tag, mask_tag);
 }
 
 NodeId sdpa(Graph& g, NodeId q, NodeId k, NodeId v, double p, BoolMask mask,

@@ -231,10 +231,13 @@ static void test_dropout_recompute() {
     NodeId pr = tempo_ops::softmax(g, z, "sm");
     BoolMask mask = BoolMask::bernoulli_keep({rows, c}, 0.25, 19);
     NodeId d = tempo_ops::dropout_recompute(g, pr, 0.25, mask, "d", "d_mask");
+    CHECK(g.tape.value_pending(d));  // lazy: built on first read
+    CHECK(g.tape.value_shape(d) == Shape({rows, c}));
     auto by_tag = g.ledger.live_by_tag();
     CHECK(by_tag.count("d") == 0);
     CHECK(by_tag.at("d_mask") == (rows * c) / 8);  // bits, vs 256 B in the reference
     std::vector<float> P = g.value(pr).to_host(), D = g.value(d).to_host();
+    CHECK(!g.tape.value_pending(d));
     std::vector<std::uint8_t> keep = mask.to_bytes();
     for (std::int64_t i = 0; i < rows * c; ++i) {
         float r = keep[i] ? (float)((double)P[i] * (1.0 / 0.75)) : 0.0f;
@@ -386,6 +389,8 @@ static void sdpa_case(std::int64_t B, std::int64_t A, std::int64_t S, std::int64
     NodeId k = g.leaf(Tensor::from_host({B, A, S, d}, kh), "k");
     NodeId v = g.leaf(Tensor::from_host({B, A, S, d}, vh), "v");
     NodeId o = tempo_ops::sdpa(g, q, k, v, p, mask, "attn_");
+    // the context GEMM consumed D's recipe (tcgen05 ctx GEMM): D was never built
+    CHECK(g.tape.node(o - 1).op == "dropout_recompute" && g.tape.value_pending(o - 1));
     auto tags = g.ledger.live_by_tag();
     CHECK(tags.count("attn_drop_out") == 0);         // D is never stashed
     CHECK(tags.at("attn_probs") == ns * 4);           // P (fp32)
