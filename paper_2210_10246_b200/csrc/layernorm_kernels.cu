@@ -57,6 +57,18 @@ constexpr int kRows = 4;           // rows in flight per CTA iteration (forward)
 constexpr int kRowsB = TM_LN_BWD_ROWS;  // rows per CTA iteration (backward)
 constexpr int kStagesB = TM_LN_BWD_STAGES;
 constexpr int kMaxThreads = 512;  // cols <= 2048 on the vector path
+// 2048 < cols <= 4096: the vector backward with 1024-thread CTAs (one row
+// per thread-column group, ROWS-row tiles; 64 registers) instead of the
+// cluster kernel
+#ifndef TM_LN_BWD_WIDE
+#define TM_LN_BWD_WIDE 1
+#endif
+#ifndef TM_LN_BWD_WIDE_ROWS
+#define TM_LN_BWD_WIDE_ROWS 1
+#endif
+constexpr int kWideThreads = 1024;
+constexpr int kRowsW = TM_LN_BWD_WIDE_ROWS;
+constexpr int kVecMaxCols = 4 * (TM_LN_BWD_WIDE ? kWideThreads : kMaxThreads);
 constexpr double kGammaMin = 1e-12;  // ops_tempo.hpp:46
 
 // Block-wide sum of kN values per thread.  `red` holds 2 buffers of
@@ -753,7 +765,7 @@ __global__ void __launch_bounds__(256) ln_fwd_generic_kernel(
 // projection's gradient d(proj) = keep ? float(double(dx) * scale) : 0
 // (dropout_backward, ops_reference.cpp:155-161) is written beside it -- one
 // pass instead of LN backward + a dropout backward re-reading dx.
-template <int NT, int CPT, bool DROP = false>
+template <int NT, int CPT, bool DROP = false, int ROWS = kRowsB>
 __global__ void __launch_bounds__(NT) ln_bwd_vec_kernel(
     const float* __restrict__ dy, const float* __restrict__ y, const float* __restrict__ rstd,
     const float* __restrict__ gamma, const float* __restrict__ beta, float* __restrict__ dx,
@@ -769,18 +781,18 @@ __global__ void __launch_bounds__(NT) ln_bwd_vec_kernel(
     extern __shared__ __align__(128) unsigned char dsm[];
     uint64_t* full = reinterpret_cast<uint64_t*>(dsm);
     float* ring = reinterpret_cast<float*>(dsm + 128);
-    __shared__ float red[2 * 2 * kRowsB * 32];
+    __shared__ float red[2 * 2 * ROWS * 32];
     int phase = 0;
-    const int tile_floats = kRowsB * cols;  // per tensor; a stage holds dy then y
-    const int64_t ntiles = (rows + kRowsB - 1) / kRowsB;
+    const int tile_floats = ROWS * cols;  // per tensor; a stage holds dy then y
+    const int64_t ntiles = (rows + ROWS - 1) / ROWS;
     if (threadIdx.x == 0) {
         for (int s = 0; s < kStagesB; ++s) mbar_init(&full[s], 1);
         mbar_fence_init();
     }
     __syncthreads();
     auto issue = [&](int64_t t, int s) {
-        const int64_t r0 = t * kRowsB;
-        const int nr = (int)min((int64_t)kRowsB, rows - r0);
+        const int64_t r0 = t * ROWS;
+        const int nr = (int)min((int64_t)ROWS, rows - r0);
         const uint32_t bytes = (uint32_t)nr * (uint32_t)cols * 4u;
         mbar_expect_tx(&full[s], 2 * bytes);
         bulk_g2s(ring + (2 * s) * tile_floats, dy + r0 * cols, bytes, &full[s]);
@@ -796,7 +808,6 @@ __global__ void __launch_bounds__(NT) ln_bwd_vec_kernel(
     int cg[CPT];
     bool act[CPT];
     float gm[CPT][4], bt[CPT][4], igf[CPT][4];
-    double btd[CPT][4], igd[CPT][4];
     double pg[CPT][4], pb[CPT][4];  // fp64 column partials
 #pragma unroll
     for (int c = 0; c < CPT; ++c) {
@@ -812,9 +823,7 @@ __global__ void __launch_bounds__(NT) ln_bwd_vec_kernel(
         for (int k = 0; k < 4; ++k) {
             gm[c][k] = ga[k];
             bt[c][k] = ba[k];
-            igd[c][k] = 1.0 / (double)ga[k];
-            igf[c][k] = (float)igd[c][k];
-            btd[c][k] = (double)ba[k];
+            igf[c][k] = (float)(1.0 / (double)ga[k]);
             pg[c][k] = 0.0;
             pb[c][k] = 0.0;
         }
@@ -823,12 +832,12 @@ __global__ void __launch_bounds__(NT) ln_bwd_vec_kernel(
     // rstd (and, DROP, the mask words) of a tile are loaded one tile ahead:
     // they are needed only after the row reduction, and a global load issued
     // there would stall the whole output loop on its latency
-    float rs_nx[kRowsB];
-    uint32_t mw_nx[kRowsB][CPT];
+    float rs_nx[ROWS];
+    uint32_t mw_nx[ROWS][CPT];
     auto prefetch = [&](int64_t t) {
-        const int64_t q0 = t * kRowsB;
+        const int64_t q0 = t * ROWS;
 #pragma unroll
-        for (int i = 0; i < kRowsB; ++i) {
+        for (int i = 0; i < ROWS; ++i) {
             const bool in = t < ntiles && q0 + i < rows;
             rs_nx[i] = in ? __ldg(rstd + q0 + i) : 0.f;
             if (DROP) {
@@ -841,10 +850,10 @@ __global__ void __launch_bounds__(NT) ln_bwd_vec_kernel(
     prefetch(blockIdx.x);
     int it = 0;
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
-        float rsv[kRowsB];
-        uint32_t mwv[kRowsB][CPT];
+        float rsv[ROWS];
+        uint32_t mwv[ROWS][CPT];
 #pragma unroll
-        for (int i = 0; i < kRowsB; ++i) {
+        for (int i = 0; i < ROWS; ++i) {
             rsv[i] = rs_nx[i];
 #pragma unroll
             for (int c = 0; c < CPT; ++c) mwv[i][c] = DROP ? mw_nx[i][c] : 0u;
@@ -852,12 +861,12 @@ __global__ void __launch_bounds__(NT) ln_bwd_vec_kernel(
         prefetch(tile + gridDim.x);
         const int st = it % kStagesB;
         mbar_wait(&full[st], (uint32_t)((it / kStagesB) & 1));
-        const int64_t r0 = tile * kRowsB;
+        const int64_t r0 = tile * ROWS;
         const float* gs = ring + (2 * st) * tile_floats;
         const float* ys = ring + (2 * st + 1) * tile_floats;
-        float4 gv[kRowsB][CPT], yv[kRowsB][CPT];
+        float4 gv[ROWS][CPT], yv[ROWS][CPT];
 #pragma unroll
-        for (int i = 0; i < kRowsB; ++i) {
+        for (int i = 0; i < ROWS; ++i) {
 #pragma unroll
             for (int c = 0; c < CPT; ++c) {
                 gv[i][c] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -868,9 +877,9 @@ __global__ void __launch_bounds__(NT) ln_bwd_vec_kernel(
                 }
             }
         }
-        float s[2 * kRowsB];
+        float s[2 * ROWS];
 #pragma unroll
-        for (int i = 0; i < kRowsB; ++i) {
+        for (int i = 0; i < ROWS; ++i) {
             float s1 = 0.0f, s2 = 0.0f;
 #pragma unroll
             for (int c = 0; c < CPT; ++c) {
@@ -887,7 +896,7 @@ __global__ void __launch_bounds__(NT) ln_bwd_vec_kernel(
             s[2 * i] = s1;
             s[2 * i + 1] = s2;
         }
-        block_sum<2 * kRowsB>(s, red, phase);
+        block_sum<2 * ROWS>(s, red, phase);
         if (threadIdx.x == 0) {  // stage consumed by every thread: refill
             const int64_t nt = tile + (int64_t)kStagesB * gridDim.x;
             if (nt < ntiles) {
@@ -896,7 +905,7 @@ __global__ void __launch_bounds__(NT) ln_bwd_vec_kernel(
             }
         }
 #pragma unroll
-        for (int i = 0; i < kRowsB; ++i) {
+        for (int i = 0; i < ROWS; ++i) {
             if (r0 + i >= rows) continue;
             const float c1 = s[2 * i] * inv_m, c2 = s[2 * i + 1] * inv_m;
             const float rs = rsv[i];
@@ -940,7 +949,9 @@ __global__ void __launch_bounds__(NT) ln_bwd_vec_kernel(
         if (!act[c]) continue;
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-            wg[cg[c] * 4 + k] = fma(-btd[c][k], pb[c][k], pg[c][k]) * igd[c][k];
+            // fp64 1/gamma and beta rebuilt here (not kept live across the
+            // row loop: registers for the 1024-thread variant)
+            wg[cg[c] * 4 + k] = fma(-(double)bt[c][k], pb[c][k], pg[c][k]) * (1.0 / (double)gm[c][k]);
             wg[cols + cg[c] * 4 + k] = pb[c][k];
         }
     }
@@ -1423,8 +1434,8 @@ __global__ void __launch_bounds__(kPeerCols * kPeerRowGroups) ln_param_reduce_pe
 inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
 bool use_vec(int64_t cols, const void* a, const void* b, const void* c, const void* d,
-             const void* e) {
-    return cols % 4 == 0 && cols <= 4 * kMaxThreads && aligned16(a) && aligned16(b) &&
+             const void* e, int64_t max_cols = 4 * kMaxThreads) {
+    return cols % 4 == 0 && cols <= max_cols && aligned16(a) && aligned16(b) &&
            aligned16(c) && aligned16(d) && aligned16(e);
 }
 
@@ -1436,6 +1447,9 @@ int bwd_threads(int64_t cols) {
 }
 const void* bwd_vec_fn(int64_t cols, bool drop = false) {
     const int t = bwd_threads(cols);
+    if (t > kMaxThreads)  // (only with TM_LN_BWD_WIDE: use_vec / cluster_bwd_ok)
+        return drop ? (const void*)ln_bwd_vec_kernel<kWideThreads, 1, true, kRowsW>
+                    : (const void*)ln_bwd_vec_kernel<kWideThreads, 1, false, kRowsW>;
 #if TM_LN_BWD_CPT2  // (off by default: measured slower; not instantiated)
     if (bwd_cpt(cols) == 2)
         return t <= 256 ? (const void*)ln_bwd_vec_kernel<256, 2>
@@ -1451,7 +1465,10 @@ const void* bwd_vec_fn(int64_t cols, bool drop = false) {
 // Stage-1 grid for the backward: its CTA count is also the number of
 // partial rows in the workspace, so it depends only on (rows, cols, device).
 size_t fwd_smem(int64_t cols) { return 128 + (size_t)kStages * kRows * cols * sizeof(float); }
-size_t bwd_smem(int64_t cols) { return 128 + (size_t)kStagesB * 2 * kRowsB * cols * sizeof(float); }
+size_t bwd_smem(int64_t cols) {
+    const int rows = cols > 4 * kMaxThreads ? kRowsW : kRowsB;
+    return 128 + (size_t)kStagesB * 2 * rows * cols * sizeof(float);
+}
 
 // long-row paths (cols % 128 == 0): forward 2048 < cols <= 16384 (the fused
 // dropout -> add -> LayerNorm forward from 1024), backward up to 8192
@@ -1459,7 +1476,7 @@ bool long_fwd_ok(int64_t cols, int64_t min_cols) {
     return cols % 128 == 0 && cols > min_cols && cols <= 16 * kLongVPL * 128;
 }
 bool cluster_bwd_ok(int64_t cols) {
-    return cols % 4 == 0 && cols > 4 * kMaxThreads && cluster_k(cols) <= 8;
+    return cols % 4 == 0 && cols > kVecMaxCols && cluster_k(cols) <= 8;
 }
 // CTAs (a multiple of K): as many clusters as can be co-resident -- a
 // persistent grid with clusters waiting for a second wave would serialise
@@ -1513,7 +1530,8 @@ size_t generic_bwd_smem(int64_t cols) {
 }
 
 int bwd_grid(int64_t rows, int64_t cols, bool vec) {
-    int64_t work = vec ? (rows + kRowsB - 1) / kRowsB : rows;
+    const int tr = cols > 4 * kMaxThreads ? kRowsW : kRowsB;  // rows per tile
+    int64_t work = vec ? (rows + tr - 1) / tr : rows;
     const void* k = !vec ? (const void*)ln_bwd_generic_kernel : bwd_vec_fn(cols);
     int block = vec ? bwd_threads(cols) : 256;
     size_t smem = vec ? bwd_smem(cols) : generic_bwd_smem(cols);
@@ -1620,7 +1638,7 @@ size_t ln_bwd_workspace(int64_t rows, int64_t cols) {
     if (rows == 0 || cols == 0) return 0;
     // The vector/generic choice also depends on pointer alignment; size for
     // the larger of the two grids.
-    int gv = (cols % 4 == 0 && cols <= 4 * kMaxThreads) ? bwd_grid(rows, cols, true) : 0;
+    int gv = (cols % 4 == 0 && cols <= kVecMaxCols) ? bwd_grid(rows, cols, true) : 0;
     int gg = bwd_grid(rows, cols, false);
     int gl = cluster_bwd_ok(cols) ? bwd_cluster_grid(rows, cols) / cluster_k(cols) : 0;
     int g = gv > gg ? gv : gg;
@@ -1645,7 +1663,7 @@ cudaError_t launch_ln_bwd(const float* dy, const float* y, const float* rstd, co
     const bool aligned = aligned16(dy) && aligned16(y) && aligned16(dx) && aligned16(gamma) &&
                          aligned16(beta) && (!drop || aligned16(dproj));
     const bool clu = cluster_bwd_ok(cols) && aligned;
-    const bool vec = !clu && use_vec(cols, dy, y, dx, gamma, beta) &&
+    const bool vec = !clu && use_vec(cols, dy, y, dx, gamma, beta, kVecMaxCols) &&
                      (!drop || aligned16(dproj));
     // the grid (= the workspace's partial rows) is the plain kernel's, also
     // for the fused variant, so one workspace query serves both
