@@ -162,7 +162,8 @@ def test_ctx_refusals(tops, cuda):
 
 
 @pytest.mark.parametrize("heads,s_q,s_k,d", [(300, 256, 256, 64), (200, 300, 128, 64),
-                                             (333, 256, 512, 32)])
+                                             (333, 256, 512, 32), (500, 1, 64, 64),
+                                             (160, 257, 96, 32)])
 def test_persistent_many_tiles(tops, cuda, heads, s_q, s_k, d):
     """More (head, 256-row) tiles than SMs: each persistent CTA loops over
     several tiles, its slice ring and accumulator hand-off running on across
