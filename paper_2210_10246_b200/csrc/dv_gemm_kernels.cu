@@ -1071,6 +1071,11 @@ __global__ void __launch_bounds__(kCThreads, 1) ctx_recompute_gemm_ta_kernel(
     const int myn = (ntiles - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
     constexpr int kMMAWarp = kCSP / 32, kLoadWarp = kCSP / 32 + 1;
     constexpr int kArrive = kCSP / 32 / (kAlt ? 2 : 1);  // producer warps per slice
+    // ALT: each half must own its ring slots and operand stages (even ring
+    // depths) -- a half waiting on a slot the other half has not drained yet
+    // would wait two phases ahead, which an mbarrier parity wait cannot tell
+    // from the phase just completed (measured: kSS = 3 corrupts and faults)
+    static_assert(!kAlt || (kSS % 2 == 0 && kAS % 2 == 0), "ALT needs even ring depths");
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < kAS; ++s) {
