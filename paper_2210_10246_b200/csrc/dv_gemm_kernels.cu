@@ -977,6 +977,9 @@ __global__ void __launch_bounds__(kCThreads, 1) ctx_recompute_gemm_kernel(
 #ifndef TM_GEMM_PERSIST
 #define TM_GEMM_PERSIST 1  // undrained instantiation: one CTA per SM looping over tiles
 #endif
+#ifndef TM_GEMM_BALL
+#define TM_GEMM_BALL 1
+#endif
 #ifndef TM_GEMM_ALT
 #define TM_GEMM_ALT 1  // undrained instantiation: the producer halves alternate slices
 #endif
@@ -1121,8 +1124,11 @@ __global__ void __launch_bounds__(kCThreads, 1) ctx_recompute_gemm_ta_kernel(
         const int m = t % kCM, mb = m >> 7;
         const int grp = kAlt ? t / kCM : 0, h = kAlt ? 0 : t / kCM;
         const int tb = kAlt ? t % kCM : t;
-        const bool bwarp = tb < 128;
-        constexpr int kKV = kTK * N / 128;  // 16 / 8 (N = 64) or 8 / 4
+        // B producers: 4 warps of the slice's half, or for dV (TM_GEMM_BALL)
+        // all 8 (A/B: dV 289 -> 285 us, ctx 294 -> 296: ctx keeps 4)
+        constexpr int kBThreads = (TM_GEMM_BALL && kAlt && DV) ? kCM : 128;
+        const bool bwarp = tb < kBThreads;
+        constexpr int kKV = kTK * N / kBThreads;  // V / dO values per B thread
         const int bn = tb % N, kb = (tb / N) * kKV;
         const uint32_t lane_base = tmem + ((uint32_t)((warp & 3) * 32) << 16);
         constexpr int kSlPerWord = 32 / kTK;  // slices per mask word (2 or 1)
