@@ -163,6 +163,74 @@ __global__ void rate(long long* cyc, int iters) {
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tm) : "memory");
 }
 
+// the dV / ctx GEMM's per-slice issue pattern: 4 K-steps x 2 M-blocks x 3
+// products (lo.hi, hi.lo, hi.hi), A from TMEM, two B tiles (hi, lo) in
+// SWIZZLE_128B smem, accumulators rotating over 2 sets; one commit per slice
+__global__ void pattern(long long* cyc, int slices, int commit_each) {
+    extern __shared__ __align__(1024) unsigned char sm[];
+    unsigned char* base = (unsigned char*)(((uintptr_t)sm + 1023) & ~(uintptr_t)1023);
+    __shared__ uint64_t bar;
+    __shared__ uint32_t tbase;
+    int t = threadIdx.x, warp = t >> 5;
+    for (int i = t; i < 32768 / 4; i += blockDim.x) ((float*)base)[i] = 0.0f;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    if (t == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&bar)));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(su32(&tbase)) : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tm = tbase;
+    const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((64u >> 3) << 17) | ((128u >> 4) << 24);
+    if (t == 0) {
+        const uint32_t bhi = su32(base), blo = su32(base + 8192);
+        long long c0 = clock64();
+        int phase = 0;
+        for (int sl = 0; sl < slices; ++sl) {
+            const uint32_t a0 = tm + (sl & 1) * 128;  // A stage
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk) {
+                const uint64_t bh = desc(bhi + kk * 32, 16, 1024), bl = desc(blo + kk * 32, 16, 1024);
+                const int set = (sl * 4 + kk) & 1;
+#pragma unroll
+                for (int mb = 0; mb < 2; ++mb) {
+                    const uint32_t ah = a0 + mb * 64 + kk * 8;
+                    const uint32_t acc = tm + 256 + set * 128 + mb * 64;
+                    const uint32_t fresh = (sl == 0 && kk < 2);
+                    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                                 "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}\n"
+                                 ::"r"(acc), "r"(ah + 32), "l"(bh), "r"(idesc), "r"(1u - fresh));
+                    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                                 "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}\n"
+                                 ::"r"(acc), "r"(ah), "l"(bl), "r"(idesc), "r"(1u));
+                    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                                 "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}\n"
+                                 ::"r"(acc), "r"(ah), "l"(bh), "r"(idesc), "r"(1u));
+                }
+            }
+            if (commit_each) {  // commit + wait per slice: the round trip the GEMM pays
+                asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(&bar)) : "memory");
+                asm volatile("{\n\t.reg .pred p;\nW_%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t@!p bra W_%=;\n}" ::"r"(su32(&bar)), "r"(phase) : "memory");
+                phase ^= 1;
+            }
+        }
+        if (!commit_each) {
+            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(&bar)) : "memory");
+            asm volatile("{\n\t.reg .pred p;\nW_%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n\t@!p bra W_%=;\n}" ::"r"(su32(&bar)) : "memory");
+        }
+        cyc[blockIdx.x] = clock64() - c0;
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tm) : "memory");
+}
+
 template <int N, bool TA>
 void run_rate(long long* dc, int ctas) {
     auto k = rate<N, TA>;
@@ -217,6 +285,19 @@ int main() {
         run_rate<64, true>(dc, ctas); run_rate<64, false>(dc, ctas);
         run_rate<128, true>(dc, ctas); run_rate<128, false>(dc, ctas);
         run_rate<256, true>(dc, ctas); run_rate<256, false>(dc, ctas);
+    }
+    cudaFuncSetAttribute(pattern, cudaFuncAttributeMaxDynamicSharedMemorySize, 40000);
+    for (int ce = 0; ce < 2; ++ce) {
+        const int slices = 512;
+        pattern<<<148, 128, 40000>>>(dc, slices, ce);
+        cudaDeviceSynchronize();
+        pattern<<<148, 128, 40000>>>(dc, slices, ce);
+        cudaError_t e = cudaDeviceSynchronize();
+        std::vector<long long> c(148);
+        cudaMemcpy(c.data(), dc, 148 * 8, cudaMemcpyDeviceToHost);
+        long long mx = 0; for (auto v : c) mx = v > mx ? v : mx;
+        printf("GEMM slice pattern (24 MMAs N=64, A tmem, 2 sets)%s: %.1f cycles/slice, %.1f cycles/MMA (%s)\n",
+               ce ? " + commit/wait per slice" : "", (double)mx / slices, (double)mx / (slices * 24), cudaGetErrorString(e));
     }
     return 0;
 }
