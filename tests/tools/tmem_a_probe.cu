@@ -197,29 +197,45 @@ __global__ void pattern(long long* cyc, int slices, int commit_each) {
             for (int kk = 0; kk < 4; ++kk) {
                 const uint64_t bh = desc(bhi + kk * 32, 16, 1024), bl = desc(blo + kk * 32, 16, 1024);
                 const int set = (sl * 4 + kk) & 1;
+                const uint32_t fresh = (sl == 0 && kk < 2);
+                if (!(commit_each & 2)) {  // the GEMM's order: 3 products per accumulator in a row
 #pragma unroll
-                for (int mb = 0; mb < 2; ++mb) {
-                    const uint32_t ah = a0 + mb * 64 + kk * 8;
-                    const uint32_t acc = tm + 256 + set * 128 + mb * 64;
-                    const uint32_t fresh = (sl == 0 && kk < 2);
-                    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-                                 "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}\n"
-                                 ::"r"(acc), "r"(ah + 32), "l"(bh), "r"(idesc), "r"(1u - fresh));
-                    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-                                 "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}\n"
-                                 ::"r"(acc), "r"(ah), "l"(bl), "r"(idesc), "r"(1u));
-                    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-                                 "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}\n"
-                                 ::"r"(acc), "r"(ah), "l"(bh), "r"(idesc), "r"(1u));
+                    for (int mb = 0; mb < 2; ++mb) {
+                        const uint32_t ah = a0 + mb * 64 + kk * 8;
+                        const uint32_t acc = tm + 256 + set * 128 + mb * 64;
+                        asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                                     "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}\n"
+                                     ::"r"(acc), "r"(ah + 32), "l"(bh), "r"(idesc), "r"(1u - fresh));
+                        asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                                     "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}\n"
+                                     ::"r"(acc), "r"(ah), "l"(bl), "r"(idesc), "r"(1u));
+                        asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                                     "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}\n"
+                                     ::"r"(acc), "r"(ah), "l"(bh), "r"(idesc), "r"(1u));
+                    }
+                } else {  // interleaved over the two M-blocks
+#pragma unroll
+                    for (int q = 0; q < 3; ++q) {
+#pragma unroll
+                        for (int mb = 0; mb < 2; ++mb) {
+                            const uint32_t ah = a0 + mb * 64 + kk * 8;
+                            const uint32_t acc = tm + 256 + set * 128 + mb * 64;
+                            const uint32_t aa = q == 0 ? ah + 32 : ah;
+                            const uint64_t bb = q == 1 ? bl : bh;
+                            asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                                         "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}\n"
+                                         ::"r"(acc), "r"(aa), "l"(bb), "r"(idesc), "r"(q == 0 ? 1u - fresh : 1u));
+                        }
+                    }
                 }
             }
-            if (commit_each) {  // commit + wait per slice: the round trip the GEMM pays
+            if (commit_each & 1) {  // commit + wait per slice: the round trip the GEMM pays
                 asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(&bar)) : "memory");
                 asm volatile("{\n\t.reg .pred p;\nW_%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t@!p bra W_%=;\n}" ::"r"(su32(&bar)), "r"(phase) : "memory");
                 phase ^= 1;
             }
         }
-        if (!commit_each) {
+        if (!(commit_each & 1)) {
             asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(&bar)) : "memory");
             asm volatile("{\n\t.reg .pred p;\nW_%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n\t@!p bra W_%=;\n}" ::"r"(su32(&bar)) : "memory");
         }
@@ -287,7 +303,7 @@ int main() {
         run_rate<256, true>(dc, ctas); run_rate<256, false>(dc, ctas);
     }
     cudaFuncSetAttribute(pattern, cudaFuncAttributeMaxDynamicSharedMemorySize, 40000);
-    for (int ce = 0; ce < 2; ++ce) {
+    for (int ce = 0; ce < 4; ++ce) {
         const int slices = 512;
         pattern<<<148, 128, 40000>>>(dc, slices, ce);
         cudaDeviceSynchronize();
@@ -296,8 +312,8 @@ int main() {
         std::vector<long long> c(148);
         cudaMemcpy(c.data(), dc, 148 * 8, cudaMemcpyDeviceToHost);
         long long mx = 0; for (auto v : c) mx = v > mx ? v : mx;
-        printf("GEMM slice pattern (24 MMAs N=64, A tmem, 2 sets)%s: %.1f cycles/slice, %.1f cycles/MMA (%s)\n",
-               ce ? " + commit/wait per slice" : "", (double)mx / slices, (double)mx / (slices * 24), cudaGetErrorString(e));
+        printf("GEMM slice pattern (24 MMAs N=64, A tmem, 2 sets)%s%s: %.1f cycles/slice, %.1f cycles/MMA (%s)\n",
+               (ce & 2) ? ", M-blocks interleaved" : "", (ce & 1) ? " + commit/wait per slice" : "", (double)mx / slices, (double)mx / (slices * 24), cudaGetErrorString(e));
     }
     return 0;
 }
