@@ -1,46 +1,33 @@
 // dv_gemm_kernels.cu -- the attention-dropout recompute fused into its
-// consumer, the dV GEMM, on the 5th-generation tensor cores (sm_100a).
+// consumers, the attention-context GEMM ctx = D @ V (forward) and its
+// backward's dV = D^T @ dO, on the 5th-generation tensor cores (sm_100a).
 //
 // The reference's Sub-Layer Dropout Recomputation keeps only P and the mask;
-// when the backward reaches the consumer of the dropped-out map D -- the
-// attention-context GEMM ctx = D @ V, whose backward needs D for
-// dV = D^T @ dO -- the consumer asks for D and the recompute rule
-// "dropout-rescale" rebuilds it (graph.cpp:46-50 -> BackwardCtx::stash,
-// tape.cpp:244-264; rule ops_tempo.cpp:17-26 = dropout_apply,
-// ops_reference.cpp:147-153).  Here D never exists in HBM: the producer warps
-// rebuild each tile of D from P and the mask bits (D = keep ? float(double(P)
-// * s) : 0, the same rounding as mask_scale, kernels.cpp:285-295, so the
-// tile is bitwise the D the forward produced) directly in shared memory, in
-// the UMMA operand layout, and tcgen05.mma consumes it.  HBM traffic per
-// attention element: P (4 B) + the mask bit, instead of writing D (4 B) in
-// attn_probs_bwd and reading it back (4 B) in a separate GEMM.
+// the consumer of the dropped-out map D gets it from the recompute rule
+// "dropout-rescale" (graph.cpp:46-50 -> BackwardCtx::stash, tape.cpp:244-264;
+// rule ops_tempo.cpp:17-26 = dropout_apply, ops_reference.cpp:147-153), and
+// the forward materialises D for ctx (ops_tempo.cpp:196-210).  Here D never
+// exists in memory at all: the producer warps rebuild D' = keep ? P : 0 (the
+// 1/(1-p) is applied in the epilogue) tile by tile and write it, split into
+// TF32 hi + lo, straight into TMEM as the A operand of tcgen05.mma.  HBM
+// traffic per attention element: P (4 B) + the mask bit.
 //
-// GEMM per (batch, head): dV[j, c] = sum_i D[i, j] dO[i, c]
-//   M = s_k (j), N = d (c), K = s_q (i).  P / D are row-major [i][j] and dO
-//   [i][c], i.e. both operands are MN-major in HBM; tcgen05 kind::tf32 gives
-//   no result for MN-major operands on this part (measured,
-//   tests/tools/umma_probe.cu: every a_major/b_major = MN variant returns 0,
-//   K-major is exact), so the producers transpose while staging: a thread
-//   owns one M (or N) index, reads it down 32 K-rows (each warp load is a
-//   coalesced 128-byte row segment) and writes 16-byte K-chunks into the
-//   canonical K-major SWIZZLE_128B layout (128-byte rows, 8-row 1 KB atoms,
-//   chunk index XOR row: conflict-free).
-// fp32 accuracy from TF32 tensor cores: 3xTF32 -- x = hi + lo with hi, lo
-//   TF32 (round-to-nearest), D^T dO ~ hi*hi + hi*lo + lo*hi, all three
-//   products accumulated in one fp32 TMEM accumulator (relative error ~2^-21
-//   per product vs fp32's 2^-24; dV within 1e-6 of the fp64 product).
+// The product kernel is ctx_recompute_gemm_ta_kernel<N, DRAIN, DV> (below,
+// "ctx with the A operand in TMEM"): persistent, warp-specialised (TMA
+// loader lane, 16 producer warps in two alternating halves, one MMA lane),
+// 32-wide K slices through a 4-deep TMA ring, 3xTF32 (hi*hi + hi*lo + lo*hi
+// -- lo*hi first), accumulation error flat in K (set rotation up to K = 1024,
+// drained ping-pong accumulators beyond).  Why A in TMEM: tcgen05 kind::tf32
+// takes no MN-major smem operands on this part (tests/tools/umma_probe.cu),
+// so D^T needs a transpose anyway; a producer thread that owns one output
+// row = one TMEM lane does it on the way in, and the MMA then reads A from
+// TMEM instead of 12 B per element of smem (tests/tools/tmem_a_probe.cu).
 //
-// CTA = one (head, 256-row block of dV): 8 producer warps + 1 MMA warp.
-//   producers: global P (+mask words) and dO -> registers (the next K-chunk
-//     of 32 rows loads while this one is staged) -> D, hi/lo split ->
-//     st.shared into stage s of a 2-deep ring -> fence.proxy.async +
-//     mbarrier arrive (full[s]);
-//   MMA warp (one elected lane): per stage, 4 K-steps x 2 M-blocks x 3
-//     tcgen05.mma.kind::tf32 (M=128, N=d, K=8) into two TMEM accumulators,
-//     tcgen05.commit -> empty[s] (the stage may be overwritten) and, after
-//     the last stage, -> acc_full;
-//   epilogue: the producer warps tcgen05.ld their TMEM lane quadrant
-//     (warp w: accumulator w/4, lanes 32*(w%4)..) and store dV rows.
+// Kept as A/B baselines and fallbacks (DESIGN 3d has the measured history):
+// dv_recompute_gemm_kernel (register-prefetch producers, smem operands; also
+// d = 128 and the path without tensor maps), dv_recompute_gemm_staged_kernel
+// and ctx_recompute_gemm_kernel (TMA staging, smem operands; TM_DV_TA=0 /
+// TM_CTX_TA=0).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
