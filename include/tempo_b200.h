@@ -269,14 +269,16 @@ int tempo_dropout_bwd(const float* dy, const uint32_t* mask, double p, float* dx
 
 /* The dropout recompute fused into its consumer: the
  * attention-context GEMM's input gradient dV = D^T @ dO, per (batch, head),
- * where D = keep ? float(double(P) / (1-p)) : 0 is rebuilt tile by tile in
- * the GEMM's shared-memory operand staging from the stashed P and mask --
+ * where D' = keep ? P : 0 is rebuilt tile by tile by the GEMM's producer
+ * warps from the stashed P and mask and written straight into tensor memory
+ * as the MMA's A operand (1/(1-p) applied to the result) --
  * the consumer's BackwardCtx::stash of the "dropout-rescale" recipe
  * (graph.cpp:46-50, tape.cpp:244-264, ops_tempo.cpp:17-26) without D ever
  * reaching HBM.  P: [heads][s_q][s_k] (the softmax output, row = query),
  * mask: its bit-packed keep bits (global element order), dO: [heads][s_q][d],
  * dV: [heads][s_k][d]; fp32 in and out, computed on the tcgen05 tensor
- * cores in 3xTF32 (within 1e-6 relative of the fp64 product).  Pair with
+ * cores in 3xTF32 (error within 2e-6 of |ref| + sum |D||dO| at any s_q:
+ * the accumulation is drained into fp32 beyond s_q = 1024).  Pair with
  * tempo_attn_probs_bwd(..., D_out = NULL).  Needs s_q % 32 == 0,
  * s_k % 256 == 0, d in {32, 64, 128} (else TEMPO_ERR_UNSUPPORTED) and
  * 16-byte aligned P, dO, dV. */
@@ -289,7 +291,7 @@ int tempo_attn_dropout_dv(const float* P, const uint32_t* mask, double p, const 
  * (ops_tempo.cpp:196-210) without D in HBM: pair with
  * tempo_softmax_dropout_fwd(..., D = NULL), so the forward writes P and the
  * bits only.  P: [heads][s_q][s_k], V: [heads][s_k][d], ctx: [heads][s_q][d],
- * fp32, within 1e-6 relative of the fp64 product.  Needs s_k % 32 == 0,
+ * fp32, error within 2e-6 of |ref| + sum |D||V| at any s_k.  Needs s_k % 32 == 0,
  * d in {32, 64} (else TEMPO_ERR_UNSUPPORTED), 16-byte aligned
  * P, V, ctx. */
 int tempo_attn_dropout_ctx(const float* P, const uint32_t* mask, double p, const float* V,
