@@ -1320,6 +1320,65 @@ __global__ void __launch_bounds__(1024) ln_param_reduce_kernel(const double* __r
     }
 }
 
+// Stage 2, narrow column blocks: 8 outputs (one 64-byte row segment = two
+// full sectors) x 64 partial-row slices per 512-thread CTA, so the grid is
+// 2*cols/8 CTAs (256 at H = 1024) instead of 2*cols/32 one-per-SM CTAs, and
+// each thread has a handful of loads in flight at once.  The 64 slice sums
+// are combined by a fixed shuffle tree inside each warp (4 slices) and then
+// over the 16 warps in a fixed order -- the same tree every run: bitwise
+// reproducible (fp addition is commutative, so both xor partners hold the
+// same bits).
+#ifndef TM_LN_REDUCE_NARROW
+#define TM_LN_REDUCE_NARROW 1
+#endif
+#ifndef TM_LN_REDUCE_COLS
+#define TM_LN_REDUCE_COLS 8
+#endif
+constexpr int kRedCols = TM_LN_REDUCE_COLS, kRedSlices = 512 / kRedCols;
+static_assert(kRedCols >= 1 && kRedCols <= 16 && (kRedCols & (kRedCols - 1)) == 0, "");
+__global__ void __launch_bounds__(kRedCols * kRedSlices) ln_param_reduce8_kernel(
+    const double* __restrict__ ws, int nparts, int cols, float* __restrict__ dgamma,
+    float* __restrict__ dbeta) {
+    grid_dep_wait();  // PDL: predecessor complete and visible
+    grid_dep_launch();
+    constexpr int kWarps = kRedCols * kRedSlices / 32;
+    __shared__ double part[kWarps][kRedCols];
+    const int tx = threadIdx.x % kRedCols, ty = threadIdx.x / kRedCols;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int64_t total = 2 * (int64_t)cols;
+    const int64_t j = (int64_t)blockIdx.x * kRedCols + tx;
+    double acc = 0.0;
+    if (j < total) {
+        constexpr int L = 8;
+        for (int c0 = ty; c0 < nparts; c0 += kRedSlices * L) {
+            double a[L];
+#pragma unroll
+            for (int l = 0; l < L; ++l) {
+                const int c = c0 + kRedSlices * l;
+                a[l] = c < nparts ? ws[(size_t)c * total + j] : 0.0;
+            }
+#pragma unroll
+            for (int l = 0; l < L; ++l) acc += a[l];  // adding +0.0 past the end is exact
+        }
+    }
+#pragma unroll
+    for (int m = kRedCols; m < 32; m <<= 1) acc += __shfl_xor_sync(0xffffffffu, acc, m);
+    if (lane < kRedCols) part[w][lane] = acc;
+    __syncthreads();
+    if (w == 0) {  // lane = q * kRedCols + column: warps q, q + Q, q + 2Q, ..., then the tree
+        constexpr int Q = 32 / kRedCols;
+        double v = 0.0;
+#pragma unroll
+        for (int k = 0; k < kWarps / Q; ++k) v += part[lane / kRedCols + Q * k][lane % kRedCols];
+#pragma unroll
+        for (int m = kRedCols; m < 32; m <<= 1) v += __shfl_xor_sync(0xffffffffu, v, m);
+        const int64_t jo = (int64_t)blockIdx.x * kRedCols + lane;
+        if (lane < kRedCols && jo < total) {
+            if (jo < cols) dgamma[jo] = (float)v; else dbeta[jo - cols] = (float)v;
+        }
+    }
+}
+
 // Stage 2 fused with the cross-rank sum (the path's one collective, SURVEY
 // 8e) over peer memory, in place of ln_param_reduce_kernel + an all-reduce.
 // CTA cb owns outputs j in [32 cb, 32 cb + 32) of the 2*cols (dgamma | dbeta):
@@ -1713,6 +1772,10 @@ cudaError_t launch_ln_param_reduce(const double* partials, int64_t nparts, int64
         cudaMemsetAsync(dbeta, 0, cols * sizeof(float), st);
         return cudaGetLastError();
     }
+    if (TM_LN_REDUCE_NARROW)
+        return launch_pdl((const void*)ln_param_reduce8_kernel,
+                          (int)((2 * cols + kRedCols - 1) / kRedCols), kRedCols * kRedSlices, 0,
+                          st, partials, (int)nparts, (int)cols, dgamma, dbeta);
     const int rgrid = (int)((2 * cols + 31) / 32);
     return launch_pdl((const void*)ln_param_reduce_kernel, rgrid, 1024, 0, st, partials,
                       (int)nparts, (int)cols, dgamma, dbeta);

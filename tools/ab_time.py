@@ -89,7 +89,26 @@ def main():
     calls["dv_gemm_only"] = (lambda: o.attn_dropout_dv(c.P.view(heads, bench.S, bench.S), c.m_att, bench.P_DROP, dO, dV=dV), [dV])
     calls["cublas_dv_only"] = (lambda: torch.matmul(c.Drec.view(heads, bench.S, bench.S).transpose(1, 2), dO, out=dV), [dV])
     calls["attn_bwd_noD"] = (lambda: o.attn_probs_bwd(c.dD, c.P, c.m_att, bench.P_DROP, write_d=False, dZ=c.dZ), [c.dZ])
+    # configs[0]: the L2-resident / launch-bound GELU pair at [1024, 3072]
+    n0 = 1024 * 3072
+    x0 = torch.randn(n0, device=dev) * 3
+    y0, dy0, dx0 = torch.empty_like(x0), torch.randn_like(x0), torch.empty_like(x0)
+    m0 = torch.empty((n0 + 31) // 32, dtype=torch.int32, device=dev)
+    calls["cfg0_gelu_fwd"] = (lambda: o.gelu_ip_fwd(x0, c.table, y=y0, mask=m0), [y0, m0])
+    calls["cfg0_gelu_bwd"] = (lambda: o.gelu_ip_bwd(dy0, y0, m0, c.table, dx=dx0), [dx0])
+    # configs[1]: LayerNorm backward at [16384, 768] (stage 1 + the dgamma/dbeta reduction)
+    r1, h1 = 16384, 768
+    x1 = torch.randn(r1, h1, device=dev) + 0.4
+    g1_ = 1 + 0.2 * torch.randn(h1, device=dev)
+    b1_ = 0.1 * torch.randn(h1, device=dev)
+    y1, rs1 = o.layernorm_ip_fwd(x1, g1_, b1_)
+    dy1, dx1 = torch.randn_like(x1), torch.empty_like(x1)
+    dgb1 = torch.empty(2 * h1, device=dev)
+    calls["cfg1_ln_bwd"] = (lambda: o.layernorm_ip_bwd(dy1, y1, rs1, g1_, b1_, dx=dx1, dgamma=dgb1[:h1], dbeta=dgb1[h1:]), [dx1, dgb1])
     ob = bench.op_bytes()
+    ob["cfg1_ln_bwd"] = r1 * h1 * 12
+    ob["cfg0_gelu_fwd"] = n0 * 8.125
+    ob["cfg0_gelu_bwd"] = n0 * 12.125
     n_a = c.P.numel()
     ob["dv_unfused"] = n_a * 16.125 + n_a * 4 + dO.numel() * 8
     ob["dv_fused"] = n_a * 12.125 + n_a * 4.125 + dO.numel() * 8
