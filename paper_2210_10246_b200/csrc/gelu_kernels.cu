@@ -25,22 +25,13 @@
 namespace tb {
 namespace {
 
-#ifndef TM_GELU_FWD_MINB
-#define TM_GELU_FWD_MINB 1
-#endif
-// configs[0]-sized tensors (n < kSmallN): register cap (CTAs per SM) and
-// grid waves of the one-chunk-per-group instantiations
-#ifndef TM_GELU_SMALL_FWD_MINB
-#define TM_GELU_SMALL_FWD_MINB 1
-#endif
-#ifndef TM_GELU_SMALL_BWD_MINB
-#define TM_GELU_SMALL_BWD_MINB 1
+#ifdef TM_GELU_FWD_MINB
+#define TM_GELU_FWD_BOUNDS __launch_bounds__(256, TM_GELU_FWD_MINB)
+#else
+#define TM_GELU_FWD_BOUNDS __launch_bounds__(256)
 #endif
 #ifndef TM_GELU_WAVES
 #define TM_GELU_WAVES 1
-#endif
-#ifndef TM_GELU_SMALL_WAVES
-#define TM_GELU_SMALL_WAVES TM_GELU_WAVES
 #endif
 #ifndef TM_GELU_FWD_U8
 #define TM_GELU_FWD_U8 4
@@ -134,8 +125,8 @@ __device__ __forceinline__ void gelu_fwd8_compute(const F8 (&v)[U], float* __res
     }
 }
 
-template <int U, int MINB = TM_GELU_FWD_MINB>
-__global__ void __launch_bounds__(256, MINB) gelu_fwd8_kernel(const float* __restrict__ x,
+template <int U>
+__global__ void TM_GELU_FWD_BOUNDS gelu_fwd8_kernel(const float* __restrict__ x,
                                                     float* __restrict__ y,
                                                     uint32_t* __restrict__ mask, int64_t n,
                                                     float xstar_gt, float xs_lo) {
@@ -498,8 +489,8 @@ __device__ __forceinline__ float gelu_h_fast(float y, uint32_t m, const FastTabl
 #ifndef TM_GELU_BWD_U8
 #define TM_GELU_BWD_U8 2
 #endif
-template <int NC4, bool HORNER, bool V8, int U8 = TM_GELU_BWD_U8, int MINB = 1>
-__global__ void __launch_bounds__(kBlock, MINB) gelu_bwd_fast_kernel(
+template <int NC4, bool HORNER, bool V8, int U8 = TM_GELU_BWD_U8>
+__global__ void __launch_bounds__(kBlock) gelu_bwd_fast_kernel(
     const float* __restrict__ dy, const float* __restrict__ y, const uint32_t* __restrict__ mask,
     float* __restrict__ dx, int64_t n, const __grid_constant__ GeluDevTable t, int vec) {
     grid_dep_wait();  // PDL: predecessor complete and visible
@@ -674,10 +665,9 @@ cudaError_t launch_gelu_fwd(const float* x, float* y, uint32_t* mask, int64_t n,
         const bool small = n < kSmallN;
         const int U = small ? 1 : TM_GELU_FWD_U8;
         const int64_t warps_needed = ((n >> 8) + U - 1) / U + 1;
-        auto k = small ? gelu_fwd8_kernel<1, TM_GELU_SMALL_FWD_MINB>
-                       : gelu_fwd8_kernel<TM_GELU_FWD_U8>;
+        auto k = small ? gelu_fwd8_kernel<1> : gelu_fwd8_kernel<TM_GELU_FWD_U8>;
         int grid = grid_for((const void*)k, kBlock, 0, (warps_needed * 32 + kBlock - 1) / kBlock, 0,
-                            small ? TM_GELU_SMALL_WAVES : TM_GELU_WAVES);
+                            TM_GELU_WAVES);
         launch(k, grid, kBlock, 0, st)(x, y, mask, n, xstar_gt, xs_lo);
     } else {
         int grid = grid_for((const void*)gelu_fwd_scalar_kernel, kBlock, 0,
@@ -718,16 +708,13 @@ cudaError_t launch_gelu_bwd(const float* dy, const float* y, const uint32_t* mas
         const bool small = n < kSmallN;  // one chunk per group (see the forward)
 #define TB_CASE(NC)                                                                       \
     case NC: {                                                                            \
-        auto k = v8 ? (small ? (hv ? gelu_bwd_fast_kernel<NC, true, true, 1,              \
-                                                          TM_GELU_SMALL_BWD_MINB>         \
-                                   : gelu_bwd_fast_kernel<NC, false, true, 1,             \
-                                                          TM_GELU_SMALL_BWD_MINB>)        \
+        auto k = v8 ? (small ? (hv ? gelu_bwd_fast_kernel<NC, true, true, 1>               \
+                                   : gelu_bwd_fast_kernel<NC, false, true, 1>)            \
                              : (hv ? gelu_bwd_fast_kernel<NC, true, true>                  \
                                    : gelu_bwd_fast_kernel<NC, false, true>))              \
                     : (hv ? gelu_bwd_fast_kernel<NC, true, false>                        \
                                 : gelu_bwd_fast_kernel<NC, false, false>);               \
-        int grid = grid_for((const void*)k, kBlock, 0, blocks, 0,                         \
-                            small ? TM_GELU_SMALL_WAVES : TM_GELU_WAVES);                 \
+        int grid = grid_for((const void*)k, kBlock, 0, blocks, 0, TM_GELU_WAVES);         \
         launch(k, grid, kBlock, 0, st)(dy, y, mask, dx, n, t, vflag);                         \
         break;                                                                            \
     }
