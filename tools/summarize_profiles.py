@@ -33,6 +33,7 @@ OP_OF_KERNEL = [  # kernel name prefix -> bench op
     ("dal_fwd_warp_kernel", "dropout_add_layernorm_fwd"),
     ("ln_bwd_vec_kernel", "layernorm_bwd"),
     ("ln_param_reduce_kernel", "layernorm_bwd"),
+    ("ln_param_reduce8_kernel", "layernorm_bwd"),
     ("dropout_fwd_vec_kernel<1>", "dropout_fwd"),
     ("dropout_fwd8_kernel<1", "dropout_fwd"),
     ("dropout_fwd8_kernel<0", "dropout_bwd"),
