@@ -704,3 +704,44 @@ def test_layernorm_nan_row(tops, port, cuda, rows, cols):
         torch.cuda.synchronize()
         assert _close_nan(yd.cpu().numpy(), ry, 1e-5, 1e-5)
         assert _close_nan(rsd.cpu().numpy(), rrs, 1e-6, 0)
+
+
+def _reduce8_order(parts, cw=8):
+    """ln_param_reduce8_kernel's fixed summation tree (layernorm_kernels.cu):
+    slice ty = 0..64 sums partial rows ty, ty+64, ... in order; a warp holds
+    slices 4w..4w+3 and adds them by the xor-8 then xor-16 shuffle tree; warp
+    0 lane q*8+c sums warps q, q+4, q+8, q+12 in order, then the same tree."""
+    nparts, total = parts.shape
+    ns = 512 // cw
+    sl = np.zeros((ns, total))
+    for ty in range(ns):
+        for c in range(ty, nparts, ns):
+            sl[ty] = sl[ty] + parts[c]
+    # per warp: slices 4w+t, t = 0..3 -> (s0 + s1) + (s2 + s3)
+    wsum = np.array([(sl[4 * w] + sl[4 * w + 1]) + (sl[4 * w + 2] + sl[4 * w + 3])
+                     for w in range(ns // 4)])
+    q = [((wsum[k] + wsum[k + 4]) + wsum[k + 8]) + wsum[k + 12] for k in range(4)]
+    return (q[0] + q[1]) + (q[2] + q[3])
+
+
+@pytest.mark.parametrize("nparts,cols", [(1, 5), (37, 768), (296, 1024), (700, 1001),
+                                         (1100, 12)])
+def test_ln_param_reduce_fixed_tree(cuda, nparts, cols):
+    """Stage 2 of the LN backward (tempo_ln_param_reduce, 8 columns x 64
+    slices per CTA) is exactly its documented fixed-order tree, bit for bit:
+    ragged column blocks (cols % 8 != 0), more partial rows than one load
+    batch (nparts > 512), one partial row."""
+    import torch
+    from paper_2210_10246_b200._capi import lib
+    g = np.random.default_rng(nparts * 7 + cols)
+    parts = g.standard_normal((nparts, 2 * cols)) * np.exp(g.uniform(-8, 8, (nparts, 1)))
+    dev = torch.from_numpy(parts).to(cuda)
+    dg = torch.full((cols,), float("nan"), device=cuda)
+    db = torch.full((cols,), float("nan"), device=cuda)
+    st = torch.cuda.current_stream().cuda_stream
+    assert lib().tempo_ln_param_reduce(dev.data_ptr(), nparts, cols, dg.data_ptr(),
+                                       db.data_ptr(), st) == 0
+    torch.cuda.synchronize()
+    want = _reduce8_order(parts).astype(np.float32)
+    assert np.array_equal(dg.cpu().numpy(), want[:cols])
+    assert np.array_equal(db.cpu().numpy(), want[cols:])
